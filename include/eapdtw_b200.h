@@ -1,0 +1,149 @@
+/*
+ * eapdtw_b200.h -- C ABI of the B200 (sm_100a) EAPrunedDTW subsequence-search
+ * hot path.  Plain pointers and sizes only; no exceptions, no torch types.
+ *
+ * Each entry point replaces one reference interface (paths relative to
+ * /root/reference/proj).  The reference C++ signatures are re-exposed on top
+ * of this ABI by include/eapdtw_b200.hpp; INTEGRATION.md shows the binding.
+ *
+ * Conventions:
+ *   - status codes: EAPDTW_OK, EAPDTW_EINVAL for exactly the conditions where
+ *     the reference throws std::invalid_argument, EAPDTW_ECUDA for a CUDA
+ *     failure (message via eapdtw_last_error(), thread-local);
+ *   - abandonment returns +inf, the reference's PRUNED (series.hpp:16);
+ *   - EAPDTW_UNBOUNDED_WINDOW == Band::unbounded_window (dtw.hpp:17);
+ *   - host pointers are copied; *_dev variants take device pointers;
+ *   - one host thread per context; calls on a context are serialised on its
+ *     stream.  There is no CPU fallback: without a GPU every compute call
+ *     returns EAPDTW_ECUDA.
+ */
+#ifndef EAPDTW_B200_H
+#define EAPDTW_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EAPDTW_OK 0
+#define EAPDTW_EINVAL 1
+#define EAPDTW_ECUDA 2
+#define EAPDTW_ENOMEM 3
+#define EAPDTW_UNBOUNDED_WINDOW ((size_t)-1)
+
+/* Algo (search.hpp:56) */
+#define EAPDTW_ALGO_FULL 0
+#define EAPDTW_ALGO_LEFT_PRUNE 1
+#define EAPDTW_ALGO_EA_PRUNED 2
+
+typedef struct eapdtw_ctx eapdtw_ctx;
+typedef struct eapdtw_search_plan eapdtw_search_plan;
+
+/* SearchConfig (search.hpp:60-66) */
+typedef struct {
+  size_t query_length; /* 0: the query's full length */
+  double window_ratio; /* window_cells = floor(window_ratio * m) (search.cpp:18-21) */
+  int32_t algorithm;   /* EAPDTW_ALGO_* */
+  int32_t use_lower_bounds;
+  int32_t tighten_ub;  /* accepted; the GPU path's pruning is already exact */
+  int32_t reserved_;
+} eapdtw_search_config;
+
+/* SearchResult = BestSoFar + SearchReport (search.hpp:50-82), flattened. */
+typedef struct {
+  uint64_t location;
+  double distance_sq;
+  int32_t found;
+  int32_t pad_;
+  uint64_t candidates_total, pruned_kim, pruned_keogh_eq, pruned_keogh_ec, dtw_calls,
+      dtw_abandoned, dp_cells_evaluated;
+  double elapsed_seconds;
+} eapdtw_search_result;
+
+/* --- errors / context ---------------------------------------------------- */
+const char* eapdtw_last_error(void);
+int eapdtw_version(void);
+int eapdtw_device_count(void);
+int eapdtw_ctx_create(eapdtw_ctx** out, int device);
+int eapdtw_ctx_destroy(eapdtw_ctx* ctx);
+/* Run on an external stream (e.g. torch.cuda.current_stream().cuda_stream). NULL: own stream. */
+int eapdtw_ctx_set_stream(eapdtw_ctx* ctx, void* cuda_stream);
+int eapdtw_ctx_synchronize(eapdtw_ctx* ctx);
+/* Number of kernels this context has launched (gpu_launches accounting). */
+uint64_t eapdtw_ctx_launches(const eapdtw_ctx* ctx);
+
+/* --- DTW kernels, one pair (dtw.hpp:69-99) ------------------------------- *
+ * ea_pruned_dtw_windowed(a, b, Band{window}, ub, cumulative_bound)  dtw.hpp:93-99
+ * dtw_windowed(a, b, Band{window})                                  dtw.hpp:72-74
+ * ea_pruned_dtw(a, b, ub)      == window EAPDTW_UNBOUNDED_WINDOW    dtw.hpp:85-87
+ * cb may be NULL (cb_len 0).  cells (nullable) receives the evaluated cells. */
+int eapdtw_ea_pruned_dtw_windowed(eapdtw_ctx* ctx, const double* a, size_t la, const double* b,
+                                  size_t lb, size_t window, double ub, const double* cb,
+                                  size_t cb_len, double* out, uint64_t* cells);
+int eapdtw_dtw_windowed(eapdtw_ctx* ctx, const double* a, size_t la, const double* b, size_t lb,
+                        size_t window, double* out, uint64_t* cells);
+
+/* --- batched pairwise (cfg1): npairs pairs of equal length len --------------
+ * out[p] = ea_pruned_dtw_windowed(a_p, b_p, Band{window}, ub[p]); ub NULL = +inf.
+ * prune 0 gives dtw_windowed (no abandoning). */
+int eapdtw_pairwise(eapdtw_ctx* ctx, const double* a, const double* b, size_t npairs, size_t len,
+                    size_t window, const double* ub, int prune, double* out, uint64_t* cells);
+int eapdtw_pairwise_dev(eapdtw_ctx* ctx, const double* a_dev, const double* b_dev, size_t npairs,
+                        size_t len, size_t window, const double* ub_dev, int prune,
+                        double* out_dev, uint64_t* cells);
+
+/* --- subsequence search (similarity_search, search.hpp:118-119) ------------ */
+int eapdtw_similarity_search(eapdtw_ctx* ctx, const double* reference, size_t n,
+                             const double* query, size_t qlen, const eapdtw_search_config* cfg,
+                             eapdtw_search_result* out);
+int eapdtw_similarity_search_dev(eapdtw_ctx* ctx, const double* reference_dev, size_t n,
+                                 const double* query, size_t qlen,
+                                 const eapdtw_search_config* cfg, eapdtw_search_result* out);
+
+/* Stepped search over one shard, for multi-GPU drivers.  The shard holds
+ * reference[global_offset : global_offset + n) (candidates plus an (m-1)-point
+ * halo); global_offset must be a multiple of 100000 (the stats reset
+ * interval, search.cpp:16) so the shard reproduces the unsharded chain.
+ * run() may be called for consecutive candidate ranges; between calls a
+ * driver may lower the threshold key (all-reduce MIN across ranks) through
+ * the device pointer returned by ub_key(). */
+int eapdtw_search_plan_create(eapdtw_ctx* ctx, const double* reference_dev, size_t n,
+                              const double* query, size_t qlen, const eapdtw_search_config* cfg,
+                              uint64_t global_offset, eapdtw_search_plan** out);
+int eapdtw_search_plan_prepare(eapdtw_search_plan* plan); /* stats, envelope, probe */
+size_t eapdtw_search_plan_candidates(const eapdtw_search_plan* plan);
+int eapdtw_search_plan_run(eapdtw_search_plan* plan, size_t begin, size_t end);
+uint64_t* eapdtw_search_plan_ub_key(eapdtw_search_plan* plan);
+/* Synchronises; location is global (offset added). */
+int eapdtw_search_plan_result(eapdtw_search_plan* plan, eapdtw_search_result* out);
+/* Device time in ms of the last prepare/run, per phase: [stats, envelope, probe, sweep]. */
+int eapdtw_search_plan_timings(eapdtw_search_plan* plan, float* ms4);
+int eapdtw_search_plan_destroy(eapdtw_search_plan* plan);
+
+/* --- batched NN1 (cfg5): per query, argmin over the database ------------- *
+ * Each query keeps a running cutoff: d_k = ea_pruned_dtw_windowed(db_k, q,
+ * Band{window}, bsf); strict < keeps the lowest index. */
+int eapdtw_nn1(eapdtw_ctx* ctx, const double* queries, size_t nq, const double* db, size_t nd,
+               size_t len, size_t window, uint64_t* argmin, double* dist, uint64_t* cells);
+int eapdtw_nn1_dev(eapdtw_ctx* ctx, const double* queries_dev, size_t nq, const double* db_dev,
+                   size_t nd, size_t len, size_t window, uint64_t* argmin, double* dist,
+                   uint64_t* cells);
+
+/* --- host-side helpers (bit-identical to the reference) -------------------- */
+/* RunningStats::over + znormalize_into (search.cpp:25-46) */
+int eapdtw_znormalize(const double* src, size_t n, double* dst);
+/* random_walk (io.cpp:124-137): mt19937_64, uniform steps in [-0.5, 0.5) */
+int eapdtw_random_walk_uniform(size_t n, uint64_t seed, double* out);
+/* Benchmark data: x0 = 0, x[i+1] = x[i] + N(0,1) (mt19937_64 + Box-Muller) */
+int eapdtw_random_walk_normal(size_t n, uint64_t seed, double* out);
+
+/* --- measurement ------------------------------------------------------------ */
+/* Measured FP64 (DADD) issue rate of this device in ops/s (the DTW roofline). */
+int eapdtw_fp64_peak(eapdtw_ctx* ctx, double* ops_per_s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EAPDTW_B200_H */

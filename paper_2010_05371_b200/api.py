@@ -1,0 +1,405 @@
+"""Python mirror of the reference's public C++ API, executed on the B200.
+
+Names, argument meaning and error behaviour follow the reference headers
+(paths relative to /root/reference/proj):
+
+* ``PRUNED``, ``is_pruned``, ``Series``          include/eapdtw/series.hpp:16-50
+* ``Band``                                        include/eapdtw/dtw.hpp:16-23
+* ``ea_pruned_dtw_windowed``, ``ea_pruned_dtw``,
+  ``dtw_windowed``                                include/eapdtw/dtw.hpp:69-99
+* ``Algo``, ``SearchConfig``, ``BestSoFar``,
+  ``SearchReport``, ``SearchResult``,
+  ``similarity_search``                           include/eapdtw/search.hpp:50-119
+
+``std::invalid_argument`` maps to ``ValueError``.  Every compute call goes
+through the C ABI of ``libeapdtw_b200.so`` (include/eapdtw_b200.h); there is
+no CPU path.  Batched entry points with no reference counterpart (``pairwise``
+for cfg1, ``nn1`` for cfg5, ``ShardedSearch`` for multi-GPU) sit beside them.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import math
+import threading
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _capi
+from ._capi import check, lib
+
+PRUNED = math.inf
+UNBOUNDED_WINDOW = _capi.UNBOUNDED_WINDOW
+_dp = C.POINTER(C.c_double)
+_u64p = C.POINTER(C.c_uint64)
+
+
+def is_pruned(v: float) -> bool:
+    """series.hpp:18"""
+    return v == PRUNED
+
+
+class Series:
+    """Validated, non-empty, finite float64 samples (series.hpp:22-50)."""
+
+    __slots__ = ("_x",)
+
+    def __init__(self, samples):
+        x = np.ascontiguousarray(np.asarray(samples, dtype=np.float64).reshape(-1))
+        if x.size == 0:
+            raise ValueError("Series: empty input")
+        bad = ~np.isfinite(x)
+        if bad.any():
+            raise ValueError(f"Series: non-finite sample at index {int(np.argmax(bad))}")
+        self._x = x
+
+    def __len__(self):
+        return self._x.size
+
+    def length(self) -> int:
+        return self._x.size
+
+    def __getitem__(self, i):
+        return self._x[i]
+
+    def view(self) -> np.ndarray:
+        return self._x
+
+    def prefix(self, n: int) -> "Series":
+        if n == 0 or n > self._x.size:
+            raise ValueError("Series::prefix: bad length")
+        return Series(self._x[:n].copy())
+
+
+@dataclass(frozen=True)
+class Band:
+    """Sakoe-Chiba band (dtw.hpp:16-23)."""
+
+    window: int = UNBOUNDED_WINDOW
+
+    @staticmethod
+    def unbounded() -> "Band":
+        return Band(UNBOUNDED_WINDOW)
+
+    @staticmethod
+    def cells(w: int) -> "Band":
+        return Band(int(w))
+
+    def is_unbounded(self) -> bool:
+        return self.window == UNBOUNDED_WINDOW
+
+
+class Algo(enum.IntEnum):
+    """search.hpp:56"""
+
+    full = _capi.ALGO_FULL
+    left_prune = _capi.ALGO_LEFT_PRUNE
+    ea_pruned = _capi.ALGO_EA_PRUNED
+
+
+@dataclass
+class SearchConfig:
+    """search.hpp:60-66"""
+
+    query_length: int = 0
+    window_ratio: float = 0.1
+    algorithm: Algo = Algo.ea_pruned
+    use_lower_bounds: bool = True
+    tighten_ub: bool = True
+
+    def to_c(self) -> _capi.SearchConfigC:
+        return _capi.SearchConfigC(int(self.query_length), float(self.window_ratio),
+                                   int(self.algorithm), int(bool(self.use_lower_bounds)),
+                                   int(bool(self.tighten_ub)), 0)
+
+
+@dataclass
+class BestSoFar:
+    """search.hpp:50-54"""
+
+    location: int = 0
+    distance_sq: float = PRUNED
+    found: bool = False
+
+
+@dataclass
+class SearchReport:
+    """search.hpp:68-77 (GPU semantics: see DESIGN.md, 'Counters')."""
+
+    candidates_total: int = 0
+    pruned_kim: int = 0
+    pruned_keogh_eq: int = 0
+    pruned_keogh_ec: int = 0
+    dtw_calls: int = 0
+    dtw_abandoned: int = 0
+    dp_cells_evaluated: int = 0
+    elapsed_seconds: float = 0.0
+
+
+@dataclass
+class SearchResult:
+    """search.hpp:79-82"""
+
+    best: BestSoFar = field(default_factory=BestSoFar)
+    report: SearchReport = field(default_factory=SearchReport)
+
+    @staticmethod
+    def from_c(r: _capi.SearchResultC) -> "SearchResult":
+        return SearchResult(
+            BestSoFar(int(r.location), float(r.distance_sq), bool(r.found)),
+            SearchReport(int(r.candidates_total), int(r.pruned_kim), int(r.pruned_keogh_eq),
+                         int(r.pruned_keogh_ec), int(r.dtw_calls), int(r.dtw_abandoned),
+                         int(r.dp_cells_evaluated), float(r.elapsed_seconds)))
+
+
+class Context:
+    """Owns one ``eapdtw_ctx`` (device, stream, scratch buffers)."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        check(lib.eapdtw_ctx_create(C.byref(h), int(device)))
+        self.handle = h
+        self.device = int(device)
+
+    def close(self):
+        if self.handle:
+            lib.eapdtw_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown order
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, stream_ptr: int | None):
+        check(lib.eapdtw_ctx_set_stream(self.handle, C.c_void_p(stream_ptr or 0)))
+
+    def synchronize(self):
+        check(lib.eapdtw_ctx_synchronize(self.handle))
+
+    @property
+    def launches(self) -> int:
+        return int(lib.eapdtw_ctx_launches(self.handle))
+
+    def fp64_peak(self) -> float:
+        v = C.c_double()
+        check(lib.eapdtw_fp64_peak(self.handle, C.byref(v)))
+        return v.value
+
+
+_tls = threading.local()
+
+
+def default_context(device: int = 0) -> Context:
+    ctxs = getattr(_tls, "ctxs", None)
+    if ctxs is None:
+        ctxs = _tls.ctxs = {}
+    if device not in ctxs:
+        ctxs[device] = Context(device)
+    return ctxs[device]
+
+
+def _as_f64(x) -> np.ndarray:
+    if isinstance(x, Series):
+        return x.view()
+    return np.ascontiguousarray(np.asarray(x, dtype=np.float64).reshape(-1))
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(_dp)
+
+
+def _window(band) -> int:
+    if band is None:
+        return UNBOUNDED_WINDOW
+    if isinstance(band, Band):
+        return band.window
+    return int(band)
+
+
+# --- DTW kernels (dtw.hpp:69-99) --------------------------------------------
+
+def ea_pruned_dtw_windowed(a, b, band, ub: float, cumulative_bound=(), *, ctx=None,
+                           return_cells: bool = False):
+    """dtw.hpp:93-99.  Exact DTW if it is <= ub, else PRUNED."""
+    ctx = ctx or default_context()
+    a, b = _as_f64(a), _as_f64(b)
+    cb = _as_f64(cumulative_bound) if len(cumulative_bound) else None
+    out = C.c_double()
+    cells = C.c_uint64(0)
+    check(lib.eapdtw_ea_pruned_dtw_windowed(
+        ctx.handle, _ptr(a), a.size, _ptr(b), b.size, _window(band), float(ub),
+        _ptr(cb) if cb is not None else None, 0 if cb is None else cb.size, C.byref(out),
+        C.byref(cells)))
+    return (out.value, cells.value) if return_cells else out.value
+
+
+def ea_pruned_dtw(a, b, ub: float, *, ctx=None, return_cells: bool = False):
+    """dtw.hpp:85-87 (unbounded band)."""
+    return ea_pruned_dtw_windowed(a, b, Band.unbounded(), ub, ctx=ctx, return_cells=return_cells)
+
+
+def dtw_windowed(a, b, band, *, ctx=None, return_cells: bool = False):
+    """dtw.hpp:72-74: the plain banded DP (no abandoning)."""
+    ctx = ctx or default_context()
+    a, b = _as_f64(a), _as_f64(b)
+    out = C.c_double()
+    cells = C.c_uint64(0)
+    check(lib.eapdtw_dtw_windowed(ctx.handle, _ptr(a), a.size, _ptr(b), b.size, _window(band),
+                                  C.byref(out), C.byref(cells)))
+    return (out.value, cells.value) if return_cells else out.value
+
+
+def dtw_full(a, b, *, ctx=None):
+    """dtw.hpp:69-70"""
+    return dtw_windowed(a, b, Band.unbounded(), ctx=ctx)
+
+
+def pairwise(a, b, band, ub=None, *, prune: bool = True, ctx=None):
+    """cfg1 batch: ``out[p] = ea_pruned_dtw_windowed(a[p], b[p], band, ub[p])``.
+
+    a, b: (npairs, len) float64 host arrays.  Returns (out, cells)."""
+    ctx = ctx or default_context()
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    if a.shape != b.shape or a.ndim != 2:
+        raise ValueError("pairwise: a and b must be (npairs, len) of equal shape")
+    n, L = a.shape
+    out = np.empty(n)
+    cells = C.c_uint64(0)
+    ubp = None
+    if ub is not None:
+        ub = np.ascontiguousarray(ub, dtype=np.float64)
+        ubp = _ptr(ub)
+    check(lib.eapdtw_pairwise(ctx.handle, _ptr(a), _ptr(b), n, L, _window(band), ubp,
+                              int(prune), out.ctypes.data_as(_dp), C.byref(cells)))
+    return out, cells.value
+
+
+def nn1(queries, db, band=None, *, ctx=None):
+    """cfg5 batch: per query the lowest-index argmin of
+    ``ea_pruned_dtw_windowed(db[k], q, band, bsf)`` with a running cutoff.
+    Returns (argmin uint64[nq], dist float64[nq], cells)."""
+    ctx = ctx or default_context()
+    q = np.ascontiguousarray(queries, dtype=np.float64)
+    d = np.ascontiguousarray(db, dtype=np.float64)
+    if q.ndim != 2 or d.ndim != 2 or q.shape[1] != d.shape[1]:
+        raise ValueError("nn1: queries (nq, len) and db (nd, len) must share len")
+    arg = np.empty(q.shape[0], dtype=np.uint64)
+    dist = np.empty(q.shape[0])
+    cells = C.c_uint64(0)
+    check(lib.eapdtw_nn1(ctx.handle, _ptr(q), q.shape[0], _ptr(d), d.shape[0], q.shape[1],
+                         _window(band), arg.ctypes.data_as(_u64p), dist.ctypes.data_as(_dp),
+                         C.byref(cells)))
+    return arg, dist, cells.value
+
+
+# --- search (search.hpp:118-119) ---------------------------------------------
+
+def similarity_search(reference, query, cfg: SearchConfig | None = None, *, ctx=None
+                      ) -> SearchResult:
+    """Nearest z-normalised subsequence of ``reference`` under windowed DTW."""
+    ctx = ctx or default_context()
+    cfg = cfg or SearchConfig()
+    ref = reference.view() if isinstance(reference, Series) else Series(reference).view()
+    q = query.view() if isinstance(query, Series) else Series(query).view()
+    res = _capi.SearchResultC()
+    c = cfg.to_c()
+    check(lib.eapdtw_similarity_search(ctx.handle, _ptr(ref), ref.size, _ptr(q), q.size,
+                                       C.byref(c), C.byref(res)))
+    return SearchResult.from_c(res)
+
+
+def similarity_search_dev(ref_dev_ptr: int, n: int, query, cfg: SearchConfig, *, ctx=None
+                          ) -> SearchResult:
+    """Same as similarity_search with the reference already resident in HBM."""
+    ctx = ctx or default_context()
+    q = _as_f64(query)
+    res = _capi.SearchResultC()
+    c = cfg.to_c()
+    check(lib.eapdtw_similarity_search_dev(ctx.handle, C.c_void_p(ref_dev_ptr), int(n), _ptr(q),
+                                           q.size, C.byref(c), C.byref(res)))
+    return SearchResult.from_c(res)
+
+
+class SearchPlan:
+    """One shard of a (possibly multi-GPU) search: stepped C-ABI plan."""
+
+    def __init__(self, ref_dev_ptr: int, n: int, query, cfg: SearchConfig, global_offset: int = 0,
+                 *, ctx=None):
+        self.ctx = ctx or default_context()
+        q = _as_f64(query)
+        self._q = q
+        c = cfg.to_c()
+        h = C.c_void_p()
+        check(lib.eapdtw_search_plan_create(self.ctx.handle, C.c_void_p(ref_dev_ptr), int(n),
+                                            _ptr(q), q.size, C.byref(c), int(global_offset),
+                                            C.byref(h)))
+        self.handle = h
+
+    @property
+    def candidates(self) -> int:
+        return int(lib.eapdtw_search_plan_candidates(self.handle))
+
+    @property
+    def ub_key_ptr(self) -> int:
+        return int(lib.eapdtw_search_plan_ub_key(self.handle))
+
+    def prepare(self):
+        check(lib.eapdtw_search_plan_prepare(self.handle))
+
+    def run(self, begin: int, end: int):
+        check(lib.eapdtw_search_plan_run(self.handle, int(begin), int(end)))
+
+    def result(self) -> SearchResult:
+        res = _capi.SearchResultC()
+        check(lib.eapdtw_search_plan_result(self.handle, C.byref(res)))
+        return SearchResult.from_c(res)
+
+    def timings(self):
+        ms = (C.c_float * 4)()
+        check(lib.eapdtw_search_plan_timings(self.handle, ms))
+        return {"stats": ms[0], "envelope": ms[1], "probe": ms[2], "sweep": ms[3]}
+
+    def close(self):
+        if self.handle:
+            lib.eapdtw_search_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# --- host helpers ------------------------------------------------------------
+
+def znormalize(x) -> np.ndarray:
+    """RunningStats::over + znormalize_into (search.cpp:25-46), bit-identical."""
+    x = _as_f64(x)
+    out = np.empty_like(x)
+    check(lib.eapdtw_znormalize(_ptr(x), x.size, _ptr(out)))
+    return out
+
+
+def random_walk(n: int, seed: int) -> np.ndarray:
+    """The reference's random_walk (io.cpp:124-137): uniform steps in [-0.5, 0.5)."""
+    out = np.empty(int(n))
+    check(lib.eapdtw_random_walk_uniform(int(n), int(seed), _ptr(out)))
+    return out
+
+
+def random_walk_normal(n: int, seed: int) -> np.ndarray:
+    """Benchmark data: x0 = 0, increments i.i.d. N(0,1) (mt19937_64 + Box-Muller)."""
+    out = np.empty(int(n))
+    check(lib.eapdtw_random_walk_normal(int(n), int(seed), _ptr(out)))
+    return out
+
+
+def window_cells_for(ratio: float, m: int) -> int:
+    """search.cpp:18-21"""
+    w = math.floor(ratio * float(m))
+    return 0 if w <= 0.0 else int(w)

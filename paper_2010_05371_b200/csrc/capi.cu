@@ -1,0 +1,781 @@
+// capi.cu -- host orchestration behind the C ABI (include/eapdtw_b200.h).
+//
+// Everything here is host C++: argument validation mirroring the reference's
+// std::invalid_argument conditions, the exact host-side query preparation of
+// similarity_search (search.cpp:131-149), device buffer management, the phase
+// sequencing of a search (stats -> envelope -> probe -> sweep) and result
+// read-back.  The compute itself is in kernels.cu.  There is no CPU fallback.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <numeric>
+#include <random>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/eapdtw_b200.h"
+#include "kernels.cuh"
+
+using namespace eapdtw_b200;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = (expr);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(EAPDTW_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));     \
+  } while (0)
+
+constexpr double kInf = std::numeric_limits<double>::infinity();
+
+// Grow-only device buffer.
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t n) {
+    if (n <= bytes) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&p, n);
+    if (e == cudaSuccess) bytes = n;
+    return e;
+  }
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+};
+
+// RunningStats (search.hpp:16-42) on the host, same operation order.
+struct HostStats {
+  double sum = 0.0, sumsq = 0.0;
+  size_t count = 0;
+  static HostStats over(const double* x, size_t n) {
+    HostStats s;
+    for (size_t i = 0; i < n; ++i) {
+      s.sum += x[i];
+      s.sumsq += x[i] * x[i];
+    }
+    s.count = n;
+    return s;
+  }
+  double mean() const { return sum / static_cast<double>(count); }
+  double stddev() const {
+    const double m = mean();
+    const double v = sumsq / static_cast<double>(count) - m * m;
+    return std::sqrt(v > 0.0 ? v : 0.0);
+  }
+};
+
+// znormalize_into (search.cpp:37-46)
+void host_znormalize(const double* src, size_t n, const HostStats& st, double* dst) {
+  const double m = st.mean();
+  const double s = st.stddev();
+  if (s < kMinStddev) {
+    std::fill(dst, dst + n, 0.0);
+    return;
+  }
+  for (size_t i = 0; i < n; ++i) dst[i] = (src[i] - m) / s;
+}
+
+bool all_finite(const double* x, size_t n) {
+  for (size_t i = 0; i < n; ++i)
+    if (!std::isfinite(x[i])) return false;
+  return true;
+}
+
+}  // namespace
+
+struct eapdtw_ctx {
+  int device = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  uint64_t launches = 0;
+  // scratch for pairwise / nn1 host-pointer variants
+  DevBuf a, b, ub, cb, out, cells, best, keys, counters;
+  DevBuf ref;  // host-pointer search copies the reference here
+};
+
+struct eapdtw_search_plan {
+  eapdtw_ctx* ctx = nullptr;
+  const double* ref = nullptr;  // device
+  size_t n = 0, m = 0, w_cells = 0;
+  int w_eff = 0;
+  int env_r = 0;
+  bool use_lb = true, have_env = false;
+  int algo = EAPDTW_ALGO_EA_PRUNED;
+  uint64_t offset = 0;
+  size_t ncand = 0;
+  DevBuf mean, sd, up, lo, q, qu, ql, order, best, key, work, counters, probe_counters;
+  cudaEvent_t ev[8] = {};
+  bool prepared = false;
+  int blocks = 0, warps = 8;
+  double guard_rel = 1e-9, guard_abs = 1e-20;
+  std::chrono::steady_clock::time_point t0;
+};
+
+extern "C" {
+
+const char* eapdtw_last_error(void) { return g_err.c_str(); }
+int eapdtw_version(void) { return 1; }
+
+int eapdtw_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+int eapdtw_ctx_create(eapdtw_ctx** out, int device) {
+  if (!out) return fail(EAPDTW_EINVAL, "ctx_create: null out");
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    return fail(EAPDTW_ECUDA, "no CUDA device: the B200 path has no CPU fallback");
+  if (device < 0 || device >= n) return fail(EAPDTW_EINVAL, "ctx_create: bad device");
+  CUDA_TRY(cudaSetDevice(device));
+  auto* c = new eapdtw_ctx();
+  c->device = device;
+  e = cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(EAPDTW_ECUDA, cudaGetErrorString(e));
+  }
+  c->stream = c->own;
+  *out = c;
+  return EAPDTW_OK;
+}
+
+int eapdtw_ctx_destroy(eapdtw_ctx* c) {
+  if (!c) return EAPDTW_OK;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (DevBuf* b : {&c->a, &c->b, &c->ub, &c->cb, &c->out, &c->cells, &c->best, &c->keys,
+                    &c->counters, &c->ref})
+    b->release();
+  if (c->own) cudaStreamDestroy(c->own);
+  delete c;
+  return EAPDTW_OK;
+}
+
+int eapdtw_ctx_set_stream(eapdtw_ctx* c, void* s) {
+  if (!c) return fail(EAPDTW_EINVAL, "null ctx");
+  c->stream = s ? static_cast<cudaStream_t>(s) : c->own;
+  return EAPDTW_OK;
+}
+
+int eapdtw_ctx_synchronize(eapdtw_ctx* c) {
+  if (!c) return fail(EAPDTW_EINVAL, "null ctx");
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return EAPDTW_OK;
+}
+
+uint64_t eapdtw_ctx_launches(const eapdtw_ctx* c) { return c ? c->launches : 0; }
+
+// ---------------------------------------------------------------------------
+// Pairwise
+// ---------------------------------------------------------------------------
+static int pairwise_impl(eapdtw_ctx* c, const double* rows_dev, const double* cols_dev,
+                         size_t npairs, size_t lr, size_t lc, size_t window, const double* ub_dev,
+                         const double* cb_dev, int prune, double* out_dev, uint64_t* cells) {
+  // effective_window (dtw.cpp:57-62): caller guarantees lr >= lc.
+  int w;
+  if (window == EAPDTW_UNBOUNDED_WINDOW || window >= lc) w = static_cast<int>(lr);
+  else w = static_cast<int>(window);
+  CUDA_TRY(c->cells.ensure(sizeof(unsigned long long)));
+  CUDA_TRY(cudaMemsetAsync(c->cells.p, 0, sizeof(unsigned long long), c->stream));
+  PairParams p{};
+  p.rows = rows_dev;
+  p.cols = cols_dev;
+  p.row_stride = static_cast<long long>(lr);
+  p.col_stride = static_cast<long long>(lc);
+  p.lr = static_cast<int>(lr);
+  p.lc = static_cast<int>(lc);
+  p.w = w;
+  p.ub = ub_dev;
+  p.cb = cb_dev;
+  p.prune = prune;
+  p.out = out_dev;
+  p.cells = c->cells.as<unsigned long long>();
+  p.npairs = static_cast<long long>(npairs);
+  CUDA_TRY(launch_pairwise(p, c->stream));
+  ++c->launches;
+  if (cells) {
+    unsigned long long h = 0;
+    CUDA_TRY(cudaMemcpyAsync(&h, c->cells.p, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    *cells = h;
+  }
+  return EAPDTW_OK;
+}
+
+static int check_cb_host(const double* cb, size_t cb_len, size_t lr) {
+  // check_cumulative_bound (dtw.cpp:64-75)
+  if (cb_len == 0) return EAPDTW_OK;
+  if (cb_len != lr)
+    return fail(EAPDTW_EINVAL, "cumulative bound: length must match the longer series");
+  for (size_t k = 0; k + 1 < cb_len; ++k)
+    if (!(cb[k] >= cb[k + 1])) return fail(EAPDTW_EINVAL, "cumulative bound: must be non-increasing");
+  if (cb[cb_len - 1] != 0.0) return fail(EAPDTW_EINVAL, "cumulative bound: final element must be 0");
+  return EAPDTW_OK;
+}
+
+static int single_pair(eapdtw_ctx* c, const double* a, size_t la, const double* b, size_t lb,
+                       size_t window, double ub, const double* cb, size_t cb_len, int prune,
+                       double* out, uint64_t* cells) {
+  if (!c) return fail(EAPDTW_EINVAL, "null ctx");
+  if (la == 0 || lb == 0 || !a || !b || !out) return fail(EAPDTW_EINVAL, "dtw: empty series");
+  // orient (dtw.cpp:48-52): longer series on rows, first argument wins ties
+  const double* rows = a;
+  const double* cols = b;
+  size_t lr = la, lc = lb;
+  if (la < lb) {
+    rows = b;
+    cols = a;
+    lr = lb;
+    lc = la;
+  }
+  if (prune) {
+    const int e = check_cb_host(cb, cb_len, lr);
+    if (e) return e;
+  }
+  if (window != EAPDTW_UNBOUNDED_WINDOW && lr - lc > window) {  // no path fits the band
+    *out = kInf;
+    if (cells) *cells = 0;
+    return EAPDTW_OK;
+  }
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(c->a.ensure(lr * 8));
+  CUDA_TRY(c->b.ensure(lc * 8));
+  CUDA_TRY(c->ub.ensure(8));
+  CUDA_TRY(c->out.ensure(8));
+  CUDA_TRY(cudaMemcpyAsync(c->a.p, rows, lr * 8, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->b.p, cols, lc * 8, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->ub.p, &ub, 8, cudaMemcpyHostToDevice, c->stream));
+  const double* cb_dev = nullptr;
+  if (prune && cb_len) {
+    CUDA_TRY(c->cb.ensure(cb_len * 8));
+    CUDA_TRY(cudaMemcpyAsync(c->cb.p, cb, cb_len * 8, cudaMemcpyHostToDevice, c->stream));
+    cb_dev = c->cb.as<double>();
+  }
+  uint64_t ncell = 0;
+  const int e = pairwise_impl(c, c->a.as<double>(), c->b.as<double>(), 1, lr, lc, window,
+                              c->ub.as<double>(), cb_dev, prune, c->out.as<double>(), &ncell);
+  if (e) return e;
+  CUDA_TRY(cudaMemcpyAsync(out, c->out.p, 8, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (cells) *cells = ncell;
+  return EAPDTW_OK;
+}
+
+int eapdtw_ea_pruned_dtw_windowed(eapdtw_ctx* c, const double* a, size_t la, const double* b,
+                                  size_t lb, size_t window, double ub, const double* cb,
+                                  size_t cb_len, double* out, uint64_t* cells) {
+  return single_pair(c, a, la, b, lb, window, ub, cb, cb_len, 1, out, cells);
+}
+
+int eapdtw_dtw_windowed(eapdtw_ctx* c, const double* a, size_t la, const double* b, size_t lb,
+                        size_t window, double* out, uint64_t* cells) {
+  return single_pair(c, a, la, b, lb, window, kInf, nullptr, 0, 0, out, cells);
+}
+
+int eapdtw_pairwise_dev(eapdtw_ctx* c, const double* a_dev, const double* b_dev, size_t npairs,
+                        size_t len, size_t window, const double* ub_dev, int prune,
+                        double* out_dev, uint64_t* cells) {
+  if (!c) return fail(EAPDTW_EINVAL, "null ctx");
+  if (len == 0) return fail(EAPDTW_EINVAL, "dtw: empty series");
+  if (npairs == 0) return EAPDTW_OK;
+  CUDA_TRY(cudaSetDevice(c->device));
+  return pairwise_impl(c, a_dev, b_dev, npairs, len, len, window, ub_dev, nullptr, prune, out_dev,
+                       cells);
+}
+
+int eapdtw_pairwise(eapdtw_ctx* c, const double* a, const double* b, size_t npairs, size_t len,
+                    size_t window, const double* ub, int prune, double* out, uint64_t* cells) {
+  if (!c) return fail(EAPDTW_EINVAL, "null ctx");
+  if (len == 0) return fail(EAPDTW_EINVAL, "dtw: empty series");
+  if (npairs == 0) return EAPDTW_OK;
+  CUDA_TRY(cudaSetDevice(c->device));
+  const size_t bytes = npairs * len * 8;
+  CUDA_TRY(c->a.ensure(bytes));
+  CUDA_TRY(c->b.ensure(bytes));
+  CUDA_TRY(c->out.ensure(npairs * 8));
+  CUDA_TRY(cudaMemcpyAsync(c->a.p, a, bytes, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->b.p, b, bytes, cudaMemcpyHostToDevice, c->stream));
+  const double* ub_dev = nullptr;
+  if (ub) {
+    CUDA_TRY(c->ub.ensure(npairs * 8));
+    CUDA_TRY(cudaMemcpyAsync(c->ub.p, ub, npairs * 8, cudaMemcpyHostToDevice, c->stream));
+    ub_dev = c->ub.as<double>();
+  }
+  const int e = pairwise_impl(c, c->a.as<double>(), c->b.as<double>(), npairs, len, len, window,
+                              ub_dev, nullptr, prune, c->out.as<double>(), cells);
+  if (e) return e;
+  CUDA_TRY(cudaMemcpyAsync(out, c->out.p, npairs * 8, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return EAPDTW_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Search plan
+// ---------------------------------------------------------------------------
+int eapdtw_search_plan_create(eapdtw_ctx* c, const double* ref_dev, size_t n, const double* query,
+                              size_t qlen, const eapdtw_search_config* cfg, uint64_t offset,
+                              eapdtw_search_plan** out) {
+  if (!c || !cfg || !out) return fail(EAPDTW_EINVAL, "search: null argument");
+  if (n == 0 || qlen == 0 || !query) return fail(EAPDTW_EINVAL, "Series: empty input");
+  // similarity_search validation (search.cpp:121-127)
+  const size_t m = cfg->query_length == 0 ? qlen : cfg->query_length;
+  if (m == 0 || m > qlen) return fail(EAPDTW_EINVAL, "similarity_search: bad query length");
+  if (m > n) return fail(EAPDTW_EINVAL, "similarity_search: query longer than reference");
+  if (!all_finite(query, qlen)) return fail(EAPDTW_EINVAL, "Series: non-finite sample");
+  if (offset % static_cast<uint64_t>(kStatsResetInterval) != 0)
+    return fail(EAPDTW_EINVAL, "search plan: shard offset must be a multiple of 100000");
+  if (m > (1u << 20)) return fail(EAPDTW_EINVAL, "search: query length above the GPU limit");
+  CUDA_TRY(cudaSetDevice(c->device));
+
+  auto* p = new eapdtw_search_plan();
+  p->t0 = std::chrono::steady_clock::now();
+  p->ctx = c;
+  p->ref = ref_dev;
+  p->n = n;
+  p->m = m;
+  p->offset = offset;
+  p->use_lb = cfg->use_lower_bounds != 0;
+  p->algo = cfg->algorithm;
+  p->ncand = n - m + 1;
+  // window_cells_for (search.cpp:18-21)
+  const double wf = std::floor(cfg->window_ratio * static_cast<double>(m));
+  p->w_cells = wf <= 0.0 ? 0 : static_cast<size_t>(wf);
+  // effective_window for two length-m series (dtw.cpp:57-62)
+  p->w_eff = p->w_cells >= m ? static_cast<int>(m) : static_cast<int>(p->w_cells);
+  p->env_r = static_cast<int>(std::min(p->w_cells, m));  // compute_envelope clamp (lower_bounds.cpp:12)
+  p->guard_rel = std::max(1e-9, 8.0 * static_cast<double>(m) * 0x1.0p-53);
+  p->guard_abs = 1e-20;
+
+  // Query preparation exactly as search.cpp:136-149.
+  std::vector<double> qn(m), qu(m), ql(m), q1(m + 1, 0.0);
+  host_znormalize(query, m, HostStats::over(query, m), qn.data());
+  const size_t r = p->env_r;
+  for (size_t j = 0; j < m; ++j) {  // compute_envelope (lower_bounds.cpp:9-49): exact max/min
+    const size_t lo = j > r ? j - r : 0;
+    const size_t hi = std::min(m - 1, j + r);
+    double mx = qn[lo], mn = qn[lo];
+    for (size_t k = lo + 1; k <= hi; ++k) {
+      mx = std::max(mx, qn[k]);
+      mn = std::min(mn, qn[k]);
+    }
+    qu[j] = mx;
+    ql[j] = mn;
+  }
+  std::vector<int> order(m);
+  std::iota(order.begin(), order.end(), 0);
+  std::sort(order.begin(), order.end(), [&](int a, int b) {
+    const double fa = std::fabs(qn[a]), fb = std::fabs(qn[b]);
+    return fa != fb ? fa > fb : a < b;
+  });
+  std::copy(qn.begin(), qn.end(), q1.begin() + 1);
+
+  const size_t nc = p->ncand;
+  cudaError_t e = cudaSuccess;
+  auto chk = [&](cudaError_t x) {
+    if (x != cudaSuccess && e == cudaSuccess) e = x;
+  };
+  chk(p->mean.ensure(nc * 8));
+  chk(p->sd.ensure(nc * 8));
+  chk(p->q.ensure((m + 1) * 8));
+  chk(p->qu.ensure(m * 8));
+  chk(p->ql.ensure(m * 8));
+  chk(p->order.ensure(m * 4));
+  chk(p->best.ensure(sizeof(BestRecord)));
+  chk(p->key.ensure(8));
+  chk(p->work.ensure(8));
+  chk(p->counters.ensure(kNumCounters * 8));
+  chk(p->probe_counters.ensure(kNumCounters * 8));
+  if (p->use_lb) {
+    chk(p->up.ensure(n * 8));
+    chk(p->lo.ensure(n * 8));
+  }
+  for (auto& ev : p->ev) chk(cudaEventCreate(&ev));
+  if (e == cudaSuccess) {
+    cudaStream_t s = c->stream;
+    chk(cudaMemcpyAsync(p->q.p, q1.data(), (m + 1) * 8, cudaMemcpyHostToDevice, s));
+    chk(cudaMemcpyAsync(p->qu.p, qu.data(), m * 8, cudaMemcpyHostToDevice, s));
+    chk(cudaMemcpyAsync(p->ql.p, ql.data(), m * 8, cudaMemcpyHostToDevice, s));
+    chk(cudaMemcpyAsync(p->order.p, order.data(), m * 4, cudaMemcpyHostToDevice, s));
+    chk(cudaMemsetAsync(p->counters.p, 0, kNumCounters * 8, s));
+    chk(cudaMemsetAsync(p->probe_counters.p, 0, kNumCounters * 8, s));
+    chk(launch_init_best(p->best.as<BestRecord>(), p->key.as<unsigned long long>(), 1, s));
+    ++c->launches;
+    // q, qu, ql and order are staged from pageable vectors: make sure the
+    // copies have consumed them before they go out of scope.
+    chk(cudaStreamSynchronize(s));
+  }
+  // Occupancy-sized persistent grid.
+  const size_t smem = search_smem_bytes(static_cast<int>(m), p->warps);
+  int per_sm = 0;
+  if (smem > 200 * 1024) {
+    p->warps = 4;
+  }
+  if (e == cudaSuccess) {
+    int dev_sms = 148;
+    cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
+    const size_t sm2 = search_smem_bytes(static_cast<int>(m), p->warps);
+    if (sm2 > 227 * 1024) {
+      e = cudaErrorInvalidValue;
+    } else {
+      per_sm = 1;
+      cudaFuncAttributes fa{};
+      (void)fa;
+      int max_smem = 0;
+      cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, c->device);
+      per_sm = std::max(1, std::min(static_cast<int>(max_smem / (sm2 + 1024)), 64 / p->warps));
+      p->blocks = dev_sms * per_sm;
+    }
+  }
+  if (e != cudaSuccess) {
+    eapdtw_search_plan_destroy(p);
+    return fail(EAPDTW_ECUDA, std::string("search plan: ") + cudaGetErrorString(e));
+  }
+  *out = p;
+  return EAPDTW_OK;
+}
+
+size_t eapdtw_search_plan_candidates(const eapdtw_search_plan* p) { return p ? p->ncand : 0; }
+uint64_t* eapdtw_search_plan_ub_key(eapdtw_search_plan* p) {
+  return p ? p->key.as<uint64_t>() : nullptr;
+}
+
+static SearchParams base_params(eapdtw_search_plan* p) {
+  SearchParams s{};
+  s.ref = p->ref;
+  s.mean = p->mean.as<double>();
+  s.sd = p->sd.as<double>();
+  s.env_up = p->have_env ? p->up.as<double>() : nullptr;
+  s.env_lo = p->have_env ? p->lo.as<double>() : nullptr;
+  s.q = p->q.as<double>();
+  s.qu = p->qu.as<double>();
+  s.ql = p->ql.as<double>();
+  s.order = p->order.as<int>();
+  s.ncand = static_cast<long long>(p->ncand);
+  s.m = static_cast<int>(p->m);
+  s.w = p->w_eff;
+  s.use_lb = p->use_lb ? 1 : 0;
+  s.prune = p->algo == EAPDTW_ALGO_FULL ? 0 : 1;
+  s.guard_rel = p->guard_rel;
+  s.guard_abs = p->guard_abs;
+  s.ub_key = p->key.as<unsigned long long>();
+  s.best = p->best.as<BestRecord>();
+  s.work = p->work.as<unsigned long long>();
+  s.counters = p->counters.as<unsigned long long>();
+  s.index_offset = static_cast<long long>(p->offset);
+  return s;
+}
+
+int eapdtw_search_plan_prepare(eapdtw_search_plan* p) {
+  if (!p) return fail(EAPDTW_EINVAL, "null plan");
+  eapdtw_ctx* c = p->ctx;
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t s = c->stream;
+  CUDA_TRY(cudaEventRecord(p->ev[0], s));
+  CUDA_TRY(launch_stats(p->ref, static_cast<long long>(p->n), static_cast<int>(p->m),
+                        p->mean.as<double>(), p->sd.as<double>(), s));
+  ++c->launches;
+  CUDA_TRY(cudaEventRecord(p->ev[1], s));
+  p->have_env = false;
+  if (p->use_lb && p->m >= 2) {
+    const cudaError_t e = launch_envelope(p->ref, static_cast<long long>(p->n), p->env_r,
+                                          p->up.as<double>(), p->lo.as<double>(), s);
+    if (e == cudaSuccess) {
+      p->have_env = true;
+      ++c->launches;
+    } else if (e != cudaErrorInvalidValue) {
+      return fail(EAPDTW_ECUDA, std::string("envelope: ") + cudaGetErrorString(e));
+    } else {
+      cudaGetLastError();  // window too wide for the tile: EC tier skipped
+    }
+  }
+  CUDA_TRY(cudaEventRecord(p->ev[2], s));
+  // Probe: evaluate evenly spaced candidates first (no lower bounds, running
+  // threshold) so the sweep starts from a finite best-so-far.  Probe hits are
+  // real candidates, so they legitimately enter the (d, index) record.
+  const size_t nprobe = std::min<size_t>(2048, std::max<size_t>(1, p->ncand / 64));
+  SearchParams sp = base_params(p);
+  sp.use_lb = 0;
+  sp.begin = 0;
+  sp.stride = static_cast<long long>(std::max<size_t>(1, p->ncand / nprobe));
+  sp.end = std::min<long long>(static_cast<long long>(p->ncand), sp.stride * static_cast<long long>(nprobe));
+  sp.counters = p->probe_counters.as<unsigned long long>();
+  CUDA_TRY(cudaMemsetAsync(p->work.p, 0, 8, s));
+  const long long probe_warps = (static_cast<long long>(nprobe) + 31) / 32;
+  const int pblocks = static_cast<int>(std::max<long long>(1, std::min<long long>(p->blocks, (probe_warps + p->warps - 1) / p->warps)));
+  CUDA_TRY(launch_search(sp, pblocks, p->warps, s));
+  ++c->launches;
+  CUDA_TRY(cudaEventRecord(p->ev[3], s));
+  p->prepared = true;
+  return EAPDTW_OK;
+}
+
+int eapdtw_search_plan_run(eapdtw_search_plan* p, size_t begin, size_t end) {
+  if (!p) return fail(EAPDTW_EINVAL, "null plan");
+  if (!p->prepared) {
+    const int e = eapdtw_search_plan_prepare(p);
+    if (e) return e;
+  }
+  end = std::min(end, p->ncand);
+  if (begin >= end) return EAPDTW_OK;
+  eapdtw_ctx* c = p->ctx;
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t s = c->stream;
+  SearchParams sp = base_params(p);
+  sp.begin = static_cast<long long>(begin);
+  sp.end = static_cast<long long>(end);
+  sp.stride = 1;
+  CUDA_TRY(cudaEventRecord(p->ev[4], s));
+  CUDA_TRY(cudaMemsetAsync(p->work.p, 0, 8, s));
+  CUDA_TRY(launch_search(sp, p->blocks, p->warps, s));
+  ++c->launches;
+  CUDA_TRY(cudaEventRecord(p->ev[5], s));
+  return EAPDTW_OK;
+}
+
+int eapdtw_search_plan_result(eapdtw_search_plan* p, eapdtw_search_result* out) {
+  if (!p || !out) return fail(EAPDTW_EINVAL, "null argument");
+  eapdtw_ctx* c = p->ctx;
+  CUDA_TRY(cudaSetDevice(c->device));
+  BestRecord rec{};
+  unsigned long long cnt[kNumCounters], pc[kNumCounters];
+  CUDA_TRY(cudaMemcpyAsync(&rec, p->best.p, sizeof(rec), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(cnt, p->counters.p, sizeof(cnt), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(pc, p->probe_counters.p, sizeof(pc), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  std::memset(out, 0, sizeof(*out));
+  out->found = rec.d != kInf ? 1 : 0;
+  out->distance_sq = rec.d;
+  out->location = out->found ? rec.idx : 0;
+  out->candidates_total = cnt[kCntCandidates];
+  out->pruned_kim = cnt[kCntKim];
+  out->pruned_keogh_eq = cnt[kCntKeoghEq];
+  out->pruned_keogh_ec = cnt[kCntKeoghEc];
+  out->dtw_calls = out->candidates_total - out->pruned_kim - out->pruned_keogh_eq - out->pruned_keogh_ec;
+  out->dtw_abandoned = cnt[kCntDtwAbandoned];
+  out->dp_cells_evaluated = cnt[kCntCells] + pc[kCntCells];
+  out->elapsed_seconds =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - p->t0).count();
+  return EAPDTW_OK;
+}
+
+int eapdtw_search_plan_timings(eapdtw_search_plan* p, float* ms4) {
+  if (!p || !ms4) return fail(EAPDTW_EINVAL, "null argument");
+  CUDA_TRY(cudaSetDevice(p->ctx->device));
+  CUDA_TRY(cudaEventSynchronize(p->ev[5]));
+  CUDA_TRY(cudaEventElapsedTime(&ms4[0], p->ev[0], p->ev[1]));
+  CUDA_TRY(cudaEventElapsedTime(&ms4[1], p->ev[1], p->ev[2]));
+  CUDA_TRY(cudaEventElapsedTime(&ms4[2], p->ev[2], p->ev[3]));
+  CUDA_TRY(cudaEventElapsedTime(&ms4[3], p->ev[4], p->ev[5]));
+  return EAPDTW_OK;
+}
+
+int eapdtw_search_plan_destroy(eapdtw_search_plan* p) {
+  if (!p) return EAPDTW_OK;
+  cudaSetDevice(p->ctx->device);
+  cudaStreamSynchronize(p->ctx->stream);
+  for (DevBuf* b : {&p->mean, &p->sd, &p->up, &p->lo, &p->q, &p->qu, &p->ql, &p->order, &p->best,
+                    &p->key, &p->work, &p->counters, &p->probe_counters})
+    b->release();
+  for (auto& ev : p->ev)
+    if (ev) cudaEventDestroy(ev);
+  delete p;
+  return EAPDTW_OK;
+}
+
+int eapdtw_similarity_search_dev(eapdtw_ctx* c, const double* ref_dev, size_t n,
+                                 const double* query, size_t qlen,
+                                 const eapdtw_search_config* cfg, eapdtw_search_result* out) {
+  if (!out) return fail(EAPDTW_EINVAL, "null out");
+  eapdtw_search_plan* p = nullptr;
+  int e = eapdtw_search_plan_create(c, ref_dev, n, query, qlen, cfg, 0, &p);
+  if (e) return e;
+  e = eapdtw_search_plan_prepare(p);
+  if (!e) e = eapdtw_search_plan_run(p, 0, p->ncand);
+  if (!e) e = eapdtw_search_plan_result(p, out);
+  eapdtw_search_plan_destroy(p);
+  return e;
+}
+
+int eapdtw_similarity_search(eapdtw_ctx* c, const double* ref, size_t n, const double* query,
+                             size_t qlen, const eapdtw_search_config* cfg,
+                             eapdtw_search_result* out) {
+  if (!c || !ref) return fail(EAPDTW_EINVAL, "null argument");
+  if (n == 0) return fail(EAPDTW_EINVAL, "Series: empty input");
+  if (!all_finite(ref, n)) return fail(EAPDTW_EINVAL, "Series: non-finite sample");
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(c->ref.ensure(n * 8));
+  CUDA_TRY(cudaMemcpyAsync(c->ref.p, ref, n * 8, cudaMemcpyHostToDevice, c->stream));
+  return eapdtw_similarity_search_dev(c, c->ref.as<double>(), n, query, qlen, cfg, out);
+}
+
+// ---------------------------------------------------------------------------
+// NN1
+// ---------------------------------------------------------------------------
+static int nn1_impl(eapdtw_ctx* c, const double* q_dev, size_t nq, const double* db_dev,
+                    size_t nd, size_t len, size_t window, uint64_t* argmin, double* dist,
+                    uint64_t* cells) {
+  int w = (window == EAPDTW_UNBOUNDED_WINDOW || window >= len) ? static_cast<int>(len)
+                                                              : static_cast<int>(window);
+  cudaStream_t s = c->stream;
+  CUDA_TRY(c->best.ensure(nq * sizeof(BestRecord)));
+  CUDA_TRY(c->keys.ensure(nq * 8));
+  CUDA_TRY(c->counters.ensure(2 * 8));
+  CUDA_TRY(cudaMemsetAsync(c->counters.p, 0, 16, s));
+  CUDA_TRY(launch_init_best(c->best.as<BestRecord>(), c->keys.as<unsigned long long>(),
+                            static_cast<long long>(nq), s));
+  ++c->launches;
+  Nn1Params p{};
+  p.queries = q_dev;
+  p.db = db_dev;
+  p.nq = static_cast<long long>(nq);
+  p.nd = static_cast<long long>(nd);
+  p.len = static_cast<int>(len);
+  p.w = w;
+  // Enough blocks to fill the GPU a few times over, but keep each query's
+  // database sweep wide enough to share a cutoff.
+  const long long target = 148LL * 8;
+  p.splits = static_cast<int>(std::max<long long>(1, std::min<long long>(
+      static_cast<long long>(nd) / 64 + 1, (target + static_cast<long long>(nq) - 1) / static_cast<long long>(nq))));
+  p.ub_keys = c->keys.as<unsigned long long>();
+  p.best = c->best.as<BestRecord>();
+  p.cells = c->counters.as<unsigned long long>();
+  p.dtw_calls = c->counters.as<unsigned long long>() + 1;
+  CUDA_TRY(launch_nn1(p, s));
+  ++c->launches;
+  std::vector<BestRecord> rec(nq);
+  unsigned long long cnt[2];
+  CUDA_TRY(cudaMemcpyAsync(rec.data(), c->best.p, nq * sizeof(BestRecord), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(cnt, c->counters.p, 16, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  for (size_t i = 0; i < nq; ++i) {
+    if (rec[i].d == kInf) {  // nothing within the band: index 0, +inf (strict < never fired)
+      argmin[i] = 0;
+      dist[i] = kInf;
+    } else {
+      argmin[i] = rec[i].idx;
+      dist[i] = rec[i].d;
+    }
+  }
+  if (cells) *cells = cnt[0];
+  return EAPDTW_OK;
+}
+
+int eapdtw_nn1_dev(eapdtw_ctx* c, const double* q_dev, size_t nq, const double* db_dev, size_t nd,
+                   size_t len, size_t window, uint64_t* argmin, double* dist, uint64_t* cells) {
+  if (!c || !argmin || !dist) return fail(EAPDTW_EINVAL, "null argument");
+  if (len == 0 || nd == 0) return fail(EAPDTW_EINVAL, "nn1: empty series");
+  if (nq == 0) return EAPDTW_OK;
+  CUDA_TRY(cudaSetDevice(c->device));
+  return nn1_impl(c, q_dev, nq, db_dev, nd, len, window, argmin, dist, cells);
+}
+
+int eapdtw_nn1(eapdtw_ctx* c, const double* queries, size_t nq, const double* db, size_t nd,
+               size_t len, size_t window, uint64_t* argmin, double* dist, uint64_t* cells) {
+  if (!c || !queries || !db || !argmin || !dist) return fail(EAPDTW_EINVAL, "null argument");
+  if (len == 0 || nd == 0) return fail(EAPDTW_EINVAL, "nn1: empty series");
+  if (nq == 0) return EAPDTW_OK;
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(c->a.ensure(nq * len * 8));
+  CUDA_TRY(c->b.ensure(nd * len * 8));
+  CUDA_TRY(cudaMemcpyAsync(c->a.p, queries, nq * len * 8, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->b.p, db, nd * len * 8, cudaMemcpyHostToDevice, c->stream));
+  return nn1_impl(c, c->a.as<double>(), nq, c->b.as<double>(), nd, len, window, argmin, dist, cells);
+}
+
+// ---------------------------------------------------------------------------
+// Host helpers
+// ---------------------------------------------------------------------------
+int eapdtw_znormalize(const double* src, size_t n, double* dst) {
+  if (!src || !dst || n == 0) return fail(EAPDTW_EINVAL, "znormalize: empty input");
+  host_znormalize(src, n, HostStats::over(src, n), dst);
+  return EAPDTW_OK;
+}
+
+int eapdtw_random_walk_uniform(size_t n, uint64_t seed, double* out) {
+  if (n == 0 || !out) return fail(EAPDTW_EINVAL, "random_walk: zero length");
+  std::mt19937_64 gen(seed);  // the standard fixes the mt19937_64 stream
+  double x = 0.0;
+  for (size_t i = 0; i < n; ++i) {
+    const double u = static_cast<double>(gen() >> 11) * 0x1.0p-53;
+    x += u - 0.5;
+    out[i] = x;
+  }
+  return EAPDTW_OK;
+}
+
+int eapdtw_random_walk_normal(size_t n, uint64_t seed, double* out) {
+  if (n == 0 || !out) return fail(EAPDTW_EINVAL, "random_walk: zero length");
+  std::mt19937_64 gen(seed);
+  auto u01 = [&]() { return (static_cast<double>(gen() >> 11) + 0.5) * 0x1.0p-53; };  // (0,1)
+  double x = 0.0;
+  out[0] = 0.0;
+  size_t i = 1;
+  while (i < n) {  // Box-Muller, both variates used
+    const double u1 = u01(), u2 = u01();
+    const double rad = std::sqrt(-2.0 * std::log(u1));
+    const double th = 6.283185307179586 * u2;
+    x += rad * std::cos(th);
+    out[i++] = x;
+    if (i < n) {
+      x += rad * std::sin(th);
+      out[i++] = x;
+    }
+  }
+  return EAPDTW_OK;
+}
+
+int eapdtw_fp64_peak(eapdtw_ctx* c, double* ops) {
+  if (!c || !ops) return fail(EAPDTW_EINVAL, "null argument");
+  CUDA_TRY(cudaSetDevice(c->device));
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  DevBuf sink;
+  CUDA_TRY(sink.ensure(256 * 8));
+  cudaEvent_t e0, e1;
+  CUDA_TRY(cudaEventCreate(&e0));
+  CUDA_TRY(cudaEventCreate(&e1));
+  const int blocks = sms * 8, iters = 1 << 14;
+  float best = 1e30f;
+  for (int rep = 0; rep < 3; ++rep) {
+    CUDA_TRY(cudaEventRecord(e0, c->stream));
+    CUDA_TRY(launch_fp64_probe(sink.as<double>(), blocks, iters, c->stream));
+    ++c->launches;
+    CUDA_TRY(cudaEventRecord(e1, c->stream));
+    CUDA_TRY(cudaEventSynchronize(e1));
+    float ms = 0;
+    CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+    best = std::min(best, ms);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  sink.release();
+  *ops = static_cast<double>(blocks) * 256.0 * iters * 8.0 / (best * 1e-3);
+  return EAPDTW_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,544 @@
+// kernels.cu -- sm_100a kernels of the subsequence-search hot path.
+//
+//   stats_chain_kernel   RunningStats chain, bit-identical to search.cpp:156-168
+//   envelope_kernel      global sliding max/min (van Herk/Gil-Werman, warp scans)
+//   search_kernel        persistent: LB_Kim -> LB_Keogh EQ -> LB_Keogh EC -> pruned DTW
+//   pairwise_kernel      warp per pair (cfg1, and the single-pair drop-in calls)
+//   nn1_kernel           block per (query, database split) with a per-query cutoff (cfg5)
+//
+// All FP64 arithmetic that must match the CPU oracle bit-for-bit uses explicitly
+// rounded intrinsics, and the library is built with -fmad=false as a second
+// line of defence.
+#include <cfloat>
+#include <climits>
+
+#include "kernels.cuh"
+
+namespace eapdtw_b200 {
+
+// ---------------------------------------------------------------------------
+// Sliding z-normalisation statistics.
+//
+// The reference keeps one running (sum, sum of squares) chain over the start
+// positions and rebuilds it from scratch every 100000 slides
+// (search.cpp:156-168).  Its bits depend on that exact sequence of roundings,
+// and SURVEY.md A.1 shows any re-association (e.g. prefix sums) misses the
+// 1e-9 distance tolerance.  The chain is therefore reproduced step-for-step:
+// the 100000-slide segments are independent, so one warp owns one segment.
+// Lane 0 runs the dependent chain over a shared-memory tile (2 DADD of latency
+// per step); the other lanes stage the next inputs and convert finished
+// (sum, sumsq) pairs into mean/stddev with correctly rounded div/sqrt
+// (RunningStats::mean/variance/stddev, search.hpp:34-41, search.cpp:35).
+// ---------------------------------------------------------------------------
+constexpr int kStatsTile = 512;
+
+__global__ void __launch_bounds__(32) stats_chain_kernel(const double* __restrict__ ref, long long n,
+                                                         int m, double* __restrict__ mean_out,
+                                                         double* __restrict__ sd_out) {
+  __shared__ double s_in[kStatsTile];
+  __shared__ double s_out[kStatsTile];
+  __shared__ double s_sum[kStatsTile];
+  __shared__ double s_sq[kStatsTile];
+  const int lane = threadIdx.x;
+  const long long ncand = n - m + 1;
+  const long long s0 = static_cast<long long>(blockIdx.x) * kStatsResetInterval;
+  const long long s1 = min(ncand, s0 + kStatsResetInterval);
+  const double dm = static_cast<double>(m);
+  double sum = 0.0, sq = 0.0;
+  if (lane == 0) {  // RunningStats::over(ref[s0 : s0+m]) (search.cpp:25-33)
+    for (int k = 0; k < m; ++k) {
+      const double x = ref[s0 + k];
+      sum = __dadd_rn(sum, x);
+      sq = __dadd_rn(sq, __dmul_rn(x, x));
+    }
+  }
+  for (long long t0 = s0; t0 < s1; t0 += kStatsTile) {
+    const int cnt = static_cast<int>(min(static_cast<long long>(kStatsTile), s1 - t0));
+    for (int k = lane; k < cnt; k += 32) {
+      const long long s = t0 + k;
+      s_in[k] = s > s0 ? ref[s + m - 1] : 0.0;
+      s_out[k] = s > s0 ? ref[s - 1] : 0.0;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      for (int k = 0; k < cnt; ++k) {
+        if (t0 + k > s0) {  // stats.add(in); stats.remove(out) (search.hpp:23-32)
+          const double in = s_in[k], out = s_out[k];
+          sum = __dsub_rn(__dadd_rn(sum, in), out);
+          sq = __dsub_rn(__dadd_rn(sq, __dmul_rn(in, in)), __dmul_rn(out, out));
+        }
+        s_sum[k] = sum;
+        s_sq[k] = sq;
+      }
+    }
+    __syncwarp();
+    for (int k = lane; k < cnt; k += 32) {
+      const double mu = __ddiv_rn(s_sum[k], dm);
+      const double var = __dsub_rn(__ddiv_rn(s_sq[k], dm), __dmul_rn(mu, mu));
+      mean_out[t0 + k] = mu;
+      sd_out[t0 + k] = __dsqrt_rn(var > 0.0 ? var : 0.0);
+    }
+    __syncwarp();
+  }
+}
+
+cudaError_t launch_stats(const double* ref, long long n, int m, double* mean, double* sd,
+                         cudaStream_t stream) {
+  const long long ncand = n - m + 1;
+  const long long nseg = (ncand + kStatsResetInterval - 1) / kStatsResetInterval;
+  stats_chain_kernel<<<static_cast<unsigned>(nseg), 32, 0, stream>>>(ref, n, m, mean, sd);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Global raw envelope for the LB_Keogh EC tier.
+//
+// The reference builds, per surviving candidate, the envelope of the
+// normalised candidate with a deque sweep (lower_bounds.cpp:9-49, called from
+// search.cpp:97).  Normalisation x -> (x-mean)/sd is monotone, so the
+// normalised envelope equals the normalised raw envelope.  Here the raw
+// envelope is built ONCE for the whole reference with radius r; at the two
+// candidate edges (j < r or j > m-1-r) the global window is a superset of the
+// candidate's clamped window, which only loosens the bound (still sound).
+// Van Herk/Gil-Werman: with blocks of K = 2r+1, max over [p-r, p+r] =
+// max(suffixmax[p-r], prefixmax[p+r]); the in-block prefix/suffix maxima are
+// warp scans with a carried value, one warp per K-block of a smem tile.
+// ---------------------------------------------------------------------------
+template <bool MAX>
+__device__ __forceinline__ double pick(double a, double b) {
+  return MAX ? (a > b ? a : b) : (a < b ? a : b);
+}
+
+template <bool MAX>
+__device__ void envelope_pass(const double* a, double* g, double* h, int len, int K) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const double ident = MAX ? -d_inf() : d_inf();
+  const int nblk = (len + K - 1) / K;
+  for (int b = warp; b < nblk; b += nw) {
+    const int start = b * K, stop = min(len, start + K);
+    double carry = ident;
+    for (int c = start; c < stop; c += 32) {  // prefix (forward) scan
+      const int idx = c + lane;
+      double x = idx < stop ? a[idx] : ident;
+      for (int off = 1; off < 32; off <<= 1) {
+        const double y = __shfl_up_sync(kFull, x, off);
+        if (lane >= off) x = pick<MAX>(x, y);
+      }
+      x = pick<MAX>(x, carry);
+      if (idx < stop) g[idx] = x;
+      carry = __shfl_sync(kFull, x, 31);
+    }
+    carry = ident;
+    for (int c = stop - 1; c >= start; c -= 32) {  // suffix (backward) scan
+      const int idx = c - lane;
+      double x = idx >= start ? a[idx] : ident;
+      for (int off = 1; off < 32; off <<= 1) {
+        const double y = __shfl_up_sync(kFull, x, off);
+        if (lane >= off) x = pick<MAX>(x, y);
+      }
+      x = pick<MAX>(x, carry);
+      if (idx >= start) h[idx] = x;
+      carry = __shfl_sync(kFull, x, 31);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) envelope_kernel(const double* __restrict__ ref, long long n,
+                                                       int r, int T, double* __restrict__ up,
+                                                       double* __restrict__ lo) {
+  extern __shared__ double smem[];
+  const int K = 2 * r + 1;
+  const int len = T + 2 * r;
+  double* a = smem;
+  double* g = a + len;
+  double* h = g + len;
+  const long long P = static_cast<long long>(blockIdx.x) * T;  // first output
+  const long long A = P - r;                                   // first input
+  for (int pass = 0; pass < 2; ++pass) {
+    const double ident = pass == 0 ? -d_inf() : d_inf();
+    for (int k = threadIdx.x; k < len; k += blockDim.x) {
+      const long long p = A + k;
+      a[k] = (p >= 0 && p < n) ? ref[p] : ident;
+    }
+    __syncthreads();
+    if (pass == 0) envelope_pass<true>(a, g, h, len, K);
+    else envelope_pass<false>(a, g, h, len, K);
+    __syncthreads();
+    double* out = pass == 0 ? up : lo;
+    for (int t = threadIdx.x; t < T; t += blockDim.x) {
+      if (P + t < n) {
+        out[P + t] = pass == 0 ? pick<true>(h[t], g[t + 2 * r]) : pick<false>(h[t], g[t + 2 * r]);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+static int envelope_tile(int r) {
+  // three arrays of (T + 2r) doubles within 96 KB
+  const int cap = (96 * 1024) / (3 * 8);
+  int T = cap - 2 * r;
+  if (T > 8192) T = 8192;
+  return T;
+}
+
+cudaError_t launch_envelope(const double* ref, long long n, int r, double* up, double* lo,
+                            cudaStream_t stream) {
+  const int T = envelope_tile(r);
+  if (T < 256) return cudaErrorInvalidValue;  // caller disables the EC tier
+  const size_t smem = 3 * static_cast<size_t>(T + 2 * r) * sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(envelope_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  const long long blocks = (n + T - 1) / T;
+  envelope_kernel<<<static_cast<unsigned>(blocks), 256, smem, stream>>>(ref, n, r, T, up, lo);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Fused persistent search kernel (the cascade_decision + kernel dispatch of
+// search.cpp:160-204, re-organised for a GPU).
+//
+// A warp claims 32 consecutive candidates at a time (atomic chunk counter, so
+// the sweep advances through the reference roughly in order, like the CPU's
+// sequential best-so-far).  The lower-bound tiers run lane-per-candidate over
+// coalesced 256-byte rows of the reference; every tier prunes against the
+// CURRENT global threshold.  Survivors are then evaluated one at a time by the
+// whole warp with warp_dtw, re-reading the threshold at every 32-row strip.
+//
+// Soundness: LB_Kim is compared exactly (it is bit-for-bit <= the DTW value,
+// see DESIGN.md); the Keogh tiers normalise by reciprocal multiplication and
+// prune only when lb > ub*(1+guard_rel) + guard_abs.
+// ---------------------------------------------------------------------------
+size_t search_smem_bytes(int m, int warps) {
+  return static_cast<size_t>(m + 1) * 8       // q (1-based)
+         + static_cast<size_t>(m) * 8 * 2     // qu, ql
+         + static_cast<size_t>(m) * 4         // order
+         + static_cast<size_t>(warps) * (m + 1) * 8  // row buffers
+         + 64;
+}
+
+__global__ void __launch_bounds__(256) search_kernel(SearchParams p) {
+  extern __shared__ double smem[];
+  const int m = p.m;
+  double* q = smem;             // [m+1]
+  double* qu = q + (m + 1);     // [m]
+  double* ql = qu + m;          // [m]
+  int* order = reinterpret_cast<int*>(ql + m);  // [m]
+  const int warps = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* rowbuf = reinterpret_cast<double*>(order + m + (m & 1)) + static_cast<size_t>(warp) * (m + 1);
+  (void)warps;
+
+  for (int k = threadIdx.x; k <= m; k += blockDim.x) q[k] = p.q[k];
+  if (p.use_lb) {
+    for (int k = threadIdx.x; k < m; k += blockDim.x) {
+      qu[k] = p.qu[k];
+      ql[k] = p.ql[k];
+      order[k] = p.order[k];
+    }
+  }
+  __syncthreads();
+
+  const double INF = d_inf();
+  unsigned long long c_kim = 0, c_eq = 0, c_ec = 0, c_calls = 0, c_aband = 0, c_cells = 0,
+                     c_cand = 0;
+  const double* __restrict__ ref = p.ref;
+
+  for (;;) {
+    unsigned long long chunk = 0;
+    if (lane == 0) chunk = atomicAdd(p.work, 1ull);
+    chunk = __shfl_sync(kFull, chunk, 0);
+    const long long base = p.begin + static_cast<long long>(chunk) * 32 * p.stride;
+    if (base >= p.end) break;
+    const long long s = base + lane * p.stride;
+    const bool valid = s < p.end;
+    c_cand += __popc(__ballot_sync(kFull, valid));
+    const double mean = valid ? p.mean[s] : 0.0;
+    const double sd = valid ? p.sd[s] : 1.0;
+    const bool constant = sd < kMinStddev;
+    bool alive = valid;
+    double ub = load_ub(p.ub_key);
+
+    if (p.use_lb) {
+      // --- Tier 1: LB_Kim on the two aligned extremities (search.cpp:81-87),
+      //     computed with the same IEEE divisions as the DTW rows.
+      if (m >= 2 && alive) {
+        const double c0 = constant ? 0.0 : __ddiv_rn(__dsub_rn(ref[s], mean), sd);
+        const double cl = constant ? 0.0 : __ddiv_rn(__dsub_rn(ref[s + m - 1], mean), sd);
+        const double kim = __dadd_rn(sq_cost(q[1], c0), sq_cost(q[m], cl));
+        if (kim > ub) {
+          alive = false;
+          ++c_kim;
+        }
+      }
+      const double rsd = constant ? 0.0 : __drcp_rn(sd);
+      // --- Tier 2: LB_Keogh EQ, query envelope vs normalised candidate
+      //     (search.cpp:92, lower_bounds.cpp:57-88), visiting order[] with a
+      //     chunked early-abandon vote.
+      double ubg = ub * (1.0 + p.guard_rel) + p.guard_abs;
+      bool pending = alive;
+      if (__any_sync(kFull, pending)) {
+        double acc = 0.0;
+        for (int k0 = 0; k0 < m; k0 += 8) {
+          const int kend = min(m, k0 + 8);
+          for (int k = k0; k < kend; ++k) {
+            const int j = order[k];
+            const double x = pending ? ref[s + j] : 0.0;
+            const double cn = __dmul_rn(__dsub_rn(x, mean), rsd);
+            const double e1 = cn - qu[j];
+            const double e2 = ql[j] - cn;
+            const double d = e1 > 0.0 ? e1 : (e2 > 0.0 ? e2 : 0.0);
+            acc = fma(d, d, acc);
+          }
+          if (pending && acc > ubg) {
+            pending = false;
+            alive = false;
+            ++c_eq;
+          }
+          if (!__any_sync(kFull, pending)) break;
+        }
+      }
+      // --- Tier 3: LB_Keogh EC, normalised query vs the candidate envelope
+      //     (search.cpp:97-99) read from the global raw envelope.
+      if (p.env_up != nullptr) {
+        ub = load_ub(p.ub_key);
+        ubg = ub * (1.0 + p.guard_rel) + p.guard_abs;
+        pending = alive;
+        if (__any_sync(kFull, pending)) {
+          double acc = 0.0;
+          for (int k0 = 0; k0 < m; k0 += 8) {
+            const int kend = min(m, k0 + 8);
+            for (int k = k0; k < kend; ++k) {
+              const int j = order[k];
+              double U = 0.0, L = 0.0;
+              if (pending) {
+                U = __dmul_rn(__dsub_rn(p.env_up[s + j], mean), rsd);
+                L = __dmul_rn(__dsub_rn(p.env_lo[s + j], mean), rsd);
+              }
+              const double qj = q[j + 1];
+              const double e1 = qj - U;
+              const double e2 = L - qj;
+              const double d = e1 > 0.0 ? e1 : (e2 > 0.0 ? e2 : 0.0);
+              acc = fma(d, d, acc);
+            }
+            if (pending && acc > ubg) {
+              pending = false;
+              alive = false;
+              ++c_ec;
+            }
+            if (!__any_sync(kFull, pending)) break;
+          }
+        }
+      }
+    }
+
+    // --- Pruned DTW for the survivors, one warp-wide evaluation each, in
+    //     index order (strict < with the lowest index on ties, search.cpp:199).
+    unsigned mask = __ballot_sync(kFull, alive);
+    while (mask) {
+      const int k = __ffs(mask) - 1;
+      mask &= mask - 1;
+      const long long cand = base + k * p.stride;
+      const double cm = __shfl_sync(kFull, mean, k);
+      const double cs = __shfl_sync(kFull, sd, k);
+      const bool cconst = cs < kMinStddev;
+      const double* crow = ref + cand;
+      auto rowval = [&](int r) -> double {
+        return cconst ? 0.0 : __ddiv_rn(__dsub_rn(crow[r], cm), cs);
+      };
+      const bool prune = p.prune != 0;
+      auto get_ub = [&]() -> double { return prune ? load_ub(p.ub_key) : INF; };
+      auto rowthr = [](double u, int) -> double { return u; };
+      const double d = warp_dtw<false>(rowval, m, q, m, p.w, get_ub, rowthr, rowbuf, c_cells);
+      ++c_calls;
+      if (d == INF) {
+        ++c_aband;
+      } else if (lane == 0) {
+        atomicMin(p.ub_key, static_cast<unsigned long long>(__double_as_longlong(d)));
+        best_record_update(p.best, d, static_cast<unsigned long long>(cand + p.index_offset));
+      }
+    }
+  }
+
+  // Per-lane tier counts are summed over the warp; chunk-level counts are warp-uniform.
+  for (int off = 16; off > 0; off >>= 1) {
+    c_kim += __shfl_xor_sync(kFull, c_kim, off);
+    c_eq += __shfl_xor_sync(kFull, c_eq, off);
+    c_ec += __shfl_xor_sync(kFull, c_ec, off);
+  }
+  if (lane == 0) {
+    atomicAdd(&p.counters[kCntKim], c_kim);
+    atomicAdd(&p.counters[kCntKeoghEq], c_eq);
+    atomicAdd(&p.counters[kCntKeoghEc], c_ec);
+    atomicAdd(&p.counters[kCntDtwCalls], c_calls);
+    atomicAdd(&p.counters[kCntDtwAbandoned], c_aband);
+    atomicAdd(&p.counters[kCntCells], c_cells);
+    atomicAdd(&p.counters[kCntCandidates], c_cand);
+  }
+}
+
+cudaError_t launch_search(const SearchParams& p, int blocks, int warps, cudaStream_t stream) {
+  const size_t smem = search_smem_bytes(p.m, warps);
+  cudaError_t e = cudaFuncSetAttribute(search_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  search_kernel<<<blocks, warps * 32, smem, stream>>>(p);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Pairwise kernel: warp per pair.  Drop-in for ea_pruned_dtw_windowed /
+// dtw_windowed (dtw.cpp:316-396) over a batch; the caller has oriented the
+// pair (longer series on rows) and resolved effective_window.
+// ---------------------------------------------------------------------------
+template <bool WITH_CB>
+__global__ void __launch_bounds__(256) pairwise_kernel(PairParams p) {
+  extern __shared__ double smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  const int lc = p.lc;
+  double* cols = smem + static_cast<size_t>(warp) * (2 * lc + 2);  // [lc+1] 1-based
+  double* rowbuf = cols + lc + 1;                                 // [lc+1]
+  const double INF = d_inf();
+  unsigned long long cells = 0;
+  for (long long pr = static_cast<long long>(blockIdx.x) * wpb + warp; pr < p.npairs;
+       pr += static_cast<long long>(gridDim.x) * wpb) {
+    const double* rows = p.rows + pr * p.row_stride;
+    const double* cg = p.cols + pr * p.col_stride;
+    for (int k = lane; k < lc; k += 32) cols[k + 1] = cg[k];
+    __syncwarp();
+    const double ub0 = p.ub ? p.ub[pr] : INF;
+    auto rowval = [&](int r) -> double { return rows[r]; };
+    auto get_ub = [&]() -> double { return p.prune ? ub0 : INF; };
+    const double* cb = WITH_CB ? p.cb + pr * p.lr : nullptr;
+    const int lr = p.lr, w = p.w;
+    // row_threshold (dtw.cpp:81-86): ub - cb[min(i+w, lr) - 1], clamped at 0.
+    auto rowthr = [&](double u, int i) -> double {
+      if (!WITH_CB || i > lr) return u;
+      const int k = min(i + w, lr);
+      const double t = __dsub_rn(u, cb[k - 1]);
+      return t > 0.0 ? t : 0.0;
+    };
+    const double d = warp_dtw<WITH_CB>(rowval, lr, cols, lc, p.w, get_ub, rowthr, rowbuf, cells);
+    if (lane == 0) p.out[pr] = d;
+    __syncwarp();
+  }
+  if (lane == 0 && p.cells) atomicAdd(p.cells, cells);
+}
+
+cudaError_t launch_pairwise(const PairParams& p, cudaStream_t stream) {
+  const int warps = 8;
+  const size_t smem = static_cast<size_t>(warps) * (2 * p.lc + 2) * sizeof(double);
+  const long long need = (p.npairs + warps - 1) / warps;
+  const int blocks = static_cast<int>(min(need, 148LL * 32));
+  cudaError_t e;
+  if (p.cb) {
+    e = cudaFuncSetAttribute(pairwise_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    pairwise_kernel<true><<<blocks, warps * 32, smem, stream>>>(p);
+  } else {
+    e = cudaFuncSetAttribute(pairwise_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    pairwise_kernel<false><<<blocks, warps * 32, smem, stream>>>(p);
+  }
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Batched NN1 (cfg5): per query a running cutoff over the database, the
+// harness loop of SURVEY.md 3.3 (ea_pruned_dtw(db[k], q, bsf), dtw.cpp:364-368).
+// Block = (query, database split); warps claim database rows in order; an
+// exact LB_Kim (first/last, valid for any band) gates the DTW.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) nn1_kernel(Nn1Params p) {
+  extern __shared__ double smem[];
+  __shared__ unsigned long long s_next;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int L = p.len;
+  const long long qi = blockIdx.x / p.splits;
+  const int part = blockIdx.x % p.splits;
+  const long long k0 = p.nd * part / p.splits, k1 = p.nd * (part + 1) / p.splits;
+  double* q = smem;  // [L+1], 1-based
+  double* rowbuf = smem + (L + 1) + static_cast<size_t>(warp) * (L + 1);
+  for (int k = threadIdx.x; k < L; k += blockDim.x) q[k + 1] = p.queries[qi * L + k];
+  if (threadIdx.x == 0) s_next = 0;
+  __syncthreads();
+  const double INF = d_inf();
+  unsigned long long* key = p.ub_keys + qi;
+  unsigned long long cells = 0, calls = 0;
+  for (;;) {
+    unsigned long long t = 0;
+    if (lane == 0) t = atomicAdd(&s_next, 1ull);
+    t = __shfl_sync(kFull, t, 0);
+    const long long k = k0 + static_cast<long long>(t);
+    if (k >= k1) break;
+    const double* row = p.db + k * L;
+    const double ub = load_ub(key);
+    if (L >= 2) {  // LB_Kim_FL (lower_bounds.cpp:51-55): exact, so no guard needed
+      const double kim = __dadd_rn(sq_cost(q[1], row[0]), sq_cost(q[L], row[L - 1]));
+      if (kim > ub) continue;
+    }
+    auto rowval = [&](int r) -> double { return row[r]; };
+    auto get_ub = [&]() -> double { return load_ub(key); };
+    auto rowthr = [](double u, int) -> double { return u; };
+    const double d = warp_dtw<false>(rowval, L, q, L, p.w, get_ub, rowthr, rowbuf, cells);
+    ++calls;
+    if (d != INF && lane == 0) {
+      atomicMin(key, static_cast<unsigned long long>(__double_as_longlong(d)));
+      best_record_update(p.best + qi, d, static_cast<unsigned long long>(k));
+    }
+  }
+  if (lane == 0) {
+    atomicAdd(p.cells, cells);
+    atomicAdd(p.dtw_calls, calls);
+  }
+}
+
+cudaError_t launch_nn1(const Nn1Params& p, cudaStream_t stream) {
+  const int warps = 8;
+  const size_t smem = static_cast<size_t>(warps + 1) * (p.len + 1) * sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(nn1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  const long long blocks = p.nq * p.splits;
+  nn1_kernel<<<static_cast<unsigned>(blocks), warps * 32, smem, stream>>>(p);
+  return cudaGetLastError();
+}
+
+__global__ void init_best_kernel(BestRecord* rec, unsigned long long* keys, long long count) {
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < count) {
+    rec[i].d = d_inf();
+    rec[i].idx = ~0ull;
+    if (keys) keys[i] = 0x7ff0000000000000ull;
+  }
+}
+
+cudaError_t launch_init_best(BestRecord* rec, unsigned long long* keys, long long count,
+                             cudaStream_t stream) {
+  init_best_kernel<<<static_cast<unsigned>((count + 255) / 256), 256, 0, stream>>>(rec, keys, count);
+  return cudaGetLastError();
+}
+
+// FP64 issue-rate probe: 8 independent DADD chains per thread; used by the
+// bench to measure the FP64 pipe peak that the DTW roofline is quoted against.
+__global__ void fp64_probe_kernel(double* sink, int iters) {
+  double a = 1e-3 * (threadIdx.x + 1);
+  double x0 = a, x1 = a + 1, x2 = a + 2, x3 = a + 3, x4 = a + 4, x5 = a + 5, x6 = a + 6, x7 = a + 7;
+  for (int i = 0; i < iters; ++i) {
+    x0 = __dadd_rn(x0, a); x1 = __dadd_rn(x1, a); x2 = __dadd_rn(x2, a); x3 = __dadd_rn(x3, a);
+    x4 = __dadd_rn(x4, a); x5 = __dadd_rn(x5, a); x6 = __dadd_rn(x6, a); x7 = __dadd_rn(x7, a);
+  }
+  const double r = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+  if (r == 0.123456789) sink[threadIdx.x] = r;  // keep the chains alive
+}
+
+cudaError_t launch_fp64_probe(double* sink, int blocks, int iters, cudaStream_t stream) {
+  fp64_probe_kernel<<<blocks, 256, 0, stream>>>(sink, iters);
+  return cudaGetLastError();
+}
+
+}  // namespace eapdtw_b200

@@ -1,0 +1,87 @@
+// kernels.cuh -- launch interface of the sm_100a kernels (host side of kernels.cu).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "dtw_warp.cuh"
+
+namespace eapdtw_b200 {
+
+constexpr long long kStatsResetInterval = 100000;  // search.cpp:16
+constexpr double kMinStddev = 1e-12;               // search.cpp:13
+
+// Tier counters accumulated on the device (SearchReport, search.hpp:68-77).
+enum Counter : int {
+  kCntKim = 0,
+  kCntKeoghEq,
+  kCntKeoghEc,
+  kCntDtwCalls,
+  kCntDtwAbandoned,
+  kCntCells,
+  kCntCandidates,
+  kNumCounters
+};
+
+struct SearchParams {
+  const double* ref;     // shard reference, n points
+  const double* mean;    // per candidate (ncand)
+  const double* sd;      // per candidate (ncand)
+  const double* env_up;  // raw sliding max of ref, radius env_r (nullptr: no EC tier)
+  const double* env_lo;  // raw sliding min of ref
+  const double* q;       // normalised query, 1-based: q[1..m] (q[0] unused)
+  const double* qu;      // query envelope upper, 0-based
+  const double* ql;      // query envelope lower, 0-based
+  const int* order;      // Keogh visiting order (search.cpp:143-149)
+  long long ncand;
+  long long begin, end, stride;  // candidates begin, begin+stride, ... < end
+  int m, w;                      // query length, effective half window
+  int use_lb;                    // Kim -> Keogh EQ -> Keogh EC cascade
+  int prune;                     // 0: Algo::full (no pruning), 1: pruned DTW
+  double guard_rel, guard_abs;   // LB soundness guard
+  unsigned long long* ub_key;    // running threshold key (order-preserving bits)
+  BestRecord* best;              // exact (d, lowest index) record
+  unsigned long long* work;      // chunk counter (zeroed before launch)
+  unsigned long long* counters;  // kNumCounters
+  long long index_offset;        // shard start in the global reference
+};
+
+struct PairParams {
+  const double* rows;  // npairs x lr (row-major, pair p at p*row_stride)
+  const double* cols;  // npairs x lc
+  long long row_stride, col_stride;
+  int lr, lc, w;
+  const double* ub;  // per pair (nullptr: +inf)
+  const double* cb;  // per pair cumulative bound, lr each (nullptr: none)
+  int prune;         // 0: full DP (dtw_windowed), 1: pruned
+  double* out;
+  unsigned long long* cells;  // one counter
+  long long npairs;
+};
+
+struct Nn1Params {
+  const double* queries;  // nq x len
+  const double* db;       // nd x len
+  long long nq, nd;
+  int len, w;
+  int splits;                     // blocks per query
+  unsigned long long* ub_keys;    // nq
+  BestRecord* best;               // nq
+  unsigned long long* cells;      // one counter
+  unsigned long long* dtw_calls;  // one counter
+};
+
+// Each launcher enqueues on `stream` and returns the launch error (no sync).
+cudaError_t launch_stats(const double* ref, long long n, int m, double* mean, double* sd,
+                         cudaStream_t stream);
+cudaError_t launch_envelope(const double* ref, long long n, int r, double* up, double* lo,
+                            cudaStream_t stream);
+size_t search_smem_bytes(int m, int warps);
+cudaError_t launch_search(const SearchParams& p, int blocks, int warps, cudaStream_t stream);
+cudaError_t launch_pairwise(const PairParams& p, cudaStream_t stream);
+cudaError_t launch_nn1(const Nn1Params& p, cudaStream_t stream);
+cudaError_t launch_init_best(BestRecord* rec, unsigned long long* keys, long long count,
+                             cudaStream_t stream);
+cudaError_t launch_fp64_probe(double* sink, int blocks, int iters, cudaStream_t stream);
+
+}  // namespace eapdtw_b200

@@ -1,0 +1,312 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle and the
+reference's golden fixtures.  Bar: bit-exact indices and distance bits."""
+import json
+import os
+import struct
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "golden.json")))
+UNB = oracle.UNBOUNDED
+
+
+def fbits(h: str) -> float:
+    return struct.unpack("<d", struct.pack("<Q", int(h, 16)))[0]
+
+
+def w_of(x):
+    return UNB if x == -1 else x
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    import paper_2010_05371_b200 as g
+    return g
+
+
+def test_worked_example(gpu):
+    we = GOLDEN["worked_example"]
+    S, T = we["S"], we["T"]
+    assert gpu.dtw_windowed(S, T, gpu.Band.unbounded()) == 9.0
+    assert gpu.dtw_windowed(S, T, gpu.Band.cells(0)) == 23.0
+    assert gpu.dtw_windowed(S, T, gpu.Band.cells(6)) == 9.0
+    assert gpu.ea_pruned_dtw(S, T, 9.0) == 9.0
+    assert gpu.is_pruned(gpu.ea_pruned_dtw(S, T, 6.0))
+    assert gpu.is_pruned(gpu.ea_pruned_dtw_windowed(S, T, gpu.Band.cells(0), 22.0))
+    assert gpu.ea_pruned_dtw_windowed(S, T, gpu.Band.cells(0), 23.0) == 23.0
+    # length gap beyond the band: no alignment (test_dtw.cpp:77-79)
+    assert gpu.is_pruned(gpu.dtw_windowed(np.ones(5), np.ones(9), gpu.Band.cells(2)))
+    # single samples (test_dtw.cpp:133-141)
+    assert gpu.dtw_full([2.0], [5.0]) == 9.0
+    assert gpu.ea_pruned_dtw([2.0], [5.0], 9.0) == 9.0
+    assert gpu.is_pruned(gpu.ea_pruned_dtw([2.0], [5.0], 8.9))
+    # ub = 0 (test_dtw.cpp:143-149)
+    assert gpu.ea_pruned_dtw([1.0, 2.0], [1.0, 2.0], 0.0) == 0.0
+    assert gpu.is_pruned(gpu.ea_pruned_dtw([1.0, 2.0], [1.0, 2.5], 0.0))
+    # discard run ending on the last column (test_dtw.cpp:307-316)
+    assert gpu.ea_pruned_dtw([0.0, 5.0, 0.0], [0.0, 1.0], 17.0) == 17.0
+    assert gpu.is_pruned(gpu.ea_pruned_dtw([0.0, 0.0], [0.0, 5.0], 10.0))
+
+
+def test_errors(gpu):
+    with pytest.raises(ValueError):
+        gpu.ea_pruned_dtw([], [1.0], 1.0)
+    with pytest.raises(ValueError):
+        gpu.ea_pruned_dtw_windowed([1.0, 2.0, 3.0], [1.0, 2.0, 4.0], gpu.Band.unbounded(), 10.0,
+                                   [1.0, 0.0])
+    with pytest.raises(ValueError):
+        gpu.ea_pruned_dtw_windowed([1.0, 2.0, 3.0], [1.0, 2.0, 4.0], gpu.Band.unbounded(), 10.0,
+                                   [0.0, 1.0, 0.0])
+    with pytest.raises(ValueError):
+        gpu.ea_pruned_dtw_windowed([1.0, 2.0, 3.0], [1.0, 2.0, 4.0], gpu.Band.unbounded(), 10.0,
+                                   [3.0, 2.0, 1.0])
+    ref = gpu.random_walk(500, 31)
+    q = gpu.random_walk(64, 32)
+    with pytest.raises(ValueError):
+        gpu.similarity_search(ref, q, gpu.SearchConfig(query_length=600))
+    with pytest.raises(ValueError):
+        gpu.similarity_search(q, ref, gpu.SearchConfig(query_length=0))
+
+
+def test_random_pairs_golden(gpu):
+    g = GOLDEN["pairs"]
+    rng = np.random.default_rng(g["seed"])
+    for it, c in enumerate(g["cases"]):
+        la, lb = (int(x) for x in rng.integers(1, 40, 2))
+        a = rng.uniform(-3, 3, la)
+        b = rng.uniform(-3, 3, lb)
+        w = int(rng.integers(0, 45)) if it % 5 else UNB
+        if it % 4 in (1, 2):  # keep the generator stream aligned with make_golden.py
+            rng.uniform(0.0, 1.0)
+        if not np.isfinite(fbits(c["full"])) and it % 4 != 3:
+            rng.uniform(0, 40)
+        ub = fbits(c["ub"])
+        band = gpu.Band(w)
+        assert gpu.dtw_windowed(a, b, band) == fbits(c["full"]), it
+        assert gpu.ea_pruned_dtw_windowed(a, b, band, ub) == fbits(c["algo2"]), it
+        # symmetry under argument swap (test_dtw.cpp:291-305)
+        assert gpu.ea_pruned_dtw_windowed(b, a, band, ub) == fbits(c["algo2"]), it
+
+
+def test_contract_sweep_vs_oracle(gpu, oracle_lib):
+    """Early-abandon contract incl. exact ties (test_dtw.cpp:183-201, acceptance crit. 4)."""
+    rng = np.random.default_rng(12345)
+    for it in range(300):
+        la, lb = (int(x) for x in rng.integers(1, 70, 2))
+        a = rng.uniform(-3, 3, la)
+        b = rng.uniform(-3, 3, lb)
+        w = int(rng.integers(0, 80)) if it % 3 else UNB
+        d = oracle_lib.dtw_windowed(a, b, w)
+        for ub in (d, d * 0.75, d * 1.25 + 1.0, np.inf,
+                   rng.uniform(0, 2 * d + 1 if np.isfinite(d) else 50.0)):
+            want = oracle_lib.ea_pruned_dtw_windowed(a, b, w, ub)
+            got = gpu.ea_pruned_dtw_windowed(a, b, gpu.Band(w), ub)
+            assert got == want, (it, ub)
+            if np.isfinite(d) and d <= ub:
+                assert got == d
+
+
+def test_genuine_cumulative_bound(gpu, oracle_lib):
+    """cb tightening never loses a qualifying result (test_dtw.cpp:326-359)."""
+    rng = np.random.default_rng(777)
+    for it in range(200):
+        n = int(rng.integers(2, 60))
+        s = rng.uniform(-3, 3, n)
+        t = rng.uniform(-3, 3, n)
+        w = int(rng.integers(0, n))
+        want = oracle_lib.dtw_windowed(s, t, w)
+        ub = want * rng.uniform(0.6, 1.4)
+        up, lo = oracle_lib.compute_envelope(s, w)
+        _, contrib, _ = oracle_lib.lb_keogh(up, lo, t)
+        cb = oracle_lib.cumulative_bound(contrib)
+        got = gpu.ea_pruned_dtw_windowed(s, t, gpu.Band(w), ub, cb)
+        if want <= ub:
+            assert got == want, it
+        else:
+            assert gpu.is_pruned(got), it
+        assert got == oracle_lib.ea_pruned_dtw_windowed(s, t, w, ub, cb), it
+        assert gpu.ea_pruned_dtw_windowed(s, t, gpu.Band(w), ub, np.zeros(n)) == \
+            gpu.ea_pruned_dtw_windowed(s, t, gpu.Band(w), ub)
+
+
+def _pw_data(case):
+    g = np.random.default_rng(case["seed"])
+    from paper_2010_05371_b200 import znormalize
+    L = case["len"]
+    a = np.stack([znormalize(np.cumsum(g.standard_normal(L))) for _ in range(case["npairs"])])
+    b = np.stack([znormalize(np.cumsum(g.standard_normal(L))) for _ in range(case["npairs"])])
+    return a, b
+
+
+def test_pairwise_golden(gpu):
+    for case in GOLDEN["pairwise"]["cases"]:
+        a, b = _pw_data(case)
+        w = gpu.Band.cells(case["window"])
+        exact, _ = gpu.pairwise(a, b, w, None, prune=False)
+        for key, ub in (("inf", None), ("x105", exact * 1.05), ("x090", exact * 0.9)):
+            out, cells = gpu.pairwise(a, b, w, ub)
+            want = np.array([fbits(h) for h in case[key]])
+            assert np.array_equal(out, want), key
+            assert cells > 0
+
+
+def test_pairwise_cfg1_full_size(gpu, oracle_lib):
+    """cfg1: 1024 pairs, L=256, w=25, cutoff +inf and 1.05x exact; bit-exact."""
+    from paper_2010_05371_b200 import random_walk_normal, znormalize
+    a = np.stack([znormalize(random_walk_normal(256, 1000 + p)) for p in range(1024)])
+    b = np.stack([znormalize(random_walk_normal(256, 5000 + p)) for p in range(1024)])
+    band = gpu.Band.cells(25)
+    exact, _ = oracle_lib.pairwise(a, b, 25, None)
+    got, _ = gpu.pairwise(a, b, band, None)
+    assert np.array_equal(got, exact)
+    ub = exact * 1.05
+    want, _ = oracle_lib.pairwise(a, b, 25, ub)
+    got, _ = gpu.pairwise(a, b, band, ub)
+    assert np.array_equal(got, want)
+    assert np.isfinite(got).all()
+
+
+@pytest.mark.parametrize("idx", range(len(GOLDEN["searches"])))
+def test_search_golden(gpu, idx):
+    c = GOLDEN["searches"][idx]
+    r = gpu.random_walk(c["n"], c["seed_ref"])
+    q = gpu.random_walk(c["m"], c["seed_query"])
+    cfg = gpu.SearchConfig(query_length=c["m"], window_ratio=c["ratio"],
+                           algorithm=gpu.Algo(c["algo"]), use_lower_bounds=c["use_lb"],
+                           tighten_ub=c["use_lb"])
+    res = gpu.similarity_search(r, q, cfg)
+    assert res.best.found
+    assert res.best.location == c["location"]
+    assert res.best.distance_sq == fbits(c["distance_sq"])
+    rep = res.report
+    assert rep.candidates_total == c["n"] - c["m"] + 1
+    assert rep.candidates_total == (rep.pruned_kim + rep.pruned_keogh_eq + rep.pruned_keogh_ec
+                                    + rep.dtw_calls)
+    assert rep.dtw_abandoned <= rep.dtw_calls
+    if not c["use_lb"]:
+        assert rep.dtw_calls == rep.candidates_total
+
+
+@pytest.mark.parametrize("idx", range(15))
+def test_acceptance_grid_golden(gpu, idx):
+    g = GOLDEN["acceptance_grid"]
+    c = g["cases"][idx]
+    r = gpu.random_walk(g["n"], g["seed_ref"])
+    q = gpu.random_walk(g["qlen"], g["seed_query"])
+    res = gpu.similarity_search(r, q, gpu.SearchConfig(query_length=c["m"],
+                                                       window_ratio=c["ratio"]))
+    assert res.best.location == c["location"]
+    assert res.best.distance_sq == fbits(c["distance_sq"])
+
+
+def test_ties_and_exact_copy(gpu):
+    """Ties go to the earliest location (test_search.cpp:209-237); an exact
+    normalised copy is found at distance 0 (test_search.cpp:143-158)."""
+    rng = np.random.default_rng(0x5ca40007)
+    m = 40
+    ref = (rng.integers(0, 13, 1500) - 6).astype(np.float64)
+    motif = (rng.integers(0, 13, m) - 6).astype(np.float64)
+    ref[200:200 + m] = motif
+    ref[900:900 + m] = motif
+    for algo in gpu.Algo:
+        for lb in (True, False):
+            cfg = gpu.SearchConfig(window_ratio=0.1, algorithm=algo, use_lower_bounds=lb,
+                                   tighten_ub=lb)
+            res = gpu.similarity_search(ref, motif, cfg)
+            assert res.best.location == 200 and res.best.distance_sq == 0.0, (algo, lb)
+    ref2 = (rng.integers(0, 13, 2000) - 6).astype(np.float64)
+    q2 = (rng.integers(0, 13, 48) - 6).astype(np.float64)
+    ref2[700:748] = q2
+    res = gpu.similarity_search(ref2, q2, gpu.SearchConfig(window_ratio=0.1))
+    assert res.best.location == 700 and res.best.distance_sq == 0.0
+
+
+def test_degenerate_queries(gpu, oracle_lib):
+    ref = gpu.random_walk(50, 41)
+    q = gpu.random_walk(1, 42)
+    res = gpu.similarity_search(ref, q, gpu.SearchConfig(window_ratio=0.1))
+    assert res.best.location == 0 and res.best.distance_sq == 0.0
+    assert res.report.candidates_total == 50
+    # constant stretches normalise to zeros (search.cpp:41-44)
+    ref = np.concatenate([gpu.random_walk(300, 1), np.full(200, 3.0), gpu.random_walk(300, 2)])
+    q = gpu.random_walk(32, 3)
+    for ratio in (0.0, 0.1, 1.0):
+        want = oracle_lib.similarity_search(ref, q, ratio)
+        got = gpu.similarity_search(ref, q, gpu.SearchConfig(window_ratio=ratio))
+        assert (got.best.location, got.best.distance_sq) == (want.location, want.distance_sq)
+    # query as long as the reference: one candidate
+    r = gpu.random_walk(64, 9)
+    q = gpu.random_walk(64, 10)
+    want = oracle_lib.similarity_search(r, q, 0.2)
+    got = gpu.similarity_search(r, q, gpu.SearchConfig(window_ratio=0.2))
+    assert (got.best.location, got.best.distance_sq) == (want.location, want.distance_sq)
+
+
+def test_nn1_golden(gpu):
+    for c in GOLDEN["nn1"]["cases"]:
+        g = np.random.default_rng(c["seed"])
+        from paper_2010_05371_b200 import znormalize
+        L = c["len"]
+        qs = np.stack([znormalize(np.cumsum(g.standard_normal(L))) for _ in range(c["nq"])])
+        db = np.stack([znormalize(np.cumsum(g.standard_normal(L))) for _ in range(c["nd"])])
+        band = gpu.Band(w_of(c["window"]))
+        arg, dist, cells = gpu.nn1(qs, db, band)
+        assert [int(x) for x in arg] == c["argmin"]
+        assert [float(x) for x in dist] == [fbits(h) for h in c["dist"]]
+        assert cells > 0
+
+
+def test_nn1_ties_lowest_index(gpu):
+    from paper_2010_05371_b200 import znormalize
+    rng = np.random.default_rng(4)
+    db = np.stack([znormalize(np.cumsum(rng.standard_normal(32))) for _ in range(200)])
+    db[150] = db[17]
+    db[190] = db[17]
+    qs = db[[17, 3]].copy()
+    arg, dist, _ = gpu.nn1(qs, db)
+    assert int(arg[0]) == 17 and dist[0] == 0.0
+    assert int(arg[1]) == 3 and dist[1] == 0.0
+
+
+def test_cfg2_full_size(gpu, oracle_lib):
+    """cfg2 at its BASELINE size: N=1e6, m=128, ratio 0.05 (w=6), full cascade."""
+    ref = gpu.random_walk_normal(1_000_000, 7)
+    q = gpu.random_walk_normal(128, 8)
+    want = oracle_lib.similarity_search(ref, q, 0.05)
+    got = gpu.similarity_search(ref, q, gpu.SearchConfig(window_ratio=0.05))
+    assert got.best.location == want.location
+    assert got.best.distance_sq == want.distance_sq
+    # cascade disabled: EAPrunedDTW alone gives the same answer
+    got2 = gpu.similarity_search(ref, q, gpu.SearchConfig(window_ratio=0.05,
+                                                          use_lower_bounds=False))
+    assert (got2.best.location, got2.best.distance_sq) == (want.location, want.distance_sq)
+
+
+def test_sharded_plan_equals_unsharded(gpu, oracle_lib):
+    """Shards at multiples of 100000 with an (m-1) halo reproduce the chain."""
+    import torch
+    ref = gpu.random_walk_normal(350_000, 17)
+    q = gpu.random_walk_normal(96, 18)
+    cfg = gpu.SearchConfig(window_ratio=0.1)
+    want = oracle_lib.similarity_search(ref, q, 0.1)
+    dref = torch.from_numpy(ref).cuda()
+    m = 96
+    ncand = ref.size - m + 1
+    best = None
+    for s0 in range(0, ncand, 100_000):
+        s1 = min(ncand, s0 + 100_000)
+        plan = gpu.SearchPlan(dref.data_ptr() + 8 * s0, (s1 - s0) + m - 1, q, cfg, s0)
+        plan.prepare()
+        mid = plan.candidates // 2
+        plan.run(0, mid)
+        plan.run(mid, plan.candidates)
+        r = plan.result()
+        plan.close()
+        cand = (r.best.distance_sq, r.best.location)
+        best = cand if best is None or cand < best else best
+    assert best == (want.distance_sq, want.location)
