@@ -112,6 +112,12 @@ int eapdtw_similarity_search_dev(eapdtw_ctx* ctx, const double* reference_dev, s
 int eapdtw_search_plan_create(eapdtw_ctx* ctx, const double* reference_dev, size_t n,
                               const double* query, size_t qlen, const eapdtw_search_config* cfg,
                               uint64_t global_offset, eapdtw_search_plan** out);
+/* Restart the search on the same inputs (best record, threshold, counters). */
+int eapdtw_search_plan_reset(eapdtw_search_plan* plan);
+/* Use a caller-owned 8-byte device threshold key (e.g. a torch int64 tensor
+ * that is all-reduced with MIN across ranks); NULL restores the plan's own.
+ * Implies reset(). */
+int eapdtw_search_plan_set_ub_key(eapdtw_search_plan* plan, uint64_t* dev_key);
 int eapdtw_search_plan_prepare(eapdtw_search_plan* plan); /* stats, envelope, probe */
 size_t eapdtw_search_plan_candidates(const eapdtw_search_plan* plan);
 int eapdtw_search_plan_run(eapdtw_search_plan* plan, size_t begin, size_t end);

@@ -83,6 +83,8 @@ SIGNATURES = [
     ("eapdtw_search_plan_create", C.c_int,
      [_vp, _vp, C.c_size_t, _dp, C.c_size_t, C.POINTER(SearchConfigC), C.c_uint64,
       C.POINTER(_vp)]),
+    ("eapdtw_search_plan_reset", C.c_int, [_vp]),
+    ("eapdtw_search_plan_set_ub_key", C.c_int, [_vp, _vp]),
     ("eapdtw_search_plan_prepare", C.c_int, [_vp]),
     ("eapdtw_search_plan_candidates", C.c_size_t, [_vp]),
     ("eapdtw_search_plan_run", C.c_int, [_vp, C.c_size_t, C.c_size_t]),

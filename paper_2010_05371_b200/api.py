@@ -300,10 +300,14 @@ def nn1(queries, db, band=None, *, ctx=None):
 
 def similarity_search(reference, query, cfg: SearchConfig | None = None, *, ctx=None
                       ) -> SearchResult:
-    """Nearest z-normalised subsequence of ``reference`` under windowed DTW."""
+    """Nearest z-normalised subsequence of ``reference`` under windowed DTW.
+
+    ``reference`` may be a Series or any float64 array (pinned host memory
+    gives the fastest copy); its Series validation (series.hpp:24-31) runs on
+    the device after the copy, the query's on the host."""
     ctx = ctx or default_context()
     cfg = cfg or SearchConfig()
-    ref = reference.view() if isinstance(reference, Series) else Series(reference).view()
+    ref = _as_f64(reference)
     q = query.view() if isinstance(query, Series) else Series(query).view()
     res = _capi.SearchResultC()
     c = cfg.to_c()
@@ -346,6 +350,13 @@ class SearchPlan:
     @property
     def ub_key_ptr(self) -> int:
         return int(lib.eapdtw_search_plan_ub_key(self.handle))
+
+    def reset(self):
+        check(lib.eapdtw_search_plan_reset(self.handle))
+
+    def set_ub_key(self, dev_ptr: int | None):
+        """Use a caller-owned int64 device key (all-reduced MIN across ranks)."""
+        check(lib.eapdtw_search_plan_set_ub_key(self.handle, C.c_void_p(dev_ptr or 0)))
 
     def prepare(self):
         check(lib.eapdtw_search_plan_prepare(self.handle))

@@ -104,6 +104,16 @@ bool all_finite(const double* x, size_t n) {
 
 }  // namespace
 
+struct PlanBuffers {
+  DevBuf mean, sd, up, lo, q, qu, ql, order, best, key, work, counters, probe_counters, flag, queue,
+      qctr;
+  void release() {
+    for (DevBuf* b : {&mean, &sd, &up, &lo, &q, &qu, &ql, &order, &best, &key, &work, &counters,
+                      &probe_counters, &flag, &queue, &qctr})
+      b->release();
+  }
+};
+
 struct eapdtw_ctx {
   int device = 0;
   cudaStream_t own = nullptr;
@@ -112,11 +122,15 @@ struct eapdtw_ctx {
   // scratch for pairwise / nn1 host-pointer variants
   DevBuf a, b, ub, cb, out, cells, best, keys, counters;
   DevBuf ref;  // host-pointer search copies the reference here
+  PlanBuffers pb;  // scratch of the one-shot search API (grow-only, reused)
 };
 
 struct eapdtw_search_plan {
   eapdtw_ctx* ctx = nullptr;
-  const double* ref = nullptr;  // device
+  PlanBuffers own;
+  PlanBuffers* buf = &own;            // the one-shot API borrows the context's buffers
+  unsigned long long* key = nullptr;  // active threshold key (own or external)
+  const double* ref = nullptr;        // device
   size_t n = 0, m = 0, w_cells = 0;
   int w_eff = 0;
   int env_r = 0;
@@ -124,9 +138,8 @@ struct eapdtw_search_plan {
   int algo = EAPDTW_ALGO_EA_PRUNED;
   uint64_t offset = 0;
   size_t ncand = 0;
-  DevBuf mean, sd, up, lo, q, qu, ql, order, best, key, work, counters, probe_counters;
   cudaEvent_t ev[8] = {};
-  bool prepared = false;
+  bool prepared = false, ran = false;
   int blocks = 0, warps = 8;
   double guard_rel = 1e-9, guard_abs = 1e-20;
   std::chrono::steady_clock::time_point t0;
@@ -170,6 +183,7 @@ int eapdtw_ctx_destroy(eapdtw_ctx* c) {
   for (DevBuf* b : {&c->a, &c->b, &c->ub, &c->cb, &c->out, &c->cells, &c->best, &c->keys,
                     &c->counters, &c->ref})
     b->release();
+  c->pb.release();
   if (c->own) cudaStreamDestroy(c->own);
   delete c;
   return EAPDTW_OK;
@@ -336,11 +350,18 @@ int eapdtw_pairwise(eapdtw_ctx* c, const double* a, const double* b, size_t npai
 
 // ---------------------------------------------------------------------------
 // Search plan
+//
+// A plan binds one (reference shard, query, config).  create() does the
+// host-side query preparation of similarity_search (search.cpp:131-149) and
+// allocates device buffers; every search then runs
+//   reset()   -> best record / threshold / counters to their initial state
+//   prepare() -> stats chain, raw envelope, probe candidates
+//   run()     -> the persistent sweep over candidate ranges
+//   result()  -> read back (location, distance, counters)
 // ---------------------------------------------------------------------------
-int eapdtw_search_plan_create(eapdtw_ctx* c, const double* ref_dev, size_t n, const double* query,
-                              size_t qlen, const eapdtw_search_config* cfg, uint64_t offset,
-                              eapdtw_search_plan** out) {
-  if (!c || !cfg || !out) return fail(EAPDTW_EINVAL, "search: null argument");
+static int plan_init(eapdtw_search_plan* p, eapdtw_ctx* c, const double* ref_dev, size_t n,
+                     const double* query, size_t qlen, const eapdtw_search_config* cfg,
+                     uint64_t offset) {
   if (n == 0 || qlen == 0 || !query) return fail(EAPDTW_EINVAL, "Series: empty input");
   // similarity_search validation (search.cpp:121-127)
   const size_t m = cfg->query_length == 0 ? qlen : cfg->query_length;
@@ -349,10 +370,11 @@ int eapdtw_search_plan_create(eapdtw_ctx* c, const double* ref_dev, size_t n, co
   if (!all_finite(query, qlen)) return fail(EAPDTW_EINVAL, "Series: non-finite sample");
   if (offset % static_cast<uint64_t>(kStatsResetInterval) != 0)
     return fail(EAPDTW_EINVAL, "search plan: shard offset must be a multiple of 100000");
-  if (m > (1u << 20)) return fail(EAPDTW_EINVAL, "search: query length above the GPU limit");
+  if (m > (1u << 16)) return fail(EAPDTW_EINVAL, "search: query length above the GPU limit (65536)");
+  if (cfg->algorithm < EAPDTW_ALGO_FULL || cfg->algorithm > EAPDTW_ALGO_EA_PRUNED)
+    return fail(EAPDTW_EINVAL, "search: bad algorithm");
   CUDA_TRY(cudaSetDevice(c->device));
 
-  auto* p = new eapdtw_search_plan();
   p->t0 = std::chrono::steady_clock::now();
   p->ctx = c;
   p->ref = ref_dev;
@@ -394,87 +416,118 @@ int eapdtw_search_plan_create(eapdtw_ctx* c, const double* ref_dev, size_t n, co
   });
   std::copy(qn.begin(), qn.end(), q1.begin() + 1);
 
+  PlanBuffers& B = *p->buf;
   const size_t nc = p->ncand;
-  cudaError_t e = cudaSuccess;
-  auto chk = [&](cudaError_t x) {
-    if (x != cudaSuccess && e == cudaSuccess) e = x;
-  };
-  chk(p->mean.ensure(nc * 8));
-  chk(p->sd.ensure(nc * 8));
-  chk(p->q.ensure((m + 1) * 8));
-  chk(p->qu.ensure(m * 8));
-  chk(p->ql.ensure(m * 8));
-  chk(p->order.ensure(m * 4));
-  chk(p->best.ensure(sizeof(BestRecord)));
-  chk(p->key.ensure(8));
-  chk(p->work.ensure(8));
-  chk(p->counters.ensure(kNumCounters * 8));
-  chk(p->probe_counters.ensure(kNumCounters * 8));
+  CUDA_TRY(B.mean.ensure(nc * 8));
+  CUDA_TRY(B.sd.ensure(nc * 8));
+  CUDA_TRY(B.q.ensure((m + 1) * 8));
+  CUDA_TRY(B.qu.ensure(m * 8));
+  CUDA_TRY(B.ql.ensure(m * 8));
+  CUDA_TRY(B.order.ensure(m * 4));
+  CUDA_TRY(B.best.ensure(sizeof(BestRecord)));
+  CUDA_TRY(B.key.ensure(8));
+  CUDA_TRY(B.work.ensure(8));
+  CUDA_TRY(B.queue.ensure(nc * 8));
+  CUDA_TRY(B.qctr.ensure(24));
+  CUDA_TRY(B.flag.ensure(8));
+  CUDA_TRY(B.counters.ensure(kNumCounters * 8));
+  CUDA_TRY(B.probe_counters.ensure(kNumCounters * 8));
   if (p->use_lb) {
-    chk(p->up.ensure(n * 8));
-    chk(p->lo.ensure(n * 8));
+    CUDA_TRY(B.up.ensure(n * 8));
+    CUDA_TRY(B.lo.ensure(n * 8));
   }
-  for (auto& ev : p->ev) chk(cudaEventCreate(&ev));
-  if (e == cudaSuccess) {
-    cudaStream_t s = c->stream;
-    chk(cudaMemcpyAsync(p->q.p, q1.data(), (m + 1) * 8, cudaMemcpyHostToDevice, s));
-    chk(cudaMemcpyAsync(p->qu.p, qu.data(), m * 8, cudaMemcpyHostToDevice, s));
-    chk(cudaMemcpyAsync(p->ql.p, ql.data(), m * 8, cudaMemcpyHostToDevice, s));
-    chk(cudaMemcpyAsync(p->order.p, order.data(), m * 4, cudaMemcpyHostToDevice, s));
-    chk(cudaMemsetAsync(p->counters.p, 0, kNumCounters * 8, s));
-    chk(cudaMemsetAsync(p->probe_counters.p, 0, kNumCounters * 8, s));
-    chk(launch_init_best(p->best.as<BestRecord>(), p->key.as<unsigned long long>(), 1, s));
-    ++c->launches;
-    // q, qu, ql and order are staged from pageable vectors: make sure the
-    // copies have consumed them before they go out of scope.
-    chk(cudaStreamSynchronize(s));
-  }
-  // Occupancy-sized persistent grid.
+  p->key = B.key.as<unsigned long long>();
+  for (auto& ev : p->ev) CUDA_TRY(cudaEventCreate(&ev));
+  cudaStream_t s = c->stream;
+  CUDA_TRY(cudaMemcpyAsync(B.q.p, q1.data(), (m + 1) * 8, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(B.qu.p, qu.data(), m * 8, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(B.ql.p, ql.data(), m * 8, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(B.order.p, order.data(), m * 4, cudaMemcpyHostToDevice, s));
+  // the staging vectors are pageable locals: wait until the copies consumed them
+  CUDA_TRY(cudaStreamSynchronize(s));
+
+  // Occupancy-sized persistent grid: as many 8-warp blocks as shared memory allows.
+  int sms = 148, max_smem = 0, optin = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, c->device);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device);
+  p->warps = 8;
+  while (p->warps > 1 && search_smem_bytes(static_cast<int>(m), p->warps) > static_cast<size_t>(optin))
+    p->warps /= 2;
   const size_t smem = search_smem_bytes(static_cast<int>(m), p->warps);
-  int per_sm = 0;
-  if (smem > 200 * 1024) {
-    p->warps = 4;
-  }
-  if (e == cudaSuccess) {
-    int dev_sms = 148;
-    cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
-    const size_t sm2 = search_smem_bytes(static_cast<int>(m), p->warps);
-    if (sm2 > 227 * 1024) {
-      e = cudaErrorInvalidValue;
-    } else {
-      per_sm = 1;
-      cudaFuncAttributes fa{};
-      (void)fa;
-      int max_smem = 0;
-      cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, c->device);
-      per_sm = std::max(1, std::min(static_cast<int>(max_smem / (sm2 + 1024)), 64 / p->warps));
-      p->blocks = dev_sms * per_sm;
-    }
-  }
-  if (e != cudaSuccess) {
+  if (smem > static_cast<size_t>(optin))
+    return fail(EAPDTW_EINVAL, "search: query length exceeds the shared-memory budget");
+  const int per_sm = std::max(1, std::min(static_cast<int>(max_smem / (smem + 1024)), 64 / p->warps));
+  p->blocks = sms * per_sm;
+  return eapdtw_search_plan_reset(p);
+}
+
+int eapdtw_search_plan_create(eapdtw_ctx* c, const double* ref_dev, size_t n, const double* query,
+                              size_t qlen, const eapdtw_search_config* cfg, uint64_t offset,
+                              eapdtw_search_plan** out) {
+  if (!c || !cfg || !out) return fail(EAPDTW_EINVAL, "search: null argument");
+  auto* p = new eapdtw_search_plan();
+  const int e = plan_init(p, c, ref_dev, n, query, qlen, cfg, offset);
+  if (e) {
+    const std::string msg = g_err;
     eapdtw_search_plan_destroy(p);
-    return fail(EAPDTW_ECUDA, std::string("search plan: ") + cudaGetErrorString(e));
+    g_err = msg;
+    return e;
   }
   *out = p;
   return EAPDTW_OK;
 }
 
+int eapdtw_search_plan_reset(eapdtw_search_plan* p) {
+  if (!p) return fail(EAPDTW_EINVAL, "null plan");
+  eapdtw_ctx* c = p->ctx;
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t s = c->stream;
+  PlanBuffers& B = *p->buf;
+  CUDA_TRY(cudaMemsetAsync(B.counters.p, 0, kNumCounters * 8, s));
+  CUDA_TRY(cudaMemsetAsync(B.probe_counters.p, 0, kNumCounters * 8, s));
+  CUDA_TRY(launch_init_best(B.best.as<BestRecord>(), p->key, 1, s));
+  ++c->launches;
+  p->prepared = false;
+  p->ran = false;
+  p->t0 = std::chrono::steady_clock::now();
+  return EAPDTW_OK;
+}
+
+int eapdtw_search_plan_set_ub_key(eapdtw_search_plan* p, uint64_t* dev_key) {
+  if (!p) return fail(EAPDTW_EINVAL, "null plan");
+  p->key = dev_key ? reinterpret_cast<unsigned long long*>(dev_key)
+                   : p->buf->key.as<unsigned long long>();
+  return eapdtw_search_plan_reset(p);
+}
+
 size_t eapdtw_search_plan_candidates(const eapdtw_search_plan* p) { return p ? p->ncand : 0; }
 uint64_t* eapdtw_search_plan_ub_key(eapdtw_search_plan* p) {
-  return p ? p->key.as<uint64_t>() : nullptr;
+  return p ? reinterpret_cast<uint64_t*>(p->key) : nullptr;
+}
+
+// Zero the chunk counter and queue counters, fill the queue with -1 (empty).
+static cudaError_t reset_work(eapdtw_search_plan* p, long long count, cudaStream_t s) {
+  PlanBuffers& B = *p->buf;
+  cudaError_t e = cudaMemsetAsync(B.work.p, 0, 8, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(B.qctr.p, 0, 24, s);
+  if (e == cudaSuccess && count > 0)
+    e = cudaMemsetAsync(B.queue.p, 0xff, static_cast<size_t>(count) * 8, s);
+  return e;
 }
 
 static SearchParams base_params(eapdtw_search_plan* p) {
+  PlanBuffers& B = *p->buf;
   SearchParams s{};
   s.ref = p->ref;
-  s.mean = p->mean.as<double>();
-  s.sd = p->sd.as<double>();
-  s.env_up = p->have_env ? p->up.as<double>() : nullptr;
-  s.env_lo = p->have_env ? p->lo.as<double>() : nullptr;
-  s.q = p->q.as<double>();
-  s.qu = p->qu.as<double>();
-  s.ql = p->ql.as<double>();
-  s.order = p->order.as<int>();
+  s.mean = B.mean.as<double>();
+  s.sd = B.sd.as<double>();
+  s.env_up = p->have_env ? B.up.as<double>() : nullptr;
+  s.env_lo = p->have_env ? B.lo.as<double>() : nullptr;
+  s.q = B.q.as<double>();
+  s.qu = B.qu.as<double>();
+  s.ql = B.ql.as<double>();
+  s.order = B.order.as<int>();
   s.ncand = static_cast<long long>(p->ncand);
   s.m = static_cast<int>(p->m);
   s.w = p->w_eff;
@@ -482,10 +535,15 @@ static SearchParams base_params(eapdtw_search_plan* p) {
   s.prune = p->algo == EAPDTW_ALGO_FULL ? 0 : 1;
   s.guard_rel = p->guard_rel;
   s.guard_abs = p->guard_abs;
-  s.ub_key = p->key.as<unsigned long long>();
-  s.best = p->best.as<BestRecord>();
-  s.work = p->work.as<unsigned long long>();
-  s.counters = p->counters.as<unsigned long long>();
+  s.ub_key = p->key;
+  s.best = B.best.as<BestRecord>();
+  s.work = B.work.as<unsigned long long>();
+  s.queue = B.queue.as<long long>();
+  s.qhead = B.qctr.as<unsigned long long>();
+  s.qtail = B.qctr.as<unsigned long long>() + 1;
+  s.chunks_done = B.qctr.as<unsigned long long>() + 2;
+  s.direct_chunk = 4;
+  s.counters = B.counters.as<unsigned long long>();
   s.index_offset = static_cast<long long>(p->offset);
   return s;
 }
@@ -493,17 +551,18 @@ static SearchParams base_params(eapdtw_search_plan* p) {
 int eapdtw_search_plan_prepare(eapdtw_search_plan* p) {
   if (!p) return fail(EAPDTW_EINVAL, "null plan");
   eapdtw_ctx* c = p->ctx;
+  PlanBuffers& B = *p->buf;
   CUDA_TRY(cudaSetDevice(c->device));
   cudaStream_t s = c->stream;
   CUDA_TRY(cudaEventRecord(p->ev[0], s));
   CUDA_TRY(launch_stats(p->ref, static_cast<long long>(p->n), static_cast<int>(p->m),
-                        p->mean.as<double>(), p->sd.as<double>(), s));
+                        B.mean.as<double>(), B.sd.as<double>(), s));
   ++c->launches;
   CUDA_TRY(cudaEventRecord(p->ev[1], s));
   p->have_env = false;
   if (p->use_lb && p->m >= 2) {
     const cudaError_t e = launch_envelope(p->ref, static_cast<long long>(p->n), p->env_r,
-                                          p->up.as<double>(), p->lo.as<double>(), s);
+                                          B.up.as<double>(), B.lo.as<double>(), s);
     if (e == cudaSuccess) {
       p->have_env = true;
       ++c->launches;
@@ -522,12 +581,12 @@ int eapdtw_search_plan_prepare(eapdtw_search_plan* p) {
   sp.use_lb = 0;
   sp.begin = 0;
   sp.stride = static_cast<long long>(std::max<size_t>(1, p->ncand / nprobe));
-  sp.end = std::min<long long>(static_cast<long long>(p->ncand), sp.stride * static_cast<long long>(nprobe));
-  sp.counters = p->probe_counters.as<unsigned long long>();
-  CUDA_TRY(cudaMemsetAsync(p->work.p, 0, 8, s));
-  const long long probe_warps = (static_cast<long long>(nprobe) + 31) / 32;
-  const int pblocks = static_cast<int>(std::max<long long>(1, std::min<long long>(p->blocks, (probe_warps + p->warps - 1) / p->warps)));
-  CUDA_TRY(launch_search(sp, pblocks, p->warps, s));
+  sp.end = std::min<long long>(static_cast<long long>(p->ncand),
+                               sp.stride * static_cast<long long>(nprobe));
+  sp.counters = B.probe_counters.as<unsigned long long>();
+  sp.direct_chunk = 1;
+  CUDA_TRY(reset_work(p, static_cast<long long>(nprobe), s));
+  CUDA_TRY(launch_search(sp, p->blocks, p->warps, s));
   ++c->launches;
   CUDA_TRY(cudaEventRecord(p->ev[3], s));
   p->prepared = true;
@@ -549,23 +608,25 @@ int eapdtw_search_plan_run(eapdtw_search_plan* p, size_t begin, size_t end) {
   sp.begin = static_cast<long long>(begin);
   sp.end = static_cast<long long>(end);
   sp.stride = 1;
-  CUDA_TRY(cudaEventRecord(p->ev[4], s));
-  CUDA_TRY(cudaMemsetAsync(p->work.p, 0, 8, s));
+  if (!p->ran) CUDA_TRY(cudaEventRecord(p->ev[4], s));
+  CUDA_TRY(reset_work(p, static_cast<long long>(end - begin), s));
   CUDA_TRY(launch_search(sp, p->blocks, p->warps, s));
   ++c->launches;
   CUDA_TRY(cudaEventRecord(p->ev[5], s));
+  p->ran = true;
   return EAPDTW_OK;
 }
 
 int eapdtw_search_plan_result(eapdtw_search_plan* p, eapdtw_search_result* out) {
   if (!p || !out) return fail(EAPDTW_EINVAL, "null argument");
   eapdtw_ctx* c = p->ctx;
+  PlanBuffers& B = *p->buf;
   CUDA_TRY(cudaSetDevice(c->device));
   BestRecord rec{};
   unsigned long long cnt[kNumCounters], pc[kNumCounters];
-  CUDA_TRY(cudaMemcpyAsync(&rec, p->best.p, sizeof(rec), cudaMemcpyDeviceToHost, c->stream));
-  CUDA_TRY(cudaMemcpyAsync(cnt, p->counters.p, sizeof(cnt), cudaMemcpyDeviceToHost, c->stream));
-  CUDA_TRY(cudaMemcpyAsync(pc, p->probe_counters.p, sizeof(pc), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(&rec, B.best.p, sizeof(rec), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(cnt, B.counters.p, sizeof(cnt), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(pc, B.probe_counters.p, sizeof(pc), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   std::memset(out, 0, sizeof(*out));
   out->found = rec.d != kInf ? 1 : 0;
@@ -575,7 +636,7 @@ int eapdtw_search_plan_result(eapdtw_search_plan* p, eapdtw_search_result* out) 
   out->pruned_kim = cnt[kCntKim];
   out->pruned_keogh_eq = cnt[kCntKeoghEq];
   out->pruned_keogh_ec = cnt[kCntKeoghEc];
-  out->dtw_calls = out->candidates_total - out->pruned_kim - out->pruned_keogh_eq - out->pruned_keogh_ec;
+  out->dtw_calls = cnt[kCntDtwCalls];
   out->dtw_abandoned = cnt[kCntDtwAbandoned];
   out->dp_cells_evaluated = cnt[kCntCells] + pc[kCntCells];
   out->elapsed_seconds =
@@ -596,29 +657,49 @@ int eapdtw_search_plan_timings(eapdtw_search_plan* p, float* ms4) {
 
 int eapdtw_search_plan_destroy(eapdtw_search_plan* p) {
   if (!p) return EAPDTW_OK;
-  cudaSetDevice(p->ctx->device);
-  cudaStreamSynchronize(p->ctx->stream);
-  for (DevBuf* b : {&p->mean, &p->sd, &p->up, &p->lo, &p->q, &p->qu, &p->ql, &p->order, &p->best,
-                    &p->key, &p->work, &p->counters, &p->probe_counters})
-    b->release();
+  if (p->ctx) {
+    cudaSetDevice(p->ctx->device);
+    cudaStreamSynchronize(p->ctx->stream);
+  }
+  p->own.release();
   for (auto& ev : p->ev)
     if (ev) cudaEventDestroy(ev);
   delete p;
   return EAPDTW_OK;
 }
 
+static int one_shot(eapdtw_ctx* c, const double* ref_dev, size_t n, const double* query,
+                    size_t qlen, const eapdtw_search_config* cfg, bool check_ref,
+                    eapdtw_search_result* out) {
+  if (!c || !cfg || !out) return fail(EAPDTW_EINVAL, "null argument");
+  eapdtw_search_plan p;
+  p.buf = &c->pb;  // reuse the context's grow-only scratch
+  int e = plan_init(&p, c, ref_dev, n, query, qlen, cfg, 0);
+  if (!e && check_ref) {
+    // Series validation (series.hpp:24-31) of the reference, on the device.
+    CUDA_TRY(cudaMemsetAsync(c->pb.flag.p, 0, 8, c->stream));
+    CUDA_TRY(launch_check_finite(ref_dev, static_cast<long long>(n),
+                                 c->pb.flag.as<unsigned long long>(), c->stream));
+    ++c->launches;
+  }
+  if (!e) e = eapdtw_search_plan_prepare(&p);
+  if (!e) e = eapdtw_search_plan_run(&p, 0, p.ncand);
+  if (!e) e = eapdtw_search_plan_result(&p, out);
+  if (!e && check_ref) {
+    unsigned long long bad = 0;
+    CUDA_TRY(cudaMemcpy(&bad, c->pb.flag.p, 8, cudaMemcpyDeviceToHost));
+    if (bad) e = fail(EAPDTW_EINVAL, "Series: non-finite sample in the reference");
+  }
+  for (auto& ev : p.ev)
+    if (ev) cudaEventDestroy(ev);
+  p.buf = &p.own;
+  return e;
+}
+
 int eapdtw_similarity_search_dev(eapdtw_ctx* c, const double* ref_dev, size_t n,
                                  const double* query, size_t qlen,
                                  const eapdtw_search_config* cfg, eapdtw_search_result* out) {
-  if (!out) return fail(EAPDTW_EINVAL, "null out");
-  eapdtw_search_plan* p = nullptr;
-  int e = eapdtw_search_plan_create(c, ref_dev, n, query, qlen, cfg, 0, &p);
-  if (e) return e;
-  e = eapdtw_search_plan_prepare(p);
-  if (!e) e = eapdtw_search_plan_run(p, 0, p->ncand);
-  if (!e) e = eapdtw_search_plan_result(p, out);
-  eapdtw_search_plan_destroy(p);
-  return e;
+  return one_shot(c, ref_dev, n, query, qlen, cfg, true, out);
 }
 
 int eapdtw_similarity_search(eapdtw_ctx* c, const double* ref, size_t n, const double* query,
@@ -626,11 +707,10 @@ int eapdtw_similarity_search(eapdtw_ctx* c, const double* ref, size_t n, const d
                              eapdtw_search_result* out) {
   if (!c || !ref) return fail(EAPDTW_EINVAL, "null argument");
   if (n == 0) return fail(EAPDTW_EINVAL, "Series: empty input");
-  if (!all_finite(ref, n)) return fail(EAPDTW_EINVAL, "Series: non-finite sample");
   CUDA_TRY(cudaSetDevice(c->device));
   CUDA_TRY(c->ref.ensure(n * 8));
   CUDA_TRY(cudaMemcpyAsync(c->ref.p, ref, n * 8, cudaMemcpyHostToDevice, c->stream));
-  return eapdtw_similarity_search_dev(c, c->ref.as<double>(), n, query, qlen, cfg, out);
+  return one_shot(c, c->ref.as<double>(), n, query, qlen, cfg, true, out);
 }
 
 // ---------------------------------------------------------------------------

@@ -23,19 +23,30 @@
 //     are non-negative and IEEE addition is monotone.  Hence the returned
 //     value is bit-identical to the full DP whenever that value is <= ub, and
 //     +inf (PRUNED, series.hpp:16) otherwise -- the contract pinned by
-//     test_dtw.cpp:183-201 and :267-289.
-//   * KILL=true additionally replaces dead cells by +inf; it is used with the
-//     per-row thresholds of a cumulative bound (row_threshold, dtw.cpp:81-86),
-//     whose thresholds grow with the row so a dead value must not come back.
+//     test_dtw.cpp:183-201 and :267-289.  Liveness inside the loop is tested
+//     on the high 32 bits only (hi(v) <= hi(ub)), which keeps a SUPERSET of
+//     the live cells (sound); the returned value is checked exactly.
+//   * KILL=true replaces dead cells by +inf with an exact test; it is used
+//     with the per-row thresholds of a cumulative bound (row_threshold,
+//     dtw.cpp:81-86), whose thresholds grow with the row so a dead value must
+//     not come back.
+//
+// Shared-memory contract (both arrays padded so no index is ever clamped):
+//   qsp    : column series, qsp[j] for j in [1, lc]; qsp[j] = +inf for
+//            j in [-kPadL, 0] and [lc+1, lc+kPadR]   (an out-of-range column
+//            costs (c - inf)^2 = +inf, which masks the matrix edges for free)
+//   rowbuf : lc+2 doubles plus the same padding; owned by the warp.
 #pragma once
-#include <cstdint>
 #include <cfloat>
 #include <climits>
+#include <cstdint>
 #include <cuda_runtime.h>
 
 namespace eapdtw_b200 {
 
 constexpr unsigned kFull = 0xffffffffu;
+constexpr int kPadL = 32;  // left padding of qsp / rowbuf (doubles)
+constexpr int kPadR = 40;  // right padding
 
 __device__ __forceinline__ double d_inf() { return __longlong_as_double(0x7ff0000000000000LL); }
 
@@ -79,23 +90,29 @@ __device__ __forceinline__ double load_ub(const unsigned long long* key) {
 // Evaluate one pruned DTW with a warp.
 //   rowval(k)  : value of row k (0-based), evaluated once per lane per strip
 //   lr         : number of rows (the longer series, reference orient dtw.cpp:48-52)
-//   qs         : column series in shared/global memory, 1-based (qs[1..lc])
+//   qsp        : padded column series (see contract above)
 //   w          : effective half window (effective_window, dtw.cpp:57-62)
 //   get_ub()   : current threshold, re-read at every strip (warp-uniform)
-//   rowthr(i)  : per-row threshold given the strip ub (identity without a cb)
-//   rowbuf     : per-warp scratch, lc+1 doubles
+//   rowthr(u,i): per-row threshold given the strip ub (identity without a cb)
+//   rowbuf     : padded per-warp scratch (see contract above)
 //   cells      : incremented (by lane 0) with the number of evaluated cells
 template <bool KILL, class RowFn, class UbFn, class RowThrFn>
-__device__ double warp_dtw(const RowFn& rowval, int lr, const double* __restrict__ qs, int lc,
+__device__ double warp_dtw(const RowFn& rowval, int lr, const double* __restrict__ qsp, int lc,
                            int w, UbFn&& get_ub, RowThrFn&& rowthr, double* __restrict__ rowbuf,
                            unsigned long long& cells) {
   const int lane = threadIdx.x & 31;
   const double INF = d_inf();
-  int lo = 0, hi = 0;  // live column range of the row held in rowbuf (row i0-1)
-  if (lane == 0) rowbuf[0] = 0.0;
+  for (int k = lane; k <= lc + 1; k += 32) rowbuf[k] = k == 0 ? 0.0 : INF;
   __syncwarp();
-  double result = INF;
-  unsigned long long ncell = 0;
+  // Band |i - j| <= w.  With w >= lr every (i, j) is inside it; the offset
+  // d = j - i + w is then shifted so the same unsigned test always passes.
+  const bool banded = w < lr;
+  const int w2 = banded ? 2 * w : INT_MAX / 2;
+  const int woff = banded ? w : INT_MAX / 4;
+  int lo = 0, hi = 0;  // live column range of the row held in rowbuf (row i0-1)
+  int written = 0;     // highest rowbuf column that may hold a non-inf value
+  unsigned cnt = 0;
+  double ub_last = INF;
 
   for (int i0 = 1; i0 <= lr; i0 += 32) {
     const double ub_strip = get_ub();
@@ -104,60 +121,69 @@ __device__ double warp_dtw(const RowFn& rowval, int lr, const double* __restrict
     // Clamp to the largest finite double so an infinite threshold never
     // makes an unreachable (+inf) cell "live".
     const double ub = fmin(rowthr(ub_strip, i), DBL_MAX);
-    const double c = active ? rowval(i - 1) : 0.0;
-    const int last_lane = min(31, lr - i0);
+    ub_last = __shfl_sync(kFull, ub, min(31, lr - i0));
+    const int ub_hi = __double2hiint(ub);
+    // Inactive rows (past lr) see c = +inf: all their cells are +inf.
+    const double c = active ? rowval(i - 1) : INF;
+    const int wl = min(31, lr - i0);  // writer lane: the last row of the strip
     const int jb = max(lo, 1);
-    const int bl = max(max(1, i - w), jb);       // first computable column of row i
-    const int bh = active ? min(lc, i + w) : -1;  // last band column of row i
-    double left = INF;
-    double v = INF;
     double top_prev = (lane == 0 && jb - 1 >= lo && jb - 1 <= hi) ? rowbuf[jb - 1] : INF;
+    int j = jb - lane;
+    int d = j - i + woff;
+    double v = INF;
     bool fin = !active;
     unsigned finmask = __ballot_sync(kFull, fin);
-    int newlo = INT_MAX, newhi = -1;
-    int j = jb - lane;
-
-    for (;;) {
-      const double shfl = __shfl_up_sync(kFull, v, 1);
-      const bool up_fin = lane == 0 ? (j > hi) : ((finmask >> (lane - 1)) & 1u);
-      double top = shfl;
-      if (lane == 0) top = (j >= lo && j <= hi) ? rowbuf[j] : INF;
+    int newlo = -1, newhi = -1;
+    int t = 0;
+    for (;; ++t) {
+      double top = __shfl_up_sync(kFull, v, 1);
+      if (lane == 0) top = rowbuf[j];
       const double diag = top_prev;
       top_prev = top;
-      const bool inb = !fin && j >= bl && j <= bh;
-      double nv = INF;
-      if (inb) nv = __dadd_rn(sq_cost(c, qs[j]), dmin2(left, dmin2(top, diag)));
-      const bool live = nv <= ub;
-      if (KILL && !live) nv = INF;
-      if (live) {
-        newlo = min(newlo, j);
-        newhi = j;
+      const bool inb = static_cast<unsigned>(d) <= static_cast<unsigned>(w2);
+      double nv = __dadd_rn(sq_cost(c, qsp[j]), dmin2(v, dmin2(top, diag)));
+      nv = inb ? nv : INF;
+      bool live;
+      if (KILL) {
+        live = nv <= ub;
+        nv = live ? nv : INF;
+      } else {
+        live = __double2hiint(nv) <= ub_hi;  // nv >= 0: superset of nv <= ub
       }
-      if (lane == last_lane && j == lc && live && i == lr) result = nv;
-      if (lane == 31 && inb) rowbuf[j] = nv;
-      left = nv;
+      if (lane == wl) rowbuf[j] = nv;
       v = nv;
-      fin = fin || j > bh || (up_fin && !live);
-      const unsigned inbmask = __ballot_sync(kFull, inb);
-      ncell += __popc(inbmask);
+      cnt += (inb && !fin) ? 1u : 0u;
+      const bool upf = lane == 0 ? (j > hi) : ((finmask >> (lane - 1)) & 1u);
+      fin = fin || j > lc || d > w2 || (upf && !live);
       finmask = __ballot_sync(kFull, fin);
+      const unsigned lm = __ballot_sync(kFull, live);
+      if ((lm >> wl) & 1u) {
+        const int jw = jb + t - wl;
+        if (newlo < 0) newlo = jw;
+        newhi = jw;
+      }
       if (finmask == kFull) break;
       ++j;
+      ++d;
     }
+    // The writer lane stopped at column jb + t - wl; anything it wrote in an
+    // earlier strip beyond that is stale and must read as +inf.
+    const int wend = jb + t - wl;
+    for (int k = max(wend + 1, 0) + lane; k <= min(written, lc + 1); k += 32) rowbuf[k] = INF;
+    written = max(wend, 0);
     __syncwarp();
-    const int lo_n = __shfl_sync(kFull, newlo, last_lane);
-    const int hi_n = __shfl_sync(kFull, newhi, last_lane);
-    if (hi_n < 0) {  // the last row of the strip has no live cell: borders collided
-      result = INF;
+    if (newhi < 0) {  // the last row of the strip has no live cell: borders collided
+      lo = -1;
       break;
     }
-    lo = lo_n;
-    hi = hi_n;
+    lo = newlo;
+    hi = newhi;
   }
-  if (lane == 0) cells += ncell;
-  // Only the lane that owns row lr holds a finite result; warp-wide min.
-  for (int off = 16; off > 0; off >>= 1) result = dmin2(result, __shfl_xor_sync(kFull, result, off));
-  return result;
+  for (int off = 16; off > 0; off >>= 1) cnt += __shfl_xor_sync(kFull, cnt, off);
+  if (lane == 0) cells += cnt;
+  if (lo < 0 || hi != lc) return INF;
+  const double r = rowbuf[lc];
+  return r <= ub_last ? r : INF;
 }
 
 }  // namespace eapdtw_b200

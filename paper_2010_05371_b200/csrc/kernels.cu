@@ -11,6 +11,7 @@
 // line of defence.
 #include <cfloat>
 #include <climits>
+#include <algorithm>
 
 #include "kernels.cuh"
 
@@ -199,38 +200,59 @@ cudaError_t launch_envelope(const double* ref, long long n, int r, double* up, d
 // Fused persistent search kernel (the cascade_decision + kernel dispatch of
 // search.cpp:160-204, re-organised for a GPU).
 //
-// A warp claims 32 consecutive candidates at a time (atomic chunk counter, so
-// the sweep advances through the reference roughly in order, like the CPU's
-// sequential best-so-far).  The lower-bound tiers run lane-per-candidate over
-// coalesced 256-byte rows of the reference; every tier prunes against the
-// CURRENT global threshold.  Survivors are then evaluated one at a time by the
-// whole warp with warp_dtw, re-reading the threshold at every 32-row strip.
+// Two kinds of work share one persistent grid:
+//   * LB chunks: a warp claims 32 consecutive candidates (atomic chunk
+//     counter, so the sweep advances through the reference in order like the
+//     CPU's sequential best-so-far) and runs the lower-bound tiers
+//     lane-per-candidate over coalesced 256-byte rows of the reference, each
+//     tier pruning against the CURRENT global threshold.  Survivors are
+//     appended to a global queue.
+//   * DTW tasks: a warp pops one survivor and evaluates it with warp_dtw,
+//     re-reading the threshold at every 32-row strip.
+// A warp always drains the queue before claiming a new chunk, so a chunk's
+// survivors are spread over the whole GPU instead of serialising on one warp.
 //
-// Soundness: LB_Kim is compared exactly (it is bit-for-bit <= the DTW value,
-// see DESIGN.md); the Keogh tiers normalise by reciprocal multiplication and
-// prune only when lb > ub*(1+guard_rel) + guard_abs.
+// Soundness: LB_Kim is computed with the DTW's own IEEE divisions and is
+// bit-for-bit <= the DTW value; the Keogh tiers normalise by
+// reciprocal multiplication and prune only when lb > ub*(1+guard_rel) +
+// guard_abs.  Survivors are evaluated exactly, and the record
+// keeps the lowest index among equal distances, so the result is the
+// reference's (first strict minimum, search.cpp:199).
 // ---------------------------------------------------------------------------
+static __host__ __device__ inline size_t padded_len(int m) { return static_cast<size_t>(m) + 2 + kPadL + kPadR; }
+
 size_t search_smem_bytes(int m, int warps) {
-  return static_cast<size_t>(m + 1) * 8       // q (1-based)
-         + static_cast<size_t>(m) * 8 * 2     // qu, ql
-         + static_cast<size_t>(m) * 4         // order
-         + static_cast<size_t>(warps) * (m + 1) * 8  // row buffers
+  return padded_len(m) * 8                        // q (padded, 1-based)
+         + static_cast<size_t>(m) * 8 * 2         // qu, ql
+         + static_cast<size_t>(m) * 4 + 8         // order
+         + static_cast<size_t>(warps) * padded_len(m) * 8  // row buffers
          + 64;
+}
+
+__device__ __forceinline__ long long vload(const long long* p) {
+  return *reinterpret_cast<const volatile long long*>(p);
+}
+__device__ __forceinline__ unsigned long long vload(const unsigned long long* p) {
+  return *reinterpret_cast<const volatile unsigned long long*>(p);
 }
 
 __global__ void __launch_bounds__(256) search_kernel(SearchParams p) {
   extern __shared__ double smem[];
   const int m = p.m;
-  double* q = smem;             // [m+1]
-  double* qu = q + (m + 1);     // [m]
-  double* ql = qu + m;          // [m]
-  int* order = reinterpret_cast<int*>(ql + m);  // [m]
-  const int warps = blockDim.x >> 5;
+  const size_t plen = padded_len(m);
+  double* qsp = smem + kPadL;                      // qsp[-kPadL .. m+1+kPadR)
+  double* qu = smem + plen;                        // [m]
+  double* ql = qu + m;                             // [m]
+  int* order = reinterpret_cast<int*>(ql + m);     // [m]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* rowbuf = reinterpret_cast<double*>(order + m + (m & 1)) + static_cast<size_t>(warp) * (m + 1);
-  (void)warps;
+  double* rowbuf = reinterpret_cast<double*>(order + m + 2 - (m & 1)) +
+                   static_cast<size_t>(warp) * plen + kPadL;
 
-  for (int k = threadIdx.x; k <= m; k += blockDim.x) q[k] = p.q[k];
+  const double INF = d_inf();
+  for (int k = threadIdx.x; k < static_cast<int>(plen); k += blockDim.x) {
+    const int j = k - kPadL;
+    smem[k] = (j >= 1 && j <= m) ? p.q[j] : INF;
+  }
   if (p.use_lb) {
     for (int k = threadIdx.x; k < m; k += blockDim.x) {
       qu[k] = p.qu[k];
@@ -240,33 +262,110 @@ __global__ void __launch_bounds__(256) search_kernel(SearchParams p) {
   }
   __syncthreads();
 
-  const double INF = d_inf();
   unsigned long long c_kim = 0, c_eq = 0, c_ec = 0, c_calls = 0, c_aband = 0, c_cells = 0,
                      c_cand = 0;
   const double* __restrict__ ref = p.ref;
+  const bool prune = p.prune != 0;
 
-  for (;;) {
-    unsigned long long chunk = 0;
-    if (lane == 0) chunk = atomicAdd(p.work, 1ull);
-    chunk = __shfl_sync(kFull, chunk, 0);
-    const long long base = p.begin + static_cast<long long>(chunk) * 32 * p.stride;
-    if (base >= p.end) break;
-    const long long s = base + lane * p.stride;
-    const bool valid = s < p.end;
-    c_cand += __popc(__ballot_sync(kFull, valid));
-    const double mean = valid ? p.mean[s] : 0.0;
-    const double sd = valid ? p.sd[s] : 1.0;
-    const bool constant = sd < kMinStddev;
-    bool alive = valid;
-    double ub = load_ub(p.ub_key);
+  // One exact pruned DTW of candidate `cand` with the whole warp.
+  auto run_dtw = [&](long long cand) {
+    const double cm = p.mean[cand];
+    const double cs = p.sd[cand];
+    const bool cconst = cs < kMinStddev;
+    const double* crow = ref + cand;
+    auto rowval = [&](int r) -> double {
+      return cconst ? 0.0 : __ddiv_rn(__dsub_rn(crow[r], cm), cs);
+    };
+    auto get_ub = [&]() -> double { return prune ? load_ub(p.ub_key) : INF; };
+    auto rowthr = [](double u, int) -> double { return u; };
+    const double d = warp_dtw<false>(rowval, m, qsp, m, p.w, get_ub, rowthr, rowbuf, c_cells);
+    ++c_calls;
+    if (d == INF) {
+      ++c_aband;
+    } else if (lane == 0) {
+      atomicMin(p.ub_key, static_cast<unsigned long long>(__double_as_longlong(d)));
+      best_record_update(p.best, d, static_cast<unsigned long long>(cand + p.index_offset));
+    }
+  };
 
-    if (p.use_lb) {
+  if (!p.use_lb) {
+    // ---- direct mode (EAPrunedDTW alone, and the probe): every candidate is
+    //      a DTW task; warps claim `direct_chunk` candidates at a time.
+    const long long K = p.direct_chunk;
+    for (;;) {
+      unsigned long long c = 0;
+      if (lane == 0) c = atomicAdd(p.work, 1ull);
+      c = __shfl_sync(kFull, c, 0);
+      const long long base = p.begin + static_cast<long long>(c) * K * p.stride;
+      if (base >= p.end) break;
+      for (long long k = 0; k < K; ++k) {
+        const long long s = base + k * p.stride;
+        if (s >= p.end) break;
+        ++c_cand;
+        run_dtw(s);
+      }
+    }
+  } else {
+    // ---- cascade mode.  Survivor queue protocol (no CAS retries):
+    //   producers reserve slots with atomicAdd(qtail) and fill them;
+    //   a consumer takes a slot with atomicAdd(qhead) only when head < tail
+    //   was observed, so it may hold a "future" slot that a producer fills a
+    //   little later -- meanwhile it keeps producing.  Once every chunk has
+    //   been published (chunks_done == nchunks) a future slot beyond the final
+    //   tail is void.
+    const long long nchunks = (p.end - p.begin + 31) / 32;
+    bool chunks_left = true;
+    long long myslot = -1;
+    for (;;) {
+      long long cand = -1;
+      bool void_slot = false;
+      if (lane == 0) {
+        if (myslot < 0 && vload(p.qhead) < vload(p.qtail))
+          myslot = static_cast<long long>(atomicAdd(p.qhead, 1ull));
+        if (myslot >= 0) {
+          cand = vload(p.queue + myslot);
+          if (cand < 0 && !chunks_left &&
+              vload(p.chunks_done) == static_cast<unsigned long long>(nchunks) &&
+              static_cast<unsigned long long>(myslot) >= vload(p.qtail))
+            void_slot = true;
+        }
+      }
+      cand = __shfl_sync(kFull, cand, 0);
+      void_slot = __shfl_sync(kFull, void_slot, 0);
+      myslot = __shfl_sync(kFull, myslot, 0);
+      if (cand >= 0) {
+        myslot = -1;
+        run_dtw(cand);
+        continue;
+      }
+      if (void_slot) break;
+      if (!chunks_left) {
+        if (myslot < 0) break;  // nothing pending, nothing left to produce
+        continue;               // wait for the pending slot to be filled
+      }
+
+      // ---- lower-bound cascade on the next chunk of 32 candidates
+      unsigned long long chunk = 0;
+      if (lane == 0) chunk = atomicAdd(p.work, 1ull);
+      chunk = __shfl_sync(kFull, chunk, 0);
+      if (static_cast<long long>(chunk) >= nchunks) {
+        chunks_left = false;
+        continue;
+      }
+      const long long s = p.begin + static_cast<long long>(chunk) * 32 + lane;
+      const bool valid = s < p.end;
+      c_cand += __popc(__ballot_sync(kFull, valid));
+      bool alive = valid;
+      const double mean = valid ? p.mean[s] : 0.0;
+      const double sd = valid ? p.sd[s] : 1.0;
+      const bool constant = sd < kMinStddev;
+      double ub = load_ub(p.ub_key);
       // --- Tier 1: LB_Kim on the two aligned extremities (search.cpp:81-87),
       //     computed with the same IEEE divisions as the DTW rows.
       if (m >= 2 && alive) {
         const double c0 = constant ? 0.0 : __ddiv_rn(__dsub_rn(ref[s], mean), sd);
         const double cl = constant ? 0.0 : __ddiv_rn(__dsub_rn(ref[s + m - 1], mean), sd);
-        const double kim = __dadd_rn(sq_cost(q[1], c0), sq_cost(q[m], cl));
+        const double kim = __dadd_rn(sq_cost(qsp[1], c0), sq_cost(qsp[m], cl));
         if (kim > ub) {
           alive = false;
           ++c_kim;
@@ -288,8 +387,8 @@ __global__ void __launch_bounds__(256) search_kernel(SearchParams p) {
             const double cn = __dmul_rn(__dsub_rn(x, mean), rsd);
             const double e1 = cn - qu[j];
             const double e2 = ql[j] - cn;
-            const double d = e1 > 0.0 ? e1 : (e2 > 0.0 ? e2 : 0.0);
-            acc = fma(d, d, acc);
+            const double dd = e1 > 0.0 ? e1 : (e2 > 0.0 ? e2 : 0.0);
+            acc = fma(dd, dd, acc);
           }
           if (pending && acc > ubg) {
             pending = false;
@@ -316,11 +415,11 @@ __global__ void __launch_bounds__(256) search_kernel(SearchParams p) {
                 U = __dmul_rn(__dsub_rn(p.env_up[s + j], mean), rsd);
                 L = __dmul_rn(__dsub_rn(p.env_lo[s + j], mean), rsd);
               }
-              const double qj = q[j + 1];
+              const double qj = qsp[j + 1];
               const double e1 = qj - U;
               const double e2 = L - qj;
-              const double d = e1 > 0.0 ? e1 : (e2 > 0.0 ? e2 : 0.0);
-              acc = fma(d, d, acc);
+              const double dd = e1 > 0.0 ? e1 : (e2 > 0.0 ? e2 : 0.0);
+              acc = fma(dd, dd, acc);
             }
             if (pending && acc > ubg) {
               pending = false;
@@ -331,37 +430,24 @@ __global__ void __launch_bounds__(256) search_kernel(SearchParams p) {
           }
         }
       }
-    }
-
-    // --- Pruned DTW for the survivors, one warp-wide evaluation each, in
-    //     index order (strict < with the lowest index on ties, search.cpp:199).
-    unsigned mask = __ballot_sync(kFull, alive);
-    while (mask) {
-      const int k = __ffs(mask) - 1;
-      mask &= mask - 1;
-      const long long cand = base + k * p.stride;
-      const double cm = __shfl_sync(kFull, mean, k);
-      const double cs = __shfl_sync(kFull, sd, k);
-      const bool cconst = cs < kMinStddev;
-      const double* crow = ref + cand;
-      auto rowval = [&](int r) -> double {
-        return cconst ? 0.0 : __ddiv_rn(__dsub_rn(crow[r], cm), cs);
-      };
-      const bool prune = p.prune != 0;
-      auto get_ub = [&]() -> double { return prune ? load_ub(p.ub_key) : INF; };
-      auto rowthr = [](double u, int) -> double { return u; };
-      const double d = warp_dtw<false>(rowval, m, q, m, p.w, get_ub, rowthr, rowbuf, c_cells);
-      ++c_calls;
-      if (d == INF) {
-        ++c_aband;
-      } else if (lane == 0) {
-        atomicMin(p.ub_key, static_cast<unsigned long long>(__double_as_longlong(d)));
-        best_record_update(p.best, d, static_cast<unsigned long long>(cand + p.index_offset));
+      // ---- publish the survivors, then mark the chunk done
+      const unsigned mask = __ballot_sync(kFull, alive);
+      if (mask) {
+        unsigned long long qb = 0;
+        if (lane == 0) qb = atomicAdd(p.qtail, static_cast<unsigned long long>(__popc(mask)));
+        qb = __shfl_sync(kFull, qb, 0);
+        if (alive) {
+          const unsigned rank = __popc(mask & ((1u << lane) - 1u));
+          reinterpret_cast<volatile long long*>(p.queue)[qb + rank] = s;
+        }
       }
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) atomicAdd(p.chunks_done, 1ull);
     }
   }
 
-  // Per-lane tier counts are summed over the warp; chunk-level counts are warp-uniform.
+  // Per-lane tier counts are summed over the warp; the others are warp-uniform.
   for (int off = 16; off > 0; off >>= 1) {
     c_kim += __shfl_xor_sync(kFull, c_kim, off);
     c_eq += __shfl_xor_sync(kFull, c_eq, off);
@@ -398,15 +484,18 @@ __global__ void __launch_bounds__(256) pairwise_kernel(PairParams p) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wpb = blockDim.x >> 5;
   const int lc = p.lc;
-  double* cols = smem + static_cast<size_t>(warp) * (2 * lc + 2);  // [lc+1] 1-based
-  double* rowbuf = cols + lc + 1;                                 // [lc+1]
+  const size_t plen = padded_len(lc);
+  double* colsp = smem + static_cast<size_t>(warp) * 2 * plen + kPadL;  // padded, 1-based
+  double* rowbuf = colsp + plen;
   const double INF = d_inf();
   unsigned long long cells = 0;
+  for (int k = lane; k < static_cast<int>(plen); k += 32) colsp[k - kPadL] = INF;
+  __syncwarp();
   for (long long pr = static_cast<long long>(blockIdx.x) * wpb + warp; pr < p.npairs;
        pr += static_cast<long long>(gridDim.x) * wpb) {
     const double* rows = p.rows + pr * p.row_stride;
     const double* cg = p.cols + pr * p.col_stride;
-    for (int k = lane; k < lc; k += 32) cols[k + 1] = cg[k];
+    for (int k = lane; k < lc; k += 32) colsp[k + 1] = cg[k];
     __syncwarp();
     const double ub0 = p.ub ? p.ub[pr] : INF;
     auto rowval = [&](int r) -> double { return rows[r]; };
@@ -420,7 +509,7 @@ __global__ void __launch_bounds__(256) pairwise_kernel(PairParams p) {
       const double t = __dsub_rn(u, cb[k - 1]);
       return t > 0.0 ? t : 0.0;
     };
-    const double d = warp_dtw<WITH_CB>(rowval, lr, cols, lc, p.w, get_ub, rowthr, rowbuf, cells);
+    const double d = warp_dtw<WITH_CB>(rowval, lr, colsp, lc, w, get_ub, rowthr, rowbuf, cells);
     if (lane == 0) p.out[pr] = d;
     __syncwarp();
   }
@@ -428,8 +517,10 @@ __global__ void __launch_bounds__(256) pairwise_kernel(PairParams p) {
 }
 
 cudaError_t launch_pairwise(const PairParams& p, cudaStream_t stream) {
-  const int warps = 8;
-  const size_t smem = static_cast<size_t>(warps) * (2 * p.lc + 2) * sizeof(double);
+  int warps = 8;
+  while (warps > 1 && static_cast<size_t>(warps) * 2 * padded_len(p.lc) * 8 > 200 * 1024) warps /= 2;
+  const size_t smem = static_cast<size_t>(warps) * 2 * padded_len(p.lc) * sizeof(double);
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
   const long long need = (p.npairs + warps - 1) / warps;
   const int blocks = static_cast<int>(min(need, 148LL * 32));
   cudaError_t e;
@@ -458,15 +549,19 @@ __global__ void __launch_bounds__(256) nn1_kernel(Nn1Params p) {
   __shared__ unsigned long long s_next;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int L = p.len;
+  const size_t plen = padded_len(L);
   const long long qi = blockIdx.x / p.splits;
   const int part = blockIdx.x % p.splits;
   const long long k0 = p.nd * part / p.splits, k1 = p.nd * (part + 1) / p.splits;
-  double* q = smem;  // [L+1], 1-based
-  double* rowbuf = smem + (L + 1) + static_cast<size_t>(warp) * (L + 1);
-  for (int k = threadIdx.x; k < L; k += blockDim.x) q[k + 1] = p.queries[qi * L + k];
+  double* qsp = smem + kPadL;  // padded, 1-based
+  double* rowbuf = smem + plen + static_cast<size_t>(warp) * plen + kPadL;
+  const double INF = d_inf();
+  for (int k = threadIdx.x; k < static_cast<int>(plen); k += blockDim.x) {
+    const int j = k - kPadL;
+    smem[k] = (j >= 1 && j <= L) ? p.queries[qi * L + j - 1] : INF;
+  }
   if (threadIdx.x == 0) s_next = 0;
   __syncthreads();
-  const double INF = d_inf();
   unsigned long long* key = p.ub_keys + qi;
   unsigned long long cells = 0, calls = 0;
   for (;;) {
@@ -478,13 +573,13 @@ __global__ void __launch_bounds__(256) nn1_kernel(Nn1Params p) {
     const double* row = p.db + k * L;
     const double ub = load_ub(key);
     if (L >= 2) {  // LB_Kim_FL (lower_bounds.cpp:51-55): exact, so no guard needed
-      const double kim = __dadd_rn(sq_cost(q[1], row[0]), sq_cost(q[L], row[L - 1]));
+      const double kim = __dadd_rn(sq_cost(qsp[1], row[0]), sq_cost(qsp[L], row[L - 1]));
       if (kim > ub) continue;
     }
     auto rowval = [&](int r) -> double { return row[r]; };
     auto get_ub = [&]() -> double { return load_ub(key); };
     auto rowthr = [](double u, int) -> double { return u; };
-    const double d = warp_dtw<false>(rowval, L, q, L, p.w, get_ub, rowthr, rowbuf, cells);
+    const double d = warp_dtw<false>(rowval, L, qsp, L, p.w, get_ub, rowthr, rowbuf, cells);
     ++calls;
     if (d != INF && lane == 0) {
       atomicMin(key, static_cast<unsigned long long>(__double_as_longlong(d)));
@@ -499,7 +594,8 @@ __global__ void __launch_bounds__(256) nn1_kernel(Nn1Params p) {
 
 cudaError_t launch_nn1(const Nn1Params& p, cudaStream_t stream) {
   const int warps = 8;
-  const size_t smem = static_cast<size_t>(warps + 1) * (p.len + 1) * sizeof(double);
+  const size_t smem = static_cast<size_t>(warps + 1) * padded_len(p.len) * sizeof(double);
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(nn1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
@@ -520,6 +616,26 @@ __global__ void init_best_kernel(BestRecord* rec, unsigned long long* keys, long
 cudaError_t launch_init_best(BestRecord* rec, unsigned long long* keys, long long count,
                              cudaStream_t stream) {
   init_best_kernel<<<static_cast<unsigned>((count + 255) / 256), 256, 0, stream>>>(rec, keys, count);
+  return cudaGetLastError();
+}
+
+// Series validation (series.hpp:24-31) for references copied from the host:
+// one streaming pass sets *flag if any sample is non-finite.
+__global__ void check_finite_kernel(const double* __restrict__ x, long long n,
+                                    unsigned long long* flag) {
+  bool bad = false;
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x[i]));
+    bad |= (b & 0x7ff0000000000000ull) == 0x7ff0000000000000ull;
+  }
+  if (__any_sync(kFull, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1ull);
+}
+
+cudaError_t launch_check_finite(const double* x, long long n, unsigned long long* flag,
+                                cudaStream_t stream) {
+  const long long blocks = std::min<long long>((n + 255) / 256, 148LL * 16);
+  check_finite_kernel<<<static_cast<unsigned>(std::max<long long>(1, blocks)), 256, 0, stream>>>(x, n, flag);
   return cudaGetLastError();
 }
 

@@ -42,6 +42,11 @@ struct SearchParams {
   unsigned long long* ub_key;    // running threshold key (order-preserving bits)
   BestRecord* best;              // exact (d, lowest index) record
   unsigned long long* work;      // chunk counter (zeroed before launch)
+  long long* queue;              // survivor queue, -1 filled before launch
+  unsigned long long* qhead;     // next slot to consume (zeroed before launch)
+  unsigned long long* qtail;     // next slot to fill (zeroed before launch)
+  unsigned long long* chunks_done;  // LB chunks published (zeroed before launch)
+  long long direct_chunk;        // candidates per claim without the cascade
   unsigned long long* counters;  // kNumCounters
   long long index_offset;        // shard start in the global reference
 };
@@ -82,6 +87,8 @@ cudaError_t launch_pairwise(const PairParams& p, cudaStream_t stream);
 cudaError_t launch_nn1(const Nn1Params& p, cudaStream_t stream);
 cudaError_t launch_init_best(BestRecord* rec, unsigned long long* keys, long long count,
                              cudaStream_t stream);
+cudaError_t launch_check_finite(const double* x, long long n, unsigned long long* flag,
+                                cudaStream_t stream);
 cudaError_t launch_fp64_probe(double* sink, int blocks, int iters, cudaStream_t stream);
 
 }  // namespace eapdtw_b200

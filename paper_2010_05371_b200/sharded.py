@@ -1,0 +1,128 @@
+"""Multi-GPU subsequence search: one process per GPU, torch.distributed (NCCL).
+
+The reference series is split into contiguous candidate ranges, one per rank.
+Shard starts are multiples of 100000 candidates -- the stats reset interval of
+similarity_search (search.cpp:16, :164-167) -- and every shard carries the
+(m-1)-point halo its last candidates need, so each rank's stats chain is
+bit-identical to the unsharded one.  The only exchange is the
+best-so-far: between candidate batches the ranks all-reduce (MIN) the 8-byte
+order-preserving threshold key, so every rank prunes with the global best.  The
+final answer is the lexicographic (distance, lowest global index) minimum,
+gathered once at the end.
+
+The compute backend is pluggable so the host logic can be exercised on CPU
+with gloo (tests/test_sharded.py): ``GpuShard`` is the product backend (the
+C-ABI search plan); a test may pass any object with the same four methods.
+"""
+from __future__ import annotations
+
+import math
+import struct
+
+import numpy as np
+
+STATS_RESET = 100_000  # search.cpp:16
+
+
+def shard_bounds(ncand: int, world: int, rank: int) -> tuple[int, int]:
+    """Candidate range [s0, s1) of ``rank``: whole 100000-candidate segments,
+    split as evenly as possible (earlier ranks take the remainder)."""
+    nseg = (ncand + STATS_RESET - 1) // STATS_RESET
+    base, extra = divmod(nseg, world)
+    seg0 = rank * base + min(rank, extra)
+    seg1 = seg0 + base + (1 if rank < extra else 0)
+    return min(ncand, seg0 * STATS_RESET), min(ncand, seg1 * STATS_RESET)
+
+
+def key_of(d: float) -> int:
+    """Order-preserving int64 key of a non-negative double (its bit pattern)."""
+    return struct.unpack("<q", struct.pack("<d", float(d)))[0]
+
+
+def double_of(k: int) -> float:
+    return struct.unpack("<d", struct.pack("<q", int(k)))[0]
+
+
+INF_KEY = key_of(math.inf)
+
+
+def lexicographic_min(records):
+    """records: iterable of (found, distance, global_location)."""
+    best = (False, math.inf, 0)
+    for found, d, loc in records:
+        if not found:
+            continue
+        if not best[0] or (d, loc) < (best[1], best[2]):
+            best = (True, float(d), int(loc))
+    return best
+
+
+class GpuShard:
+    """Backend over the C-ABI search plan for one shard (device-resident)."""
+
+    def __init__(self, ref_shard_dev_ptr: int, n_points: int, query, cfg, global_offset: int,
+                 key_tensor, ctx=None):
+        from .api import SearchPlan
+        self.plan = SearchPlan(ref_shard_dev_ptr, n_points, query, cfg, global_offset, ctx=ctx)
+        self.key = key_tensor
+        self.plan.set_ub_key(key_tensor.data_ptr())
+
+    @property
+    def candidates(self) -> int:
+        return self.plan.candidates
+
+    def reset(self):
+        self.key.fill_(INF_KEY)
+        self.plan.reset()
+
+    def prepare(self):
+        self.plan.prepare()
+
+    def run(self, begin: int, end: int):
+        self.plan.run(begin, end)
+
+    def result(self):
+        return self.plan.result()
+
+
+class ShardedSearch:
+    """Drive one rank's shard with best-so-far exchange between batches."""
+
+    def __init__(self, backend, rank: int, world: int, batches: int = 8, group=None):
+        self.backend = backend
+        self.rank = rank
+        self.world = world
+        self.batches = max(1, int(batches))
+        self.group = group
+
+    def search(self):
+        import torch.distributed as dist
+        b = self.backend
+        b.reset()
+        b.prepare()
+        nc = b.candidates
+        edges = np.linspace(0, nc, self.batches + 1).astype(np.int64)
+        if self.world > 1:
+            # share the probe phase's best before the sweep starts
+            dist.all_reduce(b.key, op=dist.ReduceOp.MIN, group=self.group)
+        for k in range(self.batches):
+            b.run(int(edges[k]), int(edges[k + 1]))
+            if self.world > 1:
+                dist.all_reduce(b.key, op=dist.ReduceOp.MIN, group=self.group)
+        res = b.result()
+        return self.finalize(res)
+
+    def finalize(self, res):
+        """Lexicographic (distance, lowest global index) across ranks."""
+        import torch
+        import torch.distributed as dist
+        mine = (bool(res.best.found), float(res.best.distance_sq), int(res.best.location))
+        if self.world == 1:
+            return mine, res
+        dev = self.backend.key.device
+        t = torch.tensor([key_of(mine[1]) if mine[0] else INF_KEY, mine[2], int(mine[0])],
+                         dtype=torch.int64, device=dev)
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        dist.all_gather(out, t, group=self.group)
+        recs = [(bool(o[2].item()), double_of(o[0].item()), int(o[1].item())) for o in out]
+        return lexicographic_min(recs), res
