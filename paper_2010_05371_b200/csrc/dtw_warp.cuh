@@ -88,61 +88,82 @@ __device__ __forceinline__ double load_ub(const unsigned long long* key) {
 }
 
 // Evaluate one pruned DTW with a warp.
-//   rowval(k)  : value of row k (0-based), evaluated once per lane per strip
+//   rowraw(k)  : raw value of row k (0-based); loaded one strip ahead
+//   rownorm(x) : row value used by the DP (identity, or the exact z-norm)
 //   lr         : number of rows (the longer series, reference orient dtw.cpp:48-52)
 //   qsp        : padded column series (see contract above)
 //   w          : effective half window (effective_window, dtw.cpp:57-62)
-//   get_ub()   : current threshold, re-read at every strip (warp-uniform)
+//   get_ub()   : current threshold (warp-uniform); read one strip ahead
 //   rowthr(u,i): per-row threshold given the strip ub (identity without a cb)
 //   rowbuf     : padded per-warp scratch (see contract above)
 //   cells      : incremented (by lane 0) with the number of evaluated cells
-template <bool KILL, class RowFn, class UbFn, class RowThrFn>
-__device__ double warp_dtw(const RowFn& rowval, int lr, const double* __restrict__ qsp, int lc,
-                           int w, UbFn&& get_ub, RowThrFn&& rowthr, double* __restrict__ rowbuf,
+template <bool KILL, class RawFn, class NormFn, class UbFn, class RowThrFn>
+__device__ double warp_dtw(const RawFn& rowraw, const NormFn& rownorm, int lr,
+                           const double* __restrict__ qsp, int lc, int w, UbFn&& get_ub,
+                           RowThrFn&& rowthr, double* __restrict__ rowbuf,
                            unsigned long long& cells) {
   const int lane = threadIdx.x & 31;
   const double INF = d_inf();
   for (int k = lane; k <= lc + 1; k += 32) rowbuf[k] = k == 0 ? 0.0 : INF;
-  __syncwarp();
-  // Band |i - j| <= w.  With w >= lr every (i, j) is inside it; the offset
-  // d = j - i + w is then shifted so the same unsigned test always passes.
+  // Band |i - j| <= w.  With w >= lr every (i, j) is inside it.
   const bool banded = w < lr;
-  const int w2 = banded ? 2 * w : INT_MAX / 2;
-  const int woff = banded ? w : INT_MAX / 4;
   int lo = 0, hi = 0;  // live column range of the row held in rowbuf (row i0-1)
   int written = 0;     // highest rowbuf column that may hold a non-inf value
   unsigned cnt = 0;
   double ub_last = INF;
+  double ub_next = get_ub();
+  double x_next = lane < lr ? rowraw(lane) : 0.0;
+  __syncwarp();
 
   for (int i0 = 1; i0 <= lr; i0 += 32) {
-    const double ub_strip = get_ub();
+    const double ub_strip = ub_next;
     const int i = i0 + lane;
     const bool active = i <= lr;
+    const double x = x_next;
+    if (i0 + 32 <= lr) {  // prefetch the next strip's threshold and row values
+      ub_next = get_ub();
+      x_next = i + 32 <= lr ? rowraw(i + 31) : 0.0;
+    }
     // Clamp to the largest finite double so an infinite threshold never
     // makes an unreachable (+inf) cell "live".
     const double ub = fmin(rowthr(ub_strip, i), DBL_MAX);
-    ub_last = __shfl_sync(kFull, ub, min(31, lr - i0));
+    const int wl = min(31, lr - i0);  // writer lane: the last row of the strip
+    ub_last = __shfl_sync(kFull, ub, wl);
     const int ub_hi = __double2hiint(ub);
     // Inactive rows (past lr) see c = +inf: all their cells are +inf.
-    const double c = active ? rowval(i - 1) : INF;
-    const int wl = min(31, lr - i0);  // writer lane: the last row of the strip
+    const double c = active ? rownorm(x) : INF;
     const int jb = max(lo, 1);
+    // Row i's band columns [bl, bh]; the lane is finished once j > bh.
+    const int bl = banded ? max(1, i - w) : 1;
+    const int bh = active ? (banded ? min(lc, i + w) : lc) : -1;
     double top_prev = (lane == 0 && jb - 1 >= lo && jb - 1 <= hi) ? rowbuf[jb - 1] : INF;
     int j = jb - lane;
-    int d = j - i + woff;
+    const double* qp = qsp + j;
+    double* rp = rowbuf + j;
     double v = INF;
     bool fin = !active;
+    int jf = fin ? j - 1 : lc + 1;  // last column computed before finishing
     unsigned finmask = __ballot_sync(kFull, fin);
-    int newlo = -1, newhi = -1;
-    int t = 0;
-    for (;; ++t) {
-      double top = __shfl_up_sync(kFull, v, 1);
-      if (lane == 0) top = rowbuf[j];
+    const bool writer = lane == wl;
+    const bool is0 = lane == 0;
+
+    // Per-lane constants of the step: band range test on jr = j - bl, the
+    // finish test jr > span, the upstream-finished bit (lane 0's upstream is
+    // the row buffer: finished once j > hi, folded into bit 31, which no
+    // other lane reads).
+    const unsigned span = static_cast<unsigned>(bh - bl);
+    int jr = j - bl;
+    const unsigned upbit = is0 ? 0x80000000u : (1u << (lane - 1));
+
+    // One wavefront step at column j+u.
+    auto step = [&](int u) {
+      const double sh = __shfl_up_sync(kFull, v, 1);
+      const double top = is0 ? rp[u] : sh;
       const double diag = top_prev;
       top_prev = top;
-      const bool inb = static_cast<unsigned>(d) <= static_cast<unsigned>(w2);
-      double nv = __dadd_rn(sq_cost(c, qsp[j]), dmin2(v, dmin2(top, diag)));
-      nv = inb ? nv : INF;
+      double nv = __dadd_rn(sq_cost(c, qp[u]), dmin2(v, dmin2(top, diag)));
+      const int jru = jr + u;
+      nv = static_cast<unsigned>(jru) <= span ? nv : INF;
       bool live;
       if (KILL) {
         live = nv <= ub;
@@ -150,34 +171,59 @@ __device__ double warp_dtw(const RowFn& rowval, int lr, const double* __restrict
       } else {
         live = __double2hiint(nv) <= ub_hi;  // nv >= 0: superset of nv <= ub
       }
-      if (lane == wl) rowbuf[j] = nv;
+      if (writer) rp[u] = nv;
       v = nv;
-      cnt += (inb && !fin) ? 1u : 0u;
-      const bool upf = lane == 0 ? (j > hi) : ((finmask >> (lane - 1)) & 1u);
-      fin = fin || j > lc || d > w2 || (upf && !live);
+      const unsigned up = (finmask & 0x7fffffffu) | (j + u > hi ? 0x80000000u : 0u);
+      const bool nf = fin || jru > static_cast<int>(span) || ((up & upbit) && !live);
+      jf = (!fin && nf) ? j + u : jf;
+      fin = nf;
       finmask = __ballot_sync(kFull, fin);
-      const unsigned lm = __ballot_sync(kFull, live);
-      if ((lm >> wl) & 1u) {
-        const int jw = jb + t - wl;
-        if (newlo < 0) newlo = jw;
-        newhi = jw;
-      }
+    };
+
+    for (;;) {
+      step(0);
+      step(1);
+      step(2);
+      step(3);
       if (finmask == kFull) break;
-      ++j;
-      ++d;
+      j += 4;
+      jr += 4;
+      qp += 4;
+      rp += 4;
     }
-    // The writer lane stopped at column jb + t - wl; anything it wrote in an
-    // earlier strip beyond that is stale and must read as +inf.
-    const int wend = jb + t - wl;
-    for (int k = max(wend + 1, 0) + lane; k <= min(written, lc + 1); k += 32) rowbuf[k] = INF;
-    written = max(wend, 0);
+    // All lanes advanced T = j - (jb - lane) + 4 steps; the writer's last
+    // column is jb - wl + T - 1.  Anything it wrote in an earlier strip beyond
+    // that is stale and must read as +inf.
+    const int wend = jb - wl + (j - (jb - lane)) + 3;
+    for (int k = max(wend + 1, 0) + lane; k <= written; k += 32) rowbuf[k] = INF;
+    written = min(max(wend, 0), lc + 1);
+    // Cells this lane evaluated inside its band before finishing.
+    const int c0 = max(jb, bl), c1 = min(jf, bh);
+    cnt += active && c1 >= c0 ? static_cast<unsigned>(c1 - c0 + 1) : 0u;
     __syncwarp();
-    if (newhi < 0) {  // the last row of the strip has no live cell: borders collided
+    // Live range of the new last row, read back from rowbuf (columns [jb, wend]).
+    const int wcol1 = min(wend, lc);
+    const int ubl_hi = __double2hiint(ub_last);
+    int nlo = INT_MAX, nhi = -1;
+    for (int k0 = jb; k0 <= wcol1; k0 += 32) {
+      const int k = k0 + lane;
+      bool lv = false;
+      if (k <= wcol1) {
+        const double rv = rowbuf[k];
+        lv = KILL ? rv <= ub_last : __double2hiint(rv) <= ubl_hi;
+      }
+      const unsigned bm = __ballot_sync(kFull, lv);
+      if (bm) {
+        if (nlo == INT_MAX) nlo = k0 + __ffs(bm) - 1;
+        nhi = k0 + 31 - __clz(bm);
+      }
+    }
+    if (nhi < 0) {  // the last row of the strip has no live cell: borders collided
       lo = -1;
       break;
     }
-    lo = newlo;
-    hi = newhi;
+    lo = nlo;
+    hi = nhi;
   }
   for (int off = 16; off > 0; off >>= 1) cnt += __shfl_xor_sync(kFull, cnt, off);
   if (lane == 0) cells += cnt;

@@ -33,53 +33,103 @@ namespace eapdtw_b200 {
 // ---------------------------------------------------------------------------
 constexpr int kStatsTile = 512;
 
-__global__ void __launch_bounds__(32) stats_chain_kernel(const double* __restrict__ ref, long long n,
+// Block of 64 threads per 100000-slide segment, double-buffered tiles:
+//   warp 0 / lane 0 : the dependent chain over tile k (reads IN/OUT, writes SUM/SQ)
+//   warp 1          : stages IN/OUT of tile k+1 and converts tile k-1 to mean/sd
+// One __syncthreads per tile; the chain thread never waits on global memory.
+__global__ void __launch_bounds__(64) stats_chain_kernel(const double* __restrict__ ref, long long n,
                                                          int m, double* __restrict__ mean_out,
                                                          double* __restrict__ sd_out) {
-  __shared__ double s_in[kStatsTile];
-  __shared__ double s_out[kStatsTile];
-  __shared__ double s_sum[kStatsTile];
-  __shared__ double s_sq[kStatsTile];
-  const int lane = threadIdx.x;
+  __shared__ double s_in[2][kStatsTile];
+  __shared__ double s_out[2][kStatsTile];
+  __shared__ double s_sum[2][kStatsTile];
+  __shared__ double s_sq[2][kStatsTile];
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
   const long long ncand = n - m + 1;
   const long long s0 = static_cast<long long>(blockIdx.x) * kStatsResetInterval;
   const long long s1 = min(ncand, s0 + kStatsResetInterval);
+  const int ntiles = static_cast<int>((s1 - s0 + kStatsTile - 1) / kStatsTile);
   const double dm = static_cast<double>(m);
   double sum = 0.0, sq = 0.0;
-  if (lane == 0) {  // RunningStats::over(ref[s0 : s0+m]) (search.cpp:25-33)
+
+  auto stage = [&](int tile) {  // warp 1: IN/OUT of `tile` into buffer tile&1
+    const long long t0 = s0 + static_cast<long long>(tile) * kStatsTile;
+    const int cnt = static_cast<int>(min(static_cast<long long>(kStatsTile), s1 - t0));
+    double* in = s_in[tile & 1];
+    double* out = s_out[tile & 1];
+    for (int k = lane; k < cnt; k += 32) {
+      const long long s = t0 + k;
+      in[k] = s > s0 ? ref[s + m - 1] : 0.0;
+      out[k] = s > s0 ? ref[s - 1] : 0.0;
+    }
+  };
+  auto convert = [&](int tile) {  // warp 1: (sum, sumsq) -> mean, stddev (search.hpp:34-41)
+    const long long t0 = s0 + static_cast<long long>(tile) * kStatsTile;
+    const int cnt = static_cast<int>(min(static_cast<long long>(kStatsTile), s1 - t0));
+    const double* sm = s_sum[tile & 1];
+    const double* sqq = s_sq[tile & 1];
+    for (int k = lane; k < cnt; k += 32) {
+      const double mu = __ddiv_rn(sm[k], dm);
+      const double var = __dsub_rn(__ddiv_rn(sqq[k], dm), __dmul_rn(mu, mu));
+      mean_out[t0 + k] = mu;
+      sd_out[t0 + k] = __dsqrt_rn(var > 0.0 ? var : 0.0);
+    }
+  };
+
+  if (tid == 0) {  // RunningStats::over(ref[s0 : s0+m]) (search.cpp:25-33)
     for (int k = 0; k < m; ++k) {
       const double x = ref[s0 + k];
       sum = __dadd_rn(sum, x);
       sq = __dadd_rn(sq, __dmul_rn(x, x));
     }
   }
-  for (long long t0 = s0; t0 < s1; t0 += kStatsTile) {
-    const int cnt = static_cast<int>(min(static_cast<long long>(kStatsTile), s1 - t0));
-    for (int k = lane; k < cnt; k += 32) {
-      const long long s = t0 + k;
-      s_in[k] = s > s0 ? ref[s + m - 1] : 0.0;
-      s_out[k] = s > s0 ? ref[s - 1] : 0.0;
-    }
-    __syncwarp();
-    if (lane == 0) {
-      for (int k = 0; k < cnt; ++k) {
-        if (t0 + k > s0) {  // stats.add(in); stats.remove(out) (search.hpp:23-32)
-          const double in = s_in[k], out = s_out[k];
-          sum = __dsub_rn(__dadd_rn(sum, in), out);
-          sq = __dsub_rn(__dadd_rn(sq, __dmul_rn(in, in)), __dmul_rn(out, out));
+  if (tid >= 32) stage(0);
+  __syncthreads();
+  for (int tile = 0; tile <= ntiles; ++tile) {
+    if (tid == 0 && tile < ntiles) {
+      const long long t0 = s0 + static_cast<long long>(tile) * kStatsTile;
+      const int cnt = static_cast<int>(min(static_cast<long long>(kStatsTile), s1 - t0));
+      const double* in = s_in[tile & 1];
+      const double* out = s_out[tile & 1];
+      double* sm = s_sum[tile & 1];
+      double* sqq = s_sq[tile & 1];
+      int k = 0;
+      if (t0 == s0) {  // the segment's first position is the batch over() result
+        sm[0] = sum;
+        sqq[0] = sq;
+        k = 1;
+      }
+      // stats.add(in); stats.remove(out) (search.hpp:23-32), 8 steps per batch
+      // of hoisted shared-memory loads so only the two DADD chains are exposed.
+      for (; k + 8 <= cnt; k += 8) {
+        double a[8], b[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          a[u] = in[k + u];
+          b[u] = out[k + u];
         }
-        s_sum[k] = sum;
-        s_sq[k] = sq;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          sum = __dsub_rn(__dadd_rn(sum, a[u]), b[u]);
+          sq = __dsub_rn(__dadd_rn(sq, __dmul_rn(a[u], a[u])), __dmul_rn(b[u], b[u]));
+          sm[k + u] = sum;
+          sqq[k + u] = sq;
+        }
+      }
+      for (; k < cnt; ++k) {
+        const double a = in[k], b = out[k];
+        sum = __dsub_rn(__dadd_rn(sum, a), b);
+        sq = __dsub_rn(__dadd_rn(sq, __dmul_rn(a, a)), __dmul_rn(b, b));
+        sm[k] = sum;
+        sqq[k] = sq;
       }
     }
-    __syncwarp();
-    for (int k = lane; k < cnt; k += 32) {
-      const double mu = __ddiv_rn(s_sum[k], dm);
-      const double var = __dsub_rn(__ddiv_rn(s_sq[k], dm), __dmul_rn(mu, mu));
-      mean_out[t0 + k] = mu;
-      sd_out[t0 + k] = __dsqrt_rn(var > 0.0 ? var : 0.0);
+    if (tid >= 32) {
+      if (tile + 1 < ntiles) stage(tile + 1);
+      if (tile >= 1) convert(tile - 1);
     }
-    __syncwarp();
+    __syncthreads();
   }
 }
 
@@ -87,7 +137,7 @@ cudaError_t launch_stats(const double* ref, long long n, int m, double* mean, do
                          cudaStream_t stream) {
   const long long ncand = n - m + 1;
   const long long nseg = (ncand + kStatsResetInterval - 1) / kStatsResetInterval;
-  stats_chain_kernel<<<static_cast<unsigned>(nseg), 32, 0, stream>>>(ref, n, m, mean, sd);
+  stats_chain_kernel<<<static_cast<unsigned>(nseg), 64, 0, stream>>>(ref, n, m, mean, sd);
   return cudaGetLastError();
 }
 
@@ -253,6 +303,7 @@ __global__ void __launch_bounds__(256) search_kernel(SearchParams p) {
     const int j = k - kPadL;
     smem[k] = (j >= 1 && j <= m) ? p.q[j] : INF;
   }
+  for (int k = lane; k < static_cast<int>(plen); k += 32) rowbuf[k - kPadL] = INF;
   if (p.use_lb) {
     for (int k = threadIdx.x; k < m; k += blockDim.x) {
       qu[k] = p.qu[k];
@@ -273,12 +324,14 @@ __global__ void __launch_bounds__(256) search_kernel(SearchParams p) {
     const double cs = p.sd[cand];
     const bool cconst = cs < kMinStddev;
     const double* crow = ref + cand;
-    auto rowval = [&](int r) -> double {
-      return cconst ? 0.0 : __ddiv_rn(__dsub_rn(crow[r], cm), cs);
+    auto rowraw = [&](int r) -> double { return crow[r]; };
+    auto rownorm = [&](double x) -> double {
+      return cconst ? 0.0 : __ddiv_rn(__dsub_rn(x, cm), cs);
     };
     auto get_ub = [&]() -> double { return prune ? load_ub(p.ub_key) : INF; };
     auto rowthr = [](double u, int) -> double { return u; };
-    const double d = warp_dtw<false>(rowval, m, qsp, m, p.w, get_ub, rowthr, rowbuf, c_cells);
+    const double d =
+        warp_dtw<false>(rowraw, rownorm, m, qsp, m, p.w, get_ub, rowthr, rowbuf, c_cells);
     ++c_calls;
     if (d == INF) {
       ++c_aband;
@@ -489,7 +542,10 @@ __global__ void __launch_bounds__(256) pairwise_kernel(PairParams p) {
   double* rowbuf = colsp + plen;
   const double INF = d_inf();
   unsigned long long cells = 0;
-  for (int k = lane; k < static_cast<int>(plen); k += 32) colsp[k - kPadL] = INF;
+  for (int k = lane; k < static_cast<int>(plen); k += 32) {
+    colsp[k - kPadL] = INF;
+    rowbuf[k - kPadL] = INF;
+  }
   __syncwarp();
   for (long long pr = static_cast<long long>(blockIdx.x) * wpb + warp; pr < p.npairs;
        pr += static_cast<long long>(gridDim.x) * wpb) {
@@ -498,7 +554,8 @@ __global__ void __launch_bounds__(256) pairwise_kernel(PairParams p) {
     for (int k = lane; k < lc; k += 32) colsp[k + 1] = cg[k];
     __syncwarp();
     const double ub0 = p.ub ? p.ub[pr] : INF;
-    auto rowval = [&](int r) -> double { return rows[r]; };
+    auto rowraw = [&](int r) -> double { return rows[r]; };
+    auto rownorm = [](double x) -> double { return x; };
     auto get_ub = [&]() -> double { return p.prune ? ub0 : INF; };
     const double* cb = WITH_CB ? p.cb + pr * p.lr : nullptr;
     const int lr = p.lr, w = p.w;
@@ -509,7 +566,8 @@ __global__ void __launch_bounds__(256) pairwise_kernel(PairParams p) {
       const double t = __dsub_rn(u, cb[k - 1]);
       return t > 0.0 ? t : 0.0;
     };
-    const double d = warp_dtw<WITH_CB>(rowval, lr, colsp, lc, w, get_ub, rowthr, rowbuf, cells);
+    const double d =
+        warp_dtw<WITH_CB>(rowraw, rownorm, lr, colsp, lc, w, get_ub, rowthr, rowbuf, cells);
     if (lane == 0) p.out[pr] = d;
     __syncwarp();
   }
@@ -560,6 +618,7 @@ __global__ void __launch_bounds__(256) nn1_kernel(Nn1Params p) {
     const int j = k - kPadL;
     smem[k] = (j >= 1 && j <= L) ? p.queries[qi * L + j - 1] : INF;
   }
+  for (int k = lane; k < static_cast<int>(plen); k += 32) rowbuf[k - kPadL] = INF;
   if (threadIdx.x == 0) s_next = 0;
   __syncthreads();
   unsigned long long* key = p.ub_keys + qi;
@@ -576,10 +635,11 @@ __global__ void __launch_bounds__(256) nn1_kernel(Nn1Params p) {
       const double kim = __dadd_rn(sq_cost(qsp[1], row[0]), sq_cost(qsp[L], row[L - 1]));
       if (kim > ub) continue;
     }
-    auto rowval = [&](int r) -> double { return row[r]; };
+    auto rowraw = [&](int r) -> double { return row[r]; };
+    auto rownorm = [](double x) -> double { return x; };
     auto get_ub = [&]() -> double { return load_ub(key); };
     auto rowthr = [](double u, int) -> double { return u; };
-    const double d = warp_dtw<false>(rowval, L, qsp, L, p.w, get_ub, rowthr, rowbuf, cells);
+    const double d = warp_dtw<false>(rowraw, rownorm, L, qsp, L, p.w, get_ub, rowthr, rowbuf, cells);
     ++calls;
     if (d != INF && lane == 0) {
       atomicMin(key, static_cast<unsigned long long>(__double_as_longlong(d)));
