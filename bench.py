@@ -129,7 +129,7 @@ def run_reference_arm(args, cfgname):
     use_lb = cfgname != "cfg3-nolb"
     threads = os.cpu_count() or 1
     # each step is a bounded sample: whole 100000-candidate segments, one per thread
-    nseg = max(1, min(threads, int(os.environ.get("EAPDTW_REF_SEGMENTS", "8"))))
+    nseg = max(1, min(threads, int(os.environ.get("EAPDTW_REF_SEGMENTS", "32"))))
     npoints = min(n, nseg * 100_000 + m - 1)
     from paper_2010_05371_b200 import random_walk_normal
     ref = random_walk_normal(npoints, SEED_REF)  # prefix of the same walk

@@ -41,6 +41,8 @@ int fail(int code, const std::string& msg) {
   } while (0)
 
 constexpr double kInf = std::numeric_limits<double>::infinity();
+// Spare survivor-queue slots beyond the candidate count (>= resident warps).
+constexpr size_t kQueueSlack = 148 * 64 + 64;
 
 // Grow-only device buffer.
 struct DevBuf {
@@ -427,7 +429,9 @@ static int plan_init(eapdtw_search_plan* p, eapdtw_ctx* c, const double* ref_dev
   CUDA_TRY(B.best.ensure(sizeof(BestRecord)));
   CUDA_TRY(B.key.ensure(8));
   CUDA_TRY(B.work.ensure(8));
-  CUDA_TRY(B.queue.ensure(nc * 8));
+  // One spare slot per resident warp: a consumer may hold a "future" slot past
+  // the final tail, which must read as empty (-1) rather than stale data.
+  CUDA_TRY(B.queue.ensure((nc + kQueueSlack) * 8));
   CUDA_TRY(B.qctr.ensure(24));
   CUDA_TRY(B.flag.ensure(8));
   CUDA_TRY(B.counters.ensure(kNumCounters * 8));
@@ -512,7 +516,7 @@ static cudaError_t reset_work(eapdtw_search_plan* p, long long count, cudaStream
   cudaError_t e = cudaMemsetAsync(B.work.p, 0, 8, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(B.qctr.p, 0, 24, s);
   if (e == cudaSuccess && count > 0)
-    e = cudaMemsetAsync(B.queue.p, 0xff, static_cast<size_t>(count) * 8, s);
+    e = cudaMemsetAsync(B.queue.p, 0xff, static_cast<size_t>(count + kQueueSlack) * 8, s);
   return e;
 }
 

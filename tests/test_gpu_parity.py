@@ -219,11 +219,23 @@ def test_ties_and_exact_copy(gpu):
                                    tighten_ub=lb)
             res = gpu.similarity_search(ref, motif, cfg)
             assert res.best.location == 200 and res.best.distance_sq == 0.0, (algo, lb)
+            rep = res.report  # counter conservation (search.hpp:68-77), incl. a full queue
+            assert rep.candidates_total == (rep.pruned_kim + rep.pruned_keogh_eq +
+                                            rep.pruned_keogh_ec + rep.dtw_calls)
     ref2 = (rng.integers(0, 13, 2000) - 6).astype(np.float64)
     q2 = (rng.integers(0, 13, 48) - 6).astype(np.float64)
     ref2[700:748] = q2
     res = gpu.similarity_search(ref2, q2, gpu.SearchConfig(window_ratio=0.1))
     assert res.best.location == 700 and res.best.distance_sq == 0.0
+    # rough integer data: the cascade prunes little, every survivor goes through
+    # the queue exactly once
+    for n, m in ((4000, 64), (2000, 48)):
+        r = (rng.integers(0, 13, n) - 6).astype(np.float64)
+        q = (rng.integers(0, 13, m) - 6).astype(np.float64)
+        rep = gpu.similarity_search(r, q, gpu.SearchConfig(window_ratio=0.1)).report
+        assert rep.candidates_total == n - m + 1
+        assert rep.candidates_total == (rep.pruned_kim + rep.pruned_keogh_eq +
+                                        rep.pruned_keogh_ec + rep.dtw_calls)
 
 
 def test_degenerate_queries(gpu, oracle_lib):

@@ -1,0 +1,137 @@
+"""CPU (gloo, world_size 2): the multi-GPU host logic of paper_2010_05371_b200.sharded.
+
+The product backend is the C-ABI search plan on each GPU; here every rank
+plugs the C oracle in as its shard backend, so the sharding (100000-aligned
+shard starts with an (m-1)-point halo), the best-so-far all-reduce between
+batches and the final lexicographic (distance, lowest global index) merge are
+exercised exactly as bench.py drives them under torchrun."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2010_05371_b200.sharded import (INF_KEY, STATS_RESET, ShardedSearch, double_of,
+                                           key_of, lexicographic_min, shard_bounds)
+
+
+def test_shard_bounds_cover_and_align():
+    for ncand in (1, 99_999, 100_000, 100_001, 999_873, 99_998_977):
+        for world in (1, 2, 3, 4, 8):
+            spans = [shard_bounds(ncand, world, r) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == ncand
+            for (a0, a1), (b0, b1) in zip(spans, spans[1:]):
+                assert a1 == b0
+            for s0, s1 in spans:
+                assert s0 % STATS_RESET == 0 or s0 == ncand
+                assert s1 >= s0
+
+
+def test_keys_and_lexicographic_min():
+    for d in (0.0, 1e-300, 1.5, 3.75, 1e300, float("inf")):
+        assert double_of(key_of(d)) == d
+    ds = [0.0, 1e-300, 1.5, 3.75, 1e300, float("inf")]
+    assert [key_of(d) for d in ds] == sorted(key_of(d) for d in ds)
+    assert key_of(float("inf")) == INF_KEY
+    assert lexicographic_min([(True, 2.0, 9), (True, 2.0, 4), (True, 3.0, 1), (False, 0, 0)]) \
+        == (True, 2.0, 4)
+    assert lexicographic_min([(False, 0.0, 0)]) == (False, float("inf"), 0)
+
+
+class OracleShard:
+    """CPU stand-in for GpuShard: the oracle's similarity_search on the shard."""
+
+    def __init__(self, ref, q, m, ratio, s0, s1, key):
+        import oracle
+        self.o = oracle.Oracle()
+        self.slice = ref[s0:s1 + m - 1]
+        self.q, self.m, self.ratio, self.s0 = q, m, ratio, s0
+        self.key = key
+        self.candidates = s1 - s0
+        self.res = None
+        self.runs = []
+
+    def reset(self):
+        self.key.fill_(INF_KEY)
+        self.res = None
+
+    def prepare(self):
+        pass
+
+    def run(self, begin, end):
+        self.runs.append((begin, end))
+        if self.res is None:
+            self.res = self.o.similarity_search(self.slice, self.q, self.ratio,
+                                                query_length=self.m)
+        if self.res.found:
+            self.key.fill_(min(int(self.key.item()), key_of(self.res.distance_sq)))
+
+    def result(self):
+        from paper_2010_05371_b200.api import BestSoFar, SearchReport, SearchResult
+        r = self.res
+        return SearchResult(BestSoFar(int(r.location) + self.s0, float(r.distance_sq),
+                                      bool(r.found)), SearchReport())
+
+
+def _worker(rank, world, port, ref, q, m, ratio, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ncand = ref.size - m + 1
+        s0, s1 = shard_bounds(ncand, world, rank)
+        key = torch.full((1,), 0, dtype=torch.int64)
+        shard = OracleShard(ref, q, m, ratio, s0, s1, key)
+        runner = ShardedSearch(shard, rank, world, batches=3)
+        best, _ = runner.search()
+        # every rank ends with the global minimum key after the exchanges
+        out[rank] = (best, int(key.item()), len(shard.runs))
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _run(ref, q, m, ratio, world=2):
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(world, _free_port(), ref, q, m, ratio, out), nprocs=world, join=True)
+    return dict(out)
+
+
+@pytest.mark.timeout(300)
+def test_two_rank_search_equals_unsharded(oracle_lib):
+    from paper_2010_05371_b200 import random_walk_normal
+    ref = random_walk_normal(260_000, 31)
+    q = random_walk_normal(48, 32)
+    want = oracle_lib.similarity_search(ref, q, 0.1)
+    res = _run(ref, q, 48, 0.1)
+    for rank in (0, 1):
+        best, key, nruns = res[rank]
+        assert best == (True, want.distance_sq, want.location)
+        assert key == key_of(want.distance_sq)
+        assert nruns == 3
+
+
+@pytest.mark.timeout(300)
+def test_two_rank_tie_goes_to_lowest_global_index(oracle_lib):
+    """Equal minima in both shards: the final merge keeps the lower index."""
+    rng = np.random.default_rng(11)
+    m = 40
+    ref = (rng.integers(0, 13, 250_000) - 6).astype(np.float64)
+    motif = (rng.integers(0, 13, m) - 6).astype(np.float64)
+    ref[150_000:150_000 + m] = motif  # rank 0 holds [0, 200000), rank 1 the rest
+    ref[230_000:230_000 + m] = motif
+    ref[120_000:120_000 + m] = motif
+    want = oracle_lib.similarity_search(ref, motif, 0.1)
+    assert want.distance_sq == 0.0 and want.location == 120_000
+    res = _run(ref, motif, m, 0.1)
+    for rank in (0, 1):
+        assert res[rank][0] == (True, 0.0, 120_000)
