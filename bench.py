@@ -331,6 +331,7 @@ def main():
             "full_band_equiv_gcups": ncand * band_cells(m, w) / (ms_max * 1e-3) / 1e9,
             "phase_ms": phase_ms,
             "counted_cells_per_search": cells_mean,
+            "sweep_counters": shard.plan.counters(),
             "result": {"location": best[2], "distance_sq": best[1]},
             "data_gen_s": t_gen,
         }

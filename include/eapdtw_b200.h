@@ -126,6 +126,9 @@ uint64_t* eapdtw_search_plan_ub_key(eapdtw_search_plan* plan);
 int eapdtw_search_plan_result(eapdtw_search_plan* plan, eapdtw_search_result* out);
 /* Device time in ms of the last prepare/run, per phase: [stats, envelope, probe, sweep]. */
 int eapdtw_search_plan_timings(eapdtw_search_plan* plan, float* ms4);
+/* Raw device counters of the last sweep (9 entries): [kim, keogh_eq, keogh_ec,
+ * dtw_calls, dtw_abandoned, cells, candidates, engine_overflows, screened]. */
+int eapdtw_search_plan_counters(eapdtw_search_plan* plan, uint64_t* out9);
 int eapdtw_search_plan_destroy(eapdtw_search_plan* plan);
 
 /* --- batched NN1 (cfg5): per query, argmin over the database ------------- *

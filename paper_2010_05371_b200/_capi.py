@@ -91,6 +91,7 @@ SIGNATURES = [
     ("eapdtw_search_plan_ub_key", _vp, [_vp]),
     ("eapdtw_search_plan_result", C.c_int, [_vp, C.POINTER(SearchResultC)]),
     ("eapdtw_search_plan_timings", C.c_int, [_vp, C.POINTER(C.c_float)]),
+    ("eapdtw_search_plan_counters", C.c_int, [_vp, _u64p]),
     ("eapdtw_search_plan_destroy", C.c_int, [_vp]),
     ("eapdtw_nn1", C.c_int,
      [_vp, _dp, C.c_size_t, _dp, C.c_size_t, C.c_size_t, C.c_size_t, _u64p, _dp, _u64p]),

@@ -369,6 +369,13 @@ class SearchPlan:
         check(lib.eapdtw_search_plan_result(self.handle, C.byref(res)))
         return SearchResult.from_c(res)
 
+    def counters(self):
+        out = (C.c_uint64 * 9)()
+        check(lib.eapdtw_search_plan_counters(self.handle, out))
+        keys = ["kim", "keogh_eq", "keogh_ec", "dtw_calls", "dtw_abandoned", "cells",
+                "candidates", "engine_overflows", "screened"]
+        return dict(zip(keys, (int(x) for x in out)))
+
     def timings(self):
         ms = (C.c_float * 4)()
         check(lib.eapdtw_search_plan_timings(self.handle, ms))

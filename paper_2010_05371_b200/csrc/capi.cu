@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <numeric>
@@ -142,7 +143,7 @@ struct eapdtw_search_plan {
   size_t ncand = 0;
   cudaEvent_t ev[8] = {};
   bool prepared = false, ran = false;
-  int blocks = 0, warps = 8;
+  int blocks = 0, warps = 8, ad_k = 0, screen_rows = 16;
   double guard_rel = 1e-9, guard_abs = 1e-20;
   std::chrono::steady_clock::time_point t0;
 };
@@ -229,6 +230,7 @@ static int pairwise_impl(eapdtw_ctx* c, const double* rows_dev, const double* co
   p.ub = ub_dev;
   p.cb = cb_dev;
   p.prune = prune;
+  p.ad_k = choose_ad_k(static_cast<int>(lr), w);
   p.out = out_dev;
   p.cells = c->cells.as<unsigned long long>();
   p.npairs = static_cast<long long>(npairs);
@@ -393,6 +395,11 @@ static int plan_init(eapdtw_search_plan* p, eapdtw_ctx* c, const double* ref_dev
   p->w_eff = p->w_cells >= m ? static_cast<int>(m) : static_cast<int>(p->w_cells);
   p->env_r = static_cast<int>(std::min(p->w_cells, m));  // compute_envelope clamp (lower_bounds.cpp:12)
   p->guard_rel = std::max(1e-9, 8.0 * static_cast<double>(m) * 0x1.0p-53);
+  // Search DTW calls are mostly short (killed within a few strips), where the
+  // strip engine's lower per-call setup wins; the anti-diagonal engine is
+  // opt-in here (EAPDTW_AD_K) and the default for pairwise / NN1 batches.
+  p->ad_k = getenv("EAPDTW_AD_K") ? choose_ad_k(static_cast<int>(m), p->w_eff) : 0;
+  if (const char* env = getenv("EAPDTW_SCREEN_ROWS")) p->screen_rows = std::max(0, atoi(env));
   p->guard_abs = 1e-20;
 
   // Query preparation exactly as search.cpp:136-149.
@@ -456,9 +463,9 @@ static int plan_init(eapdtw_search_plan* p, eapdtw_ctx* c, const double* ref_dev
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, c->device);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device);
   p->warps = 8;
-  while (p->warps > 1 && search_smem_bytes(static_cast<int>(m), p->warps) > static_cast<size_t>(optin))
+  while (p->warps > 1 && search_smem_bytes(static_cast<int>(m), p->warps, p->ad_k) > static_cast<size_t>(optin))
     p->warps /= 2;
-  const size_t smem = search_smem_bytes(static_cast<int>(m), p->warps);
+  const size_t smem = search_smem_bytes(static_cast<int>(m), p->warps, p->ad_k);
   if (smem > static_cast<size_t>(optin))
     return fail(EAPDTW_EINVAL, "search: query length exceeds the shared-memory budget");
   const int per_sm = std::max(1, std::min(static_cast<int>(max_smem / (smem + 1024)), 64 / p->warps));
@@ -547,6 +554,9 @@ static SearchParams base_params(eapdtw_search_plan* p) {
   s.qtail = B.qctr.as<unsigned long long>() + 1;
   s.chunks_done = B.qctr.as<unsigned long long>() + 2;
   s.direct_chunk = 4;
+  s.ad_k = p->ad_k;
+  s.direct = 0;
+  s.screen_rows = p->screen_rows;
   s.counters = B.counters.as<unsigned long long>();
   s.index_offset = static_cast<long long>(p->offset);
   return s;
@@ -589,6 +599,7 @@ int eapdtw_search_plan_prepare(eapdtw_search_plan* p) {
                                sp.stride * static_cast<long long>(nprobe));
   sp.counters = B.probe_counters.as<unsigned long long>();
   sp.direct_chunk = 1;
+  sp.direct = 1;
   CUDA_TRY(reset_work(p, static_cast<long long>(nprobe), s));
   CUDA_TRY(launch_search(sp, p->blocks, p->warps, s));
   ++c->launches;
@@ -645,6 +656,17 @@ int eapdtw_search_plan_result(eapdtw_search_plan* p, eapdtw_search_result* out) 
   out->dp_cells_evaluated = cnt[kCntCells] + pc[kCntCells];
   out->elapsed_seconds =
       std::chrono::duration<double>(std::chrono::steady_clock::now() - p->t0).count();
+  return EAPDTW_OK;
+}
+
+int eapdtw_search_plan_counters(eapdtw_search_plan* p, uint64_t* out8) {  // 9 entries
+  if (!p || !out8) return fail(EAPDTW_EINVAL, "null argument");
+  CUDA_TRY(cudaSetDevice(p->ctx->device));
+  unsigned long long cnt[kNumCounters];
+  CUDA_TRY(cudaMemcpyAsync(cnt, p->buf->counters.p, sizeof(cnt), cudaMemcpyDeviceToHost,
+                           p->ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(p->ctx->stream));
+  for (int k = 0; k < 9; ++k) out8[k] = k < kNumCounters ? cnt[k] : 0;
   return EAPDTW_OK;
 }
 
@@ -745,6 +767,7 @@ static int nn1_impl(eapdtw_ctx* c, const double* q_dev, size_t nq, const double*
   const long long target = 148LL * 8;
   p.splits = static_cast<int>(std::max<long long>(1, std::min<long long>(
       static_cast<long long>(nd) / 64 + 1, (target + static_cast<long long>(nq) - 1) / static_cast<long long>(nq))));
+  p.ad_k = choose_ad_k(static_cast<int>(len), w);
   p.ub_keys = c->keys.as<unsigned long long>();
   p.best = c->best.as<BestRecord>();
   p.cells = c->counters.as<unsigned long long>();

@@ -12,7 +12,10 @@
 #include <cfloat>
 #include <climits>
 #include <algorithm>
+#include <cstdlib>
 
+#include "dtw_ad.cuh"
+#include "screen.cuh"
 #include "kernels.cuh"
 
 namespace eapdtw_b200 {
@@ -269,14 +272,59 @@ cudaError_t launch_envelope(const double* ref, long long n, int r, double* up, d
 // keeps the lowest index among equal distances, so the result is the
 // reference's (first strict minimum, search.cpp:199).
 // ---------------------------------------------------------------------------
-static __host__ __device__ inline size_t padded_len(int m) { return static_cast<size_t>(m) + 2 + kPadL + kPadR; }
+// Shared-memory padding of the query / per-warp buffers: enough for the strip
+// engine (kPadL/kPadR) and for the anti-diagonal engine with K = ad_k.
+static __host__ __device__ inline int smem_pad(int ad_k) {
+  const int p = ad_k > 0 ? ad_pad(ad_k) : 0;
+  return p > kPadR ? p : kPadR;
+}
+static __host__ __device__ inline size_t padded_len(int m, int ad_k) {
+  return static_cast<size_t>(m) + 2 + 2 * static_cast<size_t>(smem_pad(ad_k));
+}
 
-size_t search_smem_bytes(int m, int warps) {
-  return padded_len(m) * 8                        // q (padded, 1-based)
-         + static_cast<size_t>(m) * 8 * 2         // qu, ql
-         + static_cast<size_t>(m) * 4 + 8         // order
-         + static_cast<size_t>(warps) * padded_len(m) * 8  // row buffers
+size_t search_smem_bytes(int m, int warps, int ad_k) {
+  return padded_len(m, ad_k) * 8                        // q (padded, 1-based)
+         + static_cast<size_t>(m) * 8 * 2               // qu, ql
+         + static_cast<size_t>(m) * 4 + 8               // order
+         + static_cast<size_t>(warps) * padded_len(m, ad_k) * 8  // per-warp DP buffers
          + 64;
+}
+
+int choose_ad_k(int n, int w) {
+  if (const char* env = getenv("EAPDTW_AD_K")) {  // experiment override: 0 (strip), 1, 3, 5
+    const int v = atoi(env);
+    if (v == 0 || v == 1 || v == 3 || v == 5) return v;
+  }
+  // The anti-diagonal engine wins (1.25-1.45x per cell, scratch/engine
+  // measurements in DESIGN.md) only when its window holds the whole band, so
+  // it can never overflow; wider bands use the strip engine.
+  const long long band = std::min(2LL * w + 1, 2LL * n - 1);
+  if (band <= 64) return 1;
+  if (band <= 192) return 3;
+  return 0;
+}
+
+// One exact pruned DTW with the whole warp: the anti-diagonal engine with
+// window 64*ad_k first, the strip engine when the live region overflows it
+// (or ad_k == 0).  Both share `buf` (their DP scratch).
+template <bool KILL, class RawFn, class NormFn, class UbFn, class RowThrFn>
+__device__ double dtw_dispatch(int ad_k, const RawFn& rowraw, const NormFn& rownorm, int lr,
+                               const double* qsp, int lc, int w, UbFn&& get_ub, RowThrFn&& rowthr,
+                               double* buf, unsigned long long& cells,
+                               unsigned long long& overflows) {
+  if (!KILL && ad_k > 0) {
+    double r = d_inf();
+    int st = kAdOverflow;
+    // odd K: lanes read shared memory at an odd 8-byte stride, i.e. without
+    // bank conflicts (2 wavefronts per 64-bit access, the minimum)
+    if (ad_k == 1) st = warp_dtw_ad<1>(rowraw, rownorm, lr, qsp, lc, w, get_ub, buf, r, cells);
+    else if (ad_k == 3) st = warp_dtw_ad<3>(rowraw, rownorm, lr, qsp, lc, w, get_ub, buf, r, cells);
+    else st = warp_dtw_ad<5>(rowraw, rownorm, lr, qsp, lc, w, get_ub, buf, r, cells);
+    if (st == kAdOk) return r;
+    ++overflows;
+    __syncwarp();
+  }
+  return warp_dtw<KILL>(rowraw, rownorm, lr, qsp, lc, w, get_ub, rowthr, buf, cells);
 }
 
 __device__ __forceinline__ long long vload(const long long* p) {
@@ -289,21 +337,22 @@ __device__ __forceinline__ unsigned long long vload(const unsigned long long* p)
 __global__ void __launch_bounds__(256) search_kernel(SearchParams p) {
   extern __shared__ double smem[];
   const int m = p.m;
-  const size_t plen = padded_len(m);
-  double* qsp = smem + kPadL;                      // qsp[-kPadL .. m+1+kPadR)
+  const int pad = smem_pad(p.ad_k);
+  const size_t plen = padded_len(m, p.ad_k);
+  double* qsp = smem + pad;                        // qsp[-pad .. m+1+pad]
   double* qu = smem + plen;                        // [m]
   double* ql = qu + m;                             // [m]
   int* order = reinterpret_cast<int*>(ql + m);     // [m]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* rowbuf = reinterpret_cast<double*>(order + m + 2 - (m & 1)) +
-                   static_cast<size_t>(warp) * plen + kPadL;
+                   static_cast<size_t>(warp) * plen + pad;
 
   const double INF = d_inf();
   for (int k = threadIdx.x; k < static_cast<int>(plen); k += blockDim.x) {
-    const int j = k - kPadL;
+    const int j = k - pad;
     smem[k] = (j >= 1 && j <= m) ? p.q[j] : INF;
   }
-  for (int k = lane; k < static_cast<int>(plen); k += 32) rowbuf[k - kPadL] = INF;
+  for (int k = lane; k < static_cast<int>(plen); k += 32) rowbuf[k - pad] = INF;
   if (p.use_lb) {
     for (int k = threadIdx.x; k < m; k += blockDim.x) {
       qu[k] = p.qu[k];
@@ -314,7 +363,7 @@ __global__ void __launch_bounds__(256) search_kernel(SearchParams p) {
   __syncthreads();
 
   unsigned long long c_kim = 0, c_eq = 0, c_ec = 0, c_calls = 0, c_aband = 0, c_cells = 0,
-                     c_cand = 0;
+                     c_cand = 0, c_ovf = 0, c_scr = 0, c_cells_lane = 0;
   const double* __restrict__ ref = p.ref;
   const bool prune = p.prune != 0;
 
@@ -330,8 +379,8 @@ __global__ void __launch_bounds__(256) search_kernel(SearchParams p) {
     };
     auto get_ub = [&]() -> double { return prune ? load_ub(p.ub_key) : INF; };
     auto rowthr = [](double u, int) -> double { return u; };
-    const double d =
-        warp_dtw<false>(rowraw, rownorm, m, qsp, m, p.w, get_ub, rowthr, rowbuf, c_cells);
+    const double d = dtw_dispatch<false>(p.ad_k, rowraw, rownorm, m, qsp, m, p.w, get_ub, rowthr,
+                                         rowbuf, c_cells, c_ovf);
     ++c_calls;
     if (d == INF) {
       ++c_aband;
@@ -341,9 +390,9 @@ __global__ void __launch_bounds__(256) search_kernel(SearchParams p) {
     }
   };
 
-  if (!p.use_lb) {
-    // ---- direct mode (EAPrunedDTW alone, and the probe): every candidate is
-    //      a DTW task; warps claim `direct_chunk` candidates at a time.
+  if (p.direct) {
+    // ---- direct mode (the probe): every candidate is a DTW task; warps
+    //      claim `direct_chunk` candidates at a time.
     const long long K = p.direct_chunk;
     for (;;) {
       unsigned long long c = 0;
@@ -415,7 +464,7 @@ __global__ void __launch_bounds__(256) search_kernel(SearchParams p) {
       double ub = load_ub(p.ub_key);
       // --- Tier 1: LB_Kim on the two aligned extremities (search.cpp:81-87),
       //     computed with the same IEEE divisions as the DTW rows.
-      if (m >= 2 && alive) {
+      if (p.use_lb && m >= 2 && alive) {
         const double c0 = constant ? 0.0 : __ddiv_rn(__dsub_rn(ref[s], mean), sd);
         const double cl = constant ? 0.0 : __ddiv_rn(__dsub_rn(ref[s + m - 1], mean), sd);
         const double kim = __dadd_rn(sq_cost(qsp[1], c0), sq_cost(qsp[m], cl));
@@ -429,7 +478,7 @@ __global__ void __launch_bounds__(256) search_kernel(SearchParams p) {
       //     (search.cpp:92, lower_bounds.cpp:57-88), visiting order[] with a
       //     chunked early-abandon vote.
       double ubg = ub * (1.0 + p.guard_rel) + p.guard_abs;
-      bool pending = alive;
+      bool pending = alive && p.use_lb;
       if (__any_sync(kFull, pending)) {
         double acc = 0.0;
         for (int k0 = 0; k0 < m; k0 += 8) {
@@ -453,7 +502,7 @@ __global__ void __launch_bounds__(256) search_kernel(SearchParams p) {
       }
       // --- Tier 3: LB_Keogh EC, normalised query vs the candidate envelope
       //     (search.cpp:97-99) read from the global raw envelope.
-      if (p.env_up != nullptr) {
+      if (p.use_lb && p.env_up != nullptr) {
         ub = load_ub(p.ub_key);
         ubg = ub * (1.0 + p.guard_rel) + p.guard_abs;
         pending = alive;
@@ -483,6 +532,23 @@ __global__ void __launch_bounds__(256) search_kernel(SearchParams p) {
           }
         }
       }
+      // --- Phase A: the first screen_rows DTW rows, lane per candidate (an
+      //     exact EAPrunedDTW prefix; a killed candidate is an abandoned DTW).
+      if (p.screen_rows > 0 && __any_sync(kFull, alive)) {
+        const double* xs = ref + s;
+        auto c_of = [&](int r) -> double {
+          return constant ? 0.0 : __ddiv_rn(__dsub_rn(xs[r - 1], mean), sd);
+        };
+        unsigned nrows = 0;
+        const bool killed =
+            screen_prefix<kScreenSlots>(alive, c_of, p.screen_rows, qsp, m, p.w,
+                                        load_ub(p.ub_key), nrows);
+        c_cells_lane += static_cast<unsigned long long>(nrows) * kScreenSlots;
+        if (killed) {
+          alive = false;
+          ++c_scr;
+        }
+      }
       // ---- publish the survivors, then mark the chunk done
       const unsigned mask = __ballot_sync(kFull, alive);
       if (mask) {
@@ -505,7 +571,13 @@ __global__ void __launch_bounds__(256) search_kernel(SearchParams p) {
     c_kim += __shfl_xor_sync(kFull, c_kim, off);
     c_eq += __shfl_xor_sync(kFull, c_eq, off);
     c_ec += __shfl_xor_sync(kFull, c_ec, off);
+    c_scr += __shfl_xor_sync(kFull, c_scr, off);
+    c_cells_lane += __shfl_xor_sync(kFull, c_cells_lane, off);
   }
+  // screened (killed) candidates are DTW evaluations abandoned in phase A
+  c_calls += c_scr;
+  c_aband += c_scr;
+  c_cells += c_cells_lane;
   if (lane == 0) {
     atomicAdd(&p.counters[kCntKim], c_kim);
     atomicAdd(&p.counters[kCntKeoghEq], c_eq);
@@ -514,11 +586,13 @@ __global__ void __launch_bounds__(256) search_kernel(SearchParams p) {
     atomicAdd(&p.counters[kCntDtwAbandoned], c_aband);
     atomicAdd(&p.counters[kCntCells], c_cells);
     atomicAdd(&p.counters[kCntCandidates], c_cand);
+    atomicAdd(&p.counters[kCntOverflows], c_ovf);
+    atomicAdd(&p.counters[kCntScreened], c_scr);
   }
 }
 
 cudaError_t launch_search(const SearchParams& p, int blocks, int warps, cudaStream_t stream) {
-  const size_t smem = search_smem_bytes(p.m, warps);
+  const size_t smem = search_smem_bytes(p.m, warps, p.ad_k);
   cudaError_t e = cudaFuncSetAttribute(search_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
@@ -537,14 +611,15 @@ __global__ void __launch_bounds__(256) pairwise_kernel(PairParams p) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wpb = blockDim.x >> 5;
   const int lc = p.lc;
-  const size_t plen = padded_len(lc);
-  double* colsp = smem + static_cast<size_t>(warp) * 2 * plen + kPadL;  // padded, 1-based
+  const int pad = smem_pad(p.ad_k);
+  const size_t plen = padded_len(max(lc, p.lr), p.ad_k);
+  double* colsp = smem + static_cast<size_t>(warp) * 2 * plen + pad;  // padded, 1-based
   double* rowbuf = colsp + plen;
   const double INF = d_inf();
-  unsigned long long cells = 0;
+  unsigned long long cells = 0, ovf = 0;
   for (int k = lane; k < static_cast<int>(plen); k += 32) {
-    colsp[k - kPadL] = INF;
-    rowbuf[k - kPadL] = INF;
+    colsp[k - pad] = INF;
+    rowbuf[k - pad] = INF;
   }
   __syncwarp();
   for (long long pr = static_cast<long long>(blockIdx.x) * wpb + warp; pr < p.npairs;
@@ -566,8 +641,8 @@ __global__ void __launch_bounds__(256) pairwise_kernel(PairParams p) {
       const double t = __dsub_rn(u, cb[k - 1]);
       return t > 0.0 ? t : 0.0;
     };
-    const double d =
-        warp_dtw<WITH_CB>(rowraw, rownorm, lr, colsp, lc, w, get_ub, rowthr, rowbuf, cells);
+    const double d = dtw_dispatch<WITH_CB>(p.ad_k, rowraw, rownorm, lr, colsp, lc, w, get_ub,
+                                           rowthr, rowbuf, cells, ovf);
     if (lane == 0) p.out[pr] = d;
     __syncwarp();
   }
@@ -576,8 +651,9 @@ __global__ void __launch_bounds__(256) pairwise_kernel(PairParams p) {
 
 cudaError_t launch_pairwise(const PairParams& p, cudaStream_t stream) {
   int warps = 8;
-  while (warps > 1 && static_cast<size_t>(warps) * 2 * padded_len(p.lc) * 8 > 200 * 1024) warps /= 2;
-  const size_t smem = static_cast<size_t>(warps) * 2 * padded_len(p.lc) * sizeof(double);
+  const size_t plen = padded_len(max(p.lc, p.lr), p.ad_k);
+  while (warps > 1 && static_cast<size_t>(warps) * 2 * plen * 8 > 200 * 1024) warps /= 2;
+  const size_t smem = static_cast<size_t>(warps) * 2 * plen * sizeof(double);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   const long long need = (p.npairs + warps - 1) / warps;
   const int blocks = static_cast<int>(min(need, 148LL * 32));
@@ -607,22 +683,23 @@ __global__ void __launch_bounds__(256) nn1_kernel(Nn1Params p) {
   __shared__ unsigned long long s_next;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int L = p.len;
-  const size_t plen = padded_len(L);
+  const int pad = smem_pad(p.ad_k);
+  const size_t plen = padded_len(L, p.ad_k);
   const long long qi = blockIdx.x / p.splits;
   const int part = blockIdx.x % p.splits;
   const long long k0 = p.nd * part / p.splits, k1 = p.nd * (part + 1) / p.splits;
-  double* qsp = smem + kPadL;  // padded, 1-based
-  double* rowbuf = smem + plen + static_cast<size_t>(warp) * plen + kPadL;
+  double* qsp = smem + pad;  // padded, 1-based
+  double* rowbuf = smem + plen + static_cast<size_t>(warp) * plen + pad;
   const double INF = d_inf();
   for (int k = threadIdx.x; k < static_cast<int>(plen); k += blockDim.x) {
-    const int j = k - kPadL;
+    const int j = k - pad;
     smem[k] = (j >= 1 && j <= L) ? p.queries[qi * L + j - 1] : INF;
   }
-  for (int k = lane; k < static_cast<int>(plen); k += 32) rowbuf[k - kPadL] = INF;
+  for (int k = lane; k < static_cast<int>(plen); k += 32) rowbuf[k - pad] = INF;
   if (threadIdx.x == 0) s_next = 0;
   __syncthreads();
   unsigned long long* key = p.ub_keys + qi;
-  unsigned long long cells = 0, calls = 0;
+  unsigned long long cells = 0, calls = 0, ovf = 0;
   for (;;) {
     unsigned long long t = 0;
     if (lane == 0) t = atomicAdd(&s_next, 1ull);
@@ -639,7 +716,8 @@ __global__ void __launch_bounds__(256) nn1_kernel(Nn1Params p) {
     auto rownorm = [](double x) -> double { return x; };
     auto get_ub = [&]() -> double { return load_ub(key); };
     auto rowthr = [](double u, int) -> double { return u; };
-    const double d = warp_dtw<false>(rowraw, rownorm, L, qsp, L, p.w, get_ub, rowthr, rowbuf, cells);
+    const double d = dtw_dispatch<false>(p.ad_k, rowraw, rownorm, L, qsp, L, p.w, get_ub, rowthr,
+                                         rowbuf, cells, ovf);
     ++calls;
     if (d != INF && lane == 0) {
       atomicMin(key, static_cast<unsigned long long>(__double_as_longlong(d)));
@@ -654,7 +732,7 @@ __global__ void __launch_bounds__(256) nn1_kernel(Nn1Params p) {
 
 cudaError_t launch_nn1(const Nn1Params& p, cudaStream_t stream) {
   const int warps = 8;
-  const size_t smem = static_cast<size_t>(warps + 1) * padded_len(p.len) * sizeof(double);
+  const size_t smem = static_cast<size_t>(warps + 1) * padded_len(p.len, p.ad_k) * sizeof(double);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(nn1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));

@@ -10,6 +10,7 @@ namespace eapdtw_b200 {
 
 constexpr long long kStatsResetInterval = 100000;  // search.cpp:16
 constexpr double kMinStddev = 1e-12;               // search.cpp:13
+constexpr int kScreenSlots = 24;                   // phase-A window (band offsets)
 
 // Tier counters accumulated on the device (SearchReport, search.hpp:68-77).
 enum Counter : int {
@@ -20,6 +21,8 @@ enum Counter : int {
   kCntDtwAbandoned,
   kCntCells,
   kCntCandidates,
+  kCntOverflows,
+  kCntScreened,
   kNumCounters
 };
 
@@ -47,6 +50,9 @@ struct SearchParams {
   unsigned long long* qtail;     // next slot to fill (zeroed before launch)
   unsigned long long* chunks_done;  // LB chunks published (zeroed before launch)
   long long direct_chunk;        // candidates per claim without the cascade
+  int ad_k;                      // anti-diagonal engine window 64*ad_k (0: strip engine only)
+  int direct;                    // 1: every candidate is a DTW task (the probe)
+  int screen_rows;               // phase-A lane screen depth (0: off)
   unsigned long long* counters;  // kNumCounters
   long long index_offset;        // shard start in the global reference
 };
@@ -59,6 +65,7 @@ struct PairParams {
   const double* ub;  // per pair (nullptr: +inf)
   const double* cb;  // per pair cumulative bound, lr each (nullptr: none)
   int prune;         // 0: full DP (dtw_windowed), 1: pruned
+  int ad_k;          // anti-diagonal engine window 64*ad_k (0: strip engine only)
   double* out;
   unsigned long long* cells;  // one counter
   long long npairs;
@@ -70,6 +77,7 @@ struct Nn1Params {
   long long nq, nd;
   int len, w;
   int splits;                     // blocks per query
+  int ad_k;                       // anti-diagonal engine window 64*ad_k (0: strip engine only)
   unsigned long long* ub_keys;    // nq
   BestRecord* best;               // nq
   unsigned long long* cells;      // one counter
@@ -81,7 +89,11 @@ cudaError_t launch_stats(const double* ref, long long n, int m, double* mean, do
                          cudaStream_t stream);
 cudaError_t launch_envelope(const double* ref, long long n, int r, double* up, double* lo,
                             cudaStream_t stream);
-size_t search_smem_bytes(int m, int warps);
+size_t search_smem_bytes(int m, int warps, int ad_k);
+// Window parameter of the anti-diagonal engine for a band of half width w
+// over series of length n: the smallest of 1/3/5 whose window 64K covers
+// the band, else 5 (odd K keeps shared-memory reads conflict-free).
+int choose_ad_k(int n, int w);
 cudaError_t launch_search(const SearchParams& p, int blocks, int warps, cudaStream_t stream);
 cudaError_t launch_pairwise(const PairParams& p, cudaStream_t stream);
 cudaError_t launch_nn1(const Nn1Params& p, cudaStream_t stream);

@@ -322,3 +322,54 @@ def test_sharded_plan_equals_unsharded(gpu, oracle_lib):
         cand = (r.best.distance_sq, r.best.location)
         best = cand if best is None or cand < best else best
     assert best == (want.distance_sq, want.location)
+
+
+def test_engines_long_series_vs_oracle(gpu, oracle_lib):
+    """Long random-walk pairs: anti-diagonal window shifts, overflow fallback
+    to the strip engine, unequal lengths, all band widths; bit-exact."""
+    from paper_2010_05371_b200 import znormalize
+    rng = np.random.default_rng(2026)
+    for it in range(120):
+        la = int(rng.integers(150, 700))
+        lb = la if it % 3 else int(rng.integers(100, la + 1))
+        a = znormalize(np.cumsum(rng.standard_normal(la)))
+        b = znormalize(np.cumsum(rng.standard_normal(lb)))
+        w = [5, 30, 70, 150, 300, UNB][it % 6]
+        if w != UNB and abs(la - lb) > w:
+            w = UNB
+        d = oracle_lib.dtw_windowed(a, b, w)
+        for ub in (np.inf, d, d * 1.05, d * 0.9, d * 3.0):
+            want = oracle_lib.ea_pruned_dtw_windowed(a, b, w, ub)
+            got = gpu.ea_pruned_dtw_windowed(a, b, gpu.Band(w), ub)
+            assert got == want, (it, la, lb, w, ub, got, want)
+    # batched: every pair in one launch, mixed cutoffs
+    a = np.stack([znormalize(np.cumsum(rng.standard_normal(400))) for _ in range(64)])
+    b = np.stack([znormalize(np.cumsum(rng.standard_normal(400))) for _ in range(64)])
+    for w in (20, 100, 250, UNB):
+        exact, _ = oracle_lib.pairwise(a, b, w, None)
+        ub = exact * rng.uniform(0.8, 1.3, 64)
+        want, _ = oracle_lib.pairwise(a, b, w, ub)
+        got, _ = gpu.pairwise(a, b, gpu.Band(w), ub)
+        assert np.array_equal(got, want), w
+
+
+@pytest.mark.parametrize("ad_k,screen", [("0", "0"), ("1", "8"), ("3", "16"), ("5", "32"),
+                                         ("0", "64"), ("3", "48")])
+def test_engine_and_screen_variants(gpu, oracle_lib, monkeypatch, ad_k, screen):
+    """Every DTW engine (strip, anti-diagonal K=1/3/5) and phase-A screen depth
+    gives the oracle's exact answer, with and without the cascade."""
+    monkeypatch.setenv("EAPDTW_AD_K", ad_k)
+    monkeypatch.setenv("EAPDTW_SCREEN_ROWS", screen)
+    for n, m, ratio, seed in [(60_000, 96, 0.1, 1), (40_000, 200, 0.3, 2), (30_000, 64, 1.0, 3),
+                              (50_000, 128, 0.05, 4)]:
+        ref = gpu.random_walk_normal(n, 100 + seed)
+        q = gpu.random_walk_normal(m, 200 + seed)
+        want = oracle_lib.similarity_search(ref, q, ratio)
+        for lb in (True, False):
+            got = gpu.similarity_search(ref, q, gpu.SearchConfig(window_ratio=ratio,
+                                                                 use_lower_bounds=lb))
+            assert (got.best.location, got.best.distance_sq) == (want.location,
+                                                                 want.distance_sq), (n, m, lb)
+            rep = got.report
+            assert rep.candidates_total == (rep.pruned_kim + rep.pruned_keogh_eq +
+                                            rep.pruned_keogh_ec + rep.dtw_calls)
