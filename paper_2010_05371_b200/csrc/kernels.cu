@@ -287,6 +287,7 @@ size_t search_smem_bytes(int m, int warps, int ad_k) {
          + static_cast<size_t>(m) * 8 * 2               // qu, ql
          + static_cast<size_t>(m) * 4 + 8               // order
          + static_cast<size_t>(warps) * padded_len(m, ad_k) * 8  // per-warp DP buffers
+         + static_cast<size_t>(warps) * 3 * kStack * 4  // per-warp tier stacks
          + 64;
 }
 
@@ -346,6 +347,8 @@ __global__ void __launch_bounds__(256) search_kernel(SearchParams p) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* rowbuf = reinterpret_cast<double*>(order + m + 2 - (m & 1)) +
                    static_cast<size_t>(warp) * plen + pad;
+  int* stacks = reinterpret_cast<int*>(reinterpret_cast<double*>(order + m + 2 - (m & 1)) +
+                                       static_cast<size_t>(blockDim.x >> 5) * plen);
 
   const double INF = d_inf();
   for (int k = threadIdx.x; k < static_cast<int>(plen); k += blockDim.x) {
@@ -416,8 +419,34 @@ __global__ void __launch_bounds__(256) search_kernel(SearchParams p) {
     //   been published (chunks_done == nchunks) a future slot beyond the final
     //   tail is void.
     const long long nchunks = (p.end - p.begin + 31) / 32;
-    bool chunks_left = true;
+    bool chunks_left = true, flushed = false;
     long long myslot = -1;
+    unsigned long long my_chunks = 0;
+    // Per-warp compaction stacks between the tiers (local candidate indices):
+    // Kim survivors -> [A] -> EQ -> [B] -> EC -> [C] -> phase-A screen -> queue.
+    // A tier runs only on a full warp of candidates (or when flushing), so
+    // lanes stay busy although each tier discards most of its input.
+    int* stkA = stacks + warp * (3 * kStack);
+    int* stkB = stkA + kStack;
+    int* stkC = stkB + kStack;
+    int nA = 0, nB = 0, nC = 0;
+
+    auto push = [&](int* stk, int& n, bool keep, long long cand) {
+      const unsigned mask = __ballot_sync(kFull, keep);
+      if (keep) stk[n + __popc(mask & ((1u << lane) - 1u))] = static_cast<int>(cand - p.begin);
+      n += __popc(mask);
+      __syncwarp();
+    };
+    // Pop up to 32 entries: lane L gets entry n-take+L (valid iff L < take).
+    auto pop = [&](int* stk, int& n, long long& cand) -> bool {
+      const int take = min(32, n);
+      const bool ok = lane < take;
+      cand = ok ? p.begin + stk[n - take + lane] : p.begin;
+      __syncwarp();
+      n -= take;
+      return ok;
+    };
+
     for (;;) {
       long long cand = -1;
       bool void_slot = false;
@@ -426,7 +455,7 @@ __global__ void __launch_bounds__(256) search_kernel(SearchParams p) {
           myslot = static_cast<long long>(atomicAdd(p.qhead, 1ull));
         if (myslot >= 0) {
           cand = vload(p.queue + myslot);
-          if (cand < 0 && !chunks_left &&
+          if (cand < 0 && flushed &&
               vload(p.chunks_done) == static_cast<unsigned long long>(nchunks) &&
               static_cast<unsigned long long>(myslot) >= vload(p.qtail))
             void_slot = true;
@@ -441,128 +470,183 @@ __global__ void __launch_bounds__(256) search_kernel(SearchParams p) {
         continue;
       }
       if (void_slot) break;
-      if (!chunks_left) {
+      if (flushed) {
         if (myslot < 0) break;  // nothing pending, nothing left to produce
         continue;               // wait for the pending slot to be filled
       }
 
-      // ---- lower-bound cascade on the next chunk of 32 candidates
-      unsigned long long chunk = 0;
-      if (lane == 0) chunk = atomicAdd(p.work, 1ull);
-      chunk = __shfl_sync(kFull, chunk, 0);
-      if (static_cast<long long>(chunk) >= nchunks) {
-        chunks_left = false;
-        continue;
-      }
-      const long long s = p.begin + static_cast<long long>(chunk) * 32 + lane;
-      const bool valid = s < p.end;
-      c_cand += __popc(__ballot_sync(kFull, valid));
-      bool alive = valid;
-      const double mean = valid ? p.mean[s] : 0.0;
-      const double sd = valid ? p.sd[s] : 1.0;
-      const bool constant = sd < kMinStddev;
-      double ub = load_ub(p.ub_key);
-      // --- Tier 1: LB_Kim on the two aligned extremities (search.cpp:81-87),
-      //     computed with the same IEEE divisions as the DTW rows.
-      if (p.use_lb && m >= 2 && alive) {
-        const double c0 = constant ? 0.0 : __ddiv_rn(__dsub_rn(ref[s], mean), sd);
-        const double cl = constant ? 0.0 : __ddiv_rn(__dsub_rn(ref[s + m - 1], mean), sd);
-        const double kim = __dadd_rn(sq_cost(qsp[1], c0), sq_cost(qsp[m], cl));
-        if (kim > ub) {
-          alive = false;
-          ++c_kim;
+      if (chunks_left) {
+        // ---- tier 1 on the next chunk of 32 candidates: LB_Kim on the two
+        //      aligned extremities (search.cpp:81-87), with the DTW's own IEEE
+        //      divisions (exact, so compared without a guard).
+        unsigned long long chunk = 0;
+        if (lane == 0) chunk = atomicAdd(p.work, 1ull);
+        chunk = __shfl_sync(kFull, chunk, 0);
+        if (static_cast<long long>(chunk) >= nchunks) {
+          chunks_left = false;  // flush the stacks below, then retire
+        } else {
+          ++my_chunks;
+          const long long s = p.begin + static_cast<long long>(chunk) * 32 + lane;
+          const bool valid = s < p.end;
+          c_cand += __popc(__ballot_sync(kFull, valid));
+          bool alive = valid;
+          if (p.use_lb && m >= 2 && alive) {
+            const double mean = p.mean[s];
+            const double sd = p.sd[s];
+            const bool constant = sd < kMinStddev;
+            const double c0 = constant ? 0.0 : __ddiv_rn(__dsub_rn(ref[s], mean), sd);
+            const double cl = constant ? 0.0 : __ddiv_rn(__dsub_rn(ref[s + m - 1], mean), sd);
+            const double kim = __dadd_rn(sq_cost(qsp[1], c0), sq_cost(qsp[m], cl));
+            if (kim > load_ub(p.ub_key)) {
+              alive = false;
+              ++c_kim;
+            }
+          }
+          if (p.use_lb) push(stkA, nA, alive, s);
+          else push(stkC, nC, alive, s);
         }
       }
-      const double rsd = constant ? 0.0 : __drcp_rn(sd);
-      // --- Tier 2: LB_Keogh EQ, query envelope vs normalised candidate
-      //     (search.cpp:92, lower_bounds.cpp:57-88), visiting order[] with a
-      //     chunked early-abandon vote.
-      double ubg = ub * (1.0 + p.guard_rel) + p.guard_abs;
-      bool pending = alive && p.use_lb;
-      if (__any_sync(kFull, pending)) {
+      const bool flush = !chunks_left;
+
+      // Two-phase early-abandoning LB_Keogh (lower_bounds.cpp:57-88): phase 1
+      // runs lane per candidate over the first kLbHead positions of order[]
+      // (the largest |q|, where nearly all prunes happen); each candidate
+      // still pending is then re-summed by the whole warp over ALL m positions
+      // in natural order (coalesced, 32 per step, a warp sum and abandon test
+      // every 128), so a survivor costs m/32 warp steps instead of holding 31
+      // idle lanes for m steps.  The bound is only gating, so the summation
+      // order is free (the guard covers the rounding).
+      auto lb_tier = [&](long long s, bool pending, const double mean, const double rsd,
+                         double ubg, auto term) -> bool {
+        bool alive = pending;
         double acc = 0.0;
-        for (int k0 = 0; k0 < m; k0 += 8) {
-          const int kend = min(m, k0 + 8);
-          for (int k = k0; k < kend; ++k) {
-            const int j = order[k];
-            const double x = pending ? ref[s + j] : 0.0;
-            const double cn = __dmul_rn(__dsub_rn(x, mean), rsd);
-            const double e1 = cn - qu[j];
-            const double e2 = ql[j] - cn;
-            const double dd = e1 > 0.0 ? e1 : (e2 > 0.0 ? e2 : 0.0);
-            acc = fma(dd, dd, acc);
-          }
+        const int head = min(m, kLbHead);
+        for (int k0 = 0; k0 < head; k0 += 8) {
+          const int kend = min(head, k0 + 8);
+          for (int k = k0; k < kend; ++k) acc += term(pending, s, order[k], mean, rsd);
           if (pending && acc > ubg) {
             pending = false;
             alive = false;
-            ++c_eq;
           }
           if (!__any_sync(kFull, pending)) break;
         }
+        if (head >= m) return alive;
+        unsigned pend = __ballot_sync(kFull, pending);
+        while (pend) {
+          const int l = __ffs(pend) - 1;
+          pend &= pend - 1;
+          const long long sl = __shfl_sync(kFull, s, l);
+          const double ml = __shfl_sync(kFull, mean, l);
+          const double rl = __shfl_sync(kFull, rsd, l);
+          double part = 0.0;
+          bool abandoned = false;
+          for (int k0 = 0; k0 < m; k0 += 128) {
+            const int kend = min(m, k0 + 128);
+            for (int j = k0 + lane; j < kend; j += 32) part += term(true, sl, j, ml, rl);
+            double tot = part;
+            for (int off = 16; off > 0; off >>= 1) tot += __shfl_xor_sync(kFull, tot, off);
+            if (tot > ubg) {
+              abandoned = true;
+              break;
+            }
+          }
+          if (lane == l && abandoned) alive = false;
+        }
+        return alive;
+      };
+      // EQ term: query envelope vs normalised candidate (reciprocal multiply).
+      auto eq_term = [&](bool on, long long s, int j, double mean, double rsd) -> double {
+        const double x = on ? ref[s + j] : 0.0;
+        const double cn = __dmul_rn(__dsub_rn(x, mean), rsd);
+        const double e1 = cn - qu[j];
+        const double e2 = ql[j] - cn;
+        const double dd = e1 > 0.0 ? e1 : (e2 > 0.0 ? e2 : 0.0);
+        return dd * dd;
+      };
+      // EC term: normalised query vs the candidate envelope (global raw envelope).
+      auto ec_term = [&](bool on, long long s, int j, double mean, double rsd) -> double {
+        double U = 0.0, L = 0.0;
+        if (on) {
+          U = __dmul_rn(__dsub_rn(p.env_up[s + j], mean), rsd);
+          L = __dmul_rn(__dsub_rn(p.env_lo[s + j], mean), rsd);
+        }
+        const double qj = qsp[j + 1];
+        const double e1 = qj - U;
+        const double e2 = L - qj;
+        const double dd = e1 > 0.0 ? e1 : (e2 > 0.0 ? e2 : 0.0);
+        return dd * dd;
+      };
+
+      // ---- tier 2: LB_Keogh EQ (search.cpp:92); prune iff lb > ub*(1+g_rel) + g_abs.
+      while (nA >= 32 || (flush && nA > 0)) {
+        long long s;
+        const bool pending = pop(stkA, nA, s);
+        const double mean = p.mean[s];
+        const double sd = p.sd[s];
+        const double rsd = sd < kMinStddev ? 0.0 : __drcp_rn(sd);
+        const double ubg = load_ub(p.ub_key) * (1.0 + p.guard_rel) + p.guard_abs;
+        const bool alive = lb_tier(s, pending, mean, rsd, ubg, eq_term);
+        if (pending && !alive) ++c_eq;
+        if (p.env_up != nullptr) push(stkB, nB, alive, s);
+        else push(stkC, nC, alive, s);
       }
-      // --- Tier 3: LB_Keogh EC, normalised query vs the candidate envelope
-      //     (search.cpp:97-99) read from the global raw envelope.
-      if (p.use_lb && p.env_up != nullptr) {
-        ub = load_ub(p.ub_key);
-        ubg = ub * (1.0 + p.guard_rel) + p.guard_abs;
-        pending = alive;
-        if (__any_sync(kFull, pending)) {
-          double acc = 0.0;
-          for (int k0 = 0; k0 < m; k0 += 8) {
-            const int kend = min(m, k0 + 8);
-            for (int k = k0; k < kend; ++k) {
-              const int j = order[k];
-              double U = 0.0, L = 0.0;
-              if (pending) {
-                U = __dmul_rn(__dsub_rn(p.env_up[s + j], mean), rsd);
-                L = __dmul_rn(__dsub_rn(p.env_lo[s + j], mean), rsd);
-              }
-              const double qj = qsp[j + 1];
-              const double e1 = qj - U;
-              const double e2 = L - qj;
-              const double dd = e1 > 0.0 ? e1 : (e2 > 0.0 ? e2 : 0.0);
-              acc = fma(dd, dd, acc);
-            }
-            if (pending && acc > ubg) {
-              pending = false;
-              alive = false;
-              ++c_ec;
-            }
-            if (!__any_sync(kFull, pending)) break;
+
+      // ---- tier 3: LB_Keogh EC (search.cpp:97-99).
+      while (nB >= 32 || (flush && nB > 0)) {
+        long long s;
+        const bool pending = pop(stkB, nB, s);
+        const double mean = p.mean[s];
+        const double sd = p.sd[s];
+        const double rsd = sd < kMinStddev ? 0.0 : __drcp_rn(sd);
+        const double ubg = load_ub(p.ub_key) * (1.0 + p.guard_rel) + p.guard_abs;
+        const bool alive = lb_tier(s, pending, mean, rsd, ubg, ec_term);
+        if (pending && !alive) ++c_ec;
+        push(stkC, nC, alive, s);
+      }
+
+      // ---- phase A: the first screen_rows DTW rows, lane per candidate (an
+      //      exact EAPrunedDTW prefix; a killed candidate is an abandoned
+      //      DTW), then publish the survivors to the queue.
+      while (nC >= 32 || (flush && nC > 0)) {
+        long long s;
+        bool alive = pop(stkC, nC, s);
+        if (p.screen_rows > 0) {
+          const double mean = p.mean[s];
+          const double sd = p.sd[s];
+          const bool constant = sd < kMinStddev;
+          const double* xs = ref + s;
+          auto c_of = [&](int r) -> double {
+            return constant ? 0.0 : __ddiv_rn(__dsub_rn(xs[r - 1], mean), sd);
+          };
+          unsigned nrows = 0;
+          const bool killed = screen_prefix<kScreenSlots>(alive, c_of, p.screen_rows, qsp, m,
+                                                          p.w, load_ub(p.ub_key), nrows);
+          c_cells_lane += static_cast<unsigned long long>(nrows) * kScreenSlots;
+          if (killed) {
+            alive = false;
+            ++c_scr;
+          }
+        }
+        const unsigned mask = __ballot_sync(kFull, alive);
+        if (mask) {
+          unsigned long long qb = 0;
+          if (lane == 0) qb = atomicAdd(p.qtail, static_cast<unsigned long long>(__popc(mask)));
+          qb = __shfl_sync(kFull, qb, 0);
+          if (alive) {
+            const unsigned rank = __popc(mask & ((1u << lane) - 1u));
+            reinterpret_cast<volatile long long*>(p.queue)[qb + rank] = s;
           }
         }
       }
-      // --- Phase A: the first screen_rows DTW rows, lane per candidate (an
-      //     exact EAPrunedDTW prefix; a killed candidate is an abandoned DTW).
-      if (p.screen_rows > 0 && __any_sync(kFull, alive)) {
-        const double* xs = ref + s;
-        auto c_of = [&](int r) -> double {
-          return constant ? 0.0 : __ddiv_rn(__dsub_rn(xs[r - 1], mean), sd);
-        };
-        unsigned nrows = 0;
-        const bool killed =
-            screen_prefix<kScreenSlots>(alive, c_of, p.screen_rows, qsp, m, p.w,
-                                        load_ub(p.ub_key), nrows);
-        c_cells_lane += static_cast<unsigned long long>(nrows) * kScreenSlots;
-        if (killed) {
-          alive = false;
-          ++c_scr;
-        }
+
+      if (flush) {
+        // Every candidate of this warp's chunks is now published: only then
+        // may they count as done (the queue's void-slot rule relies on it).
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicAdd(p.chunks_done, my_chunks);
+        flushed = true;
       }
-      // ---- publish the survivors, then mark the chunk done
-      const unsigned mask = __ballot_sync(kFull, alive);
-      if (mask) {
-        unsigned long long qb = 0;
-        if (lane == 0) qb = atomicAdd(p.qtail, static_cast<unsigned long long>(__popc(mask)));
-        qb = __shfl_sync(kFull, qb, 0);
-        if (alive) {
-          const unsigned rank = __popc(mask & ((1u << lane) - 1u));
-          reinterpret_cast<volatile long long*>(p.queue)[qb + rank] = s;
-        }
-      }
-      __threadfence();
-      __syncwarp();
-      if (lane == 0) atomicAdd(p.chunks_done, 1ull);
     }
   }
 

@@ -11,6 +11,8 @@ namespace eapdtw_b200 {
 constexpr long long kStatsResetInterval = 100000;  // search.cpp:16
 constexpr double kMinStddev = 1e-12;               // search.cpp:13
 constexpr int kScreenSlots = 24;                   // phase-A window (band offsets)
+constexpr int kStack = 64;                         // per-warp tier stack capacity
+constexpr int kLbHead = 1 << 30;                   // lane-parallel prefix of the Keogh tiers (all: the warp-cooperative tail measured slower)
 
 // Tier counters accumulated on the device (SearchReport, search.hpp:68-77).
 enum Counter : int {
