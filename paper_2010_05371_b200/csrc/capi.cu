@@ -169,6 +169,7 @@ int eapdtw_ctx_create(eapdtw_ctx** out, int device) {
   CUDA_TRY(cudaSetDevice(device));
   auto* c = new eapdtw_ctx();
   c->device = device;
+
   e = cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking);
   if (e != cudaSuccess) {
     delete c;
@@ -234,6 +235,7 @@ static int pairwise_impl(eapdtw_ctx* c, const double* rows_dev, const double* co
   p.out = out_dev;
   p.cells = c->cells.as<unsigned long long>();
   p.npairs = static_cast<long long>(npairs);
+  CUDA_TRY(set_strip_rows(c->stream));
   CUDA_TRY(launch_pairwise(p, c->stream));
   ++c->launches;
   if (cells) {
@@ -457,19 +459,30 @@ static int plan_init(eapdtw_search_plan* p, eapdtw_ctx* c, const double* ref_dev
   // the staging vectors are pageable locals: wait until the copies consumed them
   CUDA_TRY(cudaStreamSynchronize(s));
 
-  // Occupancy-sized persistent grid: as many 8-warp blocks as shared memory allows.
+  // Occupancy-sized persistent grid: the largest number of resident warps
+  // (blocks of `warps` warps, limited by shared memory and by the kernel's
+  // register budget of 2 x 256-thread blocks per SM).
   int sms = 148, max_smem = 0, optin = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, c->device);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device);
-  p->warps = 8;
-  while (p->warps > 1 && search_smem_bytes(static_cast<int>(m), p->warps, p->ad_k) > static_cast<size_t>(optin))
-    p->warps /= 2;
-  const size_t smem = search_smem_bytes(static_cast<int>(m), p->warps, p->ad_k);
-  if (smem > static_cast<size_t>(optin))
+  int best_warps = 0, best_w = 0, best_blocks = 0;
+  for (int wpb = 8; wpb >= 1; --wpb) {
+    const size_t smem = search_smem_bytes(static_cast<int>(m), wpb, p->ad_k);
+    if (smem > static_cast<size_t>(optin)) continue;
+    const int by_smem = static_cast<int>(max_smem / (smem + 1024));
+    const int by_regs = (2 * 8) / wpb;  // register budget: 16 warps per SM
+    const int per_sm = std::min(by_smem, std::max(1, by_regs));
+    if (per_sm * wpb > best_warps) {
+      best_warps = per_sm * wpb;
+      best_w = wpb;
+      best_blocks = per_sm;
+    }
+  }
+  if (best_warps == 0)
     return fail(EAPDTW_EINVAL, "search: query length exceeds the shared-memory budget");
-  const int per_sm = std::max(1, std::min(static_cast<int>(max_smem / (smem + 1024)), 64 / p->warps));
-  p->blocks = sms * per_sm;
+  p->warps = best_w;
+  p->blocks = sms * best_blocks;
   return eapdtw_search_plan_reset(p);
 }
 
@@ -499,6 +512,13 @@ int eapdtw_search_plan_reset(eapdtw_search_plan* p) {
   CUDA_TRY(cudaMemsetAsync(B.probe_counters.p, 0, kNumCounters * 8, s));
   CUDA_TRY(launch_init_best(B.best.as<BestRecord>(), p->key, 1, s));
   ++c->launches;
+  if (const char* env = getenv("EAPDTW_SEED_UB")) {  // experiment: start from a known threshold
+    const double ub = atof(env);
+    unsigned long long bits;
+    std::memcpy(&bits, &ub, 8);
+    CUDA_TRY(cudaMemcpyAsync(p->key, &bits, 8, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+  }
   p->prepared = false;
   p->ran = false;
   p->t0 = std::chrono::steady_clock::now();
@@ -600,6 +620,7 @@ int eapdtw_search_plan_prepare(eapdtw_search_plan* p) {
   sp.counters = B.probe_counters.as<unsigned long long>();
   sp.direct_chunk = 1;
   sp.direct = 1;
+  CUDA_TRY(set_strip_rows(s));
   CUDA_TRY(reset_work(p, static_cast<long long>(nprobe), s));
   CUDA_TRY(launch_search(sp, p->blocks, p->warps, s));
   ++c->launches;
@@ -772,6 +793,7 @@ static int nn1_impl(eapdtw_ctx* c, const double* q_dev, size_t nq, const double*
   p.best = c->best.as<BestRecord>();
   p.cells = c->counters.as<unsigned long long>();
   p.dtw_calls = c->counters.as<unsigned long long>() + 1;
+  CUDA_TRY(set_strip_rows(s));
   CUDA_TRY(launch_nn1(p, s));
   ++c->launches;
   std::vector<BestRecord> rec(nq);

@@ -232,4 +232,142 @@ __device__ double warp_dtw(const RawFn& rowraw, const NormFn& rownorm, int lr,
   return r <= ub_last ? r : INF;
 }
 
+
+// Two rows per lane: the same skewed wavefront over strips of 64 rows, lane L
+// owning rows i0+2L and i0+2L+1.  The lane's second row takes its top and
+// diagonal from its own first row (registers), so one __shfl_up of a double
+// and one shared-memory query read serve two cells per step, and the
+// finished-flag / ballot bookkeeping is shared too.  Same contract as
+// warp_dtw (exact value iff <= ub, else +inf); no KILL variant.
+template <class RawFn, class NormFn, class UbFn>
+__device__ double warp_dtw2(const RawFn& rowraw, const NormFn& rownorm, int lr,
+                            const double* __restrict__ qsp, int lc, int w, UbFn&& get_ub,
+                            double* __restrict__ rowbuf, unsigned long long& cells) {
+  const int lane = threadIdx.x & 31;
+  const double INF = d_inf();
+  for (int k = lane; k <= lc + 1; k += 32) rowbuf[k] = k == 0 ? 0.0 : INF;
+  const bool banded = w < lr;
+  int lo = 0, hi = 0;  // live column range of the row held in rowbuf (row i0-1)
+  int written = 0;
+  unsigned cnt = 0;
+  double ub_last = INF;
+  double ub_next = get_ub();
+  double x1n = 2 * lane < lr ? rowraw(2 * lane) : 0.0;
+  double x2n = 2 * lane + 1 < lr ? rowraw(2 * lane + 1) : 0.0;
+  __syncwarp();
+
+  for (int i0 = 1; i0 <= lr; i0 += 64) {
+    const double ub_strip = ub_next;
+    const int i1 = i0 + 2 * lane, i2 = i1 + 1;
+    const bool act1 = i1 <= lr, act2 = i2 <= lr;
+    const double x1 = x1n, x2 = x2n;
+    if (i0 + 64 <= lr) {  // prefetch the next strip's threshold and row values
+      ub_next = get_ub();
+      x1n = i1 + 64 <= lr ? rowraw(i1 + 63) : 0.0;
+      x2n = i2 + 64 <= lr ? rowraw(i2 + 63) : 0.0;
+    }
+    const double ub = fmin(ub_strip, DBL_MAX);
+    const int ub_hi = __double2hiint(ub);
+    ub_last = ub;
+    const int last = min(i0 + 63, lr);      // the strip's last row
+    const int wl = (last - i0) >> 1;         // its lane
+    const bool wsecond = ((last - i0) & 1) != 0;
+    const double c1 = act1 ? rownorm(x1) : INF;
+    const double c2 = act2 ? rownorm(x2) : INF;
+    const int jb = max(lo, 1);
+    const int bl1 = banded ? max(1, i1 - w) : 1;
+    const int bh1 = act1 ? (banded ? min(lc, i1 + w) : lc) : -1;
+    const int bl2 = banded ? max(1, i2 - w) : 1;
+    // an inactive second row simply follows the first (it never lives)
+    const int bh2 = act2 ? (banded ? min(lc, i2 + w) : lc) : lc + 64;
+    double top_prev = (lane == 0 && jb - 1 >= lo && jb - 1 <= hi) ? rowbuf[jb - 1] : INF;
+    int j = jb - lane;
+    const double* qp = qsp + j;
+    double* rp = rowbuf + j;
+    double v1 = INF, v2 = INF;
+    bool fin1 = !act1, fin2 = !act1;
+    int jf1 = fin1 ? j - 1 : lc + 1, jf2 = jf1;
+    unsigned finmask = __ballot_sync(kFull, fin2);
+    const bool w1 = lane == wl && !wsecond, w2 = lane == wl && wsecond;
+    const bool is0 = lane == 0;
+    const unsigned span1 = static_cast<unsigned>(bh1 - bl1);
+    const unsigned span2 = static_cast<unsigned>(max(bh2 - bl2, 0));
+    int jr1 = j - bl1, jr2 = j - bl2;
+    const unsigned upbit = is0 ? 0x80000000u : (1u << (lane - 1));
+
+    auto step = [&](int u) {
+      const double sh = __shfl_up_sync(kFull, v2, 1);
+      const double top = is0 ? rp[u] : sh;
+      const double diag = top_prev;
+      top_prev = top;
+      const double qj = qp[u];
+      double n1 = __dadd_rn(sq_cost(c1, qj), dmin2(v1, dmin2(top, diag)));
+      n1 = static_cast<unsigned>(jr1 + u) <= span1 ? n1 : INF;
+      double n2 = __dadd_rn(sq_cost(c2, qj), dmin2(v2, dmin2(n1, v1)));
+      n2 = static_cast<unsigned>(jr2 + u) <= span2 ? n2 : INF;
+      const bool live1 = __double2hiint(n1) <= ub_hi;  // superset of n <= ub
+      const bool live2 = __double2hiint(n2) <= ub_hi;
+      if (w1) rp[u] = n1;
+      if (w2) rp[u] = n2;
+      v1 = n1;
+      v2 = n2;
+      const unsigned up = (finmask & 0x7fffffffu) | (j + u > hi ? 0x80000000u : 0u);
+      const bool nf1 = fin1 || jr1 + u > static_cast<int>(span1) || ((up & upbit) && !live1);
+      const bool nf2 = fin2 || jr2 + u > static_cast<int>(span2) || (nf1 && !live2);
+      jf1 = (!fin1 && nf1) ? j + u : jf1;
+      jf2 = (!fin2 && nf2) ? j + u : jf2;
+      fin1 = nf1;
+      fin2 = nf2;
+      finmask = __ballot_sync(kFull, fin2);
+    };
+
+    for (;;) {
+      step(0);
+      step(1);
+      step(2);
+      step(3);
+      if (finmask == kFull) break;
+      j += 4;
+      jr1 += 4;
+      jr2 += 4;
+      qp += 4;
+      rp += 4;
+    }
+    const int wend = jb - wl + (j - (jb - lane)) + 3;
+    for (int k = max(wend + 1, 0) + lane; k <= written; k += 32) rowbuf[k] = INF;
+    written = min(max(wend, 0), lc + 1);
+    {
+      const int a0 = max(jb, bl1), a1 = min(jf1, bh1);
+      cnt += act1 && a1 >= a0 ? static_cast<unsigned>(a1 - a0 + 1) : 0u;
+      const int b0 = max(jb, bl2), b1 = min(jf2, bh2);
+      cnt += act2 && b1 >= b0 ? static_cast<unsigned>(b1 - b0 + 1) : 0u;
+    }
+    __syncwarp();
+    const int wcol1 = min(wend, lc);
+    const int ubl_hi = __double2hiint(ub_last);
+    int nlo = INT_MAX, nhi = -1;
+    for (int k0 = jb; k0 <= wcol1; k0 += 32) {
+      const int k = k0 + lane;
+      bool lv = false;
+      if (k <= wcol1) lv = __double2hiint(rowbuf[k]) <= ubl_hi;
+      const unsigned bm = __ballot_sync(kFull, lv);
+      if (bm) {
+        if (nlo == INT_MAX) nlo = k0 + __ffs(bm) - 1;
+        nhi = k0 + 31 - __clz(bm);
+      }
+    }
+    if (nhi < 0) {
+      lo = -1;
+      break;
+    }
+    lo = nlo;
+    hi = nhi;
+  }
+  for (int off = 16; off > 0; off >>= 1) cnt += __shfl_xor_sync(kFull, cnt, off);
+  if (lane == 0) cells += cnt;
+  if (lo < 0 || hi != lc) return INF;
+  const double r = rowbuf[lc];
+  return r <= ub_last ? r : INF;
+}
+
 }  // namespace eapdtw_b200

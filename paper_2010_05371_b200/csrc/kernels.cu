@@ -284,11 +284,25 @@ static __host__ __device__ inline size_t padded_len(int m, int ad_k) {
 
 size_t search_smem_bytes(int m, int warps, int ad_k) {
   return padded_len(m, ad_k) * 8                        // q (padded, 1-based)
-         + static_cast<size_t>(m) * 8 * 2               // qu, ql
-         + static_cast<size_t>(m) * 4 + 8               // order
          + static_cast<size_t>(warps) * padded_len(m, ad_k) * 8  // per-warp DP buffers
          + static_cast<size_t>(warps) * 3 * kStack * 4  // per-warp tier stacks
          + 64;
+}
+
+// Strip engine rows per lane (1 or 2), set per launch through a constant.
+__constant__ int g_strip_rows = 1;
+
+cudaError_t set_strip_rows(cudaStream_t stream) {
+  int rows = 1;  // two rows per lane measured slower on the search configs
+  if (const char* env = getenv("EAPDTW_STRIP_ROWS")) {  // experiment override: 1 or 2
+    const int r = atoi(env);
+    if (r == 1 || r == 2) rows = r;
+  }
+  static thread_local int last = -1;
+  if (rows == last) return cudaSuccess;
+  last = rows;
+  return cudaMemcpyToSymbolAsync(g_strip_rows, &rows, sizeof(int), 0, cudaMemcpyHostToDevice,
+                                 stream);
 }
 
 int choose_ad_k(int n, int w) {
@@ -325,6 +339,10 @@ __device__ double dtw_dispatch(int ad_k, const RawFn& rowraw, const NormFn& rown
     ++overflows;
     __syncwarp();
   }
+#ifdef EAPDTW_WITH_STRIP2
+  if (!KILL && g_strip_rows == 2)
+    return warp_dtw2(rowraw, rownorm, lr, qsp, lc, w, get_ub, buf, cells);
+#endif
   return warp_dtw<KILL>(rowraw, rownorm, lr, qsp, lc, w, get_ub, rowthr, buf, cells);
 }
 
@@ -335,20 +353,29 @@ __device__ __forceinline__ unsigned long long vload(const unsigned long long* p)
   return *reinterpret_cast<const volatile unsigned long long*>(p);
 }
 
-__global__ void __launch_bounds__(256) search_kernel(SearchParams p) {
+#ifndef EAPDTW_SEARCH_MIN_BLOCKS
+#define EAPDTW_SEARCH_MIN_BLOCKS 2
+#endif
+constexpr int kSearchMinBlocks = EAPDTW_SEARCH_MIN_BLOCKS;
+
+// AD_K: anti-diagonal engine window compiled into this instantiation (0: strip
+// engine only -- the default search path, which then needs far fewer registers).
+template <int AD_K>
+__global__ void __launch_bounds__(256, kSearchMinBlocks) search_kernel(SearchParams p) {
   extern __shared__ double smem[];
   const int m = p.m;
   const int pad = smem_pad(p.ad_k);
   const size_t plen = padded_len(m, p.ad_k);
   double* qsp = smem + pad;                        // qsp[-pad .. m+1+pad]
-  double* qu = smem + plen;                        // [m]
-  double* ql = qu + m;                             // [m]
-  int* order = reinterpret_cast<int*>(ql + m);     // [m]
+  // The Keogh envelope and visiting order stay in global memory: every lane
+  // reads the same element (broadcast through L1), which frees shared memory
+  // for more resident warps.
+  const double* __restrict__ qu = p.qu;
+  const double* __restrict__ ql = p.ql;
+  const int* __restrict__ order = p.order;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* rowbuf = reinterpret_cast<double*>(order + m + 2 - (m & 1)) +
-                   static_cast<size_t>(warp) * plen + pad;
-  int* stacks = reinterpret_cast<int*>(reinterpret_cast<double*>(order + m + 2 - (m & 1)) +
-                                       static_cast<size_t>(blockDim.x >> 5) * plen);
+  double* rowbuf = smem + plen + static_cast<size_t>(warp) * plen + pad;
+  int* stacks = reinterpret_cast<int*>(smem + plen + static_cast<size_t>(blockDim.x >> 5) * plen);
 
   const double INF = d_inf();
   for (int k = threadIdx.x; k < static_cast<int>(plen); k += blockDim.x) {
@@ -356,13 +383,6 @@ __global__ void __launch_bounds__(256) search_kernel(SearchParams p) {
     smem[k] = (j >= 1 && j <= m) ? p.q[j] : INF;
   }
   for (int k = lane; k < static_cast<int>(plen); k += 32) rowbuf[k - pad] = INF;
-  if (p.use_lb) {
-    for (int k = threadIdx.x; k < m; k += blockDim.x) {
-      qu[k] = p.qu[k];
-      ql[k] = p.ql[k];
-      order[k] = p.order[k];
-    }
-  }
   __syncthreads();
 
   unsigned long long c_kim = 0, c_eq = 0, c_ec = 0, c_calls = 0, c_aband = 0, c_cells = 0,
@@ -382,7 +402,7 @@ __global__ void __launch_bounds__(256) search_kernel(SearchParams p) {
     };
     auto get_ub = [&]() -> double { return prune ? load_ub(p.ub_key) : INF; };
     auto rowthr = [](double u, int) -> double { return u; };
-    const double d = dtw_dispatch<false>(p.ad_k, rowraw, rownorm, m, qsp, m, p.w, get_ub, rowthr,
+    const double d = dtw_dispatch<false>(AD_K, rowraw, rownorm, m, qsp, m, p.w, get_ub, rowthr,
                                          rowbuf, c_cells, c_ovf);
     ++c_calls;
     if (d == INF) {
@@ -677,11 +697,19 @@ __global__ void __launch_bounds__(256) search_kernel(SearchParams p) {
 
 cudaError_t launch_search(const SearchParams& p, int blocks, int warps, cudaStream_t stream) {
   const size_t smem = search_smem_bytes(p.m, warps, p.ad_k);
-  cudaError_t e = cudaFuncSetAttribute(search_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
-  if (e != cudaSuccess) return e;
-  search_kernel<<<blocks, warps * 32, smem, stream>>>(p);
-  return cudaGetLastError();
+  auto go = [&](auto kern) -> cudaError_t {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    kern<<<blocks, warps * 32, smem, stream>>>(p);
+    return cudaGetLastError();
+  };
+  switch (p.ad_k) {
+    case 1: return go(search_kernel<1>);
+    case 3: return go(search_kernel<3>);
+    case 5: return go(search_kernel<5>);
+    default: return go(search_kernel<0>);
+  }
 }
 
 // ---------------------------------------------------------------------------

@@ -96,6 +96,8 @@ size_t search_smem_bytes(int m, int warps, int ad_k);
 // over series of length n: the smallest of 1/3/5 whose window 64K covers
 // the band, else 5 (odd K keeps shared-memory reads conflict-free).
 int choose_ad_k(int n, int w);
+// Rows per lane of the strip engine (EAPDTW_STRIP_ROWS=1 or 2; default 1).
+cudaError_t set_strip_rows(cudaStream_t stream);
 cudaError_t launch_search(const SearchParams& p, int blocks, int warps, cudaStream_t stream);
 cudaError_t launch_pairwise(const PairParams& p, cudaStream_t stream);
 cudaError_t launch_nn1(const Nn1Params& p, cudaStream_t stream);

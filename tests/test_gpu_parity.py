@@ -353,13 +353,16 @@ def test_engines_long_series_vs_oracle(gpu, oracle_lib):
         assert np.array_equal(got, want), w
 
 
-@pytest.mark.parametrize("ad_k,screen", [("0", "0"), ("1", "8"), ("3", "16"), ("5", "32"),
-                                         ("0", "64"), ("3", "48")])
-def test_engine_and_screen_variants(gpu, oracle_lib, monkeypatch, ad_k, screen):
-    """Every DTW engine (strip, anti-diagonal K=1/3/5) and phase-A screen depth
-    gives the oracle's exact answer, with and without the cascade."""
+@pytest.mark.parametrize("ad_k,screen,strip", [("0", "0", "1"), ("1", "8", "2"), ("3", "16", "1"),
+                                               ("5", "32", "2"), ("0", "64", "2"),
+                                               ("3", "48", "2"), ("0", "16", "1")])
+def test_engine_and_screen_variants(gpu, oracle_lib, monkeypatch, ad_k, screen, strip):
+    """Every DTW engine (strip with 1 or 2 rows per lane, anti-diagonal K=1/3/5)
+    and phase-A screen depth gives the oracle's exact answer, with and without
+    the cascade."""
     monkeypatch.setenv("EAPDTW_AD_K", ad_k)
     monkeypatch.setenv("EAPDTW_SCREEN_ROWS", screen)
+    monkeypatch.setenv("EAPDTW_STRIP_ROWS", strip)
     for n, m, ratio, seed in [(60_000, 96, 0.1, 1), (40_000, 200, 0.3, 2), (30_000, 64, 1.0, 3),
                               (50_000, 128, 0.05, 4)]:
         ref = gpu.random_walk_normal(n, 100 + seed)
