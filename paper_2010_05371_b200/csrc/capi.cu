@@ -143,7 +143,7 @@ struct eapdtw_search_plan {
   size_t ncand = 0;
   cudaEvent_t ev[8] = {};
   bool prepared = false, ran = false;
-  int blocks = 0, warps = 8, ad_k = 0, screen_rows = 16;
+  int blocks = 0, warps = 8, ad_k = 0, screen_rows = 16, coarse_stride = 64;
   double guard_rel = 1e-9, guard_abs = 1e-20;
   std::chrono::steady_clock::time_point t0;
 };
@@ -402,6 +402,7 @@ static int plan_init(eapdtw_search_plan* p, eapdtw_ctx* c, const double* ref_dev
   // opt-in here (EAPDTW_AD_K) and the default for pairwise / NN1 batches.
   p->ad_k = getenv("EAPDTW_AD_K") ? choose_ad_k(static_cast<int>(m), p->w_eff) : 0;
   if (const char* env = getenv("EAPDTW_SCREEN_ROWS")) p->screen_rows = std::max(0, atoi(env));
+  if (const char* env = getenv("EAPDTW_COARSE_STRIDE")) p->coarse_stride = std::max(0, atoi(env));
   p->guard_abs = 1e-20;
 
   // Query preparation exactly as search.cpp:136-149.
@@ -574,6 +575,7 @@ static SearchParams base_params(eapdtw_search_plan* p) {
   s.qtail = B.qctr.as<unsigned long long>() + 1;
   s.chunks_done = B.qctr.as<unsigned long long>() + 2;
   s.direct_chunk = 4;
+  s.stride = 1;
   s.ad_k = p->ad_k;
   s.direct = 0;
   s.screen_rows = p->screen_rows;
@@ -624,6 +626,22 @@ int eapdtw_search_plan_prepare(eapdtw_search_plan* p) {
   CUDA_TRY(reset_work(p, static_cast<long long>(nprobe), s));
   CUDA_TRY(launch_search(sp, p->blocks, p->warps, s));
   ++c->launches;
+  // Coarse pass: the full cascade over every coarse_stride-th candidate, so
+  // the sweep starts from a threshold close to the final one (neighbouring
+  // windows normalise to nearly the same series).  Its candidates are real,
+  // so their exact results enter the record; their work is counted with the
+  // probe's.
+  if (p->coarse_stride > 1 && p->ncand >= 64 * static_cast<size_t>(p->coarse_stride)) {
+    SearchParams cp = base_params(p);
+    cp.begin = 0;
+    cp.end = static_cast<long long>(p->ncand);
+    cp.stride = p->coarse_stride;
+    cp.counters = B.probe_counters.as<unsigned long long>();
+    const long long count = (cp.end + cp.stride - 1) / cp.stride;
+    CUDA_TRY(reset_work(p, count, s));
+    CUDA_TRY(launch_search(cp, p->blocks, p->warps, s));
+    ++c->launches;
+  }
   CUDA_TRY(cudaEventRecord(p->ev[3], s));
   p->prepared = true;
   return EAPDTW_OK;

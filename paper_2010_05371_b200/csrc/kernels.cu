@@ -154,9 +154,12 @@ cudaError_t launch_stats(const double* ref, long long n, int m, double* mean, do
 // envelope is built ONCE for the whole reference with radius r; at the two
 // candidate edges (j < r or j > m-1-r) the global window is a superset of the
 // candidate's clamped window, which only loosens the bound (still sound).
-// Van Herk/Gil-Werman: with blocks of K = 2r+1, max over [p-r, p+r] =
-// max(suffixmax[p-r], prefixmax[p+r]); the in-block prefix/suffix maxima are
-// warp scans with a carried value, one warp per K-block of a smem tile.
+// Sparse-table doubling in shared memory: with K = 2r+1 and P the largest
+// power of two <= K, max over [p-r, p+r] = max(M_P[p-r], M_P[p+r-P+1]) where
+// M_s[i] = max(a[i .. i+s-1]).  M_P is built from M_1 = a in log2(P) fully
+// parallel passes (ping-pong buffers); max and min are done one after the
+// other.  Every pass touches the whole tile with all threads, so the kernel
+// streams at shared-memory speed instead of following a dependent scan.
 // ---------------------------------------------------------------------------
 template <bool MAX>
 __device__ __forceinline__ double pick(double a, double b) {
@@ -164,73 +167,48 @@ __device__ __forceinline__ double pick(double a, double b) {
 }
 
 template <bool MAX>
-__device__ void envelope_pass(const double* a, double* g, double* h, int len, int K) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+__device__ void envelope_doubling(const double* __restrict__ ref, long long n, long long A, int len,
+                                  int r, int T, long long P0, double* buf0, double* buf1,
+                                  double* __restrict__ out) {
   const double ident = MAX ? -d_inf() : d_inf();
-  const int nblk = (len + K - 1) / K;
-  for (int b = warp; b < nblk; b += nw) {
-    const int start = b * K, stop = min(len, start + K);
-    double carry = ident;
-    for (int c = start; c < stop; c += 32) {  // prefix (forward) scan
-      const int idx = c + lane;
-      double x = idx < stop ? a[idx] : ident;
-      for (int off = 1; off < 32; off <<= 1) {
-        const double y = __shfl_up_sync(kFull, x, off);
-        if (lane >= off) x = pick<MAX>(x, y);
-      }
-      x = pick<MAX>(x, carry);
-      if (idx < stop) g[idx] = x;
-      carry = __shfl_sync(kFull, x, 31);
-    }
-    carry = ident;
-    for (int c = stop - 1; c >= start; c -= 32) {  // suffix (backward) scan
-      const int idx = c - lane;
-      double x = idx >= start ? a[idx] : ident;
-      for (int off = 1; off < 32; off <<= 1) {
-        const double y = __shfl_up_sync(kFull, x, off);
-        if (lane >= off) x = pick<MAX>(x, y);
-      }
-      x = pick<MAX>(x, carry);
-      if (idx >= start) h[idx] = x;
-      carry = __shfl_sync(kFull, x, 31);
-    }
+  for (int k = threadIdx.x; k < len; k += blockDim.x) {
+    const long long p = A + k;
+    buf0[k] = (p >= 0 && p < n) ? ref[p] : ident;
   }
+  __syncthreads();
+  const int K = 2 * r + 1;
+  int P = 1;
+  while (2 * P <= K) P *= 2;
+  double* src = buf0;
+  double* dst = buf1;
+  for (int s = 1; s < P; s *= 2) {  // M_{2s}[i] = max(M_s[i], M_s[i+s])
+    const int valid = len - 2 * s + 1;
+    for (int k = threadIdx.x; k < valid; k += blockDim.x) dst[k] = pick<MAX>(src[k], src[k + s]);
+    __syncthreads();
+    double* t = src;
+    src = dst;
+    dst = t;
+  }
+  for (int t = threadIdx.x; t < T; t += blockDim.x) {
+    if (P0 + t < n) out[P0 + t] = pick<MAX>(src[t], src[t + K - P]);
+  }
+  __syncthreads();
 }
 
-__global__ void __launch_bounds__(256) envelope_kernel(const double* __restrict__ ref, long long n,
+__global__ void __launch_bounds__(512) envelope_kernel(const double* __restrict__ ref, long long n,
                                                        int r, int T, double* __restrict__ up,
                                                        double* __restrict__ lo) {
   extern __shared__ double smem[];
-  const int K = 2 * r + 1;
   const int len = T + 2 * r;
-  double* a = smem;
-  double* g = a + len;
-  double* h = g + len;
-  const long long P = static_cast<long long>(blockIdx.x) * T;  // first output
-  const long long A = P - r;                                   // first input
-  for (int pass = 0; pass < 2; ++pass) {
-    const double ident = pass == 0 ? -d_inf() : d_inf();
-    for (int k = threadIdx.x; k < len; k += blockDim.x) {
-      const long long p = A + k;
-      a[k] = (p >= 0 && p < n) ? ref[p] : ident;
-    }
-    __syncthreads();
-    if (pass == 0) envelope_pass<true>(a, g, h, len, K);
-    else envelope_pass<false>(a, g, h, len, K);
-    __syncthreads();
-    double* out = pass == 0 ? up : lo;
-    for (int t = threadIdx.x; t < T; t += blockDim.x) {
-      if (P + t < n) {
-        out[P + t] = pass == 0 ? pick<true>(h[t], g[t + 2 * r]) : pick<false>(h[t], g[t + 2 * r]);
-      }
-    }
-    __syncthreads();
-  }
+  const long long P0 = static_cast<long long>(blockIdx.x) * T;  // first output
+  const long long A = P0 - r;                                   // first input
+  envelope_doubling<true>(ref, n, A, len, r, T, P0, smem, smem + len, up);
+  envelope_doubling<false>(ref, n, A, len, r, T, P0, smem, smem + len, lo);
 }
 
 static int envelope_tile(int r) {
-  // three arrays of (T + 2r) doubles within 96 KB
-  const int cap = (96 * 1024) / (3 * 8);
+  // two ping-pong arrays of (T + 2r) doubles within 64 KB (3 blocks per SM)
+  const int cap = (64 * 1024) / (2 * 8);
   int T = cap - 2 * r;
   if (T > 8192) T = 8192;
   return T;
@@ -240,12 +218,12 @@ cudaError_t launch_envelope(const double* ref, long long n, int r, double* up, d
                             cudaStream_t stream) {
   const int T = envelope_tile(r);
   if (T < 256) return cudaErrorInvalidValue;  // caller disables the EC tier
-  const size_t smem = 3 * static_cast<size_t>(T + 2 * r) * sizeof(double);
+  const size_t smem = 2 * static_cast<size_t>(T + 2 * r) * sizeof(double);
   cudaError_t e = cudaFuncSetAttribute(envelope_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   const long long blocks = (n + T - 1) / T;
-  envelope_kernel<<<static_cast<unsigned>(blocks), 256, smem, stream>>>(ref, n, r, T, up, lo);
+  envelope_kernel<<<static_cast<unsigned>(blocks), 512, smem, stream>>>(ref, n, r, T, up, lo);
   return cudaGetLastError();
 }
 
@@ -438,7 +416,8 @@ __global__ void __launch_bounds__(256, kSearchMinBlocks) search_kernel(SearchPar
     //   little later -- meanwhile it keeps producing.  Once every chunk has
     //   been published (chunks_done == nchunks) a future slot beyond the final
     //   tail is void.
-    const long long nchunks = (p.end - p.begin + 31) / 32;
+    const long long ncount = (p.end - p.begin + p.stride - 1) / p.stride;
+    const long long nchunks = (ncount + 31) / 32;
     bool chunks_left = true, flushed = false;
     long long myslot = -1;
     unsigned long long my_chunks = 0;
@@ -506,7 +485,7 @@ __global__ void __launch_bounds__(256, kSearchMinBlocks) search_kernel(SearchPar
           chunks_left = false;  // flush the stacks below, then retire
         } else {
           ++my_chunks;
-          const long long s = p.begin + static_cast<long long>(chunk) * 32 + lane;
+          const long long s = p.begin + (static_cast<long long>(chunk) * 32 + lane) * p.stride;
           const bool valid = s < p.end;
           c_cand += __popc(__ballot_sync(kFull, valid));
           bool alive = valid;
