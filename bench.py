@@ -35,6 +35,13 @@ CONFIGS = {
              "cfg4: N=1e8 ref, m=1024, w=205 (ratio 205/1024), LB cascade, shards 1/2/4/8"),
 }
 SEED_REF, SEED_QUERY = 20261019, 20261020
+# batch configs (no subsequence search): (npairs or (nq, nd), length, window)
+BATCH_CONFIGS = {
+    "cfg1": "cfg1: 1024 pairs of z-normalised N(0,1) random walks, L=256, w=25 (10%), "
+            "cutoff +inf and 1.05 x exact; pairwise EAPrunedDTW",
+    "cfg5": "cfg5: 1000 queries x 20000 database series, z-normalised N(0,1) random walks, "
+            "L=512, unbounded band, running cutoff per query; NN1",
+}
 FP64_OPS_PER_CELL = 5  # DSUB, DMUL, DADD + 2 DSETP (min3) per counted cell
 
 
@@ -161,18 +168,148 @@ def run_reference_arm(args, cfgname):
     return 0
 
 
+def run_batch(args):
+    """cfg1 (pairwise) and cfg5 (NN1) lines: pairs/s through the public batch API
+    with host buffers, the device-resident kernel time from CUDA events."""
+    import torch
+
+    import paper_2010_05371_b200 as g
+    from paper_2010_05371_b200 import _capi
+    import ctypes as C
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cfg = args.config
+    if cfg == "cfg1":
+        npairs, L, w = 1024, 256, 25
+        a = np.stack([g.znormalize(g.random_walk_normal(L, 1000 + p)) for p in range(npairs)])
+        b = np.stack([g.znormalize(g.random_walk_normal(L, 500000 + p)) for p in range(npairs)])
+        units = npairs
+        unit = "pairs/s"
+    else:
+        nq, nd, L = 1000, 20000, 512
+        rng = np.random.default_rng(SEED_REF)
+        qs = np.stack([g.znormalize(np.cumsum(rng.standard_normal(L))) for _ in range(nq)])
+        db = np.stack([g.znormalize(np.cumsum(rng.standard_normal(L))) for _ in range(nd)])
+        units = nq * nd
+        unit = "query-series pairs/s"
+    if args.impl == "reference":
+        import oracle
+        lib = oracle.Reference() if oracle.Reference.available() else None
+        threads = os.cpu_count() or 1
+        times = []
+        for k in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            if cfg == "cfg1":
+                exact, _ = lib.pairwise_threads(a, b, w, None, threads=threads)
+                lib.pairwise_threads(a, b, w, exact * 1.05, threads=threads)
+                n_units = 2 * npairs
+            else:
+                nqs = max(1, min(nq, threads * 2))  # bounded sample: a subset of queries
+                lib.nn1_threads(qs[:nqs], db, oracle.UNBOUNDED, threads=threads)
+                n_units = nqs * nd
+            if k >= args.warmup:
+                times.append(time.perf_counter() - t0)
+        v = n_units / statistics.mean(times)
+        line = {"impl": "reference", "metric": unit.replace("/s", " per second"), "value": v,
+                "unit": unit, "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": statistics.mean(times) * 1e3, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic z-normalised N(0,1) random walks",
+                "config": {"workload": BATCH_CONFIGS[cfg]},
+                "cpu_baseline": {"value": v, "unit": unit, "cores": threads, "kind": "reference",
+                                 "sample": "cfg1: all 1024 pairs x 2 cutoffs" if cfg == "cfg1"
+                                 else f"{nqs} of the 1000 queries vs the full database"},
+                "e2e": {"value": v, "unit": unit, "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return 0
+    ctx = g.Context(0)
+    times, dev_ms = [], []
+    for k in range(args.warmup + args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        if cfg == "cfg1":
+            exact, cells = g.pairwise(a, b, g.Band.cells(w), None, ctx=ctx)
+            out, cells2 = g.pairwise(a, b, g.Band.cells(w), exact * 1.05, ctx=ctx)
+            cells += cells2
+            n_units = 2 * npairs
+        else:
+            arg, dist, cells = g.nn1(qs, db, ctx=ctx)
+            n_units = units
+        torch.cuda.synchronize()
+        if k >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    e2e = n_units / statistics.mean(times)
+    # device-resident: inputs already in HBM, CUDA events around the kernels
+    if cfg == "cfg1":
+        da, dbb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+        dout = torch.empty(npairs, dtype=torch.float64, device="cuda")
+        ub = torch.from_numpy(exact * 1.05).cuda()
+        ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for k in range(args.warmup + args.steps):
+            if k == args.warmup:
+                e0.record()
+            for ubp in (None, ub):
+                _capi.check(_capi.lib.eapdtw_pairwise_dev(
+                    ctx.handle, C.c_void_p(da.data_ptr()), C.c_void_p(dbb.data_ptr()), npairs, L, w,
+                    C.c_void_p(ubp.data_ptr() if ubp is not None else 0), 1,
+                    C.c_void_p(dout.data_ptr()), None))
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / args.steps
+    else:
+        dq, ddb = torch.from_numpy(qs).cuda(), torch.from_numpy(db).cuda()
+        arg2 = np.empty(nq, dtype=np.uint64)
+        dist2 = np.empty(nq)
+        ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for k in range(args.warmup + args.steps):
+            if k == args.warmup:
+                e0.record()
+            _capi.check(_capi.lib.eapdtw_nn1_dev(
+                ctx.handle, C.c_void_p(dq.data_ptr()), nq, C.c_void_p(ddb.data_ptr()), nd, L,
+                _capi.UNBOUNDED_WINDOW, arg2.ctypes.data_as(C.POINTER(C.c_uint64)),
+                dist2.ctypes.data_as(C.POINTER(C.c_double)), None))
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / args.steps
+    value = n_units / (ms * 1e-3)
+    peak = ctx.fp64_peak()
+    achieved = FP64_OPS_PER_CELL * cells / (ms * 1e-3)
+    line = {"metric": unit.replace("/s", " per second"), "value": value, "unit": unit,
+            "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic z-normalised N(0,1) random walks",
+            "config": {"workload": BATCH_CONFIGS[cfg]},
+            "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak / 1e12,
+                         "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                         "kernel": "pairwise_kernel" if cfg == "cfg1" else "nn1_kernel"},
+            "e2e": {"value": e2e, "unit": unit,
+                    "h2d_bytes_per_step": int((a.nbytes + b.nbytes) * 2) if cfg == "cfg1"
+                    else int(qs.nbytes + db.nbytes),
+                    "d2h_bytes_per_step": int(npairs * 8 * 2) if cfg == "cfg1" else nq * 16},
+            "dtw_gcups_counted": cells / (ms * 1e-3) / 1e9, "cells_per_step": cells,
+            "gpu_launches": None}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg4", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="cfg4", choices=sorted(CONFIGS) + sorted(BATCH_CONFIGS))
     ap.add_argument("--batches", type=int, default=8, help="best-so-far exchanges per search (N>1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-segments", type=int, default=20,
                     help="cpu_baseline sample: this many 100000-candidate segments")
     args = ap.parse_args()
+    if args.config in BATCH_CONFIGS:
+        return run_batch(args)
     if args.impl == "reference":
         return run_reference_arm(args, args.config)
 

@@ -44,3 +44,17 @@ def reference_lib():
     if not oracle.Reference.available():
         pytest.skip("oracle/_ref not built (needs /root/reference at build time)")
     return oracle.Reference()
+
+
+@pytest.fixture(scope="session")
+def reference_lib_optional():
+    """The threaded reference when built (fast), else the C oracle."""
+    import oracle
+    if oracle.Reference.available():
+        ref = oracle.Reference()
+
+        class _R:
+            def nn1(self, q, db, w):
+                return ref.nn1_threads(q, db, w, threads=os.cpu_count() or 1)
+        return _R()
+    return oracle.Oracle()

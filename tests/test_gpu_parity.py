@@ -376,3 +376,16 @@ def test_engine_and_screen_variants(gpu, oracle_lib, monkeypatch, ad_k, screen, 
             rep = got.report
             assert rep.candidates_total == (rep.pruned_kim + rep.pruned_keogh_eq +
                                             rep.pruned_keogh_ec + rep.dtw_calls)
+
+
+def test_nn1_cfg5_database_scale(gpu, reference_lib_optional):
+    """cfg5 shape: the full 20000 x 512 database, unbounded band, a subset of
+    queries checked against the reference loop (running cutoff, lowest index)."""
+    from paper_2010_05371_b200 import znormalize
+    rng = np.random.default_rng(55)
+    db = np.stack([znormalize(np.cumsum(rng.standard_normal(512))) for _ in range(20000)])
+    qs = np.stack([znormalize(np.cumsum(rng.standard_normal(512))) for _ in range(6)])
+    arg, dist, _ = gpu.nn1(qs, db)
+    warg, wdist, _ = reference_lib_optional.nn1(qs, db, UNB)
+    assert [int(x) for x in arg] == [int(x) for x in warg]
+    assert np.array_equal(dist, wdist)
