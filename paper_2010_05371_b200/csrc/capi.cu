@@ -143,7 +143,7 @@ struct eapdtw_search_plan {
   size_t ncand = 0;
   cudaEvent_t ev[8] = {};
   bool prepared = false, ran = false;
-  int blocks = 0, warps = 8, ad_k = 0, screen_rows = 16, coarse_stride = 64;
+  int blocks = 0, warps = 8, ad_k = 0, screen_rows = 16, coarse_stride = 64, lb_head = kLbHead;
   double guard_rel = 1e-9, guard_abs = 1e-20;
   std::chrono::steady_clock::time_point t0;
 };
@@ -402,6 +402,7 @@ static int plan_init(eapdtw_search_plan* p, eapdtw_ctx* c, const double* ref_dev
   // opt-in here (EAPDTW_AD_K) and the default for pairwise / NN1 batches.
   p->ad_k = getenv("EAPDTW_AD_K") ? choose_ad_k(static_cast<int>(m), p->w_eff) : 0;
   if (const char* env = getenv("EAPDTW_SCREEN_ROWS")) p->screen_rows = std::max(0, atoi(env));
+  if (const char* env = getenv("EAPDTW_LB_HEAD")) p->lb_head = std::max(8, atoi(env));
   if (const char* env = getenv("EAPDTW_COARSE_STRIDE")) p->coarse_stride = std::max(0, atoi(env));
   p->guard_abs = 1e-20;
 
@@ -579,6 +580,7 @@ static SearchParams base_params(eapdtw_search_plan* p) {
   s.ad_k = p->ad_k;
   s.direct = 0;
   s.screen_rows = p->screen_rows;
+  s.lb_head = p->lb_head;
   s.counters = B.counters.as<unsigned long long>();
   s.index_offset = static_cast<long long>(p->offset);
   return s;

@@ -141,19 +141,21 @@ __device__ double warp_dtw(const RawFn& rowraw, const NormFn& rownorm, int lr,
     const double* qp = qsp + j;
     double* rp = rowbuf + j;
     double v = INF;
-    bool fin = !active;
-    int jf = fin ? j - 1 : lc + 1;  // last column computed before finishing
-    unsigned finmask = __ballot_sync(kFull, fin);
+    // Finished lanes as a warp-uniform bit mask F (bit L = lane L).  Lane L
+    // is finished once its cell is dead and its upstream row (lane L-1; for
+    // lane 0 the row buffer, dead beyond column hi) was finished one step
+    // earlier -- every later cell of the row is then dead -- or once it is
+    // past its band.  Per step only the dead/alive ballot is per-lane; the
+    // chain  F |= D & (F << 1 | lane-0 bit)  is uniform bit arithmetic, and
+    // the past-band test runs once per 4 steps (a lane past its band is
+    // noticed up to 3 columns late: cells computed exactly anyway).
+    unsigned finmask = __ballot_sync(kFull, !active);
+    int jf = active ? lc + 1 : j - 1;  // last column computed before finishing
     const bool writer = lane == wl;
     const bool is0 = lane == 0;
-
-    // Per-lane constants of the step: band range test on jr = j - bl, the
-    // finish test jr > span, the upstream-finished bit (lane 0's upstream is
-    // the row buffer: finished once j > hi, folded into bit 31, which no
-    // other lane reads).
     const unsigned span = static_cast<unsigned>(bh - bl);
     int jr = j - bl;
-    const unsigned upbit = is0 ? 0x80000000u : (1u << (lane - 1));
+    int j0 = jb;  // lane 0's column (warp-uniform)
 
     // One wavefront step at column j+u.
     auto step = [&](int u) {
@@ -162,32 +164,32 @@ __device__ double warp_dtw(const RawFn& rowraw, const NormFn& rownorm, int lr,
       const double diag = top_prev;
       top_prev = top;
       double nv = __dadd_rn(sq_cost(c, qp[u]), dmin2(v, dmin2(top, diag)));
-      const int jru = jr + u;
-      nv = static_cast<unsigned>(jru) <= span ? nv : INF;
-      bool live;
+      nv = static_cast<unsigned>(jr + u) <= span ? nv : INF;
+      bool dead;
       if (KILL) {
-        live = nv <= ub;
-        nv = live ? nv : INF;
+        dead = !(nv <= ub);
+        nv = dead ? INF : nv;
       } else {
-        live = __double2hiint(nv) <= ub_hi;  // nv >= 0: superset of nv <= ub
+        dead = __double2hiint(nv) > ub_hi;  // nv >= 0: live is a superset of nv <= ub
       }
       if (writer) rp[u] = nv;
       v = nv;
-      const unsigned up = (finmask & 0x7fffffffu) | (j + u > hi ? 0x80000000u : 0u);
-      const bool nf = fin || jru > static_cast<int>(span) || ((up & upbit) && !live);
-      jf = (!fin && nf) ? j + u : jf;
-      fin = nf;
-      finmask = __ballot_sync(kFull, fin);
+      const unsigned dm = __ballot_sync(kFull, dead);
+      finmask |= dm & ((finmask << 1) | (j0 + u > hi ? 1u : 0u));
     };
 
     for (;;) {
+      const unsigned before = finmask;
       step(0);
       step(1);
       step(2);
       step(3);
+      finmask |= __ballot_sync(kFull, jr + 3 > static_cast<int>(span));
+      if (((finmask & ~before) >> lane) & 1u) jf = j + 3;
       if (finmask == kFull) break;
       j += 4;
       jr += 4;
+      j0 += 4;
       qp += 4;
       rp += 4;
     }

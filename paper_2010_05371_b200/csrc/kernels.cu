@@ -263,7 +263,8 @@ static __host__ __device__ inline size_t padded_len(int m, int ad_k) {
 size_t search_smem_bytes(int m, int warps, int ad_k) {
   return padded_len(m, ad_k) * 8                        // q (padded, 1-based)
          + static_cast<size_t>(warps) * padded_len(m, ad_k) * 8  // per-warp DP buffers
-         + static_cast<size_t>(warps) * 3 * kStack * 4  // per-warp tier stacks
+         + static_cast<size_t>(warps) * 5 * kStack * 4  // per-warp tier stacks
+         + static_cast<size_t>(warps) * 2 * kStack * 8  // continuation partial sums
          + 64;
 }
 
@@ -425,16 +426,40 @@ __global__ void __launch_bounds__(256, kSearchMinBlocks) search_kernel(SearchPar
     // Kim survivors -> [A] -> EQ -> [B] -> EC -> [C] -> phase-A screen -> queue.
     // A tier runs only on a full warp of candidates (or when flushing), so
     // lanes stay busy although each tier discards most of its input.
-    int* stkA = stacks + warp * (3 * kStack);
+    int* stkA = stacks + warp * (5 * kStack);
     int* stkB = stkA + kStack;
     int* stkC = stkB + kStack;
-    int nA = 0, nB = 0, nC = 0;
+    int* stkA2 = stkC + kStack;  // EQ continuations (candidate, partial sum)
+    int* stkB2 = stkA2 + kStack; // EC continuations
+    double* accA2 = reinterpret_cast<double*>(stacks + (blockDim.x >> 5) * (5 * kStack)) +
+                    warp * (2 * kStack);
+    double* accB2 = accA2 + kStack;
+    int nA = 0, nB = 0, nC = 0, nA2 = 0, nB2 = 0;
 
     auto push = [&](int* stk, int& n, bool keep, long long cand) {
       const unsigned mask = __ballot_sync(kFull, keep);
       if (keep) stk[n + __popc(mask & ((1u << lane) - 1u))] = static_cast<int>(cand - p.begin);
       n += __popc(mask);
       __syncwarp();
+    };
+    auto push2 = [&](int* stk, double* acs, int& n, bool keep, long long cand, double acc) {
+      const unsigned mask = __ballot_sync(kFull, keep);
+      if (keep) {
+        const int at = n + __popc(mask & ((1u << lane) - 1u));
+        stk[at] = static_cast<int>(cand - p.begin);
+        acs[at] = acc;
+      }
+      n += __popc(mask);
+      __syncwarp();
+    };
+    auto pop2 = [&](int* stk, double* acs, int& n, long long& cand, double& acc) -> bool {
+      const int take = min(32, n);
+      const bool ok = lane < take;
+      cand = ok ? p.begin + stk[n - take + lane] : p.begin;
+      acc = ok ? acs[n - take + lane] : 0.0;
+      __syncwarp();
+      n -= take;
+      return ok;
     };
     // Pop up to 32 entries: lane L gets entry n-take+L (valid iff L < take).
     auto pop = [&](int* stk, int& n, long long& cand) -> bool {
@@ -507,49 +532,20 @@ __global__ void __launch_bounds__(256, kSearchMinBlocks) search_kernel(SearchPar
       }
       const bool flush = !chunks_left;
 
-      // Two-phase early-abandoning LB_Keogh (lower_bounds.cpp:57-88): phase 1
-      // runs lane per candidate over the first kLbHead positions of order[]
-      // (the largest |q|, where nearly all prunes happen); each candidate
-      // still pending is then re-summed by the whole warp over ALL m positions
-      // in natural order (coalesced, 32 per step, a warp sum and abandon test
-      // every 128), so a survivor costs m/32 warp steps instead of holding 31
-      // idle lanes for m steps.  The bound is only gating, so the summation
-      // order is free (the guard covers the rounding).
-      auto lb_tier = [&](long long s, bool pending, const double mean, const double rsd,
-                         double ubg, auto term) -> bool {
+      // Early-abandoning LB_Keogh over order[k0, k1) (lower_bounds.cpp:57-88),
+      // lane per candidate, continuing the partial sum `acc`; the vote every 8
+      // positions lets the warp stop once every lane has abandoned.
+      auto lb_range = [&](long long s, bool pending, const double mean, const double rsd,
+                          double ubg, auto term, int k0, int k1, double& acc) -> bool {
         bool alive = pending;
-        double acc = 0.0;
-        const int head = min(m, kLbHead);
-        for (int k0 = 0; k0 < head; k0 += 8) {
-          const int kend = min(head, k0 + 8);
-          for (int k = k0; k < kend; ++k) acc += term(pending, s, order[k], mean, rsd);
+        for (int kb = k0; kb < k1; kb += 8) {
+          const int kend = min(k1, kb + 8);
+          for (int k = kb; k < kend; ++k) acc += term(pending, s, order[k], mean, rsd);
           if (pending && acc > ubg) {
             pending = false;
             alive = false;
           }
           if (!__any_sync(kFull, pending)) break;
-        }
-        if (head >= m) return alive;
-        unsigned pend = __ballot_sync(kFull, pending);
-        while (pend) {
-          const int l = __ffs(pend) - 1;
-          pend &= pend - 1;
-          const long long sl = __shfl_sync(kFull, s, l);
-          const double ml = __shfl_sync(kFull, mean, l);
-          const double rl = __shfl_sync(kFull, rsd, l);
-          double part = 0.0;
-          bool abandoned = false;
-          for (int k0 = 0; k0 < m; k0 += 128) {
-            const int kend = min(m, k0 + 128);
-            for (int j = k0 + lane; j < kend; j += 32) part += term(true, sl, j, ml, rl);
-            double tot = part;
-            for (int off = 16; off > 0; off >>= 1) tot += __shfl_xor_sync(kFull, tot, off);
-            if (tot > ubg) {
-              abandoned = true;
-              break;
-            }
-          }
-          if (lane == l && abandoned) alive = false;
         }
         return alive;
       };
@@ -576,37 +572,33 @@ __global__ void __launch_bounds__(256, kSearchMinBlocks) search_kernel(SearchPar
         return dd * dd;
       };
 
-      // ---- tier 2: LB_Keogh EQ (search.cpp:92); prune iff lb > ub*(1+g_rel) + g_abs.
-      while (nA >= 32 || (flush && nA > 0)) {
+      // ---- tiers 2/3: LB_Keogh EQ (search.cpp:92) then EC (search.cpp:97-99),
+      //      prune iff lb > ub*(1+g_rel) + g_abs.  Each tier runs in two legs:
+      //      the first kLbHead positions of order[] (largest |q|: most prunes
+      //      happen there) for a full warp, then the candidates still pending
+      //      are re-gathered into full warps with their partial sums and
+      //      finish the remaining positions -- so a warp's length is set by
+      //      its slowest lane only among candidates that got that far.
+      const int head = min(m, p.lb_head);
+      auto stage = [&](int* in, int& nin, int* cont, double* cacc, int& ncont, int* out,
+                       int& nout, auto term, unsigned long long& pruned, bool leg2) {
         long long s;
-        const bool pending = pop(stkA, nA, s);
+        double acc = 0.0;
+        const bool pending = leg2 ? pop2(cont, cacc, ncont, s, acc) : pop(in, nin, s);
         const double mean = p.mean[s];
         const double sd = p.sd[s];
         const double rsd = sd < kMinStddev ? 0.0 : __drcp_rn(sd);
         const double ubg = load_ub(p.ub_key) * (1.0 + p.guard_rel) + p.guard_abs;
-        const bool alive = lb_tier(s, pending, mean, rsd, ubg, eq_term);
-        if (pending && !alive) ++c_eq;
-        if (p.env_up != nullptr) push(stkB, nB, alive, s);
-        else push(stkC, nC, alive, s);
-      }
-
-      // ---- tier 3: LB_Keogh EC (search.cpp:97-99).
-      while (nB >= 32 || (flush && nB > 0)) {
-        long long s;
-        const bool pending = pop(stkB, nB, s);
-        const double mean = p.mean[s];
-        const double sd = p.sd[s];
-        const double rsd = sd < kMinStddev ? 0.0 : __drcp_rn(sd);
-        const double ubg = load_ub(p.ub_key) * (1.0 + p.guard_rel) + p.guard_abs;
-        const bool alive = lb_tier(s, pending, mean, rsd, ubg, ec_term);
-        if (pending && !alive) ++c_ec;
-        push(stkC, nC, alive, s);
-      }
-
+        const bool alive = leg2 ? lb_range(s, pending, mean, rsd, ubg, term, head, m, acc)
+                                : lb_range(s, pending, mean, rsd, ubg, term, 0, head, acc);
+        if (pending && !alive) ++pruned;
+        if (!leg2 && head < m) push2(cont, cacc, ncont, alive, s, acc);
+        else push(out, nout, alive, s);
+      };
       // ---- phase A: the first screen_rows DTW rows, lane per candidate (an
       //      exact EAPrunedDTW prefix; a killed candidate is an abandoned
       //      DTW), then publish the survivors to the queue.
-      while (nC >= 32 || (flush && nC > 0)) {
+      auto screen_stage = [&]() {
         long long s;
         bool alive = pop(stkC, nC, s);
         if (p.screen_rows > 0) {
@@ -635,6 +627,28 @@ __global__ void __launch_bounds__(256, kSearchMinBlocks) search_kernel(SearchPar
             const unsigned rank = __popc(mask & ((1u << lane) - 1u));
             reinterpret_cast<volatile long long*>(p.queue)[qb + rank] = s;
           }
+        }
+      };
+
+      int* eq_out = p.env_up != nullptr ? stkB : stkC;
+      int& eq_nout = p.env_up != nullptr ? nB : nC;
+      // Most downstream ready stage first, so every push lands in a stack
+      // holding < 32 entries (capacity kStack = 64); a partial warp runs only
+      // when flushing and once everything upstream has drained.
+      for (;;) {
+        const bool up_a = (nA | nA2) == 0, up_b = up_a && nB == 0, up_c = up_b && nB2 == 0;
+        if (nC >= 32 || (flush && nC > 0 && up_c)) {
+          screen_stage();
+        } else if (nB2 >= 32 || (flush && nB2 > 0 && up_b)) {
+          stage(stkB, nB, stkB2, accB2, nB2, stkC, nC, ec_term, c_ec, true);
+        } else if (nB >= 32 || (flush && nB > 0 && up_a)) {
+          stage(stkB, nB, stkB2, accB2, nB2, stkC, nC, ec_term, c_ec, false);
+        } else if (nA2 >= 32 || (flush && nA2 > 0 && nA == 0)) {
+          stage(stkA, nA, stkA2, accA2, nA2, eq_out, eq_nout, eq_term, c_eq, true);
+        } else if (nA >= 32 || (flush && nA > 0)) {
+          stage(stkA, nA, stkA2, accA2, nA2, eq_out, eq_nout, eq_term, c_eq, false);
+        } else {
+          break;
         }
       }
 

@@ -12,7 +12,7 @@ constexpr long long kStatsResetInterval = 100000;  // search.cpp:16
 constexpr double kMinStddev = 1e-12;               // search.cpp:13
 constexpr int kScreenSlots = 24;                   // phase-A window (band offsets)
 constexpr int kStack = 64;                         // per-warp tier stack capacity
-constexpr int kLbHead = 1 << 30;                   // lane-parallel prefix of the Keogh tiers (all: the warp-cooperative tail measured slower)
+constexpr int kLbHead = 256;                       // first leg of the Keogh tiers (positions of order[])
 
 // Tier counters accumulated on the device (SearchReport, search.hpp:68-77).
 enum Counter : int {
@@ -55,6 +55,7 @@ struct SearchParams {
   int ad_k;                      // anti-diagonal engine window 64*ad_k (0: strip engine only)
   int direct;                    // 1: every candidate is a DTW task (the probe)
   int screen_rows;               // phase-A lane screen depth (0: off)
+  int lb_head;                   // first leg of the Keogh tiers (positions of order[])
   unsigned long long* counters;  // kNumCounters
   long long index_offset;        // shard start in the global reference
 };
