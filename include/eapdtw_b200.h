@@ -47,7 +47,7 @@ typedef struct {
   double window_ratio; /* window_cells = floor(window_ratio * m) (search.cpp:18-21) */
   int32_t algorithm;   /* EAPDTW_ALGO_* */
   int32_t use_lower_bounds;
-  int32_t tighten_ub;  /* accepted; the GPU path's pruning is already exact */
+  int32_t tighten_ub;  /* per-row cumulative-bound thresholds (search.cpp:101-113); results unchanged */
   int32_t reserved_;
 } eapdtw_search_config;
 

@@ -137,7 +137,8 @@ struct eapdtw_search_plan {
   size_t n = 0, m = 0, w_cells = 0;
   int w_eff = 0;
   int env_r = 0;
-  bool use_lb = true, have_env = false;
+  bool use_lb = true, have_env = false, tighten = true;
+  int cb_strip = 2;
   int algo = EAPDTW_ALGO_EA_PRUNED;
   uint64_t offset = 0;
   size_t ncand = 0;
@@ -388,6 +389,10 @@ static int plan_init(eapdtw_search_plan* p, eapdtw_ctx* c, const double* ref_dev
   p->m = m;
   p->offset = offset;
   p->use_lb = cfg->use_lower_bounds != 0;
+  // tighten_ub is consulted only with the cascade and EAPrunedDTW (search.cpp:101-105, 191)
+  p->tighten = p->use_lb && cfg->tighten_ub != 0 && cfg->algorithm == EAPDTW_ALGO_EA_PRUNED;
+  if (const char* env = getenv("EAPDTW_TIGHTEN")) p->tighten = p->tighten && atoi(env) != 0;
+  if (const char* env = getenv("EAPDTW_CB_STRIP")) p->cb_strip = std::max(1, atoi(env));
   p->algo = cfg->algorithm;
   p->ncand = n - m + 1;
   // window_cells_for (search.cpp:18-21)
@@ -565,6 +570,8 @@ static SearchParams base_params(eapdtw_search_plan* p) {
   s.m = static_cast<int>(p->m);
   s.w = p->w_eff;
   s.use_lb = p->use_lb ? 1 : 0;
+  s.tighten = p->tighten ? 1 : 0;
+  s.cb_strip = p->cb_strip;
   s.prune = p->algo == EAPDTW_ALGO_FULL ? 0 : 1;
   s.guard_rel = p->guard_rel;
   s.guard_abs = p->guard_abs;
@@ -617,6 +624,7 @@ int eapdtw_search_plan_prepare(eapdtw_search_plan* p) {
   const size_t nprobe = std::min<size_t>(2048, std::max<size_t>(1, p->ncand / 64));
   SearchParams sp = base_params(p);
   sp.use_lb = 0;
+  sp.tighten = 0;
   sp.begin = 0;
   sp.stride = static_cast<long long>(std::max<size_t>(1, p->ncand / nprobe));
   sp.end = std::min<long long>(static_cast<long long>(p->ncand),

@@ -94,7 +94,8 @@ __device__ __forceinline__ double load_ub(const unsigned long long* key) {
 //   qsp        : padded column series (see contract above)
 //   w          : effective half window (effective_window, dtw.cpp:57-62)
 //   get_ub()   : current threshold (warp-uniform); read one strip ahead
-//   rowthr(u,i): per-row threshold given the strip ub (identity without a cb)
+//   rowthr(u,i,i0): row i's threshold given the strip ub (identity without a cb);
+//                 called once per strip by every lane (i0: the strip's first row)
 //   rowbuf     : padded per-warp scratch (see contract above)
 //   cells      : incremented (by lane 0) with the number of evaluated cells
 template <bool KILL, class RawFn, class NormFn, class UbFn, class RowThrFn>
@@ -126,7 +127,7 @@ __device__ double warp_dtw(const RawFn& rowraw, const NormFn& rownorm, int lr,
     }
     // Clamp to the largest finite double so an infinite threshold never
     // makes an unreachable (+inf) cell "live".
-    const double ub = fmin(rowthr(ub_strip, i), DBL_MAX);
+    const double ub = fmin(rowthr(ub_strip, i, i0), DBL_MAX);
     const int wl = min(31, lr - i0);  // writer lane: the last row of the strip
     ub_last = __shfl_sync(kFull, ub, wl);
     const int ub_hi = __double2hiint(ub);

@@ -380,7 +380,99 @@ __global__ void __launch_bounds__(256, kSearchMinBlocks) search_kernel(SearchPar
       return cconst ? 0.0 : __ddiv_rn(__dsub_rn(x, cm), cs);
     };
     auto get_ub = [&]() -> double { return prune ? load_ub(p.ub_key) : INF; };
-    auto rowthr = [](double u, int) -> double { return u; };
+    // tighten_ub (search.cpp:101-113, dtw.cpp:81-86): row i's threshold is
+    // ub - cb(k), k = min(i+w, m) - 1, cb(k) a lower bound on the cost of the
+    // positions past k that every path still has to visit.  Here cb is the
+    // larger of the EQ (per row) and EC (per column) Keogh suffix sums, each
+    // total - prefix(k).  Lazily: only a DTW still running at strip
+    // `cb_strip` pays for the totals (one coalesced pass); each strip then
+    // extends the prefix by the 32 positions its rows need (one scan).
+    // The contributions use the cascade's reciprocal normalisation: cb is
+    // lowered by an absolute guard covering that and by guard_rel * total
+    // for the summation; guard_rel also covers the rounding of the rest of
+    // the path.  Liveness only (the strip engine never kills values): the
+    // result is still the exact DTW value whenever that is <= ub.
+    const bool tight = p.tighten != 0;
+    const double rsd = cconst ? 0.0 : __drcp_rn(cs);
+    const bool have_ec = p.env_up != nullptr;
+    // EQ / EC contribution of position k (0 past the end)
+    auto contrib = [&](int k, double& ceq, double& cec, double& mag) {
+      ceq = 0.0;
+      cec = 0.0;
+      if (k >= m) return;
+      const double c = __dmul_rn(__dsub_rn(crow[k], cm), rsd);
+      const double e1 = __dsub_rn(c, qu[k]), e2 = __dsub_rn(ql[k], c);
+      const double d1 = e1 > 0.0 ? e1 : (e2 > 0.0 ? e2 : 0.0);
+      ceq = __dmul_rn(d1, d1);
+      mag = fmax(mag, fabs(c));
+      if (have_ec) {
+        const double U = __dmul_rn(__dsub_rn(p.env_up[cand + k], cm), rsd);
+        const double L = __dmul_rn(__dsub_rn(p.env_lo[cand + k], cm), rsd);
+        const double qk = qsp[k + 1];
+        const double f1 = __dsub_rn(qk, U), f2 = __dsub_rn(L, qk);
+        const double d2 = f1 > 0.0 ? f1 : (f2 > 0.0 ? f2 : 0.0);
+        cec = __dmul_rn(d2, d2);
+        mag = fmax(mag, fmax(fabs(U), fabs(L)));
+      }
+    };
+    bool cb_ready = false;
+    double tot_eq = 0.0, tot_ec = 0.0, pre_eq = 0.0, pre_ec = 0.0, cb_guard = 0.0;
+    int pre_end = 0;  // prefix sums cover positions [0, pre_end)
+    auto rowthr = [&](double u, int i, int i0) -> double {
+      if (!tight || i0 < 1 + 32 * (p.cb_strip - 1)) return u;
+      if (!cb_ready) {
+        pre_end = min(m, i0 + p.w - 1);
+        double mag = 1.0;
+        for (int k = lane; k < m; k += 32) {
+          double a, b;
+          contrib(k, a, b, mag);
+          tot_eq = __dadd_rn(tot_eq, a);
+          tot_ec = __dadd_rn(tot_ec, b);
+          if (k < pre_end) {
+            pre_eq = __dadd_rn(pre_eq, a);
+            pre_ec = __dadd_rn(pre_ec, b);
+          }
+        }
+        for (int off = 16; off > 0; off >>= 1) {
+          tot_eq = __dadd_rn(tot_eq, __shfl_xor_sync(kFull, tot_eq, off));
+          tot_ec = __dadd_rn(tot_ec, __shfl_xor_sync(kFull, tot_ec, off));
+          pre_eq = __dadd_rn(pre_eq, __shfl_xor_sync(kFull, pre_eq, off));
+          pre_ec = __dadd_rn(pre_ec, __shfl_xor_sync(kFull, pre_ec, off));
+          mag = fmax(mag, __shfl_xor_sync(kFull, mag, off));
+        }
+        // |c|, |U|, |L| are within 3 ulp of the division-normalised values
+        // (each term off by < 28 mag^2 ulp(1)); sums of <= 2m terms
+        cb_guard = 32.0 * static_cast<double>(m) * mag * mag * 0x1.0p-52 +
+                   p.guard_rel * fmax(tot_eq, tot_ec);
+        cb_ready = true;
+      }
+      // this strip's rows need prefixes through k = i0 + lane + w - 1
+      const int kk = i0 + lane + p.w - 1;
+      double a = 0.0, b = 0.0, unused = 1.0;
+      if (kk >= pre_end && kk < m) contrib(kk, a, b, unused);
+      for (int off = 1; off < 32; off <<= 1) {  // inclusive prefix scan
+        const double x = __shfl_up_sync(kFull, a, off);
+        const double y = __shfl_up_sync(kFull, b, off);
+        if (lane >= off) {
+          a = __dadd_rn(a, x);
+          b = __dadd_rn(b, y);
+        }
+      }
+      const double peq = __dadd_rn(pre_eq, a), pec = __dadd_rn(pre_ec, b);
+      // the next strip starts where this one's rows end
+      const int nxt = min(m, i0 + 32 + p.w - 1);
+      if (nxt > pre_end) {
+        const int src = min(31, nxt - 1 - (i0 + p.w - 1));
+        pre_eq = __shfl_sync(kFull, peq, src);
+        pre_ec = __shfl_sync(kFull, pec, src);
+        pre_end = nxt;
+      }
+      if (kk >= m - 1) return u;  // nothing left past k
+      const double cbv = __dsub_rn(fmax(__dsub_rn(tot_eq, peq), __dsub_rn(tot_ec, pec)), cb_guard);
+      if (!(cbv > 0.0)) return u;
+      const double t = __dsub_rn(__dmul_rn(u, 1.0 + p.guard_rel), cbv);
+      return t > 0.0 ? t : 0.0;
+    };
     const double d = dtw_dispatch<false>(AD_K, rowraw, rownorm, m, qsp, m, p.w, get_ub, rowthr,
                                          rowbuf, c_cells, c_ovf);
     ++c_calls;
@@ -740,7 +832,7 @@ __global__ void __launch_bounds__(256) pairwise_kernel(PairParams p) {
     const double* cb = WITH_CB ? p.cb + pr * p.lr : nullptr;
     const int lr = p.lr, w = p.w;
     // row_threshold (dtw.cpp:81-86): ub - cb[min(i+w, lr) - 1], clamped at 0.
-    auto rowthr = [&](double u, int i) -> double {
+    auto rowthr = [&](double u, int i, int) -> double {
       if (!WITH_CB || i > lr) return u;
       const int k = min(i + w, lr);
       const double t = __dsub_rn(u, cb[k - 1]);
@@ -820,7 +912,7 @@ __global__ void __launch_bounds__(256) nn1_kernel(Nn1Params p) {
     auto rowraw = [&](int r) -> double { return row[r]; };
     auto rownorm = [](double x) -> double { return x; };
     auto get_ub = [&]() -> double { return load_ub(key); };
-    auto rowthr = [](double u, int) -> double { return u; };
+    auto rowthr = [](double u, int, int) -> double { return u; };
     const double d = dtw_dispatch<false>(p.ad_k, rowraw, rownorm, L, qsp, L, p.w, get_ub, rowthr,
                                          rowbuf, cells, ovf);
     ++calls;

@@ -42,6 +42,8 @@ struct SearchParams {
   long long begin, end, stride;  // candidates begin, begin+stride, ... < end
   int m, w;                      // query length, effective half window
   int use_lb;                    // Kim -> Keogh EQ -> Keogh EC cascade
+  int tighten;                   // per-row thresholds from the Keogh cumulative bound (search.cpp:101-105)
+  int cb_strip;                  // first strip (1-based) that uses them
   int prune;                     // 0: Algo::full (no pruning), 1: pruned DTW
   double guard_rel, guard_abs;   // LB soundness guard
   unsigned long long* ub_key;    // running threshold key (order-preserving bits)
