@@ -108,11 +108,11 @@ bool all_finite(const double* x, size_t n) {
 }  // namespace
 
 struct PlanBuffers {
-  DevBuf mean, sd, up, lo, q, qu, ql, order, best, key, work, counters, probe_counters, flag, queue,
-      qctr;
+  DevBuf mean, sd, env, q, qul, qperm, order, best, key, work, counters, probe_counters, flag,
+      queue, qtot, qctr;
   void release() {
-    for (DevBuf* b : {&mean, &sd, &up, &lo, &q, &qu, &ql, &order, &best, &key, &work, &counters,
-                      &probe_counters, &flag, &queue, &qctr})
+    for (DevBuf* b : {&mean, &sd, &env, &q, &qul, &qperm, &order, &best, &key, &work, &counters,
+                      &probe_counters, &flag, &queue, &qtot, &qctr})
       b->release();
   }
 };
@@ -138,14 +138,18 @@ struct eapdtw_search_plan {
   int w_eff = 0;
   int env_r = 0;
   bool use_lb = true, have_env = false, tighten = true;
-  int cb_strip = 2;
+  int cb_strip = 1;
   int algo = EAPDTW_ALGO_EA_PRUNED;
   uint64_t offset = 0;
   size_t ncand = 0;
   cudaEvent_t ev[8] = {};
   bool prepared = false, ran = false;
-  int blocks = 0, warps = 8, ad_k = 0, screen_rows = 16, coarse_stride = 64, lb_head = kLbHead;
+  int blocks = 0, warps = 8, ad_k = 0, screen_rows = 16;
+  std::vector<int> coarse_strides{64};  // coarse passes, in order
+  bool coarse_blocks = false;           // coarse pass over runs of adjacent candidates
+  int probe = 2048;
   double guard_rel = 1e-9, guard_abs = 1e-20;
+  double qmax = 0.0;  // max |normalised query|
   std::chrono::steady_clock::time_point t0;
 };
 
@@ -407,8 +411,17 @@ static int plan_init(eapdtw_search_plan* p, eapdtw_ctx* c, const double* ref_dev
   // opt-in here (EAPDTW_AD_K) and the default for pairwise / NN1 batches.
   p->ad_k = getenv("EAPDTW_AD_K") ? choose_ad_k(static_cast<int>(m), p->w_eff) : 0;
   if (const char* env = getenv("EAPDTW_SCREEN_ROWS")) p->screen_rows = std::max(0, atoi(env));
-  if (const char* env = getenv("EAPDTW_LB_HEAD")) p->lb_head = std::max(8, atoi(env));
-  if (const char* env = getenv("EAPDTW_COARSE_STRIDE")) p->coarse_stride = std::max(0, atoi(env));
+  if (const char* env = getenv("EAPDTW_COARSE_STRIDE")) {  // e.g. "512,64" or "512:64"; "0": none
+    p->coarse_strides.clear();
+    for (const char* t = env; *t;) {
+      const int v = atoi(t);
+      if (v > 1) p->coarse_strides.push_back(v);
+      while (*t && *t != ',' && *t != ':') ++t;
+      if (*t) ++t;
+    }
+  }
+  if (const char* env = getenv("EAPDTW_PROBE")) p->probe = std::max(1, atoi(env));
+  if (const char* env = getenv("EAPDTW_COARSE_BLOCKS")) p->coarse_blocks = atoi(env) != 0;
   p->guard_abs = 1e-20;
 
   // Query preparation exactly as search.cpp:136-149.
@@ -433,14 +446,24 @@ static int plan_init(eapdtw_search_plan* p, eapdtw_ctx* c, const double* ref_dev
     return fa != fb ? fa > fb : a < b;
   });
   std::copy(qn.begin(), qn.end(), q1.begin() + 1);
+  // (upper, lower) per position, and the same in visiting order
+  std::vector<double> qul(2 * m), qperm(2 * m);
+  for (size_t j = 0; j < m; ++j) {
+    qul[2 * j] = qu[j];
+    qul[2 * j + 1] = ql[j];
+    qperm[2 * j] = qu[order[j]];
+    qperm[2 * j + 1] = ql[order[j]];
+  }
+  p->qmax = 0.0;
+  for (const double v : qn) p->qmax = std::max(p->qmax, std::fabs(v));
 
   PlanBuffers& B = *p->buf;
   const size_t nc = p->ncand;
   CUDA_TRY(B.mean.ensure(nc * 8));
   CUDA_TRY(B.sd.ensure(nc * 8));
   CUDA_TRY(B.q.ensure((m + 1) * 8));
-  CUDA_TRY(B.qu.ensure(m * 8));
-  CUDA_TRY(B.ql.ensure(m * 8));
+  CUDA_TRY(B.qul.ensure(m * 16));
+  CUDA_TRY(B.qperm.ensure(m * 16));
   CUDA_TRY(B.order.ensure(m * 4));
   CUDA_TRY(B.best.ensure(sizeof(BestRecord)));
   CUDA_TRY(B.key.ensure(8));
@@ -448,20 +471,20 @@ static int plan_init(eapdtw_search_plan* p, eapdtw_ctx* c, const double* ref_dev
   // One spare slot per resident warp: a consumer may hold a "future" slot past
   // the final tail, which must read as empty (-1) rather than stale data.
   CUDA_TRY(B.queue.ensure((nc + kQueueSlack) * 8));
+  CUDA_TRY(B.qtot.ensure((nc + kQueueSlack) * 8));
   CUDA_TRY(B.qctr.ensure(24));
   CUDA_TRY(B.flag.ensure(8));
   CUDA_TRY(B.counters.ensure(kNumCounters * 8));
   CUDA_TRY(B.probe_counters.ensure(kNumCounters * 8));
   if (p->use_lb) {
-    CUDA_TRY(B.up.ensure(n * 8));
-    CUDA_TRY(B.lo.ensure(n * 8));
+    CUDA_TRY(B.env.ensure(n * 16));
   }
   p->key = B.key.as<unsigned long long>();
   for (auto& ev : p->ev) CUDA_TRY(cudaEventCreate(&ev));
   cudaStream_t s = c->stream;
   CUDA_TRY(cudaMemcpyAsync(B.q.p, q1.data(), (m + 1) * 8, cudaMemcpyHostToDevice, s));
-  CUDA_TRY(cudaMemcpyAsync(B.qu.p, qu.data(), m * 8, cudaMemcpyHostToDevice, s));
-  CUDA_TRY(cudaMemcpyAsync(B.ql.p, ql.data(), m * 8, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(B.qul.p, qul.data(), m * 16, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(B.qperm.p, qperm.data(), m * 16, cudaMemcpyHostToDevice, s));
   CUDA_TRY(cudaMemcpyAsync(B.order.p, order.data(), m * 4, cudaMemcpyHostToDevice, s));
   // the staging vectors are pageable locals: wait until the copies consumed them
   CUDA_TRY(cudaStreamSynchronize(s));
@@ -560,11 +583,10 @@ static SearchParams base_params(eapdtw_search_plan* p) {
   s.ref = p->ref;
   s.mean = B.mean.as<double>();
   s.sd = B.sd.as<double>();
-  s.env_up = p->have_env ? B.up.as<double>() : nullptr;
-  s.env_lo = p->have_env ? B.lo.as<double>() : nullptr;
+  s.env = p->have_env ? B.env.as<double2>() : nullptr;
   s.q = B.q.as<double>();
-  s.qu = B.qu.as<double>();
-  s.ql = B.ql.as<double>();
+  s.qul = B.qul.as<double2>();
+  s.qperm = B.qperm.as<double2>();
   s.order = B.order.as<int>();
   s.ncand = static_cast<long long>(p->ncand);
   s.m = static_cast<int>(p->m);
@@ -579,15 +601,17 @@ static SearchParams base_params(eapdtw_search_plan* p) {
   s.best = B.best.as<BestRecord>();
   s.work = B.work.as<unsigned long long>();
   s.queue = B.queue.as<long long>();
+  s.qtot = B.qtot.as<float2>();
+  s.qmax = p->qmax;
   s.qhead = B.qctr.as<unsigned long long>();
   s.qtail = B.qctr.as<unsigned long long>() + 1;
   s.chunks_done = B.qctr.as<unsigned long long>() + 2;
   s.direct_chunk = 4;
   s.stride = 1;
+  s.chunk_span = 0;
   s.ad_k = p->ad_k;
   s.direct = 0;
   s.screen_rows = p->screen_rows;
-  s.lb_head = p->lb_head;
   s.counters = B.counters.as<unsigned long long>();
   s.index_offset = static_cast<long long>(p->offset);
   return s;
@@ -607,7 +631,7 @@ int eapdtw_search_plan_prepare(eapdtw_search_plan* p) {
   p->have_env = false;
   if (p->use_lb && p->m >= 2) {
     const cudaError_t e = launch_envelope(p->ref, static_cast<long long>(p->n), p->env_r,
-                                          B.up.as<double>(), B.lo.as<double>(), s);
+                                          B.env.as<double>(), s);
     if (e == cudaSuccess) {
       p->have_env = true;
       ++c->launches;
@@ -621,7 +645,7 @@ int eapdtw_search_plan_prepare(eapdtw_search_plan* p) {
   // Probe: evaluate evenly spaced candidates first (no lower bounds, running
   // threshold) so the sweep starts from a finite best-so-far.  Probe hits are
   // real candidates, so they legitimately enter the (d, index) record.
-  const size_t nprobe = std::min<size_t>(2048, std::max<size_t>(1, p->ncand / 64));
+  const size_t nprobe = std::min<size_t>(static_cast<size_t>(p->probe), std::max<size_t>(1, p->ncand / 64));
   SearchParams sp = base_params(p);
   sp.use_lb = 0;
   sp.tighten = 0;
@@ -641,13 +665,21 @@ int eapdtw_search_plan_prepare(eapdtw_search_plan* p) {
   // windows normalise to nearly the same series).  Its candidates are real,
   // so their exact results enter the record; their work is counted with the
   // probe's.
-  if (p->coarse_stride > 1 && p->ncand >= 64 * static_cast<size_t>(p->coarse_stride)) {
+  for (const int stride : p->coarse_strides) {
+    if (p->ncand < 64 * static_cast<size_t>(stride)) continue;
     SearchParams cp = base_params(p);
     cp.begin = 0;
     cp.end = static_cast<long long>(p->ncand);
-    cp.stride = p->coarse_stride;
     cp.counters = B.probe_counters.as<unsigned long long>();
-    const long long count = (cp.end + cp.stride - 1) / cp.stride;
+    long long count;
+    if (p->coarse_blocks) {  // runs of 32 adjacent candidates every 32*stride
+      cp.stride = 1;
+      cp.chunk_span = 32LL * stride;
+      count = 32 * ((cp.end + cp.chunk_span - 1) / cp.chunk_span);
+    } else {
+      cp.stride = stride;
+      count = (cp.end + cp.stride - 1) / cp.stride;
+    }
     CUDA_TRY(reset_work(p, count, s));
     CUDA_TRY(launch_search(cp, p->blocks, p->warps, s));
     ++c->launches;

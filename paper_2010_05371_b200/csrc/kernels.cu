@@ -189,21 +189,20 @@ __device__ void envelope_doubling(const double* __restrict__ ref, long long n, l
     src = dst;
     dst = t;
   }
-  for (int t = threadIdx.x; t < T; t += blockDim.x) {
-    if (P0 + t < n) out[P0 + t] = pick<MAX>(src[t], src[t + K - P]);
+  for (int t = threadIdx.x; t < T; t += blockDim.x) {  // interleaved (max, min)
+    if (P0 + t < n) out[2 * (P0 + t) + (MAX ? 0 : 1)] = pick<MAX>(src[t], src[t + K - P]);
   }
   __syncthreads();
 }
 
 __global__ void __launch_bounds__(512) envelope_kernel(const double* __restrict__ ref, long long n,
-                                                       int r, int T, double* __restrict__ up,
-                                                       double* __restrict__ lo) {
+                                                       int r, int T, double* __restrict__ env) {
   extern __shared__ double smem[];
   const int len = T + 2 * r;
   const long long P0 = static_cast<long long>(blockIdx.x) * T;  // first output
   const long long A = P0 - r;                                   // first input
-  envelope_doubling<true>(ref, n, A, len, r, T, P0, smem, smem + len, up);
-  envelope_doubling<false>(ref, n, A, len, r, T, P0, smem, smem + len, lo);
+  envelope_doubling<true>(ref, n, A, len, r, T, P0, smem, smem + len, env);
+  envelope_doubling<false>(ref, n, A, len, r, T, P0, smem, smem + len, env);
 }
 
 static int envelope_tile(int r) {
@@ -214,7 +213,7 @@ static int envelope_tile(int r) {
   return T;
 }
 
-cudaError_t launch_envelope(const double* ref, long long n, int r, double* up, double* lo,
+cudaError_t launch_envelope(const double* ref, long long n, int r, double* env,
                             cudaStream_t stream) {
   const int T = envelope_tile(r);
   if (T < 256) return cudaErrorInvalidValue;  // caller disables the EC tier
@@ -223,7 +222,7 @@ cudaError_t launch_envelope(const double* ref, long long n, int r, double* up, d
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   const long long blocks = (n + T - 1) / T;
-  envelope_kernel<<<static_cast<unsigned>(blocks), 512, smem, stream>>>(ref, n, r, T, up, lo);
+  envelope_kernel<<<static_cast<unsigned>(blocks), 512, smem, stream>>>(ref, n, r, T, env);
   return cudaGetLastError();
 }
 
@@ -263,8 +262,7 @@ static __host__ __device__ inline size_t padded_len(int m, int ad_k) {
 size_t search_smem_bytes(int m, int warps, int ad_k) {
   return padded_len(m, ad_k) * 8                        // q (padded, 1-based)
          + static_cast<size_t>(warps) * padded_len(m, ad_k) * 8  // per-warp DP buffers
-         + static_cast<size_t>(warps) * 5 * kStack * 4  // per-warp tier stacks
-         + static_cast<size_t>(warps) * 2 * kStack * 8  // continuation partial sums
+         + static_cast<size_t>(warps) * kStackBytesPerWarp  // per-warp tier stacks
          + 64;
 }
 
@@ -349,8 +347,8 @@ __global__ void __launch_bounds__(256, kSearchMinBlocks) search_kernel(SearchPar
   // The Keogh envelope and visiting order stay in global memory: every lane
   // reads the same element (broadcast through L1), which frees shared memory
   // for more resident warps.
-  const double* __restrict__ qu = p.qu;
-  const double* __restrict__ ql = p.ql;
+  const double2* __restrict__ qul = p.qul;
+  const double2* __restrict__ qperm = p.qperm;
   const int* __restrict__ order = p.order;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* rowbuf = smem + plen + static_cast<size_t>(warp) * plen + pad;
@@ -369,8 +367,10 @@ __global__ void __launch_bounds__(256, kSearchMinBlocks) search_kernel(SearchPar
   const double* __restrict__ ref = p.ref;
   const bool prune = p.prune != 0;
 
-  // One exact pruned DTW of candidate `cand` with the whole warp.
-  auto run_dtw = [&](long long cand) {
+  // One exact pruned DTW of candidate `cand` with the whole warp.  teq / tec:
+  // the candidate's LB_Keogh EQ / EC totals from the cascade (rounded down),
+  // when have_tot.
+  auto run_dtw = [&](long long cand, bool have_tot, double teq, double tec) {
     const double cm = p.mean[cand];
     const double cs = p.sd[cand];
     const bool cconst = cs < kMinStddev;
@@ -384,72 +384,63 @@ __global__ void __launch_bounds__(256, kSearchMinBlocks) search_kernel(SearchPar
     // ub - cb(k), k = min(i+w, m) - 1, cb(k) a lower bound on the cost of the
     // positions past k that every path still has to visit.  Here cb is the
     // larger of the EQ (per row) and EC (per column) Keogh suffix sums, each
-    // total - prefix(k).  Lazily: only a DTW still running at strip
-    // `cb_strip` pays for the totals (one coalesced pass); each strip then
-    // extends the prefix by the 32 positions its rows need (one scan).
-    // The contributions use the cascade's reciprocal normalisation: cb is
-    // lowered by an absolute guard covering that and by guard_rel * total
-    // for the summation; guard_rel also covers the rounding of the rest of
-    // the path.  Liveness only (the strip engine never kills values): the
-    // result is still the exact DTW value whenever that is <= ub.
-    const bool tight = p.tighten != 0;
+    // total - prefix(k): the totals come with the candidate from the
+    // cascade, and each strip extends the prefix by the 32 positions its
+    // rows need (one coalesced load per lane, one warp scan).  The terms are
+    // the cascade's (reciprocal normalisation); cb is lowered by guard_rel *
+    // total for the summation order and by 8 ulp * (T + qmax sqrt(m T)) for
+    // the normalisation (each term is off by < 2 dd (|dd| + qmax) * 3 ulp).
+    // guard_rel also covers the rounding of the rest of the path.  Liveness
+    // only (the strip engine never kills values): the result is still the
+    // exact DTW value whenever that is <= ub.
+    const bool tight = p.tighten != 0 && have_tot;
     const double rsd = cconst ? 0.0 : __drcp_rn(cs);
-    const bool have_ec = p.env_up != nullptr;
+    const bool have_ec = p.env != nullptr;
     // EQ / EC contribution of position k (0 past the end)
-    auto contrib = [&](int k, double& ceq, double& cec, double& mag) {
+    auto contrib = [&](int k, double& ceq, double& cec) {
       ceq = 0.0;
       cec = 0.0;
       if (k >= m) return;
       const double c = __dmul_rn(__dsub_rn(crow[k], cm), rsd);
-      const double e1 = __dsub_rn(c, qu[k]), e2 = __dsub_rn(ql[k], c);
+      const double2 b = qul[k];
+      const double e1 = __dsub_rn(c, b.x), e2 = __dsub_rn(b.y, c);
       const double d1 = e1 > 0.0 ? e1 : (e2 > 0.0 ? e2 : 0.0);
       ceq = __dmul_rn(d1, d1);
-      mag = fmax(mag, fabs(c));
       if (have_ec) {
-        const double U = __dmul_rn(__dsub_rn(p.env_up[cand + k], cm), rsd);
-        const double L = __dmul_rn(__dsub_rn(p.env_lo[cand + k], cm), rsd);
+        const double2 e = p.env[cand + k];
+        const double U = __dmul_rn(__dsub_rn(e.x, cm), rsd);
+        const double L = __dmul_rn(__dsub_rn(e.y, cm), rsd);
         const double qk = qsp[k + 1];
         const double f1 = __dsub_rn(qk, U), f2 = __dsub_rn(L, qk);
         const double d2 = f1 > 0.0 ? f1 : (f2 > 0.0 ? f2 : 0.0);
         cec = __dmul_rn(d2, d2);
-        mag = fmax(mag, fmax(fabs(U), fabs(L)));
       }
     };
-    bool cb_ready = false;
-    double tot_eq = 0.0, tot_ec = 0.0, pre_eq = 0.0, pre_ec = 0.0, cb_guard = 0.0;
-    int pre_end = 0;  // prefix sums cover positions [0, pre_end)
+    const double tmax = fmax(teq, tec);
+    const double cb_guard =
+        p.guard_rel * tmax +
+        8.0 * 0x1.0p-52 * (tmax + p.qmax * __dsqrt_rn(static_cast<double>(m) * tmax));
+    double pre_eq = 0.0, pre_ec = 0.0;
+    int pre_end = -1;  // prefix sums cover positions [0, pre_end) once started
     auto rowthr = [&](double u, int i, int i0) -> double {
       if (!tight || i0 < 1 + 32 * (p.cb_strip - 1)) return u;
-      if (!cb_ready) {
+      if (pre_end < 0) {  // positions before this strip's first k
         pre_end = min(m, i0 + p.w - 1);
-        double mag = 1.0;
-        for (int k = lane; k < m; k += 32) {
+        for (int k = lane; k < pre_end; k += 32) {
           double a, b;
-          contrib(k, a, b, mag);
-          tot_eq = __dadd_rn(tot_eq, a);
-          tot_ec = __dadd_rn(tot_ec, b);
-          if (k < pre_end) {
-            pre_eq = __dadd_rn(pre_eq, a);
-            pre_ec = __dadd_rn(pre_ec, b);
-          }
+          contrib(k, a, b);
+          pre_eq = __dadd_rn(pre_eq, a);
+          pre_ec = __dadd_rn(pre_ec, b);
         }
         for (int off = 16; off > 0; off >>= 1) {
-          tot_eq = __dadd_rn(tot_eq, __shfl_xor_sync(kFull, tot_eq, off));
-          tot_ec = __dadd_rn(tot_ec, __shfl_xor_sync(kFull, tot_ec, off));
           pre_eq = __dadd_rn(pre_eq, __shfl_xor_sync(kFull, pre_eq, off));
           pre_ec = __dadd_rn(pre_ec, __shfl_xor_sync(kFull, pre_ec, off));
-          mag = fmax(mag, __shfl_xor_sync(kFull, mag, off));
         }
-        // |c|, |U|, |L| are within 3 ulp of the division-normalised values
-        // (each term off by < 28 mag^2 ulp(1)); sums of <= 2m terms
-        cb_guard = 32.0 * static_cast<double>(m) * mag * mag * 0x1.0p-52 +
-                   p.guard_rel * fmax(tot_eq, tot_ec);
-        cb_ready = true;
       }
       // this strip's rows need prefixes through k = i0 + lane + w - 1
       const int kk = i0 + lane + p.w - 1;
-      double a = 0.0, b = 0.0, unused = 1.0;
-      if (kk >= pre_end && kk < m) contrib(kk, a, b, unused);
+      double a = 0.0, b = 0.0;
+      if (kk >= pre_end && kk < m) contrib(kk, a, b);
       for (int off = 1; off < 32; off <<= 1) {  // inclusive prefix scan
         const double x = __shfl_up_sync(kFull, a, off);
         const double y = __shfl_up_sync(kFull, b, off);
@@ -468,7 +459,7 @@ __global__ void __launch_bounds__(256, kSearchMinBlocks) search_kernel(SearchPar
         pre_end = nxt;
       }
       if (kk >= m - 1) return u;  // nothing left past k
-      const double cbv = __dsub_rn(fmax(__dsub_rn(tot_eq, peq), __dsub_rn(tot_ec, pec)), cb_guard);
+      const double cbv = __dsub_rn(fmax(__dsub_rn(teq, peq), __dsub_rn(tec, pec)), cb_guard);
       if (!(cbv > 0.0)) return u;
       const double t = __dsub_rn(__dmul_rn(u, 1.0 + p.guard_rel), cbv);
       return t > 0.0 ? t : 0.0;
@@ -498,7 +489,7 @@ __global__ void __launch_bounds__(256, kSearchMinBlocks) search_kernel(SearchPar
         const long long s = base + k * p.stride;
         if (s >= p.end) break;
         ++c_cand;
-        run_dtw(s);
+        run_dtw(s, false, 0.0, 0.0);
       }
     }
   } else {
@@ -509,59 +500,63 @@ __global__ void __launch_bounds__(256, kSearchMinBlocks) search_kernel(SearchPar
     //   little later -- meanwhile it keeps producing.  Once every chunk has
     //   been published (chunks_done == nchunks) a future slot beyond the final
     //   tail is void.
-    const long long ncount = (p.end - p.begin + p.stride - 1) / p.stride;
-    const long long nchunks = (ncount + 31) / 32;
+    // chunk c covers candidates begin + c*span + lane*stride
+    const long long span = p.chunk_span > 0 ? p.chunk_span : 32 * p.stride;
+    const long long nchunks = (p.end - p.begin + span - 1) / span;
     bool chunks_left = true, flushed = false;
     long long myslot = -1;
     unsigned long long my_chunks = 0;
     // Per-warp compaction stacks between the tiers (local candidate indices):
     // Kim survivors -> [A] -> EQ -> [B] -> EC -> [C] -> phase-A screen -> queue.
     // A tier runs only on a full warp of candidates (or when flushing), so
-    // lanes stay busy although each tier discards most of its input.
-    int* stkA = stacks + warp * (5 * kStack);
-    int* stkB = stkA + kStack;
-    int* stkC = stkB + kStack;
-    int* stkA2 = stkC + kStack;  // EQ continuations (candidate, partial sum)
-    int* stkB2 = stkA2 + kStack; // EC continuations
-    double* accA2 = reinterpret_cast<double*>(stacks + (blockDim.x >> 5) * (5 * kStack)) +
-                    warp * (2 * kStack);
+    // lanes stay busy although each tier discards most of its input.  Each
+    // tier runs in two legs: the first kLbHead positions of order[] (largest
+    // |q|: most prunes happen there), then the candidates still pending are
+    // re-gathered into full warps [A2], [B2] with their partial sums.
+    // Survivors carry their EQ / EC totals (rounded down) to the DTW, for the
+    // cumulative-bound row thresholds.
+    unsigned char* wbase = reinterpret_cast<unsigned char*>(stacks) + warp * kStackBytesPerWarp;
+    int* stkA = reinterpret_cast<int*>(wbase);
+    int* stkA2 = stkA + kStack;
+    int* stkB = stkA2 + kStack;
+    int* stkB2 = stkB + kStack;
+    int* stkC = stkB2 + kStack;
+    float* teqB = reinterpret_cast<float*>(stkC + kStack);  // B: EQ total
+    float* teqB2 = teqB + kStack;                             // B2: EQ total
+    float2* totC = reinterpret_cast<float2*>(teqB2 + kStack); // C: (EQ, EC) totals
+    double* accA2 = reinterpret_cast<double*>(totC + kStack);
     double* accB2 = accA2 + kStack;
-    int nA = 0, nB = 0, nC = 0, nA2 = 0, nB2 = 0;
+    int nA = 0, nA2 = 0, nB = 0, nB2 = 0, nC = 0;
 
-    auto push = [&](int* stk, int& n, bool keep, long long cand) {
-      const unsigned mask = __ballot_sync(kFull, keep);
-      if (keep) stk[n + __popc(mask & ((1u << lane) - 1u))] = static_cast<int>(cand - p.begin);
-      n += __popc(mask);
-      __syncwarp();
-    };
-    auto push2 = [&](int* stk, double* acs, int& n, bool keep, long long cand, double acc) {
+    // push: ballot-compacted append of the lanes with keep; pop: up to 32
+    // entries, lane L gets entry n-take+L (valid iff L < take).
+    auto push = [&](int* stk, int& n, bool keep, long long cand, double* acc_arr, double acc,
+                    float* f_arr, float f, float2* f2_arr, float2 f2) {
       const unsigned mask = __ballot_sync(kFull, keep);
       if (keep) {
         const int at = n + __popc(mask & ((1u << lane) - 1u));
         stk[at] = static_cast<int>(cand - p.begin);
-        acs[at] = acc;
+        if (acc_arr) acc_arr[at] = acc;
+        if (f_arr) f_arr[at] = f;
+        if (f2_arr) f2_arr[at] = f2;
       }
       n += __popc(mask);
       __syncwarp();
     };
-    auto pop2 = [&](int* stk, double* acs, int& n, long long& cand, double& acc) -> bool {
+    auto pop = [&](int* stk, int& n, long long& cand, const double* acc_arr, double& acc,
+                   const float* f_arr, float& f, const float2* f2_arr, float2& f2) -> bool {
       const int take = min(32, n);
       const bool ok = lane < take;
-      cand = ok ? p.begin + stk[n - take + lane] : p.begin;
-      acc = ok ? acs[n - take + lane] : 0.0;
+      const int at = ok ? n - take + lane : 0;
+      cand = ok ? p.begin + stk[at] : p.begin;
+      acc = (ok && acc_arr) ? acc_arr[at] : 0.0;
+      f = (ok && f_arr) ? f_arr[at] : 0.0f;
+      f2 = (ok && f2_arr) ? f2_arr[at] : make_float2(0.0f, 0.0f);
       __syncwarp();
       n -= take;
       return ok;
     };
-    // Pop up to 32 entries: lane L gets entry n-take+L (valid iff L < take).
-    auto pop = [&](int* stk, int& n, long long& cand) -> bool {
-      const int take = min(32, n);
-      const bool ok = lane < take;
-      cand = ok ? p.begin + stk[n - take + lane] : p.begin;
-      __syncwarp();
-      n -= take;
-      return ok;
-    };
+    const float2 z2 = make_float2(0.0f, 0.0f);
 
     for (;;) {
       long long cand = -1;
@@ -579,12 +574,22 @@ __global__ void __launch_bounds__(256, kSearchMinBlocks) search_kernel(SearchPar
       }
       cand = __shfl_sync(kFull, cand, 0);
       void_slot = __shfl_sync(kFull, void_slot, 0);
-      myslot = __shfl_sync(kFull, myslot, 0);
       if (cand >= 0) {
+        float2 tot = z2;
+        if (lane == 0) {
+          __threadfence();
+          const unsigned long long raw =
+              *reinterpret_cast<const volatile unsigned long long*>(p.qtot + myslot);
+          tot = make_float2(__uint_as_float(static_cast<unsigned>(raw)),
+                            __uint_as_float(static_cast<unsigned>(raw >> 32)));
+        }
+        tot.x = __shfl_sync(kFull, tot.x, 0);
+        tot.y = __shfl_sync(kFull, tot.y, 0);
         myslot = -1;
-        run_dtw(cand);
+        run_dtw(cand, p.use_lb != 0, static_cast<double>(tot.x), static_cast<double>(tot.y));
         continue;
       }
+      myslot = __shfl_sync(kFull, myslot, 0);
       if (void_slot) break;
       if (flushed) {
         if (myslot < 0) break;  // nothing pending, nothing left to produce
@@ -602,7 +607,7 @@ __global__ void __launch_bounds__(256, kSearchMinBlocks) search_kernel(SearchPar
           chunks_left = false;  // flush the stacks below, then retire
         } else {
           ++my_chunks;
-          const long long s = p.begin + (static_cast<long long>(chunk) * 32 + lane) * p.stride;
+          const long long s = p.begin + static_cast<long long>(chunk) * span + lane * p.stride;
           const bool valid = s < p.end;
           c_cand += __popc(__ballot_sync(kFull, valid));
           bool alive = valid;
@@ -618,21 +623,51 @@ __global__ void __launch_bounds__(256, kSearchMinBlocks) search_kernel(SearchPar
               ++c_kim;
             }
           }
-          if (p.use_lb) push(stkA, nA, alive, s);
-          else push(stkC, nC, alive, s);
+          if (p.use_lb) push(stkA, nA, alive, s, nullptr, 0.0, nullptr, 0.0f, nullptr, z2);
+          else push(stkC, nC, alive, s, nullptr, 0.0, nullptr, 0.0f, totC, z2);
         }
       }
       const bool flush = !chunks_left;
 
       // Early-abandoning LB_Keogh over order[k0, k1) (lower_bounds.cpp:57-88),
-      // lane per candidate, continuing the partial sum `acc`; the vote every 8
-      // positions lets the warp stop once every lane has abandoned.
-      auto lb_range = [&](long long s, bool pending, const double mean, const double rsd,
-                          double ubg, auto term, int k0, int k1, double& acc) -> bool {
+      // lane per candidate, continuing the partial sum `acc`; the vote every
+      // kLbGroup positions lets the warp stop once every lane has abandoned.
+      //   EQ: query envelope qperm[k] (warp-uniform) vs the candidate
+      //       normalised by reciprocal multiplication;
+      //   EC: query value vs the candidate's (global raw) envelope, normalised.
+      // Lanes without a candidate point at p.begin: loads stay in bounds.
+      auto lb_range = [&](auto ec_tag, long long s, bool pending, const double mean,
+                          const double rsd, double ubg, int k0, int k1, double& acc) -> bool {
+        constexpr bool EC = decltype(ec_tag)::value;
         bool alive = pending;
-        for (int kb = k0; kb < k1; kb += 8) {
-          const int kend = min(k1, kb + 8);
-          for (int k = kb; k < kend; ++k) acc += term(pending, s, order[k], mean, rsd);
+        const double* xs = ref + s;
+        const double2* es = EC ? p.env + s : nullptr;
+        auto term = [&](int k) {
+          const int j = order[k];
+          double a, U, L;
+          if (!EC) {
+            const double2 b = qperm[k];
+            a = __dmul_rn(__dsub_rn(xs[j], mean), rsd);
+            U = b.x;
+            L = b.y;
+          } else {
+            const double2 e = es[j];
+            a = qsp[j + 1];
+            U = __dmul_rn(__dsub_rn(e.x, mean), rsd);
+            L = __dmul_rn(__dsub_rn(e.y, mean), rsd);
+          }
+          const double e1 = __dsub_rn(a, U), e2 = __dsub_rn(L, a);
+          const double dd = e1 > 0.0 ? e1 : (e2 > 0.0 ? e2 : 0.0);
+          acc = __dadd_rn(acc, __dmul_rn(dd, dd));
+        };
+        // groups of kLbGroup positions: all their loads are in flight together
+        for (int kb = k0; kb < k1; kb += kLbGroup) {
+          if (kb + kLbGroup <= k1) {
+#pragma unroll
+            for (int u = 0; u < kLbGroup; ++u) term(kb + u);
+          } else {
+            for (int k = kb; k < k1; ++k) term(k);
+          }
           if (pending && acc > ubg) {
             pending = false;
             alive = false;
@@ -641,58 +676,58 @@ __global__ void __launch_bounds__(256, kSearchMinBlocks) search_kernel(SearchPar
         }
         return alive;
       };
-      // EQ term: query envelope vs normalised candidate (reciprocal multiply).
-      auto eq_term = [&](bool on, long long s, int j, double mean, double rsd) -> double {
-        const double x = on ? ref[s + j] : 0.0;
-        const double cn = __dmul_rn(__dsub_rn(x, mean), rsd);
-        const double e1 = cn - qu[j];
-        const double e2 = ql[j] - cn;
-        const double dd = e1 > 0.0 ? e1 : (e2 > 0.0 ? e2 : 0.0);
-        return dd * dd;
-      };
-      // EC term: normalised query vs the candidate envelope (global raw envelope).
-      auto ec_term = [&](bool on, long long s, int j, double mean, double rsd) -> double {
-        double U = 0.0, L = 0.0;
-        if (on) {
-          U = __dmul_rn(__dsub_rn(p.env_up[s + j], mean), rsd);
-          L = __dmul_rn(__dsub_rn(p.env_lo[s + j], mean), rsd);
-        }
-        const double qj = qsp[j + 1];
-        const double e1 = qj - U;
-        const double e2 = L - qj;
-        const double dd = e1 > 0.0 ? e1 : (e2 > 0.0 ? e2 : 0.0);
-        return dd * dd;
-      };
 
       // ---- tiers 2/3: LB_Keogh EQ (search.cpp:92) then EC (search.cpp:97-99),
-      //      prune iff lb > ub*(1+g_rel) + g_abs.  Each tier runs in two legs:
-      //      the first kLbHead positions of order[] (largest |q|: most prunes
-      //      happen there) for a full warp, then the candidates still pending
-      //      are re-gathered into full warps with their partial sums and
-      //      finish the remaining positions -- so a warp's length is set by
-      //      its slowest lane only among candidates that got that far.
-      const int head = min(m, p.lb_head);
-      auto stage = [&](int* in, int& nin, int* cont, double* cacc, int& ncont, int* out,
-                       int& nout, auto term, unsigned long long& pruned, bool leg2) {
+      //      prune iff lb > ub*(1+g_rel) + g_abs.
+      const int head = min(m, kLbHead);
+      const bool have_ec = p.env != nullptr;
+      // EC == false: EQ tier (A -> A2 -> B, or C without an EC tier).
+      auto stage = [&](auto ec_tag, bool leg2) {
+        constexpr bool EC = decltype(ec_tag)::value;
         long long s;
         double acc = 0.0;
-        const bool pending = leg2 ? pop2(cont, cacc, ncont, s, acc) : pop(in, nin, s);
+        float teq = 0.0f;
+        float2 unused2;
+        float unusedf;
+        bool pending;
+        if (!EC) {
+          pending = leg2 ? pop(stkA2, nA2, s, accA2, acc, nullptr, unusedf, nullptr, unused2)
+                         : pop(stkA, nA, s, nullptr, acc, nullptr, unusedf, nullptr, unused2);
+        } else {
+          pending = leg2 ? pop(stkB2, nB2, s, accB2, acc, teqB2, teq, nullptr, unused2)
+                         : pop(stkB, nB, s, nullptr, acc, teqB, teq, nullptr, unused2);
+        }
         const double mean = p.mean[s];
         const double sd = p.sd[s];
         const double rsd = sd < kMinStddev ? 0.0 : __drcp_rn(sd);
         const double ubg = load_ub(p.ub_key) * (1.0 + p.guard_rel) + p.guard_abs;
-        const bool alive = leg2 ? lb_range(s, pending, mean, rsd, ubg, term, head, m, acc)
-                                : lb_range(s, pending, mean, rsd, ubg, term, 0, head, acc);
-        if (pending && !alive) ++pruned;
-        if (!leg2 && head < m) push2(cont, cacc, ncont, alive, s, acc);
-        else push(out, nout, alive, s);
+        const bool alive = leg2 ? lb_range(ec_tag, s, pending, mean, rsd, ubg, head, m, acc)
+                                : lb_range(ec_tag, s, pending, mean, rsd, ubg, 0, head, acc);
+        if (pending && !alive) {
+          if (EC) ++c_ec;
+          else ++c_eq;
+        }
+        const float tot = __double2float_rz(acc);  // rounded down: a weaker, sound total
+        if (!leg2 && head < m) {
+          if (EC) push(stkB2, nB2, alive, s, accB2, acc, teqB2, teq, nullptr, z2);
+          else push(stkA2, nA2, alive, s, accA2, acc, nullptr, 0.0f, nullptr, z2);
+        } else if (EC) {
+          push(stkC, nC, alive, s, nullptr, 0.0, nullptr, 0.0f, totC, make_float2(teq, tot));
+        } else if (have_ec) {
+          push(stkB, nB, alive, s, nullptr, 0.0, teqB, tot, nullptr, z2);
+        } else {
+          push(stkC, nC, alive, s, nullptr, 0.0, nullptr, 0.0f, totC, make_float2(tot, 0.0f));
+        }
       };
       // ---- phase A: the first screen_rows DTW rows, lane per candidate (an
       //      exact EAPrunedDTW prefix; a killed candidate is an abandoned
-      //      DTW), then publish the survivors to the queue.
+      //      DTW), then publish the survivors (+ totals) to the queue.
       auto screen_stage = [&]() {
         long long s;
-        bool alive = pop(stkC, nC, s);
+        double unused;
+        float unusedf;
+        float2 tot;
+        bool alive = pop(stkC, nC, s, nullptr, unused, nullptr, unusedf, totC, tot);
         if (p.screen_rows > 0) {
           const double mean = p.mean[s];
           const double sd = p.sd[s];
@@ -716,14 +751,14 @@ __global__ void __launch_bounds__(256, kSearchMinBlocks) search_kernel(SearchPar
           if (lane == 0) qb = atomicAdd(p.qtail, static_cast<unsigned long long>(__popc(mask)));
           qb = __shfl_sync(kFull, qb, 0);
           if (alive) {
-            const unsigned rank = __popc(mask & ((1u << lane) - 1u));
-            reinterpret_cast<volatile long long*>(p.queue)[qb + rank] = s;
+            const unsigned long long slot = qb + __popc(mask & ((1u << lane) - 1u));
+            p.qtot[slot] = tot;
+            __threadfence();  // the totals are visible before the slot is
+            reinterpret_cast<volatile long long*>(p.queue)[slot] = s;
           }
         }
       };
 
-      int* eq_out = p.env_up != nullptr ? stkB : stkC;
-      int& eq_nout = p.env_up != nullptr ? nB : nC;
       // Most downstream ready stage first, so every push lands in a stack
       // holding < 32 entries (capacity kStack = 64); a partial warp runs only
       // when flushing and once everything upstream has drained.
@@ -732,13 +767,13 @@ __global__ void __launch_bounds__(256, kSearchMinBlocks) search_kernel(SearchPar
         if (nC >= 32 || (flush && nC > 0 && up_c)) {
           screen_stage();
         } else if (nB2 >= 32 || (flush && nB2 > 0 && up_b)) {
-          stage(stkB, nB, stkB2, accB2, nB2, stkC, nC, ec_term, c_ec, true);
+          stage(std::true_type{}, true);
         } else if (nB >= 32 || (flush && nB > 0 && up_a)) {
-          stage(stkB, nB, stkB2, accB2, nB2, stkC, nC, ec_term, c_ec, false);
+          stage(std::true_type{}, false);
         } else if (nA2 >= 32 || (flush && nA2 > 0 && nA == 0)) {
-          stage(stkA, nA, stkA2, accA2, nA2, eq_out, eq_nout, eq_term, c_eq, true);
+          stage(std::false_type{}, true);
         } else if (nA >= 32 || (flush && nA > 0)) {
-          stage(stkA, nA, stkA2, accA2, nA2, eq_out, eq_nout, eq_term, c_eq, false);
+          stage(std::false_type{}, false);
         } else {
           break;
         }

@@ -12,7 +12,13 @@ constexpr long long kStatsResetInterval = 100000;  // search.cpp:16
 constexpr double kMinStddev = 1e-12;               // search.cpp:13
 constexpr int kScreenSlots = 24;                   // phase-A window (band offsets)
 constexpr int kStack = 64;                         // per-warp tier stack capacity
+#ifndef EAPDTW_LB_GROUP
+#define EAPDTW_LB_GROUP 8
+#endif
+constexpr int kLbGroup = EAPDTW_LB_GROUP;          // Keogh positions per abandon vote
 constexpr int kLbHead = 256;                       // first leg of the Keogh tiers (positions of order[])
+// A, A2, B, B2, C indices; B, B2 EQ totals; C (EQ, EC) totals; A2, B2 partial sums
+constexpr int kStackBytesPerWarp = kStack * (5 * 4 + 2 * 4 + 8 + 2 * 8);
 
 // Tier counters accumulated on the device (SearchReport, search.hpp:68-77).
 enum Counter : int {
@@ -32,24 +38,26 @@ struct SearchParams {
   const double* ref;     // shard reference, n points
   const double* mean;    // per candidate (ncand)
   const double* sd;      // per candidate (ncand)
-  const double* env_up;  // raw sliding max of ref, radius env_r (nullptr: no EC tier)
-  const double* env_lo;  // raw sliding min of ref
+  const double2* env;    // raw sliding (max, min) of ref, radius env_r (nullptr: no EC tier)
   const double* q;       // normalised query, 1-based: q[1..m] (q[0] unused)
-  const double* qu;      // query envelope upper, 0-based
-  const double* ql;      // query envelope lower, 0-based
+  const double2* qul;    // query envelope (upper, lower) per position, 0-based
+  const double2* qperm;  // the same in visiting order: qperm[k] = qul[order[k]]
   const int* order;      // Keogh visiting order (search.cpp:143-149)
   long long ncand;
   long long begin, end, stride;  // candidates begin, begin+stride, ... < end
+  long long chunk_span;          // cascade: chunk c starts at begin + c*chunk_span (0: 32*stride)
   int m, w;                      // query length, effective half window
   int use_lb;                    // Kim -> Keogh EQ -> Keogh EC cascade
   int tighten;                   // per-row thresholds from the Keogh cumulative bound (search.cpp:101-105)
   int cb_strip;                  // first strip (1-based) that uses them
   int prune;                     // 0: Algo::full (no pruning), 1: pruned DTW
   double guard_rel, guard_abs;   // LB soundness guard
+  double qmax;                   // max |q| (cumulative-bound guard)
   unsigned long long* ub_key;    // running threshold key (order-preserving bits)
   BestRecord* best;              // exact (d, lowest index) record
   unsigned long long* work;      // chunk counter (zeroed before launch)
   long long* queue;              // survivor queue, -1 filled before launch
+  float2* qtot;                  // per queue slot: LB_Keogh EQ / EC totals (rounded down)
   unsigned long long* qhead;     // next slot to consume (zeroed before launch)
   unsigned long long* qtail;     // next slot to fill (zeroed before launch)
   unsigned long long* chunks_done;  // LB chunks published (zeroed before launch)
@@ -57,7 +65,6 @@ struct SearchParams {
   int ad_k;                      // anti-diagonal engine window 64*ad_k (0: strip engine only)
   int direct;                    // 1: every candidate is a DTW task (the probe)
   int screen_rows;               // phase-A lane screen depth (0: off)
-  int lb_head;                   // first leg of the Keogh tiers (positions of order[])
   unsigned long long* counters;  // kNumCounters
   long long index_offset;        // shard start in the global reference
 };
@@ -92,7 +99,8 @@ struct Nn1Params {
 // Each launcher enqueues on `stream` and returns the launch error (no sync).
 cudaError_t launch_stats(const double* ref, long long n, int m, double* mean, double* sd,
                          cudaStream_t stream);
-cudaError_t launch_envelope(const double* ref, long long n, int r, double* up, double* lo,
+// env: 2n doubles, (max, min) interleaved
+cudaError_t launch_envelope(const double* ref, long long n, int r, double* env,
                             cudaStream_t stream);
 size_t search_smem_bytes(int m, int warps, int ad_k);
 // Window parameter of the anti-diagonal engine for a band of half width w
