@@ -701,8 +701,8 @@ __global__ void __launch_bounds__(256, kSearchMinBlocks) search_kernel(SearchPar
         const double sd = p.sd[s];
         const double rsd = sd < kMinStddev ? 0.0 : __drcp_rn(sd);
         const double ubg = load_ub(p.ub_key) * (1.0 + p.guard_rel) + p.guard_abs;
-        const bool alive = leg2 ? lb_range(ec_tag, s, pending, mean, rsd, ubg, head, m, acc)
-                                : lb_range(ec_tag, s, pending, mean, rsd, ubg, 0, head, acc);
+        const bool alive =
+            lb_range(ec_tag, s, pending, mean, rsd, ubg, leg2 ? head : 0, leg2 ? m : head, acc);
         if (pending && !alive) {
           if (EC) ++c_ec;
           else ++c_eq;
@@ -766,16 +766,24 @@ __global__ void __launch_bounds__(256, kSearchMinBlocks) search_kernel(SearchPar
         const bool up_a = (nA | nA2) == 0, up_b = up_a && nB == 0, up_c = up_b && nB2 == 0;
         if (nC >= 32 || (flush && nC > 0 && up_c)) {
           screen_stage();
-        } else if (nB2 >= 32 || (flush && nB2 > 0 && up_b)) {
-          stage(std::true_type{}, true);
-        } else if (nB >= 32 || (flush && nB > 0 && up_a)) {
-          stage(std::true_type{}, false);
-        } else if (nA2 >= 32 || (flush && nA2 > 0 && nA == 0)) {
-          stage(std::false_type{}, true);
-        } else if (nA >= 32 || (flush && nA > 0)) {
-          stage(std::false_type{}, false);
         } else {
-          break;
+          // one inlined copy per tier (code size: the kernel is i-cache bound)
+          int tier = 0;  // 1: EQ, 2: EC
+          bool leg2 = false;
+          if (nB2 >= 32 || (flush && nB2 > 0 && up_b)) {
+            tier = 2;
+            leg2 = true;
+          } else if (nB >= 32 || (flush && nB > 0 && up_a)) {
+            tier = 2;
+          } else if (nA2 >= 32 || (flush && nA2 > 0 && nA == 0)) {
+            tier = 1;
+            leg2 = true;
+          } else if (nA >= 32 || (flush && nA > 0)) {
+            tier = 1;
+          }
+          if (tier == 0) break;
+          if (tier == 2) stage(std::true_type{}, leg2);
+          else stage(std::false_type{}, leg2);
         }
       }
 
