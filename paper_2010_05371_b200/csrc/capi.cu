@@ -474,8 +474,8 @@ static int plan_init(eapdtw_search_plan* p, eapdtw_ctx* c, const double* ref_dev
   CUDA_TRY(B.qtot.ensure((nc + kQueueSlack) * 8));
   CUDA_TRY(B.qctr.ensure(24));
   CUDA_TRY(B.flag.ensure(8));
-  CUDA_TRY(B.counters.ensure(kNumCounters * 8));
-  CUDA_TRY(B.probe_counters.ensure(kNumCounters * 8));
+  CUDA_TRY(B.counters.ensure(kNumCountersExt * 8));
+  CUDA_TRY(B.probe_counters.ensure(kNumCountersExt * 8));
   if (p->use_lb) {
     CUDA_TRY(B.env.ensure(n * 16));
   }
@@ -538,8 +538,8 @@ int eapdtw_search_plan_reset(eapdtw_search_plan* p) {
   CUDA_TRY(cudaSetDevice(c->device));
   cudaStream_t s = c->stream;
   PlanBuffers& B = *p->buf;
-  CUDA_TRY(cudaMemsetAsync(B.counters.p, 0, kNumCounters * 8, s));
-  CUDA_TRY(cudaMemsetAsync(B.probe_counters.p, 0, kNumCounters * 8, s));
+  CUDA_TRY(cudaMemsetAsync(B.counters.p, 0, kNumCountersExt * 8, s));
+  CUDA_TRY(cudaMemsetAsync(B.probe_counters.p, 0, kNumCountersExt * 8, s));
   CUDA_TRY(launch_init_best(B.best.as<BestRecord>(), p->key, 1, s));
   ++c->launches;
   if (const char* env = getenv("EAPDTW_SEED_UB")) {  // experiment: start from a known threshold
@@ -719,7 +719,7 @@ int eapdtw_search_plan_result(eapdtw_search_plan* p, eapdtw_search_result* out) 
   PlanBuffers& B = *p->buf;
   CUDA_TRY(cudaSetDevice(c->device));
   BestRecord rec{};
-  unsigned long long cnt[kNumCounters], pc[kNumCounters];
+  unsigned long long cnt[kNumCountersExt], pc[kNumCountersExt];
   CUDA_TRY(cudaMemcpyAsync(&rec, B.best.p, sizeof(rec), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaMemcpyAsync(cnt, B.counters.p, sizeof(cnt), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaMemcpyAsync(pc, B.probe_counters.p, sizeof(pc), cudaMemcpyDeviceToHost, c->stream));
@@ -737,6 +737,19 @@ int eapdtw_search_plan_result(eapdtw_search_plan* p, eapdtw_search_result* out) 
   out->dp_cells_evaluated = cnt[kCntCells] + pc[kCntCells];
   out->elapsed_seconds =
       std::chrono::duration<double>(std::chrono::steady_clock::now() - p->t0).count();
+#ifdef EAPDTW_PHASE_CLOCKS
+  {
+    unsigned long long dbg[8];
+    debug_read_reset(dbg);
+    std::fprintf(stderr, "strip steps %llu strips %llu cells %llu -> lane eff %.3f\n", dbg[0], dbg[1],
+                 cnt[kCntCells], cnt[kCntCells] / (32.0 * dbg[0] + 1));
+  }
+  std::fprintf(stderr,
+               "phase warp-Gcycles: dtw %.3f eq %.3f ec %.3f screen %.3f | stage hit %llu miss "
+               "%llu\n",
+               cnt[kClkDtw] * 1e-9, cnt[kClkEq] * 1e-9, cnt[kClkEc] * 1e-9,
+               cnt[kClkScreen] * 1e-9, cnt[kStageHit], cnt[kStageMiss]);
+#endif
   return EAPDTW_OK;
 }
 

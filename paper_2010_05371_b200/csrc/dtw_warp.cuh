@@ -44,6 +44,10 @@
 
 namespace eapdtw_b200 {
 
+#ifdef EAPDTW_PHASE_CLOCKS
+__device__ unsigned long long g_dbg[8];  // strip steps, strips
+#endif
+
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kPadL = 32;  // left padding of qsp / rowbuf (doubles)
 constexpr int kPadR = 40;  // right padding
@@ -117,6 +121,9 @@ __device__ double warp_dtw(const RawFn& rowraw, const NormFn& rownorm, int lr,
   __syncwarp();
 
   for (int i0 = 1; i0 <= lr; i0 += 32) {
+#ifdef EAPDTW_PHASE_CLOCKS
+    if (lane == 0) atomicAdd(&g_dbg[1], 1ull);
+#endif
     const double ub_strip = ub_next;
     const int i = i0 + lane;
     const bool active = i <= lr;
@@ -187,6 +194,9 @@ __device__ double warp_dtw(const RawFn& rowraw, const NormFn& rownorm, int lr,
       step(3);
       finmask |= __ballot_sync(kFull, jr + 3 > static_cast<int>(span));
       if (((finmask & ~before) >> lane) & 1u) jf = j + 3;
+#ifdef EAPDTW_PHASE_CLOCKS
+      if (lane == 0) atomicAdd(&g_dbg[0], 4ull);
+#endif
       if (finmask == kFull) break;
       j += 4;
       jr += 4;
@@ -237,15 +247,20 @@ __device__ double warp_dtw(const RawFn& rowraw, const NormFn& rownorm, int lr,
 
 
 // Two rows per lane: the same skewed wavefront over strips of 64 rows, lane L
-// owning rows i0+2L and i0+2L+1.  The lane's second row takes its top and
-// diagonal from its own first row (registers), so one __shfl_up of a double
-// and one shared-memory query read serve two cells per step, and the
-// finished-flag / ballot bookkeeping is shared too.  Same contract as
-// warp_dtw (exact value iff <= ub, else +inf); no KILL variant.
-template <class RawFn, class NormFn, class UbFn>
+// owning rows i0+2L and i0+2L+1, both at the same column in a step: the
+// second row's top is the first row's new cell and its diagonal the first
+// row's previous cell (registers).  Lanes stay one column apart, so a strip
+// of 64 rows costs the same 31-step fill as a 32-row strip of warp_dtw, and
+// the shuffle, query read, ballots and finish bookkeeping of a step serve two
+// cells.  Same contract as warp_dtw<false> (exact value iff <= ub, else
+// +inf).  thr2(u, i0, t1, t2): the thresholds of the lane's two rows given
+// the strip ub (cumulative bound, or t1 = t2 = u); called once per strip by
+// every lane.
+template <class RawFn, class NormFn, class UbFn, class Thr2Fn>
 __device__ double warp_dtw2(const RawFn& rowraw, const NormFn& rownorm, int lr,
                             const double* __restrict__ qsp, int lc, int w, UbFn&& get_ub,
-                            double* __restrict__ rowbuf, unsigned long long& cells) {
+                            Thr2Fn&& thr2, double* __restrict__ rowbuf,
+                            unsigned long long& cells) {
   const int lane = threadIdx.x & 31;
   const double INF = d_inf();
   for (int k = lane; k <= lc + 1; k += 32) rowbuf[k] = k == 0 ? 0.0 : INF;
@@ -269,12 +284,15 @@ __device__ double warp_dtw2(const RawFn& rowraw, const NormFn& rownorm, int lr,
       x1n = i1 + 64 <= lr ? rowraw(i1 + 63) : 0.0;
       x2n = i2 + 64 <= lr ? rowraw(i2 + 63) : 0.0;
     }
-    const double ub = fmin(ub_strip, DBL_MAX);
-    const int ub_hi = __double2hiint(ub);
-    ub_last = ub;
-    const int last = min(i0 + 63, lr);      // the strip's last row
-    const int wl = (last - i0) >> 1;         // its lane
+    double t1, t2;
+    thr2(ub_strip, i0, t1, t2);
+    t1 = fmin(t1, DBL_MAX);  // an infinite threshold never makes +inf live
+    t2 = fmin(t2, DBL_MAX);
+    const int hi1 = __double2hiint(t1), hi2 = __double2hiint(t2);
+    const int last = min(i0 + 63, lr);  // the strip's last row
+    const int wl = (last - i0) >> 1;    // its lane
     const bool wsecond = ((last - i0) & 1) != 0;
+    ub_last = __shfl_sync(kFull, wsecond ? t2 : t1, wl);
     const double c1 = act1 ? rownorm(x1) : INF;
     const double c2 = act2 ? rownorm(x2) : INF;
     const int jb = max(lo, 1);
@@ -288,15 +306,19 @@ __device__ double warp_dtw2(const RawFn& rowraw, const NormFn& rownorm, int lr,
     const double* qp = qsp + j;
     double* rp = rowbuf + j;
     double v1 = INF, v2 = INF;
-    bool fin1 = !act1, fin2 = !act1;
-    int jf1 = fin1 ? j - 1 : lc + 1, jf2 = jf1;
-    unsigned finmask = __ballot_sync(kFull, fin2);
+    // Finished rows as warp-uniform masks (bit L = lane L): row 1 of lane L
+    // finishes when its cell is dead and lane L-1's row 2 (for lane 0 the
+    // row buffer, dead beyond hi) was finished a step earlier; row 2 when its
+    // cell is dead and row 1 is finished; or once past the band (tested once
+    // per 4 steps).  A lane is done when its row 2 is.
+    unsigned f1 = __ballot_sync(kFull, !act1), f2 = f1;
+    int jf1 = act1 ? lc + 1 : j - 1, jf2 = jf1;
     const bool w1 = lane == wl && !wsecond, w2 = lane == wl && wsecond;
     const bool is0 = lane == 0;
     const unsigned span1 = static_cast<unsigned>(bh1 - bl1);
     const unsigned span2 = static_cast<unsigned>(max(bh2 - bl2, 0));
     int jr1 = j - bl1, jr2 = j - bl2;
-    const unsigned upbit = is0 ? 0x80000000u : (1u << (lane - 1));
+    int j0 = jb;  // lane 0's column (warp-uniform)
 
     auto step = [&](int u) {
       const double sh = __shfl_up_sync(kFull, v2, 1);
@@ -308,31 +330,31 @@ __device__ double warp_dtw2(const RawFn& rowraw, const NormFn& rownorm, int lr,
       n1 = static_cast<unsigned>(jr1 + u) <= span1 ? n1 : INF;
       double n2 = __dadd_rn(sq_cost(c2, qj), dmin2(v2, dmin2(n1, v1)));
       n2 = static_cast<unsigned>(jr2 + u) <= span2 ? n2 : INF;
-      const bool live1 = __double2hiint(n1) <= ub_hi;  // superset of n <= ub
-      const bool live2 = __double2hiint(n2) <= ub_hi;
       if (w1) rp[u] = n1;
       if (w2) rp[u] = n2;
       v1 = n1;
       v2 = n2;
-      const unsigned up = (finmask & 0x7fffffffu) | (j + u > hi ? 0x80000000u : 0u);
-      const bool nf1 = fin1 || jr1 + u > static_cast<int>(span1) || ((up & upbit) && !live1);
-      const bool nf2 = fin2 || jr2 + u > static_cast<int>(span2) || (nf1 && !live2);
-      jf1 = (!fin1 && nf1) ? j + u : jf1;
-      jf2 = (!fin2 && nf2) ? j + u : jf2;
-      fin1 = nf1;
-      fin2 = nf2;
-      finmask = __ballot_sync(kFull, fin2);
+      const unsigned d1 = __ballot_sync(kFull, __double2hiint(n1) > hi1);  // dead (superset)
+      const unsigned d2 = __ballot_sync(kFull, __double2hiint(n2) > hi2);
+      f1 |= d1 & ((f2 << 1) | (j0 + u > hi ? 1u : 0u));
+      f2 |= d2 & f1;
     };
 
     for (;;) {
+      const unsigned b1 = f1, b2 = f2;
       step(0);
       step(1);
       step(2);
       step(3);
-      if (finmask == kFull) break;
+      f1 |= __ballot_sync(kFull, jr1 + 3 > static_cast<int>(span1));
+      f2 |= __ballot_sync(kFull, jr2 + 3 > static_cast<int>(span2)) & f1;
+      if (((f1 & ~b1) >> lane) & 1u) jf1 = j + 3;
+      if (((f2 & ~b2) >> lane) & 1u) jf2 = j + 3;
+      if (f2 == kFull) break;
       j += 4;
       jr1 += 4;
       jr2 += 4;
+      j0 += 4;
       qp += 4;
       rp += 4;
     }

@@ -28,110 +28,155 @@ namespace eapdtw_b200 {
 // (search.cpp:156-168).  Its bits depend on that exact sequence of roundings,
 // and SURVEY.md A.1 shows any re-association (e.g. prefix sums) misses the
 // 1e-9 distance tolerance.  The chain is therefore reproduced step-for-step:
-// the 100000-slide segments are independent, so one warp owns one segment.
-// Lane 0 runs the dependent chain over a shared-memory tile (2 DADD of latency
-// per step); the other lanes stage the next inputs and convert finished
-// (sum, sumsq) pairs into mean/stddev with correctly rounded div/sqrt
-// (RunningStats::mean/variance/stddev, search.hpp:34-41, search.cpp:35).
+// the 100000-slide segments are independent chains.
+//
+// A chain is a serial dependency (2 DADD of latency per slide), so the kernel
+// is latency-bound: what matters is the slide period and how many chains share
+// an SM.  An FP64 warp instruction occupies the pipe for the whole warp even
+// with one lane active, so kStatsChains chains run side by side in lanes
+// 0..kStatsChains-1 of warp 0 (measured: one chain per warp at 7 warps/SM ran
+// at 49 cycles/slide, FP64-pipe bound; alone it runs at ~20).  Their inputs
+// come from shared memory, one packed 16-byte (in, out) load per slide, and
+// their (sum, sumsq) go back as one 16-byte store (tiles padded against bank
+// conflicts).  Warp 1 keeps the next tile of every chain in flight with
+// cp.async (no register round trip; loading the chains straight from global
+// memory measured 71 cycles/slide, DRAM-latency bound), and warps 1..3
+// convert the previous tile's (sum, sumsq) into mean/stddev with correctly
+// rounded div/sqrt (RunningStats::mean/variance/stddev, search.hpp:34-41,
+// search.cpp:35) and write them out coalesced (per-slide global stores from
+// the chain lanes measured 184 cycles/slide).
 // ---------------------------------------------------------------------------
-constexpr int kStatsTile = 512;
+#ifndef EAPDTW_STATS_CHAINS
+#define EAPDTW_STATS_CHAINS 2
+#endif
+#ifndef EAPDTW_STATS_TILE
+#define EAPDTW_STATS_TILE 256
+#endif
+constexpr int kStatsTile = EAPDTW_STATS_TILE;      // slides per tile
+constexpr int kStatsChains = EAPDTW_STATS_CHAINS;  // segments (chains) per block
+constexpr int kStatsRow = kStatsTile + 1;  // padded tile row (16-byte entries)
 
-// Block of 64 threads per 100000-slide segment, double-buffered tiles:
-//   warp 0 / lane 0 : the dependent chain over tile k (reads IN/OUT, writes SUM/SQ)
-//   warp 1          : stages IN/OUT of tile k+1 and converts tile k-1 to mean/sd
-// One __syncthreads per tile; the chain thread never waits on global memory.
-__global__ void __launch_bounds__(64) stats_chain_kernel(const double* __restrict__ ref, long long n,
-                                                         int m, double* __restrict__ mean_out,
-                                                         double* __restrict__ sd_out) {
-  __shared__ double s_in[2][kStatsTile];
-  __shared__ double s_out[2][kStatsTile];
-  __shared__ double s_sum[2][kStatsTile];
-  __shared__ double s_sq[2][kStatsTile];
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gmem_src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
+__global__ void __launch_bounds__(128) stats_chain_kernel(const double* __restrict__ ref, long long n,
+                                                          int m, double* __restrict__ mean_out,
+                                                          double* __restrict__ sd_out) {
+  extern __shared__ double2 ssm[];
+  double2* s_io = ssm;                                     // [2][chains][row]: (in, out)
+  double2* s_acc = ssm + 2 * kStatsChains * kStatsRow;     // [2][chains][row]: (sum, sumsq)
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const long long ncand = n - m + 1;
-  const long long s0 = static_cast<long long>(blockIdx.x) * kStatsResetInterval;
-  const long long s1 = min(ncand, s0 + kStatsResetInterval);
-  const int ntiles = static_cast<int>((s1 - s0 + kStatsTile - 1) / kStatsTile);
+  const long long nseg = (ncand + kStatsResetInterval - 1) / kStatsResetInterval;
+  const long long seg0 = static_cast<long long>(blockIdx.x) * kStatsChains;
+  const int nch = static_cast<int>(min(static_cast<long long>(kStatsChains), nseg - seg0));
+  // chain 0 is the longest of the block (only the reference's last segment is short)
+  const long long len0 = min(static_cast<long long>(kStatsResetInterval),
+                             ncand - seg0 * kStatsResetInterval);
+  const int ntiles = static_cast<int>((len0 + kStatsTile - 1) / kStatsTile);
+  auto seg_len = [&](int c) -> long long {
+    const long long s0 = (seg0 + c) * kStatsResetInterval;
+    return min(static_cast<long long>(kStatsResetInterval), ncand - s0);
+  };
+  auto tile_cnt = [&](int c, int tile) -> int {
+    const long long t0 = static_cast<long long>(tile) * kStatsTile;
+    return static_cast<int>(max(0LL, min(static_cast<long long>(kStatsTile), seg_len(c) - t0)));
+  };
+
+  auto stage = [&](int tile) {  // warp 1: (in, out) of `tile` for every chain, asynchronously
+    for (int c = 0; c < nch; ++c) {
+      const long long s0 = (seg0 + c) * kStatsResetInterval;
+      const long long t0 = static_cast<long long>(tile) * kStatsTile;
+      const int cnt = tile_cnt(c, tile);
+      double2* io = s_io + ((tile & 1) * kStatsChains + c) * kStatsRow;
+      for (int k = lane; k < cnt; k += 32) {
+        const long long s = s0 + t0 + k;
+        if (s > s0) {
+          cp_async8(&io[k].x, ref + s + m - 1);
+          cp_async8(&io[k].y, ref + s - 1);
+        }
+      }
+    }
+  };
+  // warps 1..3: (sum, sumsq) of `tile` -> mean, stddev (search.hpp:34-41,
+  // search.cpp:35), correctly rounded div/sqrt, written out coalesced
   const double dm = static_cast<double>(m);
+  auto flush = [&](int tile) {
+    const int h = tid - 32;  // 0 .. 95
+    for (int c = 0; c < nch; ++c) {
+      const long long s0 = (seg0 + c) * kStatsResetInterval;
+      const long long t0 = static_cast<long long>(tile) * kStatsTile;
+      const int cnt = tile_cnt(c, tile);
+      const double2* acc = s_acc + ((tile & 1) * kStatsChains + c) * kStatsRow;
+      for (int k = h; k < cnt; k += 96) {
+        const double2 v = acc[k];
+        const double mu = __ddiv_rn(v.x, dm);
+        const double var = __dsub_rn(__ddiv_rn(v.y, dm), __dmul_rn(mu, mu));
+        mean_out[s0 + t0 + k] = mu;
+        sd_out[s0 + t0 + k] = __dsqrt_rn(var > 0.0 ? var : 0.0);
+      }
+    }
+  };
+
+  const bool chain = tid < nch;  // warp 0, lanes 0..nch-1
   double sum = 0.0, sq = 0.0;
-
-  auto stage = [&](int tile) {  // warp 1: IN/OUT of `tile` into buffer tile&1
-    const long long t0 = s0 + static_cast<long long>(tile) * kStatsTile;
-    const int cnt = static_cast<int>(min(static_cast<long long>(kStatsTile), s1 - t0));
-    double* in = s_in[tile & 1];
-    double* out = s_out[tile & 1];
-    for (int k = lane; k < cnt; k += 32) {
-      const long long s = t0 + k;
-      in[k] = s > s0 ? ref[s + m - 1] : 0.0;
-      out[k] = s > s0 ? ref[s - 1] : 0.0;
-    }
-  };
-  auto convert = [&](int tile) {  // warp 1: (sum, sumsq) -> mean, stddev (search.hpp:34-41)
-    const long long t0 = s0 + static_cast<long long>(tile) * kStatsTile;
-    const int cnt = static_cast<int>(min(static_cast<long long>(kStatsTile), s1 - t0));
-    const double* sm = s_sum[tile & 1];
-    const double* sqq = s_sq[tile & 1];
-    for (int k = lane; k < cnt; k += 32) {
-      const double mu = __ddiv_rn(sm[k], dm);
-      const double var = __dsub_rn(__ddiv_rn(sqq[k], dm), __dmul_rn(mu, mu));
-      mean_out[t0 + k] = mu;
-      sd_out[t0 + k] = __dsqrt_rn(var > 0.0 ? var : 0.0);
-    }
-  };
-
-  if (tid == 0) {  // RunningStats::over(ref[s0 : s0+m]) (search.cpp:25-33)
+  int clen = 0;
+  if (chain) {  // RunningStats::over(ref[s0 : s0+m]) (search.cpp:25-33)
+    const long long s0 = (seg0 + tid) * kStatsResetInterval;
+    clen = static_cast<int>(seg_len(tid));
+#pragma unroll 16
     for (int k = 0; k < m; ++k) {
       const double x = ref[s0 + k];
       sum = __dadd_rn(sum, x);
       sq = __dadd_rn(sq, __dmul_rn(x, x));
     }
   }
-  if (tid >= 32) stage(0);
+  const bool stager = tid >= 32 && tid < 64;  // warp 1
+  if (stager) {
+    stage(0);
+    cp_async_wait_all();
+  }
   __syncthreads();
   for (int tile = 0; tile <= ntiles; ++tile) {
-    if (tid == 0 && tile < ntiles) {
-      const long long t0 = s0 + static_cast<long long>(tile) * kStatsTile;
-      const int cnt = static_cast<int>(min(static_cast<long long>(kStatsTile), s1 - t0));
-      const double* in = s_in[tile & 1];
-      const double* out = s_out[tile & 1];
-      double* sm = s_sum[tile & 1];
-      double* sqq = s_sq[tile & 1];
+    if (stager && tile + 1 < ntiles) stage(tile + 1);  // in flight during this tile
+    if (chain && tile < ntiles) {
+      const int t0 = tile * kStatsTile;
+      const int cnt = max(0, min(kStatsTile, clen - t0));
+      const double2* io = s_io + ((tile & 1) * kStatsChains + tid) * kStatsRow;
+      double2* acc = s_acc + ((tile & 1) * kStatsChains + tid) * kStatsRow;
       int k = 0;
-      if (t0 == s0) {  // the segment's first position is the batch over() result
-        sm[0] = sum;
-        sqq[0] = sq;
+      if (t0 == 0 && cnt > 0) {  // the segment's first position is the batch over() result
+        acc[0] = make_double2(sum, sq);
         k = 1;
       }
       // stats.add(in); stats.remove(out) (search.hpp:23-32), 8 steps per batch
       // of hoisted shared-memory loads so only the two DADD chains are exposed.
       for (; k + 8 <= cnt; k += 8) {
-        double a[8], b[8];
+        double2 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = io[k + u];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-          a[u] = in[k + u];
-          b[u] = out[k + u];
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          sum = __dsub_rn(__dadd_rn(sum, a[u]), b[u]);
-          sq = __dsub_rn(__dadd_rn(sq, __dmul_rn(a[u], a[u])), __dmul_rn(b[u], b[u]));
-          sm[k + u] = sum;
-          sqq[k + u] = sq;
+          sum = __dsub_rn(__dadd_rn(sum, v[u].x), v[u].y);
+          sq = __dsub_rn(__dadd_rn(sq, __dmul_rn(v[u].x, v[u].x)), __dmul_rn(v[u].y, v[u].y));
+          acc[k + u] = make_double2(sum, sq);
         }
       }
       for (; k < cnt; ++k) {
-        const double a = in[k], b = out[k];
-        sum = __dsub_rn(__dadd_rn(sum, a), b);
-        sq = __dsub_rn(__dadd_rn(sq, __dmul_rn(a, a)), __dmul_rn(b, b));
-        sm[k] = sum;
-        sqq[k] = sq;
+        const double2 v = io[k];
+        sum = __dsub_rn(__dadd_rn(sum, v.x), v.y);
+        sq = __dsub_rn(__dadd_rn(sq, __dmul_rn(v.x, v.x)), __dmul_rn(v.y, v.y));
+        acc[k] = make_double2(sum, sq);
       }
     }
-    if (tid >= 32) {
-      if (tile + 1 < ntiles) stage(tile + 1);
-      if (tile >= 1) convert(tile - 1);
-    }
+    if (tid >= 32 && tile >= 1) flush(tile - 1);
+    if (stager) cp_async_wait_all();
     __syncthreads();
   }
 }
@@ -140,7 +185,16 @@ cudaError_t launch_stats(const double* ref, long long n, int m, double* mean, do
                          cudaStream_t stream) {
   const long long ncand = n - m + 1;
   const long long nseg = (ncand + kStatsResetInterval - 1) / kStatsResetInterval;
-  stats_chain_kernel<<<static_cast<unsigned>(nseg), 64, 0, stream>>>(ref, n, m, mean, sd);
+  const long long blocks = (nseg + kStatsChains - 1) / kStatsChains;
+  const size_t smem = 4 * static_cast<size_t>(kStatsChains) * kStatsRow * sizeof(double2);
+  static bool configured = false;
+  if (!configured) {
+    const cudaError_t e = cudaFuncSetAttribute(
+        stats_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  stats_chain_kernel<<<static_cast<unsigned>(blocks), 128, smem, stream>>>(ref, n, m, mean, sd);
   return cudaGetLastError();
 }
 
@@ -261,7 +315,7 @@ static __host__ __device__ inline size_t padded_len(int m, int ad_k) {
 
 size_t search_smem_bytes(int m, int warps, int ad_k) {
   return padded_len(m, ad_k) * 8                        // q (padded, 1-based)
-         + static_cast<size_t>(warps) * padded_len(m, ad_k) * 8  // per-warp DP buffers
+         + static_cast<size_t>(warps) * (padded_len(m, ad_k) + kStageExtra) * 8  // per-warp buffers
          + static_cast<size_t>(warps) * kStackBytesPerWarp  // per-warp tier stacks
          + 64;
 }
@@ -316,10 +370,6 @@ __device__ double dtw_dispatch(int ad_k, const RawFn& rowraw, const NormFn& rown
     ++overflows;
     __syncwarp();
   }
-#ifdef EAPDTW_WITH_STRIP2
-  if (!KILL && g_strip_rows == 2)
-    return warp_dtw2(rowraw, rownorm, lr, qsp, lc, w, get_ub, buf, cells);
-#endif
   return warp_dtw<KILL>(rowraw, rownorm, lr, qsp, lc, w, get_ub, rowthr, buf, cells);
 }
 
@@ -329,6 +379,23 @@ __device__ __forceinline__ long long vload(const long long* p) {
 __device__ __forceinline__ unsigned long long vload(const unsigned long long* p) {
   return *reinterpret_cast<const volatile unsigned long long*>(p);
 }
+
+#ifdef EAPDTW_PHASE_CLOCKS
+#define PHASE_BEGIN() const long long _t0 = clock64()
+#define PHASE_END(idx) \
+  if (lane == 0) atomicAdd(&p.counters[idx], static_cast<unsigned long long>(clock64() - _t0))
+#else
+#define PHASE_BEGIN() (void)0
+#define PHASE_END(idx) (void)0
+#endif
+
+#ifdef EAPDTW_PHASE_CLOCKS
+void debug_read_reset(unsigned long long* out8) {
+  cudaMemcpyFromSymbol(out8, g_dbg, 8 * sizeof(unsigned long long));
+  unsigned long long z[8] = {};
+  cudaMemcpyToSymbol(g_dbg, z, sizeof(z));
+}
+#endif
 
 #ifndef EAPDTW_SEARCH_MIN_BLOCKS
 #define EAPDTW_SEARCH_MIN_BLOCKS 2
@@ -351,8 +418,10 @@ __global__ void __launch_bounds__(256, kSearchMinBlocks) search_kernel(SearchPar
   const double2* __restrict__ qperm = p.qperm;
   const int* __restrict__ order = p.order;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* rowbuf = smem + plen + static_cast<size_t>(warp) * plen + pad;
-  int* stacks = reinterpret_cast<int*>(smem + plen + static_cast<size_t>(blockDim.x >> 5) * plen);
+  // per-warp buffer: the DTW row buffer, or the LB_Keogh EQ staging tile
+  const size_t wlen = plen + kStageExtra;
+  double* rowbuf = smem + plen + static_cast<size_t>(warp) * wlen + pad;
+  int* stacks = reinterpret_cast<int*>(smem + plen + static_cast<size_t>(blockDim.x >> 5) * wlen);
 
   const double INF = d_inf();
   for (int k = threadIdx.x; k < static_cast<int>(plen); k += blockDim.x) {
@@ -464,8 +533,69 @@ __global__ void __launch_bounds__(256, kSearchMinBlocks) search_kernel(SearchPar
       const double t = __dsub_rn(__dmul_rn(u, 1.0 + p.guard_rel), cbv);
       return t > 0.0 ? t : 0.0;
     };
+#ifdef EAPDTW_SEARCH_STRIP2
+    // thresholds of a lane's two rows i0+2L, i0+2L+1 (positions k1 = kstrip +
+    // 2L, k2 = k1 + 1): prefix = pre + exclusive scan of the lane pairs
+    auto thr2 = [&](double u, int i0, double& t1, double& t2) {
+      t1 = u;
+      t2 = u;
+      const int kstrip = i0 + p.w - 1;
+      if (!tight || kstrip >= m - 1) return;
+      if (pre_end < 0) {  // positions before the first strip's k
+        pre_end = kstrip;
+        for (int k = lane; k < pre_end; k += 32) {
+          double a, b;
+          contrib(k, a, b);
+          pre_eq = __dadd_rn(pre_eq, a);
+          pre_ec = __dadd_rn(pre_ec, b);
+        }
+        for (int off = 16; off > 0; off >>= 1) {
+          pre_eq = __dadd_rn(pre_eq, __shfl_xor_sync(kFull, pre_eq, off));
+          pre_ec = __dadd_rn(pre_ec, __shfl_xor_sync(kFull, pre_ec, off));
+        }
+      }
+      const int k1 = kstrip + 2 * lane;
+      double a1 = 0.0, b1 = 0.0, a2 = 0.0, b2 = 0.0;
+      if (k1 < m) contrib(k1, a1, b1);
+      if (k1 + 1 < m) contrib(k1 + 1, a2, b2);
+      double sa = __dadd_rn(a1, a2), sb = __dadd_rn(b1, b2);
+      for (int off = 1; off < 32; off <<= 1) {  // inclusive scan of the pair sums
+        const double x = __shfl_up_sync(kFull, sa, off);
+        const double y = __shfl_up_sync(kFull, sb, off);
+        if (lane >= off) {
+          sa = __dadd_rn(sa, x);
+          sb = __dadd_rn(sb, y);
+        }
+      }
+      double ea = __shfl_up_sync(kFull, sa, 1), eb = __shfl_up_sync(kFull, sb, 1);
+      if (lane == 0) ea = eb = 0.0;
+      ea = __dadd_rn(pre_eq, ea);  // prefix through k1 - 1
+      eb = __dadd_rn(pre_ec, eb);
+      const double p1a = __dadd_rn(ea, a1), p1b = __dadd_rn(eb, b1);  // through k1
+      const double p2a = __dadd_rn(pre_eq, sa), p2b = __dadd_rn(pre_ec, sb);  // through k1 + 1
+      const int nxt = min(m, kstrip + 64);
+      const int src = (nxt - 1 - kstrip) >> 1;  // lane holding position nxt - 1 (its k1 or k1+1)
+      pre_eq = __shfl_sync(kFull, p2a, src);
+      pre_ec = __shfl_sync(kFull, p2b, src);
+      pre_end = nxt;
+      auto thr = [&](double pa, double pb, int kk) -> double {
+        if (kk >= m - 1) return u;  // nothing left past k
+        const double cbv = __dsub_rn(fmax(__dsub_rn(teq, pa), __dsub_rn(tec, pb)), cb_guard);
+        if (!(cbv > 0.0)) return u;
+        const double t = __dsub_rn(__dmul_rn(u, 1.0 + p.guard_rel), cbv);
+        return t > 0.0 ? t : 0.0;
+      };
+      t1 = thr(p1a, p1b, k1);
+      t2 = thr(p2a, p2b, k1 + 1);
+    };
+    const double d = AD_K == 0
+                         ? warp_dtw2(rowraw, rownorm, m, qsp, m, p.w, get_ub, thr2, rowbuf, c_cells)
+                         : dtw_dispatch<false>(AD_K, rowraw, rownorm, m, qsp, m, p.w, get_ub,
+                                               rowthr, rowbuf, c_cells, c_ovf);
+#else
     const double d = dtw_dispatch<false>(AD_K, rowraw, rownorm, m, qsp, m, p.w, get_ub, rowthr,
                                          rowbuf, c_cells, c_ovf);
+#endif
     ++c_calls;
     if (d == INF) {
       ++c_aband;
@@ -505,6 +635,7 @@ __global__ void __launch_bounds__(256, kSearchMinBlocks) search_kernel(SearchPar
     const long long nchunks = (p.end - p.begin + span - 1) / span;
     bool chunks_left = true, flushed = false;
     long long myslot = -1;
+    long long my_next = 0, my_end = 0;  // claimed chunk range
     unsigned long long my_chunks = 0;
     // Per-warp compaction stacks between the tiers (local candidate indices):
     // Kim survivors -> [A] -> EQ -> [B] -> EC -> [C] -> phase-A screen -> queue.
@@ -586,7 +717,9 @@ __global__ void __launch_bounds__(256, kSearchMinBlocks) search_kernel(SearchPar
         tot.x = __shfl_sync(kFull, tot.x, 0);
         tot.y = __shfl_sync(kFull, tot.y, 0);
         myslot = -1;
+        PHASE_BEGIN();
         run_dtw(cand, p.use_lb != 0, static_cast<double>(tot.x), static_cast<double>(tot.y));
+        PHASE_END(kClkDtw);
         continue;
       }
       myslot = __shfl_sync(kFull, myslot, 0);
@@ -600,10 +733,16 @@ __global__ void __launch_bounds__(256, kSearchMinBlocks) search_kernel(SearchPar
         // ---- tier 1 on the next chunk of 32 candidates: LB_Kim on the two
         //      aligned extremities (search.cpp:81-87), with the DTW's own IEEE
         //      divisions (exact, so compared without a guard).
-        unsigned long long chunk = 0;
-        if (lane == 0) chunk = atomicAdd(p.work, 1ull);
-        chunk = __shfl_sync(kFull, chunk, 0);
-        if (static_cast<long long>(chunk) >= nchunks) {
+        // chunks are claimed kSuperChunk at a time, so the tier stacks hold
+        // candidates from a short stretch of the reference (EQ staging below)
+        if (my_next >= my_end) {
+          unsigned long long c0 = 0;
+          if (lane == 0) c0 = atomicAdd(p.work, static_cast<unsigned long long>(kSuperChunk));
+          my_next = static_cast<long long>(__shfl_sync(kFull, c0, 0));
+          my_end = my_next + kSuperChunk;
+        }
+        const long long chunk = my_next++;
+        if (chunk >= nchunks) {
           chunks_left = false;  // flush the stacks below, then retire
         } else {
           ++my_chunks;
@@ -636,11 +775,11 @@ __global__ void __launch_bounds__(256, kSearchMinBlocks) search_kernel(SearchPar
       //       normalised by reciprocal multiplication;
       //   EC: query value vs the candidate's (global raw) envelope, normalised.
       // Lanes without a candidate point at p.begin: loads stay in bounds.
-      auto lb_range = [&](auto ec_tag, long long s, bool pending, const double mean,
-                          const double rsd, double ubg, int k0, int k1, double& acc) -> bool {
+      auto lb_range = [&](auto ec_tag, const double* xs, long long s, bool pending,
+                          const double mean, const double rsd, double ubg, int k0, int k1,
+                          double& acc) -> bool {
         constexpr bool EC = decltype(ec_tag)::value;
         bool alive = pending;
-        const double* xs = ref + s;
         const double2* es = EC ? p.env + s : nullptr;
         auto term = [&](int k) {
           const int j = order[k];
@@ -701,8 +840,33 @@ __global__ void __launch_bounds__(256, kSearchMinBlocks) search_kernel(SearchPar
         const double sd = p.sd[s];
         const double rsd = sd < kMinStddev ? 0.0 : __drcp_rn(sd);
         const double ubg = load_ub(p.ub_key) * (1.0 + p.guard_rel) + p.guard_abs;
-        const bool alive =
-            lb_range(ec_tag, s, pending, mean, rsd, ubg, leg2 ? head : 0, leg2 ? m : head, acc);
+        // EQ: stage the batch's stretch of the reference in the warp's buffer
+        // when it fits, so the order[]-permuted reads hit shared memory
+        // instead of L2 (the DP row buffer is free between DTW tasks).
+        const double* xs = ref + s;
+        if (!EC) {
+          int lo = pending ? static_cast<int>(s - p.begin) : INT_MAX;
+          int hi = pending ? static_cast<int>(s - p.begin) : INT_MIN;
+          for (int off = 16; off > 0; off >>= 1) {
+            lo = min(lo, __shfl_xor_sync(kFull, lo, off));
+            hi = max(hi, __shfl_xor_sync(kFull, hi, off));
+          }
+          const long long len = static_cast<long long>(hi) - lo + m;
+#ifdef EAPDTW_PHASE_CLOCKS
+          if (lane == 0) atomicAdd(&p.counters[hi >= lo && len <= static_cast<long long>(wlen)
+                                                   ? kStageHit : kStageMiss], 1ull);
+#endif
+          if (hi >= lo && len <= static_cast<long long>(wlen)) {
+            double* sbuf = rowbuf - pad;
+            const double* src = ref + p.begin + lo;
+            for (int t = lane; t < static_cast<int>(len); t += 32) sbuf[t] = src[t];
+            __syncwarp();
+            if (pending) xs = sbuf + (s - p.begin - lo);
+          }
+        }
+        const bool alive = lb_range(ec_tag, xs, s, pending, mean, rsd, ubg, leg2 ? head : 0,
+                                    leg2 ? m : head, acc);
+        __syncwarp();
         if (pending && !alive) {
           if (EC) ++c_ec;
           else ++c_eq;
@@ -765,7 +929,9 @@ __global__ void __launch_bounds__(256, kSearchMinBlocks) search_kernel(SearchPar
       for (;;) {
         const bool up_a = (nA | nA2) == 0, up_b = up_a && nB == 0, up_c = up_b && nB2 == 0;
         if (nC >= 32 || (flush && nC > 0 && up_c)) {
+          PHASE_BEGIN();
           screen_stage();
+          PHASE_END(kClkScreen);
         } else {
           // one inlined copy per tier (code size: the kernel is i-cache bound)
           int tier = 0;  // 1: EQ, 2: EC
@@ -782,8 +948,10 @@ __global__ void __launch_bounds__(256, kSearchMinBlocks) search_kernel(SearchPar
             tier = 1;
           }
           if (tier == 0) break;
+          PHASE_BEGIN();
           if (tier == 2) stage(std::true_type{}, leg2);
           else stage(std::false_type{}, leg2);
+          PHASE_END(tier == 2 ? kClkEc : kClkEq);
         }
       }
 

@@ -16,6 +16,8 @@ constexpr int kStack = 64;                         // per-warp tier stack capaci
 #define EAPDTW_LB_GROUP 8
 #endif
 constexpr int kLbGroup = EAPDTW_LB_GROUP;          // Keogh positions per abandon vote
+constexpr int kSuperChunk = 4;                     // LB chunks (of 32 candidates) per claim
+constexpr int kStageExtra = 128;                   // extra doubles per warp buffer: EQ staging span
 constexpr int kLbHead = 256;                       // first leg of the Keogh tiers (positions of order[])
 // A, A2, B, B2, C indices; B, B2 EQ totals; C (EQ, EC) totals; A2, B2 partial sums
 constexpr int kStackBytesPerWarp = kStack * (5 * 4 + 2 * 4 + 8 + 2 * 8);
@@ -31,7 +33,17 @@ enum Counter : int {
   kCntCandidates,
   kCntOverflows,
   kCntScreened,
-  kNumCounters
+  kNumCounters,
+  // phase clocks (builds with -DEAPDTW_PHASE_CLOCKS only): warp-cycles per phase
+  kClkDtw = kNumCounters,
+  kClkEq,
+  kClkEc,
+  kClkScreen,
+  kClkKim,
+  kClkWait,
+  kStageHit,
+  kStageMiss,
+  kNumCountersExt
 };
 
 struct SearchParams {
@@ -116,6 +128,9 @@ cudaError_t launch_init_best(BestRecord* rec, unsigned long long* keys, long lon
                              cudaStream_t stream);
 cudaError_t launch_check_finite(const double* x, long long n, unsigned long long* flag,
                                 cudaStream_t stream);
+#ifdef EAPDTW_PHASE_CLOCKS
+void debug_read_reset(unsigned long long* out8);
+#endif
 cudaError_t launch_fp64_probe(double* sink, int blocks, int iters, cudaStream_t stream);
 
 }  // namespace eapdtw_b200
