@@ -739,8 +739,10 @@ int eapdtw_search_plan_result(eapdtw_search_plan* p, eapdtw_search_result* out) 
       std::chrono::duration<double>(std::chrono::steady_clock::now() - p->t0).count();
 #ifdef EAPDTW_PHASE_CLOCKS
   {
-    unsigned long long dbg[8];
+    unsigned long long dbg[16];
     debug_read_reset(dbg);
+    std::fprintf(stderr, "strips/DTW bins [1,2,3-4,5-8,9-16,17+]: calls %llu %llu %llu %llu %llu %llu | steps %llu %llu %llu %llu %llu %llu\n",
+                 dbg[2], dbg[3], dbg[4], dbg[5], dbg[6], dbg[7], dbg[8], dbg[9], dbg[10], dbg[11], dbg[12], dbg[13]);
     std::fprintf(stderr, "strip steps %llu strips %llu cells %llu -> lane eff %.3f\n", dbg[0], dbg[1],
                  cnt[kCntCells], cnt[kCntCells] / (32.0 * dbg[0] + 1));
   }

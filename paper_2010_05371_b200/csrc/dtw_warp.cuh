@@ -45,7 +45,7 @@
 namespace eapdtw_b200 {
 
 #ifdef EAPDTW_PHASE_CLOCKS
-__device__ unsigned long long g_dbg[8];  // strip steps, strips
+__device__ unsigned long long g_dbg[16];  // strip steps, strips, per-bin DTWs / steps
 #endif
 
 constexpr unsigned kFull = 0xffffffffu;
@@ -120,9 +120,14 @@ __device__ double warp_dtw(const RawFn& rowraw, const NormFn& rownorm, int lr,
   double x_next = lane < lr ? rowraw(lane) : 0.0;
   __syncwarp();
 
+#ifdef EAPDTW_PHASE_CLOCKS
+  int dbg_strips = 0;
+  unsigned long long dbg_steps = 0;
+#endif
   for (int i0 = 1; i0 <= lr; i0 += 32) {
 #ifdef EAPDTW_PHASE_CLOCKS
     if (lane == 0) atomicAdd(&g_dbg[1], 1ull);
+    ++dbg_strips;
 #endif
     const double ub_strip = ub_next;
     const int i = i0 + lane;
@@ -195,7 +200,7 @@ __device__ double warp_dtw(const RawFn& rowraw, const NormFn& rownorm, int lr,
       finmask |= __ballot_sync(kFull, jr + 3 > static_cast<int>(span));
       if (((finmask & ~before) >> lane) & 1u) jf = j + 3;
 #ifdef EAPDTW_PHASE_CLOCKS
-      if (lane == 0) atomicAdd(&g_dbg[0], 4ull);
+      dbg_steps += 4;
 #endif
       if (finmask == kFull) break;
       j += 4;
@@ -238,6 +243,14 @@ __device__ double warp_dtw(const RawFn& rowraw, const NormFn& rownorm, int lr,
     lo = nlo;
     hi = nhi;
   }
+#ifdef EAPDTW_PHASE_CLOCKS
+  if (lane == 0) {
+    atomicAdd(&g_dbg[0], dbg_steps);
+    const int bin = dbg_strips <= 1 ? 0 : dbg_strips <= 2 ? 1 : dbg_strips <= 4 ? 2 : dbg_strips <= 8 ? 3 : dbg_strips <= 16 ? 4 : 5;
+    atomicAdd(&g_dbg[2 + bin], 1ull);
+    atomicAdd(&g_dbg[8 + bin], dbg_steps);
+  }
+#endif
   for (int off = 16; off > 0; off >>= 1) cnt += __shfl_xor_sync(kFull, cnt, off);
   if (lane == 0) cells += cnt;
   if (lo < 0 || hi != lc) return INF;

@@ -391,8 +391,8 @@ __device__ __forceinline__ unsigned long long vload(const unsigned long long* p)
 
 #ifdef EAPDTW_PHASE_CLOCKS
 void debug_read_reset(unsigned long long* out8) {
-  cudaMemcpyFromSymbol(out8, g_dbg, 8 * sizeof(unsigned long long));
-  unsigned long long z[8] = {};
+  cudaMemcpyFromSymbol(out8, g_dbg, 16 * sizeof(unsigned long long));
+  unsigned long long z[16] = {};
   cudaMemcpyToSymbol(g_dbg, z, sizeof(z));
 }
 #endif
@@ -757,9 +757,50 @@ __global__ void __launch_bounds__(256, kSearchMinBlocks) search_kernel(SearchPar
             const double c0 = constant ? 0.0 : __ddiv_rn(__dsub_rn(ref[s], mean), sd);
             const double cl = constant ? 0.0 : __ddiv_rn(__dsub_rn(ref[s + m - 1], mean), sd);
             const double kim = __dadd_rn(sq_cost(qsp[1], c0), sq_cost(qsp[m], cl));
-            if (kim > load_ub(p.ub_key)) {
+            const double ub = load_ub(p.ub_key);
+            if (kim > ub) {
               alive = false;
               ++c_kim;
+            } else {
+              // LB_Kim over L points at each end (the UCR-suite form,
+              // extended): a warping path visits one cell of each layer
+              // max(i, j) = k from the start and one of each layer from the
+              // end, so the minimum cost of each layer adds to the corners.
+              // Cells outside the band only lower a minimum.  A sum in another
+              // order than the DTW's, so it prunes with the Keogh guard.  L
+              // grows with m: the layers cost O(L^2) per candidate and pay
+              // off only when what they save (Keogh, DTW) is long.
+              auto layers = [&](auto l_tag) -> double {
+                constexpr int L = decltype(l_tag)::value;
+                double cf[L], cb[L];
+#pragma unroll
+                for (int t = 0; t < L; ++t) {
+                  cf[t] = constant ? 0.0 : __ddiv_rn(__dsub_rn(ref[s + t], mean), sd);
+                  cb[t] = constant ? 0.0 : __ddiv_rn(__dsub_rn(ref[s + m - 1 - t], mean), sd);
+                }
+                double lb = kim;
+#pragma unroll
+                for (int l = 1; l < L; ++l) {
+                  double f = sq_cost(qsp[1 + l], cf[l]);
+                  double bk = sq_cost(qsp[m - l], cb[l]);
+#pragma unroll
+                  for (int t = 0; t < l; ++t) {
+                    f = dmin2(f, dmin2(sq_cost(qsp[1 + l], cf[t]), sq_cost(qsp[1 + t], cf[l])));
+                    bk = dmin2(bk, dmin2(sq_cost(qsp[m - l], cb[t]), sq_cost(qsp[m - t], cb[l])));
+                  }
+                  lb = __dadd_rn(lb, __dadd_rn(f, bk));
+                }
+                return lb;
+              };
+              double kim3 = kim;
+              if (m >= 2 * kKimLayersLong && m >= kKimLongFrom)
+                kim3 = layers(std::integral_constant<int, kKimLayersLong>{});
+              else if (m >= 2 * kKimLayers)
+                kim3 = layers(std::integral_constant<int, kKimLayers>{});
+              if (kim3 > ub * (1.0 + p.guard_rel) + p.guard_abs) {
+                alive = false;
+                ++c_kim;
+              }
             }
           }
           if (p.use_lb) push(stkA, nA, alive, s, nullptr, 0.0, nullptr, 0.0f, nullptr, z2);

@@ -16,6 +16,12 @@ constexpr int kStack = 64;                         // per-warp tier stack capaci
 #define EAPDTW_LB_GROUP 8
 #endif
 constexpr int kLbGroup = EAPDTW_LB_GROUP;          // Keogh positions per abandon vote
+#ifndef EAPDTW_KIM_LAYERS
+#define EAPDTW_KIM_LAYERS 3
+#endif
+constexpr int kKimLayers = EAPDTW_KIM_LAYERS;     // LB_Kim points per end (short queries)
+constexpr int kKimLayersLong = 8;                  // ... for m >= kKimLongFrom
+constexpr int kKimLongFrom = 768;
 constexpr int kSuperChunk = 4;                     // LB chunks (of 32 candidates) per claim
 constexpr int kStageExtra = 128;                   // extra doubles per warp buffer: EQ staging span
 constexpr int kLbHead = 256;                       // first leg of the Keogh tiers (positions of order[])
@@ -129,7 +135,7 @@ cudaError_t launch_init_best(BestRecord* rec, unsigned long long* keys, long lon
 cudaError_t launch_check_finite(const double* x, long long n, unsigned long long* flag,
                                 cudaStream_t stream);
 #ifdef EAPDTW_PHASE_CLOCKS
-void debug_read_reset(unsigned long long* out8);
+void debug_read_reset(unsigned long long* out16);
 #endif
 cudaError_t launch_fp64_probe(double* sink, int blocks, int iters, cudaStream_t stream);
 
