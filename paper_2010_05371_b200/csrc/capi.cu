@@ -145,7 +145,7 @@ struct eapdtw_search_plan {
   cudaEvent_t ev[8] = {};
   bool prepared = false, ran = false;
   int blocks = 0, warps = 8, ad_k = 0, screen_rows = 16;
-  std::vector<int> coarse_strides;  // coarse passes, in order (none: measured slower since the cascade sped up)
+  std::vector<int> coarse_strides{64};  // coarse passes, in order
   bool coarse_blocks = false;           // coarse pass over runs of adjacent candidates
   int probe = 2048;
   double guard_rel = 1e-9, guard_abs = 1e-20;
