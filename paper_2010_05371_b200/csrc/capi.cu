@@ -144,7 +144,7 @@ struct eapdtw_search_plan {
   size_t ncand = 0;
   cudaEvent_t ev[8] = {};
   bool prepared = false, ran = false;
-  int blocks = 0, warps = 8, ad_k = 0, screen_rows = 16;
+  int blocks = 0, warps = 8, ad_k = 0, screen_rows = 8;
   std::vector<int> coarse_strides{64};  // coarse passes, in order
   bool coarse_blocks = false;           // coarse pass over runs of adjacent candidates
   int probe = 2048;
