@@ -513,6 +513,10 @@ static int plan_init(eapdtw_search_plan* p, eapdtw_ctx* c, const double* ref_dev
     return fail(EAPDTW_EINVAL, "search: query length exceeds the shared-memory budget");
   p->warps = best_w;
   p->blocks = sms * best_blocks;
+  if (const char* env = getenv("EAPDTW_WARPS")) {  // experiment: fewer warps per block
+    const int wv = atoi(env);
+    if (wv >= 1 && wv < p->warps) p->warps = wv;
+  }
   return eapdtw_search_plan_reset(p);
 }
 

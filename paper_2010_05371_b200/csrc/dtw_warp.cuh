@@ -170,14 +170,16 @@ __device__ double warp_dtw(const RawFn& rowraw, const NormFn& rownorm, int lr,
     int jr = j - bl;
     int j0 = jb;  // lane 0's column (warp-uniform)
 
-    // One wavefront step at column j+u.
-    auto step = [&](int u) {
+    // One wavefront step at column j+u.  RANGE: apply the band test (a block
+    // of 4 steps with every lane inside its band skips it).
+    auto step = [&](auto range_tag, int u) {
+      constexpr bool RANGE = decltype(range_tag)::value;
       const double sh = __shfl_up_sync(kFull, v, 1);
       const double top = is0 ? rp[u] : sh;
       const double diag = top_prev;
       top_prev = top;
       double nv = __dadd_rn(sq_cost(c, qp[u]), dmin2(v, dmin2(top, diag)));
-      nv = static_cast<unsigned>(jr + u) <= span ? nv : INF;
+      if (RANGE) nv = static_cast<unsigned>(jr + u) <= span ? nv : INF;
       bool dead;
       if (KILL) {
         dead = !(nv <= ub);
@@ -193,11 +195,21 @@ __device__ double warp_dtw(const RawFn& rowraw, const NormFn& rownorm, int lr,
 
     for (;;) {
       const unsigned before = finmask;
-      step(0);
-      step(1);
-      step(2);
-      step(3);
-      finmask |= __ballot_sync(kFull, jr + 3 > static_cast<int>(span));
+#ifdef EAPDTW_STRIP_FASTPATH
+      if (__all_sync(kFull, !active || (jr >= 0 && static_cast<unsigned>(jr) + 3u <= span))) {
+        step(std::false_type{}, 0);
+        step(std::false_type{}, 1);
+        step(std::false_type{}, 2);
+        step(std::false_type{}, 3);
+      } else
+#endif
+      {
+        step(std::true_type{}, 0);
+        step(std::true_type{}, 1);
+        step(std::true_type{}, 2);
+        step(std::true_type{}, 3);
+        finmask |= __ballot_sync(kFull, jr + 3 > static_cast<int>(span));
+      }
       if (((finmask & ~before) >> lane) & 1u) jf = j + 3;
 #ifdef EAPDTW_PHASE_CLOCKS
       dbg_steps += 4;

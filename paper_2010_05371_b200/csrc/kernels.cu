@@ -397,6 +397,9 @@ void debug_read_reset(unsigned long long* out8) {
 }
 #endif
 
+#ifndef EAPDTW_SEARCH_THREADS
+#define EAPDTW_SEARCH_THREADS 256
+#endif
 #ifndef EAPDTW_SEARCH_MIN_BLOCKS
 #define EAPDTW_SEARCH_MIN_BLOCKS 2
 #endif
@@ -405,7 +408,7 @@ constexpr int kSearchMinBlocks = EAPDTW_SEARCH_MIN_BLOCKS;
 // AD_K: anti-diagonal engine window compiled into this instantiation (0: strip
 // engine only -- the default search path, which then needs far fewer registers).
 template <int AD_K>
-__global__ void __launch_bounds__(256, kSearchMinBlocks) search_kernel(SearchParams p) {
+__global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) search_kernel(SearchParams p) {
   extern __shared__ double smem[];
   const int m = p.m;
   const int pad = smem_pad(p.ad_k);
@@ -490,15 +493,25 @@ __global__ void __launch_bounds__(256, kSearchMinBlocks) search_kernel(SearchPar
         p.guard_rel * tmax +
         8.0 * 0x1.0p-52 * (tmax + p.qmax * __dsqrt_rn(static_cast<double>(m) * tmax));
     double pre_eq = 0.0, pre_ec = 0.0;
-    int pre_end = -1;  // prefix sums cover positions [0, pre_end) once started
+    int pre_end = -1;  // (2-rows-per-lane variant) prefixes cover [0, pre_end) once started
+    // Row i's remaining cost: every path still visits every later row
+    // (0-based positions >= i: EQ terms are per candidate position = row),
+    // and every column past i+w (0-based >= i+w: EC terms are per query
+    // position = column).  So the EQ suffix starts w positions earlier than
+    // the reference's single k = min(i+w, m) - 1 (which must also serve EC);
+    // the bound is tighter and still sound.  Each strip extends both
+    // prefixes by 32 positions (one lane each, one warp scan each).
+    int pre_end_eq = -1, pre_end_ec = -1;
     auto rowthr = [&](double u, int i, int i0) -> double {
       if (!tight || i0 < 1 + 32 * (p.cb_strip - 1)) return u;
-      if (pre_end < 0) {  // positions before this strip's first k
-        pre_end = min(m, i0 + p.w - 1);
-        for (int k = lane; k < pre_end; k += 32) {
+      const int k_eq = i0 - 1, k_ec = i0 + p.w - 1;  // lane 0's positions
+      if (pre_end_eq < 0) {  // positions before this strip's first ones
+        pre_end_eq = min(m, k_eq);
+        pre_end_ec = min(m, k_ec);
+        for (int k = lane; k < pre_end_ec; k += 32) {
           double a, b;
           contrib(k, a, b);
-          pre_eq = __dadd_rn(pre_eq, a);
+          if (k < pre_end_eq) pre_eq = __dadd_rn(pre_eq, a);
           pre_ec = __dadd_rn(pre_ec, b);
         }
         for (int off = 16; off > 0; off >>= 1) {
@@ -506,11 +519,12 @@ __global__ void __launch_bounds__(256, kSearchMinBlocks) search_kernel(SearchPar
           pre_ec = __dadd_rn(pre_ec, __shfl_xor_sync(kFull, pre_ec, off));
         }
       }
-      // this strip's rows need prefixes through k = i0 + lane + w - 1
-      const int kk = i0 + lane + p.w - 1;
-      double a = 0.0, b = 0.0;
-      if (kk >= pre_end && kk < m) contrib(kk, a, b);
-      for (int off = 1; off < 32; off <<= 1) {  // inclusive prefix scan
+      // this strip's rows need prefixes through k_eq + lane and k_ec + lane
+      const int ke = k_eq + lane, kc = k_ec + lane;
+      double a = 0.0, b = 0.0, unused;
+      if (ke >= pre_end_eq && ke < m) contrib(ke, a, unused);
+      if (kc >= pre_end_ec && kc < m) contrib(kc, unused, b);
+      for (int off = 1; off < 32; off <<= 1) {  // inclusive prefix scans
         const double x = __shfl_up_sync(kFull, a, off);
         const double y = __shfl_up_sync(kFull, b, off);
         if (lane >= off) {
@@ -520,15 +534,19 @@ __global__ void __launch_bounds__(256, kSearchMinBlocks) search_kernel(SearchPar
       }
       const double peq = __dadd_rn(pre_eq, a), pec = __dadd_rn(pre_ec, b);
       // the next strip starts where this one's rows end
-      const int nxt = min(m, i0 + 32 + p.w - 1);
-      if (nxt > pre_end) {
-        const int src = min(31, nxt - 1 - (i0 + p.w - 1));
-        pre_eq = __shfl_sync(kFull, peq, src);
-        pre_ec = __shfl_sync(kFull, pec, src);
-        pre_end = nxt;
+      const int nxe = min(m, k_eq + 32), nxc = min(m, k_ec + 32);
+      if (nxe > pre_end_eq) {
+        pre_eq = __shfl_sync(kFull, peq, min(31, nxe - 1 - k_eq));
+        pre_end_eq = nxe;
       }
-      if (kk >= m - 1) return u;  // nothing left past k
-      const double cbv = __dsub_rn(fmax(__dsub_rn(teq, peq), __dsub_rn(tec, pec)), cb_guard);
+      if (nxc > pre_end_ec) {
+        pre_ec = __shfl_sync(kFull, pec, min(31, nxc - 1 - k_ec));
+        pre_end_ec = nxc;
+      }
+      if (i >= m) return u;  // the last row: nothing left
+      const double ceq = __dsub_rn(teq, peq);
+      const double cec = kc < m - 1 ? __dsub_rn(tec, pec) : 0.0;
+      const double cbv = __dsub_rn(fmax(ceq, cec), cb_guard);
       if (!(cbv > 0.0)) return u;
       const double t = __dsub_rn(__dmul_rn(u, 1.0 + p.guard_rel), cbv);
       return t > 0.0 ? t : 0.0;
