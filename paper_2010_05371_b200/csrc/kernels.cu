@@ -66,15 +66,16 @@ __device__ __forceinline__ void cp_async_wait_all() {
 
 __global__ void __launch_bounds__(128) stats_chain_kernel(const double* __restrict__ ref, long long n,
                                                           int m, double* __restrict__ mean_out,
-                                                          double* __restrict__ sd_out) {
+                                                          double* __restrict__ sd_out,
+                                                          long long seg_begin, long long seg_end) {
   extern __shared__ double2 ssm[];
   double2* s_io = ssm;                                     // [2][chains][row]: (in, out)
   double2* s_acc = ssm + 2 * kStatsChains * kStatsRow;     // [2][chains][row]: (sum, sumsq)
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const long long ncand = n - m + 1;
-  const long long nseg = (ncand + kStatsResetInterval - 1) / kStatsResetInterval;
-  const long long seg0 = static_cast<long long>(blockIdx.x) * kStatsChains;
+  const long long nseg = seg_end;  // segments [seg_begin, seg_end) of this launch
+  const long long seg0 = seg_begin + static_cast<long long>(blockIdx.x) * kStatsChains;
   const int nch = static_cast<int>(min(static_cast<long long>(kStatsChains), nseg - seg0));
   // chain 0 is the longest of the block (only the reference's last segment is short)
   const long long len0 = min(static_cast<long long>(kStatsResetInterval),
@@ -182,10 +183,12 @@ __global__ void __launch_bounds__(128) stats_chain_kernel(const double* __restri
 }
 
 cudaError_t launch_stats(const double* ref, long long n, int m, double* mean, double* sd,
-                         cudaStream_t stream) {
+                         cudaStream_t stream, long long seg_begin, long long seg_end) {
   const long long ncand = n - m + 1;
   const long long nseg = (ncand + kStatsResetInterval - 1) / kStatsResetInterval;
-  const long long blocks = (nseg + kStatsChains - 1) / kStatsChains;
+  if (seg_end < 0 || seg_end > nseg) seg_end = nseg;
+  if (seg_begin >= seg_end) return cudaSuccess;
+  const long long blocks = (seg_end - seg_begin + kStatsChains - 1) / kStatsChains;
   const size_t smem = 4 * static_cast<size_t>(kStatsChains) * kStatsRow * sizeof(double2);
   static bool configured = false;
   if (!configured) {
@@ -194,7 +197,8 @@ cudaError_t launch_stats(const double* ref, long long n, int m, double* mean, do
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  stats_chain_kernel<<<static_cast<unsigned>(blocks), 128, smem, stream>>>(ref, n, m, mean, sd);
+  stats_chain_kernel<<<static_cast<unsigned>(blocks), 128, smem, stream>>>(ref, n, m, mean, sd,
+                                                                           seg_begin, seg_end);
   return cudaGetLastError();
 }
 
@@ -250,16 +254,17 @@ __device__ void envelope_doubling(const double* __restrict__ ref, long long n, l
 }
 
 __global__ void __launch_bounds__(512) envelope_kernel(const double* __restrict__ ref, long long n,
-                                                       int r, int T, double* __restrict__ env) {
+                                                       int r, int T, double* __restrict__ env,
+                                                       long long tile_begin) {
   extern __shared__ double smem[];
   const int len = T + 2 * r;
-  const long long P0 = static_cast<long long>(blockIdx.x) * T;  // first output
+  const long long P0 = (tile_begin + blockIdx.x) * T;  // first output
   const long long A = P0 - r;                                   // first input
   envelope_doubling<true>(ref, n, A, len, r, T, P0, smem, smem + len, env);
   envelope_doubling<false>(ref, n, A, len, r, T, P0, smem, smem + len, env);
 }
 
-static int envelope_tile(int r) {
+int envelope_tile(int r) {
   // two ping-pong arrays of (T + 2r) doubles within 64 KB (3 blocks per SM)
   const int cap = (64 * 1024) / (2 * 8);
   int T = cap - 2 * r;
@@ -268,15 +273,18 @@ static int envelope_tile(int r) {
 }
 
 cudaError_t launch_envelope(const double* ref, long long n, int r, double* env,
-                            cudaStream_t stream) {
+                            cudaStream_t stream, long long tile_begin, long long tile_end) {
   const int T = envelope_tile(r);
   if (T < 256) return cudaErrorInvalidValue;  // caller disables the EC tier
   const size_t smem = 2 * static_cast<size_t>(T + 2 * r) * sizeof(double);
   cudaError_t e = cudaFuncSetAttribute(envelope_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  const long long blocks = (n + T - 1) / T;
-  envelope_kernel<<<static_cast<unsigned>(blocks), 512, smem, stream>>>(ref, n, r, T, env);
+  const long long ntiles = (n + T - 1) / T;
+  if (tile_end < 0 || tile_end > ntiles) tile_end = ntiles;
+  if (tile_begin >= tile_end) return cudaSuccess;
+  envelope_kernel<<<static_cast<unsigned>(tile_end - tile_begin), 512, smem, stream>>>(
+      ref, n, r, T, env, tile_begin);
   return cudaGetLastError();
 }
 

@@ -115,11 +115,14 @@ struct Nn1Params {
 };
 
 // Each launcher enqueues on `stream` and returns the launch error (no sync).
+// Segments [seg_begin, seg_end) of kStatsResetInterval candidates (-1: all).
 cudaError_t launch_stats(const double* ref, long long n, int m, double* mean, double* sd,
-                         cudaStream_t stream);
-// env: 2n doubles, (max, min) interleaved
+                         cudaStream_t stream, long long seg_begin = 0, long long seg_end = -1);
+// env: 2n doubles, (max, min) interleaved; output tiles [tile_begin, tile_end)
+// of envelope_tile(r) positions (-1: all).  Tile t reads ref[tT - r, (t+1)T + r).
+int envelope_tile(int r);
 cudaError_t launch_envelope(const double* ref, long long n, int r, double* env,
-                            cudaStream_t stream);
+                            cudaStream_t stream, long long tile_begin = 0, long long tile_end = -1);
 size_t search_smem_bytes(int m, int warps, int ad_k);
 // Window parameter of the anti-diagonal engine for a band of half width w
 // over series of length n: the smallest of 1/3/5 whose window 64K covers

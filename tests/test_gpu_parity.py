@@ -409,3 +409,27 @@ def test_tighten_ub_never_changes_the_result(gpu, oracle_lib, m, ratio):
     want2 = oracle_lib.similarity_search(ref2, q, ratio)
     got2 = gpu.similarity_search(ref2, q, gpu.SearchConfig(window_ratio=ratio))
     assert (got2.best.location, got2.best.distance_sq) == (want2.location, want2.distance_sq)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,m,ratio,lb", [(450_000, 128, 0.1, True), (1_234_567, 300, 0.2, True),
+                                          (700_001, 64, 0.05, False), (1_500_000, 256, 0.2, True)])
+def test_streamed_host_search_equals_device_search(gpu, oracle_lib, monkeypatch, n, m, ratio, lb):
+    """The host-pointer search streams long references in two parts (the second
+    part's copy under the first part's sweep): same answer as the oracle and as
+    the unstreamed path, including a best match planted in each part."""
+    ref = gpu.random_walk_normal(n, 90 + m)
+    q = gpu.random_walk_normal(m, 91 + m)
+    cfg = gpu.SearchConfig(window_ratio=ratio, use_lower_bounds=lb, tighten_ub=lb)
+    for plant in (None, n // 5, n - m - 3):
+        r = ref.copy()
+        if plant is not None:
+            r[plant:plant + m] = q * 2.0 - 1.0
+        want = oracle_lib.similarity_search(r, q, ratio, use_lb=lb, tighten=lb)
+        monkeypatch.setenv("EAPDTW_STREAMED", "1")
+        got = gpu.similarity_search(r, q, cfg)
+        monkeypatch.setenv("EAPDTW_STREAMED", "0")
+        plain = gpu.similarity_search(r, q, cfg)
+        assert (got.best.location, got.best.distance_sq) == (want.location, want.distance_sq)
+        assert (plain.best.location, plain.best.distance_sq) == (want.location, want.distance_sq)
+        assert got.report.candidates_total == n - m + 1
