@@ -126,9 +126,10 @@ uint64_t* eapdtw_search_plan_ub_key(eapdtw_search_plan* plan);
 int eapdtw_search_plan_result(eapdtw_search_plan* plan, eapdtw_search_result* out);
 /* Device time in ms of the last prepare/run, per phase: [stats, envelope, probe, sweep]. */
 int eapdtw_search_plan_timings(eapdtw_search_plan* plan, float* ms4);
-/* Raw device counters of the last sweep (9 entries): [kim, keogh_eq, keogh_ec,
- * dtw_calls, dtw_abandoned, cells, candidates, engine_overflows, screened]. */
-int eapdtw_search_plan_counters(eapdtw_search_plan* plan, uint64_t* out9);
+/* Raw device counters of the last sweep (10 entries): [kim, keogh_eq, keogh_ec,
+ * dtw_calls, dtw_abandoned, cells (exact FP64 engine), candidates,
+ * engine_overflows, screened, cells_f32 (FP32 screening engine)]. */
+int eapdtw_search_plan_counters(eapdtw_search_plan* plan, uint64_t* out10);
 int eapdtw_search_plan_destroy(eapdtw_search_plan* plan);
 
 /* --- batched NN1 (cfg5): per query, argmin over the database ------------- *

@@ -370,10 +370,10 @@ class SearchPlan:
         return SearchResult.from_c(res)
 
     def counters(self):
-        out = (C.c_uint64 * 9)()
+        out = (C.c_uint64 * 10)()
         check(lib.eapdtw_search_plan_counters(self.handle, out))
         keys = ["kim", "keogh_eq", "keogh_ec", "dtw_calls", "dtw_abandoned", "cells",
-                "candidates", "engine_overflows", "screened"]
+                "candidates", "engine_overflows", "screened", "cells_f32"]
         return dict(zip(keys, (int(x) for x in out)))
 
     def timings(self):

@@ -147,6 +147,7 @@ struct eapdtw_search_plan {
   cudaEvent_t ev[8] = {};
   bool prepared = false, ran = false;
   int blocks = 0, warps = 8, ad_k = 0, screen_rows = 8;
+  int use_f32 = 1;  // FP32 screening engine ahead of the exact one (EAPDTW_F32=0: off)
   std::vector<int> coarse_strides{64};  // coarse passes, in order
   bool coarse_blocks = false;           // coarse pass over runs of adjacent candidates
   int probe = 2048;
@@ -419,6 +420,7 @@ static int plan_init(eapdtw_search_plan* p, eapdtw_ctx* c, const double* ref_dev
   // opt-in here (EAPDTW_AD_K) and the default for pairwise / NN1 batches.
   p->ad_k = getenv("EAPDTW_AD_K") ? choose_ad_k(static_cast<int>(m), p->w_eff) : 0;
   if (const char* env = getenv("EAPDTW_SCREEN_ROWS")) p->screen_rows = std::max(0, atoi(env));
+  if (const char* env = getenv("EAPDTW_F32")) p->use_f32 = atoi(env) != 0;
   if (const char* env = getenv("EAPDTW_COARSE_STRIDE")) {  // e.g. "512,64" or "512:64"; "0": none
     p->coarse_strides.clear();
     for (const char* t = env; *t;) {
@@ -624,6 +626,16 @@ static SearchParams base_params(eapdtw_search_plan* p) {
   s.ad_k = p->ad_k;
   s.direct = 0;
   s.screen_rows = p->screen_rows;
+  {
+    // z-normalised rows satisfy |c| <= sqrt(m - 1); the engine checks the
+    // bound per strip (degenerate statistics fall back to the exact engine)
+    const double cmax = std::sqrt(static_cast<double>(p->m)) + 1.0;
+    const F32Guard g = make_f32_guard(static_cast<int>(p->m), static_cast<int>(p->m), cmax, p->qmax);
+    s.use_f32 = p->use_f32;
+    s.f32_a = g.a;
+    s.f32_b = g.b;
+    s.f32_cmax = static_cast<float>(cmax);
+  }
   s.counters = B.counters.as<unsigned long long>();
   s.index_offset = static_cast<long long>(p->offset);
   return s;
@@ -776,7 +788,8 @@ int eapdtw_search_plan_result(eapdtw_search_plan* p, eapdtw_search_result* out) 
   out->pruned_keogh_ec = cnt[kCntKeoghEc];
   out->dtw_calls = cnt[kCntDtwCalls];
   out->dtw_abandoned = cnt[kCntDtwAbandoned];
-  out->dp_cells_evaluated = cnt[kCntCells] + pc[kCntCells];
+  // cells of both engines (the FP32 screen and the exact FP64 pass)
+  out->dp_cells_evaluated = cnt[kCntCells] + pc[kCntCells] + cnt[kCntCellsF32] + pc[kCntCellsF32];
   out->elapsed_seconds =
       std::chrono::duration<double>(std::chrono::steady_clock::now() - p->t0).count();
 #ifdef EAPDTW_PHASE_CLOCKS
@@ -797,14 +810,14 @@ int eapdtw_search_plan_result(eapdtw_search_plan* p, eapdtw_search_result* out) 
   return EAPDTW_OK;
 }
 
-int eapdtw_search_plan_counters(eapdtw_search_plan* p, uint64_t* out8) {  // 9 entries
+int eapdtw_search_plan_counters(eapdtw_search_plan* p, uint64_t* out8) {  // 10 entries
   if (!p || !out8) return fail(EAPDTW_EINVAL, "null argument");
   CUDA_TRY(cudaSetDevice(p->ctx->device));
   unsigned long long cnt[kNumCounters];
   CUDA_TRY(cudaMemcpyAsync(cnt, p->buf->counters.p, sizeof(cnt), cudaMemcpyDeviceToHost,
                            p->ctx->stream));
   CUDA_TRY(cudaStreamSynchronize(p->ctx->stream));
-  for (int k = 0; k < 9; ++k) out8[k] = k < kNumCounters ? cnt[k] : 0;
+  for (int k = 0; k < 10; ++k) out8[k] = k < kNumCounters ? cnt[k] : 0;
   return EAPDTW_OK;
 }
 

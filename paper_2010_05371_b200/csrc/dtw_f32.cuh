@@ -1,0 +1,194 @@
+// dtw_f32.cuh -- FP32 screening pass in front of the exact FP64 pruned DTW.
+//
+// Almost every DTW the search starts is abandoned (cfg4: all but ~60 of 3.8 M
+// tasks).  Proving "this candidate's DTW exceeds ub" does not need the exact
+// FP64 value, only a sound bound, so the strip engine of dtw_warp.cuh is run
+// here in FP32 (1 SHFL instead of 2 per step, FMNMX3 instead of 2 DSETP + 4
+// selects, FP32 latency and the 128-lane FP32 pipe) against a threshold that
+// is INFLATED by the worst-case FP32 error.  A candidate this pass abandons
+// is abandoned by the reference too; every other candidate is re-evaluated by
+// the exact FP64 engine (warp_dtw), so results keep the reference's bits.
+//
+// Soundness.  Let P be the argmin path of the FP64 DP
+// (dtw.cpp:115 semantics) and S*(P) the real-arithmetic sum of its exact
+// costs (c_i - q_j)^2 over the FP64 values c_i, q_j.  The FP64 DP value of a
+// cell on P is the rounded sum of P's prefix, so S*(prefix) <= v64 (1 + e64),
+// e64 = (2L + 8) 2^-53, L = lr + lc.  The FP32 pass uses cf = fl32(c') with
+// c' = (x - mean) * rcp(sd) in FP64, |cf - c| <= u' |c|, u' = 2^-24 + 2^-49,
+// and qf = fl32(q).  Each FP32 cost is <= (1+u)^3 (|c - q| + u'(|c|+|q|))^2 and
+// the DP adds one rounding per cell, so by Minkowski's inequality the FP32
+// value of the cell is <= (1+u)^(L+3) (sqrt(S*) + u' sqrt(L) (cmax + qmax))^2.
+// Hence, with the FP64 engine's liveness threshold t of a row,
+//     T32(t) = a (sqrt(t) + b)^2,   a >= (1 + e64)(1+u)^(L+4),
+//                                   b >= u' sqrt(L) (cmax + qmax),
+// evaluated with upward rounding, keeps every cell the FP64 engine would keep
+// on P live.  cmax is enforced per strip: a row value with |cf| > cmax aborts
+// the pass ("undecided", so the FP64 engine runs).
+#pragma once
+#include <cfloat>
+#include <climits>
+#include <cmath>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "dtw_warp.cuh"
+
+namespace eapdtw_b200 {
+
+__device__ __forceinline__ float f_inf() { return __int_as_float(0x7f800000); }
+
+// FP32 three-input minimum (FMNMX3 on sm_100a).
+__device__ __forceinline__ float fmin3f(float a, float b, float c) {
+  float d;
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
+// T32 = a (sqrt(t) + b)^2 rounded up, clamped to FLT_MAX (an infinite or huge
+// threshold never makes a +inf cell live).
+struct F32Guard {
+  float a, b;
+};
+__device__ __forceinline__ float f32_threshold(double t, F32Guard g) {
+  const float tf = __double2float_ru(t);  // +inf when t > FLT_MAX
+  const float s = __fadd_ru(__fsqrt_ru(tf), g.b);
+  return fminf(__fmul_ru(__fmul_ru(s, s), g.a), FLT_MAX);
+}
+
+// Host: the guard constants for series lengths lr, lc and value bounds.
+static inline F32Guard make_f32_guard(int lr, int lc, double cmax, double qmax) {
+  const double L = static_cast<double>(lr) + lc;
+  const double u = 0x1.0p-24, up = 0x1.0p-24 + 0x1.0p-49;
+  const double e64 = (2.0 * L + 8.0) * 0x1.0p-53;
+  // (1+u)^(L+4) <= exp((L+4) u); margins absorb the host's own rounding
+  const double a = (1.0 + e64) * std::exp((L + 4.0) * u) * (1.0 + 0x1.0p-40);
+  const double b = up * std::sqrt(L) * (cmax + qmax) * (1.0 + 0x1.0p-40) + 1e-18;
+  F32Guard g;
+  g.a = std::nextafter(static_cast<float>(a), FLT_MAX);
+  g.b = std::nextafter(static_cast<float>(b), FLT_MAX);
+  return g;
+}
+
+constexpr int kF32Undecided = 1;  // a row value exceeded cmax: run the FP64 engine
+
+// FP32 screening strip engine: the schedule of warp_dtw<false> (dtw_warp.cuh)
+// on floats.  Returns the FP32 value (<= its threshold) or +inf (proven > ub);
+// status = kF32Undecided when a row value exceeded cmax (result meaningless).
+//   rowraw(k)  : raw value of row k (0-based); loaded one strip ahead
+//   rownorm(x) : the row value as float (|value| <= cmax checked here)
+//   qsp        : padded float column series (kPadL / kPadR of +inf)
+//   rowthr(u, i, i0): float threshold of row i given the strip's ub (double)
+//   rowbuf     : padded per-warp float scratch
+template <class RawFn, class NormFn, class UbFn, class RowThrFn>
+__device__ float warp_dtw_f32(const RawFn& rowraw, const NormFn& rownorm, int lr,
+                              const float* __restrict__ qsp, int lc, int w, float cmax,
+                              UbFn&& get_ub, RowThrFn&& rowthr, float* __restrict__ rowbuf,
+                              unsigned long long& cells, int& status) {
+  const int lane = threadIdx.x & 31;
+  const float INF = f_inf();
+  status = 0;
+  for (int k = lane; k <= lc + 1; k += 32) rowbuf[k] = k == 0 ? 0.0f : INF;
+  const bool banded = w < lr;
+  int lo = 0, hi = 0;  // live column range of the row held in rowbuf (row i0-1)
+  int written = 0;
+  unsigned cnt = 0;
+  float ub_last = INF;
+  double ub_next = get_ub();
+  double x_next = lane < lr ? rowraw(lane) : 0.0;
+  __syncwarp();
+
+  for (int i0 = 1; i0 <= lr; i0 += 32) {
+    const double ub_strip = ub_next;
+    const int i = i0 + lane;
+    const bool active = i <= lr;
+    const double x = x_next;
+    if (i0 + 32 <= lr) {
+      ub_next = get_ub();
+      x_next = i + 32 <= lr ? rowraw(i + 31) : 0.0;
+    }
+    const float ub = rowthr(ub_strip, i, i0);
+    const int wl = min(31, lr - i0);
+    ub_last = __shfl_sync(kFull, ub, wl);
+    const float c = active ? rownorm(x) : INF;
+    if (__any_sync(kFull, active && !(fabsf(c) <= cmax))) {
+      status = kF32Undecided;
+      break;
+    }
+    const int jb = max(lo, 1);
+    const int bl = banded ? max(1, i - w) : 1;
+    const int bh = active ? (banded ? min(lc, i + w) : lc) : -1;
+    float top_prev = (lane == 0 && jb - 1 >= lo && jb - 1 <= hi) ? rowbuf[jb - 1] : INF;
+    int j = jb - lane;
+    const float* qp = qsp + j;
+    float* rp = rowbuf + j;
+    float v = INF;
+    unsigned finmask = __ballot_sync(kFull, !active);
+    int jf = active ? lc + 1 : j - 1;
+    const bool writer = lane == wl;
+    const bool is0 = lane == 0;
+    const unsigned span = static_cast<unsigned>(bh - bl);
+    int jr = j - bl;
+    int j0 = jb;
+
+    auto step = [&](int u) {
+      const float sh = __shfl_up_sync(kFull, v, 1);
+      const float top = is0 ? rp[u] : sh;
+      const float diag = top_prev;
+      top_prev = top;
+      const float d = __fsub_rn(c, qp[u]);
+      float nv = __fadd_rn(__fmul_rn(d, d), fmin3f(v, top, diag));
+      nv = static_cast<unsigned>(jr + u) <= span ? nv : INF;
+      if (writer) rp[u] = nv;
+      v = nv;
+      const unsigned dm = __ballot_sync(kFull, nv > ub);
+      finmask |= dm & ((finmask << 1) | (j0 + u > hi ? 1u : 0u));
+    };
+
+    for (;;) {
+      const unsigned before = finmask;
+      step(0);
+      step(1);
+      step(2);
+      step(3);
+      finmask |= __ballot_sync(kFull, jr + 3 > static_cast<int>(span));
+      if (((finmask & ~before) >> lane) & 1u) jf = j + 3;
+      if (finmask == kFull) break;
+      j += 4;
+      jr += 4;
+      j0 += 4;
+      qp += 4;
+      rp += 4;
+    }
+    const int wend = jb - wl + (j - (jb - lane)) + 3;
+    for (int k = max(wend + 1, 0) + lane; k <= written; k += 32) rowbuf[k] = INF;
+    written = min(max(wend, 0), lc + 1);
+    const int c0 = max(jb, bl), c1 = min(jf, bh);
+    cnt += active && c1 >= c0 ? static_cast<unsigned>(c1 - c0 + 1) : 0u;
+    __syncwarp();
+    const int wcol1 = min(wend, lc);
+    int nlo = INT_MAX, nhi = -1;
+    for (int k0 = jb; k0 <= wcol1; k0 += 32) {
+      const int k = k0 + lane;
+      const bool lv = k <= wcol1 && rowbuf[k] <= ub_last;
+      const unsigned bm = __ballot_sync(kFull, lv);
+      if (bm) {
+        if (nlo == INT_MAX) nlo = k0 + __ffs(bm) - 1;
+        nhi = k0 + 31 - __clz(bm);
+      }
+    }
+    if (nhi < 0) {
+      lo = -1;
+      break;
+    }
+    lo = nlo;
+    hi = nhi;
+  }
+  for (int off = 16; off > 0; off >>= 1) cnt += __shfl_xor_sync(kFull, cnt, off);
+  if (lane == 0) cells += cnt;
+  __syncwarp();
+  if (status != 0 || lo < 0 || hi != lc) return INF;
+  const float r = rowbuf[lc];
+  return r <= ub_last ? r : INF;
+}
+
+}  // namespace eapdtw_b200

@@ -325,6 +325,7 @@ size_t search_smem_bytes(int m, int warps, int ad_k) {
   return padded_len(m, ad_k) * 8                        // q (padded, 1-based)
          + static_cast<size_t>(warps) * (padded_len(m, ad_k) + kStageExtra) * 8  // per-warp buffers
          + static_cast<size_t>(warps) * kStackBytesPerWarp  // per-warp tier stacks
+         + (padded_len(m, ad_k) * 4 + 7) / 8 * 8              // q as float (FP32 screen)
          + 64;
 }
 
@@ -433,17 +434,26 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
   const size_t wlen = plen + kStageExtra;
   double* rowbuf = smem + plen + static_cast<size_t>(warp) * wlen + pad;
   int* stacks = reinterpret_cast<int*>(smem + plen + static_cast<size_t>(blockDim.x >> 5) * wlen);
+  // the query as float (FP32 screen), after the stacks; padded like qsp
+  float* q32base = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(stacks) +
+                                            static_cast<size_t>(blockDim.x >> 5) * kStackBytesPerWarp);
+  const float* qsp32 = q32base + pad;
+  // The FP32 engine's row buffer aliases the warp's FP64 one (both engines
+  // initialise [0, lc+1] on entry and never depend on the padding contents:
+  // out-of-band cells are +inf by the band test).
+  float* rowbuf32 = reinterpret_cast<float*>(rowbuf);
 
   const double INF = d_inf();
   for (int k = threadIdx.x; k < static_cast<int>(plen); k += blockDim.x) {
     const int j = k - pad;
     smem[k] = (j >= 1 && j <= m) ? p.q[j] : INF;
+    q32base[k] = (j >= 1 && j <= m) ? __double2float_rn(p.q[j]) : f_inf();
   }
   for (int k = lane; k < static_cast<int>(plen); k += 32) rowbuf[k - pad] = INF;
   __syncthreads();
 
   unsigned long long c_kim = 0, c_eq = 0, c_ec = 0, c_calls = 0, c_aband = 0, c_cells = 0,
-                     c_cand = 0, c_ovf = 0, c_scr = 0, c_cells_lane = 0;
+                     c_cand = 0, c_ovf = 0, c_scr = 0, c_cells_lane = 0, c_cells32 = 0;
   const double* __restrict__ ref = p.ref;
   const bool prune = p.prune != 0;
 
@@ -619,8 +629,30 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
                          : dtw_dispatch<false>(AD_K, rowraw, rownorm, m, qsp, m, p.w, get_ub,
                                                rowthr, rowbuf, c_cells, c_ovf);
 #else
-    const double d = dtw_dispatch<false>(AD_K, rowraw, rownorm, m, qsp, m, p.w, get_ub, rowthr,
-                                         rowbuf, c_cells, c_ovf);
+    // FP32 screen first (dtw_f32.cuh) once a finite threshold exists: it
+    // abandons with a sound, error-inflated threshold; whatever it cannot
+    // abandon is evaluated exactly below.
+    bool screened = false;
+    if (p.use_f32 && prune && __shfl_sync(kFull, load_ub(p.ub_key), 0) < INF) {
+      const F32Guard g{p.f32_a, p.f32_b};
+      auto rownorm32 = [&](double x) -> float {
+        return cconst ? 0.0f : __double2float_rn(__dmul_rn(__dsub_rn(x, cm), rsd));
+      };
+      auto rowthr32 = [&](double u, int i, int i0) -> float {
+        return f32_threshold(rowthr(u, i, i0), g);
+      };
+      int st = 0;
+      const float r32 = warp_dtw_f32(rowraw, rownorm32, m, qsp32, m, p.w, p.f32_cmax, get_ub,
+                                     rowthr32, rowbuf32, c_cells32, st);
+      screened = st == 0 && r32 == f_inf();
+      // the cumulative-bound prefixes restart for the exact pass
+      pre_eq = pre_ec = 0.0;
+      pre_end_eq = pre_end_ec = -1;
+      __syncwarp();
+    }
+    const double d = screened ? INF
+                              : dtw_dispatch<false>(AD_K, rowraw, rownorm, m, qsp, m, p.w, get_ub,
+                                                    rowthr, rowbuf, c_cells, c_ovf);
 #endif
     ++c_calls;
     if (d == INF) {
@@ -1055,6 +1087,7 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
     atomicAdd(&p.counters[kCntCandidates], c_cand);
     atomicAdd(&p.counters[kCntOverflows], c_ovf);
     atomicAdd(&p.counters[kCntScreened], c_scr);
+    atomicAdd(&p.counters[kCntCellsF32], c_cells32);
   }
 }
 

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include "dtw_warp.cuh"
+#include "dtw_f32.cuh"
 
 namespace eapdtw_b200 {
 
@@ -23,7 +24,7 @@ constexpr int kKimLayers = EAPDTW_KIM_LAYERS;     // LB_Kim points per end (shor
 constexpr int kKimLayersLong = 8;                  // ... for m >= kKimLongFrom
 constexpr int kKimLongFrom = 768;
 constexpr int kSuperChunk = 4;                     // LB chunks (of 32 candidates) per claim
-constexpr int kStageExtra = 128;                   // extra doubles per warp buffer: EQ staging span
+constexpr int kStageExtra = 64;                    // extra doubles per warp buffer: EQ staging span
 constexpr int kLbHead = 256;                       // first leg of the Keogh tiers (positions of order[])
 // A, A2, B, B2, C indices; B, B2 EQ totals; C (EQ, EC) totals; A2, B2 partial sums
 constexpr int kStackBytesPerWarp = kStack * (5 * 4 + 2 * 4 + 8 + 2 * 8);
@@ -39,6 +40,7 @@ enum Counter : int {
   kCntCandidates,
   kCntOverflows,
   kCntScreened,
+  kCntCellsF32,  // cells evaluated by the FP32 screening engine
   kNumCounters,
   // phase clocks (builds with -DEAPDTW_PHASE_CLOCKS only): warp-cycles per phase
   kClkDtw = kNumCounters,
@@ -83,6 +85,8 @@ struct SearchParams {
   int ad_k;                      // anti-diagonal engine window 64*ad_k (0: strip engine only)
   int direct;                    // 1: every candidate is a DTW task (the probe)
   int screen_rows;               // phase-A lane screen depth (0: off)
+  int use_f32;                   // FP32 screening engine ahead of the exact FP64 one
+  float f32_a, f32_b, f32_cmax;  // its threshold guard (dtw_f32.cuh) and row-value bound
   unsigned long long* counters;  // kNumCounters
   long long index_offset;        // shard start in the global reference
 };
