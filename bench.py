@@ -43,6 +43,26 @@ BATCH_CONFIGS = {
             "L=512, unbounded band, running cutoff per query; NN1",
 }
 FP64_OPS_PER_CELL = 5  # DSUB, DMUL, DADD + 2 DSETP (min3) per counted cell
+FP32_OPS_PER_CELL = 4  # FSUB, FMUL, FADD + 1 FMNMX3 per counted cell of the FP32 screen
+
+
+def mixed_roofline(cells64, cells32, seconds, p64, p32, kernel):
+    """Issue roofline over both DTW engines: achieved = FP ops / time; frac = the
+    time the FP pipes would need at their measured peaks / the measured time
+    (so peak = achieved / frac is the cell-mix-weighted peak)."""
+    ops = FP64_OPS_PER_CELL * cells64 + FP32_OPS_PER_CELL * cells32
+    busy = FP64_OPS_PER_CELL * cells64 / p64 + FP32_OPS_PER_CELL * cells32 / p32
+    frac = busy / seconds
+    achieved = ops / seconds
+    bound = "fp32" if FP32_OPS_PER_CELL * cells32 / p32 > FP64_OPS_PER_CELL * cells64 / p64 else "fp64"
+    return {"bound": bound, "achieved": achieved / 1e12, "peak": achieved / frac / 1e12 if frac else None,
+            "unit": "TFLOP/s", "frac": frac, "traffic": None, "kernel": kernel,
+            "cells_fp64": cells64, "cells_fp32": cells32,
+            "peak_fp64": p64 / 1e12, "peak_fp32": p32 / 1e12,
+            "note": "CUDA-core issue roofline: 5 FP64-pipe ops per counted cell of the exact "
+                    "FP64 engine, 4 FP32 ops per counted cell of the FP32 screening engine; "
+                    "peaks = DADD / FADD rates measured on this GPU in this run; frac = "
+                    "(time at peak) / measured time"}
 
 
 def band_cells(m: int, w: int) -> int:
@@ -276,16 +296,15 @@ def run_batch(args):
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / args.steps
     value = n_units / (ms * 1e-3)
-    peak = ctx.fp64_peak()
-    achieved = FP64_OPS_PER_CELL * cells / (ms * 1e-3)
+    cells32 = ctx.last_cells_f32 if cfg != "cfg1" else 0
+    roof = mixed_roofline(cells - cells32, cells32, ms * 1e-3, ctx.fp64_peak(), ctx.fp32_peak(),
+                          "pairwise_kernel" if cfg == "cfg1" else "nn1_kernel")
     line = {"metric": unit.replace("/s", " per second"), "value": value, "unit": unit,
             "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic z-normalised N(0,1) random walks",
             "config": {"workload": BATCH_CONFIGS[cfg]},
-            "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak / 1e12,
-                         "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
-                         "kernel": "pairwise_kernel" if cfg == "cfg1" else "nn1_kernel"},
+            "roofline": roof,
             "e2e": {"value": e2e, "unit": unit,
                     "h2d_bytes_per_step": int((a.nbytes + b.nbytes) * 2) if cfg == "cfg1"
                     else int(qs.nbytes + db.nbytes),
@@ -342,6 +361,7 @@ def main():
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
     fp64_peak = ctx.fp64_peak()  # measured DADD issue rate (ops/s) on this GPU
+    fp32_peak = ctx.fp32_peak()  # measured FADD issue rate (ops/s)
 
     dref = torch.from_numpy(ref[s0:s0 + npts]).to(f"cuda:{local}")
     key = torch.full((1,), 0, dtype=torch.int64, device=f"cuda:{local}")
@@ -361,6 +381,7 @@ def main():
     launches0 = ctx.launches
     phases = []
     cells = []
+    sweep_cnt = []
     results = []
     barrier()
     torch.cuda.synchronize()
@@ -372,6 +393,7 @@ def main():
             best, res = runner.search()
             phases.append(shard.plan.timings())
             cells.append(res.report.dp_cells_evaluated)
+            sweep_cnt.append(shard.plan.counters())
             results.append(best)
         e1.record(stream)
         torch.cuda.synchronize()
@@ -387,7 +409,9 @@ def main():
     # ---- roofline of the dominant kernel (the sweep: LB tiers + pruned DTW)
     sweep_ms = statistics.mean(p["sweep"] for p in phases)
     cells_mean = statistics.mean(cells)
-    achieved = FP64_OPS_PER_CELL * cells_mean / (sweep_ms * 1e-3)
+    c64 = statistics.mean(c["cells"] for c in sweep_cnt)
+    c32 = statistics.mean(c["cells_f32"] for c in sweep_cnt)
+    roof = mixed_roofline(c64, c32, sweep_ms * 1e-3, fp64_peak, fp32_peak, "search_kernel (sweep)")
     phase_ms = {k: statistics.mean(p[k] for p in phases) for k in phases[0]}
 
     # ---- e2e: the public API with host buffers (pinned), H2D + search + D2H every step
@@ -454,11 +478,7 @@ def main():
                        "l2": "inputs larger than L2 (800 MB reference vs 126 MB L2)"
                        if n * 8 > 126e6 else "reference smaller than L2",
                        "batches_per_search": runner.batches},
-            "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": fp64_peak / 1e12,
-                         "unit": "TFLOP/s", "frac": achieved / fp64_peak, "traffic": traffic,
-                         "kernel": "search_kernel (sweep)",
-                         "note": "FP64 CUDA-core issue roofline: 5 FP64-pipe ops per counted DTW "
-                                 "cell; peak = DADD rate measured on this GPU (eapdtw_fp64_peak)"},
+            "roofline": dict(roof, traffic=traffic),
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "subsequences/s",
                     "h2d_bytes_per_step": npts * 8 + m * 8, "d2h_bytes_per_step": 88},

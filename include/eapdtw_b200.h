@@ -73,6 +73,9 @@ int eapdtw_ctx_set_stream(eapdtw_ctx* ctx, void* cuda_stream);
 int eapdtw_ctx_synchronize(eapdtw_ctx* ctx);
 /* Number of kernels this context has launched (gpu_launches accounting). */
 uint64_t eapdtw_ctx_launches(const eapdtw_ctx* ctx);
+/* Cells of the last eapdtw_nn1(_dev) call evaluated by the FP32 screening
+ * engine (included in that call's *cells total). */
+uint64_t eapdtw_ctx_last_cells_f32(const eapdtw_ctx* ctx);
 
 /* --- DTW kernels, one pair (dtw.hpp:69-99) ------------------------------- *
  * ea_pruned_dtw_windowed(a, b, Band{window}, ub, cumulative_bound)  dtw.hpp:93-99
@@ -152,6 +155,8 @@ int eapdtw_random_walk_normal(size_t n, uint64_t seed, double* out);
 /* --- measurement ------------------------------------------------------------ */
 /* Measured FP64 (DADD) issue rate of this device in ops/s (the DTW roofline). */
 int eapdtw_fp64_peak(eapdtw_ctx* ctx, double* ops_per_s);
+/* Measured FP32 add issue rate (ops/s): the roofline of the FP32 screening engine. */
+int eapdtw_fp32_peak(eapdtw_ctx* ctx, double* ops_per_s);
 
 #ifdef __cplusplus
 }

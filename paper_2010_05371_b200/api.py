@@ -188,6 +188,16 @@ class Context:
         check(lib.eapdtw_fp64_peak(self.handle, C.byref(v)))
         return v.value
 
+    def fp32_peak(self) -> float:
+        v = C.c_double()
+        check(lib.eapdtw_fp32_peak(self.handle, C.byref(v)))
+        return v.value
+
+    @property
+    def last_cells_f32(self) -> int:
+        """FP32-screen share of the last nn1 call's cells."""
+        return int(lib.eapdtw_ctx_last_cells_f32(self.handle))
+
 
 _tls = threading.local()
 

@@ -122,6 +122,7 @@ struct eapdtw_ctx {
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
   uint64_t launches = 0;
+  uint64_t last_cells_f32 = 0;  // FP32-screen share of the last nn1 call's cells
   // scratch for pairwise / nn1 host-pointer variants
   DevBuf a, b, ub, cb, out, cells, best, keys, counters;
   DevBuf ref;  // host-pointer search copies the reference here
@@ -993,8 +994,8 @@ static int nn1_impl(eapdtw_ctx* c, const double* q_dev, size_t nq, const double*
   cudaStream_t s = c->stream;
   CUDA_TRY(c->best.ensure(nq * sizeof(BestRecord)));
   CUDA_TRY(c->keys.ensure(nq * 8));
-  CUDA_TRY(c->counters.ensure(2 * 8));
-  CUDA_TRY(cudaMemsetAsync(c->counters.p, 0, 16, s));
+  CUDA_TRY(c->counters.ensure(3 * 8));
+  CUDA_TRY(cudaMemsetAsync(c->counters.p, 0, 24, s));
   CUDA_TRY(launch_init_best(c->best.as<BestRecord>(), c->keys.as<unsigned long long>(),
                             static_cast<long long>(nq), s));
   ++c->launches;
@@ -1013,15 +1014,26 @@ static int nn1_impl(eapdtw_ctx* c, const double* q_dev, size_t nq, const double*
   p.ad_k = choose_ad_k(static_cast<int>(len), w);
   p.ub_keys = c->keys.as<unsigned long long>();
   p.best = c->best.as<BestRecord>();
-  p.cells = c->counters.as<unsigned long long>();
-  p.dtw_calls = c->counters.as<unsigned long long>() + 1;
+  p.cells = c->counters.as<unsigned long long>();  // [FP64 cells, FP32 cells]
+  p.dtw_calls = c->counters.as<unsigned long long>() + 2;
+  {
+    // FP32 screen (dtw_f32.cuh) for z-normalised data: |values| <= sqrt(len)
+    // + 1, checked per query (block) and per strip of database rows.
+    const double cmax = std::sqrt(static_cast<double>(len)) + 1.0;
+    const F32Guard g = make_f32_guard(static_cast<int>(len), static_cast<int>(len), cmax, cmax);
+    p.use_f32 = 1;
+    if (const char* env = getenv("EAPDTW_F32")) p.use_f32 = atoi(env) != 0;
+    p.f32_a = g.a;
+    p.f32_b = g.b;
+    p.f32_cmax = static_cast<float>(cmax);
+  }
   CUDA_TRY(set_strip_rows(s));
   CUDA_TRY(launch_nn1(p, s));
   ++c->launches;
   std::vector<BestRecord> rec(nq);
-  unsigned long long cnt[2];
+  unsigned long long cnt[3];
   CUDA_TRY(cudaMemcpyAsync(rec.data(), c->best.p, nq * sizeof(BestRecord), cudaMemcpyDeviceToHost, s));
-  CUDA_TRY(cudaMemcpyAsync(cnt, c->counters.p, 16, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(cnt, c->counters.p, 24, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
   for (size_t i = 0; i < nq; ++i) {
     if (rec[i].d == kInf) {  // nothing within the band: index 0, +inf (strict < never fired)
@@ -1032,9 +1044,12 @@ static int nn1_impl(eapdtw_ctx* c, const double* q_dev, size_t nq, const double*
       dist[i] = rec[i].d;
     }
   }
-  if (cells) *cells = cnt[0];
+  if (cells) *cells = cnt[0] + cnt[1];  // both engines
+  c->last_cells_f32 = cnt[1];
   return EAPDTW_OK;
 }
+
+uint64_t eapdtw_ctx_last_cells_f32(const eapdtw_ctx* c) { return c ? c->last_cells_f32 : 0; }
 
 int eapdtw_nn1_dev(eapdtw_ctx* c, const double* q_dev, size_t nq, const double* db_dev, size_t nd,
                    size_t len, size_t window, uint64_t* argmin, double* dist, uint64_t* cells) {
@@ -1100,7 +1115,7 @@ int eapdtw_random_walk_normal(size_t n, uint64_t seed, double* out) {
   return EAPDTW_OK;
 }
 
-int eapdtw_fp64_peak(eapdtw_ctx* c, double* ops) {
+static int fp_peak(eapdtw_ctx* c, int bits, double* ops) {
   if (!c || !ops) return fail(EAPDTW_EINVAL, "null argument");
   CUDA_TRY(cudaSetDevice(c->device));
   int sms = 148;
@@ -1114,7 +1129,8 @@ int eapdtw_fp64_peak(eapdtw_ctx* c, double* ops) {
   float best = 1e30f;
   for (int rep = 0; rep < 3; ++rep) {
     CUDA_TRY(cudaEventRecord(e0, c->stream));
-    CUDA_TRY(launch_fp64_probe(sink.as<double>(), blocks, iters, c->stream));
+    if (bits == 64) CUDA_TRY(launch_fp64_probe(sink.as<double>(), blocks, iters, c->stream));
+    else CUDA_TRY(launch_fp32_probe(sink.as<float>(), blocks, iters, c->stream));
     ++c->launches;
     CUDA_TRY(cudaEventRecord(e1, c->stream));
     CUDA_TRY(cudaEventSynchronize(e1));
@@ -1128,5 +1144,8 @@ int eapdtw_fp64_peak(eapdtw_ctx* c, double* ops) {
   *ops = static_cast<double>(blocks) * 256.0 * iters * 8.0 / (best * 1e-3);
   return EAPDTW_OK;
 }
+
+int eapdtw_fp64_peak(eapdtw_ctx* c, double* ops) { return fp_peak(c, 64, ops); }
+int eapdtw_fp32_peak(eapdtw_ctx* c, double* ops) { return fp_peak(c, 32, ops); }
 
 }  // extern "C"

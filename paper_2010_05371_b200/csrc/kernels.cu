@@ -406,6 +406,9 @@ void debug_read_reset(unsigned long long* out8) {
 }
 #endif
 
+#ifndef EAPDTW_F32_ROWS
+#define EAPDTW_F32_ROWS 1
+#endif
 #ifndef EAPDTW_SEARCH_THREADS
 #define EAPDTW_SEARCH_THREADS 256
 #endif
@@ -642,8 +645,13 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
         return f32_threshold(rowthr(u, i, i0), g);
       };
       int st = 0;
+#if EAPDTW_F32_ROWS == 2  // two rows per lane (experiment)
+      const float r32 = warp_dtw2_f32(rowraw, rownorm32, m, qsp32, m, p.w, p.f32_cmax, get_ub,
+                                      rowthr32, rowbuf32, c_cells32, st);
+#else
       const float r32 = warp_dtw_f32(rowraw, rownorm32, m, qsp32, m, p.w, p.f32_cmax, get_ub,
                                      rowthr32, rowbuf32, c_cells32, st);
+#endif
       screened = st == 0 && r32 == f_inf();
       // the cumulative-bound prefixes restart for the exact pass
       pre_eq = pre_ec = 0.0;
@@ -1196,18 +1204,31 @@ __global__ void __launch_bounds__(256) nn1_kernel(Nn1Params p) {
   const long long qi = blockIdx.x / p.splits;
   const int part = blockIdx.x % p.splits;
   const long long k0 = p.nd * part / p.splits, k1 = p.nd * (part + 1) / p.splits;
+  __shared__ int s_qbig;  // some |q| > f32_cmax: no FP32 screen for this query
   double* qsp = smem + pad;  // padded, 1-based
   double* rowbuf = smem + plen + static_cast<size_t>(warp) * plen + pad;
+  float* q32base = reinterpret_cast<float*>(smem + static_cast<size_t>(blockDim.x / 32 + 1) * plen);
+  const float* qsp32 = q32base + pad;
+  float* rowbuf32 = reinterpret_cast<float*>(rowbuf);  // aliases the FP64 row (dtw_f32.cuh)
   const double INF = d_inf();
+  if (threadIdx.x == 0) {
+    s_next = 0;
+    s_qbig = 0;
+  }
+  __syncthreads();
   for (int k = threadIdx.x; k < static_cast<int>(plen); k += blockDim.x) {
     const int j = k - pad;
-    smem[k] = (j >= 1 && j <= L) ? p.queries[qi * L + j - 1] : INF;
+    const double qv = (j >= 1 && j <= L) ? p.queries[qi * L + j - 1] : INF;
+    smem[k] = qv;
+    q32base[k] = (j >= 1 && j <= L) ? __double2float_rn(qv) : f_inf();
+    if (j >= 1 && j <= L && !(fabs(qv) <= static_cast<double>(p.f32_cmax))) s_qbig = 1;
   }
   for (int k = lane; k < static_cast<int>(plen); k += 32) rowbuf[k - pad] = INF;
-  if (threadIdx.x == 0) s_next = 0;
   __syncthreads();
+  const bool use_f32 = p.use_f32 != 0 && s_qbig == 0;
+  const F32Guard g{p.f32_a, p.f32_b};
   unsigned long long* key = p.ub_keys + qi;
-  unsigned long long cells = 0, calls = 0, ovf = 0;
+  unsigned long long cells = 0, cells32 = 0, calls = 0, ovf = 0;
   for (;;) {
     unsigned long long t = 0;
     if (lane == 0) t = atomicAdd(&s_next, 1ull);
@@ -1224,8 +1245,19 @@ __global__ void __launch_bounds__(256) nn1_kernel(Nn1Params p) {
     auto rownorm = [](double x) -> double { return x; };
     auto get_ub = [&]() -> double { return load_ub(key); };
     auto rowthr = [](double u, int, int) -> double { return u; };
-    const double d = dtw_dispatch<false>(p.ad_k, rowraw, rownorm, L, qsp, L, p.w, get_ub, rowthr,
-                                         rowbuf, cells, ovf);
+    bool screened = false;
+    if (use_f32 && __shfl_sync(kFull, ub, 0) < INF) {  // FP32 screen (dtw_f32.cuh)
+      auto rownorm32 = [](double x) -> float { return __double2float_rn(x); };
+      auto rowthr32 = [&](double u, int, int) -> float { return f32_threshold(u, g); };
+      int st = 0;
+      const float r32 = warp_dtw_f32(rowraw, rownorm32, L, qsp32, L, p.w, p.f32_cmax, get_ub,
+                                     rowthr32, rowbuf32, cells32, st);
+      screened = st == 0 && r32 == f_inf();
+      __syncwarp();
+    }
+    const double d = screened ? INF
+                              : dtw_dispatch<false>(p.ad_k, rowraw, rownorm, L, qsp, L, p.w,
+                                                    get_ub, rowthr, rowbuf, cells, ovf);
     ++calls;
     if (d != INF && lane == 0) {
       atomicMin(key, static_cast<unsigned long long>(__double_as_longlong(d)));
@@ -1234,13 +1266,15 @@ __global__ void __launch_bounds__(256) nn1_kernel(Nn1Params p) {
   }
   if (lane == 0) {
     atomicAdd(p.cells, cells);
+    atomicAdd(p.cells + 1, cells32);
     atomicAdd(p.dtw_calls, calls);
   }
 }
 
 cudaError_t launch_nn1(const Nn1Params& p, cudaStream_t stream) {
   const int warps = 8;
-  const size_t smem = static_cast<size_t>(warps + 1) * padded_len(p.len, p.ad_k) * sizeof(double);
+  const size_t smem = static_cast<size_t>(warps + 1) * padded_len(p.len, p.ad_k) * sizeof(double) +
+                     padded_len(p.len, p.ad_k) * sizeof(float);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(nn1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
@@ -1300,6 +1334,24 @@ __global__ void fp64_probe_kernel(double* sink, int iters) {
 
 cudaError_t launch_fp64_probe(double* sink, int blocks, int iters, cudaStream_t stream) {
   fp64_probe_kernel<<<blocks, 256, 0, stream>>>(sink, iters);
+  return cudaGetLastError();
+}
+
+// FP32 issue-rate probe (the roofline of the FP32 screening engine): 8
+// independent FADD chains per thread.
+__global__ void fp32_probe_kernel(float* sink, int iters) {
+  const float a = 1e-3f * (threadIdx.x + 1);
+  float x0 = a, x1 = a + 1, x2 = a + 2, x3 = a + 3, x4 = a + 4, x5 = a + 5, x6 = a + 6, x7 = a + 7;
+  for (int i = 0; i < iters; ++i) {
+    x0 = __fadd_rn(x0, a); x1 = __fadd_rn(x1, a); x2 = __fadd_rn(x2, a); x3 = __fadd_rn(x3, a);
+    x4 = __fadd_rn(x4, a); x5 = __fadd_rn(x5, a); x6 = __fadd_rn(x6, a); x7 = __fadd_rn(x7, a);
+  }
+  const float r = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+  if (r == 0.123456789f) sink[threadIdx.x] = r;  // keep the chains alive
+}
+
+cudaError_t launch_fp32_probe(float* sink, int blocks, int iters, cudaStream_t stream) {
+  fp32_probe_kernel<<<blocks, 256, 0, stream>>>(sink, iters);
   return cudaGetLastError();
 }
 

@@ -114,8 +114,10 @@ struct Nn1Params {
   int ad_k;                       // anti-diagonal engine window 64*ad_k (0: strip engine only)
   unsigned long long* ub_keys;    // nq
   BestRecord* best;               // nq
-  unsigned long long* cells;      // one counter
+  unsigned long long* cells;      // two counters: exact FP64 engine, FP32 screen
   unsigned long long* dtw_calls;  // one counter
+  int use_f32;                    // FP32 screen for queries with max |q| <= f32_cmax
+  float f32_a, f32_b, f32_cmax;   // guard built with qmax = cmax (dtw_f32.cuh)
 };
 
 // Each launcher enqueues on `stream` and returns the launch error (no sync).
@@ -145,5 +147,6 @@ cudaError_t launch_check_finite(const double* x, long long n, unsigned long long
 void debug_read_reset(unsigned long long* out16);
 #endif
 cudaError_t launch_fp64_probe(double* sink, int blocks, int iters, cudaStream_t stream);
+cudaError_t launch_fp32_probe(float* sink, int blocks, int iters, cudaStream_t stream);
 
 }  // namespace eapdtw_b200
