@@ -799,14 +799,14 @@ int eapdtw_search_plan_result(eapdtw_search_plan* p, eapdtw_search_result* out) 
     debug_read_reset(dbg);
     std::fprintf(stderr, "strips/DTW bins [1,2,3-4,5-8,9-16,17+]: calls %llu %llu %llu %llu %llu %llu | steps %llu %llu %llu %llu %llu %llu\n",
                  dbg[2], dbg[3], dbg[4], dbg[5], dbg[6], dbg[7], dbg[8], dbg[9], dbg[10], dbg[11], dbg[12], dbg[13]);
-    std::fprintf(stderr, "strip steps %llu strips %llu cells %llu -> lane eff %.3f\n", dbg[0], dbg[1],
-                 cnt[kCntCells], cnt[kCntCells] / (32.0 * dbg[0] + 1));
+    std::fprintf(stderr, "strip steps %llu strips %llu cells %llu (f32 %llu) -> lane eff %.3f\n", dbg[0], dbg[1],
+                 cnt[kCntCells], cnt[kCntCellsF32], (cnt[kCntCells] + cnt[kCntCellsF32]) / (32.0 * dbg[0] + 1));
   }
   std::fprintf(stderr,
-               "phase warp-Gcycles: dtw %.3f eq %.3f ec %.3f screen %.3f | stage hit %llu miss "
+               "phase warp-Gcycles: dtw %.3f eq %.3f ec %.3f screen %.3f kim %.3f | stage hit %llu miss "
                "%llu\n",
                cnt[kClkDtw] * 1e-9, cnt[kClkEq] * 1e-9, cnt[kClkEc] * 1e-9,
-               cnt[kClkScreen] * 1e-9, cnt[kStageHit], cnt[kStageMiss]);
+               cnt[kClkScreen] * 1e-9, cnt[kClkKim] * 1e-9, cnt[kStageHit], cnt[kStageMiss]);
 #endif
   return EAPDTW_OK;
 }

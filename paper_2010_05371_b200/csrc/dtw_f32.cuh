@@ -31,7 +31,13 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "dtw_warp.cuh"
+
+#ifndef EAPDTW_F32_FASTRANGE
+#define EAPDTW_F32_FASTRANGE 0  // block fast path without the band test (experiment)
+#endif
 
 namespace eapdtw_b200 {
 
@@ -96,8 +102,16 @@ __device__ float warp_dtw_f32(const RawFn& rowraw, const NormFn& rownorm, int lr
   double ub_next = get_ub();
   double x_next = lane < lr ? rowraw(lane) : 0.0;
   __syncwarp();
+#ifdef EAPDTW_PHASE_CLOCKS
+  int dbg_strips = 0;
+  unsigned long long dbg_steps = 0;
+#endif
 
   for (int i0 = 1; i0 <= lr; i0 += 32) {
+#ifdef EAPDTW_PHASE_CLOCKS
+    if (lane == 0) atomicAdd(&g_dbg[1], 1ull);
+    ++dbg_strips;
+#endif
     const double ub_strip = ub_next;
     const int i = i0 + lane;
     const bool active = i <= lr;
@@ -130,28 +144,56 @@ __device__ float warp_dtw_f32(const RawFn& rowraw, const NormFn& rownorm, int lr
     int jr = j - bl;
     int j0 = jb;
 
-    auto step = [&](int u) {
+    // One wavefront step at column j+u (RANGE: with the band test).  Every
+    // lane loads its row-buffer cell (only lane 0 uses it as its top): one
+    // select instead of a predicated load and two moves.  Deadness is
+    // accumulated over the block of 4 steps (alld).
+    auto step = [&](auto range_tag, int u, bool& alld) {
+      constexpr bool RANGE = decltype(range_tag)::value;
       const float sh = __shfl_up_sync(kFull, v, 1);
-      const float top = is0 ? rp[u] : sh;
+      const float rb = rp[u];
+      const float top = is0 ? rb : sh;
       const float diag = top_prev;
       top_prev = top;
       const float d = __fsub_rn(c, qp[u]);
       float nv = __fadd_rn(__fmul_rn(d, d), fmin3f(v, top, diag));
-      nv = static_cast<unsigned>(jr + u) <= span ? nv : INF;
+      if (RANGE) nv = static_cast<unsigned>(jr + u) <= span ? nv : INF;
       if (writer) rp[u] = nv;
       v = nv;
-      const unsigned dm = __ballot_sync(kFull, nv > ub);
-      finmask |= dm & ((finmask << 1) | (j0 + u > hi ? 1u : 0u));
+      alld = alld && nv > ub;
     };
 
     for (;;) {
       const unsigned before = finmask;
-      step(0);
-      step(1);
-      step(2);
-      step(3);
+      bool alld = true;
+#if EAPDTW_F32_FASTRANGE
+      if (__all_sync(kFull, !active || (jr >= 0 && jr + 3 <= static_cast<int>(span)))) {
+        step(std::false_type{}, 0, alld);
+        step(std::false_type{}, 1, alld);
+        step(std::false_type{}, 2, alld);
+        step(std::false_type{}, 3, alld);
+      } else
+#endif
+      {
+        step(std::true_type{}, 0, alld);
+        step(std::true_type{}, 1, alld);
+        step(std::true_type{}, 2, alld);
+        step(std::true_type{}, 3, alld);
+      }
+      // Finished lanes, once per block (conservative): lane L is finished
+      // after step u if it was dead in all 4 steps and lane L-1 (lane 0: the
+      // row buffer, dead beyond column hi) was finished after step u-1.  Four
+      // chained updates, one per step, with the block's all-dead mask D.
+      const unsigned D = __ballot_sync(kFull, alld);
+      finmask |= D & ((finmask << 1) | (j0 > hi ? 1u : 0u));
+      finmask |= D & ((finmask << 1) | (j0 + 1 > hi ? 1u : 0u));
+      finmask |= D & ((finmask << 1) | (j0 + 2 > hi ? 1u : 0u));
+      finmask |= D & ((finmask << 1) | (j0 + 3 > hi ? 1u : 0u));
       finmask |= __ballot_sync(kFull, jr + 3 > static_cast<int>(span));
       if (((finmask & ~before) >> lane) & 1u) jf = j + 3;
+#ifdef EAPDTW_PHASE_CLOCKS
+      dbg_steps += 4;
+#endif
       if (finmask == kFull) break;
       j += 4;
       jr += 4;
@@ -183,6 +225,14 @@ __device__ float warp_dtw_f32(const RawFn& rowraw, const NormFn& rownorm, int lr
     lo = nlo;
     hi = nhi;
   }
+#ifdef EAPDTW_PHASE_CLOCKS
+  if (lane == 0) {
+    atomicAdd(&g_dbg[0], dbg_steps);
+    const int bin = dbg_strips <= 1 ? 0 : dbg_strips <= 2 ? 1 : dbg_strips <= 4 ? 2 : dbg_strips <= 8 ? 3 : dbg_strips <= 16 ? 4 : 5;
+    atomicAdd(&g_dbg[2 + bin], 1ull);
+    atomicAdd(&g_dbg[8 + bin], dbg_steps);
+  }
+#endif
   for (int off = 16; off > 0; off >>= 1) cnt += __shfl_xor_sync(kFull, cnt, off);
   if (lane == 0) cells += cnt;
   __syncwarp();

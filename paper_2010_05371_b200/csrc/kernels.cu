@@ -795,6 +795,7 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
         continue;               // wait for the pending slot to be filled
       }
 
+      PHASE_BEGIN();
       if (chunks_left) {
         // ---- tier 1 on the next chunk of 32 candidates: LB_Kim on the two
         //      aligned extremities (search.cpp:81-87), with the DTW's own IEEE
@@ -873,6 +874,7 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
           else push(stkC, nC, alive, s, nullptr, 0.0, nullptr, 0.0f, totC, z2);
         }
       }
+      PHASE_END(kClkKim);
       const bool flush = !chunks_left;
 
       // Early-abandoning LB_Keogh over order[k0, k1) (lower_bounds.cpp:57-88),
