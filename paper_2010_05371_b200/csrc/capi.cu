@@ -612,6 +612,10 @@ static SearchParams base_params(eapdtw_search_plan* p) {
   s.prune = p->algo == EAPDTW_ALGO_FULL ? 0 : 1;
   s.guard_rel = p->guard_rel;
   s.guard_abs = p->guard_abs;
+  // 2 * 3u * sqrt(m) * cmax, cmax = sqrt(m) + 1 + qmax (z-normalised windows
+  // and envelope values, the query), with margin
+  s.guard_sqrt = 8.0 * 0x1.0p-53 * std::sqrt(static_cast<double>(p->m)) *
+                 (std::sqrt(static_cast<double>(p->m)) + 1.0 + p->qmax);
   s.ub_key = p->key;
   s.best = B.best.as<BestRecord>();
   s.work = B.work.as<unsigned long long>();

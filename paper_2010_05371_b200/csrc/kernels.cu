@@ -382,6 +382,16 @@ __device__ double dtw_dispatch(int ad_k, const RawFn& rowraw, const NormFn& rown
   return warp_dtw<KILL>(rowraw, rownorm, lr, qsp, lc, w, get_ub, rowthr, buf, cells);
 }
 
+// Pruning threshold of the guarded lower bounds (Kim layers, Keogh EQ/EC):
+// a bound prunes iff it exceeds ub (1 + g_rel) + g_abs + g_sqrt sqrt(ub).
+// g_rel covers a summation order other than the DTW's; g_sqrt the
+// reciprocal normalisation (each normalised value is within 3 ulp of the
+// reference's division, so by Minkowski the bound moves by at most
+// 2 sqrt(lb) * 3u sqrt(m) cmax); g_abs the square of that term.
+__device__ __forceinline__ double lb_guard(const SearchParams& p, double ub) {
+  return ub * (1.0 + p.guard_rel) + p.guard_abs + p.guard_sqrt * __dsqrt_ru(ub);
+}
+
 __device__ __forceinline__ long long vload(const long long* p) {
   return *reinterpret_cast<const volatile long long*>(p);
 }
@@ -406,6 +416,12 @@ void debug_read_reset(unsigned long long* out8) {
 }
 #endif
 
+#ifndef EAPDTW_KIM_PREFETCH
+#define EAPDTW_KIM_PREFETCH 1  // 1: prefetch the next LB chunk to L1, 2: to L2
+#endif
+#ifndef EAPDTW_KIM_RSD
+#define EAPDTW_KIM_RSD 1  // Kim layers normalised by reciprocal multiplication
+#endif
 #ifndef EAPDTW_F32_ROWS
 #define EAPDTW_F32_ROWS 1
 #endif
@@ -814,6 +830,26 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
         } else {
           ++my_chunks;
           const long long s = p.begin + static_cast<long long>(chunk) * span + lane * p.stride;
+#if EAPDTW_KIM_PREFETCH
+          // pull the next chunk of this claim toward the SM while this one
+          // is processed (the Kim tier is memory-latency bound)
+          if (my_next < my_end && my_next < nchunks) {
+            const long long s2 = s + span;
+            if (s2 < p.end) {
+#if EAPDTW_KIM_PREFETCH == 1
+              asm volatile("prefetch.global.L1 [%0];" ::"l"(p.mean + s2));
+              asm volatile("prefetch.global.L1 [%0];" ::"l"(p.sd + s2));
+              asm volatile("prefetch.global.L1 [%0];" ::"l"(ref + s2));
+              asm volatile("prefetch.global.L1 [%0];" ::"l"(ref + s2 + m - 1));
+#else
+              asm volatile("prefetch.global.L2 [%0];" ::"l"(p.mean + s2));
+              asm volatile("prefetch.global.L2 [%0];" ::"l"(p.sd + s2));
+              asm volatile("prefetch.global.L2 [%0];" ::"l"(ref + s2));
+              asm volatile("prefetch.global.L2 [%0];" ::"l"(ref + s2 + m - 1));
+#endif
+            }
+          }
+#endif
           const bool valid = s < p.end;
           c_cand += __popc(__ballot_sync(kFull, valid));
           bool alive = valid;
@@ -840,11 +876,24 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
               auto layers = [&](auto l_tag) -> double {
                 constexpr int L = decltype(l_tag)::value;
                 double cf[L], cb[L];
+#if EAPDTW_KIM_RSD
+                // reciprocal normalisation (the bound is guarded anyway, like
+                // the Keogh tiers); the corners t = 0 keep their exact values
+                const double rsd = constant ? 0.0 : __drcp_rn(sd);
+                cf[0] = c0;
+                cb[0] = cl;
+#pragma unroll
+                for (int t = 1; t < L; ++t) {
+                  cf[t] = __dmul_rn(__dsub_rn(ref[s + t], mean), rsd);
+                  cb[t] = __dmul_rn(__dsub_rn(ref[s + m - 1 - t], mean), rsd);
+                }
+#else
 #pragma unroll
                 for (int t = 0; t < L; ++t) {
                   cf[t] = constant ? 0.0 : __ddiv_rn(__dsub_rn(ref[s + t], mean), sd);
                   cb[t] = constant ? 0.0 : __ddiv_rn(__dsub_rn(ref[s + m - 1 - t], mean), sd);
                 }
+#endif
                 double lb = kim;
 #pragma unroll
                 for (int l = 1; l < L; ++l) {
@@ -864,7 +913,7 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
                 kim3 = layers(std::integral_constant<int, kKimLayersLong>{});
               else if (m >= 2 * kKimLayers)
                 kim3 = layers(std::integral_constant<int, kKimLayers>{});
-              if (kim3 > ub * (1.0 + p.guard_rel) + p.guard_abs) {
+              if (kim3 > lb_guard(p, ub)) {
                 alive = false;
                 ++c_kim;
               }
@@ -948,7 +997,7 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
         const double mean = p.mean[s];
         const double sd = p.sd[s];
         const double rsd = sd < kMinStddev ? 0.0 : __drcp_rn(sd);
-        const double ubg = load_ub(p.ub_key) * (1.0 + p.guard_rel) + p.guard_abs;
+        const double ubg = lb_guard(p, load_ub(p.ub_key));
         // EQ: stage the batch's stretch of the reference in the warp's buffer
         // when it fits, so the order[]-permuted reads hit shared memory
         // instead of L2 (the DP row buffer is free between DTW tasks).
@@ -1238,7 +1287,9 @@ __global__ void __launch_bounds__(256) nn1_kernel(Nn1Params p) {
     const long long k = k0 + static_cast<long long>(t);
     if (k >= k1) break;
     const double* row = p.db + k * L;
-    const double ub = load_ub(key);
+    // warp-uniform: lanes need not load in lockstep, and the `continue`
+    // below must not split the warp (its collectives name every lane)
+    const double ub = __shfl_sync(kFull, load_ub(key), 0);
     if (L >= 2) {  // LB_Kim_FL (lower_bounds.cpp:51-55): exact, so no guard needed
       const double kim = __dadd_rn(sq_cost(qsp[1], row[0]), sq_cost(qsp[L], row[L - 1]));
       if (kim > ub) continue;

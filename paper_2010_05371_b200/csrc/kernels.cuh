@@ -72,6 +72,7 @@ struct SearchParams {
   int cb_strip;                  // first strip (1-based) that uses them
   int prune;                     // 0: Algo::full (no pruning), 1: pruned DTW
   double guard_rel, guard_abs;   // LB soundness guard
+  double guard_sqrt;             // ... and its reciprocal-normalisation term (lb_guard)
   double qmax;                   // max |q| (cumulative-bound guard)
   unsigned long long* ub_key;    // running threshold key (order-preserving bits)
   BestRecord* best;              // exact (d, lowest index) record

@@ -435,3 +435,49 @@ def test_streamed_host_search_equals_device_search(gpu, oracle_lib, monkeypatch,
         assert (got.best.location, got.best.distance_sq) == (want.location, want.distance_sq)
         assert (plain.best.location, plain.best.distance_sq) == (want.location, want.distance_sq)
         assert got.report.candidates_total == n - m + 1
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,m,ratio,lb", [(300_000, 128, 0.05, True), (200_000, 512, 0.1, False),
+                                          (150_000, 1024, 0.2, True), (60_000, 257, 1.0, True)])
+def test_fp32_screen_never_changes_the_result(gpu, oracle_lib, monkeypatch, n, m, ratio, lb):
+    """The FP32 screening engine (dtw_f32.cuh) only abandons with an
+    error-inflated threshold: with it (default) and without it (EAPDTW_F32=0)
+    the search returns the oracle's (location, d) bit for bit, including
+    planted near-ties whose DTW differs from the best by far less than the
+    FP32 guard."""
+    ref = gpu.random_walk_normal(n, 70 + m)
+    q = gpu.random_walk_normal(m, 71 + m)
+    r = ref.copy()
+    a, b = n // 3, (2 * n) // 3
+    r[a:a + m] = q * 3.0 + 7.0
+    r[b:b + m] = q * 3.0 + 7.0
+    r[b + m // 2] += 1e-7  # second copy: d2 a hair above the first (0)
+    for arr in (ref, r):
+        want = oracle_lib.similarity_search(arr, q, ratio, use_lb=lb, tighten=lb)
+        cfg = gpu.SearchConfig(window_ratio=ratio, use_lower_bounds=lb, tighten_ub=lb)
+        monkeypatch.setenv("EAPDTW_F32", "1")
+        on = gpu.similarity_search(arr, q, cfg)
+        monkeypatch.setenv("EAPDTW_F32", "0")
+        off = gpu.similarity_search(arr, q, cfg)
+        monkeypatch.delenv("EAPDTW_F32")
+        assert (on.best.location, on.best.distance_sq) == (want.location, want.distance_sq)
+        assert (off.best.location, off.best.distance_sq) == (want.location, want.distance_sq)
+
+
+@pytest.mark.gpu
+def test_fp32_screen_falls_back_on_large_values(gpu, reference_lib_optional):
+    """Series that are not z-normalised (|x| above the FP32 screen's value
+    bound sqrt(len)+1) make the screen undecided: the exact engine answers.
+    Mixed database: some rows within the bound, some far outside."""
+    rng = np.random.default_rng(77)
+    L = 128
+    db = np.cumsum(rng.standard_normal((3000, L)), axis=1)
+    db[::3] *= 40.0                    # every third row far outside the bound
+    qs = np.cumsum(rng.standard_normal((5, L)), axis=1)
+    qs[1] *= 40.0                      # one query outside too
+    for band in (UNB, 12):
+        arg, dist, _ = gpu.nn1(qs, db, gpu.Band(band))
+        warg, wdist, _ = reference_lib_optional.nn1(qs, db, band)
+        assert [int(x) for x in arg] == [int(x) for x in warg]
+        assert np.array_equal(dist, wdist)
