@@ -129,6 +129,10 @@ struct eapdtw_ctx {
   PlanBuffers pb;  // scratch of the one-shot search API (grow-only, reused)
   cudaStream_t copy = nullptr;  // H2D stream of the streamed host-pointer search
   cudaEvent_t copied[2] = {nullptr, nullptr};
+  // side stream of the preparation: the envelope runs there, concurrently
+  // with the (latency-bound) stats chain on the main stream
+  cudaStream_t aux = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
 };
 
 struct eapdtw_search_plan {
@@ -149,6 +153,7 @@ struct eapdtw_search_plan {
   bool prepared = false, ran = false;
   int blocks = 0, warps = 8, ad_k = 0, screen_rows = 8;
   int use_f32 = 1;  // FP32 screening engine ahead of the exact one (EAPDTW_F32=0: off)
+  bool overlap_prep = false;  // stats || envelope on two streams (measured slower: the chain shares its SMs)
   std::vector<int> coarse_strides{64};  // coarse passes, in order
   bool coarse_blocks = false;           // coarse pass over runs of adjacent candidates
   int probe = 2048;
@@ -203,6 +208,12 @@ int eapdtw_ctx_destroy(eapdtw_ctx* c) {
   }
   for (cudaEvent_t& ev : c->copied)
     if (ev) cudaEventDestroy(ev);
+  if (c->aux) {
+    cudaStreamSynchronize(c->aux);
+    cudaStreamDestroy(c->aux);
+  }
+  if (c->fork) cudaEventDestroy(c->fork);
+  if (c->join) cudaEventDestroy(c->join);
   if (c->own) cudaStreamDestroy(c->own);
   delete c;
   return EAPDTW_OK;
@@ -422,6 +433,7 @@ static int plan_init(eapdtw_search_plan* p, eapdtw_ctx* c, const double* ref_dev
   p->ad_k = getenv("EAPDTW_AD_K") ? choose_ad_k(static_cast<int>(m), p->w_eff) : 0;
   if (const char* env = getenv("EAPDTW_SCREEN_ROWS")) p->screen_rows = std::max(0, atoi(env));
   if (const char* env = getenv("EAPDTW_F32")) p->use_f32 = atoi(env) != 0;
+  if (const char* env = getenv("EAPDTW_OVERLAP_PREP")) p->overlap_prep = atoi(env) != 0;
   if (const char* env = getenv("EAPDTW_COARSE_STRIDE")) {  // e.g. "512,64" or "512:64"; "0": none
     p->coarse_strides.clear();
     for (const char* t = env; *t;) {
@@ -474,7 +486,7 @@ static int plan_init(eapdtw_search_plan* p, eapdtw_ctx* c, const double* ref_dev
   CUDA_TRY(B.sd.ensure(nc * 8));
   CUDA_TRY(B.q.ensure((m + 1) * 8));
   CUDA_TRY(B.qul.ensure(m * 16));
-  CUDA_TRY(B.qperm.ensure(m * 16));
+  CUDA_TRY(B.qperm.ensure(m * 16 + m * 8));  // double2 per position, then the float2 copy
   CUDA_TRY(B.order.ensure(m * 4));
   CUDA_TRY(B.best.ensure(sizeof(BestRecord)));
   CUDA_TRY(B.key.ensure(8));
@@ -496,6 +508,13 @@ static int plan_init(eapdtw_search_plan* p, eapdtw_ctx* c, const double* ref_dev
   CUDA_TRY(cudaMemcpyAsync(B.q.p, q1.data(), (m + 1) * 8, cudaMemcpyHostToDevice, s));
   CUDA_TRY(cudaMemcpyAsync(B.qul.p, qul.data(), m * 16, cudaMemcpyHostToDevice, s));
   CUDA_TRY(cudaMemcpyAsync(B.qperm.p, qperm.data(), m * 16, cudaMemcpyHostToDevice, s));
+  {
+    std::vector<float> qp32(2 * m);  // FP32 Keogh tiers: fl32 of the envelope (guarded)
+    for (size_t k = 0; k < 2 * m; ++k) qp32[k] = static_cast<float>(qperm[k]);
+    // synchronous: the host vector dies at scope exit
+    CUDA_TRY(cudaMemcpy(static_cast<char*>(B.qperm.p) + m * 16, qp32.data(), m * 8,
+                        cudaMemcpyHostToDevice));
+  }
   CUDA_TRY(cudaMemcpyAsync(B.order.p, order.data(), m * 4, cudaMemcpyHostToDevice, s));
   // the staging vectors are pageable locals: wait until the copies consumed them
   CUDA_TRY(cudaStreamSynchronize(s));
@@ -602,6 +621,7 @@ static SearchParams base_params(eapdtw_search_plan* p) {
   s.q = B.q.as<double>();
   s.qul = B.qul.as<double2>();
   s.qperm = B.qperm.as<double2>();
+  s.qperm32 = reinterpret_cast<const float2*>(static_cast<char*>(B.qperm.p) + p->m * 16);
   s.order = B.order.as<int>();
   s.ncand = static_cast<long long>(p->ncand);
   s.m = static_cast<int>(p->m);
@@ -640,6 +660,10 @@ static SearchParams base_params(eapdtw_search_plan* p) {
     s.f32_a = g.a;
     s.f32_b = g.b;
     s.f32_cmax = static_cast<float>(cmax);
+    // FP32 Keogh tiers: m terms, each value within 4 u32 of the reference's
+    const F32Guard gl = make_f32_guard(static_cast<int>(p->m), 0, cmax, p->qmax, 4.0);
+    s.lb32_a = gl.a;
+    s.lb32_b = gl.b;
   }
   s.counters = B.counters.as<unsigned long long>();
   s.index_offset = static_cast<long long>(p->offset);
@@ -656,12 +680,14 @@ static int stage_stats(eapdtw_search_plan* p, long long seg_b, long long seg_e) 
 }
 
 // first: decides whether the EC tier exists (the envelope window fits a tile)
-static int stage_env(eapdtw_search_plan* p, long long tile_b, long long tile_e, bool first) {
+static int stage_env(eapdtw_search_plan* p, long long tile_b, long long tile_e, bool first,
+                     cudaStream_t stream = nullptr) {
   PlanBuffers& B = *p->buf;
   if (!(p->use_lb && p->m >= 2)) return EAPDTW_OK;
   if (!first && !p->have_env) return EAPDTW_OK;
   const cudaError_t e = launch_envelope(p->ref, static_cast<long long>(p->n), p->env_r,
-                                        B.env.as<double>(), p->ctx->stream, tile_b, tile_e);
+                                        B.env.as<double>(), stream ? stream : p->ctx->stream,
+                                        tile_b, tile_e);
   if (e == cudaSuccess) {
     if (first) p->have_env = true;
     ++p->ctx->launches;
@@ -670,6 +696,32 @@ static int stage_env(eapdtw_search_plan* p, long long tile_b, long long tile_e, 
   } else {
     cudaGetLastError();  // window too wide for the tile: EC tier skipped
   }
+  return EAPDTW_OK;
+}
+
+// Stats chain (main stream) and envelope (side stream) concurrently: the
+// chain is latency-bound on few SMs, the envelope streams HBM.  Work already
+// enqueued on the main stream precedes both; the main stream waits for the
+// envelope before returning (everything after needs both).
+static int stage_stats_env(eapdtw_search_plan* p, long long seg_b, long long seg_e,
+                           long long tile_b, long long tile_e, bool first) {
+  eapdtw_ctx* c = p->ctx;
+  int e;
+  if (!p->overlap_prep) {
+    if ((e = stage_stats(p, seg_b, seg_e))) return e;
+    return stage_env(p, tile_b, tile_e, first);
+  }
+  if (!c->aux) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
+  }
+  CUDA_TRY(cudaEventRecord(c->fork, c->stream));
+  CUDA_TRY(cudaStreamWaitEvent(c->aux, c->fork, 0));
+  if ((e = stage_env(p, tile_b, tile_e, first, c->aux))) return e;
+  CUDA_TRY(cudaEventRecord(c->join, c->aux));
+  if ((e = stage_stats(p, seg_b, seg_e))) return e;
+  CUDA_TRY(cudaStreamWaitEvent(c->stream, c->join, 0));
   return EAPDTW_OK;
 }
 
@@ -736,10 +788,15 @@ int eapdtw_search_plan_prepare(eapdtw_search_plan* p) {
   cudaStream_t s = c->stream;
   int e;
   CUDA_TRY(cudaEventRecord(p->ev[0], s));
-  if ((e = stage_stats(p, 0, -1))) return e;
-  CUDA_TRY(cudaEventRecord(p->ev[1], s));
   p->have_env = false;
-  if ((e = stage_env(p, 0, -1, true))) return e;
+  if (p->overlap_prep) {  // stats || envelope: the "stats" phase spans both
+    if ((e = stage_stats_env(p, 0, -1, 0, -1, true))) return e;
+    CUDA_TRY(cudaEventRecord(p->ev[1], s));
+  } else {
+    if ((e = stage_stats(p, 0, -1))) return e;
+    CUDA_TRY(cudaEventRecord(p->ev[1], s));
+    if ((e = stage_env(p, 0, -1, true))) return e;
+  }
   CUDA_TRY(cudaEventRecord(p->ev[2], s));
   if ((e = stage_probe(p, p->ncand))) return e;
   if ((e = stage_coarse(p, 0, p->ncand))) return e;
@@ -940,8 +997,7 @@ static int one_shot_streamed(eapdtw_ctx* c, const double* host_ref, size_t n,
                                c->pb.flag.as<unsigned long long>(), s));
   ++c->launches;
   p.have_env = false;
-  if ((e = stage_stats(&p, 0, seg1))) return finish(e);
-  if ((e = stage_env(&p, 0, te1, true))) return finish(e);
+  if ((e = stage_stats_env(&p, 0, seg1, 0, te1, true))) return finish(e);
   if ((e = stage_probe(&p, c1))) return finish(e);
   if ((e = stage_coarse(&p, 0, c1))) return finish(e);
   p.prepared = true;
@@ -953,8 +1009,7 @@ static int one_shot_streamed(eapdtw_ctx* c, const double* host_ref, size_t n,
                                  c->pb.flag.as<unsigned long long>(), s));
     ++c->launches;
   }
-  if ((e = stage_stats(&p, seg1, -1))) return finish(e);
-  if ((e = stage_env(&p, te1, -1, false))) return finish(e);
+  if ((e = stage_stats_env(&p, seg1, -1, te1, -1, false))) return finish(e);
   if ((e = stage_coarse(&p, c1, ncand))) return finish(e);
   if ((e = eapdtw_search_plan_run(&p, c1, ncand))) return finish(e);
   if ((e = eapdtw_search_plan_result(&p, out))) return finish(e);

@@ -62,9 +62,12 @@ __device__ __forceinline__ float f32_threshold(double t, F32Guard g) {
 }
 
 // Host: the guard constants for series lengths lr, lc and value bounds.
-static inline F32Guard make_f32_guard(int lr, int lc, double cmax, double qmax) {
+// vfac: each FP32 value is within vfac * u' of the FP64 one (1 for the DTW's
+// rounded conversions; 4 for the Keogh terms' convert-multiply chain).
+static inline F32Guard make_f32_guard(int lr, int lc, double cmax, double qmax,
+                                      double vfac = 1.0) {
   const double L = static_cast<double>(lr) + lc;
-  const double u = 0x1.0p-24, up = 0x1.0p-24 + 0x1.0p-49;
+  const double u = 0x1.0p-24, up = vfac * (0x1.0p-24 + 0x1.0p-49);
   const double e64 = (2.0 * L + 8.0) * 0x1.0p-53;
   // (1+u)^(L+4) <= exp((L+4) u); margins absorb the host's own rounding
   const double a = (1.0 + e64) * std::exp((L + 4.0) * u) * (1.0 + 0x1.0p-40);
@@ -73,6 +76,13 @@ static inline F32Guard make_f32_guard(int lr, int lc, double cmax, double qmax) 
   g.a = std::nextafter(static_cast<float>(a), FLT_MAX);
   g.b = std::nextafter(static_cast<float>(b), FLT_MAX);
   return g;
+}
+
+// The inverse: a lower bound on the exact value v given its FP32 sum x <= a
+// (sqrt(v) + b)^2, i.e. v >= (sqrt(x / a) - b)^2 (rounded down; 0 if negative).
+__device__ __forceinline__ float f32_lower(float x, F32Guard g) {
+  const float s = __fsub_rd(__fsqrt_rd(__fdiv_rd(x, g.a)), g.b);
+  return s > 0.0f ? __fmul_rd(s, s) : 0.0f;
 }
 
 constexpr int kF32Undecided = 1;  // a row value exceeded cmax: run the FP64 engine
@@ -156,8 +166,11 @@ __device__ float warp_dtw_f32(const RawFn& rowraw, const NormFn& rownorm, int lr
       const float diag = top_prev;
       top_prev = top;
       const float d = __fsub_rn(c, qp[u]);
-      float nv = __fadd_rn(__fmul_rn(d, d), fmin3f(v, top, diag));
-      if (RANGE) nv = static_cast<unsigned>(jr + u) <= span ? nv : INF;
+      // the band test masks the cost (off the step's dependency chain):
+      // +inf + min(...) = +inf
+      float cst = __fmul_rn(d, d);
+      if (RANGE) cst = static_cast<unsigned>(jr + u) <= span ? cst : INF;
+      const float nv = __fadd_rn(cst, fmin3f(v, top, diag));
       if (writer) rp[u] = nv;
       v = nv;
       alld = alld && nv > ub;

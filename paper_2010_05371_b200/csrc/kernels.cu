@@ -422,6 +422,14 @@ void debug_read_reset(unsigned long long* out8) {
 #ifndef EAPDTW_KIM_RSD
 #define EAPDTW_KIM_RSD 1  // Kim layers normalised by reciprocal multiplication
 #endif
+#ifndef EAPDTW_LB_F32
+#define EAPDTW_LB_F32 0  // LB_Keogh EQ/EC terms in FP32 (guarded; measured no faster)
+#endif
+#if EAPDTW_LB_F32
+using lbacc_t = float;
+#else
+using lbacc_t = double;
+#endif
 #ifndef EAPDTW_F32_ROWS
 #define EAPDTW_F32_ROWS 1
 #endif
@@ -447,6 +455,7 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
   // for more resident warps.
   const double2* __restrict__ qul = p.qul;
   const double2* __restrict__ qperm = p.qperm;
+  const float2* __restrict__ qperm32 = p.qperm32;
   const int* __restrict__ order = p.order;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // per-warp buffer: the DTW row buffer, or the LB_Keogh EQ staging tile
@@ -934,11 +943,35 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
       //   EC: query value vs the candidate's (global raw) envelope, normalised.
       // Lanes without a candidate point at p.begin: loads stay in bounds.
       auto lb_range = [&](auto ec_tag, const double* xs, long long s, bool pending,
-                          const double mean, const double rsd, double ubg, int k0, int k1,
-                          double& acc) -> bool {
+                          const double mean, const double rsd, lbacc_t ubg, int k0, int k1,
+                          lbacc_t& acc) -> bool {
         constexpr bool EC = decltype(ec_tag)::value;
         bool alive = pending;
         const double2* es = EC ? p.env + s : nullptr;
+#if EAPDTW_LB_F32
+        // FP32 terms (guarded like the FP32 DTW screen, dtw_f32.cuh): the
+        // centring x - mean stays FP64 (no cancellation), the rest is FP32;
+        // U >= L, so at most one of a - U, L - a is positive: max3 with 0.
+        const float rsdf = __double2float_rn(rsd);
+        auto term = [&](int k) {
+          const int j = order[k];
+          float a, U, L;
+          if (!EC) {
+            const float2 b = qperm32[k];
+            a = __fmul_rn(__double2float_rn(__dsub_rn(xs[j], mean)), rsdf);
+            U = b.x;
+            L = b.y;
+          } else {
+            const double2 e = es[j];
+            a = qsp32[j + 1];
+            U = __fmul_rn(__double2float_rn(__dsub_rn(e.x, mean)), rsdf);
+            L = __fmul_rn(__double2float_rn(__dsub_rn(e.y, mean)), rsdf);
+          }
+          float dd;
+          asm("max.f32 %0, %1, %2, %3;" : "=f"(dd) : "f"(__fsub_rn(a, U)), "f"(__fsub_rn(L, a)), "f"(0.0f));
+          acc = __fmaf_rn(dd, dd, acc);
+        };
+#else
         auto term = [&](int k) {
           const int j = order[k];
           double a, U, L;
@@ -957,6 +990,7 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
           const double dd = e1 > 0.0 ? e1 : (e2 > 0.0 ? e2 : 0.0);
           acc = __dadd_rn(acc, __dmul_rn(dd, dd));
         };
+#endif
         // groups of kLbGroup positions: all their loads are in flight together
         for (int kb = k0; kb < k1; kb += kLbGroup) {
           if (kb + kLbGroup <= k1) {
@@ -982,22 +1016,28 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
       auto stage = [&](auto ec_tag, bool leg2) {
         constexpr bool EC = decltype(ec_tag)::value;
         long long s;
-        double acc = 0.0;
+        double acc_d = 0.0;
         float teq = 0.0f;
         float2 unused2;
         float unusedf;
         bool pending;
         if (!EC) {
-          pending = leg2 ? pop(stkA2, nA2, s, accA2, acc, nullptr, unusedf, nullptr, unused2)
-                         : pop(stkA, nA, s, nullptr, acc, nullptr, unusedf, nullptr, unused2);
+          pending = leg2 ? pop(stkA2, nA2, s, accA2, acc_d, nullptr, unusedf, nullptr, unused2)
+                         : pop(stkA, nA, s, nullptr, acc_d, nullptr, unusedf, nullptr, unused2);
         } else {
-          pending = leg2 ? pop(stkB2, nB2, s, accB2, acc, teqB2, teq, nullptr, unused2)
-                         : pop(stkB, nB, s, nullptr, acc, teqB, teq, nullptr, unused2);
+          pending = leg2 ? pop(stkB2, nB2, s, accB2, acc_d, teqB2, teq, nullptr, unused2)
+                         : pop(stkB, nB, s, nullptr, acc_d, teqB, teq, nullptr, unused2);
         }
+        lbacc_t acc = static_cast<lbacc_t>(acc_d);  // a leg-2 partial sum (exact in float mode)
         const double mean = p.mean[s];
         const double sd = p.sd[s];
         const double rsd = sd < kMinStddev ? 0.0 : __drcp_rn(sd);
+#if EAPDTW_LB_F32
+        const F32Guard glb{p.lb32_a, p.lb32_b};
+        const float ubg = f32_threshold(lb_guard(p, load_ub(p.ub_key)), glb);
+#else
         const double ubg = lb_guard(p, load_ub(p.ub_key));
+#endif
         // EQ: stage the batch's stretch of the reference in the warp's buffer
         // when it fits, so the order[]-permuted reads hit shared memory
         // instead of L2 (the DP row buffer is free between DTW tasks).
@@ -1029,7 +1069,13 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
           if (EC) ++c_ec;
           else ++c_eq;
         }
+#if EAPDTW_LB_F32
+        // a sound lower bound on the exact total (the cumulative-bound rows
+        // subtract FP64 prefixes from it)
+        const float tot = f32_lower(acc, glb);
+#else
         const float tot = __double2float_rz(acc);  // rounded down: a weaker, sound total
+#endif
         if (!leg2 && head < m) {
           if (EC) push(stkB2, nB2, alive, s, accB2, acc, teqB2, teq, nullptr, z2);
           else push(stkA2, nA2, alive, s, accA2, acc, nullptr, 0.0f, nullptr, z2);
@@ -1245,7 +1291,10 @@ cudaError_t launch_pairwise(const PairParams& p, cudaStream_t stream) {
 // Block = (query, database split); warps claim database rows in order; an
 // exact LB_Kim (first/last, valid for any band) gates the DTW.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) nn1_kernel(Nn1Params p) {
+#ifndef EAPDTW_NN1_MINB
+#define EAPDTW_NN1_MINB 3
+#endif
+__global__ void __launch_bounds__(256, EAPDTW_NN1_MINB) nn1_kernel(Nn1Params p) {
   extern __shared__ double smem[];
   __shared__ unsigned long long s_next;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

@@ -62,6 +62,7 @@ struct SearchParams {
   const double* q;       // normalised query, 1-based: q[1..m] (q[0] unused)
   const double2* qul;    // query envelope (upper, lower) per position, 0-based
   const double2* qperm;  // the same in visiting order: qperm[k] = qul[order[k]]
+  const float2* qperm32; // ... as float (FP32 Keogh tiers)
   const int* order;      // Keogh visiting order (search.cpp:143-149)
   long long ncand;
   long long begin, end, stride;  // candidates begin, begin+stride, ... < end
@@ -88,6 +89,7 @@ struct SearchParams {
   int screen_rows;               // phase-A lane screen depth (0: off)
   int use_f32;                   // FP32 screening engine ahead of the exact FP64 one
   float f32_a, f32_b, f32_cmax;  // its threshold guard (dtw_f32.cuh) and row-value bound
+  float lb32_a, lb32_b;          // guard of the FP32 Keogh tiers (same form)
   unsigned long long* counters;  // kNumCounters
   long long index_offset;        // shard start in the global reference
 };

@@ -10,7 +10,9 @@ int main(int argc, char** argv) {
   const int m = atoi(argv[4]), w = atoi(argv[5]);
   const double ub = atof(argv[6]);
   const int cnt = atoi(argv[7]);
-  FILE* per = argc > 8 ? fopen(argv[8], "w") : NULL;
+  FILE* per = argc > 8 && argv[8][0] != '-' ? fopen(argv[8], "w") : NULL;
+  double* CC = NULL;
+  if (argc > 9) { CC = malloc(sizeof(double) * m * cnt); FILE* g = fopen(argv[9], "rb"); if (fread(CC, 8, (size_t)m * cnt, g)) {} fclose(g); }
   long long cells_before = 0;
   double* Z = malloc(sizeof(double) * m * cnt);
   double* Q = malloc(sizeof(double) * m);
@@ -45,7 +47,9 @@ int main(int argc, char** argv) {
         if (prev[j] < mn) mn = prev[j];
         if (cur[j - 1] < mn) mn = cur[j - 1];
         double v = d * d + mn;
-        if (v > thr) v = INFINITY;
+        double t2 = thr;
+        if (CC) { double cc = CC[(size_t)c * m + j - 1]; double tc = ub - cc; if (tc < t2) t2 = tc; }
+        if (v > t2) v = INFINITY;
         cur[j] = v;
         if (v != INFINITY) { if (j < lo) lo = j; hi = j; ++cells; }
       }
