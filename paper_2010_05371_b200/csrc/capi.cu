@@ -109,10 +109,10 @@ bool all_finite(const double* x, size_t n) {
 
 struct PlanBuffers {
   DevBuf mean, sd, env, q, qul, qperm, order, best, key, work, counters, probe_counters, flag,
-      queue, qtot, qctr;
+      queue, qtot, qctr, rank, rlist;
   void release() {
     for (DevBuf* b : {&mean, &sd, &env, &q, &qul, &qperm, &order, &best, &key, &work, &counters,
-                      &probe_counters, &flag, &queue, &qtot, &qctr})
+                      &probe_counters, &flag, &queue, &qtot, &qctr, &rank, &rlist})
       b->release();
   }
 };
@@ -154,8 +154,12 @@ struct eapdtw_search_plan {
   int blocks = 0, warps = 8, ad_k = 0, screen_rows = 8;
   int use_f32 = 1;  // FP32 screening engine ahead of the exact one (EAPDTW_F32=0: off)
   bool overlap_prep = false;  // stats || envelope on two streams (measured slower: the chain shares its SMs)
-  std::vector<int> coarse_strides{64};  // coarse passes, in order
+  std::vector<int> coarse_strides{};  // coarse passes, in order (the rank pass replaced them)
   bool coarse_blocks = false;           // coarse pass over runs of adjacent candidates
+  // rank pass (warm start): the cascade over the ~rank_k candidates with the
+  // smallest layered LB_Kim among every rank_stride-th (0: off)
+  long long rank_stride = 16, rank_k = 16384;
+  int rank_waves = 1;  // waves k/16^(n-1) .. k/16, k
   int probe = 2048;
   double guard_rel = 1e-9, guard_abs = 1e-20;
   double qmax = 0.0;  // max |normalised query|
@@ -445,6 +449,13 @@ static int plan_init(eapdtw_search_plan* p, eapdtw_ctx* c, const double* ref_dev
   }
   if (const char* env = getenv("EAPDTW_PROBE")) p->probe = std::max(1, atoi(env));
   if (const char* env = getenv("EAPDTW_COARSE_BLOCKS")) p->coarse_blocks = atoi(env) != 0;
+  if (const char* env = getenv("EAPDTW_RANK")) {  // "S:K", "0": off
+    p->rank_stride = std::max(0, atoi(env));
+    if (const char* c2 = strchr(env, ':')) {
+      p->rank_k = std::max(1, atoi(c2 + 1));
+      if (const char* c3 = strchr(c2 + 1, ':')) p->rank_waves = std::max(1, std::min(4, atoi(c3 + 1)));
+    }
+  }
   p->guard_abs = 1e-20;
 
   // Query preparation exactly as search.cpp:136-149.
@@ -756,6 +767,46 @@ static int stage_probe(eapdtw_search_plan* p, size_t cand_end) {
 // (neighbouring windows normalise to nearly the same series).  Its candidates
 // are real, so their exact results enter the record; their work is counted
 // with the probe's.
+// Rank pass over [cb, ce) (kernels.cu: rank_kernel): the layered LB_Kim of
+// every rank_stride-th candidate, then the full cascade over the ~rank_k with
+// the smallest bound.  Real candidates: their exact results enter the record,
+// their work counts with the probe's.
+static int stage_rank(eapdtw_search_plan* p, size_t cb, size_t ce) {
+  if (p->rank_stride <= 0 || !p->use_lb || p->m < 2 || p->algo == EAPDTW_ALGO_FULL) return EAPDTW_OK;
+  const long long S = p->rank_stride;
+  if (static_cast<long long>(ce - cb) < 64 * S) return EAPDTW_OK;
+  PlanBuffers& B = *p->buf;
+  cudaStream_t s = p->ctx->stream;
+  const long long cap = 4 * p->rank_k;
+  CUDA_TRY(B.rank.ensure(rank_scratch_bytes(static_cast<long long>(ce - cb), S)));
+  CUDA_TRY(B.rlist.ensure(static_cast<size_t>(cap) * 8 + 64));
+  SearchParams rp = base_params(p);
+  rp.begin = static_cast<long long>(cb);
+  rp.end = static_cast<long long>(ce);
+  rp.counters = B.probe_counters.as<unsigned long long>();
+  long long* list = B.rlist.as<long long>();
+  unsigned long long* nlist = reinterpret_cast<unsigned long long*>(list + cap);
+  CUDA_TRY(launch_rank(rp, S, B.rank.p, s));
+  ++p->ctx->launches;
+  rp.list = list;
+  rp.nlist = nlist;
+  rp.list_cap = cap;
+  const long long nsamp = (static_cast<long long>(ce - cb) + S - 1) / S;
+  // waves of growing rank: each starts from the threshold the better-ranked
+  // candidates before it left
+  int wave = 0;
+  for (long long k = std::max<long long>(32, p->rank_k >> (4 * (p->rank_waves - 1)));;
+       k = std::min(p->rank_k, k << 4), ++wave) {
+    CUDA_TRY(launch_rank_select(rp, S, wave, k, cap, B.rank.p, list, nlist, s));
+    p->ctx->launches += 2;
+    CUDA_TRY(reset_work(p, std::min(cap, nsamp), s));  // the queue holds ncand + slack slots
+    CUDA_TRY(launch_search(rp, p->blocks, p->warps, s));
+    ++p->ctx->launches;
+    if (k >= p->rank_k || wave >= 14) break;
+  }
+  return EAPDTW_OK;
+}
+
 static int stage_coarse(eapdtw_search_plan* p, size_t cb, size_t ce) {
   PlanBuffers& B = *p->buf;
   cudaStream_t s = p->ctx->stream;
@@ -799,6 +850,7 @@ int eapdtw_search_plan_prepare(eapdtw_search_plan* p) {
   }
   CUDA_TRY(cudaEventRecord(p->ev[2], s));
   if ((e = stage_probe(p, p->ncand))) return e;
+  if ((e = stage_rank(p, 0, p->ncand))) return e;
   if ((e = stage_coarse(p, 0, p->ncand))) return e;
   CUDA_TRY(cudaEventRecord(p->ev[3], s));
   p->prepared = true;
@@ -999,6 +1051,7 @@ static int one_shot_streamed(eapdtw_ctx* c, const double* host_ref, size_t n,
   p.have_env = false;
   if ((e = stage_stats_env(&p, 0, seg1, 0, te1, true))) return finish(e);
   if ((e = stage_probe(&p, c1))) return finish(e);
+  if ((e = stage_rank(&p, 0, c1))) return finish(e);
   if ((e = stage_coarse(&p, 0, c1))) return finish(e);
   p.prepared = true;
   if ((e = eapdtw_search_plan_run(&p, 0, c1))) return finish(e);

@@ -723,7 +723,9 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
     //   tail is void.
     // chunk c covers candidates begin + c*span + lane*stride
     const long long span = p.chunk_span > 0 ? p.chunk_span : 32 * p.stride;
-    const long long nchunks = (p.end - p.begin + span - 1) / span;
+    const long long nlist =
+        p.list ? min(static_cast<long long>(vload(p.nlist)), p.list_cap) : 0;
+    const long long nchunks = p.list ? (nlist + 31) / 32 : (p.end - p.begin + span - 1) / span;
     bool chunks_left = true, flushed = false;
     long long myslot = -1;
     long long my_next = 0, my_end = 0;  // claimed chunk range
@@ -816,8 +818,18 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
       myslot = __shfl_sync(kFull, myslot, 0);
       if (void_slot) break;
       if (flushed) {
-        if (myslot < 0) break;  // nothing pending, nothing left to produce
-        continue;               // wait for the pending slot to be filled
+        if (myslot < 0) {
+          // Nothing of its own left: keep consuming while other warps may
+          // still publish survivors (a short list or the sweep's tail would
+          // otherwise leave their DTW tasks to a few warps).
+          bool done = false;
+          if (lane == 0)
+            done = vload(p.chunks_done) >= static_cast<unsigned long long>(nchunks) &&
+                   vload(p.qhead) >= vload(p.qtail);
+          if (__shfl_sync(kFull, done, 0)) break;
+          __nanosleep(256);
+        }
+        continue;  // claim a new slot, or wait for the pending one to be filled
       }
 
       PHASE_BEGIN();
@@ -838,11 +850,15 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
           chunks_left = false;  // flush the stacks below, then retire
         } else {
           ++my_chunks;
-          const long long s = p.begin + static_cast<long long>(chunk) * span + lane * p.stride;
+          long long s = p.begin + static_cast<long long>(chunk) * span + lane * p.stride;
+          if (p.list) {  // rank pass: the chunk's candidates come from the list
+            const long long li = chunk * 32 + lane;
+            s = li < nlist ? p.list[li] : p.end;
+          }
 #if EAPDTW_KIM_PREFETCH
           // pull the next chunk of this claim toward the SM while this one
           // is processed (the Kim tier is memory-latency bound)
-          if (my_next < my_end && my_next < nchunks) {
+          if (!p.list && my_next < my_end && my_next < nchunks) {
             const long long s2 = s + span;
             if (s2 < p.end) {
 #if EAPDTW_KIM_PREFETCH == 1
@@ -860,6 +876,7 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
           }
 #endif
           const bool valid = s < p.end;
+          if (!valid) s = p.begin;  // loads stay in bounds
           c_cand += __popc(__ballot_sync(kFull, valid));
           bool alive = valid;
           if (p.use_lb && m >= 2 && alive) {
@@ -1194,6 +1211,148 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
     atomicAdd(&p.counters[kCntScreened], c_scr);
     atomicAdd(&p.counters[kCntCellsF32], c_cells32);
   }
+}
+
+// ---------------------------------------------------------------------------
+// Rank pass: a warm start for the threshold.  A uniform sample (the probe, a
+// strided coarse pass) finds a near-final threshold only after ~1e6 exact
+// candidates; ranking every S-th candidate by its layered LB_Kim and running
+// the cascade over the ~k most promising ones finds a better one for less
+// (DESIGN.md section 6).  The bound here only ranks: no soundness needed.
+// ---------------------------------------------------------------------------
+template <int L>
+__device__ double kim_layers_rank(const double* __restrict__ ref, long long s, int m, double mean,
+                                  double sd, const double* __restrict__ q1) {
+  const bool constant = sd < kMinStddev;
+  const double rsd = constant ? 0.0 : __drcp_rn(sd);
+  double cf[L], cb[L];
+#pragma unroll
+  for (int t = 0; t < L; ++t) {
+    cf[t] = __dmul_rn(__dsub_rn(ref[s + t], mean), rsd);
+    cb[t] = __dmul_rn(__dsub_rn(ref[s + m - 1 - t], mean), rsd);
+  }
+  double lb = __dadd_rn(sq_cost(q1[1], cf[0]), sq_cost(q1[m], cb[0]));
+#pragma unroll
+  for (int l = 1; l < L; ++l) {
+    double f = sq_cost(q1[1 + l], cf[l]);
+    double bk = sq_cost(q1[m - l], cb[l]);
+#pragma unroll
+    for (int t = 0; t < l; ++t) {
+      f = dmin2(f, dmin2(sq_cost(q1[1 + l], cf[t]), sq_cost(q1[1 + t], cf[l])));
+      bk = dmin2(bk, dmin2(sq_cost(q1[m - l], cb[t]), sq_cost(q1[m - t], cb[l])));
+    }
+    lb = __dadd_rn(lb, __dadd_rn(f, bk));
+  }
+  return lb;
+}
+
+constexpr int kRankBins = 1 << 16;  // float bits >> 15 of a non-negative bound
+
+__global__ void __launch_bounds__(256) rank_kernel(SearchParams p, long long S, long long nsamp,
+                                                   float* __restrict__ lbv,
+                                                   unsigned* __restrict__ hist) {
+  const int m = p.m;
+  const int L = min(m / 2, m >= kKimLongFrom ? kKimLayersLong : kKimLayers);
+  for (long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; k < nsamp;
+       k += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long s = p.begin + k * S;
+    const double mean = p.mean[s], sd = p.sd[s];
+    double lb;
+    if (L >= 8) lb = kim_layers_rank<8>(p.ref, s, m, mean, sd, p.q);
+    else if (L >= 3) lb = kim_layers_rank<3>(p.ref, s, m, mean, sd, p.q);
+    else lb = kim_layers_rank<1>(p.ref, s, m, mean, sd, p.q);
+    const float f = fminf(__double2float_rd(lb), 3.0e38f);
+    lbv[k] = f;
+    atomicAdd(&hist[__float_as_uint(f) >> 15], 1u);
+  }
+}
+
+// One block: the first bin where the cumulative count reaches k; *thr = the
+// first float-bit pattern past it (all candidates when fewer than k).
+__global__ void __launch_bounds__(1024) rank_threshold_kernel(const unsigned* __restrict__ hist,
+                                                              long long k, unsigned* thr) {
+  __shared__ unsigned long long part[1024];
+  constexpr int per = kRankBins / 1024;
+  const int t = threadIdx.x;
+  unsigned long long c = 0;
+  for (int b = 0; b < per; ++b) c += hist[t * per + b];
+  part[t] = c;
+  __syncthreads();
+  if (t == 0) {
+    unsigned long long acc = 0;
+    unsigned out = 0xffffffffu;
+    for (int i = 0; i < 1024 && out == 0xffffffffu; ++i) {
+      if (acc + part[i] >= static_cast<unsigned long long>(k)) {
+        for (int b = 0; b < per; ++b) {
+          acc += hist[i * per + b];
+          if (acc >= static_cast<unsigned long long>(k)) {
+            out = static_cast<unsigned>(i * per + b + 1) << 15;
+            break;
+          }
+        }
+      } else {
+        acc += part[i];
+      }
+    }
+    *thr = out;
+  }
+}
+
+__global__ void __launch_bounds__(256) rank_select_kernel(const float* __restrict__ lbv,
+                                                          long long nsamp, long long begin,
+                                                          long long S, const unsigned* thr_lo,
+                                                          const unsigned* thr,
+                                                          long long cap, long long* list,
+                                                          unsigned long long* nlist) {
+  const unsigned th = *thr, tl = thr_lo ? *thr_lo : 0u;
+  const int lane = threadIdx.x & 31;
+  for (long long k0 = static_cast<long long>(blockIdx.x) * blockDim.x; k0 < nsamp;
+       k0 += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long k = k0 + threadIdx.x;
+    const bool sel = k < nsamp && __float_as_uint(lbv[k]) < th && __float_as_uint(lbv[k]) >= tl;
+    const unsigned mask = __ballot_sync(kFull, sel);
+    if (!mask) continue;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(nlist, static_cast<unsigned long long>(__popc(mask)));
+    base = __shfl_sync(kFull, base, 0);
+    const unsigned long long at = base + __popc(mask & ((1u << lane) - 1u));
+    if (sel && at < static_cast<unsigned long long>(cap)) list[at] = begin + k * S;
+  }
+}
+
+size_t rank_scratch_bytes(long long ncand, long long S) {
+  const long long nsamp = (ncand + S - 1) / S;
+  return static_cast<size_t>(nsamp) * 4 + kRankBins * 4 + 64;
+}
+
+cudaError_t launch_rank(const SearchParams& p, long long S, void* scratch, cudaStream_t stream) {
+  const long long nsamp = (p.end - p.begin + S - 1) / S;
+  if (nsamp <= 0) return cudaSuccess;
+  unsigned* hist = static_cast<unsigned*>(scratch);
+  float* lbv = reinterpret_cast<float*>(hist + kRankBins + 16);
+  cudaError_t e = cudaMemsetAsync(hist, 0, (kRankBins + 16) * 4, stream);
+  if (e != cudaSuccess) return e;
+  const int blocks = static_cast<int>(std::min<long long>((nsamp + 255) / 256, 148LL * 8));
+  rank_kernel<<<blocks, 256, 0, stream>>>(p, S, nsamp, lbv, hist);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rank_select(const SearchParams& p, long long S, int wave, long long k,
+                               long long cap, void* scratch, long long* list,
+                               unsigned long long* nlist, cudaStream_t stream) {
+  const long long nsamp = (p.end - p.begin + S - 1) / S;
+  if (nsamp <= 0) return cudaSuccess;
+  unsigned* hist = static_cast<unsigned*>(scratch);
+  unsigned* thr = hist + kRankBins;  // 16 slots: one threshold per wave
+  const float* lbv = reinterpret_cast<const float*>(hist + kRankBins + 16);
+  cudaError_t e = cudaMemsetAsync(nlist, 0, 8, stream);
+  if (e != cudaSuccess) return e;
+  rank_threshold_kernel<<<1, 1024, 0, stream>>>(hist, k, thr + wave);
+  const int blocks = static_cast<int>(std::min<long long>((nsamp + 255) / 256, 148LL * 8));
+  rank_select_kernel<<<blocks, 256, 0, stream>>>(lbv, nsamp, p.begin, S,
+                                                 wave > 0 ? thr + wave - 1 : nullptr, thr + wave,
+                                                 cap, list, nlist);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_search(const SearchParams& p, int blocks, int warps, cudaStream_t stream) {

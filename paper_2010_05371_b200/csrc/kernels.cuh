@@ -92,6 +92,11 @@ struct SearchParams {
   float lb32_a, lb32_b;          // guard of the FP32 Keogh tiers (same form)
   unsigned long long* counters;  // kNumCounters
   long long index_offset;        // shard start in the global reference
+  // list mode (rank pass): chunk c covers list[32c .. 32c+31] (candidate
+  // indices in [begin, end)); the count is read on the device
+  const long long* list;
+  const unsigned long long* nlist;
+  long long list_cap;            // entries past it were not written
 };
 
 struct PairParams {
@@ -140,6 +145,16 @@ int choose_ad_k(int n, int w);
 // Rows per lane of the strip engine (EAPDTW_STRIP_ROWS=1 or 2; default 1).
 cudaError_t set_strip_rows(cudaStream_t stream);
 cudaError_t launch_search(const SearchParams& p, int blocks, int warps, cudaStream_t stream);
+// Rank pass (the threshold's warm start): the layered LB_Kim of every S-th
+// candidate of [p.begin, p.end), then the candidates whose bound is among the
+// ~k smallest (a 2^16-bin histogram of the float bits) into list (<= cap,
+// count in *nlist).  scratch: 4 * ceil((end-begin)/S) + 4 * 65536 + 8 bytes.
+size_t rank_scratch_bytes(long long ncand, long long S);
+cudaError_t launch_rank(const SearchParams& p, long long S, void* scratch, cudaStream_t stream);
+// Wave w selects the candidates ranked in [k_{w-1}, k_w) (disjoint waves).
+cudaError_t launch_rank_select(const SearchParams& p, long long S, int wave, long long k,
+                               long long cap, void* scratch, long long* list,
+                               unsigned long long* nlist, cudaStream_t stream);
 cudaError_t launch_pairwise(const PairParams& p, cudaStream_t stream);
 cudaError_t launch_nn1(const Nn1Params& p, cudaStream_t stream);
 cudaError_t launch_init_best(BestRecord* rec, unsigned long long* keys, long long count,
