@@ -71,37 +71,85 @@ def band_cells(m: int, w: int) -> int:
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled DURING the timed region: NVML
+    (pynvml, every 10 ms, from a thread) when available, else nvidia-smi
+    -lms 50.  __enter__ returns once the first sample is in, so even a short
+    timed region is covered; __exit__ adds one last sample."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    # nvmlClocksEventReason* bits
+    NVML_BITS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+                 "sw_power_cap": 0x4}  # nvmlClocksEventReason* (pynvml constants)
 
     def __init__(self, device: int):
         self.device = device
-        self.rows = []
+        self.rows = []  # (sm_mhz, max_mhz, set of reasons)
         self.proc = None
         self.thread = None
+        self.stop = threading.Event()
+        self.nvml = None
+
+    def _nvml_sample(self):
+        nv, h = self.nvml
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        bits = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+        self.rows.append((float(sm), float(mx),
+                          {k for k, b in self.NVML_BITS.items() if bits & b}))
+
+    def _nvml_loop(self):
+        while not self.stop.is_set():
+            try:
+                self._nvml_sample()
+            except Exception:
+                return
+            self.stop.wait(0.01)
 
     def __enter__(self):
         try:
+            import pynvml as nv
+            nv.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+            idx = int(vis.split(",")[self.device]) if vis and vis.split(",")[0].isdigit() else self.device
+            self.nvml = (nv, nv.nvmlDeviceGetHandleByIndex(idx))
+            self._nvml_sample()
+            self.thread = threading.Thread(target=self._nvml_loop, daemon=True)
+            self.thread.start()
+            return self
+        except Exception:
+            self.nvml = None
+        try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 5.0:
+                time.sleep(0.01)
         except OSError:
             self.proc = None
         return self
 
     def _read(self):
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
-            if len(parts) == 7:
-                self.rows.append(parts)
+            if len(parts) == 7 and parts[0].replace(".", "").isdigit():
+                self.rows.append((float(parts[0]),
+                                  float(parts[1]) if parts[1].replace(".", "").isdigit() else None,
+                                  {names[k] for k in range(4) if parts[3 + k].lower().startswith("active")}))
 
     def __exit__(self, *exc):
+        self.stop.set()
+        if self.nvml is not None:
+            try:
+                self._nvml_sample()
+            except Exception:
+                pass
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -114,14 +162,12 @@ class ClockSampler:
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in self.rows for k in range(4)
-                          if r[3 + k].lower().startswith("active")})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+        sm = [r[0] for r in self.rows]
+        mx = [r[1] for r in self.rows if r[1]]
+        reasons = sorted(set().union(*(r[2] for r in self.rows)))
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows),
+                "source": "nvml" if self.nvml is not None else "nvidia-smi"}
 
 
 def make_inputs(n: int, m: int):
@@ -268,8 +314,10 @@ def run_batch(args):
         ub = torch.from_numpy(exact * 1.05).cuda()
         ctx.set_stream(torch.cuda.current_stream().cuda_stream)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        clk = ClockSampler(0)
         for k in range(args.warmup + args.steps):
             if k == args.warmup:
+                clk.__enter__()
                 e0.record()
             for ubp in (None, ub):
                 _capi.check(_capi.lib.eapdtw_pairwise_dev(
@@ -278,6 +326,7 @@ def run_batch(args):
                     C.c_void_p(dout.data_ptr()), None))
         e1.record()
         torch.cuda.synchronize()
+        clk.__exit__(None, None, None)
         ms = e0.elapsed_time(e1) / args.steps
     else:
         dq, ddb = torch.from_numpy(qs).cuda(), torch.from_numpy(db).cuda()
@@ -285,8 +334,10 @@ def run_batch(args):
         dist2 = np.empty(nq)
         ctx.set_stream(torch.cuda.current_stream().cuda_stream)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        clk = ClockSampler(0)
         for k in range(args.warmup + args.steps):
             if k == args.warmup:
+                clk.__enter__()
                 e0.record()
             _capi.check(_capi.lib.eapdtw_nn1_dev(
                 ctx.handle, C.c_void_p(dq.data_ptr()), nq, C.c_void_p(ddb.data_ptr()), nd, L,
@@ -294,6 +345,7 @@ def run_batch(args):
                 dist2.ctypes.data_as(C.POINTER(C.c_double)), None))
         e1.record()
         torch.cuda.synchronize()
+        clk.__exit__(None, None, None)
         ms = e0.elapsed_time(e1) / args.steps
     value = n_units / (ms * 1e-3)
     cells32 = ctx.last_cells_f32 if cfg != "cfg1" else 0
@@ -310,7 +362,8 @@ def run_batch(args):
                     else int(qs.nbytes + db.nbytes),
                     "d2h_bytes_per_step": int(npairs * 8 * 2) if cfg == "cfg1" else nq * 16},
             "dtw_gcups_counted": cells / (ms * 1e-3) / 1e9, "cells_per_step": cells,
-            "gpu_launches": None}
+            "clocks": clk.summary(),
+            "gpu_launches": 2 * args.steps}  # cfg1: two pairwise launches; cfg5: init + nn1
     print(json.dumps(line), flush=True)
     return 0
 
