@@ -151,7 +151,7 @@ struct eapdtw_search_plan {
   size_t ncand = 0;
   cudaEvent_t ev[8] = {};
   bool prepared = false, ran = false;
-  int blocks = 0, warps = 8, ad_k = 0, screen_rows = 8;
+  int blocks = 0, warps = 8, ad_k = 0, screen_rows = 2;  // screen depth: 2 measured best with the FP32 engine
   int use_f32 = 1;  // FP32 screening engine ahead of the exact one (EAPDTW_F32=0: off)
   bool overlap_prep = false;  // stats || envelope on two streams (measured slower: the chain shares its SMs)
   std::vector<int> coarse_strides{};  // coarse passes, in order (the rank pass replaced them)

@@ -419,6 +419,9 @@ void debug_read_reset(unsigned long long* out8) {
 #ifndef EAPDTW_KIM_PREFETCH
 #define EAPDTW_KIM_PREFETCH 1  // 1: prefetch the next LB chunk to L1, 2: to L2
 #endif
+#ifndef EAPDTW_KIM_CORNER_RSD
+#define EAPDTW_KIM_CORNER_RSD 1  // corner LB_Kim by reciprocal too (guarded)
+#endif
 #ifndef EAPDTW_KIM_RSD
 #define EAPDTW_KIM_RSD 1  // Kim layers normalised by reciprocal multiplication
 #endif
@@ -883,11 +886,23 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
             const double mean = p.mean[s];
             const double sd = p.sd[s];
             const bool constant = sd < kMinStddev;
+#if EAPDTW_KIM_CORNER_RSD
+            // corners by reciprocal normalisation too: one reciprocal instead
+            // of two divisions per candidate; the corner bound is then
+            // guarded like the layers
+            const double rsd0 = constant ? 0.0 : __drcp_rn(sd);
+            const double c0 = __dmul_rn(__dsub_rn(ref[s], mean), rsd0);
+            const double cl = __dmul_rn(__dsub_rn(ref[s + m - 1], mean), rsd0);
+            const double kim = __dadd_rn(sq_cost(qsp[1], c0), sq_cost(qsp[m], cl));
+            const double ub = load_ub(p.ub_key);
+            if (kim > lb_guard(p, ub)) {
+#else
             const double c0 = constant ? 0.0 : __ddiv_rn(__dsub_rn(ref[s], mean), sd);
             const double cl = constant ? 0.0 : __ddiv_rn(__dsub_rn(ref[s + m - 1], mean), sd);
             const double kim = __dadd_rn(sq_cost(qsp[1], c0), sq_cost(qsp[m], cl));
             const double ub = load_ub(p.ub_key);
             if (kim > ub) {
+#endif
               alive = false;
               ++c_kim;
             } else {
@@ -905,7 +920,11 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
 #if EAPDTW_KIM_RSD
                 // reciprocal normalisation (the bound is guarded anyway, like
                 // the Keogh tiers); the corners t = 0 keep their exact values
+#if EAPDTW_KIM_CORNER_RSD
+                const double rsd = rsd0;
+#else
                 const double rsd = constant ? 0.0 : __drcp_rn(sd);
+#endif
                 cf[0] = c0;
                 cb[0] = cl;
 #pragma unroll
