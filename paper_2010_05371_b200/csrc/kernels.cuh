@@ -23,7 +23,10 @@ constexpr int kLbGroup = EAPDTW_LB_GROUP;          // Keogh positions per abando
 constexpr int kKimLayers = EAPDTW_KIM_LAYERS;     // LB_Kim points per end (short queries)
 constexpr int kKimLayersLong = 8;                  // ... for m >= kKimLongFrom
 constexpr int kKimLongFrom = 768;
-constexpr int kSuperChunk = 4;                     // LB chunks (of 32 candidates) per claim
+#ifndef EAPDTW_SUPER_CHUNK
+#define EAPDTW_SUPER_CHUNK 4
+#endif
+constexpr int kSuperChunk = EAPDTW_SUPER_CHUNK;    // LB chunks (of 32 candidates) per claim
 constexpr int kStageExtra = 64;                    // extra doubles per warp buffer: EQ staging span
 constexpr int kLbHead = 256;                       // first leg of the Keogh tiers (positions of order[])
 // A, A2, B, B2, C indices; B, B2 EQ totals; C (EQ, EC) totals; A2, B2 partial sums
