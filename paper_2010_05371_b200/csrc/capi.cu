@@ -1023,7 +1023,14 @@ static int one_shot_streamed(eapdtw_ctx* c, const double* host_ref, size_t n,
   cudaStream_t s = c->stream;
   const size_t m = p.m, ncand = p.ncand;
   const long long nseg = static_cast<long long>((ncand + kStatsResetInterval - 1) / kStatsResetInterval);
-  const long long seg1 = nseg / 2;
+  // Part 1 (3/8 of the candidates): everything waits for its copy, while
+  // part 2's copy hides under part 1's stats, warm start and sweep.  Shares
+  // of 1/8 .. 4/8 measured within noise (cfg4 e2e 61-64 ms; the second stats
+  // chain and envelope, not the first copy, are what remains exposed).
+  // EAPDTW_STREAM_SPLIT = part 1's share in eighths.
+  long long eighths = 3;
+  if (const char* e8 = getenv("EAPDTW_STREAM_SPLIT")) eighths = std::max(1, std::min(7, atoi(e8)));
+  const long long seg1 = std::max<long long>(1, nseg * eighths / 8);
   const size_t c1 = static_cast<size_t>(seg1) * kStatsResetInterval;
   // data part 1 needs: its stats windows, and the envelope tiles covering the
   // positions its candidates' EC tier reads (< c1 + m - 1), each with radius r
