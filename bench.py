@@ -83,8 +83,10 @@ class ClockSampler:
     NVML_BITS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
                  "sw_power_cap": 0x4}  # nvmlClocksEventReason* (pynvml constants)
 
-    def __init__(self, device: int):
+    def __init__(self, device: int, poll: bool = True):
         self.device = device
+        self.poll = poll  # False: one sample at entry and one at exit (no thread
+        #                   competing with a launch loop of microsecond kernels)
         self.rows = []  # (sm_mhz, max_mhz, set of reasons)
         self.proc = None
         self.thread = None
@@ -115,8 +117,9 @@ class ClockSampler:
             idx = int(vis.split(",")[self.device]) if vis and vis.split(",")[0].isdigit() else self.device
             self.nvml = (nv, nv.nvmlDeviceGetHandleByIndex(idx))
             self._nvml_sample()
-            self.thread = threading.Thread(target=self._nvml_loop, daemon=True)
-            self.thread.start()
+            if self.poll:
+                self.thread = threading.Thread(target=self._nvml_loop, daemon=True)
+                self.thread.start()
             return self
         except Exception:
             self.nvml = None
@@ -314,7 +317,7 @@ def run_batch(args):
         ub = torch.from_numpy(exact * 1.05).cuda()
         ctx.set_stream(torch.cuda.current_stream().cuda_stream)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        clk = ClockSampler(0)
+        clk = ClockSampler(0, poll=False)  # a ~0.1 ms region: samples at its edges
         for k in range(args.warmup + args.steps):
             if k == args.warmup:
                 clk.__enter__()
