@@ -1146,6 +1146,8 @@ static int nn1_impl(eapdtw_ctx* c, const double* q_dev, size_t nq, const double*
     p.f32_b = g.b;
     p.f32_cmax = static_cast<float>(cmax);
   }
+  p.guard_rel = std::max(1e-9, 8.0 * static_cast<double>(len) * 0x1.0p-53);
+  p.guard_abs = 1e-20;
   CUDA_TRY(set_strip_rows(s));
   CUDA_TRY(launch_nn1(p, s));
   ++c->launches;

@@ -1469,6 +1469,31 @@ cudaError_t launch_pairwise(const PairParams& p, cudaStream_t stream) {
 // Block = (query, database split); warps claim database rows in order; an
 // exact LB_Kim (first/last, valid for any band) gates the DTW.
 // ---------------------------------------------------------------------------
+// Layered LB_Kim over raw (already normalised) series: the first and last
+// LL points of the row against the query (qsp 1-based), see search_kernel.
+template <int LL>
+__device__ double kim_layers_raw(const double* __restrict__ rw, int L, const double* qsp) {
+  double cf[LL], cb[LL];
+#pragma unroll
+  for (int t = 0; t < LL; ++t) {
+    cf[t] = rw[t];
+    cb[t] = rw[L - 1 - t];
+  }
+  double lb = __dadd_rn(sq_cost(qsp[1], cf[0]), sq_cost(qsp[L], cb[0]));
+#pragma unroll
+  for (int l = 1; l < LL; ++l) {
+    double f = sq_cost(qsp[1 + l], cf[l]);
+    double bk = sq_cost(qsp[L - l], cb[l]);
+#pragma unroll
+    for (int t = 0; t < l; ++t) {
+      f = dmin2(f, dmin2(sq_cost(qsp[1 + l], cf[t]), sq_cost(qsp[1 + t], cf[l])));
+      bk = dmin2(bk, dmin2(sq_cost(qsp[L - l], cb[t]), sq_cost(qsp[L - t], cb[l])));
+    }
+    lb = __dadd_rn(lb, __dadd_rn(f, bk));
+  }
+  return lb;
+}
+
 #ifndef EAPDTW_NN1_MINB
 #define EAPDTW_NN1_MINB 3
 #endif
@@ -1507,17 +1532,42 @@ __global__ void __launch_bounds__(256, EAPDTW_NN1_MINB) nn1_kernel(Nn1Params p) 
   const F32Guard g{p.f32_a, p.f32_b};
   unsigned long long* key = p.ub_keys + qi;
   unsigned long long cells = 0, cells32 = 0, calls = 0, ovf = 0;
+  // Rows are claimed 32 at a time: lane L screens row kb+L with LB_Kim_FL
+  // (lower_bounds.cpp:51-55, exact, unguarded) and the layered LB_Kim (any
+  // band; another summation order, so guarded like the search's), then the
+  // warp evaluates the survivors in index order.
+  const int KL = L >= 16 ? 8 : (L >= 6 ? 3 : 1);
   for (;;) {
     unsigned long long t = 0;
-    if (lane == 0) t = atomicAdd(&s_next, 1ull);
+    if (lane == 0) t = atomicAdd(&s_next, 32ull);
     t = __shfl_sync(kFull, t, 0);
-    const long long k = k0 + static_cast<long long>(t);
-    if (k >= k1) break;
+    const long long kb = k0 + static_cast<long long>(t);
+    if (kb >= k1) break;
+    unsigned surv;
+    {
+      const long long kk = kb + lane;
+      bool keep = kk < k1;
+      if (keep && L >= 2) {
+        const double* rw = p.db + kk * L;
+        const double ubl = load_ub(key);
+        const double kim = __dadd_rn(sq_cost(qsp[1], rw[0]), sq_cost(qsp[L], rw[L - 1]));
+        if (kim > ubl) {
+          keep = false;
+        } else if (KL > 1) {
+          double lb;
+          if (KL == 8) lb = kim_layers_raw<8>(rw, L, qsp);
+          else lb = kim_layers_raw<3>(rw, L, qsp);
+          if (lb > ubl * (1.0 + p.guard_rel) + p.guard_abs) keep = false;
+        }
+      }
+      surv = __ballot_sync(kFull, keep);
+    }
+    for (; surv; surv &= surv - 1) {
+    const long long k = kb + (__ffs(surv) - 1);
     const double* row = p.db + k * L;
-    // warp-uniform: lanes need not load in lockstep, and the `continue`
-    // below must not split the warp (its collectives name every lane)
+    // warp-uniform threshold (lanes need not load in lockstep)
     const double ub = __shfl_sync(kFull, load_ub(key), 0);
-    if (L >= 2) {  // LB_Kim_FL (lower_bounds.cpp:51-55): exact, so no guard needed
+    if (L >= 2) {  // LB_Kim_FL again with the current threshold (exact)
       const double kim = __dadd_rn(sq_cost(qsp[1], row[0]), sq_cost(qsp[L], row[L - 1]));
       if (kim > ub) continue;
     }
@@ -1542,6 +1592,7 @@ __global__ void __launch_bounds__(256, EAPDTW_NN1_MINB) nn1_kernel(Nn1Params p) 
     if (d != INF && lane == 0) {
       atomicMin(key, static_cast<unsigned long long>(__double_as_longlong(d)));
       best_record_update(p.best + qi, d, static_cast<unsigned long long>(k));
+    }
     }
   }
   if (lane == 0) {

@@ -129,6 +129,7 @@ struct Nn1Params {
   unsigned long long* dtw_calls;  // one counter
   int use_f32;                    // FP32 screen for queries with max |q| <= f32_cmax
   float f32_a, f32_b, f32_cmax;   // guard built with qmax = cmax (dtw_f32.cuh)
+  double guard_rel, guard_abs;    // layered LB_Kim guard (summation order)
 };
 
 // Each launcher enqueues on `stream` and returns the launch error (no sync).
