@@ -481,3 +481,26 @@ def test_fp32_screen_falls_back_on_large_values(gpu, reference_lib_optional):
         warg, wdist, _ = reference_lib_optional.nn1(qs, db, band)
         assert [int(x) for x in arg] == [int(x) for x in warg]
         assert np.array_equal(dist, wdist)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("rank", ["0", "16:16384", "4:512", "8:64:3"])
+def test_warm_start_never_changes_the_result(gpu, oracle_lib, monkeypatch, rank):
+    """The warm start (probe, rank pass with its list mode and waves, coarse
+    pass) only changes the order in which candidates are tried: the answer is
+    the oracle's, with the best match planted where the rank pass does not
+    look (not a multiple of the rank stride) and a tie planted later."""
+    n, m, ratio = 400_000, 200, 0.1
+    ref = gpu.random_walk_normal(n, 501)
+    q = gpu.random_walk_normal(m, 502)
+    r = ref.copy()
+    r[123_457:123_457 + m] = q * 0.5 + 3.0   # exact z-normalised copy (d = 0)
+    r[300_001:300_001 + m] = q * 2.0 - 1.0   # a second copy: tie, higher index
+    want = oracle_lib.similarity_search(r, q, ratio)
+    monkeypatch.setenv("EAPDTW_RANK", rank)
+    for coarse in ("0", "64"):
+        monkeypatch.setenv("EAPDTW_COARSE_STRIDE", coarse)
+        got = gpu.similarity_search(r, q, gpu.SearchConfig(window_ratio=ratio))
+        assert (got.best.location, got.best.distance_sq) == (want.location, want.distance_sq)
+        rep = got.report
+        assert rep.candidates_total == n - m + 1
