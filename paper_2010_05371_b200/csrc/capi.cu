@@ -160,6 +160,7 @@ struct eapdtw_search_plan {
   // smallest layered LB_Kim among every rank_stride-th (0: off)
   long long rank_stride = 16, rank_k = 16384;
   int rank_waves = 1;  // waves k/16^(n-1) .. k/16, k
+  bool rank_ub = true;  // upper-bound wave first (narrow-band DTW of the k/16 best)
   int probe = 2048;
   double guard_rel = 1e-9, guard_abs = 1e-20;
   double qmax = 0.0;  // max |normalised query|
@@ -449,6 +450,7 @@ static int plan_init(eapdtw_search_plan* p, eapdtw_ctx* c, const double* ref_dev
   }
   if (const char* env = getenv("EAPDTW_PROBE")) p->probe = std::max(1, atoi(env));
   if (const char* env = getenv("EAPDTW_COARSE_BLOCKS")) p->coarse_blocks = atoi(env) != 0;
+  if (const char* env = getenv("EAPDTW_RANK_UB")) p->rank_ub = atoi(env) != 0;
   if (const char* env = getenv("EAPDTW_RANK")) {  // "S:K", "0": off
     p->rank_stride = std::max(0, atoi(env));
     if (const char* c2 = strchr(env, ':')) {
@@ -740,7 +742,18 @@ static int stage_stats_env(eapdtw_search_plan* p, long long seg_b, long long seg
 // bounds, running threshold) so the sweep starts from a finite best-so-far.
 // Probe hits are real candidates, so they legitimately enter the (d, index)
 // record.
+// The upper-bound wave pays off for wide bands only (cfg4: -0.7 ms; w/16 < 4
+// makes the narrow band too loose a bound, cfg2 +0.1 ms).
+static bool rank_ub_applies(const eapdtw_search_plan* p) { return p->rank_ub && p->w_eff >= 64; }
+
+static bool rank_applies(const eapdtw_search_plan* p, size_t cb, size_t ce) {
+  return p->rank_stride > 0 && p->use_lb && p->m >= 2 && p->algo != EAPDTW_ALGO_FULL &&
+         static_cast<long long>(ce - cb) >= 64 * p->rank_stride;
+}
+
 static int stage_probe(eapdtw_search_plan* p, size_t cand_end) {
+  // the rank pass's upper-bound wave gives the first finite threshold
+  if (rank_ub_applies(p) && rank_applies(p, 0, cand_end) && !getenv("EAPDTW_PROBE")) return EAPDTW_OK;
   PlanBuffers& B = *p->buf;
   cudaStream_t s = p->ctx->stream;
   const size_t nprobe =
@@ -772,9 +785,8 @@ static int stage_probe(eapdtw_search_plan* p, size_t cand_end) {
 // the smallest bound.  Real candidates: their exact results enter the record,
 // their work counts with the probe's.
 static int stage_rank(eapdtw_search_plan* p, size_t cb, size_t ce) {
-  if (p->rank_stride <= 0 || !p->use_lb || p->m < 2 || p->algo == EAPDTW_ALGO_FULL) return EAPDTW_OK;
+  if (!rank_applies(p, cb, ce)) return EAPDTW_OK;
   const long long S = p->rank_stride;
-  if (static_cast<long long>(ce - cb) < 64 * S) return EAPDTW_OK;
   PlanBuffers& B = *p->buf;
   cudaStream_t s = p->ctx->stream;
   const long long cap = 4 * p->rank_k;
@@ -792,9 +804,29 @@ static int stage_rank(eapdtw_search_plan* p, size_t cb, size_t ce) {
   rp.nlist = nlist;
   rp.list_cap = cap;
   const long long nsamp = (static_cast<long long>(ce - cb) + S - 1) / S;
-  // waves of growing rank: each starts from the threshold the better-ranked
-  // candidates before it left
+  // Upper-bound wave: the rank_k/16 best-ranked candidates' DTW in a band of
+  // w/16 cells.  Fewer paths, so each value is >= that candidate's DTW (the
+  // FP DP is monotone in its predecessor set): a valid threshold, computed
+  // ~16x cheaper than the full-band DTW; it tightens the key only (ub_only).
   int wave = 0;
+  if (rank_ub_applies(p)) {
+    SearchParams up = rp;
+    up.direct = 1;
+    up.direct_chunk = 1;
+    up.use_lb = 0;
+    up.tighten = 0;
+    up.ub_only = 1;
+    up.w = std::max(0, p->w_eff / 16);
+    CUDA_TRY(launch_rank_select(up, S, wave, std::max<long long>(32, p->rank_k / 16), cap,
+                                B.rank.p, list, nlist, s));
+    p->ctx->launches += 2;
+    CUDA_TRY(reset_work(p, 0, s));
+    CUDA_TRY(launch_search(up, p->blocks, p->warps, s));
+    ++p->ctx->launches;
+    ++wave;
+  }
+  // then the cascade over the ranks past it (waves of growing rank, each
+  // starting from the threshold the better-ranked candidates before it left)
   for (long long k = std::max<long long>(32, p->rank_k >> (4 * (p->rank_waves - 1)));;
        k = std::min(p->rank_k, k << 4), ++wave) {
     CUDA_TRY(launch_rank_select(rp, S, wave, k, cap, B.rank.p, list, nlist, s));

@@ -695,7 +695,10 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
       ++c_aband;
     } else if (lane == 0) {
       atomicMin(p.ub_key, static_cast<unsigned long long>(__double_as_longlong(d)));
-      best_record_update(p.best, d, static_cast<unsigned long long>(cand + p.index_offset));
+      // ub_only: d is an upper bound (a narrower band's DTW), a threshold
+      // but not an answer
+      if (!p.ub_only)
+        best_record_update(p.best, d, static_cast<unsigned long long>(cand + p.index_offset));
     }
   };
 
@@ -703,10 +706,19 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
     // ---- direct mode (the probe): every candidate is a DTW task; warps
     //      claim `direct_chunk` candidates at a time.
     const long long K = p.direct_chunk;
+    const long long nlist =
+        p.list ? min(static_cast<long long>(vload(p.nlist)), p.list_cap) : 0;
     for (;;) {
       unsigned long long c = 0;
       if (lane == 0) c = atomicAdd(p.work, 1ull);
       c = __shfl_sync(kFull, c, 0);
+      if (p.list) {  // the candidates come from the list
+        const long long li = static_cast<long long>(c);
+        if (li >= nlist) break;
+        ++c_cand;
+        run_dtw(p.list[li], false, 0.0, 0.0);
+        continue;
+      }
       const long long base = p.begin + static_cast<long long>(c) * K * p.stride;
       if (base >= p.end) break;
       for (long long k = 0; k < K; ++k) {

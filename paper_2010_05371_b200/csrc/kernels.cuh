@@ -100,6 +100,7 @@ struct SearchParams {
   const long long* list;
   const unsigned long long* nlist;
   long long list_cap;            // entries past it were not written
+  int ub_only;                   // results tighten the threshold only (no record update)
 };
 
 struct PairParams {
