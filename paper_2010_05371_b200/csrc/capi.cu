@@ -816,8 +816,11 @@ static int stage_rank(eapdtw_search_plan* p, size_t cb, size_t ce) {
     up.use_lb = 0;
     up.tighten = 0;
     up.ub_only = 1;
-    up.w = std::max(0, p->w_eff / 16);
-    CUDA_TRY(launch_rank_select(up, S, wave, std::max<long long>(32, p->rank_k / 16), cap,
+    int wdiv = 4, kdiv = 16;  // band w/4 measured best of w/16, w/8, w/4, w/2 (cfg4 -0.5 ms vs w/16)
+    if (const char* e = getenv("EAPDTW_RANK_UBW")) wdiv = std::max(1, atoi(e));
+    if (const char* e = getenv("EAPDTW_RANK_UBK")) kdiv = std::max(1, atoi(e));
+    up.w = std::max(0, p->w_eff / wdiv);
+    CUDA_TRY(launch_rank_select(up, S, wave, std::max<long long>(32, p->rank_k / kdiv), cap,
                                 B.rank.p, list, nlist, s));
     p->ctx->launches += 2;
     CUDA_TRY(reset_work(p, 0, s));
@@ -827,6 +830,8 @@ static int stage_rank(eapdtw_search_plan* p, size_t cb, size_t ce) {
   }
   // then the cascade over the ranks past it (waves of growing rank, each
   // starting from the threshold the better-ranked candidates before it left)
+  if (const char* e = getenv("EAPDTW_RANK_CASCADE"))
+    if (atoi(e) == 0) return EAPDTW_OK;
   for (long long k = std::max<long long>(32, p->rank_k >> (4 * (p->rank_waves - 1)));;
        k = std::min(p->rank_k, k << 4), ++wave) {
     CUDA_TRY(launch_rank_select(rp, S, wave, k, cap, B.rank.p, list, nlist, s));
