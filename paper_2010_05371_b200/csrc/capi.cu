@@ -1185,6 +1185,8 @@ static int nn1_impl(eapdtw_ctx* c, const double* q_dev, size_t nq, const double*
   }
   p.guard_rel = std::max(1e-9, 8.0 * static_cast<double>(len) * 0x1.0p-53);
   p.guard_abs = 1e-20;
+  p.warm = 1;
+  if (const char* env = getenv("EAPDTW_NN1_WARM")) p.warm = atoi(env) != 0;
   CUDA_TRY(set_strip_rows(s));
   CUDA_TRY(launch_nn1(p, s));
   ++c->launches;

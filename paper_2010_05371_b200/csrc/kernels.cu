@@ -1549,13 +1549,52 @@ __global__ void __launch_bounds__(256, EAPDTW_NN1_MINB) nn1_kernel(Nn1Params p) 
   // band; another summation order, so guarded like the search's), then the
   // warp evaluates the survivors in index order.
   const int KL = L >= 16 ? 8 : (L >= 6 ? 3 : 1);
+  // Warm start: each warp first evaluates the row with the smallest layered
+  // LB_Kim among its 1/8 of the block's rows, so the running cutoff starts
+  // near its final value (the main loop skips those rows).
+  __shared__ long long s_warm[32];
+  long long my_warm = -1;
+  if (p.warm && KL > 1) {
+    double bl = INF;
+    long long bk = -1;
+    const int nw = blockDim.x >> 5;
+    for (long long kk = k0 + warp * 32 + lane; kk < k1; kk += static_cast<long long>(nw) * 32) {
+      const double* rw = p.db + kk * L;
+      const double lb = KL == 8 ? kim_layers_raw<8>(rw, L, qsp) : kim_layers_raw<3>(rw, L, qsp);
+      if (lb < bl) {
+        bl = lb;
+        bk = kk;
+      }
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+      const double ol = __shfl_xor_sync(kFull, bl, off);
+      const long long ok = __shfl_xor_sync(kFull, bk, off);
+      if (ol < bl || (ol == bl && ok >= 0 && (bk < 0 || ok < bk))) {
+        bl = ol;
+        bk = ok;
+      }
+    }
+    my_warm = bk;
+    if (lane == 0) s_warm[warp] = bk;
+  } else if (lane == 0) {
+    s_warm[warp] = -1;
+  }
+  __syncthreads();
+  const int nwarm = p.warm && KL > 1 ? static_cast<int>(blockDim.x >> 5) : 0;
+  bool warm_pending = my_warm >= 0;
   for (;;) {
+    long long kb;
+    unsigned surv;
+    if (warm_pending) {  // this warp's warm-start row, alone
+      warm_pending = false;
+      kb = my_warm;
+      surv = 1u;
+    } else {
     unsigned long long t = 0;
     if (lane == 0) t = atomicAdd(&s_next, 32ull);
     t = __shfl_sync(kFull, t, 0);
-    const long long kb = k0 + static_cast<long long>(t);
+    kb = k0 + static_cast<long long>(t);
     if (kb >= k1) break;
-    unsigned surv;
     {
       const long long kk = kb + lane;
       bool keep = kk < k1;
@@ -1572,7 +1611,10 @@ __global__ void __launch_bounds__(256, EAPDTW_NN1_MINB) nn1_kernel(Nn1Params p) 
           if (lb > ubl * (1.0 + p.guard_rel) + p.guard_abs) keep = false;
         }
       }
+      for (int w2 = 0; w2 < nwarm; ++w2)  // warm-start rows are done already
+        if (s_warm[w2] == kk) keep = false;
       surv = __ballot_sync(kFull, keep);
+    }
     }
     for (; surv; surv &= surv - 1) {
     const long long k = kb + (__ffs(surv) - 1);

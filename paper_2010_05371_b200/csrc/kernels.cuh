@@ -131,6 +131,7 @@ struct Nn1Params {
   int use_f32;                    // FP32 screen for queries with max |q| <= f32_cmax
   float f32_a, f32_b, f32_cmax;   // guard built with qmax = cmax (dtw_f32.cuh)
   double guard_rel, guard_abs;    // layered LB_Kim guard (summation order)
+  int warm;                       // per-warp warm start (best layered-Kim row first)
 };
 
 // Each launcher enqueues on `stream` and returns the launch error (no sync).
