@@ -109,10 +109,10 @@ bool all_finite(const double* x, size_t n) {
 
 struct PlanBuffers {
   DevBuf mean, sd, env, q, qul, qperm, order, best, key, work, counters, probe_counters, flag,
-      queue, qtot, qctr, rank, rlist;
+      queue, qtot, qctr, rank, rlist, scratch;
   void release() {
     for (DevBuf* b : {&mean, &sd, &env, &q, &qul, &qperm, &order, &best, &key, &work, &counters,
-                      &probe_counters, &flag, &queue, &qtot, &qctr, &rank, &rlist})
+                      &probe_counters, &flag, &queue, &qtot, &qctr, &rank, &rlist, &scratch})
       b->release();
   }
 };
@@ -544,7 +544,7 @@ static int plan_init(eapdtw_search_plan* p, eapdtw_ctx* c, const double* ref_dev
     const size_t smem = search_smem_bytes(static_cast<int>(m), wpb, p->ad_k);
     if (smem > static_cast<size_t>(optin)) continue;
     const int by_smem = static_cast<int>(max_smem / (smem + 1024));
-    const int by_regs = (2 * 8) / wpb;  // register budget: 16 warps per SM
+    const int by_regs = (search_blocks_per_sm_by_regs() * 8) / wpb;  // register budget
     const int per_sm = std::min(by_smem, std::max(1, by_regs));
     if (per_sm * wpb > best_warps) {
       best_warps = per_sm * wpb;
@@ -560,6 +560,8 @@ static int plan_init(eapdtw_search_plan* p, eapdtw_ctx* c, const double* ref_dev
     const int wv = atoi(env);
     if (wv >= 1 && wv < p->warps) p->warps = wv;
   }
+  if (const size_t sd = search_scratch_doubles(static_cast<int>(m), p->blocks, p->warps, p->ad_k))
+    CUDA_TRY(p->buf->scratch.ensure(sd * 8));
   return eapdtw_search_plan_reset(p);
 }
 
@@ -680,6 +682,7 @@ static SearchParams base_params(eapdtw_search_plan* p) {
   }
   s.counters = B.counters.as<unsigned long long>();
   s.index_offset = static_cast<long long>(p->offset);
+  s.dtw_scratch = B.scratch.p ? B.scratch.as<double>() : nullptr;
   return s;
 }
 

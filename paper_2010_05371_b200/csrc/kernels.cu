@@ -321,9 +321,23 @@ static __host__ __device__ inline size_t padded_len(int m, int ad_k) {
   return static_cast<size_t>(m) + 2 + 2 * static_cast<size_t>(smem_pad(ad_k));
 }
 
+// Lean layout (EAPDTW_SEARCH_LEAN): the per-warp shared buffer holds only the
+// FP32 engine's float row; the exact engine's row lives in global scratch
+// and there is no EQ staging, so three 8-warp blocks fit an SM.
+#ifndef EAPDTW_SEARCH_LEAN
+#define EAPDTW_SEARCH_LEAN 0
+#endif
+static __host__ __device__ inline size_t warp_buf_doubles(int m, int ad_k) {
+#if EAPDTW_SEARCH_LEAN
+  return (padded_len(m, ad_k) + 1) / 2;
+#else
+  return padded_len(m, ad_k) + kStageExtra;
+#endif
+}
+
 size_t search_smem_bytes(int m, int warps, int ad_k) {
   return padded_len(m, ad_k) * 8                        // q (padded, 1-based)
-         + static_cast<size_t>(warps) * (padded_len(m, ad_k) + kStageExtra) * 8  // per-warp buffers
+         + static_cast<size_t>(warps) * warp_buf_doubles(m, ad_k) * 8  // per-warp buffers
          + static_cast<size_t>(warps) * kStackBytesPerWarp  // per-warp tier stacks
          + (padded_len(m, ad_k) * 4 + 7) / 8 * 8              // q as float (FP32 screen)
          + 64;
@@ -440,7 +454,11 @@ using lbacc_t = double;
 #define EAPDTW_SEARCH_THREADS 256
 #endif
 #ifndef EAPDTW_SEARCH_MIN_BLOCKS
+#if EAPDTW_SEARCH_LEAN
+#define EAPDTW_SEARCH_MIN_BLOCKS 3
+#else
 #define EAPDTW_SEARCH_MIN_BLOCKS 2
+#endif
 #endif
 constexpr int kSearchMinBlocks = EAPDTW_SEARCH_MIN_BLOCKS;
 
@@ -462,8 +480,14 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
   const int* __restrict__ order = p.order;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // per-warp buffer: the DTW row buffer, or the LB_Keogh EQ staging tile
-  const size_t wlen = plen + kStageExtra;
+  const size_t wlen = warp_buf_doubles(m, p.ad_k);
+#if EAPDTW_SEARCH_LEAN
+  double* rowbuf = p.dtw_scratch +
+                   (static_cast<size_t>(blockIdx.x) * (blockDim.x >> 5) + warp) * plen + pad;
+  float* rowbuf32 = reinterpret_cast<float*>(smem + plen + static_cast<size_t>(warp) * wlen) + pad;
+#else
   double* rowbuf = smem + plen + static_cast<size_t>(warp) * wlen + pad;
+#endif
   int* stacks = reinterpret_cast<int*>(smem + plen + static_cast<size_t>(blockDim.x >> 5) * wlen);
   // the query as float (FP32 screen), after the stacks; padded like qsp
   float* q32base = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(stacks) +
@@ -472,7 +496,9 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
   // The FP32 engine's row buffer aliases the warp's FP64 one (both engines
   // initialise [0, lc+1] on entry and never depend on the padding contents:
   // out-of-band cells are +inf by the band test).
+#if !EAPDTW_SEARCH_LEAN
   float* rowbuf32 = reinterpret_cast<float*>(rowbuf);
+#endif
 
   const double INF = d_inf();
   for (int k = threadIdx.x; k < static_cast<int>(plen); k += blockDim.x) {
@@ -1102,7 +1128,7 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
           if (lane == 0) atomicAdd(&p.counters[hi >= lo && len <= static_cast<long long>(wlen)
                                                    ? kStageHit : kStageMiss], 1ull);
 #endif
-          if (hi >= lo && len <= static_cast<long long>(wlen)) {
+          if (!EAPDTW_SEARCH_LEAN && hi >= lo && len <= static_cast<long long>(wlen)) {
             double* sbuf = rowbuf - pad;
             const double* src = ref + p.begin + lo;
             for (int t = lane; t < static_cast<int>(len); t += 32) sbuf[t] = src[t];
@@ -1384,6 +1410,12 @@ cudaError_t launch_rank_select(const SearchParams& p, long long S, int wave, lon
                                                  wave > 0 ? thr + wave - 1 : nullptr, thr + wave,
                                                  cap, list, nlist);
   return cudaGetLastError();
+}
+
+int search_blocks_per_sm_by_regs() { return kSearchMinBlocks; }
+
+size_t search_scratch_doubles(int m, int blocks, int warps, int ad_k) {
+  return EAPDTW_SEARCH_LEAN ? static_cast<size_t>(blocks) * warps * padded_len(m, ad_k) : 0;
 }
 
 cudaError_t launch_search(const SearchParams& p, int blocks, int warps, cudaStream_t stream) {

@@ -101,7 +101,11 @@ struct SearchParams {
   const unsigned long long* nlist;
   long long list_cap;            // entries past it were not written
   int ub_only;                   // results tighten the threshold only (no record update)
+  double* dtw_scratch;           // lean layout: the exact engine's row per warp (global)
 };
+// Resident 8-warp search blocks per SM the kernel's register budget allows.
+int search_blocks_per_sm_by_regs();
+size_t search_scratch_doubles(int m, int blocks, int warps, int ad_k);
 
 struct PairParams {
   const double* rows;  // npairs x lr (row-major, pair p at p*row_stride)
