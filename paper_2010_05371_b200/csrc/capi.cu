@@ -1044,24 +1044,10 @@ int eapdtw_similarity_search_dev(eapdtw_ctx* c, const double* ref_dev, size_t n,
 static int one_shot_streamed(eapdtw_ctx* c, const double* host_ref, size_t n,
                              const double* query, size_t qlen, const eapdtw_search_config* cfg,
                              eapdtw_search_result* out) {
-  eapdtw_search_plan p;
-  p.buf = &c->pb;
-  double* dref = c->ref.as<double>();
-  int e = plan_init(&p, c, dref, n, query, qlen, cfg, 0);
-  auto finish = [&](int rc) {
-    for (auto& ev : p.ev)
-      if (ev) cudaEventDestroy(ev);
-    p.buf = &p.own;
-    return rc;
-  };
-  if (e) return finish(e);
-  if (!c->copy) {
-    CUDA_TRY(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
-    for (cudaEvent_t& ev : c->copied)
-      CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-  }
-  cudaStream_t s = c->stream;
-  const size_t m = p.m, ncand = p.ncand;
+  // The copies are issued first, so they overlap the host-side plan set-up
+  // (query preparation, buffers): the split depends on n and m only.
+  const size_t m = cfg->query_length == 0 ? qlen : cfg->query_length;
+  const size_t ncand = n - m + 1;
   const long long nseg = static_cast<long long>((ncand + kStatsResetInterval - 1) / kStatsResetInterval);
   // Part 1 (3/8 of the candidates): everything waits for its copy, while
   // part 2's copy hides under part 1's stats, warm start and sweep.  Shares
@@ -1072,23 +1058,45 @@ static int one_shot_streamed(eapdtw_ctx* c, const double* host_ref, size_t n,
   if (const char* e8 = getenv("EAPDTW_STREAM_SPLIT")) eighths = std::max(1, std::min(7, atoi(e8)));
   const long long seg1 = std::max<long long>(1, nseg * eighths / 8);
   const size_t c1 = static_cast<size_t>(seg1) * kStatsResetInterval;
-  // data part 1 needs: its stats windows, and the envelope tiles covering the
-  // positions its candidates' EC tier reads (< c1 + m - 1), each with radius r
-  size_t d1 = c1 + m - 1;
-  long long te1 = 0;
-  const int T = envelope_tile(p.env_r);
-  if (p.use_lb && T >= 256) {
-    te1 = static_cast<long long>((c1 + m - 1 + T - 1) / T);
-    d1 = std::max(d1, static_cast<size_t>(te1) * T + p.env_r);
+  // data part 1 needs: its stats windows (< c1 + m - 1) and the envelope
+  // tiles covering the positions its candidates' EC tier reads, each with
+  // radius r <= m: within c1 + 2m + the largest tile (8192)
+  const size_t d1 = std::min(n, c1 + 2 * m + 8192);
+  double* dref = c->ref.as<double>();
+  if (!c->copy) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+    for (cudaEvent_t& ev : c->copied)
+      CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   }
-  d1 = std::min(d1, n);
-  CUDA_TRY(cudaEventRecord(p.ev[0], s));  // the copy must not overtake earlier work on s
-  CUDA_TRY(cudaStreamWaitEvent(c->copy, p.ev[0], 0));
+  if (!c->fork) CUDA_TRY(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
+  cudaStream_t s = c->stream;
+  CUDA_TRY(cudaEventRecord(c->fork, s));  // the copy must not overtake earlier work on s
+  CUDA_TRY(cudaStreamWaitEvent(c->copy, c->fork, 0));
   CUDA_TRY(cudaMemcpyAsync(dref, host_ref, d1 * 8, cudaMemcpyHostToDevice, c->copy));
   CUDA_TRY(cudaEventRecord(c->copied[0], c->copy));
   CUDA_TRY(cudaMemcpyAsync(dref + d1, host_ref + d1, (n - d1) * 8, cudaMemcpyHostToDevice,
                            c->copy));
   CUDA_TRY(cudaEventRecord(c->copied[1], c->copy));
+
+  eapdtw_search_plan p;
+  p.buf = &c->pb;
+  int e = plan_init(&p, c, dref, n, query, qlen, cfg, 0);
+  auto finish = [&](int rc) {
+    // an early error return must not leave the copy reading caller memory
+    if (rc) cudaStreamSynchronize(c->copy);
+    for (auto& ev : p.ev)
+      if (ev) cudaEventDestroy(ev);
+    p.buf = &p.own;
+    return rc;
+  };
+  if (e) return finish(e);
+  long long te1 = 0;
+  const int T = envelope_tile(p.env_r);
+  if (p.use_lb && T >= 256) {
+    // tiles [0, te1) read positions < te1*T + r <= c1 + 2m + T - 2 <= d1 (or n)
+    te1 = static_cast<long long>((c1 + m - 1 + T - 1) / T);
+  }
+  CUDA_TRY(cudaEventRecord(p.ev[0], s));
   // ---- part 1
   CUDA_TRY(cudaStreamWaitEvent(s, c->copied[0], 0));
   CUDA_TRY(cudaMemsetAsync(c->pb.flag.p, 0, 8, s));
