@@ -12,6 +12,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <limits>
 #include <mutex>
@@ -278,6 +279,55 @@ int ref_nn1_threads(const double* queries, size_t nq, const double* db, size_t n
   for (auto& t : pool) t.join();
   if (cells) *cells = total;
   return err;
+}
+
+// ---- file formats (io.cpp), used only to generate tests/golden/io_golden.json ----
+
+// io.cpp:50-55; writes at most cap-1 chars + NUL
+int ref_format_double(double v, char* buf, size_t cap) {
+  return guarded([&] {
+    const std::string s = format_double(v);
+    std::snprintf(buf, cap, "%s", s.c_str());
+  });
+}
+
+// io.cpp:57-74 (SearchReport/BestSoFar from a ref_search_result)
+int ref_emit_stats(const ref_search_result* r, const char* path) {
+  return guarded([&] {
+    SearchReport rep;
+    rep.candidates_total = r->candidates_total;
+    rep.pruned_kim = r->pruned_kim;
+    rep.pruned_keogh_eq = r->pruned_keogh_eq;
+    rep.pruned_keogh_ec = r->pruned_keogh_ec;
+    rep.dtw_calls = r->dtw_calls;
+    rep.dtw_abandoned = r->dtw_abandoned;
+    rep.dp_cells_evaluated = r->dp_cells_evaluated;
+    rep.elapsed_seconds = r->elapsed_seconds;
+    BestSoFar best;
+    best.location = r->location;
+    best.distance_sq = r->distance_sq;
+    best.found = r->found != 0;
+    emit_stats(rep, best, path);
+  });
+}
+
+// io.cpp:17-42; on failure copies the exception message into err
+int ref_load_series(const char* path, double* out, size_t cap, size_t* n, char* err,
+                    size_t errcap) {
+  try {
+    const Series s = load_series(path);
+    *n = s.length();
+    std::copy_n(s.begin(), std::min(cap, s.length()), out);
+    return kOk;
+  } catch (const std::exception& e) {
+    std::snprintf(err, errcap, "%s", e.what());
+    return kOther;
+  }
+}
+
+// io.cpp:44-48
+int ref_save_series(const double* s, size_t n, const char* path) {
+  return guarded([&] { save_series(Series(std::vector<double>(s, s + n)), path); });
 }
 
 }  // extern "C"
