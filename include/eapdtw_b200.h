@@ -105,6 +105,20 @@ int eapdtw_similarity_search_dev(eapdtw_ctx* ctx, const double* reference_dev, s
                                  const double* query, size_t qlen,
                                  const eapdtw_search_config* cfg, eapdtw_search_result* out);
 
+/* Device-resident reference: one upload + one Series validation
+ * (series.hpp:24-31) shared by many searches -- the reference CLI's
+ * query-length x window-ratio grid (run_bench, eapdtw_cli.cpp:110-142, which
+ * calls similarity_search once per grid point on the same reference) and
+ * multi-query drivers.  The handle owns its HBM copy until series_free. */
+typedef struct eapdtw_series eapdtw_series;
+int eapdtw_series_upload(eapdtw_ctx* ctx, const double* host, size_t n, eapdtw_series** out);
+const double* eapdtw_series_device_ptr(const eapdtw_series* s);
+size_t eapdtw_series_length(const eapdtw_series* s);
+int eapdtw_series_free(eapdtw_series* s);
+int eapdtw_similarity_search_series(eapdtw_ctx* ctx, const eapdtw_series* reference,
+                                    const double* query, size_t qlen,
+                                    const eapdtw_search_config* cfg, eapdtw_search_result* out);
+
 /* Stepped search over one shard, for multi-GPU drivers.  The shard holds
  * reference[global_offset : global_offset + n) (candidates plus an (m-1)-point
  * halo); global_offset must be a multiple of 100000 (the stats reset

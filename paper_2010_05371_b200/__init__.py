@@ -12,6 +12,7 @@ from .api import (  # noqa: F401
     Band,
     BestSoFar,
     Context,
+    DeviceSeries,
     SearchConfig,
     SearchPlan,
     SearchReport,
@@ -29,6 +30,7 @@ from .api import (  # noqa: F401
     random_walk_normal,
     similarity_search,
     similarity_search_dev,
+    search_grid,
     window_cells_for,
     znormalize,
 )

@@ -81,6 +81,12 @@ SIGNATURES = [
     ("eapdtw_similarity_search_dev", C.c_int,
      [_vp, _vp, C.c_size_t, _dp, C.c_size_t, C.POINTER(SearchConfigC),
       C.POINTER(SearchResultC)]),
+    ("eapdtw_series_upload", C.c_int, [_vp, _dp, C.c_size_t, C.POINTER(_vp)]),
+    ("eapdtw_series_device_ptr", _vp, [_vp]),
+    ("eapdtw_series_length", C.c_size_t, [_vp]),
+    ("eapdtw_series_free", C.c_int, [_vp]),
+    ("eapdtw_similarity_search_series", C.c_int,
+     [_vp, _vp, _dp, C.c_size_t, C.POINTER(SearchConfigC), C.POINTER(SearchResultC)]),
     ("eapdtw_search_plan_create", C.c_int,
      [_vp, _vp, C.c_size_t, _dp, C.c_size_t, C.POINTER(SearchConfigC), C.c_uint64,
       C.POINTER(_vp)]),

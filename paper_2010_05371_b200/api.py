@@ -338,6 +338,75 @@ def similarity_search_dev(ref_dev_ptr: int, n: int, query, cfg: SearchConfig, *,
     return SearchResult.from_c(res)
 
 
+class DeviceSeries:
+    """A reference series resident in HBM (``eapdtw_series``): uploaded and
+    validated once, then searched any number of times -- the reference CLI's
+    bench grid (eapdtw_cli.cpp:110-142) and multi-query searches."""
+
+    def __init__(self, samples, *, ctx=None):
+        self.ctx = ctx or default_context()
+        x = samples.view() if isinstance(samples, Series) else _as_f64(samples)
+        h = C.c_void_p()
+        check(lib.eapdtw_series_upload(self.ctx.handle, _ptr(x), x.size, C.byref(h)))
+        self.handle = h
+
+    def __len__(self) -> int:
+        return int(lib.eapdtw_series_length(self.handle))
+
+    @property
+    def device_ptr(self) -> int:
+        return int(lib.eapdtw_series_device_ptr(self.handle))
+
+    def search(self, query, cfg: SearchConfig | None = None) -> SearchResult:
+        """similarity_search (search.hpp:118-119) against this reference."""
+        cfg = cfg or SearchConfig()
+        q = query.view() if isinstance(query, Series) else Series(query).view()
+        res = _capi.SearchResultC()
+        c = cfg.to_c()
+        check(lib.eapdtw_similarity_search_series(self.ctx.handle, self.handle, _ptr(q), q.size,
+                                                  C.byref(c), C.byref(res)))
+        return SearchResult.from_c(res)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib.eapdtw_series_free(self.handle)
+            self.handle = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def search_grid(reference, query, lengths, ratios, algos=(Algo.ea_pruned,), *,
+                use_lower_bounds: bool = True, tighten_ub: bool = True, ctx=None):
+    """The reference CLI's bench grid (run_bench, eapdtw_cli.cpp:110-142):
+    for each algorithm, query length (a prefix of ``query``) and window
+    ratio, one similarity_search of the same reference.  The reference is
+    uploaded to HBM once.  Yields ``(algo, length, ratio, SearchResult)`` in
+    the reference's loop order (algo, then length, then ratio)."""
+    own = not isinstance(reference, DeviceSeries)
+    ref = DeviceSeries(reference, ctx=ctx) if own else reference
+    try:
+        for algo in algos:
+            for length in lengths:
+                for ratio in ratios:
+                    cfg = SearchConfig(query_length=int(length), window_ratio=float(ratio),
+                                       algorithm=Algo(algo), use_lower_bounds=use_lower_bounds,
+                                       tighten_ub=tighten_ub and use_lower_bounds)
+                    yield Algo(algo), int(length), float(ratio), ref.search(query, cfg)
+    finally:
+        if own:
+            ref.close()
+
+
 class SearchPlan:
     """One shard of a (possibly multi-GPU) search: stepped C-ABI plan."""
 

@@ -1033,6 +1033,70 @@ int eapdtw_similarity_search_dev(eapdtw_ctx* c, const double* ref_dev, size_t n,
   return one_shot(c, ref_dev, n, query, qlen, cfg, true, out);
 }
 
+// ---------------------------------------------------------------------------
+// Device-resident series: one upload (and one Series validation,
+// series.hpp:24-31) serves many searches -- the CLI's query-length x
+// window-ratio grid (eapdtw_cli.cpp:110-142) and multi-query drivers.
+// ---------------------------------------------------------------------------
+struct eapdtw_series {
+  int device = 0;
+  DevBuf data;
+  size_t n = 0;
+};
+
+int eapdtw_series_upload(eapdtw_ctx* c, const double* host, size_t n, eapdtw_series** out) {
+  if (!c || !host || !out) return fail(EAPDTW_EINVAL, "null argument");
+  if (n == 0) return fail(EAPDTW_EINVAL, "Series: empty input");
+  *out = nullptr;
+  CUDA_TRY(cudaSetDevice(c->device));
+  auto* s = new eapdtw_series;
+  s->device = c->device;
+  s->n = n;
+  cudaError_t e = s->data.ensure(n * 8);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(s->data.p, host, n * 8, cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess) e = c->pb.flag.ensure(8);
+  if (e == cudaSuccess) e = cudaMemsetAsync(c->pb.flag.p, 0, 8, c->stream);
+  if (e == cudaSuccess) {
+    e = launch_check_finite(s->data.as<double>(), static_cast<long long>(n),
+                            c->pb.flag.as<unsigned long long>(), c->stream);
+    ++c->launches;
+  }
+  unsigned long long bad = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&bad, c->pb.flag.p, 8, cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess || bad) {
+    s->data.release();
+    delete s;
+    if (e != cudaSuccess) return fail(EAPDTW_ECUDA, std::string("series_upload: ") + cudaGetErrorString(e));
+    return fail(EAPDTW_EINVAL, "Series: non-finite sample in the reference");
+  }
+  *out = s;
+  return EAPDTW_OK;
+}
+
+const double* eapdtw_series_device_ptr(const eapdtw_series* s) {
+  return s ? s->data.as<const double>() : nullptr;
+}
+
+size_t eapdtw_series_length(const eapdtw_series* s) { return s ? s->n : 0; }
+
+int eapdtw_series_free(eapdtw_series* s) {
+  if (!s) return EAPDTW_OK;
+  cudaSetDevice(s->device);
+  cudaDeviceSynchronize();
+  s->data.release();
+  delete s;
+  return EAPDTW_OK;
+}
+
+int eapdtw_similarity_search_series(eapdtw_ctx* c, const eapdtw_series* ref, const double* query,
+                                    size_t qlen, const eapdtw_search_config* cfg,
+                                    eapdtw_search_result* out) {
+  if (!c || !ref) return fail(EAPDTW_EINVAL, "null argument");
+  if (ref->device != c->device) return fail(EAPDTW_EINVAL, "series lives on another device");
+  return one_shot(c, ref->data.as<const double>(), ref->n, query, qlen, cfg, false, out);
+}
+
 // Host-pointer search of a long reference, streamed: the reference goes to the
 // device in two parts on a copy stream, and the second part's copy runs under
 // the first part's sweep.  Part 1 is the candidates of the first half of the
