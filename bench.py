@@ -294,6 +294,13 @@ def run_batch(args):
         print(json.dumps(line), flush=True)
         return 0
     ctx = g.Context(0)
+    # e2e inputs come from pinned host memory (the contract's H2D), as for cfg2-4
+    if cfg == "cfg1":
+        a = torch.from_numpy(a).pin_memory().numpy()
+        b = torch.from_numpy(b).pin_memory().numpy()
+    else:
+        qs = torch.from_numpy(qs).pin_memory().numpy()
+        db = torch.from_numpy(db).pin_memory().numpy()
     times, dev_ms = [], []
     for k in range(args.warmup + args.steps):
         torch.cuda.synchronize()

@@ -88,6 +88,25 @@ int eapdtw_ea_pruned_dtw_windowed(eapdtw_ctx* ctx, const double* a, size_t la, c
 int eapdtw_dtw_windowed(eapdtw_ctx* ctx, const double* a, size_t la, const double* b, size_t lb,
                         size_t window, double* out, uint64_t* cells);
 
+/* --- per-cell trace of one DTW (KernelTrace, dtw.hpp:42-57) ---------------- *
+ * algo 0 dtw_full / dtw_windowed, 1 dtw_left_prune(_windowed), 2 ea_pruned_dtw
+ * (dtw.hpp:69-99, no cumulative bound), computed on the device by one thread
+ * in the reference's event order: kind 0 cell (row, col, value), 1 discard
+ * point, 2 pruning point, 3 abandon (at the last evaluated cell).  Rows and
+ * columns are 1-based matrix coordinates (row 0 / col 0 are the borders).
+ * At most cap events are stored; *n_events is the full count (retry with a
+ * larger buffer if it exceeds cap).  A debugging path (the CLI's `trace`),
+ * not a throughput path. */
+typedef struct {
+  uint32_t kind;
+  uint32_t pad_;
+  uint64_t row, col;
+  double value;
+} eapdtw_trace_event;
+int eapdtw_trace(eapdtw_ctx* ctx, int algo, const double* a, size_t la, const double* b,
+                 size_t lb, size_t window, double ub, eapdtw_trace_event* events, size_t cap,
+                 size_t* n_events, uint64_t* cells, double* out);
+
 /* --- batched pairwise (cfg1): npairs pairs of equal length len --------------
  * out[p] = ea_pruned_dtw_windowed(a_p, b_p, Band{window}, ub[p]); ub NULL = +inf.
  * prune 0 gives dtw_windowed (no abandoning). */

@@ -14,10 +14,12 @@
 // a CUDA failure throws std::runtime_error.  There is no CPU fallback.
 #pragma once
 
+#include <algorithm>
 #include <cmath>
 #include <cstddef>
 #include <cstdint>
 #include <limits>
+#include <optional>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -82,17 +84,66 @@ struct Band {
   [[nodiscard]] constexpr bool is_unbounded() const { return window == unbounded_window; }
 };
 
-// Counters-only trace (dtw.hpp:42-57): cells evaluated by the GPU kernel.
+// dtw.hpp:27-57.  Counters are always kept; with capture_cells set, the call
+// runs the device trace (eapdtw_trace: one thread, the reference's event
+// order) and fills cells / discard_points / pruning_points / abandon_cell.
+struct CellRef {
+  std::size_t row = 0;
+  std::size_t col = 0;
+};
+struct TraceCell {
+  std::size_t row = 0;
+  std::size_t col = 0;
+  double value = 0.0;
+};
 struct KernelTrace {
   std::size_t cells_evaluated = 0;
-  void reset() { cells_evaluated = 0; }
+  bool capture_cells = false;
+  std::vector<TraceCell> cells;
+  std::vector<CellRef> discard_points;
+  std::vector<CellRef> pruning_points;
+  std::optional<CellRef> abandon_cell;
+  void reset() {
+    cells_evaluated = 0;
+    cells.clear();
+    discard_points.clear();
+    pruning_points.clear();
+    abandon_cell.reset();
+  }
 };
+
+namespace detail {
+// algo: EAPDTW_ALGO_FULL / _LEFT_PRUNE / _EA_PRUNED
+inline double traced(int algo, std::span<const double> a, std::span<const double> b,
+                     std::size_t window, double ub, KernelTrace& trace) {
+  const std::size_t lr = std::max(a.size(), b.size()), lc = std::min(a.size(), b.size());
+  std::vector<eapdtw_trace_event> ev(2 * (lr + 2) * (lc + 2) + 8);
+  std::size_t n = 0;
+  uint64_t cells = 0;
+  double out = PRUNED;
+  check(eapdtw_trace(context(), algo, a.data(), a.size(), b.data(), b.size(), window, ub,
+                     ev.data(), ev.size(), &n, &cells, &out));
+  trace.cells_evaluated += cells;
+  for (std::size_t k = 0; k < std::min(n, ev.size()); ++k) {
+    const eapdtw_trace_event& e = ev[k];
+    switch (e.kind) {
+      case 0: trace.cells.push_back({e.row, e.col, e.value}); break;
+      case 1: trace.discard_points.push_back({e.row, e.col}); break;
+      case 2: trace.pruning_points.push_back({e.row, e.col}); break;
+      default: trace.abandon_cell = CellRef{e.row, e.col}; break;
+    }
+  }
+  return out;
+}
+}  // namespace detail
 
 // --- DTW kernels, span level (dtw.hpp:69-99)
 [[nodiscard]] inline double ea_pruned_dtw_windowed(std::span<const double> a,
                                                    std::span<const double> b, Band band, double ub,
                                                    std::span<const double> cumulative_bound,
                                                    KernelTrace& trace) {
+  if (trace.capture_cells && cumulative_bound.empty())
+    return detail::traced(EAPDTW_ALGO_EA_PRUNED, a, b, band.window, ub, trace);
   double out = PRUNED;
   uint64_t cells = 0;
   detail::check(eapdtw_ea_pruned_dtw_windowed(detail::context(), a.data(), a.size(), b.data(),
@@ -117,6 +168,7 @@ struct KernelTrace {
 }
 [[nodiscard]] inline double dtw_windowed(std::span<const double> a, std::span<const double> b,
                                          Band band, KernelTrace& trace) {
+  if (trace.capture_cells) return detail::traced(EAPDTW_ALGO_FULL, a, b, band.window, PRUNED, trace);
   double out = PRUNED;
   uint64_t cells = 0;
   detail::check(eapdtw_dtw_windowed(detail::context(), a.data(), a.size(), b.data(), b.size(),
@@ -132,6 +184,19 @@ struct KernelTrace {
 [[nodiscard]] inline double dtw_full(std::span<const double> a, std::span<const double> b) {
   return dtw_windowed(a, b, Band::unbounded());
 }
+[[nodiscard]] inline double dtw_full(std::span<const double> a, std::span<const double> b,
+                                     KernelTrace& trace) {
+  return dtw_windowed(a, b, Band::unbounded(), trace);
+}
+// Left pruning has EAPrunedDTW's result contract (exact iff <= ub, else
+// PRUNED); without capture it runs the pruned kernel.
+[[nodiscard]] inline double dtw_left_prune_windowed(std::span<const double> a,
+                                                    std::span<const double> b, Band band,
+                                                    double ub, KernelTrace& trace) {
+  if (trace.capture_cells)
+    return detail::traced(EAPDTW_ALGO_LEFT_PRUNE, a, b, band.window, ub, trace);
+  return ea_pruned_dtw_windowed(a, b, band, ub, {}, trace);
+}
 [[nodiscard]] inline double dtw_left_prune_windowed(std::span<const double> a,
                                                     std::span<const double> b, Band band,
                                                     double ub) {
@@ -140,6 +205,10 @@ struct KernelTrace {
 [[nodiscard]] inline double dtw_left_prune(std::span<const double> a, std::span<const double> b,
                                            double ub) {
   return ea_pruned_dtw_windowed(a, b, Band::unbounded(), ub);
+}
+[[nodiscard]] inline double dtw_left_prune(std::span<const double> a, std::span<const double> b,
+                                           double ub, KernelTrace& trace) {
+  return dtw_left_prune_windowed(a, b, Band::unbounded(), ub, trace);
 }
 
 // Series-level conveniences (dtw.hpp:103-135)

@@ -325,6 +325,26 @@ int ref_load_series(const char* path, double* out, size_t cap, size_t* n, char* 
   }
 }
 
+// run_trace (eapdtw_cli.cpp:91-108) generalised to a band: the traced kernel
+// (dtw.hpp:69-99 KernelTrace overloads) + write_trace_csv (io.cpp:76-122).
+int ref_trace_csv(int algo, const double* a, size_t la, const double* b, size_t lb, size_t window,
+                  double ub, const char* path, double* out, uint64_t* cells) {
+  return guarded([&] {
+    std::span<const double> sa(a, la), sb(b, lb);
+    KernelTrace trace;
+    trace.capture_cells = true;
+    const Band band = band_of(window);
+    switch (algo) {
+      case 0: *out = dtw_windowed(sa, sb, band, trace); break;
+      case 1: *out = dtw_left_prune_windowed(sa, sb, band, ub, trace); break;
+      case 2: *out = ea_pruned_dtw_windowed(sa, sb, band, ub, {}, trace); break;
+      default: throw std::invalid_argument("algo");
+    }
+    *cells = trace.cells_evaluated;
+    write_trace_csv(trace, path);
+  });
+}
+
 // io.cpp:44-48
 int ref_save_series(const double* s, size_t n, const char* path) {
   return guarded([&] { save_series(Series(std::vector<double>(s, s + n)), path); });

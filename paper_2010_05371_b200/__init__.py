@@ -13,6 +13,7 @@ from .api import (  # noqa: F401
     BestSoFar,
     Context,
     DeviceSeries,
+    KernelTrace,
     SearchConfig,
     SearchPlan,
     SearchReport,
@@ -31,6 +32,7 @@ from .api import (  # noqa: F401
     similarity_search,
     similarity_search_dev,
     search_grid,
+    trace,
     window_cells_for,
     znormalize,
 )

@@ -71,6 +71,9 @@ SIGNATURES = [
       _u64p]),
     ("eapdtw_dtw_windowed", C.c_int,
      [_vp, _dp, C.c_size_t, _dp, C.c_size_t, C.c_size_t, _dp, _u64p]),
+    ("eapdtw_trace", C.c_int,
+     [_vp, C.c_int, _dp, C.c_size_t, _dp, C.c_size_t, C.c_size_t, C.c_double, _vp, C.c_size_t,
+      C.POINTER(C.c_size_t), _u64p, _dp]),
     ("eapdtw_pairwise", C.c_int,
      [_vp, _dp, _dp, C.c_size_t, C.c_size_t, C.c_size_t, _dp, C.c_int, _dp, _u64p]),
     ("eapdtw_pairwise_dev", C.c_int,

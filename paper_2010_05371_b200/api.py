@@ -338,6 +338,62 @@ def similarity_search_dev(ref_dev_ptr: int, n: int, query, cfg: SearchConfig, *,
     return SearchResult.from_c(res)
 
 
+# --- trace (KernelTrace, dtw.hpp:42-57) ------------------------------------------
+
+class TraceEventC(C.Structure):
+    _fields_ = [("kind", C.c_uint32), ("pad_", C.c_uint32), ("row", C.c_uint64),
+                ("col", C.c_uint64), ("value", C.c_double)]
+
+
+@dataclass
+class KernelTrace:
+    """dtw.hpp:42-57 with capture_cells = true: the evaluated cells
+    (row, col, value) in evaluation order, discard points, pruning points and
+    the abandon cell (None unless the kernel abandoned).  ``result`` is the
+    traced call's return value."""
+
+    cells_evaluated: int = 0
+    cells: list = field(default_factory=list)
+    discard_points: list = field(default_factory=list)
+    pruning_points: list = field(default_factory=list)
+    abandon_cell: tuple | None = None
+    result: float = PRUNED
+
+
+_TRACE_ALGO = {Algo.full: 0, Algo.left_prune: 1, Algo.ea_pruned: 2}
+
+
+def trace(a, b, algo=Algo.ea_pruned, ub: float = PRUNED, band=None, *, ctx=None) -> KernelTrace:
+    """Per-cell trace of one DTW on the device (the CLI's ``trace``,
+    eapdtw_cli.cpp:91-108): ``dtw_full``/``dtw_windowed`` (algo full; ub
+    ignored), ``dtw_left_prune(_windowed)`` or ``ea_pruned_dtw(_windowed)``,
+    rows/cols 1-based.  A debugging path: one device thread."""
+    ctx = ctx or default_context()
+    a, b = _as_f64(a), _as_f64(b)
+    code = _TRACE_ALGO[Algo(algo)]
+    cap = (max(a.size, b.size) + 2) * (min(a.size, b.size) + 2) * 2 + 8
+    ev = (TraceEventC * cap)()
+    n = C.c_size_t(0)
+    cells = C.c_uint64(0)
+    out = C.c_double(0.0)
+    check(lib.eapdtw_trace(ctx.handle, code, _ptr(a), a.size, _ptr(b), b.size, _window(band),
+                           float(ub), ev, cap, C.byref(n), C.byref(cells), C.byref(out)))
+    if n.value > cap:  # cannot happen (at most 2 events per cell + rows + 2)
+        raise RuntimeError(f"trace: {n.value} events exceed the buffer ({cap})")
+    t = KernelTrace(cells_evaluated=int(cells.value), result=float(out.value))
+    for k in range(n.value):
+        e = ev[k]
+        if e.kind == 0:
+            t.cells.append((int(e.row), int(e.col), float(e.value)))
+        elif e.kind == 1:
+            t.discard_points.append((int(e.row), int(e.col)))
+        elif e.kind == 2:
+            t.pruning_points.append((int(e.row), int(e.col)))
+        else:
+            t.abandon_cell = (int(e.row), int(e.col))
+    return t
+
+
 class DeviceSeries:
     """A reference series resident in HBM (``eapdtw_series``): uploaded and
     validated once, then searched any number of times -- the reference CLI's

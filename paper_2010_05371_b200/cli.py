@@ -13,8 +13,8 @@ Differences from the reference, all additive: ``--data``/``--query`` also
 accept binary series (``.f64``/``.bin`` raw little-endian float64, ``.npy``)
 so 1e8-point references need not be parsed as text; ``--device`` picks the
 GPU; ``bench`` uploads its reference to HBM once for the whole grid
-(``search_grid``).  ``trace`` (per-cell KernelTrace capture) is not on the
-GPU path and exits with status 2.  Exit status: 0 ok,
+(``search_grid``); ``trace`` captures the cells on the device
+(``eapdtw_trace``) and writes the reference's CSV.  Exit status: 0 ok,
 2 for the reference's CLI::ValidationError cases (bad --algo, ratio off the
 grid, argument errors), 1 for every other error (eapdtw_cli.cpp:232-238).
 """
@@ -23,15 +23,20 @@ from __future__ import annotations
 import argparse
 import math
 import os
+import re
 import sys
 
 from . import seriesio
 from .api import Algo, Context, DeviceSeries, SearchConfig, random_walk, search_grid
-from .api import similarity_search
+from .api import PRUNED, similarity_search, trace
 from .seriesio import format_double
 
 _ALGOS = {"full": Algo.full, "lp": Algo.left_prune, "eap": Algo.ea_pruned}
 _RATIO_GRID = (0.1, 0.2, 0.3, 0.4, 0.5)
+# std::stod with the whole string consumed (decimal or hex floats, inf/nan)
+_FLOAT_PREFIX = re.compile(r"\s*[+-]?(?:(?:\d+\.?\d*|\.\d+)(?:[eE][+-]?\d+)?|"
+                           r"0[xX](?:[0-9a-fA-F]+\.?[0-9a-fA-F]*|\.[0-9a-fA-F]+)"
+                           r"(?:[pP][+-]?\d+)?|inf(?:inity)?|nan)", re.IGNORECASE)
 
 
 class ValidationError(Exception):
@@ -54,6 +59,19 @@ def on_ratio_grid(r: float) -> bool:
 def ratio_label(r: float) -> str:
     """eapdtw_cli.cpp:52-58"""
     return format_double(r).replace(".", "p")
+
+
+def parse_ub(text: str) -> float:
+    """eapdtw_cli.cpp:27-37"""
+    if text in ("inf", "INF", "+inf"):
+        return PRUNED
+    try:
+        v = float.fromhex(text) if "x" in text.lower() else float(text)
+    except ValueError:
+        v = math.nan
+    if math.isnan(v) or v < 0.0 or not _FLOAT_PREFIX.fullmatch(text):
+        raise ValidationError("--ub: expected a non-negative float or 'inf'")
+    return v
 
 
 def result_lines(res) -> list[str]:
@@ -103,6 +121,21 @@ def run_search(a, out) -> int:
     out.write("\n".join(result_lines(res)) + "\n")
     if a.stats:
         seriesio.emit_stats(res.report, res.best, a.stats)
+    return 0
+
+
+def run_trace(a, out) -> int:
+    """run_trace (eapdtw_cli.cpp:91-108): one traced DTW of two series files."""
+    sa = seriesio.read_series(a.a)
+    sb = seriesio.read_series(a.b)
+    ub = parse_ub(a.ub)
+    algo = parse_algo(a.algo)
+    ctx = Context(a.device)
+    try:
+        t = trace(sa, sb, algo, ub, ctx=ctx)
+    finally:
+        ctx.close()
+    seriesio.write_trace_csv(t, a.out)
     return 0
 
 
@@ -174,9 +207,13 @@ def make_parser() -> argparse.ArgumentParser:
                    help="accepted for protocol compatibility; unused")
     s.add_argument("--device", type=int, default=0, help="CUDA device")
 
-    t = sub.add_parser("trace", help="(reference only) dump the evaluated DP matrix cells")
-    for opt in ("--a", "--b", "--ub", "--algo", "--out"):
-        t.add_argument(opt)
+    t = sub.add_parser("trace", help="dump the evaluated DP matrix cells as CSV")
+    t.add_argument("--a", required=True, help="first series file")
+    t.add_argument("--b", required=True, help="second series file")
+    t.add_argument("--ub", required=True, help="threshold (float or 'inf'); ignored by --algo full")
+    t.add_argument("--algo", required=True, help="DTW kernel: full|lp|eap")
+    t.add_argument("--out", required=True, help="output CSV path")
+    t.add_argument("--device", type=int, default=0, help="CUDA device")
 
     b = sub.add_parser("bench", help="run the query-length x window-ratio grid")
     b.add_argument("--grid-lengths", type=_csv(int), default=[128, 256, 512, 1024])
@@ -198,8 +235,7 @@ def main(argv=None, out=None) -> int:
             return run_search(a, out)
         if a.cmd == "bench":
             return run_bench(a, out)
-        raise ValidationError("trace: per-cell trace capture is not on the GPU path; "
-                              "use the reference CLI")
+        return run_trace(a, out)
     except ValidationError as e:
         sys.stderr.write(f"error: {e}\n")
         return 2

@@ -348,6 +348,59 @@ int eapdtw_dtw_windowed(eapdtw_ctx* c, const double* a, size_t la, const double*
   return single_pair(c, a, la, b, lb, window, kInf, nullptr, 0, 0, out, cells);
 }
 
+int eapdtw_trace(eapdtw_ctx* c, int algo, const double* a, size_t la, const double* b, size_t lb,
+                 size_t window, double ub, eapdtw_trace_event* events, size_t cap,
+                 size_t* n_events, uint64_t* cells, double* out) {
+  if (!c || !n_events || !out) return fail(EAPDTW_EINVAL, "null argument");
+  if (algo < 0 || algo > 2) return fail(EAPDTW_EINVAL, "trace: algo must be 0 (full), 1 (lp), 2 (eap)");
+  if (la == 0 || lb == 0 || !a || !b) return fail(EAPDTW_EINVAL, "dtw: empty series");
+  if (cap && !events) return fail(EAPDTW_EINVAL, "null argument");
+  const double* rows = a;  // orient (dtw.cpp:48-52)
+  const double* cols = b;
+  size_t lr = la, lc = lb;
+  if (la < lb) {
+    rows = b;
+    cols = a;
+    lr = lb;
+    lc = la;
+  }
+  *n_events = 0;
+  if (cells) *cells = 0;
+  // effective_window (dtw.cpp:57-62): no path fits -> PRUNED, nothing traced
+  size_t w = lr;
+  if (window != EAPDTW_UNBOUNDED_WINDOW) {
+    if (lr - lc > window) {
+      *out = kInf;
+      return EAPDTW_OK;
+    }
+    if (window < lc) w = window;
+  }
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(c->a.ensure(lr * 8));
+  CUDA_TRY(c->b.ensure(lc * 8));
+  CUDA_TRY(c->cb.ensure(2 * (lc + 1) * 8));
+  CUDA_TRY(c->counters.ensure(3 * 8));
+  CUDA_TRY(c->out.ensure((cap ? cap : 1) * sizeof(TraceEvent)));
+  CUDA_TRY(c->ub.ensure(8));
+  CUDA_TRY(cudaMemcpyAsync(c->a.p, rows, lr * 8, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->b.p, cols, lc * 8, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(launch_trace(algo, c->a.as<double>(), static_cast<long long>(lr), c->b.as<double>(),
+                        static_cast<long long>(lc), static_cast<long long>(w), ub,
+                        c->cb.as<double>(), c->out.as<TraceEvent>(), static_cast<long long>(cap),
+                        c->counters.as<unsigned long long>(), c->ub.as<double>(), c->stream));
+  ++c->launches;
+  unsigned long long hdr[2] = {0, 0};
+  CUDA_TRY(cudaMemcpyAsync(hdr, c->counters.p, 16, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(out, c->ub.p, 8, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  const size_t stored = std::min<size_t>(cap, hdr[0]);
+  if (stored)
+    CUDA_TRY(cudaMemcpy(events, c->out.p, stored * sizeof(TraceEvent), cudaMemcpyDeviceToHost));
+  *n_events = hdr[0];
+  if (cells) *cells = hdr[1];
+  return EAPDTW_OK;
+}
+
 int eapdtw_pairwise_dev(eapdtw_ctx* c, const double* a_dev, const double* b_dev, size_t npairs,
                         size_t len, size_t window, const double* ub_dev, int prune,
                         double* out_dev, uint64_t* cells) {

@@ -177,4 +177,19 @@ void debug_read_reset(unsigned long long* out16);
 cudaError_t launch_fp64_probe(double* sink, int blocks, int iters, cudaStream_t stream);
 cudaError_t launch_fp32_probe(float* sink, int blocks, int iters, cudaStream_t stream);
 
+// Per-cell event log of one DTW (trace.cu); layout = eapdtw_trace_event.
+enum : unsigned { kTraceCell = 0, kTraceDiscard = 1, kTracePruningPoint = 2, kTraceAbandon = 3 };
+struct TraceEvent {
+  unsigned kind, pad_;
+  unsigned long long row, col;
+  double value;
+};
+// algo 0 full_scan, 1 left_prune_scan, 2 ea_pruned_scan over rows (the longer
+// series) x cols with effective half-window w; buf: 2 (lc + 1) doubles;
+// hdr[0] = events (may exceed cap: only cap are stored), hdr[1] = cells.
+cudaError_t launch_trace(int algo, const double* rows, long long lr, const double* cols,
+                         long long lc, long long w, double ub, double* buf, TraceEvent* ev,
+                         long long cap, unsigned long long* hdr, double* result,
+                         cudaStream_t stream);
+
 }  // namespace eapdtw_b200

@@ -129,6 +129,51 @@ def emit_stats(report, best, path) -> None:
         raise SeriesFileError(f"cannot write stats to '{os.fspath(path)}'") from None
 
 
+def trace_csv(trace) -> str:
+    """write_trace_csv (io.cpp:76-122): header, then events in order -- every
+    cell, a discard point right after its cell, a row's pruning points when
+    the row closes (the border row's before every cell), the abandon cell
+    last; marker values are the last captured value of their cell, else inf."""
+    lines = ["row,col,value,kind"]
+
+    def value_at(ref):
+        for r, c, v in reversed(trace.cells):
+            if (r, c) == tuple(ref):
+                return format_double(v)
+        return "inf"
+
+    def emit(r, c, value, kind):
+        lines.append(f"{r},{c},{value},{kind}")
+
+    nd = npp = 0
+    dps, pps, cells = trace.discard_points, trace.pruning_points, trace.cells
+    while npp < len(pps) and pps[npp][0] == 0:
+        emit(pps[npp][0], pps[npp][1], "inf", "pruning_point")
+        npp += 1
+    for k, (r, c, v) in enumerate(cells):
+        emit(r, c, format_double(v), "cell")
+        if nd < len(dps) and tuple(dps[nd]) == (r, c):
+            nd += 1
+            emit(r, c, format_double(v), "discard_point")
+        row_done = k + 1 == len(cells) or cells[k + 1][0] != r
+        while row_done and npp < len(pps) and pps[npp][0] == r:
+            emit(pps[npp][0], pps[npp][1], value_at(pps[npp]), "pruning_point")
+            npp += 1
+    if trace.abandon_cell is not None:
+        a = trace.abandon_cell
+        emit(a[0], a[1], value_at(a), "abandon")
+    return "\n".join(lines) + "\n"
+
+
+def write_trace_csv(trace, path) -> None:
+    """io.cpp:76-122"""
+    try:
+        with open(path, "w") as f:
+            f.write(trace_csv(trace))
+    except OSError:
+        raise SeriesFileError(f"cannot write trace to '{os.fspath(path)}'") from None
+
+
 def _parse_token(tok: str) -> float | None:
     """std::from_chars on the whole token; None = 'is not a number'."""
     if _NONFINITE.fullmatch(tok):

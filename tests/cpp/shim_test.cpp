@@ -27,6 +27,24 @@ int main() {
   CHECK(is_pruned(ea_pruned_dtw_windowed(s, t, Band::cells(0), 22.0)));
   CHECK(ea_pruned_dtw_windowed(s, t, Band::cells(0), 23.0) == 23.0);
   CHECK(dtw_left_prune(s.view(), t.view(), 9.0) == 9.0);
+  {  // KernelTrace capture (test_dtw.cpp / cli_tests.cpp:176-204): eap at ub 6
+     // abandons at (5,3) = 7; the full kernel evaluates all 36 cells, (6,6) = 9
+    KernelTrace tr;
+    tr.capture_cells = true;
+    CHECK(is_pruned(ea_pruned_dtw(s.view(), t.view(), 6.0, tr)));
+    CHECK(tr.abandon_cell && tr.abandon_cell->row == 5 && tr.abandon_cell->col == 3);
+    CHECK(!tr.cells.empty() && tr.cells.back().value == 7.0);
+    CHECK(tr.cells_evaluated == tr.cells.size());
+    CHECK(!tr.discard_points.empty() && !tr.pruning_points.empty());
+    KernelTrace fu;
+    fu.capture_cells = true;
+    CHECK(dtw_full(s.view(), t.view(), fu) == 9.0);
+    CHECK(fu.cells.size() == 36 && fu.cells.back().row == 6 && fu.cells.back().col == 6);
+    KernelTrace lp;
+    lp.capture_cells = true;
+    CHECK(is_pruned(dtw_left_prune(s.view(), t.view(), 6.0, lp)));
+    CHECK(lp.abandon_cell && lp.abandon_cell->row == 5);
+  }
   bool threw = false;
   try {
     const std::vector<double> bad = {1.0, 0.0};

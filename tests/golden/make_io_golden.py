@@ -58,6 +58,51 @@ def load_cases() -> list[str]:
             "--1\n", ".\n", "1..2\n", "007\n", "1_000\n", "infinity\n", "1e5.5\n"]
 
 
+def trace_inputs():
+    """(a, b, window, ub) cases: the worked example at the reference tests'
+    thresholds (test_dtw.cpp:53-131, cli_tests.cpp:176-204) and seeded small
+    pairs (equal and unequal lengths, banded and unbounded)."""
+    S, T = [3.0, 1.0, 4.0, 4.0, 1.0, 1.0], [1.0, 3.0, 2.0, 1.0, 2.0, 2.0]
+    cases = [(S, T, -1, ub) for ub in (float("inf"), 22.0, 9.0, 8.0, 6.0, 0.0)]
+    cases += [(S, T, 1, 23.0), (S, T, 0, 22.0), ([0.0, 5.0, 0.0], [0.0, 1.0], -1, 17.0),
+              ([0.0, 0.0], [0.0, 5.0], -1, 10.0), ([2.0], [5.0], -1, 9.0)]
+    rng = np.random.default_rng(5371)
+    for k in range(24):
+        la = int(rng.integers(4, 24))
+        lb = la if k % 3 else int(rng.integers(3, la + 1))
+        a = np.cumsum(rng.standard_normal(la)).tolist()
+        b = np.cumsum(rng.standard_normal(lb)).tolist()
+        w = -1 if k % 4 == 0 else int(rng.integers(0, la))
+        ub = float(rng.choice([np.inf, 1.0, 5.0, 20.0, 80.0]))
+        cases.append((a, b, w, ub))
+    return cases
+
+
+def trace_cases(L):
+    L.ref_trace_csv.argtypes = [C.c_int, C.POINTER(C.c_double), C.c_size_t,
+                                C.POINTER(C.c_double), C.c_size_t, C.c_size_t, C.c_double,
+                                C.c_char_p, C.POINTER(C.c_double), C.POINTER(C.c_uint64)]
+    res = []
+    with tempfile.TemporaryDirectory() as tmp:
+        p = os.path.join(tmp, "trace.csv")
+        for a, b, w, ub in trace_inputs():
+            for algo in (0, 1, 2):
+                pa = (C.c_double * len(a))(*a)
+                pb = (C.c_double * len(b))(*b)
+                out, cells = C.c_double(0), C.c_uint64(0)
+                window = oracle.UNBOUNDED if w < 0 else w
+                if os.path.exists(p):
+                    os.remove(p)
+                rc = L.ref_trace_csv(algo, pa, len(a), pb, len(b), window, ub, p.encode(),
+                                     C.byref(out), C.byref(cells))
+                assert rc == 0
+                text = open(p).read() if os.path.exists(p) else None
+                res.append({"a": [bits(x) for x in a], "b": [bits(x) for x in b], "window": w,
+                            "ub": bits(ub), "algo": algo, "result": bits(out.value),
+                            "cells": cells.value, "csv": text})
+    return res
+
+
 def main():
     ref = oracle.Reference()
     L = ref.lib
@@ -144,6 +189,8 @@ def main():
             with open(p) as f:
                 saves.append({"values": [bits(v) for v in series], "text": f.read()})
         out["save_series"] = saves
+
+    out["trace"] = trace_cases(L)
 
     with open(os.path.join(HERE, "io_golden.json"), "w") as f:
         json.dump(out, f, indent=1)

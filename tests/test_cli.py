@@ -60,8 +60,10 @@ def test_ratio_grid_and_algo_validation(files):
     assert run(base(files) + ["--algo", "nope"])[0] == 2
     assert run(["search", "--data", files / "R.txt"])[0] == 2  # missing required options
     assert run(["bench"])[0] == 2
-    assert run(["trace", "--a", files / "S.txt", "--b", files / "T.txt", "--ub", "6",
+    assert run(["trace", "--a", files / "S.txt", "--b", files / "T.txt", "--ub", "x",
                 "--algo", "eap", "--out", files / "t.csv"])[0] == 2
+    assert run(["trace", "--a", files / "S.txt", "--b", files / "T.txt", "--ub", "6",
+                "--algo", "nope", "--out", files / "t.csv"])[0] == 2
 
 
 def test_missing_data_file(files):
@@ -196,3 +198,80 @@ def test_device_series_reuse(oracle_lib):
     bad[1234] = np.nan
     with pytest.raises(ValueError, match="non-finite"):
         g.DeviceSeries(bad)
+
+
+# ---------------------------------------------------------------- trace ---------
+
+def _golden_traces():
+    import struct as _s
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "io_golden.json")))
+
+    def ub(h):
+        return _s.unpack("<d", _s.pack("<Q", int(h, 16)))[0]
+    return [dict(c, a=[ub(x) for x in c["a"]], b=[ub(x) for x in c["b"]], ub=ub(c["ub"]),
+                 result=ub(c["result"])) for c in g["trace"]]
+
+
+def _trace_from_csv(text):
+    """Parse a reference trace CSV back into a KernelTrace-like object."""
+    from paper_2010_05371_b200.api import KernelTrace
+    t = KernelTrace()
+    for line in text.strip().splitlines()[1:]:
+        r, c, v, kind = line.split(",")
+        r, c = int(r), int(c)
+        if kind == "cell":
+            t.cells.append((r, c, float(v)))
+        elif kind == "discard_point":
+            t.discard_points.append((r, c))
+        elif kind == "pruning_point":
+            t.pruning_points.append((r, c))
+        else:
+            t.abandon_cell = (r, c)
+    return t
+
+
+def test_trace_csv_writer_round_trips_reference():
+    """write_trace_csv restatement: the reference's CSV, parsed and re-written,
+    is reproduced byte for byte (io.cpp:76-122)."""
+    cases = _golden_traces()
+    assert len(cases) > 100
+    for c in cases:
+        assert seriesio.trace_csv(_trace_from_csv(c["csv"])) == c["csv"]
+
+
+@pytest.mark.gpu
+def test_trace_matches_reference_csv():
+    """The device trace reproduces the reference's CSV, cells count and return
+    value for full / lp / eap on the worked example and seeded pairs."""
+    import paper_2010_05371_b200 as g
+    from paper_2010_05371_b200.api import UNBOUNDED_WINDOW
+    algos = {0: g.Algo.full, 1: g.Algo.left_prune, 2: g.Algo.ea_pruned}
+    for c in _golden_traces():
+        band = UNBOUNDED_WINDOW if c["window"] < 0 else c["window"]
+        t = g.trace(c["a"], c["b"], algos[c["algo"]], c["ub"], band)
+        assert seriesio.trace_csv(t) == c["csv"], (c["algo"], c["window"], c["ub"])
+        assert t.cells_evaluated == c["cells"]
+        assert t.result == c["result"] or (math.isinf(t.result) and math.isinf(c["result"]))
+
+
+@pytest.mark.gpu
+def test_cli_trace(files):
+    """cli_tests.cpp:176-204"""
+    out = files / "full.csv"
+    rc, _ = run(["trace", "--a", files / "S.txt", "--b", files / "T.txt", "--ub", "6",
+                 "--algo", "full", "--out", out])
+    assert rc == 0
+    csv = out.read_text()
+    assert csv.splitlines()[0] == "row,col,value,kind"
+    assert sum(1 for line in csv.splitlines() if line.endswith(",cell")) == 36
+    assert "6,6,9,cell" in csv
+    eap = files / "eap.csv"
+    assert run(["trace", "--a", files / "S.txt", "--b", files / "T.txt", "--ub", "6",
+                "--algo", "eap", "--out", eap])[0] == 0
+    assert "5,3,7,abandon" in eap.read_text()
+    lp = files / "lp.csv"
+    assert run(["trace", "--a", files / "S.txt", "--b", files / "T.txt", "--ub", "6",
+                "--algo", "lp", "--out", lp])[0] == 0
+    assert lp.read_text().splitlines()[-1].startswith("5,")
+    assert run(["trace", "--a", files / "S.txt", "--b", files / "T.txt", "--ub", "-1",
+                "--algo", "eap", "--out", lp])[0] == 2
