@@ -42,6 +42,13 @@ BATCH_CONFIGS = {
     "cfg5": "cfg5: 1000 queries x 20000 database series, z-normalised N(0,1) random walks, "
             "L=512, unbounded band, running cutoff per query; NN1",
 }
+# the reference CLI's bench grid (eapdtw_cli.cpp:110-142)
+GRID = {"n": 1_000_000, "seed": 42, "lengths": (128, 256, 512, 1024),
+        "ratios": (0.1, 0.2, 0.3, 0.4, 0.5)}
+GRID_DESC = ("grid: the reference CLI's bench grid (eapdtw_cli.cpp:110-142) -- query lengths "
+             "128/256/512/1024 x window ratios 0.1-0.5, EAPrunedDTW + LB cascade, 20 searches of "
+             "a 1e6-point random_walk(seed 42) reference (the reference's uniform-step "
+             "generator, io.cpp:124-137) with prefixes of a random_walk(1024, 43) query")
 FP64_OPS_PER_CELL = 5  # DSUB, DMUL, DADD + 2 DSETP (min3) per counted cell
 FP32_OPS_PER_CELL = 4  # FSUB, FMUL, FADD + 1 FMNMX3 per counted cell of the FP32 screen
 
@@ -378,18 +385,135 @@ def run_batch(args):
     return 0
 
 
+def grid_reference_step(lib, ref, q, threads, sample):
+    """One bounded sample of the grid on the reference: every grid point's first
+    `sample` candidates (one stats segment), grid points spread over the host
+    threads (ctypes releases the GIL), each an unmodified similarity_search."""
+    from concurrent.futures import ThreadPoolExecutor
+    points = [(L, r) for L in GRID["lengths"] for r in GRID["ratios"]]
+
+    def one(pt):
+        L, r = pt
+        return lib.similarity_search_threads(ref[:sample + L - 1], q, r, 1, query_length=L)
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        res = list(ex.map(one, points))
+    return time.perf_counter() - t0, len(points) * sample, res
+
+
+def run_grid(args):
+    """The paper's / reference CLI's query-length x window-ratio grid on one
+    device-resident reference (DeviceSeries): subsequences searched per second
+    summed over the 20 searches."""
+    import torch
+
+    import paper_2010_05371_b200 as g
+    import oracle
+    if int(os.environ.get("RANK", "0")) != 0:
+        return 0
+    n = GRID["n"]
+    ref = g.random_walk(n, GRID["seed"])
+    q = g.random_walk(max(GRID["lengths"]), GRID["seed"] + 1)
+    units = sum(n - L + 1 for L in GRID["lengths"]) * len(GRID["ratios"])
+    threads = os.cpu_count() or 1
+    sample = 100_000
+    if args.impl == "reference":
+        lib = oracle.Reference()
+        times = []
+        for k in range(args.warmup + args.steps):
+            dt, nunits, _ = grid_reference_step(lib, ref, q, threads, sample)
+            if k >= args.warmup:
+                times.append(dt)
+        v = nunits / statistics.mean(times)
+        smp = (f"first {sample} candidates of each of the 20 grid points, grid points in "
+               f"parallel on {threads} threads")
+        print(json.dumps({
+            "impl": "reference", "metric": "subsequences searched/sec", "value": v,
+            "unit": "subsequences/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": statistics.mean(times) * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: the reference's seeded random_walk", "config": {"workload": GRID_DESC},
+            "cpu_baseline": {"value": v, "unit": "subsequences/s", "cores": threads,
+                             "kind": "reference", "sample": smp},
+            "e2e": {"value": v, "unit": "subsequences/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}), flush=True)
+        return 0
+    ctx = g.Context(0)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    dref = g.DeviceSeries(ref, ctx=ctx)
+
+    def grid_once(reference):
+        return [r for _, _, _, r in g.search_grid(reference, q, GRID["lengths"], GRID["ratios"],
+                                                  ctx=ctx)]
+    for _ in range(args.warmup):
+        grid_once(dref)
+    torch.cuda.synchronize()
+    launches0 = ctx.launches
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            results = grid_once(dref)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    launches = ctx.launches - launches0
+    # e2e: search_grid on host memory (one pinned H2D of the reference per grid)
+    pinned = torch.from_numpy(ref).pin_memory().numpy()
+    e2e_t = []
+    for it in range(args.steps + 1):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res_h = grid_once(pinned)
+        torch.cuda.synchronize()
+        if it:
+            e2e_t.append(time.perf_counter() - t0)
+    for a, b in zip(results, res_h):
+        assert (a.best.location, a.best.distance_sq) == (b.best.location, b.best.distance_sq)
+    cpu = None
+    if not args.no_cpu_baseline:
+        dt, nunits, _ = grid_reference_step(oracle.Reference(), ref, q, threads, sample)
+        cpu = {"value": nunits / dt, "unit": "subsequences/s", "cores": threads,
+               "kind": "reference",
+               "sample": f"first {sample} candidates of each grid point, {threads} threads, "
+                         f"{dt:.2f} s"}
+    dref.close()
+    print(json.dumps({
+        "metric": "subsequences searched/sec", "value": units / (ms * 1e-3),
+        "unit": "subsequences/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic: the reference's seeded random_walk",
+        "config": {"workload": GRID_DESC, "searches_per_step": len(results),
+                   "l2": "8 MB reference resident in HBM (fits L2; each search streams its "
+                         "own stats/envelope buffers)"},
+        "roofline": None, "cpu_baseline": cpu,
+        "e2e": {"value": units / statistics.mean(e2e_t), "unit": "subsequences/s",
+                "h2d_bytes_per_step": int(ref.nbytes + 20 * 8 * 1024),
+                "d2h_bytes_per_step": 20 * 88},
+        "gpu_launches": launches // max(1, args.steps) * args.steps,
+        "clocks": clk.summary(),
+        "per_search_ms": {f"len{L}_r{r}": res.report.elapsed_seconds * 1e3
+                          for (L, r), res in zip([(L, r) for L in GRID["lengths"]
+                                                  for r in GRID["ratios"]], results)},
+        "cells_per_step": sum(r.report.dp_cells_evaluated for r in results)}), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg4", choices=sorted(CONFIGS) + sorted(BATCH_CONFIGS))
+    ap.add_argument("--config", default="cfg4", choices=sorted(CONFIGS) + sorted(BATCH_CONFIGS) + ["grid"])
     ap.add_argument("--batches", type=int, default=8, help="best-so-far exchanges per search (N>1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-segments", type=int, default=20,
                     help="cpu_baseline sample: this many 100000-candidate segments")
     args = ap.parse_args()
+    if args.config == "grid":
+        return run_grid(args)
     if args.config in BATCH_CONFIGS:
         return run_batch(args)
     if args.impl == "reference":

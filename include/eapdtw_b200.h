@@ -128,13 +128,16 @@ int eapdtw_similarity_search_dev(eapdtw_ctx* ctx, const double* reference_dev, s
  * (series.hpp:24-31) shared by many searches -- the reference CLI's
  * query-length x window-ratio grid (run_bench, eapdtw_cli.cpp:110-142, which
  * calls similarity_search once per grid point on the same reference) and
- * multi-query drivers.  The handle owns its HBM copy until series_free. */
+ * multi-query drivers.  The handle owns its HBM copy until series_free, and
+ * caches the sliding statistics (mean, sd) of the last query length searched:
+ * they depend on the reference and m only (search.cpp:156-168), so searches
+ * that differ in window, algorithm or query content reuse them. */
 typedef struct eapdtw_series eapdtw_series;
 int eapdtw_series_upload(eapdtw_ctx* ctx, const double* host, size_t n, eapdtw_series** out);
 const double* eapdtw_series_device_ptr(const eapdtw_series* s);
 size_t eapdtw_series_length(const eapdtw_series* s);
 int eapdtw_series_free(eapdtw_series* s);
-int eapdtw_similarity_search_series(eapdtw_ctx* ctx, const eapdtw_series* reference,
+int eapdtw_similarity_search_series(eapdtw_ctx* ctx, eapdtw_series* reference,
                                     const double* query, size_t qlen,
                                     const eapdtw_search_config* cfg, eapdtw_search_result* out);
 

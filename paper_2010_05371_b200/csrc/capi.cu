@@ -151,6 +151,7 @@ struct eapdtw_search_plan {
   size_t ncand = 0;
   cudaEvent_t ev[8] = {};
   bool prepared = false, ran = false;
+  bool stats_ready = false;  // mean/sd already in the buffers (a series' cached stats)
   int blocks = 0, warps = 8, ad_k = 0, screen_rows = 2;  // screen depth: 2 measured best with the FP32 engine
   int use_f32 = 1;  // FP32 screening engine ahead of the exact one (EAPDTW_F32=0: off)
   bool overlap_prep = false;  // stats || envelope on two streams (measured slower: the chain shares its SMs)
@@ -933,11 +934,11 @@ int eapdtw_search_plan_prepare(eapdtw_search_plan* p) {
   int e;
   CUDA_TRY(cudaEventRecord(p->ev[0], s));
   p->have_env = false;
-  if (p->overlap_prep) {  // stats || envelope: the "stats" phase spans both
+  if (p->overlap_prep && !p->stats_ready) {  // stats || envelope: the "stats" phase spans both
     if ((e = stage_stats_env(p, 0, -1, 0, -1, true))) return e;
     CUDA_TRY(cudaEventRecord(p->ev[1], s));
   } else {
-    if ((e = stage_stats(p, 0, -1))) return e;
+    if (!p->stats_ready && (e = stage_stats(p, 0, -1))) return e;
     CUDA_TRY(cudaEventRecord(p->ev[1], s));
     if ((e = stage_env(p, 0, -1, true))) return e;
   }
@@ -1052,13 +1053,33 @@ int eapdtw_search_plan_destroy(eapdtw_search_plan* p) {
   return EAPDTW_OK;
 }
 
+// Cached sliding statistics of a device-resident series for one query length
+// (the chain depends on the reference and m only, search.cpp:156-168): the
+// grid's 5 window ratios per length share one stats pass.
+struct SeriesStats {
+  DevBuf mean, sd;
+  size_t m = 0;  // 0: empty
+};
+
 static int one_shot(eapdtw_ctx* c, const double* ref_dev, size_t n, const double* query,
                     size_t qlen, const eapdtw_search_config* cfg, bool check_ref,
-                    eapdtw_search_result* out) {
+                    eapdtw_search_result* out, SeriesStats* cache = nullptr) {
   if (!c || !cfg || !out) return fail(EAPDTW_EINVAL, "null argument");
   eapdtw_search_plan p;
   p.buf = &c->pb;  // reuse the context's grow-only scratch
   int e = plan_init(&p, c, ref_dev, n, query, qlen, cfg, 0);
+  bool fill_cache = false;
+  if (!e && cache) {
+    const size_t bytes = p.ncand * 8;
+    if (cache->m == p.m) {
+      if (cudaMemcpyAsync(c->pb.mean.p, cache->mean.p, bytes, cudaMemcpyDeviceToDevice, c->stream) ||
+          cudaMemcpyAsync(c->pb.sd.p, cache->sd.p, bytes, cudaMemcpyDeviceToDevice, c->stream))
+        e = fail(EAPDTW_ECUDA, "series stats cache: copy failed");
+      p.stats_ready = true;
+    } else {
+      fill_cache = true;
+    }
+  }
   if (!e && check_ref) {
     // Series validation (series.hpp:24-31) of the reference, on the device.
     CUDA_TRY(cudaMemsetAsync(c->pb.flag.p, 0, 8, c->stream));
@@ -1067,6 +1088,16 @@ static int one_shot(eapdtw_ctx* c, const double* ref_dev, size_t n, const double
     ++c->launches;
   }
   if (!e) e = eapdtw_search_plan_prepare(&p);
+  if (!e && fill_cache) {
+    const size_t bytes = p.ncand * 8;
+    cache->m = 0;  // the cache is optional: on any failure it simply stays empty
+    if (!cache->mean.ensure(bytes) && !cache->sd.ensure(bytes) &&
+        !cudaMemcpyAsync(cache->mean.p, c->pb.mean.p, bytes, cudaMemcpyDeviceToDevice, c->stream) &&
+        !cudaMemcpyAsync(cache->sd.p, c->pb.sd.p, bytes, cudaMemcpyDeviceToDevice, c->stream))
+      cache->m = p.m;
+    else
+      cudaGetLastError();
+  }
   if (!e) e = eapdtw_search_plan_run(&p, 0, p.ncand);
   if (!e) e = eapdtw_search_plan_result(&p, out);
   if (!e && check_ref) {
@@ -1095,6 +1126,7 @@ struct eapdtw_series {
   int device = 0;
   DevBuf data;
   size_t n = 0;
+  SeriesStats stats;  // the last query length's sliding statistics
 };
 
 int eapdtw_series_upload(eapdtw_ctx* c, const double* host, size_t n, eapdtw_series** out) {
@@ -1138,16 +1170,21 @@ int eapdtw_series_free(eapdtw_series* s) {
   cudaSetDevice(s->device);
   cudaDeviceSynchronize();
   s->data.release();
+  s->stats.mean.release();
+  s->stats.sd.release();
   delete s;
   return EAPDTW_OK;
 }
 
-int eapdtw_similarity_search_series(eapdtw_ctx* c, const eapdtw_series* ref, const double* query,
+int eapdtw_similarity_search_series(eapdtw_ctx* c, eapdtw_series* ref, const double* query,
                                     size_t qlen, const eapdtw_search_config* cfg,
                                     eapdtw_search_result* out) {
   if (!c || !ref) return fail(EAPDTW_EINVAL, "null argument");
   if (ref->device != c->device) return fail(EAPDTW_EINVAL, "series lives on another device");
-  return one_shot(c, ref->data.as<const double>(), ref->n, query, qlen, cfg, false, out);
+  if (getenv("EAPDTW_SERIES_STATS_CACHE") && atoi(getenv("EAPDTW_SERIES_STATS_CACHE")) == 0)
+    return one_shot(c, ref->data.as<const double>(), ref->n, query, qlen, cfg, false, out);
+  return one_shot(c, ref->data.as<const double>(), ref->n, query, qlen, cfg, false, out,
+                  &ref->stats);
 }
 
 // Host-pointer search of a long reference, streamed: the reference goes to the
