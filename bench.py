@@ -253,9 +253,11 @@ def run_batch(args):
     from paper_2010_05371_b200 import _capi
     import ctypes as C
     rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return 0
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     cfg = args.config
+    sharded = cfg == "cfg5" and (world > 1 or args.shard_nn1) and args.impl != "reference"
+    if rank != 0 and not sharded:
+        return 0  # cfg1 (and the reference arm) run on rank 0; cfg5 shards its database
     if cfg == "cfg1":
         npairs, L, w = 1024, 256, 25
         a = np.stack([g.znormalize(g.random_walk_normal(L, 1000 + p)) for p in range(npairs)])
@@ -269,6 +271,8 @@ def run_batch(args):
         db = np.stack([g.znormalize(np.cumsum(rng.standard_normal(L))) for _ in range(nd)])
         units = nq * nd
         unit = "query-series pairs/s"
+    if sharded:
+        return run_nn1_sharded(args, qs, db, rank, world)
     if args.impl == "reference":
         import oracle
         lib = oracle.Reference() if oracle.Reference.available() else None
@@ -401,6 +405,82 @@ def grid_reference_step(lib, ref, q, threads, sample):
     return time.perf_counter() - t0, len(points) * sample, res
 
 
+def run_nn1_sharded(args, qs, db, rank, world):
+    """cfg5 over N GPUs: each rank holds 1/N of the database rows
+    and all queries; 4 batches per rank with an NCCL all-reduce (MIN) of the
+    per-query cutoffs between them, then one all-gather and a lexicographic
+    (distance, lowest global index) merge.  Time = max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2010_05371_b200 as g
+    from paper_2010_05371_b200.sharded import GpuNN1Shard, ShardedNN1, db_shard_bounds
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    nq, nd = qs.shape[0], db.shape[0]
+    d0, d1 = db_shard_bounds(nd, world, rank)
+    ctx = g.Context(local)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    dq = torch.from_numpy(qs).to(dev)
+    ddb = torch.from_numpy(db[d0:d1]).to(dev)
+    shard = GpuNN1Shard(dq, ddb, ctx=ctx)
+    runner = ShardedNN1(shard, rank, world, d0, batches=4, device=dev)
+    for _ in range(args.warmup):
+        runner.search()
+    shard.cells = 0
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = ctx.launches
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            arg, dd = runner.search()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    cells_timed = shard.cells / max(1, args.steps)
+    dist.barrier()
+    ms = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    launches = ctx.launches - launches0
+    # e2e: pinned host shard -> HBM, then the sharded search, every step
+    qp, dbp = torch.from_numpy(qs).pin_memory(), torch.from_numpy(db[d0:d1]).pin_memory()
+    e2e_t = []
+    for it in range(args.steps + 1):
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        dq.copy_(qp, non_blocking=True)
+        ddb.copy_(dbp, non_blocking=True)
+        runner.search()
+        torch.cuda.synchronize()
+        if it:
+            e2e_t.append(time.perf_counter() - t0)
+    te = torch.tensor([statistics.mean(e2e_t)], dtype=torch.float64, device=dev)
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        unit = "query-series pairs/s"
+        print(json.dumps({
+            "metric": "query-series pairs per second", "value": nq * nd / (ms * 1e-3),
+            "unit": unit, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic z-normalised N(0,1) random walks",
+            "config": {"workload": BATCH_CONFIGS["cfg5"], "parallelism": f"db{world}",
+                       "batches_per_rank": runner.batches},
+            "roofline": None,
+            "e2e": {"value": nq * nd / float(te.item()), "unit": unit,
+                    "h2d_bytes_per_step": int(qs.nbytes + db[d0:d1].nbytes),
+                    "d2h_bytes_per_step": nq * 16 * runner.batches},
+            "gpu_launches": launches, "clocks": clk.summary(),
+            "cells_per_step_rank0": cells_timed}), flush=True)
+    dist.destroy_process_group()
+    return 0
+
+
 def run_grid(args):
     """The paper's / reference CLI's query-length x window-ratio grid on one
     device-resident reference (DeviceSeries): subsequences searched per second
@@ -509,6 +589,8 @@ def main():
     ap.add_argument("--config", default="cfg4", choices=sorted(CONFIGS) + sorted(BATCH_CONFIGS) + ["grid"])
     ap.add_argument("--batches", type=int, default=8, help="best-so-far exchanges per search (N>1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard-nn1", action="store_true",
+                    help="cfg5: the sharded driver (batches + cutoff all-reduce) even at N=1")
     ap.add_argument("--cpu-segments", type=int, default=20,
                     help="cpu_baseline sample: this many 100000-candidate segments")
     args = ap.parse_args()

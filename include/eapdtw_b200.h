@@ -180,6 +180,18 @@ int eapdtw_nn1_dev(eapdtw_ctx* ctx, const double* queries_dev, size_t nq, const 
                    size_t nd, size_t len, size_t window, uint64_t* argmin, double* dist,
                    uint64_t* cells);
 
+/* One shard / batch of a multi-GPU NN1: the same search
+ * starting from a per-query cutoff (cutoff_dev: nq non-negative doubles on the
+ * device, +inf = none), e.g. the all-reduced MIN of every rank's best so far.
+ * A database row is reported iff its distance is <= the cutoff (ties with the
+ * cutoff are kept, so a lexicographic (distance, global index) merge across
+ * shards keeps the lowest index); a query with no such row gets argmin 0 and
+ * dist +inf.  argmin is local to db_dev. */
+int eapdtw_nn1_dev_cutoff(eapdtw_ctx* ctx, const double* queries_dev, size_t nq,
+                          const double* db_dev, size_t nd, size_t len, size_t window,
+                          const double* cutoff_dev, uint64_t* argmin, double* dist,
+                          uint64_t* cells);
+
 /* --- host-side helpers (bit-identical to the reference) -------------------- */
 /* RunningStats::over + znormalize_into (search.cpp:25-46) */
 int eapdtw_znormalize(const double* src, size_t n, double* dst);

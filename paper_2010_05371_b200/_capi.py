@@ -107,6 +107,8 @@ SIGNATURES = [
      [_vp, _dp, C.c_size_t, _dp, C.c_size_t, C.c_size_t, C.c_size_t, _u64p, _dp, _u64p]),
     ("eapdtw_nn1_dev", C.c_int,
      [_vp, _vp, C.c_size_t, _vp, C.c_size_t, C.c_size_t, C.c_size_t, _u64p, _dp, _u64p]),
+    ("eapdtw_nn1_dev_cutoff", C.c_int,
+     [_vp, _vp, C.c_size_t, _vp, C.c_size_t, C.c_size_t, C.c_size_t, _vp, _u64p, _dp, _u64p]),
     ("eapdtw_znormalize", C.c_int, [_dp, C.c_size_t, _dp]),
     ("eapdtw_random_walk_uniform", C.c_int, [C.c_size_t, C.c_uint64, _dp]),
     ("eapdtw_random_walk_normal", C.c_int, [C.c_size_t, C.c_uint64, _dp]),

@@ -1309,7 +1309,7 @@ int eapdtw_similarity_search(eapdtw_ctx* c, const double* ref, size_t n, const d
 // ---------------------------------------------------------------------------
 static int nn1_impl(eapdtw_ctx* c, const double* q_dev, size_t nq, const double* db_dev,
                     size_t nd, size_t len, size_t window, uint64_t* argmin, double* dist,
-                    uint64_t* cells) {
+                    uint64_t* cells, const double* cutoff_dev = nullptr) {
   int w = (window == EAPDTW_UNBOUNDED_WINDOW || window >= len) ? static_cast<int>(len)
                                                               : static_cast<int>(window);
   cudaStream_t s = c->stream;
@@ -1320,6 +1320,10 @@ static int nn1_impl(eapdtw_ctx* c, const double* q_dev, size_t nq, const double*
   CUDA_TRY(launch_init_best(c->best.as<BestRecord>(), c->keys.as<unsigned long long>(),
                             static_cast<long long>(nq), s));
   ++c->launches;
+  // a starting cutoff per query: the threshold key is the bit pattern of a
+  // non-negative double (order-preserving), so the cutoffs are copied in as is
+  if (cutoff_dev)
+    CUDA_TRY(cudaMemcpyAsync(c->keys.p, cutoff_dev, nq * 8, cudaMemcpyDeviceToDevice, s));
   Nn1Params p{};
   p.queries = q_dev;
   p.db = db_dev;
@@ -1383,6 +1387,16 @@ int eapdtw_nn1_dev(eapdtw_ctx* c, const double* q_dev, size_t nq, const double* 
   if (nq == 0) return EAPDTW_OK;
   CUDA_TRY(cudaSetDevice(c->device));
   return nn1_impl(c, q_dev, nq, db_dev, nd, len, window, argmin, dist, cells);
+}
+
+int eapdtw_nn1_dev_cutoff(eapdtw_ctx* c, const double* q_dev, size_t nq, const double* db_dev,
+                          size_t nd, size_t len, size_t window, const double* cutoff_dev,
+                          uint64_t* argmin, double* dist, uint64_t* cells) {
+  if (!c || !argmin || !dist || !cutoff_dev) return fail(EAPDTW_EINVAL, "null argument");
+  if (len == 0 || nd == 0) return fail(EAPDTW_EINVAL, "nn1: empty series");
+  if (nq == 0) return EAPDTW_OK;
+  CUDA_TRY(cudaSetDevice(c->device));
+  return nn1_impl(c, q_dev, nq, db_dev, nd, len, window, argmin, dist, cells, cutoff_dev);
 }
 
 int eapdtw_nn1(eapdtw_ctx* c, const double* queries, size_t nq, const double* db, size_t nd,

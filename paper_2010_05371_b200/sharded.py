@@ -126,3 +126,105 @@ class ShardedSearch:
         dist.all_gather(out, t, group=self.group)
         recs = [(bool(o[2].item()), double_of(o[0].item()), int(o[1].item())) for o in out]
         return lexicographic_min(recs), res
+
+
+# --- batched NN1 (cfg5) over a database sharded across ranks -----
+
+def db_shard_bounds(nd: int, world: int, rank: int) -> tuple[int, int]:
+    """Database rows [d0, d1) of ``rank``: contiguous, as even as possible
+    (earlier ranks take the remainder), so global index order = rank order."""
+    base, extra = divmod(nd, world)
+    d0 = rank * base + min(rank, extra)
+    return d0, d0 + base + (1 if rank < extra else 0)
+
+
+def merge_nn1(best_d, best_i, d, i):
+    """Per-query lexicographic (distance, lowest global index) merge, in place.
+    Entries with d = +inf carry no match."""
+    take = np.isfinite(d) & ((d < best_d) | ((d == best_d) & (i < best_i)))
+    best_d[take] = d[take]
+    best_i[take] = i[take]
+
+
+class GpuNN1Shard:
+    """Backend over eapdtw_nn1_dev_cutoff: the queries and this rank's database
+    rows resident on its GPU (torch float64 tensors, row-major)."""
+
+    def __init__(self, queries_dev, db_shard_dev, window=None, ctx=None):
+        from .api import default_context
+        self.ctx = ctx or default_context()
+        self.q = queries_dev
+        self.db = db_shard_dev
+        self.window = window
+        self.nq, self.len = int(queries_dev.shape[0]), int(queries_dev.shape[1])
+        self.rows = int(db_shard_dev.shape[0])
+        self.cells = 0
+
+    def run(self, b0: int, b1: int, cutoff):
+        """(argmin local to [b0, b1), dist) of every query over rows [b0, b1),
+        starting from the per-query cutoff tensor (device float64)."""
+        import ctypes as C
+
+        from . import _capi
+        from .api import _window
+        arg = np.empty(self.nq, dtype=np.uint64)
+        dist = np.empty(self.nq)
+        cells = C.c_uint64(0)
+        import torch
+        # the cutoff was written (H2D copy / all-reduce) on torch's stream
+        torch.cuda.current_stream(self.q.device).synchronize()
+        ptr = self.db.data_ptr() + b0 * self.len * 8
+        _capi.check(_capi.lib.eapdtw_nn1_dev_cutoff(
+            self.ctx.handle, C.c_void_p(self.q.data_ptr()), self.nq, C.c_void_p(ptr), b1 - b0,
+            self.len, _window(self.window), C.c_void_p(cutoff.data_ptr()),
+            arg.ctypes.data_as(C.POINTER(C.c_uint64)), dist.ctypes.data_as(C.POINTER(C.c_double)),
+            C.byref(cells)))
+        self.cells += cells.value
+        return arg.astype(np.int64), dist
+
+
+class ShardedNN1:
+    """One rank's part of a sharded NN1: its database rows [offset, offset +
+    rows) in ``batches`` batches; between batches the ranks all-reduce (MIN)
+    the per-query best distance, which is the next batch's cutoff everywhere.
+    The final answer per query is the lexicographic (distance, lowest global
+    index) minimum over the ranks (one all-gather)."""
+
+    def __init__(self, backend, rank: int, world: int, offset: int, batches: int = 4,
+                 device=None, group=None):
+        self.backend = backend
+        self.rank, self.world = rank, world
+        self.offset = int(offset)
+        self.batches = max(1, int(batches))
+        self.device = device
+        self.group = group
+
+    def search(self):
+        import torch
+        import torch.distributed as dist
+        b = self.backend
+        nq = b.nq
+        best_d = np.full(nq, math.inf)
+        best_i = np.zeros(nq, dtype=np.int64)
+        cutoff = torch.full((nq,), math.inf, dtype=torch.float64, device=self.device)
+        edges = np.linspace(0, b.rows, self.batches + 1).astype(np.int64)
+        for k in range(self.batches):
+            b0, b1 = int(edges[k]), int(edges[k + 1])
+            if b1 > b0:
+                arg, d = b.run(b0, b1, cutoff)
+                merge_nn1(best_d, best_i, d, arg + self.offset + b0)
+            cutoff = torch.from_numpy(best_d.copy()).to(cutoff.device)
+            if self.world > 1:
+                dist.all_reduce(cutoff, op=dist.ReduceOp.MIN, group=self.group)
+        if self.world == 1:
+            return best_i, best_d
+        mine = torch.stack([torch.from_numpy(best_d).view(torch.int64),
+                            torch.from_numpy(best_i)]).to(cutoff.device)
+        parts = [torch.empty_like(mine) for _ in range(self.world)]
+        dist.all_gather(parts, mine, group=self.group)
+        out_d = np.full(nq, math.inf)
+        out_i = np.zeros(nq, dtype=np.int64)
+        for p in parts:  # rank order = global index order
+            p = p.cpu()
+            merge_nn1(out_d, out_i, p[0].view(torch.float64).numpy(), p[1].numpy())
+        return out_i, out_d

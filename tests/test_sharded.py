@@ -135,3 +135,108 @@ def test_two_rank_tie_goes_to_lowest_global_index(oracle_lib):
     res = _run(ref, motif, m, 0.1)
     for rank in (0, 1):
         assert res[rank][0] == (True, 0.0, 120_000)
+
+
+# --- sharded NN1 (cfg5) ------------------------------------------------
+
+class OracleNN1Shard:
+    """CPU stand-in for GpuNN1Shard: the oracle's NN1 over rows [b0, b1) of the
+    shard, with eapdtw_nn1_dev_cutoff's contract (a row counts iff its distance
+    is <= the query's cutoff; none -> argmin 0, +inf)."""
+
+    def __init__(self, queries, db_shard):
+        import oracle
+        self.o = oracle.Oracle()
+        self.qs, self.db = queries, db_shard
+        self.nq, self.rows = queries.shape[0], db_shard.shape[0]
+        self.cutoffs = []
+
+    def run(self, b0, b1, cutoff):
+        c = cutoff.numpy().copy()
+        self.cutoffs.append(c)
+        arg, d, _ = self.o.nn1(self.qs, self.db[b0:b1])
+        arg = np.asarray(arg, dtype=np.int64)
+        d = np.asarray(d, dtype=np.float64)
+        out = d > c
+        arg[out] = 0
+        d[out] = np.inf
+        return arg, d
+
+
+def _nn1_worker(rank, world, port, qs, db, batches, out):
+    from paper_2010_05371_b200.sharded import ShardedNN1, db_shard_bounds
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        d0, d1 = db_shard_bounds(db.shape[0], world, rank)
+        shard = OracleNN1Shard(qs, db[d0:d1])
+        arg, d = ShardedNN1(shard, rank, world, d0, batches=batches).search()
+        out[rank] = (arg.tolist(), d.tolist(), [c.tolist() for c in shard.cutoffs])
+    finally:
+        dist.destroy_process_group()
+
+
+def test_db_shard_bounds():
+    from paper_2010_05371_b200.sharded import db_shard_bounds
+    for nd in (1, 7, 20000, 20001):
+        for world in (1, 2, 3, 8):
+            spans = [db_shard_bounds(nd, world, r) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == nd
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+
+
+@pytest.mark.timeout(300)
+def test_two_rank_nn1_equals_unsharded(oracle_lib):
+    """Database split over 2 ranks x 3 batches with the cutoff all-reduce:
+    per query the unsharded argmin and distance, ties to the lowest global
+    index (exact copies planted in both ranks' halves)."""
+    from paper_2010_05371_b200 import znormalize
+    rng = np.random.default_rng(77)
+    L, nq, nd = 32, 6, 60
+    qs = np.stack([znormalize(np.cumsum(rng.standard_normal(L))) for _ in range(nq)])
+    db = np.stack([znormalize(np.cumsum(rng.standard_normal(L))) for _ in range(nd)])
+    db[40] = qs[0]  # rank 1 holds rows 30..59: an exact copy there ...
+    db[12] = qs[0]  # ... and a lower-index one in rank 0
+    db[55] = qs[1]  # only in rank 1
+    want_arg, want_d, _ = oracle_lib.nn1(qs, db)
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_nn1_worker, args=(2, _free_port(), qs, db, 3, out), nprocs=2, join=True)
+    for rank in (0, 1):
+        arg, d, cutoffs = out[rank]
+        assert arg == [int(x) for x in want_arg]
+        assert d == [float(x) for x in want_d]
+        assert arg[0] == 12 and d[0] == 0.0 and arg[1] == 55
+        # the second batch already starts from the global best of the first
+        assert all(np.isinf(cutoffs[0]))
+        assert not np.isinf(cutoffs[1]).any()
+
+
+@pytest.mark.gpu
+def test_gpu_nn1_shard_batches_and_cutoffs(oracle_lib):
+    """eapdtw_nn1_dev_cutoff through GpuNN1Shard: 3 batches with the cutoff
+    carried (world 1) equal the oracle; a cutoff at the exact distance keeps
+    the match (ties kept); just below it finds nothing."""
+    from paper_2010_05371_b200 import Context, znormalize
+    from paper_2010_05371_b200.sharded import GpuNN1Shard, ShardedNN1
+    rng = np.random.default_rng(5)
+    L, nq, nd = 128, 40, 3000
+    qs = np.stack([znormalize(np.cumsum(rng.standard_normal(L))) for _ in range(nq)])
+    db = np.stack([znormalize(np.cumsum(rng.standard_normal(L))) for _ in range(nd)])
+    db[2500] = qs[3]
+    db[100] = qs[3]
+    want_arg, want_d, _ = oracle_lib.nn1(qs, db)
+    ctx = Context(0)
+    shard = GpuNN1Shard(torch.from_numpy(qs).cuda(), torch.from_numpy(db).cuda(), ctx=ctx)
+    arg, d = ShardedNN1(shard, 0, 1, 0, batches=3, device="cuda").search()
+    assert arg.tolist() == [int(x) for x in want_arg]
+    assert d.tolist() == [float(x) for x in want_d]
+    assert arg[3] == 100 and d[3] == 0.0
+    exact = torch.from_numpy(np.asarray(want_d)).cuda()
+    a2, d2 = shard.run(0, nd, exact)
+    assert a2.tolist() == [int(x) for x in want_arg] and d2.tolist() == d.tolist()
+    below = torch.from_numpy(np.nextafter(np.asarray(want_d), 0.0)).cuda()
+    a3, d3 = shard.run(0, nd, below)
+    assert np.isinf(d3[np.asarray(want_d) > 0]).all()
+    ctx.close()
