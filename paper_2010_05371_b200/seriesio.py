@@ -36,8 +36,6 @@ import numpy as np
 # it also accepts (rejected afterwards as "not finite").
 _NUMBER = re.compile(r"-?(?:\d+\.?\d*|\.\d+)(?:[eE][+-]?\d+)?")
 _NONFINITE = re.compile(r"-?(?:inf(?:inity)?|nan(?:\([0-9A-Za-z_]*\))?)", re.IGNORECASE)
-_DBL_MAX = 1.7976931348623157e308
-_DBL_TRUE_MIN = 5e-324
 
 
 class SeriesFileError(RuntimeError):

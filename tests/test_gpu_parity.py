@@ -504,3 +504,26 @@ def test_warm_start_never_changes_the_result(gpu, oracle_lib, monkeypatch, rank)
         assert (got.best.location, got.best.distance_sq) == (want.location, want.distance_sq)
         rep = got.report
         assert rep.candidates_total == n - m + 1
+
+
+FULL = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "full_size_golden.json")))
+
+
+@pytest.mark.parametrize("name", sorted(FULL))
+def test_baseline_configs_full_size_vs_reference(gpu, name):
+    """cfg2-cfg4 at their BASELINE sizes against the unmodified reference's
+    answer (tests/golden/full_size_golden.json, make_full_size_golden.py):
+    bit-exact location and distance through the host-pointer API (streamed
+    for cfg4) and through a device-resident series."""
+    c = FULL[name]
+    ref = gpu.random_walk_normal(c["n"], c["seed_ref"])
+    q = gpu.random_walk_normal(c["m"], c["seed_query"])
+    cfg = gpu.SearchConfig(window_ratio=c["ratio"], use_lower_bounds=c["use_lb"],
+                           tighten_ub=c["use_lb"])
+    want = (c["location"], fbits(c["distance_sq"]))
+    got = gpu.similarity_search(ref, q, cfg)
+    assert (got.best.location, got.best.distance_sq) == want
+    assert got.report.candidates_total == c["n"] - c["m"] + 1
+    with gpu.DeviceSeries(ref) as dref:
+        got2 = dref.search(q, cfg)
+    assert (got2.best.location, got2.best.distance_sq) == want
