@@ -718,6 +718,12 @@ def main():
                "sample": f"first {npoints} points ({ncs} candidates) of the same reference, "
                          f"{seg} shards of 100000 candidates on {cores} threads, {dt:.2f} s"}
 
+    ncu_summary = None  # issue-slot / FP64-pipe utilisation of the sweep from the committed ncu capture
+    try:
+        ncu_summary = json.load(open(os.path.join(ROOT, "profiles", "search_kernel_ncu.json"))).get(
+            args.config)
+    except Exception:
+        ncu_summary = None
     traffic = None
     prof = os.path.join(ROOT, "profiles", "search_kernel_traffic.json")
     if os.path.exists(prof):
@@ -747,7 +753,7 @@ def main():
                        "l2": "inputs larger than L2 (800 MB reference vs 126 MB L2)"
                        if n * 8 > 126e6 else "reference smaller than L2",
                        "batches_per_search": runner.batches},
-            "roofline": dict(roof, traffic=traffic),
+            "roofline": dict(roof, traffic=traffic, ncu=ncu_summary),
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "subsequences/s",
                     "h2d_bytes_per_step": npts * 8 + m * 8, "d2h_bytes_per_step": 88},
