@@ -131,7 +131,9 @@ int eapdtw_similarity_search_dev(eapdtw_ctx* ctx, const double* reference_dev, s
  * multi-query drivers.  The handle owns its HBM copy until series_free, and
  * caches the sliding statistics (mean, sd) of the last query length searched:
  * they depend on the reference and m only (search.cpp:156-168), so searches
- * that differ in window, algorithm or query content reuse them. */
+ * that differ in window, algorithm or query content reuse them.  The cache
+ * serves the first context that searches the series; other contexts (other
+ * host threads) may search it too, without the cache. */
 typedef struct eapdtw_series eapdtw_series;
 int eapdtw_series_upload(eapdtw_ctx* ctx, const double* host, size_t n, eapdtw_series** out);
 const double* eapdtw_series_device_ptr(const eapdtw_series* s);

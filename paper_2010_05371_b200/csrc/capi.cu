@@ -16,6 +16,7 @@
 #include <numeric>
 #include <random>
 #include <string>
+#include <mutex>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -1056,9 +1057,14 @@ int eapdtw_search_plan_destroy(eapdtw_search_plan* p) {
 // Cached sliding statistics of a device-resident series for one query length
 // (the chain depends on the reference and m only, search.cpp:156-168): the
 // grid's 5 window ratios per length share one stats pass.
+// The cache belongs to the first context that fills it: its copies are
+// ordered on that context's stream, so other contexts searching the same
+// series (other host threads) neither read nor refill it.
 struct SeriesStats {
   DevBuf mean, sd;
   size_t m = 0;  // 0: empty
+  const eapdtw_ctx* owner = nullptr;
+  std::mutex mu;
 };
 
 static int one_shot(eapdtw_ctx* c, const double* ref_dev, size_t n, const double* query,
@@ -1069,6 +1075,11 @@ static int one_shot(eapdtw_ctx* c, const double* ref_dev, size_t n, const double
   p.buf = &c->pb;  // reuse the context's grow-only scratch
   int e = plan_init(&p, c, ref_dev, n, query, qlen, cfg, 0);
   bool fill_cache = false;
+  if (cache) {
+    std::lock_guard<std::mutex> lock(cache->mu);
+    if (!cache->owner) cache->owner = c;
+    if (cache->owner != c) cache = nullptr;
+  }
   if (!e && cache) {
     const size_t bytes = p.ncand * 8;
     if (cache->m == p.m) {
