@@ -38,6 +38,9 @@ _NUMBER = re.compile(r"-?(?:\d+\.?\d*|\.\d+)(?:[eE][+-]?\d+)?")
 _NONFINITE = re.compile(r"-?(?:inf(?:inity)?|nan(?:\([0-9A-Za-z_]*\))?)", re.IGNORECASE)
 
 
+_CSPACE = re.compile(r"[ \t\n\v\f\r]+")
+
+
 class SeriesFileError(RuntimeError):
     """io.cpp's std::runtime_error for unreadable or malformed series files."""
 
@@ -197,7 +200,9 @@ def load_series(path) -> np.ndarray:
     except OSError:
         raise SeriesFileError(f"cannot open '{p}'") from None
     out = []
-    for index, tok in enumerate(text.split(), start=1):
+    # operator>> splits on the C locale's isspace set only (not on the
+    # latin-1 bytes Python's str.split() also treats as whitespace)
+    for index, tok in enumerate((t for t in _CSPACE.split(text) if t), start=1):
         v = _parse_token(tok)
         if v is None:
             raise SeriesFileError(f"'{p}': token {index} ('{tok}') is not a number")

@@ -101,3 +101,27 @@ def test_binary_validation(tmp_path):
         seriesio.load_series_binary(q)
     with pytest.raises(seriesio.SeriesFileError, match="cannot open"):
         seriesio.load_series_binary(tmp_path / "nope.f64")
+
+
+def test_load_series_splits_on_c_whitespace_only(tmp_path):
+    """operator>> (io.cpp:24) splits on " \\t\\n\\v\\f\\r" only: a NBSP (0xA0)
+    or 0x1C byte stays inside the token, which then is not a number."""
+    p = tmp_path / "s.txt"
+    p.write_bytes(b"1\x0b2\x0c3\r4")
+    assert seriesio.load_series(p).tolist() == [1.0, 2.0, 3.0, 4.0]
+    for sep in (b"\xa0", b"\x1c", b"\x85"):
+        p.write_bytes(b"1" + sep + b"2")
+        with pytest.raises(seriesio.SeriesFileError, match="token 1"):
+            seriesio.load_series(p)
+
+
+def test_module_entry_point_validation_exit_code(tmp_path):
+    """python -m paper_2010_05371_b200 is the CLI (exit 2 on a validation error)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(HERE)
+    r = subprocess.run([sys.executable, "-m", "paper_2010_05371_b200", "search", "--data", "x",
+                        "--query", "y", "--query-len", "8", "--window-ratio", "0.6",
+                        "--algo", "eap"], cwd=root, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 2
+    assert r.stderr.startswith("error: --window-ratio")
