@@ -244,6 +244,18 @@ def run_reference_arm(args, cfgname):
     return 0
 
 
+def committed_ncu(cfg):
+    """(DRAM bytes per launch, pipe/issue utilisation) of cfg's dominant kernel
+    from the committed ncu capture (profiles/summarize.py report ... cfg)."""
+    out = []
+    for name in ("search_kernel_traffic.json", "search_kernel_ncu.json"):
+        try:
+            out.append(json.load(open(os.path.join(ROOT, "profiles", name))).get(cfg))
+        except Exception:
+            out.append(None)
+    return tuple(out)
+
+
 def run_batch(args):
     """cfg1 (pairwise) and cfg5 (NN1) lines: pairs/s through the public batch API
     with host buffers, the device-resident kernel time from CUDA events."""
@@ -372,6 +384,7 @@ def run_batch(args):
     cells32 = ctx.last_cells_f32 if cfg != "cfg1" else 0
     roof = mixed_roofline(cells - cells32, cells32, ms * 1e-3, ctx.fp64_peak(), ctx.fp32_peak(),
                           "pairwise_kernel" if cfg == "cfg1" else "nn1_kernel")
+    roof["traffic"], roof["ncu"] = committed_ncu(cfg)
     line = {"metric": unit.replace("/s", " per second"), "value": value, "unit": unit,
             "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -718,19 +731,8 @@ def main():
                "sample": f"first {npoints} points ({ncs} candidates) of the same reference, "
                          f"{seg} shards of 100000 candidates on {cores} threads, {dt:.2f} s"}
 
-    ncu_summary = None  # issue-slot / FP64-pipe utilisation of the sweep from the committed ncu capture
-    try:
-        ncu_summary = json.load(open(os.path.join(ROOT, "profiles", "search_kernel_ncu.json"))).get(
-            args.config)
-    except Exception:
-        ncu_summary = None
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "search_kernel_traffic.json")
-    if os.path.exists(prof):
-        try:
-            traffic = json.load(open(prof)).get(args.config)
-        except Exception:
-            traffic = None
+    # DRAM traffic and issue-slot / pipe utilisation of the sweep (committed ncu capture)
+    traffic, ncu_summary = committed_ncu(args.config)
 
     if rank == 0:
         best = results[-1]

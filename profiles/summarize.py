@@ -32,6 +32,13 @@ KEYS = [
     "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio",
     "smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio",
     "smsp__average_warps_issue_stalled_not_selected_per_issue_active.ratio",
+    # per-pipe utilisation: the DTW engines' min3 / compare / select / integer
+    # work runs on the ALU pipe, the FP32 sub/mul/add on the FMA pipe
+    "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_alu.max.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
 ]
 
 
@@ -75,6 +82,22 @@ def report(src, out, cfg=None):
             return float(v.replace(",", "")) * scale
         traffic = to_bytes(*d["dram__bytes_read.sum"]) + to_bytes(*d["dram__bytes_write.sum"])
         path = os.path.join(HERE, "search_kernel_traffic.json")
+        pipes = os.path.join(HERE, "search_kernel_ncu.json")
+        cur_p = json.load(open(pipes)) if os.path.exists(pipes) else {}
+
+        def pct(k):
+            return float(d[k][0].replace(",", "")) if k in d else None
+        cur_p[cfg] = {
+            "source": f"profiles/{os.path.basename(out)} (ncu --set full of {d.get('Kernel Name', ('?',))[0]})",
+            "issue_slots_busy_pct": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+            "alu_pipe_pct": pct("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
+            "fma_pipe_pct": pct("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"),
+            "fp64_pipe_active_pct": pct("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+            "lsu_pipe_pct": pct("sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"),
+            "warps_active_pct": pct("sm__warps_active.avg.pct_of_peak_sustained_active"),
+            "dram_bytes": to_bytes(*d["dram__bytes_read.sum"]) + to_bytes(*d["dram__bytes_write.sum"]),
+        }
+        json.dump(cur_p, open(pipes, "w"), indent=1)
         cur = json.load(open(path)) if os.path.exists(path) else {}
         cur[cfg] = traffic
         json.dump(cur, open(path, "w"), indent=1)
