@@ -44,7 +44,7 @@ BATCH_CONFIGS = {
 }
 # the reference CLI's bench grid (eapdtw_cli.cpp:110-142)
 GRID = {"n": 1_000_000, "seed": 42, "lengths": (128, 256, 512, 1024),
-        "ratios": (0.1, 0.2, 0.3, 0.4, 0.5)}
+        "ratios": (0.1, 0.2, 0.3, 0.4, 0.5), "concurrency": 4}
 GRID_DESC = ("grid: the reference CLI's bench grid (eapdtw_cli.cpp:110-142) -- query lengths "
              "128/256/512/1024 x window ratios 0.1-0.5, EAPrunedDTW + LB cascade, 20 searches of "
              "a 1e6-point random_walk(seed 42) reference (the reference's uniform-step "
@@ -538,11 +538,11 @@ def run_grid(args):
 
     def grid_once(reference):
         return [r for _, _, _, r in g.search_grid(reference, q, GRID["lengths"], GRID["ratios"],
-                                                  ctx=ctx)]
+                                                  ctx=ctx, concurrency=GRID["concurrency"])]
     for _ in range(args.warmup):
         grid_once(dref)
     torch.cuda.synchronize()
-    launches0 = ctx.launches
+    launches0 = g.api.total_launches()  # the worker contexts' launches included
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(0) as clk:
         e0.record(stream)
@@ -551,7 +551,7 @@ def run_grid(args):
         e1.record(stream)
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
-    launches = ctx.launches - launches0
+    launches = g.api.total_launches() - launches0
     # e2e: search_grid on host memory (one pinned H2D of the reference per grid)
     pinned = torch.from_numpy(ref).pin_memory().numpy()
     e2e_t = []
@@ -578,6 +578,7 @@ def run_grid(args):
         "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic: the reference's seeded random_walk",
         "config": {"workload": GRID_DESC, "searches_per_step": len(results),
+                   "concurrency": f"{GRID['concurrency']} contexts (streams), one per query length",
                    "l2": "8 MB reference resident in HBM (fits L2; each search streams its "
                          "own stats/envelope buffers)"},
         "roofline": None, "cpu_baseline": cpu,

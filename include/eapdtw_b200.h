@@ -73,6 +73,8 @@ int eapdtw_ctx_set_stream(eapdtw_ctx* ctx, void* cuda_stream);
 int eapdtw_ctx_synchronize(eapdtw_ctx* ctx);
 /* Number of kernels this context has launched (gpu_launches accounting). */
 uint64_t eapdtw_ctx_launches(const eapdtw_ctx* ctx);
+/* Kernels launched by every context of this process so far. */
+uint64_t eapdtw_total_launches(void);
 /* Cells of the last eapdtw_nn1(_dev) call evaluated by the FP32 screening
  * engine (included in that call's *cells total). */
 uint64_t eapdtw_ctx_last_cells_f32(const eapdtw_ctx* ctx);
@@ -131,9 +133,9 @@ int eapdtw_similarity_search_dev(eapdtw_ctx* ctx, const double* reference_dev, s
  * multi-query drivers.  The handle owns its HBM copy until series_free, and
  * caches the sliding statistics (mean, sd) of the last query length searched:
  * they depend on the reference and m only (search.cpp:156-168), so searches
- * that differ in window, algorithm or query content reuse them.  The cache
- * serves the first context that searches the series; other contexts (other
- * host threads) may search it too, without the cache. */
+ * that differ in window, algorithm or query content reuse them.  Several
+ * contexts (one per host thread) may search one series concurrently; each
+ * keeps its own cache entry. */
 typedef struct eapdtw_series eapdtw_series;
 int eapdtw_series_upload(eapdtw_ctx* ctx, const double* host, size_t n, eapdtw_series** out);
 const double* eapdtw_series_device_ptr(const eapdtw_series* s);

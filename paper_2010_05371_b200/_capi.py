@@ -65,6 +65,7 @@ SIGNATURES = [
     ("eapdtw_ctx_set_stream", C.c_int, [_vp, _vp]),
     ("eapdtw_ctx_synchronize", C.c_int, [_vp]),
     ("eapdtw_ctx_launches", C.c_uint64, [_vp]),
+    ("eapdtw_total_launches", C.c_uint64, []),
     ("eapdtw_ctx_last_cells_f32", C.c_uint64, [_vp]),
     ("eapdtw_ea_pruned_dtw_windowed", C.c_int,
      [_vp, _dp, C.c_size_t, _dp, C.c_size_t, C.c_size_t, C.c_double, _dp, C.c_size_t, _dp,

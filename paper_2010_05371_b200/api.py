@@ -199,6 +199,11 @@ class Context:
         return int(lib.eapdtw_ctx_last_cells_f32(self.handle))
 
 
+def total_launches() -> int:
+    """Kernels launched by every context of this process (eapdtw_total_launches)."""
+    return int(lib.eapdtw_total_launches())
+
+
 _tls = threading.local()
 
 
@@ -413,13 +418,16 @@ class DeviceSeries:
     def device_ptr(self) -> int:
         return int(lib.eapdtw_series_device_ptr(self.handle))
 
-    def search(self, query, cfg: SearchConfig | None = None) -> SearchResult:
-        """similarity_search (search.hpp:118-119) against this reference."""
+    def search(self, query, cfg: SearchConfig | None = None, *, ctx=None) -> SearchResult:
+        """similarity_search (search.hpp:118-119) against this reference, on
+        ``ctx`` (default: the context that uploaded it; any context on the
+        same device may search it, one host thread per context)."""
         cfg = cfg or SearchConfig()
+        ctx = ctx or self.ctx
         q = query.view() if isinstance(query, Series) else Series(query).view()
         res = _capi.SearchResultC()
         c = cfg.to_c()
-        check(lib.eapdtw_similarity_search_series(self.ctx.handle, self.handle, _ptr(q), q.size,
+        check(lib.eapdtw_similarity_search_series(ctx.handle, self.handle, _ptr(q), q.size,
                                                   C.byref(c), C.byref(res)))
         return SearchResult.from_c(res)
 
@@ -441,23 +449,84 @@ class DeviceSeries:
             pass
 
 
+# Worker contexts of concurrent grids, kept between calls: a fresh context
+# allocates its scratch on first use (cudaMalloc/cudaFree synchronise the
+# device), which would cost more than the overlap gains.
+_pool_lock = threading.Lock()
+_pool: dict = {}
+
+
+def _pool_get(device: int) -> Context:
+    with _pool_lock:
+        free = _pool.setdefault(device, [])
+        if free:
+            return free.pop()
+    return Context(device)
+
+
+def _pool_put(ctx: Context) -> None:
+    with _pool_lock:
+        _pool.setdefault(ctx.device, []).append(ctx)
+
+
 def search_grid(reference, query, lengths, ratios, algos=(Algo.ea_pruned,), *,
-                use_lower_bounds: bool = True, tighten_ub: bool = True, ctx=None):
+                use_lower_bounds: bool = True, tighten_ub: bool = True, ctx=None,
+                concurrency: int = 1):
     """The reference CLI's bench grid (run_bench, eapdtw_cli.cpp:110-142):
     for each algorithm, query length (a prefix of ``query``) and window
     ratio, one similarity_search of the same reference.  The reference is
     uploaded to HBM once.  Yields ``(algo, length, ratio, SearchResult)`` in
-    the reference's loop order (algo, then length, then ratio)."""
+    the reference's loop order (algo, then length, then ratio).
+
+    ``concurrency`` > 1 runs the query lengths on that many contexts (CUDA
+    streams, one host thread each) against the same resident series: one
+    length's searches share their stats chain, and different lengths' latency-
+    bound phases overlap.  Results are identical; they are yielded once all
+    workers finish."""
     own = not isinstance(reference, DeviceSeries)
     ref = DeviceSeries(reference, ctx=ctx) if own else reference
+
+    def cfg_of(algo, length, ratio):
+        return SearchConfig(query_length=int(length), window_ratio=float(ratio),
+                            algorithm=Algo(algo), use_lower_bounds=use_lower_bounds,
+                            tighten_ub=tighten_ub and use_lower_bounds)
     try:
+        workers = max(1, min(int(concurrency), len(lengths)))
+        if workers == 1:
+            for algo in algos:
+                for length in lengths:
+                    for ratio in ratios:
+                        yield (Algo(algo), int(length), float(ratio),
+                               ref.search(query, cfg_of(algo, length, ratio)))
+            return
+        import threading
+        results, errors = {}, []
+
+        def work(my_lengths):
+            wctx = _pool_get(ref.ctx.device)
+            try:
+                for length in my_lengths:  # same m consecutively: stats cache hits
+                    for algo in algos:
+                        for ratio in ratios:
+                            results[(Algo(algo), int(length), float(ratio))] = ref.search(
+                                query, cfg_of(algo, length, ratio), ctx=wctx)
+            except Exception as e:  # noqa: BLE001 -- re-raised in the caller
+                errors.append(e)
+            finally:
+                _pool_put(wctx)
+        threads = [threading.Thread(target=work, args=(list(lengths)[w::workers],))
+                   for w in range(workers)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        if errors:
+            raise errors[0]
         for algo in algos:
             for length in lengths:
                 for ratio in ratios:
-                    cfg = SearchConfig(query_length=int(length), window_ratio=float(ratio),
-                                       algorithm=Algo(algo), use_lower_bounds=use_lower_bounds,
-                                       tighten_ub=tighten_ub and use_lower_bounds)
-                    yield Algo(algo), int(length), float(ratio), ref.search(query, cfg)
+                    key = (Algo(algo), int(length), float(ratio))
+                    yield key + (results[key],)
     finally:
         if own:
             ref.close()

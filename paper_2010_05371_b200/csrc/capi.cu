@@ -16,6 +16,9 @@
 #include <numeric>
 #include <random>
 #include <string>
+#include <atomic>
+#include <map>
+#include <memory>
 #include <mutex>
 #include <vector>
 
@@ -118,11 +121,29 @@ struct PlanBuffers {
   }
 };
 
+// Kernel launches of one context, also added to a process-wide total (the
+// concurrent grid's worker contexts are short-lived).
+static std::atomic<uint64_t> g_total_launches{0};
+struct LaunchCounter {
+  uint64_t n = 0;
+  LaunchCounter& operator++() {
+    ++n;
+    g_total_launches.fetch_add(1, std::memory_order_relaxed);
+    return *this;
+  }
+  LaunchCounter& operator+=(uint64_t k) {
+    n += k;
+    g_total_launches.fetch_add(k, std::memory_order_relaxed);
+    return *this;
+  }
+  operator uint64_t() const { return n; }
+};
+
 struct eapdtw_ctx {
   int device = 0;
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
-  uint64_t launches = 0;
+  LaunchCounter launches;
   uint64_t last_cells_f32 = 0;  // FP32-screen share of the last nn1 call's cells
   // scratch for pairwise / nn1 host-pointer variants
   DevBuf a, b, ub, cb, out, cells, best, keys, counters;
@@ -239,7 +260,9 @@ int eapdtw_ctx_synchronize(eapdtw_ctx* c) {
   return EAPDTW_OK;
 }
 
-uint64_t eapdtw_ctx_launches(const eapdtw_ctx* c) { return c ? c->launches : 0; }
+uint64_t eapdtw_ctx_launches(const eapdtw_ctx* c) { return c ? static_cast<uint64_t>(c->launches) : 0; }
+
+uint64_t eapdtw_total_launches(void) { return g_total_launches.load(); }
 
 // ---------------------------------------------------------------------------
 // Pairwise
@@ -1057,14 +1080,12 @@ int eapdtw_search_plan_destroy(eapdtw_search_plan* p) {
 // Cached sliding statistics of a device-resident series for one query length
 // (the chain depends on the reference and m only, search.cpp:156-168): the
 // grid's 5 window ratios per length share one stats pass.
-// The cache belongs to the first context that fills it: its copies are
-// ordered on that context's stream, so other contexts searching the same
-// series (other host threads) neither read nor refill it.
+// One cache per (series, context): a context's copies are ordered on its own
+// stream, so contexts on other host threads searching the same series each
+// keep their own entry.
 struct SeriesStats {
   DevBuf mean, sd;
   size_t m = 0;  // 0: empty
-  const eapdtw_ctx* owner = nullptr;
-  std::mutex mu;
 };
 
 static int one_shot(eapdtw_ctx* c, const double* ref_dev, size_t n, const double* query,
@@ -1075,11 +1096,6 @@ static int one_shot(eapdtw_ctx* c, const double* ref_dev, size_t n, const double
   p.buf = &c->pb;  // reuse the context's grow-only scratch
   int e = plan_init(&p, c, ref_dev, n, query, qlen, cfg, 0);
   bool fill_cache = false;
-  if (cache) {
-    std::lock_guard<std::mutex> lock(cache->mu);
-    if (!cache->owner) cache->owner = c;
-    if (cache->owner != c) cache = nullptr;
-  }
   if (!e && cache) {
     const size_t bytes = p.ncand * 8;
     if (cache->m == p.m) {
@@ -1137,7 +1153,8 @@ struct eapdtw_series {
   int device = 0;
   DevBuf data;
   size_t n = 0;
-  SeriesStats stats;  // the last query length's sliding statistics
+  std::mutex mu;  // guards the map, not the entries (one host thread per context)
+  std::map<const eapdtw_ctx*, std::unique_ptr<SeriesStats>> stats;  // last m's stats, per context
 };
 
 int eapdtw_series_upload(eapdtw_ctx* c, const double* host, size_t n, eapdtw_series** out) {
@@ -1181,8 +1198,10 @@ int eapdtw_series_free(eapdtw_series* s) {
   cudaSetDevice(s->device);
   cudaDeviceSynchronize();
   s->data.release();
-  s->stats.mean.release();
-  s->stats.sd.release();
+  for (auto& kv : s->stats) {
+    kv.second->mean.release();
+    kv.second->sd.release();
+  }
   delete s;
   return EAPDTW_OK;
 }
@@ -1194,8 +1213,14 @@ int eapdtw_similarity_search_series(eapdtw_ctx* c, eapdtw_series* ref, const dou
   if (ref->device != c->device) return fail(EAPDTW_EINVAL, "series lives on another device");
   if (getenv("EAPDTW_SERIES_STATS_CACHE") && atoi(getenv("EAPDTW_SERIES_STATS_CACHE")) == 0)
     return one_shot(c, ref->data.as<const double>(), ref->n, query, qlen, cfg, false, out);
-  return one_shot(c, ref->data.as<const double>(), ref->n, query, qlen, cfg, false, out,
-                  &ref->stats);
+  SeriesStats* cache = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(ref->mu);
+    auto& slot = ref->stats[c];
+    if (!slot) slot = std::make_unique<SeriesStats>();
+    cache = slot.get();
+  }
+  return one_shot(c, ref->data.as<const double>(), ref->n, query, qlen, cfg, false, out, cache);
 }
 
 // Host-pointer search of a long reference, streamed: the reference goes to the

@@ -13,12 +13,33 @@
 #include <climits>
 #include <algorithm>
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "dtw_ad.cuh"
 #include "screen.cuh"
 #include "kernels.cuh"
 
 namespace eapdtw_b200 {
+
+// Raise a kernel's dynamic shared-memory limit, never lower it: the attribute
+// is per function (and device), so with several contexts launching the same
+// kernel from different host threads a smaller request must not undercut a
+// concurrent larger launch.  Thread-safe; one real call per new maximum.
+static cudaError_t ensure_dyn_smem(const void* func, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> granted;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& cur = granted[{dev, func}];
+  if (bytes <= cur) return cudaSuccess;
+  e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+  if (e == cudaSuccess) cur = bytes;
+  return e;
+}
 
 // ---------------------------------------------------------------------------
 // Sliding z-normalisation statistics.
@@ -190,12 +211,9 @@ cudaError_t launch_stats(const double* ref, long long n, int m, double* mean, do
   if (seg_begin >= seg_end) return cudaSuccess;
   const long long blocks = (seg_end - seg_begin + kStatsChains - 1) / kStatsChains;
   const size_t smem = 4 * static_cast<size_t>(kStatsChains) * kStatsRow * sizeof(double2);
-  static bool configured = false;
-  if (!configured) {
-    const cudaError_t e = cudaFuncSetAttribute(
-        stats_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  {
+    const cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(stats_chain_kernel), smem);
     if (e != cudaSuccess) return e;
-    configured = true;
   }
   stats_chain_kernel<<<static_cast<unsigned>(blocks), 128, smem, stream>>>(ref, n, m, mean, sd,
                                                                            seg_begin, seg_end);
@@ -277,8 +295,7 @@ cudaError_t launch_envelope(const double* ref, long long n, int r, double* env,
   const int T = envelope_tile(r);
   if (T < 256) return cudaErrorInvalidValue;  // caller disables the EC tier
   const size_t smem = 2 * static_cast<size_t>(T + 2 * r) * sizeof(double);
-  cudaError_t e = cudaFuncSetAttribute(envelope_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
+  cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(envelope_kernel), smem);
   if (e != cudaSuccess) return e;
   const long long ntiles = (n + T - 1) / T;
   if (tile_end < 0 || tile_end > ntiles) tile_end = ntiles;
@@ -1421,8 +1438,7 @@ size_t search_scratch_doubles(int m, int blocks, int warps, int ad_k) {
 cudaError_t launch_search(const SearchParams& p, int blocks, int warps, cudaStream_t stream) {
   const size_t smem = search_smem_bytes(p.m, warps, p.ad_k);
   auto go = [&](auto kern) -> cudaError_t {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+    cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(kern), smem);
     if (e != cudaSuccess) return e;
     kern<<<blocks, warps * 32, smem, stream>>>(p);
     return cudaGetLastError();
@@ -1494,13 +1510,11 @@ cudaError_t launch_pairwise(const PairParams& p, cudaStream_t stream) {
   const int blocks = static_cast<int>(min(need, 148LL * 32));
   cudaError_t e;
   if (p.cb) {
-    e = cudaFuncSetAttribute(pairwise_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
+    e = ensure_dyn_smem(reinterpret_cast<const void*>(pairwise_kernel<true>), smem);
     if (e != cudaSuccess) return e;
     pairwise_kernel<true><<<blocks, warps * 32, smem, stream>>>(p);
   } else {
-    e = cudaFuncSetAttribute(pairwise_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
+    e = ensure_dyn_smem(reinterpret_cast<const void*>(pairwise_kernel<false>), smem);
     if (e != cudaSuccess) return e;
     pairwise_kernel<false><<<blocks, warps * 32, smem, stream>>>(p);
   }
@@ -1693,8 +1707,7 @@ cudaError_t launch_nn1(const Nn1Params& p, cudaStream_t stream) {
   const size_t smem = static_cast<size_t>(warps + 1) * padded_len(p.len, p.ad_k) * sizeof(double) +
                      padded_len(p.len, p.ad_k) * sizeof(float);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(nn1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
+  cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(nn1_kernel), smem);
   if (e != cudaSuccess) return e;
   const long long blocks = p.nq * p.splits;
   nn1_kernel<<<static_cast<unsigned>(blocks), warps * 32, smem, stream>>>(p);

@@ -275,3 +275,23 @@ def test_cli_trace(files):
     assert lp.read_text().splitlines()[-1].startswith("5,")
     assert run(["trace", "--a", files / "S.txt", "--b", files / "T.txt", "--ub", "-1",
                 "--algo", "eap", "--out", lp])[0] == 2
+
+
+@pytest.mark.gpu
+def test_concurrent_grid_equals_serial_and_oracle(oracle_lib):
+    """search_grid(concurrency=3): query lengths on 3 contexts / host threads
+    against one resident series (per-context stats caches, thread-safe kernel
+    attributes) gives the serial grid's and the oracle's results."""
+    import paper_2010_05371_b200 as g
+    ref = random_walk(150_000, 3)
+    q = random_walk(160, 4)
+    lengths, ratios = (64, 96, 128, 160), (0.1, 0.3)
+    algos = (g.Algo.ea_pruned, g.Algo.full)
+    with g.DeviceSeries(ref) as dref:
+        serial = list(g.search_grid(dref, q, lengths, ratios, algos))
+        conc = list(g.search_grid(dref, q, lengths, ratios, algos, concurrency=3))
+    assert [k[:3] for k in serial] == [k[:3] for k in conc]
+    for (algo, length, ratio, a), (_, _, _, b) in zip(serial, conc):
+        want = oracle_lib.similarity_search(ref, q, ratio, length, int(algo))
+        assert (a.best.location, a.best.distance_sq) == (want.location, want.distance_sq)
+        assert (b.best.location, b.best.distance_sq) == (want.location, want.distance_sq)
