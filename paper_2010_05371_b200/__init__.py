@@ -32,6 +32,7 @@ from .api import (  # noqa: F401
     similarity_search,
     similarity_search_dev,
     search_grid,
+    search_many,
     trace,
     window_cells_for,
     znormalize,

@@ -532,6 +532,50 @@ def search_grid(reference, query, lengths, ratios, algos=(Algo.ea_pruned,), *,
             ref.close()
 
 
+def search_many(reference, queries, cfg: SearchConfig | None = None, *, ctx=None,
+                concurrency: int = 4) -> list:
+    """similarity_search of every query in ``queries`` against one reference
+    uploaded to HBM once; returns the SearchResults in input order.  Queries
+    are spread over ``concurrency`` pooled contexts (streams / host threads);
+    each context caches the sliding stats of its last query length, so
+    queries of equal length after a worker's first reuse them."""
+    cfg = cfg or SearchConfig()
+    queries = list(queries)
+    own = not isinstance(reference, DeviceSeries)
+    ref = DeviceSeries(reference, ctx=ctx) if own else reference
+    try:
+        workers = max(1, min(int(concurrency), len(queries)))
+        if workers == 1:
+            return [ref.search(q, cfg) for q in queries]
+        import threading
+        out, errors = [None] * len(queries), []
+
+        def work(idx):
+            wctx = _pool_get(ref.ctx.device)
+            try:
+                for k in idx:
+                    out[k] = ref.search(queries[k], cfg, ctx=wctx)
+            except Exception as e:  # noqa: BLE001 -- re-raised in the caller
+                errors.append(e)
+            finally:
+                _pool_put(wctx)
+        # equal lengths stay together within a worker (stats cache hits)
+        order = sorted(range(len(queries)),
+                       key=lambda k: len(queries[k]) if cfg.query_length == 0 else 0)
+        threads = [threading.Thread(target=work, args=(order[w::workers],))
+                   for w in range(workers)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        if errors:
+            raise errors[0]
+        return out
+    finally:
+        if own:
+            ref.close()
+
+
 class SearchPlan:
     """One shard of a (possibly multi-GPU) search: stepped C-ABI plan."""
 

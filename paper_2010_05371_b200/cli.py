@@ -13,7 +13,7 @@ Differences from the reference, all additive: ``--data``/``--query`` also
 accept binary series (``.f64``/``.bin`` raw little-endian float64, ``.npy``)
 so 1e8-point references need not be parsed as text; ``--device`` picks the
 GPU; ``bench`` uploads its reference to HBM once for the whole grid
-(``search_grid``); ``trace`` captures the cells on the device
+(``search_grid``) and ``--concurrency N`` searches N query lengths at once; ``trace`` captures the cells on the device
 (``eapdtw_trace``) and writes the reference's CSV.  Exit status: 0 ok,
 2 for the reference's CLI::ValidationError cases (bad --algo, ratio off the
 grid, argument errors), 1 for every other error (eapdtw_cli.cpp:232-238).
@@ -152,7 +152,7 @@ def run_bench(a, out) -> int:
             names = {algo: name for name, algo in algos}
             for algo, length, ratio, res in search_grid(ref, query, a.grid_lengths,
                                                         a.grid_ratios, [x for _, x in algos],
-                                                        ctx=ctx):
+                                                        ctx=ctx, concurrency=a.concurrency):
                 name = names[algo]
                 seriesio.emit_stats(res.report, res.best,
                                     os.path.join(a.stats_dir, stats_file_name(name, length, ratio)))
@@ -224,6 +224,9 @@ def make_parser() -> argparse.ArgumentParser:
                    help="synthetic random-walk reference length")
     b.add_argument("--seed", type=_nonneg_int, default=42, help="random-walk seed")
     b.add_argument("--device", type=int, default=0, help="CUDA device")
+    b.add_argument("--concurrency", type=int, default=1,
+                   help="query lengths searched concurrently (contexts / streams); results "
+                        "are identical, lines are printed once the grid completes")
     return p
 
 

@@ -161,7 +161,7 @@ def test_bench_grid_matches_oracle(tmp_path, oracle_lib):
     d = tmp_path / "bench"
     rc, out = run(["bench", "--grid-lengths", "64,128", "--grid-ratios", "0.1,0.2,0.5",
                    "--algos", "full,lp,eap", "--stats-dir", d, "--synthetic", 20000,
-                   "--seed", 9])
+                   "--seed", 9, "--concurrency", 2])
     assert rc == 0, out
     lines = out.strip().splitlines()
     assert len(lines) == 3 * 2 * 3
@@ -295,3 +295,19 @@ def test_concurrent_grid_equals_serial_and_oracle(oracle_lib):
         want = oracle_lib.similarity_search(ref, q, ratio, length, int(algo))
         assert (a.best.location, a.best.distance_sq) == (want.location, want.distance_sq)
         assert (b.best.location, b.best.distance_sq) == (want.location, want.distance_sq)
+
+
+@pytest.mark.gpu
+def test_search_many_equals_oracle(oracle_lib):
+    """search_many: 7 queries (two lengths) over 3 pooled contexts against one
+    resident series, each equal to the oracle's search."""
+    import paper_2010_05371_b200 as g
+    ref = g.random_walk_normal(250_000, 41)
+    qs = [g.random_walk_normal(128 if k % 2 else 200, 50 + k) for k in range(7)]
+    ref[1000:1128] = qs[1]  # one exact copy
+    cfg = g.SearchConfig(window_ratio=0.1)
+    got = g.search_many(ref, qs, cfg, concurrency=3)
+    for q, r in zip(qs, got):
+        want = oracle_lib.similarity_search(ref, q, 0.1)
+        assert (r.best.location, r.best.distance_sq) == (want.location, want.distance_sq)
+    assert got[1].best.location == 1000 and got[1].best.distance_sq < 1e-12
