@@ -579,6 +579,9 @@ def run_grid(args):
         "dtype": "f64", "data": "synthetic: the reference's seeded random_walk",
         "config": {"workload": GRID_DESC, "searches_per_step": len(results),
                    "concurrency": f"{GRID['concurrency']} contexts (streams), one per query length",
+                   "timing": "CUDA events on the caller's stream around the grid; every search "
+                             "returns synchronously (its worker stream drained), so the span "
+                             "covers all worker streams",
                    "l2": "8 MB reference resident in HBM (fits L2; each search streams its "
                          "own stats/envelope buffers)"},
         "roofline": None, "cpu_baseline": cpu,
