@@ -1367,11 +1367,16 @@ static int nn1_impl(eapdtw_ctx* c, const double* q_dev, size_t nq, const double*
   p.nd = static_cast<long long>(nd);
   p.len = static_cast<int>(len);
   p.w = w;
-  // Enough blocks to fill the GPU a few times over, but keep each query's
-  // database sweep wide enough to share a cutoff.
-  const long long target = 148LL * 8;
+  // Many small blocks: a block's cost varies with its query, so with few
+  // waves the last one leaves SMs idle (ncu: ALU-pipe use 58-95% across SMs
+  // at 2 splits).  cfg5 (1000 queries) sweep of splits per query: 2 -> 187.8
+  // ms, 4 -> 159.9, 6 -> 148.2, 10 -> 145.3, 16 -> 152.1 (the extra splits
+  // re-warm more cutoffs; scratch/nn1_splits.sh).  ~64 blocks per SM, each
+  // block keeping at least 64 database rows.
+  const long long target = 148LL * 64;
   p.splits = static_cast<int>(std::max<long long>(1, std::min<long long>(
       static_cast<long long>(nd) / 64 + 1, (target + static_cast<long long>(nq) - 1) / static_cast<long long>(nq))));
+  if (const char* env = getenv("EAPDTW_NN1_SPLITS")) p.splits = std::max(1, atoi(env));  // experiment
   p.ad_k = choose_ad_k(static_cast<int>(len), w);
   p.ub_keys = c->keys.as<unsigned long long>();
   p.best = c->best.as<BestRecord>();
