@@ -180,14 +180,18 @@ __device__ float warp_dtw_f32(const RawFn& rowraw, const NormFn& rownorm, int lr
       const unsigned before = finmask;
       bool alld = true;
 #if EAPDTW_F32_FASTRANGE
-      if (__all_sync(kFull, !active || (jr >= 0 && jr + 3 <= static_cast<int>(span)))) {
+      if (!banded || __all_sync(kFull, !active || (jr >= 0 && jr + 3 <= static_cast<int>(span)))) {
+#else
+      // Unbounded band: the band is the whole row, and the +inf padding of
+      // qsp (dtw_warp.cuh) already makes every out-of-range column cost +inf,
+      // so the per-step band test (3 ALU-pipe ops per cell) is dropped.
+      if (!banded) {
+#endif
         step(std::false_type{}, 0, alld);
         step(std::false_type{}, 1, alld);
         step(std::false_type{}, 2, alld);
         step(std::false_type{}, 3, alld);
-      } else
-#endif
-      {
+      } else {
         step(std::true_type{}, 0, alld);
         step(std::true_type{}, 1, alld);
         step(std::true_type{}, 2, alld);
