@@ -95,7 +95,15 @@ constexpr int kF32Undecided = 1;  // a row value exceeded cmax: run the FP64 eng
 //   qsp        : padded float column series (kPadL / kPadR of +inf)
 //   rowthr(u, i, i0): float threshold of row i given the strip's ub (double)
 //   rowbuf     : padded per-warp float scratch
-template <class RawFn, class NormFn, class UbFn, class RowThrFn>
+// BLK: wavefront steps per block of finish bookkeeping (ballots, finish
+// masks, loop counters).  8 in the search and in NN1 (measured against 4:
+// cfg4 -2%, cfg3-nolb -3%, cfg5 -9%, NN1 being ALU-pipe bound; 16: cfg5 +1%):
+// the per-block work is amortised over twice the cells at the cost of up to 4
+// more steps at a strip's end.
+// UNB: also instantiate the unbounded-band path without the per-step band
+// test (NN1); the search kernel keeps one copy of the step loop (i-cache:
+// the second copy cost the cfg4 sweep ~4 ms).
+template <int BLK = 4, bool UNB = false, class RawFn, class NormFn, class UbFn, class RowThrFn>
 __device__ float warp_dtw_f32(const RawFn& rowraw, const NormFn& rownorm, int lr,
                               const float* __restrict__ qsp, int lc, int w, float cmax,
                               UbFn&& get_ub, RowThrFn&& rowthr, float* __restrict__ rowbuf,
@@ -185,40 +193,34 @@ __device__ float warp_dtw_f32(const RawFn& rowraw, const NormFn& rownorm, int lr
       // Unbounded band: the band is the whole row, and the +inf padding of
       // qsp (dtw_warp.cuh) already makes every out-of-range column cost +inf,
       // so the per-step band test (3 ALU-pipe ops per cell) is dropped.
-      if (!banded) {
+      if (UNB && !banded) {
 #endif
-        step(std::false_type{}, 0, alld);
-        step(std::false_type{}, 1, alld);
-        step(std::false_type{}, 2, alld);
-        step(std::false_type{}, 3, alld);
+#pragma unroll
+        for (int u = 0; u < BLK; ++u) step(std::false_type{}, u, alld);
       } else {
-        step(std::true_type{}, 0, alld);
-        step(std::true_type{}, 1, alld);
-        step(std::true_type{}, 2, alld);
-        step(std::true_type{}, 3, alld);
+#pragma unroll
+        for (int u = 0; u < BLK; ++u) step(std::true_type{}, u, alld);
       }
       // Finished lanes, once per block (conservative): lane L is finished
-      // after step u if it was dead in all 4 steps and lane L-1 (lane 0: the
-      // row buffer, dead beyond column hi) was finished after step u-1.  Four
-      // chained updates, one per step, with the block's all-dead mask D.
+      // after step u if it was dead in all BLK steps and lane L-1 (lane 0:
+      // the row buffer, dead beyond column hi) was finished after step u-1.
+      // BLK chained updates, one per step, with the block's all-dead mask D.
       const unsigned D = __ballot_sync(kFull, alld);
-      finmask |= D & ((finmask << 1) | (j0 > hi ? 1u : 0u));
-      finmask |= D & ((finmask << 1) | (j0 + 1 > hi ? 1u : 0u));
-      finmask |= D & ((finmask << 1) | (j0 + 2 > hi ? 1u : 0u));
-      finmask |= D & ((finmask << 1) | (j0 + 3 > hi ? 1u : 0u));
-      finmask |= __ballot_sync(kFull, jr + 3 > static_cast<int>(span));
-      if (((finmask & ~before) >> lane) & 1u) jf = j + 3;
+#pragma unroll
+      for (int u = 0; u < BLK; ++u) finmask |= D & ((finmask << 1) | (j0 + u > hi ? 1u : 0u));
+      finmask |= __ballot_sync(kFull, jr + (BLK - 1) > static_cast<int>(span));
+      if (((finmask & ~before) >> lane) & 1u) jf = j + (BLK - 1);
 #ifdef EAPDTW_PHASE_CLOCKS
-      dbg_steps += 4;
+      dbg_steps += BLK;
 #endif
       if (finmask == kFull) break;
-      j += 4;
-      jr += 4;
-      j0 += 4;
-      qp += 4;
-      rp += 4;
+      j += BLK;
+      jr += BLK;
+      j0 += BLK;
+      qp += BLK;
+      rp += BLK;
     }
-    const int wend = jb - wl + (j - (jb - lane)) + 3;
+    const int wend = jb - wl + (j - (jb - lane)) + (BLK - 1);
     for (int k = max(wend + 1, 0) + lane; k <= written; k += 32) rowbuf[k] = INF;
     written = min(max(wend, 0), lc + 1);
     const int c0 = max(jb, bl), c1 = min(jf, bh);

@@ -27,6 +27,15 @@ namespace eapdtw_b200 {
 // is per function (and device), so with several contexts launching the same
 // kernel from different host threads a smaller request must not undercut a
 // concurrent larger launch.  Thread-safe; one real call per new maximum.
+#ifndef EAPDTW_NN1_STEP_BLOCK
+#define EAPDTW_NN1_STEP_BLOCK 8  // FP32 engine steps per finish-bookkeeping block in NN1 (dtw_f32.cuh)
+#endif
+constexpr int kNn1StepBlock = EAPDTW_NN1_STEP_BLOCK;
+#ifndef EAPDTW_SEARCH_STEP_BLOCK
+#define EAPDTW_SEARCH_STEP_BLOCK 8  // the same in the search kernel (4 -> 8: cfg4 -2%, cfg3-nolb -3%)
+#endif
+constexpr int kSearchStepBlock = EAPDTW_SEARCH_STEP_BLOCK;
+
 static cudaError_t ensure_dyn_smem(const void* func, size_t bytes) {
   static std::mutex mu;
   static std::map<std::pair<int, const void*>, size_t> granted;
@@ -720,7 +729,7 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
       const float r32 = warp_dtw2_f32(rowraw, rownorm32, m, qsp32, m, p.w, p.f32_cmax, get_ub,
                                       rowthr32, rowbuf32, c_cells32, st);
 #else
-      const float r32 = warp_dtw_f32(rowraw, rownorm32, m, qsp32, m, p.w, p.f32_cmax, get_ub,
+      const float r32 = warp_dtw_f32<kSearchStepBlock>(rowraw, rownorm32, m, qsp32, m, p.w, p.f32_cmax, get_ub,
                                      rowthr32, rowbuf32, c_cells32, st);
 #endif
       screened = st == 0 && r32 == f_inf();
@@ -1680,7 +1689,7 @@ __global__ void __launch_bounds__(256, EAPDTW_NN1_MINB) nn1_kernel(Nn1Params p) 
       auto rownorm32 = [](double x) -> float { return __double2float_rn(x); };
       auto rowthr32 = [&](double u, int, int) -> float { return f32_threshold(u, g); };
       int st = 0;
-      const float r32 = warp_dtw_f32(rowraw, rownorm32, L, qsp32, L, p.w, p.f32_cmax, get_ub,
+      const float r32 = warp_dtw_f32<kNn1StepBlock, true>(rowraw, rownorm32, L, qsp32, L, p.w, p.f32_cmax, get_ub,
                                      rowthr32, rowbuf32, cells32, st);
       screened = st == 0 && r32 == f_inf();
       __syncwarp();
