@@ -1562,7 +1562,7 @@ __device__ double kim_layers_raw(const double* __restrict__ rw, int L, const dou
 }
 
 #ifndef EAPDTW_NN1_MINB
-#define EAPDTW_NN1_MINB 3
+#define EAPDTW_NN1_MINB 4  // 4 blocks/SM (64 registers, spills off the step loop): cfg5 -2% vs 3, 2: +17%
 #endif
 __global__ void __launch_bounds__(256, EAPDTW_NN1_MINB) nn1_kernel(Nn1Params p) {
   extern __shared__ double smem[];
