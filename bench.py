@@ -187,58 +187,118 @@ def make_inputs(n: int, m: int):
     return ref, q
 
 
-def cpu_reference_search(ref, q, m, ratio, use_lb, threads, npoints):
-    """Time the UNMODIFIED reference (oracle/_ref) on a bounded sample."""
-    import oracle
-    sample = ref[:npoints]
-    if oracle.Reference.available():
-        lib = oracle.Reference()
-        t0 = time.perf_counter()
-        res = lib.similarity_search_threads(sample, q, ratio, threads, query_length=m,
-                                            use_lb=use_lb, tighten=use_lb)
-        dt = time.perf_counter() - t0
-        return res, dt, "reference", threads
-    lib = oracle.Oracle()  # the C restatement, single thread
+def search_config(cfgname: str, world: int, batches: int) -> dict:
+    """The bench line's ``config`` for a search workload -- the SAME dict on
+    both arms (ours and --impl reference), so the driver compares like with
+    like."""
+    n, m, ratio, desc = CONFIGS[cfgname]
+    return {"workload": desc, "n": n, "m": m,
+            "window_cells": int(np.floor(ratio * m)), "window_ratio": ratio,
+            "parallelism": f"shards{world}",
+            "l2": "inputs larger than L2 (800 MB reference vs 126 MB L2)"
+            if n * 8 > 126e6 else "reference smaller than L2",
+            "batches_per_search": batches if world > 1 else 1}
+
+
+# The reference's similarity_search is sequential (SPEC.md:359-360); the CPU
+# arm shards candidate starts at multiples of 100000 (the stats reset
+# interval, search.cpp:16), one unmodified similarity_search per host thread,
+# merged by (distance, lowest index) -- bit-identical to the unsharded search
+# (SURVEY Appendix C).  Each shard starts from ub = +inf like any call of the
+# reference's API, so shards are 1e6 candidates long (10 reset segments): long
+# enough for the reference's best-so-far to converge as it does in the full
+# run (calibration against a full-size run: DESIGN.md section 6).
+REF_SHARD = 1_000_000
+
+
+def reference_shards(ncand: int, threads: int, step: int):
+    """Candidate ranges [s0, s1) of one timed step: `threads` shards of
+    REF_SHARD candidates, rotating through the whole reference step by step
+    (so the K timed steps sample K x threads different stretches).  Small
+    configurations (ncand <= threads x REF_SHARD) run whole, split into
+    100000-aligned shards."""
+    if ncand <= threads * REF_SHARD:
+        per = max(100_000, -(-ncand // threads // 100_000) * 100_000)
+        return [(s, min(ncand, s + per)) for s in range(0, ncand, per)]
+    nsh = ncand // REF_SHARD  # whole shards only
+    return [((step * threads + j) % nsh * REF_SHARD, (step * threads + j) % nsh * REF_SHARD
+             + REF_SHARD) for j in range(threads)]
+
+
+def reference_step(lib, ref, q, m, ratio, use_lb, shards, threads):
+    """Run the unmodified reference over `shards` on `threads` host threads
+    (ctypes releases the GIL); returns (seconds, candidates, best)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    def one(sh):
+        s0, s1 = sh
+        r = lib.similarity_search_threads(ref[s0:s1 + m - 1], q, ratio, 1, query_length=m,
+                                          use_lb=use_lb, tighten=use_lb)
+        return (float(r.distance_sq), int(r.location) + s0) if r.found else None
     t0 = time.perf_counter()
-    res = lib.similarity_search(sample, q, ratio, query_length=m, use_lb=use_lb, tighten=use_lb)
-    return res, time.perf_counter() - t0, "port", 1
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        res = [r for r in ex.map(one, shards) if r is not None]
+    dt = time.perf_counter() - t0
+    return dt, sum(s1 - s0 for s0, s1 in shards), min(res) if res else None
+
+
+def reference_inputs(n: int, m: int):
+    """The bench inputs generated by the oracle's copy of the generator (the
+    reference arm must not load the product library)."""
+    import oracle
+    o = oracle.Oracle()
+    return o.random_walk_normal(n, SEED_REF), o.random_walk_normal(m, SEED_QUERY)
 
 
 def run_reference_arm(args, cfgname):
+    """--impl reference: the unmodified reference (oracle/_ref, compiled from
+    /root/reference by oracle/Makefile) on the host cores, same workload,
+    metric and config as our arm."""
+    import oracle
     n, m, ratio, desc = CONFIGS[cfgname]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     use_lb = cfgname != "cfg3-nolb"
     threads = os.cpu_count() or 1
-    # each step is a bounded sample: whole 100000-candidate segments, one per thread
-    nseg = max(1, min(threads, int(os.environ.get("EAPDTW_REF_SEGMENTS", "32"))))
-    npoints = min(n, nseg * 100_000 + m - 1)
-    from paper_2010_05371_b200 import random_walk_normal
-    ref = random_walk_normal(npoints, SEED_REF)  # prefix of the same walk
-    q = random_walk_normal(m, SEED_QUERY)
-    times = []
-    res = None
-    for k in range(args.warmup + args.steps):
-        res, dt, kind, cores = cpu_reference_search(ref, q, m, ratio, use_lb, nseg, npoints)
-        if k >= args.warmup:
-            times.append(dt)
-    ncs = npoints - m + 1
-    mean_t = sum(times) / len(times)
-    value = ncs / mean_t
+    lib = oracle.Reference()
+    ref, q = reference_inputs(n, m)
+    ncand = n - m + 1
+    # warm-up steps are untimed: one 100000-candidate shard per thread
+    warm = [(s, min(ncand, s + 100_000)) for s in range(0, min(ncand, threads * 100_000), 100_000)]
+    for _ in range(args.warmup):
+        reference_step(lib, ref, q, m, ratio, use_lb, warm, threads)
+    times, cands, best = [], 0, None
+    for k in range(args.steps):
+        shards = reference_shards(ncand, threads, k)
+        dt, c, b = reference_step(lib, ref, q, m, ratio, use_lb, shards, threads)
+        times.append(dt)
+        cands += c
+        best = b if best is None or (b is not None and b < best) else best
+    value = cands / sum(times)
+    shards0 = reference_shards(ncand, threads, 0)
+    whole = sum(s1 - s0 for s0, s1 in shards0) == ncand
+    sample = ("the whole search per step" if whole else
+              f"{len(shards0)} shards of {REF_SHARD} candidates per step, rotating through the "
+              f"reference ({args.steps} steps: {cands} of {ncand} candidates)")
     line = {
         "impl": "reference", "metric": "subsequences searched/sec", "value": value,
         "unit": "subsequences/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": mean_t * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic: seeded N(0,1) random walks (no public dataset)",
-        "config": {"workload": desc, "n": n, "m": m, "window_ratio": ratio},
-        "cpu_baseline": {"value": value, "unit": "subsequences/s", "cores": cores, "kind": kind,
-                         "sample": f"first {npoints} points ({ncs} candidates) of the cfg "
-                                   f"reference per step, sharded at 100000-candidate segments"},
+        "warmup": args.warmup, "ms_per_step": statistics.mean(times) * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: seeded N(0,1) random walks (mt19937_64 + Box-Muller), "
+                "no public dataset",
+        "config": search_config(cfgname, world, args.batches),
+        "cpu_baseline": {"value": value, "unit": "subsequences/s", "cores": threads,
+                         "kind": "reference",
+                         "sample": sample + "; unmodified similarity_search per shard on "
+                                   f"{threads} host threads, shards 100000-aligned; "
+                                   "warm-up steps: one 100000-candidate shard per thread"},
         "e2e": {"value": value, "unit": "subsequences/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
-        "result": {"location": int(res.location), "distance_sq": float(res.distance_sq)},
+        "result_over_sample": None if best is None else {"location": best[1],
+                                                         "distance_sq": best[0]},
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -259,10 +319,6 @@ def committed_ncu(cfg):
 def run_batch(args):
     """cfg1 (pairwise) and cfg5 (NN1) lines: pairs/s through the public batch API
     with host buffers, the device-resident kernel time from CUDA events."""
-    import torch
-
-    import paper_2010_05371_b200 as g
-    from paper_2010_05371_b200 import _capi
     import ctypes as C
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -270,17 +326,28 @@ def run_batch(args):
     sharded = cfg == "cfg5" and (world > 1 or args.shard_nn1) and args.impl != "reference"
     if rank != 0 and not sharded:
         return 0  # cfg1 (and the reference arm) run on rank 0; cfg5 shards its database
+    if args.impl == "reference":
+        # the reference arm never loads the product library: the reference's
+        # own znormalize and the oracle's copy of the generator
+        import oracle
+        zn, rwn = oracle.Reference().znormalize, oracle.Oracle().random_walk_normal
+    else:
+        import torch
+
+        import paper_2010_05371_b200 as g
+        from paper_2010_05371_b200 import _capi
+        zn, rwn = g.znormalize, g.random_walk_normal
     if cfg == "cfg1":
         npairs, L, w = 1024, 256, 25
-        a = np.stack([g.znormalize(g.random_walk_normal(L, 1000 + p)) for p in range(npairs)])
-        b = np.stack([g.znormalize(g.random_walk_normal(L, 500000 + p)) for p in range(npairs)])
+        a = np.stack([zn(rwn(L, 1000 + p)) for p in range(npairs)])
+        b = np.stack([zn(rwn(L, 500000 + p)) for p in range(npairs)])
         units = npairs
         unit = "pairs/s"
     else:
         nq, nd, L = 1000, 20000, 512
         rng = np.random.default_rng(SEED_REF)
-        qs = np.stack([g.znormalize(np.cumsum(rng.standard_normal(L))) for _ in range(nq)])
-        db = np.stack([g.znormalize(np.cumsum(rng.standard_normal(L))) for _ in range(nd)])
+        qs = np.stack([zn(np.cumsum(rng.standard_normal(L))) for _ in range(nq)])
+        db = np.stack([zn(np.cumsum(rng.standard_normal(L))) for _ in range(nd)])
         units = nq * nd
         unit = "query-series pairs/s"
     if sharded:
@@ -498,15 +565,19 @@ def run_grid(args):
     """The paper's / reference CLI's query-length x window-ratio grid on one
     device-resident reference (DeviceSeries): subsequences searched per second
     summed over the 20 searches."""
-    import torch
-
-    import paper_2010_05371_b200 as g
     import oracle
     if int(os.environ.get("RANK", "0")) != 0:
         return 0
     n = GRID["n"]
-    ref = g.random_walk(n, GRID["seed"])
-    q = g.random_walk(max(GRID["lengths"]), GRID["seed"] + 1)
+    if args.impl == "reference":  # the reference's own random_walk (io.cpp:124-137)
+        ref = oracle.Reference().random_walk(n, GRID["seed"])
+        q = oracle.Reference().random_walk(max(GRID["lengths"]), GRID["seed"] + 1)
+    else:
+        import torch
+
+        import paper_2010_05371_b200 as g
+        ref = g.random_walk(n, GRID["seed"])
+        q = g.random_walk(max(GRID["lengths"]), GRID["seed"] + 1)
     units = sum(n - L + 1 for L in GRID["lengths"]) * len(GRID["ratios"])
     threads = os.cpu_count() or 1
     sample = 100_000
@@ -608,8 +679,6 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--shard-nn1", action="store_true",
                     help="cfg5: the sharded driver (batches + cutoff all-reduce) even at N=1")
-    ap.add_argument("--cpu-segments", type=int, default=20,
-                    help="cpu_baseline sample: this many 100000-candidate segments")
     args = ap.parse_args()
     if args.config == "grid":
         return run_grid(args)
@@ -703,7 +772,7 @@ def main():
     # ---- e2e: the public API with host buffers (pinned), H2D + search + D2H every step
     pinned = torch.from_numpy(ref[s0:s0 + npts]).pin_memory()
     e2e_times = []
-    for it in range(max(2, min(args.steps, 3)) + 1):
+    for it in range(args.steps + 1):
         barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -726,14 +795,15 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        seg = min(args.cpu_segments, (ncand + 99_999) // 100_000)
-        npoints = min(n, seg * 100_000 + m - 1)
-        threads = min(os.cpu_count() or 1, seg)
-        r_cpu, dt, kind, cores = cpu_reference_search(ref, q, m, ratio, use_lb, threads, npoints)
-        ncs = npoints - m + 1
-        cpu = {"value": ncs / dt, "unit": "subsequences/s", "cores": cores, "kind": kind,
-               "sample": f"first {npoints} points ({ncs} candidates) of the same reference, "
-                         f"{seg} shards of 100000 candidates on {cores} threads, {dt:.2f} s"}
+        # one step of the reference arm's sample (oracle/_ref on the host cores)
+        import oracle
+        threads = os.cpu_count() or 1
+        shards = reference_shards(ncand, threads, 0)
+        dt, c, _ = reference_step(oracle.Reference(), ref, q, m, ratio, use_lb, shards, threads)
+        cpu = {"value": c / dt, "unit": "subsequences/s", "cores": threads, "kind": "reference",
+               "sample": f"{len(shards)} shards ({c} candidates) of the same reference, one "
+                         f"unmodified similarity_search per shard on {threads} threads, "
+                         f"{dt:.2f} s"}
 
     # DRAM traffic and issue-slot / pipe utilisation of the sweep (committed ncu capture)
     traffic, ncu_summary = committed_ncu(args.config)
@@ -754,11 +824,7 @@ def main():
             "dtype": "f64",
             "data": "synthetic: seeded N(0,1) random walks (mt19937_64 + Box-Muller), "
                     "no public dataset",
-            "config": {"workload": desc, "n": n, "m": m, "window_cells": w,
-                       "window_ratio": ratio, "parallelism": f"shards{world}",
-                       "l2": "inputs larger than L2 (800 MB reference vs 126 MB L2)"
-                       if n * 8 > 126e6 else "reference smaller than L2",
-                       "batches_per_search": runner.batches},
+            "config": search_config(args.config, world, args.batches),
             "roofline": dict(roof, traffic=traffic, ncu=ncu_summary),
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "subsequences/s",

@@ -68,8 +68,23 @@ int eapdtw_version(void);
 int eapdtw_device_count(void);
 int eapdtw_ctx_create(eapdtw_ctx** out, int device);
 int eapdtw_ctx_destroy(eapdtw_ctx* ctx);
-/* Run on an external stream (e.g. torch.cuda.current_stream().cuda_stream). NULL: own stream. */
+/* Run on an external stream (e.g. torch.cuda.current_stream().cuda_stream).
+ * NULL: the context's own (non-blocking) stream.  The legacy default stream
+ * (torch's default stream reports handle 0) must be passed as
+ * EAPDTW_STREAM_LEGACY (cudaStreamLegacy), not NULL. */
+#define EAPDTW_STREAM_LEGACY ((void*)0x1)
 int eapdtw_ctx_set_stream(eapdtw_ctx* ctx, void* cuda_stream);
+/* Engine options (no environment variables are read).  Names and defaults:
+ *   ad_k -1 (exact-engine window: -1 auto, 0 strip, 1/3/5 anti-diagonal 64K),
+ *   screen_rows 2, f32 1 (FP32 screening engine), streamed -1 (auto/0/1),
+ *   stream_split 3, rank_stride 16, rank_k 16384, rank_waves 1, rank_ub 1,
+ *   rank_ub_w 4, rank_ub_k 16, rank_cascade 1, coarse_stride 0, probe 2048,
+ *   probe_force 0, tighten 1, cb_strip 1, warps 0, nn1_splits 0, nn1_warm 1,
+ *   series_cache 1.
+ * Every value returns the reference's answer; the defaults are the fastest
+ * measured.  EAPDTW_EINVAL for an unknown name or out-of-range value. */
+int eapdtw_ctx_set_option(eapdtw_ctx* ctx, const char* name, int64_t value);
+int eapdtw_ctx_get_option(const eapdtw_ctx* ctx, const char* name, int64_t* value);
 int eapdtw_ctx_synchronize(eapdtw_ctx* ctx);
 /* Number of kernels this context has launched (gpu_launches accounting). */
 uint64_t eapdtw_ctx_launches(const eapdtw_ctx* ctx);
@@ -195,6 +210,19 @@ int eapdtw_nn1_dev_cutoff(eapdtw_ctx* ctx, const double* queries_dev, size_t nq,
                           const double* db_dev, size_t nd, size_t len, size_t window,
                           const double* cutoff_dev, uint64_t* argmin, double* dist,
                           uint64_t* cells);
+
+/* --- the search's preparation kernels, exposed for checking -------------------
+ * Sliding statistics of every length-m window of ref (the RunningStats chain of
+ * similarity_search, search.cpp:156-168, reset every 100000 slides): mean[s]
+ * and sd[s] for s in [0, n-m+1), computed by the search's own stats kernel.
+ * Raw sliding envelope of radius r (compute_envelope's window,
+ * lower_bounds.cpp:9-49, clamped to [0, n)): upper[p] = max(ref[p-r .. p+r]),
+ * lower[p] = min(...), computed by the search's envelope kernel.  Host
+ * pointers in and out; EAPDTW_EINVAL when the envelope tile cannot hold 2r+1. */
+int eapdtw_sliding_stats(eapdtw_ctx* ctx, const double* ref, size_t n, size_t m, double* mean,
+                         double* sd);
+int eapdtw_sliding_envelope(eapdtw_ctx* ctx, const double* ref, size_t n, size_t r, double* upper,
+                            double* lower);
 
 /* --- host-side helpers (bit-identical to the reference) -------------------- */
 /* RunningStats::over + znormalize_into (search.cpp:25-46) */

@@ -152,6 +152,15 @@ class Oracle(_Lib):
                                    C.POINTER(C.c_int)]
         L.orc_lb_keogh.restype = C.c_double
         L.orc_cumulative_bound.argtypes = [_dp, C.c_size_t, _dp]
+        L.orc_random_walk_normal.argtypes = [C.c_size_t, C.c_uint64, _dp]
+
+    def random_walk_normal(self, n, seed):
+        """Benchmark data: x0 = 0, x[i+1] = x[i] + N(0,1) (mt19937_64 +
+        Box-Muller), identical to the product's eapdtw_random_walk_normal."""
+        out = np.empty(n)
+        if self.lib.orc_random_walk_normal(n, seed, out.ctypes.data_as(_dp)):
+            raise ValueError("invalid argument")
+        return out
 
     def sliding_stats(self, ref, m):
         ref, pr = _arr(ref)

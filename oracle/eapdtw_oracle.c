@@ -518,3 +518,66 @@ int orc_nn1(const double* queries, size_t nq, const double* db, size_t nd, size_
   }
   return ORC_OK;
 }
+
+/* ---- benchmark data generator (not a reference algorithm) -------------------
+ * x0 = 0, x[i+1] = x[i] + N(0,1): std::mt19937_64 (the C++ standard fixes its
+ * output stream: word 64, n 312, m 156, r 31, a 0xB5026F5AA96619E9, tempering
+ * u 29 / s 17 / t 37 / l 43, init multiplier 6364136223846793005) mapped to
+ * (0,1) as (k >> 11 + 0.5) 2^-53 and Box-Muller with both variates used -- the
+ * same definition as the product's eapdtw_random_walk_normal, restated here so
+ * bench.py's reference arm generates its inputs without loading the product
+ * library.  tests/test_oracle.py checks the two agree bit for bit. */
+typedef struct {
+  uint64_t mt[312];
+  int idx;
+} orc_mt64;
+
+static void mt64_seed(orc_mt64* g, uint64_t seed) {
+  g->mt[0] = seed;
+  for (int i = 1; i < 312; ++i)
+    g->mt[i] = 6364136223846793005ULL * (g->mt[i - 1] ^ (g->mt[i - 1] >> 62)) + (uint64_t)i;
+  g->idx = 312;
+}
+
+static uint64_t mt64_next(orc_mt64* g) {
+  const uint64_t upper = 0xFFFFFFFF80000000ULL, lower = 0x7FFFFFFFULL;
+  if (g->idx >= 312) {
+    for (int i = 0; i < 312; ++i) {
+      const uint64_t y = (g->mt[i] & upper) | (g->mt[(i + 1) % 312] & lower);
+      uint64_t v = g->mt[(i + 156) % 312] ^ (y >> 1);
+      if (y & 1ULL) v ^= 0xB5026F5AA96619E9ULL;
+      g->mt[i] = v;
+    }
+    g->idx = 0;
+  }
+  uint64_t y = g->mt[g->idx++];
+  y ^= (y >> 29) & 0x5555555555555555ULL;
+  y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
+  y ^= (y << 37) & 0xFFF7EEE000000000ULL;
+  y ^= y >> 43;
+  return y;
+}
+
+int orc_random_walk_normal(size_t n, uint64_t seed, double* out) {
+  if (n == 0 || !out) return ORC_EINVAL;
+  orc_mt64* g = (orc_mt64*)malloc(sizeof(orc_mt64));
+  if (!g) return ORC_ENOMEM;
+  mt64_seed(g, seed);
+  double x = 0.0;
+  out[0] = 0.0;
+  size_t i = 1;
+  while (i < n) {
+    const double u1 = ((double)(mt64_next(g) >> 11) + 0.5) * 0x1.0p-53;
+    const double u2 = ((double)(mt64_next(g) >> 11) + 0.5) * 0x1.0p-53;
+    const double rad = sqrt(-2.0 * log(u1));
+    const double th = 6.283185307179586 * u2;
+    x += rad * cos(th);
+    out[i++] = x;
+    if (i < n) {
+      x += rad * sin(th);
+      out[i++] = x;
+    }
+  }
+  free(g);
+  return ORC_OK;
+}

@@ -31,6 +31,8 @@ from .api import (  # noqa: F401
     random_walk_normal,
     similarity_search,
     similarity_search_dev,
+    sliding_envelope,
+    sliding_stats,
     search_grid,
     search_many,
     trace,

@@ -63,6 +63,8 @@ SIGNATURES = [
     ("eapdtw_ctx_create", C.c_int, [C.POINTER(_vp), C.c_int]),
     ("eapdtw_ctx_destroy", C.c_int, [_vp]),
     ("eapdtw_ctx_set_stream", C.c_int, [_vp, _vp]),
+    ("eapdtw_ctx_set_option", C.c_int, [_vp, C.c_char_p, C.c_int64]),
+    ("eapdtw_ctx_get_option", C.c_int, [_vp, C.c_char_p, C.POINTER(C.c_int64)]),
     ("eapdtw_ctx_synchronize", C.c_int, [_vp]),
     ("eapdtw_ctx_launches", C.c_uint64, [_vp]),
     ("eapdtw_total_launches", C.c_uint64, []),
@@ -110,6 +112,8 @@ SIGNATURES = [
      [_vp, _vp, C.c_size_t, _vp, C.c_size_t, C.c_size_t, C.c_size_t, _u64p, _dp, _u64p]),
     ("eapdtw_nn1_dev_cutoff", C.c_int,
      [_vp, _vp, C.c_size_t, _vp, C.c_size_t, C.c_size_t, C.c_size_t, _vp, _u64p, _dp, _u64p]),
+    ("eapdtw_sliding_stats", C.c_int, [_vp, _dp, C.c_size_t, C.c_size_t, _dp, _dp]),
+    ("eapdtw_sliding_envelope", C.c_int, [_vp, _dp, C.c_size_t, C.c_size_t, _dp, _dp]),
     ("eapdtw_znormalize", C.c_int, [_dp, C.c_size_t, _dp]),
     ("eapdtw_random_walk_uniform", C.c_int, [C.c_size_t, C.c_uint64, _dp]),
     ("eapdtw_random_walk_normal", C.c_int, [C.c_size_t, C.c_uint64, _dp]),

@@ -19,6 +19,7 @@ for cfg1, ``nn1`` for cfg5, ``ShardedSearch`` for multi-GPU) sit beside them.
 from __future__ import annotations
 
 import ctypes as C
+import contextlib
 import enum
 import math
 import threading
@@ -174,7 +175,37 @@ class Context:
             pass
 
     def set_stream(self, stream_ptr: int | None):
-        check(lib.eapdtw_ctx_set_stream(self.handle, C.c_void_p(stream_ptr or 0)))
+        """Run on a CUDA stream handle (e.g. ``torch.cuda.current_stream().cuda_stream``).
+        Handle 0 is the legacy default stream (torch's default stream), passed
+        on as cudaStreamLegacy; None restores the context's own stream."""
+        if stream_ptr is None:
+            h = None
+        elif int(stream_ptr) == 0:
+            h = 1  # EAPDTW_STREAM_LEGACY (cudaStreamLegacy)
+        else:
+            h = int(stream_ptr)
+        check(lib.eapdtw_ctx_set_stream(self.handle, C.c_void_p(h)))
+
+    def set_option(self, name: str, value: int):
+        """Engine option (include/eapdtw_b200.h: eapdtw_ctx_set_option)."""
+        check(lib.eapdtw_ctx_set_option(self.handle, name.encode(), int(value)))
+
+    def get_option(self, name: str) -> int:
+        v = C.c_int64()
+        check(lib.eapdtw_ctx_get_option(self.handle, name.encode(), C.byref(v)))
+        return int(v.value)
+
+    @contextlib.contextmanager
+    def options(self, **kw):
+        """Set options for the duration of a ``with`` block."""
+        old = {k: self.get_option(k) for k in kw}
+        try:
+            for k, v in kw.items():
+                self.set_option(k, v)
+            yield self
+        finally:
+            for k, v in old.items():
+                self.set_option(k, v)
 
     def synchronize(self):
         check(lib.eapdtw_ctx_synchronize(self.handle))
@@ -642,6 +673,30 @@ class SearchPlan:
 
 
 # --- host helpers ------------------------------------------------------------
+
+def sliding_stats(reference, m: int, *, ctx=None):
+    """(mean, sd) of every length-m window, by the search's stats kernel
+    (the RunningStats chain of similarity_search, search.cpp:156-168)."""
+    ctx = ctx or default_context()
+    r = _as_f64(reference)
+    nc = r.size - int(m) + 1
+    mean = np.empty(max(nc, 0))
+    sd = np.empty(max(nc, 0))
+    check(lib.eapdtw_sliding_stats(ctx.handle, _ptr(r), r.size, int(m), _ptr(mean), _ptr(sd)))
+    return mean, sd
+
+
+def sliding_envelope(reference, r: int, *, ctx=None):
+    """(upper, lower): the sliding max / min of radius r over the whole series
+    (compute_envelope's window, lower_bounds.cpp:9-49), by the search's
+    envelope kernel."""
+    ctx = ctx or default_context()
+    x = _as_f64(reference)
+    up = np.empty(x.size)
+    lo = np.empty(x.size)
+    check(lib.eapdtw_sliding_envelope(ctx.handle, _ptr(x), x.size, int(r), _ptr(up), _ptr(lo)))
+    return up, lo
+
 
 def znormalize(x) -> np.ndarray:
     """RunningStats::over + znormalize_into (search.cpp:25-46), bit-identical."""

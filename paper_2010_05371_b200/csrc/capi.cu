@@ -46,8 +46,48 @@ int fail(int code, const std::string& msg) {
   } while (0)
 
 constexpr double kInf = std::numeric_limits<double>::infinity();
-// Spare survivor-queue slots beyond the candidate count (>= resident warps).
-constexpr size_t kQueueSlack = 148 * 64 + 64;
+
+// Engine options of a context (eapdtw_ctx_set_option).  The defaults are the
+// measured best; the others exist so tests can pin that
+// every variant returns the reference's answer.  Nothing is read from the
+// environment: a search depends on its arguments and these options only.
+enum Opt : int {
+  kOptAdK = 0,        // exact-engine window: -1 auto (search: strip; pairwise/NN1: choose_ad_k), 0/1/3/5
+  kOptScreenRows,     // phase-A lane screen depth (rows)
+  kOptF32,            // FP32 screening engine ahead of the exact one
+  kOptStreamed,       // host-pointer search streamed in two parts: -1 auto, 0, 1
+  kOptStreamSplit,    // part 1's share of a streamed search, in eighths
+  kOptRankStride,     // rank pass: every S-th candidate (0: off)
+  kOptRankK,          // ... the ~K best by layered LB_Kim
+  kOptRankWaves,      // ... in this many waves of growing rank
+  kOptRankUb,         // ... upper-bound wave first (narrow-band DTW)
+  kOptRankUbW,        // ... its band divisor
+  kOptRankUbK,        // ... its list divisor
+  kOptRankCascade,    // ... cascade over the ranked list
+  kOptCoarseStride,   // coarse pass over every S-th candidate (0: off)
+  kOptProbe,          // probe candidates
+  kOptProbeForce,     // run the probe even when the upper-bound wave applies
+  kOptTighten,        // tighten_ub honoured (0: ignored; results unchanged either way)
+  kOptCbStrip,        // first strip using the cumulative-bound thresholds
+  kOptWarps,          // warps per search block (0: occupancy-sized)
+  kOptNn1Splits,      // NN1 blocks per query (0: auto)
+  kOptNn1Warm,        // NN1 per-warp warm start
+  kOptSeriesCache,    // device-resident series keep their last stats
+  kNumOpts
+};
+struct OptDef {
+  const char* name;
+  long long def, lo, hi;
+};
+constexpr OptDef kOpts[kNumOpts] = {
+    {"ad_k", -1, -1, 5},          {"screen_rows", 2, 0, 64},    {"f32", 1, 0, 1},
+    {"streamed", -1, -1, 1},      {"stream_split", 3, 1, 7},    {"rank_stride", 16, 0, 1 << 20},
+    {"rank_k", 16384, 1, 1 << 24}, {"rank_waves", 1, 1, 4},     {"rank_ub", 1, 0, 1},
+    {"rank_ub_w", 4, 1, 1 << 16}, {"rank_ub_k", 16, 1, 1 << 16}, {"rank_cascade", 1, 0, 1},
+    {"coarse_stride", 0, 0, 1 << 20}, {"probe", 2048, 1, 1 << 24}, {"probe_force", 0, 0, 1},
+    {"tighten", 1, 0, 1},         {"cb_strip", 1, 1, 1 << 16},  {"warps", 0, 0, 8},
+    {"nn1_splits", 0, 0, 1 << 16}, {"nn1_warm", 1, 0, 1},       {"series_cache", 1, 0, 1},
+};
 
 // Grow-only device buffer.
 struct DevBuf {
@@ -141,6 +181,10 @@ struct LaunchCounter {
 
 struct eapdtw_ctx {
   int device = 0;
+  long long opt[kNumOpts];
+  eapdtw_ctx() {
+    for (int k = 0; k < kNumOpts; ++k) opt[k] = kOpts[k].def;
+  }
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
   LaunchCounter launches;
@@ -151,10 +195,7 @@ struct eapdtw_ctx {
   PlanBuffers pb;  // scratch of the one-shot search API (grow-only, reused)
   cudaStream_t copy = nullptr;  // H2D stream of the streamed host-pointer search
   cudaEvent_t copied[2] = {nullptr, nullptr};
-  // side stream of the preparation: the envelope runs there, concurrently
-  // with the (latency-bound) stats chain on the main stream
-  cudaStream_t aux = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr;
+  cudaEvent_t fork = nullptr;  // orders the streamed copy after earlier work
 };
 
 struct eapdtw_search_plan {
@@ -176,15 +217,17 @@ struct eapdtw_search_plan {
   bool stats_ready = false;  // mean/sd already in the buffers (a series' cached stats)
   int blocks = 0, warps = 8, ad_k = 0, screen_rows = 2;  // screen depth: 2 measured best with the FP32 engine
   int use_f32 = 1;  // FP32 screening engine ahead of the exact one (EAPDTW_F32=0: off)
-  bool overlap_prep = false;  // stats || envelope on two streams (measured slower: the chain shares its SMs)
-  std::vector<int> coarse_strides{};  // coarse passes, in order (the rank pass replaced them)
-  bool coarse_blocks = false;           // coarse pass over runs of adjacent candidates
+  int coarse_stride = 0;  // coarse pass (the rank pass replaced it; 0: off)
   // rank pass (warm start): the cascade over the ~rank_k candidates with the
   // smallest layered LB_Kim among every rank_stride-th (0: off)
   long long rank_stride = 16, rank_k = 16384;
   int rank_waves = 1;  // waves k/16^(n-1) .. k/16, k
   bool rank_ub = true;  // upper-bound wave first (narrow-band DTW of the k/16 best)
+  int rank_ub_w = 4, rank_ub_k = 16;  // its band and list divisors
+  bool rank_cascade = true;
   int probe = 2048;
+  bool probe_force = false;
+  size_t queue_slack = 0;  // spare survivor-queue slots (>= resident warps)
   double guard_rel = 1e-9, guard_abs = 1e-20;
   double qmax = 0.0;  // max |normalised query|
   std::chrono::steady_clock::time_point t0;
@@ -236,12 +279,7 @@ int eapdtw_ctx_destroy(eapdtw_ctx* c) {
   }
   for (cudaEvent_t& ev : c->copied)
     if (ev) cudaEventDestroy(ev);
-  if (c->aux) {
-    cudaStreamSynchronize(c->aux);
-    cudaStreamDestroy(c->aux);
-  }
   if (c->fork) cudaEventDestroy(c->fork);
-  if (c->join) cudaEventDestroy(c->join);
   if (c->own) cudaStreamDestroy(c->own);
   delete c;
   return EAPDTW_OK;
@@ -251,6 +289,30 @@ int eapdtw_ctx_set_stream(eapdtw_ctx* c, void* s) {
   if (!c) return fail(EAPDTW_EINVAL, "null ctx");
   c->stream = s ? static_cast<cudaStream_t>(s) : c->own;
   return EAPDTW_OK;
+}
+
+int eapdtw_ctx_set_option(eapdtw_ctx* c, const char* name, int64_t value) {
+  if (!c || !name) return fail(EAPDTW_EINVAL, "null argument");
+  for (int k = 0; k < kNumOpts; ++k) {
+    if (std::strcmp(name, kOpts[k].name) != 0) continue;
+    if (value < kOpts[k].lo || value > kOpts[k].hi)
+      return fail(EAPDTW_EINVAL, std::string("option out of range: ") + name);
+    if (k == kOptAdK && !(value == -1 || value == 0 || value == 1 || value == 3 || value == 5))
+      return fail(EAPDTW_EINVAL, "option ad_k: -1, 0, 1, 3 or 5");
+    c->opt[k] = value;
+    return EAPDTW_OK;
+  }
+  return fail(EAPDTW_EINVAL, std::string("unknown option: ") + name);
+}
+
+int eapdtw_ctx_get_option(const eapdtw_ctx* c, const char* name, int64_t* value) {
+  if (!c || !name || !value) return fail(EAPDTW_EINVAL, "null argument");
+  for (int k = 0; k < kNumOpts; ++k)
+    if (std::strcmp(name, kOpts[k].name) == 0) {
+      *value = c->opt[k];
+      return EAPDTW_OK;
+    }
+  return fail(EAPDTW_EINVAL, std::string("unknown option: ") + name);
 }
 
 int eapdtw_ctx_synchronize(eapdtw_ctx* c) {
@@ -287,11 +349,10 @@ static int pairwise_impl(eapdtw_ctx* c, const double* rows_dev, const double* co
   p.ub = ub_dev;
   p.cb = cb_dev;
   p.prune = prune;
-  p.ad_k = choose_ad_k(static_cast<int>(lr), w);
+  p.ad_k = c->opt[kOptAdK] >= 0 ? static_cast<int>(c->opt[kOptAdK]) : choose_ad_k(static_cast<int>(lr), w);
   p.out = out_dev;
   p.cells = c->cells.as<unsigned long long>();
   p.npairs = static_cast<long long>(npairs);
-  CUDA_TRY(set_strip_rows(c->stream));
   CUDA_TRY(launch_pairwise(p, c->stream));
   ++c->launches;
   if (cells) {
@@ -499,8 +560,9 @@ static int plan_init(eapdtw_search_plan* p, eapdtw_ctx* c, const double* ref_dev
   p->use_lb = cfg->use_lower_bounds != 0;
   // tighten_ub is consulted only with the cascade and EAPrunedDTW (search.cpp:101-105, 191)
   p->tighten = p->use_lb && cfg->tighten_ub != 0 && cfg->algorithm == EAPDTW_ALGO_EA_PRUNED;
-  if (const char* env = getenv("EAPDTW_TIGHTEN")) p->tighten = p->tighten && atoi(env) != 0;
-  if (const char* env = getenv("EAPDTW_CB_STRIP")) p->cb_strip = std::max(1, atoi(env));
+  const long long* o = c->opt;
+  p->tighten = p->tighten && o[kOptTighten] != 0;
+  p->cb_strip = static_cast<int>(o[kOptCbStrip]);
   p->algo = cfg->algorithm;
   p->ncand = n - m + 1;
   // window_cells_for (search.cpp:18-21)
@@ -513,29 +575,19 @@ static int plan_init(eapdtw_search_plan* p, eapdtw_ctx* c, const double* ref_dev
   // Search DTW calls are mostly short (killed within a few strips), where the
   // strip engine's lower per-call setup wins; the anti-diagonal engine is
   // opt-in here (EAPDTW_AD_K) and the default for pairwise / NN1 batches.
-  p->ad_k = getenv("EAPDTW_AD_K") ? choose_ad_k(static_cast<int>(m), p->w_eff) : 0;
-  if (const char* env = getenv("EAPDTW_SCREEN_ROWS")) p->screen_rows = std::max(0, atoi(env));
-  if (const char* env = getenv("EAPDTW_F32")) p->use_f32 = atoi(env) != 0;
-  if (const char* env = getenv("EAPDTW_OVERLAP_PREP")) p->overlap_prep = atoi(env) != 0;
-  if (const char* env = getenv("EAPDTW_COARSE_STRIDE")) {  // e.g. "512,64" or "512:64"; "0": none
-    p->coarse_strides.clear();
-    for (const char* t = env; *t;) {
-      const int v = atoi(t);
-      if (v > 1) p->coarse_strides.push_back(v);
-      while (*t && *t != ',' && *t != ':') ++t;
-      if (*t) ++t;
-    }
-  }
-  if (const char* env = getenv("EAPDTW_PROBE")) p->probe = std::max(1, atoi(env));
-  if (const char* env = getenv("EAPDTW_COARSE_BLOCKS")) p->coarse_blocks = atoi(env) != 0;
-  if (const char* env = getenv("EAPDTW_RANK_UB")) p->rank_ub = atoi(env) != 0;
-  if (const char* env = getenv("EAPDTW_RANK")) {  // "S:K", "0": off
-    p->rank_stride = std::max(0, atoi(env));
-    if (const char* c2 = strchr(env, ':')) {
-      p->rank_k = std::max(1, atoi(c2 + 1));
-      if (const char* c3 = strchr(c2 + 1, ':')) p->rank_waves = std::max(1, std::min(4, atoi(c3 + 1)));
-    }
-  }
+  p->ad_k = o[kOptAdK] > 0 ? static_cast<int>(o[kOptAdK]) : 0;
+  p->screen_rows = static_cast<int>(o[kOptScreenRows]);
+  p->use_f32 = static_cast<int>(o[kOptF32]);
+  p->coarse_stride = static_cast<int>(o[kOptCoarseStride]);
+  p->probe = static_cast<int>(o[kOptProbe]);
+  p->probe_force = o[kOptProbeForce] != 0;
+  p->rank_ub = o[kOptRankUb] != 0;
+  p->rank_stride = o[kOptRankStride];
+  p->rank_k = o[kOptRankK];
+  p->rank_waves = static_cast<int>(o[kOptRankWaves]);
+  p->rank_ub_w = static_cast<int>(o[kOptRankUbW]);
+  p->rank_ub_k = static_cast<int>(o[kOptRankUbK]);
+  p->rank_cascade = o[kOptRankCascade] != 0;
   p->guard_abs = 1e-20;
 
   // Query preparation exactly as search.cpp:136-149.
@@ -582,10 +634,6 @@ static int plan_init(eapdtw_search_plan* p, eapdtw_ctx* c, const double* ref_dev
   CUDA_TRY(B.best.ensure(sizeof(BestRecord)));
   CUDA_TRY(B.key.ensure(8));
   CUDA_TRY(B.work.ensure(8));
-  // One spare slot per resident warp: a consumer may hold a "future" slot past
-  // the final tail, which must read as empty (-1) rather than stale data.
-  CUDA_TRY(B.queue.ensure((nc + kQueueSlack) * 8));
-  CUDA_TRY(B.qtot.ensure((nc + kQueueSlack) * 8));
   CUDA_TRY(B.qctr.ensure(24));
   CUDA_TRY(B.flag.ensure(8));
   CUDA_TRY(B.counters.ensure(kNumCountersExt * 8));
@@ -634,12 +682,12 @@ static int plan_init(eapdtw_search_plan* p, eapdtw_ctx* c, const double* ref_dev
     return fail(EAPDTW_EINVAL, "search: query length exceeds the shared-memory budget");
   p->warps = best_w;
   p->blocks = sms * best_blocks;
-  if (const char* env = getenv("EAPDTW_WARPS")) {  // experiment: fewer warps per block
-    const int wv = atoi(env);
-    if (wv >= 1 && wv < p->warps) p->warps = wv;
-  }
-  if (const size_t sd = search_scratch_doubles(static_cast<int>(m), p->blocks, p->warps, p->ad_k))
-    CUDA_TRY(p->buf->scratch.ensure(sd * 8));
+  if (o[kOptWarps] >= 1 && o[kOptWarps] < p->warps) p->warps = static_cast<int>(o[kOptWarps]);
+  // One spare slot per resident warp: a consumer may hold a "future" slot past
+  // the final tail, which must read as empty (-1) rather than stale data.
+  p->queue_slack = static_cast<size_t>(p->blocks) * p->warps + 64;
+  CUDA_TRY(B.queue.ensure((nc + p->queue_slack) * 8));
+  CUDA_TRY(B.qtot.ensure((nc + p->queue_slack) * 8));
   return eapdtw_search_plan_reset(p);
 }
 
@@ -669,13 +717,6 @@ int eapdtw_search_plan_reset(eapdtw_search_plan* p) {
   CUDA_TRY(cudaMemsetAsync(B.probe_counters.p, 0, kNumCountersExt * 8, s));
   CUDA_TRY(launch_init_best(B.best.as<BestRecord>(), p->key, 1, s));
   ++c->launches;
-  if (const char* env = getenv("EAPDTW_SEED_UB")) {  // experiment: start from a known threshold
-    const double ub = atof(env);
-    unsigned long long bits;
-    std::memcpy(&bits, &ub, 8);
-    CUDA_TRY(cudaMemcpyAsync(p->key, &bits, 8, cudaMemcpyHostToDevice, s));
-    CUDA_TRY(cudaStreamSynchronize(s));
-  }
   p->prepared = false;
   p->ran = false;
   p->t0 = std::chrono::steady_clock::now();
@@ -700,7 +741,7 @@ static cudaError_t reset_work(eapdtw_search_plan* p, long long count, cudaStream
   cudaError_t e = cudaMemsetAsync(B.work.p, 0, 8, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(B.qctr.p, 0, 24, s);
   if (e == cudaSuccess && count > 0)
-    e = cudaMemsetAsync(B.queue.p, 0xff, static_cast<size_t>(count + kQueueSlack) * 8, s);
+    e = cudaMemsetAsync(B.queue.p, 0xff, static_cast<size_t>(count) * 8 + p->queue_slack * 8, s);
   return e;
 }
 
@@ -714,7 +755,6 @@ static SearchParams base_params(eapdtw_search_plan* p) {
   s.q = B.q.as<double>();
   s.qul = B.qul.as<double2>();
   s.qperm = B.qperm.as<double2>();
-  s.qperm32 = reinterpret_cast<const float2*>(static_cast<char*>(B.qperm.p) + p->m * 16);
   s.order = B.order.as<int>();
   s.ncand = static_cast<long long>(p->ncand);
   s.m = static_cast<int>(p->m);
@@ -753,14 +793,9 @@ static SearchParams base_params(eapdtw_search_plan* p) {
     s.f32_a = g.a;
     s.f32_b = g.b;
     s.f32_cmax = static_cast<float>(cmax);
-    // FP32 Keogh tiers: m terms, each value within 4 u32 of the reference's
-    const F32Guard gl = make_f32_guard(static_cast<int>(p->m), 0, cmax, p->qmax, 4.0);
-    s.lb32_a = gl.a;
-    s.lb32_b = gl.b;
   }
   s.counters = B.counters.as<unsigned long long>();
   s.index_offset = static_cast<long long>(p->offset);
-  s.dtw_scratch = B.scratch.p ? B.scratch.as<double>() : nullptr;
   return s;
 }
 
@@ -793,30 +828,13 @@ static int stage_env(eapdtw_search_plan* p, long long tile_b, long long tile_e, 
   return EAPDTW_OK;
 }
 
-// Stats chain (main stream) and envelope (side stream) concurrently: the
-// chain is latency-bound on few SMs, the envelope streams HBM.  Work already
-// enqueued on the main stream precedes both; the main stream waits for the
-// envelope before returning (everything after needs both).
+// Stats chain then envelope on the context stream.  (Running them on two
+// streams measured slower: the latency-bound chain shares its SMs.)
 static int stage_stats_env(eapdtw_search_plan* p, long long seg_b, long long seg_e,
                            long long tile_b, long long tile_e, bool first) {
-  eapdtw_ctx* c = p->ctx;
   int e;
-  if (!p->overlap_prep) {
-    if ((e = stage_stats(p, seg_b, seg_e))) return e;
-    return stage_env(p, tile_b, tile_e, first);
-  }
-  if (!c->aux) {
-    CUDA_TRY(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
-    CUDA_TRY(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
-    CUDA_TRY(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
-  }
-  CUDA_TRY(cudaEventRecord(c->fork, c->stream));
-  CUDA_TRY(cudaStreamWaitEvent(c->aux, c->fork, 0));
-  if ((e = stage_env(p, tile_b, tile_e, first, c->aux))) return e;
-  CUDA_TRY(cudaEventRecord(c->join, c->aux));
   if ((e = stage_stats(p, seg_b, seg_e))) return e;
-  CUDA_TRY(cudaStreamWaitEvent(c->stream, c->join, 0));
-  return EAPDTW_OK;
+  return stage_env(p, tile_b, tile_e, first);
 }
 
 // Probe: evaluate evenly spaced candidates of [0, cand_end) first (no lower
@@ -834,7 +852,7 @@ static bool rank_applies(const eapdtw_search_plan* p, size_t cb, size_t ce) {
 
 static int stage_probe(eapdtw_search_plan* p, size_t cand_end) {
   // the rank pass's upper-bound wave gives the first finite threshold
-  if (rank_ub_applies(p) && rank_applies(p, 0, cand_end) && !getenv("EAPDTW_PROBE")) return EAPDTW_OK;
+  if (rank_ub_applies(p) && rank_applies(p, 0, cand_end) && !p->probe_force) return EAPDTW_OK;
   PlanBuffers& B = *p->buf;
   cudaStream_t s = p->ctx->stream;
   const size_t nprobe =
@@ -849,7 +867,6 @@ static int stage_probe(eapdtw_search_plan* p, size_t cand_end) {
   sp.counters = B.probe_counters.as<unsigned long long>();
   sp.direct_chunk = 1;
   sp.direct = 1;
-  CUDA_TRY(set_strip_rows(s));
   CUDA_TRY(reset_work(p, static_cast<long long>(nprobe), s));
   CUDA_TRY(launch_search(sp, p->blocks, p->warps, s));
   ++p->ctx->launches;
@@ -897,9 +914,8 @@ static int stage_rank(eapdtw_search_plan* p, size_t cb, size_t ce) {
     up.use_lb = 0;
     up.tighten = 0;
     up.ub_only = 1;
-    int wdiv = 4, kdiv = 16;  // band w/4 measured best of w/16, w/8, w/4, w/2 (cfg4 -0.5 ms vs w/16)
-    if (const char* e = getenv("EAPDTW_RANK_UBW")) wdiv = std::max(1, atoi(e));
-    if (const char* e = getenv("EAPDTW_RANK_UBK")) kdiv = std::max(1, atoi(e));
+    // band w/4 measured best of w/16, w/8, w/4, w/2 (cfg4 -0.5 ms vs w/16)
+    const int wdiv = p->rank_ub_w, kdiv = p->rank_ub_k;
     up.w = std::max(0, p->w_eff / wdiv);
     CUDA_TRY(launch_rank_select(up, S, wave, std::max<long long>(32, p->rank_k / kdiv), cap,
                                 B.rank.p, list, nlist, s));
@@ -911,8 +927,7 @@ static int stage_rank(eapdtw_search_plan* p, size_t cb, size_t ce) {
   }
   // then the cascade over the ranks past it (waves of growing rank, each
   // starting from the threshold the better-ranked candidates before it left)
-  if (const char* e = getenv("EAPDTW_RANK_CASCADE"))
-    if (atoi(e) == 0) return EAPDTW_OK;
+  if (!p->rank_cascade) return EAPDTW_OK;
   for (long long k = std::max<long long>(32, p->rank_k >> (4 * (p->rank_waves - 1)));;
        k = std::min(p->rank_k, k << 4), ++wave) {
     CUDA_TRY(launch_rank_select(rp, S, wave, k, cap, B.rank.p, list, nlist, s));
@@ -926,27 +941,19 @@ static int stage_rank(eapdtw_search_plan* p, size_t cb, size_t ce) {
 }
 
 static int stage_coarse(eapdtw_search_plan* p, size_t cb, size_t ce) {
+  const int stride = p->coarse_stride;
+  if (stride <= 1 || ce - cb < 64 * static_cast<size_t>(stride)) return EAPDTW_OK;
   PlanBuffers& B = *p->buf;
   cudaStream_t s = p->ctx->stream;
-  for (const int stride : p->coarse_strides) {
-    if (ce - cb < 64 * static_cast<size_t>(stride)) continue;
-    SearchParams cp = base_params(p);
-    cp.begin = static_cast<long long>(cb);
-    cp.end = static_cast<long long>(ce);
-    cp.counters = B.probe_counters.as<unsigned long long>();
-    long long count;
-    if (p->coarse_blocks) {  // runs of 32 adjacent candidates every 32*stride
-      cp.stride = 1;
-      cp.chunk_span = 32LL * stride;
-      count = 32 * ((cp.end - cp.begin + cp.chunk_span - 1) / cp.chunk_span);
-    } else {
-      cp.stride = stride;
-      count = (cp.end - cp.begin + cp.stride - 1) / cp.stride;
-    }
-    CUDA_TRY(reset_work(p, count, s));
-    CUDA_TRY(launch_search(cp, p->blocks, p->warps, s));
-    ++p->ctx->launches;
-  }
+  SearchParams cp = base_params(p);
+  cp.begin = static_cast<long long>(cb);
+  cp.end = static_cast<long long>(ce);
+  cp.counters = B.probe_counters.as<unsigned long long>();
+  cp.stride = stride;
+  const long long count = (cp.end - cp.begin + cp.stride - 1) / cp.stride;
+  CUDA_TRY(reset_work(p, count, s));
+  CUDA_TRY(launch_search(cp, p->blocks, p->warps, s));
+  ++p->ctx->launches;
   return EAPDTW_OK;
 }
 
@@ -958,14 +965,9 @@ int eapdtw_search_plan_prepare(eapdtw_search_plan* p) {
   int e;
   CUDA_TRY(cudaEventRecord(p->ev[0], s));
   p->have_env = false;
-  if (p->overlap_prep && !p->stats_ready) {  // stats || envelope: the "stats" phase spans both
-    if ((e = stage_stats_env(p, 0, -1, 0, -1, true))) return e;
-    CUDA_TRY(cudaEventRecord(p->ev[1], s));
-  } else {
-    if (!p->stats_ready && (e = stage_stats(p, 0, -1))) return e;
-    CUDA_TRY(cudaEventRecord(p->ev[1], s));
-    if ((e = stage_env(p, 0, -1, true))) return e;
-  }
+  if (!p->stats_ready && (e = stage_stats(p, 0, -1))) return e;
+  CUDA_TRY(cudaEventRecord(p->ev[1], s));
+  if ((e = stage_env(p, 0, -1, true))) return e;
   CUDA_TRY(cudaEventRecord(p->ev[2], s));
   if ((e = stage_probe(p, p->ncand))) return e;
   if ((e = stage_rank(p, 0, p->ncand))) return e;
@@ -1211,7 +1213,7 @@ int eapdtw_similarity_search_series(eapdtw_ctx* c, eapdtw_series* ref, const dou
                                     eapdtw_search_result* out) {
   if (!c || !ref) return fail(EAPDTW_EINVAL, "null argument");
   if (ref->device != c->device) return fail(EAPDTW_EINVAL, "series lives on another device");
-  if (getenv("EAPDTW_SERIES_STATS_CACHE") && atoi(getenv("EAPDTW_SERIES_STATS_CACHE")) == 0)
+  if (c->opt[kOptSeriesCache] == 0)
     return one_shot(c, ref->data.as<const double>(), ref->n, query, qlen, cfg, false, out);
   SeriesStats* cache = nullptr;
   {
@@ -1243,9 +1245,8 @@ static int one_shot_streamed(eapdtw_ctx* c, const double* host_ref, size_t n,
   // part 2's copy hides under part 1's stats, warm start and sweep.  Shares
   // of 1/8 .. 4/8 measured within noise (cfg4 e2e 61-64 ms; the second stats
   // chain and envelope, not the first copy, are what remains exposed).
-  // EAPDTW_STREAM_SPLIT = part 1's share in eighths.
-  long long eighths = 3;
-  if (const char* e8 = getenv("EAPDTW_STREAM_SPLIT")) eighths = std::max(1, std::min(7, atoi(e8)));
+  // Option stream_split = part 1's share in eighths.
+  const long long eighths = c->opt[kOptStreamSplit];
   const long long seg1 = std::max<long long>(1, nseg * eighths / 8);
   const size_t c1 = static_cast<size_t>(seg1) * kStatsResetInterval;
   // data part 1 needs: its stats windows (< c1 + m - 1) and the envelope
@@ -1253,32 +1254,41 @@ static int one_shot_streamed(eapdtw_ctx* c, const double* host_ref, size_t n,
   // radius r <= m: within c1 + 2m + the largest tile (8192)
   const size_t d1 = std::min(n, c1 + 2 * m + 8192);
   double* dref = c->ref.as<double>();
-  if (!c->copy) {
-    CUDA_TRY(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
-    for (cudaEvent_t& ev : c->copied)
-      CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-  }
-  if (!c->fork) CUDA_TRY(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
-  cudaStream_t s = c->stream;
-  CUDA_TRY(cudaEventRecord(c->fork, s));  // the copy must not overtake earlier work on s
-  CUDA_TRY(cudaStreamWaitEvent(c->copy, c->fork, 0));
-  CUDA_TRY(cudaMemcpyAsync(dref, host_ref, d1 * 8, cudaMemcpyHostToDevice, c->copy));
-  CUDA_TRY(cudaEventRecord(c->copied[0], c->copy));
-  CUDA_TRY(cudaMemcpyAsync(dref + d1, host_ref + d1, (n - d1) * 8, cudaMemcpyHostToDevice,
-                           c->copy));
-  CUDA_TRY(cudaEventRecord(c->copied[1], c->copy));
-
   eapdtw_search_plan p;
   p.buf = &c->pb;
-  int e = plan_init(&p, c, dref, n, query, qlen, cfg, 0);
+  // Every return after the copies are queued goes through finish(): an error
+  // must not leave the copy stream reading the caller's host buffer.
+  bool queued = false;
   auto finish = [&](int rc) {
-    // an early error return must not leave the copy reading caller memory
-    if (rc) cudaStreamSynchronize(c->copy);
+    if (queued) cudaStreamSynchronize(c->copy);
     for (auto& ev : p.ev)
       if (ev) cudaEventDestroy(ev);
     p.buf = &p.own;
     return rc;
   };
+#define CUDA_TRY_F(expr)                                                                   \
+  do {                                                                                     \
+    cudaError_t e_ = (expr);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
+      return finish(fail(EAPDTW_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_))); \
+  } while (0)
+  if (!c->copy) {
+    CUDA_TRY_F(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+    for (cudaEvent_t& ev : c->copied)
+      CUDA_TRY_F(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  }
+  if (!c->fork) CUDA_TRY_F(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
+  cudaStream_t s = c->stream;
+  CUDA_TRY_F(cudaEventRecord(c->fork, s));  // the copy must not overtake earlier work on s
+  CUDA_TRY_F(cudaStreamWaitEvent(c->copy, c->fork, 0));
+  queued = true;
+  CUDA_TRY_F(cudaMemcpyAsync(dref, host_ref, d1 * 8, cudaMemcpyHostToDevice, c->copy));
+  CUDA_TRY_F(cudaEventRecord(c->copied[0], c->copy));
+  CUDA_TRY_F(cudaMemcpyAsync(dref + d1, host_ref + d1, (n - d1) * 8, cudaMemcpyHostToDevice,
+                             c->copy));
+  CUDA_TRY_F(cudaEventRecord(c->copied[1], c->copy));
+
+  int e = plan_init(&p, c, dref, n, query, qlen, cfg, 0);
   if (e) return finish(e);
   long long te1 = 0;
   const int T = envelope_tile(p.env_r);
@@ -1286,12 +1296,12 @@ static int one_shot_streamed(eapdtw_ctx* c, const double* host_ref, size_t n,
     // tiles [0, te1) read positions < te1*T + r <= c1 + 2m + T - 2 <= d1 (or n)
     te1 = static_cast<long long>((c1 + m - 1 + T - 1) / T);
   }
-  CUDA_TRY(cudaEventRecord(p.ev[0], s));
+  CUDA_TRY_F(cudaEventRecord(p.ev[0], s));
   // ---- part 1
-  CUDA_TRY(cudaStreamWaitEvent(s, c->copied[0], 0));
-  CUDA_TRY(cudaMemsetAsync(c->pb.flag.p, 0, 8, s));
-  CUDA_TRY(launch_check_finite(dref, static_cast<long long>(d1),
-                               c->pb.flag.as<unsigned long long>(), s));
+  CUDA_TRY_F(cudaStreamWaitEvent(s, c->copied[0], 0));
+  CUDA_TRY_F(cudaMemsetAsync(c->pb.flag.p, 0, 8, s));
+  CUDA_TRY_F(launch_check_finite(dref, static_cast<long long>(d1),
+                                 c->pb.flag.as<unsigned long long>(), s));
   ++c->launches;
   p.have_env = false;
   if ((e = stage_stats_env(&p, 0, seg1, 0, te1, true))) return finish(e);
@@ -1301,10 +1311,10 @@ static int one_shot_streamed(eapdtw_ctx* c, const double* host_ref, size_t n,
   p.prepared = true;
   if ((e = eapdtw_search_plan_run(&p, 0, c1))) return finish(e);
   // ---- part 2
-  CUDA_TRY(cudaStreamWaitEvent(s, c->copied[1], 0));
+  CUDA_TRY_F(cudaStreamWaitEvent(s, c->copied[1], 0));
   if (n > d1) {
-    CUDA_TRY(launch_check_finite(dref + d1, static_cast<long long>(n - d1),
-                                 c->pb.flag.as<unsigned long long>(), s));
+    CUDA_TRY_F(launch_check_finite(dref + d1, static_cast<long long>(n - d1),
+                                   c->pb.flag.as<unsigned long long>(), s));
     ++c->launches;
   }
   if ((e = stage_stats_env(&p, seg1, -1, te1, -1, false))) return finish(e);
@@ -1312,9 +1322,10 @@ static int one_shot_streamed(eapdtw_ctx* c, const double* host_ref, size_t n,
   if ((e = eapdtw_search_plan_run(&p, c1, ncand))) return finish(e);
   if ((e = eapdtw_search_plan_result(&p, out))) return finish(e);
   unsigned long long bad = 0;
-  CUDA_TRY(cudaMemcpy(&bad, c->pb.flag.p, 8, cudaMemcpyDeviceToHost));
+  CUDA_TRY_F(cudaMemcpy(&bad, c->pb.flag.p, 8, cudaMemcpyDeviceToHost));
   if (bad) return finish(fail(EAPDTW_EINVAL, "Series: non-finite sample in the reference"));
   return finish(EAPDTW_OK);
+#undef CUDA_TRY_F
 }
 
 int eapdtw_similarity_search(eapdtw_ctx* c, const double* ref, size_t n, const double* query,
@@ -1328,8 +1339,7 @@ int eapdtw_similarity_search(eapdtw_ctx* c, const double* ref, size_t n, const d
   // sweep (measured: cfg4 e2e +1.2%; below ~5e7 points the second stats
   // chain and coarse pass cost more than the hidden copy, e.g. cfg3 -30%)
   bool streamed = cfg && query && qlen > 0 && n >= 4 * static_cast<size_t>(kStatsResetInterval);
-  const char* env = getenv("EAPDTW_STREAMED");
-  if (env) streamed = streamed && atoi(env) != 0;
+  if (c->opt[kOptStreamed] >= 0) streamed = streamed && c->opt[kOptStreamed] != 0;
   else streamed = streamed && n >= 50000000;
   if (streamed) {
     const size_t m = cfg->query_length == 0 ? qlen : cfg->query_length;
@@ -1376,8 +1386,8 @@ static int nn1_impl(eapdtw_ctx* c, const double* q_dev, size_t nq, const double*
   const long long target = 148LL * 64;
   p.splits = static_cast<int>(std::max<long long>(1, std::min<long long>(
       static_cast<long long>(nd) / 64 + 1, (target + static_cast<long long>(nq) - 1) / static_cast<long long>(nq))));
-  if (const char* env = getenv("EAPDTW_NN1_SPLITS")) p.splits = std::max(1, atoi(env));  // experiment
-  p.ad_k = choose_ad_k(static_cast<int>(len), w);
+  if (c->opt[kOptNn1Splits] > 0) p.splits = static_cast<int>(c->opt[kOptNn1Splits]);
+  p.ad_k = c->opt[kOptAdK] >= 0 ? static_cast<int>(c->opt[kOptAdK]) : choose_ad_k(static_cast<int>(len), w);
   p.ub_keys = c->keys.as<unsigned long long>();
   p.best = c->best.as<BestRecord>();
   p.cells = c->counters.as<unsigned long long>();  // [FP64 cells, FP32 cells]
@@ -1387,17 +1397,14 @@ static int nn1_impl(eapdtw_ctx* c, const double* q_dev, size_t nq, const double*
     // + 1, checked per query (block) and per strip of database rows.
     const double cmax = std::sqrt(static_cast<double>(len)) + 1.0;
     const F32Guard g = make_f32_guard(static_cast<int>(len), static_cast<int>(len), cmax, cmax);
-    p.use_f32 = 1;
-    if (const char* env = getenv("EAPDTW_F32")) p.use_f32 = atoi(env) != 0;
+    p.use_f32 = static_cast<int>(c->opt[kOptF32]);
     p.f32_a = g.a;
     p.f32_b = g.b;
     p.f32_cmax = static_cast<float>(cmax);
   }
   p.guard_rel = std::max(1e-9, 8.0 * static_cast<double>(len) * 0x1.0p-53);
   p.guard_abs = 1e-20;
-  p.warm = 1;
-  if (const char* env = getenv("EAPDTW_NN1_WARM")) p.warm = atoi(env) != 0;
-  CUDA_TRY(set_strip_rows(s));
+  p.warm = static_cast<int>(c->opt[kOptNn1Warm]);
   CUDA_TRY(launch_nn1(p, s));
   ++c->launches;
   std::vector<BestRecord> rec(nq);
@@ -1451,6 +1458,67 @@ int eapdtw_nn1(eapdtw_ctx* c, const double* queries, size_t nq, const double* db
   CUDA_TRY(cudaMemcpyAsync(c->a.p, queries, nq * len * 8, cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(cudaMemcpyAsync(c->b.p, db, nd * len * 8, cudaMemcpyHostToDevice, c->stream));
   return nn1_impl(c, c->a.as<double>(), nq, c->b.as<double>(), nd, len, window, argmin, dist, cells);
+}
+
+// ---------------------------------------------------------------------------
+// The preparation kernels on their own (checking: tests compare them with the
+// oracle element by element)
+// ---------------------------------------------------------------------------
+int eapdtw_sliding_stats(eapdtw_ctx* c, const double* ref, size_t n, size_t m, double* mean,
+                         double* sd) {
+  if (!c || !ref || !mean || !sd) return fail(EAPDTW_EINVAL, "null argument");
+  if (n == 0 || m == 0 || m > n) return fail(EAPDTW_EINVAL, "sliding_stats: bad lengths");
+  CUDA_TRY(cudaSetDevice(c->device));
+  const size_t nc = n - m + 1;
+  DevBuf dref, dmean, dsd;
+  auto done = [&](int rc) {
+    dref.release();
+    dmean.release();
+    dsd.release();
+    return rc;
+  };
+  cudaError_t e = dref.ensure(n * 8);
+  if (!e) e = dmean.ensure(nc * 8);
+  if (!e) e = dsd.ensure(nc * 8);
+  if (!e) e = cudaMemcpyAsync(dref.p, ref, n * 8, cudaMemcpyHostToDevice, c->stream);
+  if (!e) e = launch_stats(dref.as<double>(), static_cast<long long>(n), static_cast<int>(m),
+                           dmean.as<double>(), dsd.as<double>(), c->stream);
+  if (!e) ++c->launches;
+  if (!e) e = cudaMemcpyAsync(mean, dmean.p, nc * 8, cudaMemcpyDeviceToHost, c->stream);
+  if (!e) e = cudaMemcpyAsync(sd, dsd.p, nc * 8, cudaMemcpyDeviceToHost, c->stream);
+  if (!e) e = cudaStreamSynchronize(c->stream);
+  if (e) return done(fail(EAPDTW_ECUDA, std::string("sliding_stats: ") + cudaGetErrorString(e)));
+  return done(EAPDTW_OK);
+}
+
+int eapdtw_sliding_envelope(eapdtw_ctx* c, const double* ref, size_t n, size_t r, double* upper,
+                            double* lower) {
+  if (!c || !ref || !upper || !lower) return fail(EAPDTW_EINVAL, "null argument");
+  if (n == 0) return fail(EAPDTW_EINVAL, "sliding_envelope: empty series");
+  if (envelope_tile(static_cast<int>(std::min<size_t>(r, 1u << 20))) < 256)
+    return fail(EAPDTW_EINVAL, "sliding_envelope: radius too large for the envelope tile");
+  CUDA_TRY(cudaSetDevice(c->device));
+  DevBuf dref, denv;
+  auto done = [&](int rc) {
+    dref.release();
+    denv.release();
+    return rc;
+  };
+  std::vector<double> env(2 * n);
+  cudaError_t e = dref.ensure(n * 8);
+  if (!e) e = denv.ensure(2 * n * 8);
+  if (!e) e = cudaMemcpyAsync(dref.p, ref, n * 8, cudaMemcpyHostToDevice, c->stream);
+  if (!e) e = launch_envelope(dref.as<double>(), static_cast<long long>(n), static_cast<int>(r),
+                              denv.as<double>(), c->stream);
+  if (!e) ++c->launches;
+  if (!e) e = cudaMemcpyAsync(env.data(), denv.p, 2 * n * 8, cudaMemcpyDeviceToHost, c->stream);
+  if (!e) e = cudaStreamSynchronize(c->stream);
+  if (e) return done(fail(EAPDTW_ECUDA, std::string("sliding_envelope: ") + cudaGetErrorString(e)));
+  for (size_t k = 0; k < n; ++k) {
+    upper[k] = env[2 * k];
+    lower[k] = env[2 * k + 1];
+  }
+  return done(EAPDTW_OK);
 }
 
 // ---------------------------------------------------------------------------

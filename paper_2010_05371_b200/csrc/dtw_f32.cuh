@@ -35,12 +35,6 @@
 
 #include "dtw_warp.cuh"
 
-#ifndef EAPDTW_F32_FASTFIN
-#define EAPDTW_F32_FASTFIN 1  // closed-form finish masks (BLK == 8; 0: the chained updates)
-#endif
-#ifndef EAPDTW_F32_FASTRANGE
-#define EAPDTW_F32_FASTRANGE 0  // block fast path without the band test (experiment)
-#endif
 
 namespace eapdtw_b200 {
 
@@ -190,14 +184,10 @@ __device__ float warp_dtw_f32(const RawFn& rowraw, const NormFn& rownorm, int lr
     for (;;) {
       const unsigned before = finmask;
       bool alld = true;
-#if EAPDTW_F32_FASTRANGE
-      if (!banded || __all_sync(kFull, !active || (jr >= 0 && jr + 3 <= static_cast<int>(span)))) {
-#else
       // Unbounded band: the band is the whole row, and the +inf padding of
       // qsp (dtw_warp.cuh) already makes every out-of-range column cost +inf,
       // so the per-step band test (3 ALU-pipe ops per cell) is dropped.
       if (UNB && !banded) {
-#endif
 #pragma unroll
         for (int u = 0; u < BLK; ++u) step(std::false_type{}, u, alld);
       } else {
@@ -209,7 +199,7 @@ __device__ float warp_dtw_f32(const RawFn& rowraw, const NormFn& rownorm, int lr
       // the row buffer, dead beyond column hi) was finished after step u-1.
       // BLK chained updates, one per step, with the block's all-dead mask D.
       const unsigned D = __ballot_sync(kFull, alld);
-      if constexpr (EAPDTW_F32_FASTFIN && BLK == 8) {
+      if constexpr (BLK == 8) {
         // Closed form of the BLK chained updates (same result; identity
         // checked in tests/test_finish_mask.py): a lane of D finishes if a
         // run of D lanes joins it to a seed within reach.  Seeds: lanes just
@@ -279,155 +269,6 @@ __device__ float warp_dtw_f32(const RawFn& rowraw, const NormFn& rownorm, int lr
     atomicAdd(&g_dbg[8 + bin], dbg_steps);
   }
 #endif
-  for (int off = 16; off > 0; off >>= 1) cnt += __shfl_xor_sync(kFull, cnt, off);
-  if (lane == 0) cells += cnt;
-  __syncwarp();
-  if (status != 0 || lo < 0 || hi != lc) return INF;
-  const float r = rowbuf[lc];
-  return r <= ub_last ? r : INF;
-}
-
-// Two rows per lane (the schedule of warp_dtw2, dtw_warp.cuh) in FP32: strips
-// of 64 rows, lane L owning rows i0+2L and i0+2L+1 at the same column; the
-// shuffle, query read, ballots and finish bookkeeping of a step serve two
-// cells.  Same contract as warp_dtw_f32.  rowthr(u, i, i0) is the 32-row
-// threshold function of warp_dtw_f32 (lane L: row i0+L); it is called for
-// the strip's two 32-row halves in order and redistributed by shuffles.
-template <class RawFn, class NormFn, class UbFn, class RowThrFn>
-__device__ float warp_dtw2_f32(const RawFn& rowraw, const NormFn& rownorm, int lr,
-                               const float* __restrict__ qsp, int lc, int w, float cmax,
-                               UbFn&& get_ub, RowThrFn&& rowthr, float* __restrict__ rowbuf,
-                               unsigned long long& cells, int& status) {
-  const int lane = threadIdx.x & 31;
-  const float INF = f_inf();
-  status = 0;
-  for (int k = lane; k <= lc + 1; k += 32) rowbuf[k] = k == 0 ? 0.0f : INF;
-  const bool banded = w < lr;
-  int lo = 0, hi = 0;  // live column range of the row held in rowbuf (row i0-1)
-  int written = 0;
-  unsigned cnt = 0;
-  float ub_last = INF;
-  double ub_next = get_ub();
-  double x1n = 2 * lane < lr ? rowraw(2 * lane) : 0.0;
-  double x2n = 2 * lane + 1 < lr ? rowraw(2 * lane + 1) : 0.0;
-  __syncwarp();
-
-  for (int i0 = 1; i0 <= lr; i0 += 64) {
-    const double ub_strip = ub_next;
-    const int i1 = i0 + 2 * lane, i2 = i1 + 1;
-    const bool act1 = i1 <= lr, act2 = i2 <= lr;
-    const double x1 = x1n, x2 = x2n;
-    if (i0 + 64 <= lr) {  // prefetch the next strip's threshold and row values
-      ub_next = get_ub();
-      x1n = i1 + 64 <= lr ? rowraw(i1 + 63) : 0.0;
-      x2n = i2 + 64 <= lr ? rowraw(i2 + 63) : 0.0;
-    }
-    // thresholds of rows i0 + lane and i0 + 32 + lane, then lane L takes
-    // rows i0 + 2L, i0 + 2L + 1
-    const float ta = rowthr(ub_strip, i0 + lane, i0);
-    const float tb = rowthr(ub_strip, i0 + 32 + lane, i0 + 32);
-    const int s1 = (2 * lane) & 31, s2 = (2 * lane + 1) & 31;
-    const float a1 = __shfl_sync(kFull, ta, s1), b1 = __shfl_sync(kFull, tb, s1);
-    const float a2 = __shfl_sync(kFull, ta, s2), b2 = __shfl_sync(kFull, tb, s2);
-    const float t1 = lane < 16 ? a1 : b1, t2 = lane < 16 ? a2 : b2;
-    const int last = min(i0 + 63, lr);  // the strip's last row
-    const int wl = (last - i0) >> 1;    // its lane
-    const bool wsecond = ((last - i0) & 1) != 0;
-    ub_last = __shfl_sync(kFull, wsecond ? t2 : t1, wl);
-    const float c1 = act1 ? rownorm(x1) : INF;
-    const float c2 = act2 ? rownorm(x2) : INF;
-    if (__any_sync(kFull, (act1 && !(fabsf(c1) <= cmax)) || (act2 && !(fabsf(c2) <= cmax)))) {
-      status = kF32Undecided;
-      break;
-    }
-    const int jb = max(lo, 1);
-    const int bl1 = banded ? max(1, i1 - w) : 1;
-    const int bh1 = act1 ? (banded ? min(lc, i1 + w) : lc) : -1;
-    const int bl2 = banded ? max(1, i2 - w) : 1;
-    // an inactive second row simply follows the first (it never lives)
-    const int bh2 = act2 ? (banded ? min(lc, i2 + w) : lc) : lc + 64;
-    float top_prev = (lane == 0 && jb - 1 >= lo && jb - 1 <= hi) ? rowbuf[jb - 1] : INF;
-    int j = jb - lane;
-    const float* qp = qsp + j;
-    float* rp = rowbuf + j;
-    float v1 = INF, v2 = INF;
-    unsigned f1 = __ballot_sync(kFull, !act1), f2 = f1;
-    int jf1 = act1 ? lc + 1 : j - 1, jf2 = jf1;
-    const bool w1 = lane == wl && !wsecond, w2 = lane == wl && wsecond;
-    const bool is0 = lane == 0;
-    const unsigned span1 = static_cast<unsigned>(bh1 - bl1);
-    const unsigned span2 = static_cast<unsigned>(max(bh2 - bl2, 0));
-    int jr1 = j - bl1, jr2 = j - bl2;
-    int j0 = jb;  // lane 0's column (warp-uniform)
-
-    auto step = [&](int u) {
-      const float sh = __shfl_up_sync(kFull, v2, 1);
-      const float top = is0 ? rp[u] : sh;
-      const float diag = top_prev;
-      top_prev = top;
-      const float qj = qp[u];
-      const float e1 = __fsub_rn(c1, qj);
-      float n1 = __fadd_rn(__fmul_rn(e1, e1), fmin3f(v1, top, diag));
-      n1 = static_cast<unsigned>(jr1 + u) <= span1 ? n1 : INF;
-      const float e2 = __fsub_rn(c2, qj);
-      float n2 = __fadd_rn(__fmul_rn(e2, e2), fmin3f(v2, n1, v1));
-      n2 = static_cast<unsigned>(jr2 + u) <= span2 ? n2 : INF;
-      if (w1) rp[u] = n1;
-      if (w2) rp[u] = n2;
-      v1 = n1;
-      v2 = n2;
-      const unsigned d1 = __ballot_sync(kFull, n1 > t1);
-      const unsigned d2 = __ballot_sync(kFull, n2 > t2);
-      f1 |= d1 & ((f2 << 1) | (j0 + u > hi ? 1u : 0u));
-      f2 |= d2 & f1;
-    };
-
-    for (;;) {
-      const unsigned b1m = f1, b2m = f2;
-      step(0);
-      step(1);
-      step(2);
-      step(3);
-      f1 |= __ballot_sync(kFull, jr1 + 3 > static_cast<int>(span1));
-      f2 |= __ballot_sync(kFull, jr2 + 3 > static_cast<int>(span2)) & f1;
-      if (((f1 & ~b1m) >> lane) & 1u) jf1 = j + 3;
-      if (((f2 & ~b2m) >> lane) & 1u) jf2 = j + 3;
-      if (f2 == kFull) break;
-      j += 4;
-      jr1 += 4;
-      jr2 += 4;
-      j0 += 4;
-      qp += 4;
-      rp += 4;
-    }
-    const int wend = jb - wl + (j - (jb - lane)) + 3;
-    for (int k = max(wend + 1, 0) + lane; k <= written; k += 32) rowbuf[k] = INF;
-    written = min(max(wend, 0), lc + 1);
-    {
-      const int a0 = max(jb, bl1), a1c = min(jf1, bh1);
-      cnt += act1 && a1c >= a0 ? static_cast<unsigned>(a1c - a0 + 1) : 0u;
-      const int b0 = max(jb, bl2), b1c = min(jf2, bh2);
-      cnt += act2 && b1c >= b0 ? static_cast<unsigned>(b1c - b0 + 1) : 0u;
-    }
-    __syncwarp();
-    const int wcol1 = min(wend, lc);
-    int nlo = INT_MAX, nhi = -1;
-    for (int k0 = jb; k0 <= wcol1; k0 += 32) {
-      const int k = k0 + lane;
-      const bool lv = k <= wcol1 && rowbuf[k] <= ub_last;
-      const unsigned bm = __ballot_sync(kFull, lv);
-      if (bm) {
-        if (nlo == INT_MAX) nlo = k0 + __ffs(bm) - 1;
-        nhi = k0 + 31 - __clz(bm);
-      }
-    }
-    if (nhi < 0) {
-      lo = -1;
-      break;
-    }
-    lo = nlo;
-    hi = nhi;
-  }
   for (int off = 16; off > 0; off >>= 1) cnt += __shfl_xor_sync(kFull, cnt, off);
   if (lane == 0) cells += cnt;
   __syncwarp();

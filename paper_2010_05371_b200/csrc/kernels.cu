@@ -347,18 +347,8 @@ static __host__ __device__ inline size_t padded_len(int m, int ad_k) {
   return static_cast<size_t>(m) + 2 + 2 * static_cast<size_t>(smem_pad(ad_k));
 }
 
-// Lean layout (EAPDTW_SEARCH_LEAN): the per-warp shared buffer holds only the
-// FP32 engine's float row; the exact engine's row lives in global scratch
-// and there is no EQ staging, so three 8-warp blocks fit an SM.
-#ifndef EAPDTW_SEARCH_LEAN
-#define EAPDTW_SEARCH_LEAN 0
-#endif
 static __host__ __device__ inline size_t warp_buf_doubles(int m, int ad_k) {
-#if EAPDTW_SEARCH_LEAN
-  return (padded_len(m, ad_k) + 1) / 2;
-#else
   return padded_len(m, ad_k) + kStageExtra;
-#endif
 }
 
 size_t search_smem_bytes(int m, int warps, int ad_k) {
@@ -369,27 +359,7 @@ size_t search_smem_bytes(int m, int warps, int ad_k) {
          + 64;
 }
 
-// Strip engine rows per lane (1 or 2), set per launch through a constant.
-__constant__ int g_strip_rows = 1;
-
-cudaError_t set_strip_rows(cudaStream_t stream) {
-  int rows = 1;  // two rows per lane measured slower on the search configs
-  if (const char* env = getenv("EAPDTW_STRIP_ROWS")) {  // experiment override: 1 or 2
-    const int r = atoi(env);
-    if (r == 1 || r == 2) rows = r;
-  }
-  static thread_local int last = -1;
-  if (rows == last) return cudaSuccess;
-  last = rows;
-  return cudaMemcpyToSymbolAsync(g_strip_rows, &rows, sizeof(int), 0, cudaMemcpyHostToDevice,
-                                 stream);
-}
-
 int choose_ad_k(int n, int w) {
-  if (const char* env = getenv("EAPDTW_AD_K")) {  // experiment override: 0 (strip), 1, 3, 5
-    const int v = atoi(env);
-    if (v == 0 || v == 1 || v == 3 || v == 5) return v;
-  }
   // The anti-diagonal engine wins (1.25-1.45x per cell, scratch/engine
   // measurements in DESIGN.md) only when its window holds the whole band, so
   // it can never overflow; wider bands use the strip engine.
@@ -465,26 +435,11 @@ void debug_read_reset(unsigned long long* out8) {
 #ifndef EAPDTW_KIM_RSD
 #define EAPDTW_KIM_RSD 1  // Kim layers normalised by reciprocal multiplication
 #endif
-#ifndef EAPDTW_LB_F32
-#define EAPDTW_LB_F32 0  // LB_Keogh EQ/EC terms in FP32 (guarded; measured no faster)
-#endif
-#if EAPDTW_LB_F32
-using lbacc_t = float;
-#else
-using lbacc_t = double;
-#endif
-#ifndef EAPDTW_F32_ROWS
-#define EAPDTW_F32_ROWS 1
-#endif
 #ifndef EAPDTW_SEARCH_THREADS
 #define EAPDTW_SEARCH_THREADS 256
 #endif
 #ifndef EAPDTW_SEARCH_MIN_BLOCKS
-#if EAPDTW_SEARCH_LEAN
-#define EAPDTW_SEARCH_MIN_BLOCKS 3
-#else
 #define EAPDTW_SEARCH_MIN_BLOCKS 2
-#endif
 #endif
 constexpr int kSearchMinBlocks = EAPDTW_SEARCH_MIN_BLOCKS;
 
@@ -502,18 +457,11 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
   // for more resident warps.
   const double2* __restrict__ qul = p.qul;
   const double2* __restrict__ qperm = p.qperm;
-  const float2* __restrict__ qperm32 = p.qperm32;
   const int* __restrict__ order = p.order;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // per-warp buffer: the DTW row buffer, or the LB_Keogh EQ staging tile
   const size_t wlen = warp_buf_doubles(m, p.ad_k);
-#if EAPDTW_SEARCH_LEAN
-  double* rowbuf = p.dtw_scratch +
-                   (static_cast<size_t>(blockIdx.x) * (blockDim.x >> 5) + warp) * plen + pad;
-  float* rowbuf32 = reinterpret_cast<float*>(smem + plen + static_cast<size_t>(warp) * wlen) + pad;
-#else
   double* rowbuf = smem + plen + static_cast<size_t>(warp) * wlen + pad;
-#endif
   int* stacks = reinterpret_cast<int*>(smem + plen + static_cast<size_t>(blockDim.x >> 5) * wlen);
   // the query as float (FP32 screen), after the stacks; padded like qsp
   float* q32base = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(stacks) +
@@ -522,9 +470,7 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
   // The FP32 engine's row buffer aliases the warp's FP64 one (both engines
   // initialise [0, lc+1] on entry and never depend on the padding contents:
   // out-of-band cells are +inf by the band test).
-#if !EAPDTW_SEARCH_LEAN
   float* rowbuf32 = reinterpret_cast<float*>(rowbuf);
-#endif
 
   const double INF = d_inf();
   for (int k = threadIdx.x; k < static_cast<int>(plen); k += blockDim.x) {
@@ -594,7 +540,6 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
         p.guard_rel * tmax +
         8.0 * 0x1.0p-52 * (tmax + p.qmax * __dsqrt_rn(static_cast<double>(m) * tmax));
     double pre_eq = 0.0, pre_ec = 0.0;
-    int pre_end = -1;  // (2-rows-per-lane variant) prefixes cover [0, pre_end) once started
     // Row i's remaining cost: every path still visits every later row
     // (0-based positions >= i: EQ terms are per candidate position = row),
     // and every column past i+w (0-based >= i+w: EC terms are per query
@@ -652,66 +597,6 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
       const double t = __dsub_rn(__dmul_rn(u, 1.0 + p.guard_rel), cbv);
       return t > 0.0 ? t : 0.0;
     };
-#ifdef EAPDTW_SEARCH_STRIP2
-    // thresholds of a lane's two rows i0+2L, i0+2L+1 (positions k1 = kstrip +
-    // 2L, k2 = k1 + 1): prefix = pre + exclusive scan of the lane pairs
-    auto thr2 = [&](double u, int i0, double& t1, double& t2) {
-      t1 = u;
-      t2 = u;
-      const int kstrip = i0 + p.w - 1;
-      if (!tight || kstrip >= m - 1) return;
-      if (pre_end < 0) {  // positions before the first strip's k
-        pre_end = kstrip;
-        for (int k = lane; k < pre_end; k += 32) {
-          double a, b;
-          contrib(k, a, b);
-          pre_eq = __dadd_rn(pre_eq, a);
-          pre_ec = __dadd_rn(pre_ec, b);
-        }
-        for (int off = 16; off > 0; off >>= 1) {
-          pre_eq = __dadd_rn(pre_eq, __shfl_xor_sync(kFull, pre_eq, off));
-          pre_ec = __dadd_rn(pre_ec, __shfl_xor_sync(kFull, pre_ec, off));
-        }
-      }
-      const int k1 = kstrip + 2 * lane;
-      double a1 = 0.0, b1 = 0.0, a2 = 0.0, b2 = 0.0;
-      if (k1 < m) contrib(k1, a1, b1);
-      if (k1 + 1 < m) contrib(k1 + 1, a2, b2);
-      double sa = __dadd_rn(a1, a2), sb = __dadd_rn(b1, b2);
-      for (int off = 1; off < 32; off <<= 1) {  // inclusive scan of the pair sums
-        const double x = __shfl_up_sync(kFull, sa, off);
-        const double y = __shfl_up_sync(kFull, sb, off);
-        if (lane >= off) {
-          sa = __dadd_rn(sa, x);
-          sb = __dadd_rn(sb, y);
-        }
-      }
-      double ea = __shfl_up_sync(kFull, sa, 1), eb = __shfl_up_sync(kFull, sb, 1);
-      if (lane == 0) ea = eb = 0.0;
-      ea = __dadd_rn(pre_eq, ea);  // prefix through k1 - 1
-      eb = __dadd_rn(pre_ec, eb);
-      const double p1a = __dadd_rn(ea, a1), p1b = __dadd_rn(eb, b1);  // through k1
-      const double p2a = __dadd_rn(pre_eq, sa), p2b = __dadd_rn(pre_ec, sb);  // through k1 + 1
-      const int nxt = min(m, kstrip + 64);
-      const int src = (nxt - 1 - kstrip) >> 1;  // lane holding position nxt - 1 (its k1 or k1+1)
-      pre_eq = __shfl_sync(kFull, p2a, src);
-      pre_ec = __shfl_sync(kFull, p2b, src);
-      pre_end = nxt;
-      auto thr = [&](double pa, double pb, int kk) -> double {
-        if (kk >= m - 1) return u;  // nothing left past k
-        const double cbv = __dsub_rn(fmax(__dsub_rn(teq, pa), __dsub_rn(tec, pb)), cb_guard);
-        if (!(cbv > 0.0)) return u;
-        const double t = __dsub_rn(__dmul_rn(u, 1.0 + p.guard_rel), cbv);
-        return t > 0.0 ? t : 0.0;
-      };
-      t1 = thr(p1a, p1b, k1);
-      t2 = thr(p2a, p2b, k1 + 1);
-    };
-    const double d = AD_K == 0
-                         ? warp_dtw2(rowraw, rownorm, m, qsp, m, p.w, get_ub, thr2, rowbuf, c_cells)
-                         : dtw_dispatch<false>(AD_K, rowraw, rownorm, m, qsp, m, p.w, get_ub,
-                                               rowthr, rowbuf, c_cells, c_ovf);
-#else
     // FP32 screen first (dtw_f32.cuh) once a finite threshold exists: it
     // abandons with a sound, error-inflated threshold; whatever it cannot
     // abandon is evaluated exactly below.
@@ -725,13 +610,8 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
         return f32_threshold(rowthr(u, i, i0), g);
       };
       int st = 0;
-#if EAPDTW_F32_ROWS == 2  // two rows per lane (experiment)
-      const float r32 = warp_dtw2_f32(rowraw, rownorm32, m, qsp32, m, p.w, p.f32_cmax, get_ub,
-                                      rowthr32, rowbuf32, c_cells32, st);
-#else
       const float r32 = warp_dtw_f32<kSearchStepBlock>(rowraw, rownorm32, m, qsp32, m, p.w, p.f32_cmax, get_ub,
                                      rowthr32, rowbuf32, c_cells32, st);
-#endif
       screened = st == 0 && r32 == f_inf();
       // the cumulative-bound prefixes restart for the exact pass
       pre_eq = pre_ec = 0.0;
@@ -741,7 +621,6 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
     const double d = screened ? INF
                               : dtw_dispatch<false>(AD_K, rowraw, rownorm, m, qsp, m, p.w, get_ub,
                                                     rowthr, rowbuf, c_cells, c_ovf);
-#endif
     ++c_calls;
     if (d == INF) {
       ++c_aband;
@@ -1043,35 +922,11 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
       //   EC: query value vs the candidate's (global raw) envelope, normalised.
       // Lanes without a candidate point at p.begin: loads stay in bounds.
       auto lb_range = [&](auto ec_tag, const double* xs, long long s, bool pending,
-                          const double mean, const double rsd, lbacc_t ubg, int k0, int k1,
-                          lbacc_t& acc) -> bool {
+                          const double mean, const double rsd, double ubg, int k0, int k1,
+                          double& acc) -> bool {
         constexpr bool EC = decltype(ec_tag)::value;
         bool alive = pending;
         const double2* es = EC ? p.env + s : nullptr;
-#if EAPDTW_LB_F32
-        // FP32 terms (guarded like the FP32 DTW screen, dtw_f32.cuh): the
-        // centring x - mean stays FP64 (no cancellation), the rest is FP32;
-        // U >= L, so at most one of a - U, L - a is positive: max3 with 0.
-        const float rsdf = __double2float_rn(rsd);
-        auto term = [&](int k) {
-          const int j = order[k];
-          float a, U, L;
-          if (!EC) {
-            const float2 b = qperm32[k];
-            a = __fmul_rn(__double2float_rn(__dsub_rn(xs[j], mean)), rsdf);
-            U = b.x;
-            L = b.y;
-          } else {
-            const double2 e = es[j];
-            a = qsp32[j + 1];
-            U = __fmul_rn(__double2float_rn(__dsub_rn(e.x, mean)), rsdf);
-            L = __fmul_rn(__double2float_rn(__dsub_rn(e.y, mean)), rsdf);
-          }
-          float dd;
-          asm("max.f32 %0, %1, %2, %3;" : "=f"(dd) : "f"(__fsub_rn(a, U)), "f"(__fsub_rn(L, a)), "f"(0.0f));
-          acc = __fmaf_rn(dd, dd, acc);
-        };
-#else
         auto term = [&](int k) {
           const int j = order[k];
           double a, U, L;
@@ -1090,7 +945,6 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
           const double dd = e1 > 0.0 ? e1 : (e2 > 0.0 ? e2 : 0.0);
           acc = __dadd_rn(acc, __dmul_rn(dd, dd));
         };
-#endif
         // groups of kLbGroup positions: all their loads are in flight together
         for (int kb = k0; kb < k1; kb += kLbGroup) {
           if (kb + kLbGroup <= k1) {
@@ -1128,16 +982,11 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
           pending = leg2 ? pop(stkB2, nB2, s, accB2, acc_d, teqB2, teq, nullptr, unused2)
                          : pop(stkB, nB, s, nullptr, acc_d, teqB, teq, nullptr, unused2);
         }
-        lbacc_t acc = static_cast<lbacc_t>(acc_d);  // a leg-2 partial sum (exact in float mode)
+        double acc = acc_d;  // a leg-2 partial sum
         const double mean = p.mean[s];
         const double sd = p.sd[s];
         const double rsd = sd < kMinStddev ? 0.0 : __drcp_rn(sd);
-#if EAPDTW_LB_F32
-        const F32Guard glb{p.lb32_a, p.lb32_b};
-        const float ubg = f32_threshold(lb_guard(p, load_ub(p.ub_key)), glb);
-#else
         const double ubg = lb_guard(p, load_ub(p.ub_key));
-#endif
         // EQ: stage the batch's stretch of the reference in the warp's buffer
         // when it fits, so the order[]-permuted reads hit shared memory
         // instead of L2 (the DP row buffer is free between DTW tasks).
@@ -1154,7 +1003,7 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
           if (lane == 0) atomicAdd(&p.counters[hi >= lo && len <= static_cast<long long>(wlen)
                                                    ? kStageHit : kStageMiss], 1ull);
 #endif
-          if (!EAPDTW_SEARCH_LEAN && hi >= lo && len <= static_cast<long long>(wlen)) {
+          if (hi >= lo && len <= static_cast<long long>(wlen)) {
             double* sbuf = rowbuf - pad;
             const double* src = ref + p.begin + lo;
             for (int t = lane; t < static_cast<int>(len); t += 32) sbuf[t] = src[t];
@@ -1169,13 +1018,7 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
           if (EC) ++c_ec;
           else ++c_eq;
         }
-#if EAPDTW_LB_F32
-        // a sound lower bound on the exact total (the cumulative-bound rows
-        // subtract FP64 prefixes from it)
-        const float tot = f32_lower(acc, glb);
-#else
         const float tot = __double2float_rz(acc);  // rounded down: a weaker, sound total
-#endif
         if (!leg2 && head < m) {
           if (EC) push(stkB2, nB2, alive, s, accB2, acc, teqB2, teq, nullptr, z2);
           else push(stkA2, nA2, alive, s, accA2, acc, nullptr, 0.0f, nullptr, z2);
@@ -1439,10 +1282,6 @@ cudaError_t launch_rank_select(const SearchParams& p, long long S, int wave, lon
 }
 
 int search_blocks_per_sm_by_regs() { return kSearchMinBlocks; }
-
-size_t search_scratch_doubles(int m, int blocks, int warps, int ad_k) {
-  return EAPDTW_SEARCH_LEAN ? static_cast<size_t>(blocks) * warps * padded_len(m, ad_k) : 0;
-}
 
 cudaError_t launch_search(const SearchParams& p, int blocks, int warps, cudaStream_t stream) {
   const size_t smem = search_smem_bytes(p.m, warps, p.ad_k);

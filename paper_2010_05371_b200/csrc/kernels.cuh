@@ -65,7 +65,6 @@ struct SearchParams {
   const double* q;       // normalised query, 1-based: q[1..m] (q[0] unused)
   const double2* qul;    // query envelope (upper, lower) per position, 0-based
   const double2* qperm;  // the same in visiting order: qperm[k] = qul[order[k]]
-  const float2* qperm32; // ... as float (FP32 Keogh tiers)
   const int* order;      // Keogh visiting order (search.cpp:143-149)
   long long ncand;
   long long begin, end, stride;  // candidates begin, begin+stride, ... < end
@@ -92,7 +91,6 @@ struct SearchParams {
   int screen_rows;               // phase-A lane screen depth (0: off)
   int use_f32;                   // FP32 screening engine ahead of the exact FP64 one
   float f32_a, f32_b, f32_cmax;  // its threshold guard (dtw_f32.cuh) and row-value bound
-  float lb32_a, lb32_b;          // guard of the FP32 Keogh tiers (same form)
   unsigned long long* counters;  // kNumCounters
   long long index_offset;        // shard start in the global reference
   // list mode (rank pass): chunk c covers list[32c .. 32c+31] (candidate
@@ -101,11 +99,9 @@ struct SearchParams {
   const unsigned long long* nlist;
   long long list_cap;            // entries past it were not written
   int ub_only;                   // results tighten the threshold only (no record update)
-  double* dtw_scratch;           // lean layout: the exact engine's row per warp (global)
 };
 // Resident 8-warp search blocks per SM the kernel's register budget allows.
 int search_blocks_per_sm_by_regs();
-size_t search_scratch_doubles(int m, int blocks, int warps, int ad_k);
 
 struct PairParams {
   const double* rows;  // npairs x lr (row-major, pair p at p*row_stride)
@@ -152,8 +148,6 @@ size_t search_smem_bytes(int m, int warps, int ad_k);
 // over series of length n: the smallest of 1/3/5 whose window 64K covers
 // the band, else 5 (odd K keeps shared-memory reads conflict-free).
 int choose_ad_k(int n, int w);
-// Rows per lane of the strip engine (EAPDTW_STRIP_ROWS=1 or 2; default 1).
-cudaError_t set_strip_rows(cudaStream_t stream);
 cudaError_t launch_search(const SearchParams& p, int blocks, int warps, cudaStream_t stream);
 // Rank pass (the threshold's warm start): the layered LB_Kim of every S-th
 // candidate of [p.begin, p.end), then the candidates whose bound is among the

@@ -46,6 +46,29 @@ def double_of(k: int) -> float:
 INF_KEY = key_of(math.inf)
 
 
+def all_reduce_min(t, group=None):
+    """In-place MIN all-reduce.  Under gloo a CUDA tensor goes through a host
+    copy (ordered on torch's current stream); NCCL reduces it in place."""
+    import torch.distributed as dist
+    if t.is_cuda and dist.get_backend(group) == "gloo":
+        c = t.cpu()
+        dist.all_reduce(c, op=dist.ReduceOp.MIN, group=group)
+        t.copy_(c)
+    else:
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+
+
+def all_gather(t, world, group=None):
+    """all_gather of one tensor per rank (host copies under gloo)."""
+    import torch
+    import torch.distributed as dist
+    if t.is_cuda and dist.get_backend(group) == "gloo":
+        t = t.cpu()
+    out = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(out, t, group=group)
+    return out
+
+
 def lexicographic_min(records):
     """records: iterable of (found, distance, global_location)."""
     best = (False, math.inf, 0)
@@ -58,12 +81,22 @@ def lexicographic_min(records):
 
 
 class GpuShard:
-    """Backend over the C-ABI search plan for one shard (device-resident)."""
+    """Backend over the C-ABI search plan for one shard (device-resident).
+
+    The plan's context runs on torch's current stream of the key's device, so
+    the kernels, the key's fill, the collectives on the key (NCCL waits on
+    that stream) and any host copy of it are ordered with one another."""
 
     def __init__(self, ref_shard_dev_ptr: int, n_points: int, query, cfg, global_offset: int,
                  key_tensor, ctx=None):
-        from .api import SearchPlan
-        self.plan = SearchPlan(ref_shard_dev_ptr, n_points, query, cfg, global_offset, ctx=ctx)
+        import torch
+
+        from .api import Context, SearchPlan
+        self.own_ctx = ctx is None
+        self.ctx = ctx or Context(key_tensor.device.index or 0)
+        self.ctx.set_stream(torch.cuda.current_stream(key_tensor.device).cuda_stream)
+        self.plan = SearchPlan(ref_shard_dev_ptr, n_points, query, cfg, global_offset,
+                               ctx=self.ctx)
         self.key = key_tensor
         self.plan.set_ub_key(key_tensor.data_ptr())
 
@@ -83,6 +116,11 @@ class GpuShard:
 
     def result(self):
         return self.plan.result()
+
+    def close(self):
+        self.plan.close()
+        if self.own_ctx:
+            self.ctx.close()
 
 
 class ShardedSearch:
@@ -104,26 +142,24 @@ class ShardedSearch:
         edges = np.linspace(0, nc, self.batches + 1).astype(np.int64)
         if self.world > 1:
             # share the probe phase's best before the sweep starts
-            dist.all_reduce(b.key, op=dist.ReduceOp.MIN, group=self.group)
+            all_reduce_min(b.key, self.group)
         for k in range(self.batches):
             b.run(int(edges[k]), int(edges[k + 1]))
             if self.world > 1:
-                dist.all_reduce(b.key, op=dist.ReduceOp.MIN, group=self.group)
+                all_reduce_min(b.key, self.group)
         res = b.result()
         return self.finalize(res)
 
     def finalize(self, res):
         """Lexicographic (distance, lowest global index) across ranks."""
         import torch
-        import torch.distributed as dist
         mine = (bool(res.best.found), float(res.best.distance_sq), int(res.best.location))
         if self.world == 1:
             return mine, res
         dev = self.backend.key.device
         t = torch.tensor([key_of(mine[1]) if mine[0] else INF_KEY, mine[2], int(mine[0])],
                          dtype=torch.int64, device=dev)
-        out = [torch.empty_like(t) for _ in range(self.world)]
-        dist.all_gather(out, t, group=self.group)
+        out = all_gather(t, self.world, self.group)
         recs = [(bool(o[2].item()), double_of(o[0].item()), int(o[1].item())) for o in out]
         return lexicographic_min(recs), res
 
@@ -201,7 +237,6 @@ class ShardedNN1:
 
     def search(self):
         import torch
-        import torch.distributed as dist
         b = self.backend
         nq = b.nq
         best_d = np.full(nq, math.inf)
@@ -215,13 +250,12 @@ class ShardedNN1:
                 merge_nn1(best_d, best_i, d, arg + self.offset + b0)
             cutoff = torch.from_numpy(best_d.copy()).to(cutoff.device)
             if self.world > 1:
-                dist.all_reduce(cutoff, op=dist.ReduceOp.MIN, group=self.group)
+                all_reduce_min(cutoff, self.group)
         if self.world == 1:
             return best_i, best_d
         mine = torch.stack([torch.from_numpy(best_d).view(torch.int64),
                             torch.from_numpy(best_i)]).to(cutoff.device)
-        parts = [torch.empty_like(mine) for _ in range(self.world)]
-        dist.all_gather(parts, mine, group=self.group)
+        parts = all_gather(mine, self.world, self.group)
         out_d = np.full(nq, math.inf)
         out_i = np.zeros(nq, dtype=np.int64)
         for p in parts:  # rank order = global index order

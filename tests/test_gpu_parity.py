@@ -353,24 +353,21 @@ def test_engines_long_series_vs_oracle(gpu, oracle_lib):
         assert np.array_equal(got, want), w
 
 
-@pytest.mark.parametrize("ad_k,screen,strip", [("0", "0", "1"), ("1", "8", "2"), ("3", "16", "1"),
-                                               ("5", "32", "2"), ("0", "64", "2"),
-                                               ("3", "48", "2"), ("0", "16", "1")])
-def test_engine_and_screen_variants(gpu, oracle_lib, monkeypatch, ad_k, screen, strip):
-    """Every DTW engine (strip with 1 or 2 rows per lane, anti-diagonal K=1/3/5)
-    and phase-A screen depth gives the oracle's exact answer, with and without
-    the cascade."""
-    monkeypatch.setenv("EAPDTW_AD_K", ad_k)
-    monkeypatch.setenv("EAPDTW_SCREEN_ROWS", screen)
-    monkeypatch.setenv("EAPDTW_STRIP_ROWS", strip)
+@pytest.mark.parametrize("ad_k,screen", [(0, 0), (1, 8), (3, 16), (5, 32), (0, 64), (3, 48),
+                                          (0, 16)])
+def test_engine_and_screen_variants(gpu, oracle_lib, ad_k, screen):
+    """Every exact DTW engine (strip, anti-diagonal K=1/3/5) and phase-A screen
+    depth gives the oracle's exact answer, with and without the cascade."""
+    ctx = gpu.default_context()
     for n, m, ratio, seed in [(60_000, 96, 0.1, 1), (40_000, 200, 0.3, 2), (30_000, 64, 1.0, 3),
                               (50_000, 128, 0.05, 4)]:
         ref = gpu.random_walk_normal(n, 100 + seed)
         q = gpu.random_walk_normal(m, 200 + seed)
         want = oracle_lib.similarity_search(ref, q, ratio)
         for lb in (True, False):
-            got = gpu.similarity_search(ref, q, gpu.SearchConfig(window_ratio=ratio,
-                                                                 use_lower_bounds=lb))
+            with ctx.options(ad_k=ad_k, screen_rows=screen):
+                got = gpu.similarity_search(ref, q, gpu.SearchConfig(window_ratio=ratio,
+                                                                     use_lower_bounds=lb))
             assert (got.best.location, got.best.distance_sq) == (want.location,
                                                                  want.distance_sq), (n, m, lb)
             rep = got.report
@@ -416,7 +413,7 @@ def test_tighten_ub_never_changes_the_result(gpu, oracle_lib, m, ratio):
 @pytest.mark.gpu
 @pytest.mark.parametrize("n,m,ratio,lb", [(450_000, 128, 0.1, True), (1_234_567, 300, 0.2, True),
                                           (700_001, 64, 0.05, False), (1_500_000, 256, 0.2, True)])
-def test_streamed_host_search_equals_device_search(gpu, oracle_lib, monkeypatch, n, m, ratio, lb):
+def test_streamed_host_search_equals_device_search(gpu, oracle_lib, n, m, ratio, lb):
     """The host-pointer search streams long references in two parts (the second
     part's copy under the first part's sweep): same answer as the oracle and as
     the unstreamed path, including a best match planted in each part."""
@@ -428,10 +425,11 @@ def test_streamed_host_search_equals_device_search(gpu, oracle_lib, monkeypatch,
         if plant is not None:
             r[plant:plant + m] = q * 2.0 - 1.0
         want = oracle_lib.similarity_search(r, q, ratio, use_lb=lb, tighten=lb)
-        monkeypatch.setenv("EAPDTW_STREAMED", "1")
-        got = gpu.similarity_search(r, q, cfg)
-        monkeypatch.setenv("EAPDTW_STREAMED", "0")
-        plain = gpu.similarity_search(r, q, cfg)
+        ctx = gpu.default_context()
+        with ctx.options(streamed=1):
+            got = gpu.similarity_search(r, q, cfg)
+        with ctx.options(streamed=0):
+            plain = gpu.similarity_search(r, q, cfg)
         assert (got.best.location, got.best.distance_sq) == (want.location, want.distance_sq)
         assert (plain.best.location, plain.best.distance_sq) == (want.location, want.distance_sq)
         assert got.report.candidates_total == n - m + 1
@@ -440,9 +438,9 @@ def test_streamed_host_search_equals_device_search(gpu, oracle_lib, monkeypatch,
 @pytest.mark.gpu
 @pytest.mark.parametrize("n,m,ratio,lb", [(300_000, 128, 0.05, True), (200_000, 512, 0.1, False),
                                           (150_000, 1024, 0.2, True), (60_000, 257, 1.0, True)])
-def test_fp32_screen_never_changes_the_result(gpu, oracle_lib, monkeypatch, n, m, ratio, lb):
+def test_fp32_screen_never_changes_the_result(gpu, oracle_lib, n, m, ratio, lb):
     """The FP32 screening engine (dtw_f32.cuh) only abandons with an
-    error-inflated threshold: with it (default) and without it (EAPDTW_F32=0)
+    error-inflated threshold: with it (default) and without it (option f32=0)
     the search returns the oracle's (location, d) bit for bit, including
     planted near-ties whose DTW differs from the best by far less than the
     FP32 guard."""
@@ -456,11 +454,11 @@ def test_fp32_screen_never_changes_the_result(gpu, oracle_lib, monkeypatch, n, m
     for arr in (ref, r):
         want = oracle_lib.similarity_search(arr, q, ratio, use_lb=lb, tighten=lb)
         cfg = gpu.SearchConfig(window_ratio=ratio, use_lower_bounds=lb, tighten_ub=lb)
-        monkeypatch.setenv("EAPDTW_F32", "1")
-        on = gpu.similarity_search(arr, q, cfg)
-        monkeypatch.setenv("EAPDTW_F32", "0")
-        off = gpu.similarity_search(arr, q, cfg)
-        monkeypatch.delenv("EAPDTW_F32")
+        ctx = gpu.default_context()
+        with ctx.options(f32=1):
+            on = gpu.similarity_search(arr, q, cfg)
+        with ctx.options(f32=0):
+            off = gpu.similarity_search(arr, q, cfg)
         assert (on.best.location, on.best.distance_sq) == (want.location, want.distance_sq)
         assert (off.best.location, off.best.distance_sq) == (want.location, want.distance_sq)
 
@@ -484,8 +482,8 @@ def test_fp32_screen_falls_back_on_large_values(gpu, reference_lib_optional):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("rank", ["0", "16:16384", "4:512", "8:64:3"])
-def test_warm_start_never_changes_the_result(gpu, oracle_lib, monkeypatch, rank):
+@pytest.mark.parametrize("rank", [(0, 16384, 1), (16, 16384, 1), (4, 512, 1), (8, 64, 3)])
+def test_warm_start_never_changes_the_result(gpu, oracle_lib, rank):
     """The warm start (probe, rank pass with its list mode and waves, coarse
     pass) only changes the order in which candidates are tried: the answer is
     the oracle's, with the best match planted where the rank pass does not
@@ -497,10 +495,11 @@ def test_warm_start_never_changes_the_result(gpu, oracle_lib, monkeypatch, rank)
     r[123_457:123_457 + m] = q * 0.5 + 3.0   # exact z-normalised copy (d = 0)
     r[300_001:300_001 + m] = q * 2.0 - 1.0   # a second copy: tie, higher index
     want = oracle_lib.similarity_search(r, q, ratio)
-    monkeypatch.setenv("EAPDTW_RANK", rank)
-    for coarse in ("0", "64"):
-        monkeypatch.setenv("EAPDTW_COARSE_STRIDE", coarse)
-        got = gpu.similarity_search(r, q, gpu.SearchConfig(window_ratio=ratio))
+    ctx = gpu.default_context()
+    for coarse in (0, 64):
+        with ctx.options(rank_stride=rank[0], rank_k=rank[1], rank_waves=rank[2],
+                         coarse_stride=coarse):
+            got = gpu.similarity_search(r, q, gpu.SearchConfig(window_ratio=ratio))
         assert (got.best.location, got.best.distance_sq) == (want.location, want.distance_sq)
         rep = got.report
         assert rep.candidates_total == n - m + 1
@@ -527,3 +526,35 @@ def test_baseline_configs_full_size_vs_reference(gpu, name):
     with gpu.DeviceSeries(ref) as dref:
         got2 = dref.search(q, cfg)
     assert (got2.best.location, got2.best.distance_sq) == want
+
+
+NN1_GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "nn1_cfg5_golden.json")
+
+
+@pytest.mark.skipif(not os.path.exists(NN1_GOLDEN), reason="cfg5 golden not generated")
+def test_nn1_cfg5_full_size_vs_reference(gpu):
+    """cfg5 at its BASELINE size: all 1000 queries x 20000 series x 512,
+    unbounded band, against the unmodified reference's running-cutoff loop
+    (tests/golden/make_nn1_golden.py): every argmin and distance bit, through
+    the host API and through device-resident inputs."""
+    import importlib.util
+    import torch
+    spec = importlib.util.spec_from_file_location(
+        "make_nn1_golden", os.path.join(os.path.dirname(__file__), "golden", "make_nn1_golden.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    gold = json.load(open(NN1_GOLDEN))
+    qs, db = mod.cfg5_inputs(gpu.znormalize)
+    want_arg = np.array(gold["argmin"], dtype=np.uint64)
+    want_d = np.array([fbits(h) for h in gold["distance_sq"]])
+    arg, dist, _ = gpu.nn1(qs, db)
+    assert np.array_equal(np.asarray(arg, dtype=np.uint64), want_arg)
+    assert np.array_equal(dist.view(np.uint64), want_d.view(np.uint64))
+    # the same through the sharded batch path on one GPU (cutoffs carried
+    # between database batches, lexicographic merge)
+    from paper_2010_05371_b200.sharded import GpuNN1Shard, ShardedNN1
+    dq, ddb = torch.from_numpy(qs).cuda(), torch.from_numpy(db).cuda()
+    sh = ShardedNN1(GpuNN1Shard(dq, ddb), 0, 1, 0, batches=3, device=dq.device)
+    ai, ad = sh.search()
+    assert np.array_equal(np.asarray(ai, dtype=np.uint64), want_arg)
+    assert np.array_equal(ad.view(np.uint64), want_d.view(np.uint64))

@@ -155,3 +155,18 @@ def test_sliding_stats_chain(oracle_lib):
         mu = sm / 64
         assert mean[s] == mu
     assert np.allclose(mean, np.convolve(ref, np.ones(64) / 64, "valid"), rtol=1e-9, atol=1e-6)
+
+
+def test_oracle_generator_equals_product_generator():
+    """bench.py's reference arm generates its inputs with the oracle's copy of
+    the benchmark generator (it must not load the product library): same bits
+    as eapdtw_random_walk_normal (host code, no GPU needed)."""
+    import numpy as np
+
+    import oracle
+    from paper_2010_05371_b200 import random_walk_normal
+    o = oracle.Oracle()
+    for n, seed in [(1, 3), (2, 5), (1001, 20261019), (1_000_003, 20261020)]:
+        a = o.random_walk_normal(n, seed)
+        b = random_walk_normal(n, seed)
+        assert np.array_equal(a.view(np.uint64), b.view(np.uint64)), (n, seed)

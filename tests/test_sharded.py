@@ -240,3 +240,67 @@ def test_gpu_nn1_shard_batches_and_cutoffs(oracle_lib):
     a3, d3 = shard.run(0, nd, below)
     assert np.isinf(d3[np.asarray(want_d) > 0]).all()
     ctx.close()
+
+
+# --- the same host logic on real kernels: 2 gloo ranks sharing cuda:0 -----------
+# The ranks' kernels never wait on one another (the exchange happens on the
+# host between launches), so two processes on one GPU are safe here.
+
+def _gpu_worker(rank, world, port, ref, q, m, ratio, qs, db, out):
+    import paper_2010_05371_b200 as g
+    from paper_2010_05371_b200.sharded import (GpuNN1Shard, GpuShard, ShardedNN1,
+                                               db_shard_bounds)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        ncand = ref.size - m + 1
+        s0, s1 = shard_bounds(ncand, world, rank)
+        dref = torch.from_numpy(ref[s0:s1 + m - 1].copy()).cuda()
+        key = torch.full((1,), INF_KEY, dtype=torch.int64, device="cuda")
+        shard = GpuShard(dref.data_ptr(), dref.numel(), q, g.SearchConfig(window_ratio=ratio),
+                         s0, key)
+        best, _ = ShardedSearch(shard, rank, world, batches=4).search()
+        shard.close()
+        d0, d1 = db_shard_bounds(db.shape[0], world, rank)
+        nshard = GpuNN1Shard(torch.from_numpy(qs).cuda(), torch.from_numpy(db[d0:d1].copy()).cuda())
+        arg, d = ShardedNN1(nshard, rank, world, d0, batches=3, device="cuda").search()
+        out[rank] = (best, int(key.item()), arg.tolist(), d.tolist())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(600)
+def test_two_rank_gpu_shards_equal_oracle(oracle_lib):
+    """cfg2-size search (N=1e6, m=128, w=6%) split over 2 ranks on cuda:0,
+    GpuShard + ShardedSearch with the key all-reduced between 4 batches, and a
+    2-rank GpuNN1Shard + ShardedNN1 with cutoffs carried between batches: both
+    equal the oracle (ties across ranks to the lowest global index)."""
+    from paper_2010_05371_b200 import random_walk_normal, znormalize
+    ref = random_walk_normal(1_000_000, 7)
+    q = random_walk_normal(128, 8)
+    m, ratio = 128, 0.05
+    ref[850_001:850_001 + m] = q * 1.7 - 0.2   # exact copy in rank 1's shard ...
+    ref[250_003:250_003 + m] = q * 0.3 + 4.0   # ... and a lower-index one in rank 0's
+    want = oracle_lib.similarity_search(ref, q, ratio)
+    assert want.distance_sq == 0.0 and want.location == 250_003
+    rng = np.random.default_rng(9)
+    L = 96
+    qs = np.stack([znormalize(np.cumsum(rng.standard_normal(L))) for _ in range(12)])
+    db = np.stack([znormalize(np.cumsum(rng.standard_normal(L))) for _ in range(2000)])
+    db[1500] = qs[2]
+    db[300] = qs[2]
+    want_arg, want_d, _ = oracle_lib.nn1(qs, db)
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_gpu_worker, args=(2, _free_port(), ref, q, m, ratio, qs, db, out), nprocs=2,
+             join=True)
+    for rank in (0, 1):
+        best, key, arg, d = out[rank]
+        assert best == (True, 0.0, 250_003)
+        assert key == key_of(0.0)
+        assert arg == [int(x) for x in want_arg]
+        assert d == [float(x) for x in want_d]
+        assert arg[2] == 300
