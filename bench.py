@@ -304,6 +304,12 @@ def run_reference_arm(args, cfgname):
     return 0
 
 
+def apply_opts(ctx, args):
+    for kv in args.opt:
+        k, v = kv.split("=", 1)
+        ctx.set_option(k, int(v))
+
+
 def committed_ncu(cfg):
     """(DRAM bytes per launch, pipe/issue utilisation) of cfg's dominant kernel
     from the committed ncu capture (profiles/summarize.py report ... cfg)."""
@@ -384,6 +390,7 @@ def run_batch(args):
         print(json.dumps(line), flush=True)
         return 0
     ctx = g.Context(0)
+    apply_opts(ctx, args)
     # e2e inputs come from pinned host memory (the contract's H2D), as for cfg2-4
     if cfg == "cfg1":
         a = torch.from_numpy(a).pin_memory().numpy()
@@ -677,6 +684,8 @@ def main():
     ap.add_argument("--config", default="cfg4", choices=sorted(CONFIGS) + sorted(BATCH_CONFIGS) + ["grid"])
     ap.add_argument("--batches", type=int, default=8, help="best-so-far exchanges per search (N>1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--opt", action="append", default=[], metavar="NAME=VALUE",
+                    help="engine option of the context (eapdtw_ctx_set_option), for experiments")
     ap.add_argument("--shard-nn1", action="store_true",
                     help="cfg5: the sharded driver (batches + cutoff all-reduce) even at N=1")
     args = ap.parse_args()
@@ -713,6 +722,7 @@ def main():
     npts = (s1 - s0) + m - 1
 
     ctx = g.Context(local)
+    apply_opts(ctx, args)
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
     fp64_peak = ctx.fp64_peak()  # measured DADD issue rate (ops/s) on this GPU

@@ -73,6 +73,7 @@ enum Opt : int {
   kOptNn1Splits,      // NN1 blocks per query (0: auto)
   kOptNn1Warm,        // NN1 per-warp warm start
   kOptSeriesCache,    // device-resident series keep their last stats
+  kOptProbeStrips,    // FP32 strip screen: strips probed in each direction before committing (0: forward only)
   kNumOpts
 };
 struct OptDef {
@@ -87,6 +88,7 @@ constexpr OptDef kOpts[kNumOpts] = {
     {"coarse_stride", 0, 0, 1 << 20}, {"probe", 2048, 1, 1 << 24}, {"probe_force", 0, 0, 1},
     {"tighten", 1, 0, 1},         {"cb_strip", 1, 1, 1 << 16},  {"warps", 0, 0, 8},
     {"nn1_splits", 0, 0, 1 << 16}, {"nn1_warm", 1, 0, 1},       {"series_cache", 1, 0, 1},
+    {"probe_strips", 1, 0, 8},
 };
 
 // Grow-only device buffer.
@@ -577,6 +579,7 @@ static int plan_init(eapdtw_search_plan* p, eapdtw_ctx* c, const double* ref_dev
   // opt-in here (EAPDTW_AD_K) and the default for pairwise / NN1 batches.
   p->ad_k = o[kOptAdK] > 0 ? static_cast<int>(o[kOptAdK]) : 0;
   p->screen_rows = static_cast<int>(o[kOptScreenRows]);
+
   p->use_f32 = static_cast<int>(o[kOptF32]);
   p->coarse_stride = static_cast<int>(o[kOptCoarseStride]);
   p->probe = static_cast<int>(o[kOptProbe]);
@@ -784,6 +787,7 @@ static SearchParams base_params(eapdtw_search_plan* p) {
   s.ad_k = p->ad_k;
   s.direct = 0;
   s.screen_rows = p->screen_rows;
+  s.probe_strips = static_cast<int>(p->ctx->opt[kOptProbeStrips]);
   {
     // z-normalised rows satisfy |c| <= sqrt(m - 1); the engine checks the
     // bound per strip (degenerate statistics fall back to the exact engine)
@@ -1036,10 +1040,11 @@ int eapdtw_search_plan_result(eapdtw_search_plan* p, eapdtw_search_result* out) 
                  cnt[kCntCells], cnt[kCntCellsF32], (cnt[kCntCells] + cnt[kCntCellsF32]) / (32.0 * dbg[0] + 1));
   }
   std::fprintf(stderr,
-               "phase warp-Gcycles: dtw %.3f eq %.3f ec %.3f screen %.3f kim %.3f | stage hit %llu miss "
-               "%llu\n",
-               cnt[kClkDtw] * 1e-9, cnt[kClkEq] * 1e-9, cnt[kClkEc] * 1e-9,
-               cnt[kClkScreen] * 1e-9, cnt[kClkKim] * 1e-9, cnt[kStageHit], cnt[kStageMiss]);
+               "phase warp-Gcycles: total %.3f dtw %.3f eq %.3f ec %.3f screen %.3f kim %.3f wait %.3f | "
+               "stage hit %llu miss %llu\n",
+               cnt[kClkTotal] * 1e-9, cnt[kClkDtw] * 1e-9, cnt[kClkEq] * 1e-9, cnt[kClkEc] * 1e-9,
+               cnt[kClkScreen] * 1e-9, cnt[kClkKim] * 1e-9, cnt[kClkWait] * 1e-9, cnt[kStageHit],
+               cnt[kStageMiss]);
 #endif
   return EAPDTW_OK;
 }
@@ -1405,6 +1410,7 @@ static int nn1_impl(eapdtw_ctx* c, const double* q_dev, size_t nq, const double*
   p.guard_rel = std::max(1e-9, 8.0 * static_cast<double>(len) * 0x1.0p-53);
   p.guard_abs = 1e-20;
   p.warm = static_cast<int>(c->opt[kOptNn1Warm]);
+  p.probe_strips = static_cast<int>(c->opt[kOptProbeStrips]);
   CUDA_TRY(launch_nn1(p, s));
   ++c->launches;
   std::vector<BestRecord> rec(nq);

@@ -85,13 +85,18 @@ __device__ __forceinline__ float f32_lower(float x, F32Guard g) {
 constexpr int kF32Undecided = 1;  // a row value exceeded cmax: run the FP64 engine
 
 // FP32 screening strip engine: the schedule of warp_dtw<false> (dtw_warp.cuh)
-// on floats.  Returns the FP32 value (<= its threshold) or +inf (proven > ub);
-// status = kF32Undecided when a row value exceeded cmax (result meaningless).
+// on floats, resumable strip by strip (F32Strip holds the state between
+// strips), so a caller can probe a pair in both directions (f32_probe_pair).
 //   rowraw(k)  : raw value of row k (0-based); loaded one strip ahead
 //   rownorm(x) : the row value as float (|value| <= cmax checked here)
 //   qsp        : padded float column series (kPadL / kPadR of +inf)
 //   rowthr(u, i, i0): float threshold of row i given the strip's ub (double)
-//   rowbuf     : padded per-warp float scratch
+//   rowbuf     : padded per-warp float scratch (its own per direction)
+// REV: the pair is processed reversed -- row k of the pass is the caller's
+// rowraw(k) (the caller reverses the rows), column j is qsp[lc + 1 - j].
+// The DTW of the reversed pair is the same real sum over the reversed paths,
+// and the band |i - j| <= w maps onto itself, so the screen's soundness
+// argument (above) holds unchanged; only the evaluation order differs.
 // BLK: wavefront steps per block of finish bookkeeping (ballots, finish
 // masks, loop counters).  8 in the search and in NN1 (measured against 4:
 // cfg4 -2%, cfg3-nolb -3%, cfg5 -9%, NN1 being ALU-pipe bound; 16: cfg5 +1%):
@@ -100,29 +105,55 @@ constexpr int kF32Undecided = 1;  // a row value exceeded cmax: run the FP64 eng
 // UNB: also instantiate the unbounded-band path without the per-step band
 // test (NN1); the search kernel keeps one copy of the step loop (i-cache:
 // the second copy cost the cfg4 sweep ~4 ms).
-template <int BLK = 4, bool UNB = false, class RawFn, class NormFn, class UbFn, class RowThrFn>
-__device__ float warp_dtw_f32(const RawFn& rowraw, const NormFn& rownorm, int lr,
-                              const float* __restrict__ qsp, int lc, int w, float cmax,
-                              UbFn&& get_ub, RowThrFn&& rowthr, float* __restrict__ rowbuf,
-                              unsigned long long& cells, int& status) {
+// Warp-uniform, so a caller can keep it in memory between strip runs.
+struct F32Strip {
+  int lo, hi;     // live column range of the row held in rowbuf (row i0 - 1); lo < 0: dead
+  int written;    // highest rowbuf column that may hold a non-inf value
+  int i0;         // first row of the next strip
+  unsigned cnt;   // evaluated cells (warp total)
+  float ub_last;  // threshold of the row held in rowbuf
+  float slack;    // ub_last - min of that row (after a strip run with want_slack)
+  int status;     // 0, or kF32Undecided
+};
+
+__device__ inline void f32_strip_begin(F32Strip& s, int lc, float* __restrict__ rowbuf) {
   const int lane = threadIdx.x & 31;
   const float INF = f_inf();
-  status = 0;
   for (int k = lane; k <= lc + 1; k += 32) rowbuf[k] = k == 0 ? 0.0f : INF;
-  const bool banded = w < lr;
-  int lo = 0, hi = 0;  // live column range of the row held in rowbuf (row i0-1)
-  int written = 0;
-  unsigned cnt = 0;
-  float ub_last = INF;
-  double ub_next = get_ub();
-  double x_next = lane < lr ? rowraw(lane) : 0.0;
+  s.lo = 0;
+  s.hi = 0;
+  s.written = 0;
+  s.i0 = 1;
+  s.cnt = 0;
+  s.ub_last = INF;
+  s.slack = INF;
+  s.status = 0;
   __syncwarp();
+}
+
+// Runs up to max_strips strips (all: lr).  Stops early when the borders
+// collide (s.lo < 0: proven > ub) or a row value exceeds cmax.
+template <int BLK, bool UNB, bool REV, class RawFn, class NormFn, class UbFn, class RowThrFn>
+__device__ void f32_strip_run(F32Strip& s, int max_strips, bool want_slack, const RawFn& rowraw,
+                              const NormFn& rownorm, int lr, const float* __restrict__ qsp, int lc,
+                              int w, float cmax, UbFn&& get_ub, RowThrFn&& rowthr,
+                              float* __restrict__ rowbuf) {
+  const int lane = threadIdx.x & 31;
+  const float INF = f_inf();
+  const bool banded = w < lr;
+  int lo = s.lo, hi = s.hi, written = s.written;
+  unsigned cnt = 0;
+  float ub_last = s.ub_last;
+  int i0 = s.i0;
+  // the first strip's threshold and row values (then one strip ahead)
+  double ub_next = get_ub();
+  double x_next = i0 + lane <= lr ? rowraw(i0 - 1 + lane) : 0.0;
 #ifdef EAPDTW_PHASE_CLOCKS
   int dbg_strips = 0;
   unsigned long long dbg_steps = 0;
 #endif
 
-  for (int i0 = 1; i0 <= lr; i0 += 32) {
+  for (int ns = 0; ns < max_strips && i0 <= lr && lo >= 0; ++ns, i0 += 32) {
 #ifdef EAPDTW_PHASE_CLOCKS
     if (lane == 0) atomicAdd(&g_dbg[1], 1ull);
     ++dbg_strips;
@@ -140,7 +171,7 @@ __device__ float warp_dtw_f32(const RawFn& rowraw, const NormFn& rownorm, int lr
     ub_last = __shfl_sync(kFull, ub, wl);
     const float c = active ? rownorm(x) : INF;
     if (__any_sync(kFull, active && !(fabsf(c) <= cmax))) {
-      status = kF32Undecided;
+      s.status = kF32Undecided;
       break;
     }
     const int jb = max(lo, 1);
@@ -148,7 +179,8 @@ __device__ float warp_dtw_f32(const RawFn& rowraw, const NormFn& rownorm, int lr
     const int bh = active ? (banded ? min(lc, i + w) : lc) : -1;
     float top_prev = (lane == 0 && jb - 1 >= lo && jb - 1 <= hi) ? rowbuf[jb - 1] : INF;
     int j = jb - lane;
-    const float* qp = qsp + j;
+    // column j of the pass: qsp[j] forward, qsp[lc + 1 - j] reversed
+    const float* qp = REV ? qsp + (lc + 1 - j) : qsp + j;
     float* rp = rowbuf + j;
     float v = INF;
     unsigned finmask = __ballot_sync(kFull, !active);
@@ -162,7 +194,9 @@ __device__ float warp_dtw_f32(const RawFn& rowraw, const NormFn& rownorm, int lr
     // One wavefront step at column j+u (RANGE: with the band test).  Every
     // lane loads its row-buffer cell (only lane 0 uses it as its top): one
     // select instead of a predicated load and two moves.  Deadness is
-    // accumulated over the block of 4 steps (alld).
+    // accumulated over the block of steps (alld).  The cost and the
+    // accumulation are one FFMA (d*d + min, one rounding where the T32 bound
+    // allows two).
     auto step = [&](auto range_tag, int u, bool& alld) {
       constexpr bool RANGE = decltype(range_tag)::value;
       const float sh = __shfl_up_sync(kFull, v, 1);
@@ -170,12 +204,11 @@ __device__ float warp_dtw_f32(const RawFn& rowraw, const NormFn& rownorm, int lr
       const float top = is0 ? rb : sh;
       const float diag = top_prev;
       top_prev = top;
-      const float d = __fsub_rn(c, qp[u]);
-      // the band test masks the cost (off the step's dependency chain):
-      // +inf + min(...) = +inf
-      float cst = __fmul_rn(d, d);
-      if (RANGE) cst = static_cast<unsigned>(jr + u) <= span ? cst : INF;
-      const float nv = __fadd_rn(cst, fmin3f(v, top, diag));
+      float d = __fsub_rn(c, REV ? qp[-u] : qp[u]);
+      // the band test masks the difference (off the step's dependency
+      // chain): inf * inf + min(...) = +inf
+      if (RANGE) d = static_cast<unsigned>(jr + u) <= span ? d : INF;
+      const float nv = __fmaf_rn(d, d, fmin3f(v, top, diag));
       if (writer) rp[u] = nv;
       v = nv;
       alld = alld && nv > ub;
@@ -234,7 +267,7 @@ __device__ float warp_dtw_f32(const RawFn& rowraw, const NormFn& rownorm, int lr
       j += BLK;
       jr += BLK;
       j0 += BLK;
-      qp += BLK;
+      qp += REV ? -BLK : BLK;
       rp += BLK;
     }
     const int wend = jb - wl + (j - (jb - lane)) + (BLK - 1);
@@ -245,17 +278,24 @@ __device__ float warp_dtw_f32(const RawFn& rowraw, const NormFn& rownorm, int lr
     __syncwarp();
     const int wcol1 = min(wend, lc);
     int nlo = INT_MAX, nhi = -1;
+    float vmin = INF;
     for (int k0 = jb; k0 <= wcol1; k0 += 32) {
       const int k = k0 + lane;
-      const bool lv = k <= wcol1 && rowbuf[k] <= ub_last;
-      const unsigned bm = __ballot_sync(kFull, lv);
+      const float rv = k <= wcol1 ? rowbuf[k] : INF;
+      vmin = fminf(vmin, rv);
+      const unsigned bm = __ballot_sync(kFull, rv <= ub_last);
       if (bm) {
         if (nlo == INT_MAX) nlo = k0 + __ffs(bm) - 1;
         nhi = k0 + 31 - __clz(bm);
       }
     }
+    if (want_slack) {
+      for (int off = 16; off > 0; off >>= 1) vmin = fminf(vmin, __shfl_xor_sync(kFull, vmin, off));
+      s.slack = ub_last - vmin;
+    }
     if (nhi < 0) {
       lo = -1;
+      i0 += 32;
       break;
     }
     lo = nlo;
@@ -270,11 +310,91 @@ __device__ float warp_dtw_f32(const RawFn& rowraw, const NormFn& rownorm, int lr
   }
 #endif
   for (int off = 16; off > 0; off >>= 1) cnt += __shfl_xor_sync(kFull, cnt, off);
-  if (lane == 0) cells += cnt;
+  s.lo = lo;
+  s.hi = hi;
+  s.written = written;
+  s.i0 = i0;
+  s.cnt += cnt;
+  s.ub_last = ub_last;
+}
+
+// The pass's outcome: +inf if proven > ub (or undecided: status), else the
+// FP32 value of the final cell.  Adds the evaluated cells to `cells`.
+__device__ inline float f32_strip_end(F32Strip& s, int lc, const float* __restrict__ rowbuf,
+                                      unsigned long long& cells, int& status) {
+  const int lane = threadIdx.x & 31;
+  if (lane == 0) cells += s.cnt;
+  s.cnt = 0;
   __syncwarp();
-  if (status != 0 || lo < 0 || hi != lc) return INF;
+  status = s.status;
+  if (s.status != 0 || s.lo < 0 || s.hi != lc) return f_inf();
   const float r = rowbuf[lc];
-  return r <= ub_last ? r : INF;
+  return r <= s.ub_last ? r : f_inf();
+}
+
+// One whole FP32 pass, forward.
+template <int BLK = 4, bool UNB = false, class RawFn, class NormFn, class UbFn, class RowThrFn>
+__device__ float warp_dtw_f32(const RawFn& rowraw, const NormFn& rownorm, int lr,
+                              const float* __restrict__ qsp, int lc, int w, float cmax,
+                              UbFn&& get_ub, RowThrFn&& rowthr, float* __restrict__ rowbuf,
+                              unsigned long long& cells, int& status) {
+  F32Strip s;
+  f32_strip_begin(s, lc, rowbuf);
+  f32_strip_run<BLK, UNB, false>(s, lr, false, rowraw, rownorm, lr, qsp, lc, w, cmax, get_ub,
+                                 rowthr, rowbuf);
+  return f32_strip_end(s, lc, rowbuf, cells, status);
+}
+
+// Probe both directions, continue the likelier to die.  The FP32 pass runs
+// `probe` strips forward and `probe` strips on the reversed pair (its own row
+// buffer rowbuf_r), then finishes the direction whose last row has the
+// smaller slack (threshold minus the row's smallest value: the closer to an
+// all-dead row).  A pair the screen will abandon is abandoned by whichever
+// direction gets there first; the cfg4 design study (tools/live_study.c)
+// measured 1.7x fewer live cells than forward alone (the death rows of the
+// two directions are heavy-tailed and weakly correlated).  probe = 0: the
+// forward pass alone.  Returns +inf when proven > ub; otherwise a value (or
+// status kF32Undecided): run the exact engine.  (One inlined strip loop per
+// direction: the phases share it.)
+// st: two F32Strip in shared memory (the warp's): the inactive direction's
+// state stays there, not in registers (the search kernel is at its register
+// budget; local memory would miss L1 under the large shared-memory carve-out).
+template <int BLK, bool UNB, class RawF, class RawR, class NormFn, class UbFn, class ThrF, class ThrR>
+__device__ float f32_probe_pair(const RawF& raw_f, const RawR& raw_r, const NormFn& rownorm, int lr,
+                                const float* __restrict__ qsp, int lc, int w, float cmax,
+                                UbFn&& get_ub, ThrF&& thr_f, ThrR&& thr_r,
+                                float* __restrict__ rowbuf_f, float* __restrict__ rowbuf_r,
+                                int probe, F32Strip* st, unsigned long long& cells, int& status) {
+  F32Strip& f = st[0];
+  F32Strip& r = st[1];
+  f32_strip_begin(f, lc, rowbuf_f);
+  if (probe <= 0 || lr <= 32 * probe) probe = 0;
+  bool use_r = false;
+  // phase 0: forward probe (or the whole forward pass); 1: reversed probe;
+  // 2: the rest of the chosen direction
+  for (int phase = 0; phase < 3; ++phase) {
+    if (phase == 1) {
+      if (probe == 0 || f.lo < 0 || f.status != 0) break;
+      f32_strip_begin(r, lc, rowbuf_r);
+    }
+    if (phase == 2) {
+      use_r = r.lo < 0 || r.status != 0 || r.slack < f.slack;
+      int unused;
+      if (use_r) f32_strip_end(f, lc, rowbuf_f, cells, unused);  // the dropped direction's cells count
+      else f32_strip_end(r, lc, rowbuf_r, cells, unused);
+    }
+    const bool rev = phase == 1 || (phase == 2 && use_r);
+    const int n = (phase < 2 && probe > 0) ? probe : lr;
+    if (rev)
+      f32_strip_run<BLK, UNB, true>(r, n, phase == 1, raw_r, rownorm, lr, qsp, lc, w, cmax, get_ub,
+                                    thr_r, rowbuf_r);
+    else
+      f32_strip_run<BLK, UNB, false>(f, n, phase == 0, raw_f, rownorm, lr, qsp, lc, w, cmax,
+                                     get_ub, thr_f, rowbuf_f);
+    if (phase == 0 && probe == 0) break;
+  }
+  return use_r ? f32_strip_end(r, lc, rowbuf_r, cells, status)
+               : f32_strip_end(f, lc, rowbuf_f, cells, status);
 }
 
 }  // namespace eapdtw_b200

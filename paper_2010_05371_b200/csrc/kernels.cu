@@ -347,15 +347,21 @@ static __host__ __device__ inline size_t padded_len(int m, int ad_k) {
   return static_cast<size_t>(m) + 2 + 2 * static_cast<size_t>(smem_pad(ad_k));
 }
 
+// Per-warp buffer: the exact engine's row (or the EQ staging tile), which
+// the FP32 screen's two float rows (forward and reversed pass) alias.
 static __host__ __device__ inline size_t warp_buf_doubles(int m, int ad_k) {
   return padded_len(m, ad_k) + kStageExtra;
+}
+// The query as float (FP32 screen), padded like the FP64 copy.
+static __host__ __device__ inline size_t q32_len(int m) {
+  return static_cast<size_t>(m) + 2 + 2 * static_cast<size_t>(kPadR);
 }
 
 size_t search_smem_bytes(int m, int warps, int ad_k) {
   return padded_len(m, ad_k) * 8                        // q (padded, 1-based)
          + static_cast<size_t>(warps) * warp_buf_doubles(m, ad_k) * 8  // per-warp buffers
          + static_cast<size_t>(warps) * kStackBytesPerWarp  // per-warp tier stacks
-         + (padded_len(m, ad_k) * 4 + 7) / 8 * 8              // q as float (FP32 screen)
+         + (q32_len(m) * 4 + 7) / 8 * 8                       // q as float (FP32 screens)
          + 64;
 }
 
@@ -443,8 +449,8 @@ void debug_read_reset(unsigned long long* out8) {
 #endif
 constexpr int kSearchMinBlocks = EAPDTW_SEARCH_MIN_BLOCKS;
 
-// AD_K: anti-diagonal engine window compiled into this instantiation (0: strip
-// engine only -- the default search path, which then needs far fewer registers).
+// AD_K: the exact engine's anti-diagonal window compiled into this
+// instantiation (0: strip engine only -- the default search path).
 template <int AD_K>
 __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) search_kernel(SearchParams p) {
   extern __shared__ double smem[];
@@ -463,24 +469,37 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
   const size_t wlen = warp_buf_doubles(m, p.ad_k);
   double* rowbuf = smem + plen + static_cast<size_t>(warp) * wlen + pad;
   int* stacks = reinterpret_cast<int*>(smem + plen + static_cast<size_t>(blockDim.x >> 5) * wlen);
-  // the query as float (FP32 screen), after the stacks; padded like qsp
+  // the query as float (FP32 screens), after the stacks
   float* q32base = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(stacks) +
                                             static_cast<size_t>(blockDim.x >> 5) * kStackBytesPerWarp);
-  const float* qsp32 = q32base + pad;
+  const float* qsp32 = q32base + kPadR;
+  const int q32n = static_cast<int>(q32_len(m));
+  // this warp's FP32 probe state: two F32Strip, then two cumulative-bound prefixes
+  unsigned char* pstate = reinterpret_cast<unsigned char*>(stacks) + warp * kStackBytesPerWarp +
+                          (kStackBytesPerWarp - kProbeStateBytes);
+  F32Strip* probe_st = reinterpret_cast<F32Strip*>(pstate);
   // The FP32 engine's row buffer aliases the warp's FP64 one (both engines
   // initialise [0, lc+1] on entry and never depend on the padding contents:
   // out-of-band cells are +inf by the band test).
   float* rowbuf32 = reinterpret_cast<float*>(rowbuf);
+  // the FP32 probe's second (reversed-pass) row follows the first
+  const int rowbuf32_len = m + 2 + kPadL + kPadR + 8;
 
   const double INF = d_inf();
   for (int k = threadIdx.x; k < static_cast<int>(plen); k += blockDim.x) {
     const int j = k - pad;
     smem[k] = (j >= 1 && j <= m) ? p.q[j] : INF;
+  }
+  for (int k = threadIdx.x; k < q32n; k += blockDim.x) {
+    const int j = k - kPadR;
     q32base[k] = (j >= 1 && j <= m) ? __double2float_rn(p.q[j]) : f_inf();
   }
   for (int k = lane; k < static_cast<int>(plen); k += 32) rowbuf[k - pad] = INF;
   __syncthreads();
 
+#ifdef EAPDTW_PHASE_CLOCKS
+  const long long t_kernel0 = clock64();
+#endif
   unsigned long long c_kim = 0, c_eq = 0, c_ec = 0, c_calls = 0, c_aband = 0, c_cells = 0,
                      c_cand = 0, c_ovf = 0, c_scr = 0, c_cells_lane = 0, c_cells32 = 0;
   const double* __restrict__ ref = p.ref;
@@ -516,30 +535,28 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
     const double rsd = cconst ? 0.0 : __drcp_rn(cs);
     const bool have_ec = p.env != nullptr;
     // EQ / EC contribution of position k (0 past the end)
-    auto contrib = [&](int k, double& ceq, double& cec) {
-      ceq = 0.0;
-      cec = 0.0;
-      if (k >= m) return;
+    auto contrib_eq = [&](int k) -> double {
+      if (k >= m) return 0.0;
       const double c = __dmul_rn(__dsub_rn(crow[k], cm), rsd);
       const double2 b = qul[k];
       const double e1 = __dsub_rn(c, b.x), e2 = __dsub_rn(b.y, c);
       const double d1 = e1 > 0.0 ? e1 : (e2 > 0.0 ? e2 : 0.0);
-      ceq = __dmul_rn(d1, d1);
-      if (have_ec) {
-        const double2 e = p.env[cand + k];
-        const double U = __dmul_rn(__dsub_rn(e.x, cm), rsd);
-        const double L = __dmul_rn(__dsub_rn(e.y, cm), rsd);
-        const double qk = qsp[k + 1];
-        const double f1 = __dsub_rn(qk, U), f2 = __dsub_rn(L, qk);
-        const double d2 = f1 > 0.0 ? f1 : (f2 > 0.0 ? f2 : 0.0);
-        cec = __dmul_rn(d2, d2);
-      }
+      return __dmul_rn(d1, d1);
+    };
+    auto contrib_ec = [&](int k) -> double {
+      if (k >= m || !have_ec) return 0.0;
+      const double2 e = p.env[cand + k];
+      const double U = __dmul_rn(__dsub_rn(e.x, cm), rsd);
+      const double L = __dmul_rn(__dsub_rn(e.y, cm), rsd);
+      const double qk = qsp[k + 1];
+      const double f1 = __dsub_rn(qk, U), f2 = __dsub_rn(L, qk);
+      const double d2 = f1 > 0.0 ? f1 : (f2 > 0.0 ? f2 : 0.0);
+      return __dmul_rn(d2, d2);
     };
     const double tmax = fmax(teq, tec);
     const double cb_guard =
         p.guard_rel * tmax +
         8.0 * 0x1.0p-52 * (tmax + p.qmax * __dsqrt_rn(static_cast<double>(m) * tmax));
-    double pre_eq = 0.0, pre_ec = 0.0;
     // Row i's remaining cost: every path still visits every later row
     // (0-based positions >= i: EQ terms are per candidate position = row),
     // and every column past i+w (0-based >= i+w: EC terms are per query
@@ -547,29 +564,43 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
     // the reference's single k = min(i+w, m) - 1 (which must also serve EC);
     // the bound is tighter and still sound.  Each strip extends both
     // prefixes by 32 positions (one lane each, one warp scan each).
-    int pre_end_eq = -1, pre_end_ec = -1;
-    auto rowthr = [&](double u, int i, int i0) -> double {
+    // A pass over the REVERSED pair (the FP32 screen's probe, dtw_f32.cuh)
+    // sees position k of the pass at the candidate's / query's position
+    // m-1-k, so its prefixes run over the positions from the end: the same
+    // bound for the mirrored problem.
+    struct CbPrefix {
+      double eq, ec;
+      int end_eq, end_ec;  // the prefixes cover pass positions [0, end) once started (-1: not yet)
+    };
+    static_assert(2 * sizeof(F32Strip) + 2 * sizeof(CbPrefix) <= kProbeStateBytes, "probe state");
+    // (both directions' prefix states in the warp's shared probe state:
+    // memory, not registers -- the kernel is at its register budget)
+    CbPrefix* cbp = reinterpret_cast<CbPrefix*>(pstate + 2 * sizeof(F32Strip));
+    if (lane == 0) cbp[0] = cbp[1] = CbPrefix{0.0, 0.0, -1, -1};
+    __syncwarp();
+    auto rowthr_dir = [&](auto rev_tag, CbPrefix& st, double u, int i, int i0) -> double {
+      constexpr bool REV = decltype(rev_tag)::value;
       if (!tight || i0 < 1 + 32 * (p.cb_strip - 1)) return u;
+      auto pos = [&](int k) { return REV ? m - 1 - k : k; };
       const int k_eq = i0 - 1, k_ec = i0 + p.w - 1;  // lane 0's positions
-      if (pre_end_eq < 0) {  // positions before this strip's first ones
-        pre_end_eq = min(m, k_eq);
-        pre_end_ec = min(m, k_ec);
-        for (int k = lane; k < pre_end_ec; k += 32) {
-          double a, b;
-          contrib(k, a, b);
-          if (k < pre_end_eq) pre_eq = __dadd_rn(pre_eq, a);
-          pre_ec = __dadd_rn(pre_ec, b);
-        }
+      if (st.end_eq < 0) {  // positions before this strip's first ones
+        st.end_eq = min(m, k_eq);
+        st.end_ec = min(m, k_ec);
+        double eq = 0.0, ec = 0.0;
+        for (int k = lane; k < st.end_eq; k += 32) eq = __dadd_rn(eq, contrib_eq(pos(k)));
+        for (int k = lane; k < st.end_ec; k += 32) ec = __dadd_rn(ec, contrib_ec(pos(k)));
         for (int off = 16; off > 0; off >>= 1) {
-          pre_eq = __dadd_rn(pre_eq, __shfl_xor_sync(kFull, pre_eq, off));
-          pre_ec = __dadd_rn(pre_ec, __shfl_xor_sync(kFull, pre_ec, off));
+          eq = __dadd_rn(eq, __shfl_xor_sync(kFull, eq, off));
+          ec = __dadd_rn(ec, __shfl_xor_sync(kFull, ec, off));
         }
+        st.eq = eq;
+        st.ec = ec;
       }
       // this strip's rows need prefixes through k_eq + lane and k_ec + lane
       const int ke = k_eq + lane, kc = k_ec + lane;
-      double a = 0.0, b = 0.0, unused;
-      if (ke >= pre_end_eq && ke < m) contrib(ke, a, unused);
-      if (kc >= pre_end_ec && kc < m) contrib(kc, unused, b);
+      double a = 0.0, b = 0.0;
+      if (ke >= st.end_eq && ke < m) a = contrib_eq(pos(ke));
+      if (kc >= st.end_ec && kc < m) b = contrib_ec(pos(kc));
       for (int off = 1; off < 32; off <<= 1) {  // inclusive prefix scans
         const double x = __shfl_up_sync(kFull, a, off);
         const double y = __shfl_up_sync(kFull, b, off);
@@ -578,16 +609,16 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
           b = __dadd_rn(b, y);
         }
       }
-      const double peq = __dadd_rn(pre_eq, a), pec = __dadd_rn(pre_ec, b);
+      const double peq = __dadd_rn(st.eq, a), pec = __dadd_rn(st.ec, b);
       // the next strip starts where this one's rows end
       const int nxe = min(m, k_eq + 32), nxc = min(m, k_ec + 32);
-      if (nxe > pre_end_eq) {
-        pre_eq = __shfl_sync(kFull, peq, min(31, nxe - 1 - k_eq));
-        pre_end_eq = nxe;
+      if (nxe > st.end_eq) {
+        st.eq = __shfl_sync(kFull, peq, min(31, nxe - 1 - k_eq));
+        st.end_eq = nxe;
       }
-      if (nxc > pre_end_ec) {
-        pre_ec = __shfl_sync(kFull, pec, min(31, nxc - 1 - k_ec));
-        pre_end_ec = nxc;
+      if (nxc > st.end_ec) {
+        st.ec = __shfl_sync(kFull, pec, min(31, nxc - 1 - k_ec));
+        st.end_ec = nxc;
       }
       if (i >= m) return u;  // the last row: nothing left
       const double ceq = __dsub_rn(teq, peq);
@@ -596,6 +627,9 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
       if (!(cbv > 0.0)) return u;
       const double t = __dsub_rn(__dmul_rn(u, 1.0 + p.guard_rel), cbv);
       return t > 0.0 ? t : 0.0;
+    };
+    auto rowthr = [&](double u, int i, int i0) -> double {
+      return rowthr_dir(std::false_type{}, cbp[0], u, i, i0);
     };
     // FP32 screen first (dtw_f32.cuh) once a finite threshold exists: it
     // abandons with a sound, error-inflated threshold; whatever it cannot
@@ -609,13 +643,20 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
       auto rowthr32 = [&](double u, int i, int i0) -> float {
         return f32_threshold(rowthr(u, i, i0), g);
       };
-      int st = 0;
-      const float r32 = warp_dtw_f32<kSearchStepBlock>(rowraw, rownorm32, m, qsp32, m, p.w, p.f32_cmax, get_ub,
-                                     rowthr32, rowbuf32, c_cells32, st);
-      screened = st == 0 && r32 == f_inf();
+      auto rowthr32_r = [&](double u, int i, int i0) -> float {
+        return f32_threshold(rowthr_dir(std::true_type{}, cbp[1], u, i, i0), g);
+      };
+      auto rowraw_r = [&](int r) -> double { return crow[m - 1 - r]; };
+      {
+        // both directions probed, then the likelier to die (dtw_f32.cuh)
+        int st = 0;
+        const float r32 = f32_probe_pair<kSearchStepBlock, false>(
+            rowraw, rowraw_r, rownorm32, m, qsp32, m, p.w, p.f32_cmax, get_ub, rowthr32,
+            rowthr32_r, rowbuf32, rowbuf32 + rowbuf32_len, p.probe_strips, probe_st, c_cells32, st);
+        screened = st == 0 && r32 == f_inf();
+      }
       // the cumulative-bound prefixes restart for the exact pass
-      pre_eq = pre_ec = 0.0;
-      pre_end_eq = pre_end_ec = -1;
+      if (lane == 0) cbp[0] = CbPrefix{0.0, 0.0, -1, -1};
       __syncwarp();
     }
     const double d = screened ? INF
@@ -633,33 +674,12 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
     }
   };
 
-  if (p.direct) {
-    // ---- direct mode (the probe): every candidate is a DTW task; warps
-    //      claim `direct_chunk` candidates at a time.
-    const long long K = p.direct_chunk;
-    const long long nlist =
-        p.list ? min(static_cast<long long>(vload(p.nlist)), p.list_cap) : 0;
-    for (;;) {
-      unsigned long long c = 0;
-      if (lane == 0) c = atomicAdd(p.work, 1ull);
-      c = __shfl_sync(kFull, c, 0);
-      if (p.list) {  // the candidates come from the list
-        const long long li = static_cast<long long>(c);
-        if (li >= nlist) break;
-        ++c_cand;
-        run_dtw(p.list[li], false, 0.0, 0.0);
-        continue;
-      }
-      const long long base = p.begin + static_cast<long long>(c) * K * p.stride;
-      if (base >= p.end) break;
-      for (long long k = 0; k < K; ++k) {
-        const long long s = base + k * p.stride;
-        if (s >= p.end) break;
-        ++c_cand;
-        run_dtw(s, false, 0.0, 0.0);
-      }
-    }
-  } else {
+  // ---- direct mode (the probe, the rank pass's upper-bound wave): every
+  //      candidate is a DTW task, claimed one at a time.
+  // ---- cascade mode: LB chunks and queued DTW tasks (below).
+  // Both modes feed the ONE call site of run_dtw at the bottom of the loop
+  // (code size: the kernel is instruction-cache sensitive).
+  {
     // ---- cascade mode.  Survivor queue protocol (no CAS retries):
     //   producers reserve slots with atomicAdd(qtail) and fill them;
     //   a consumer takes a slot with atomicAdd(qhead) only when head < tail
@@ -728,8 +748,27 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
     };
     const float2 z2 = make_float2(0.0f, 0.0f);
 
+    const long long nlist_d =
+        p.list ? min(static_cast<long long>(vload(p.nlist)), p.list_cap) : 0;
     for (;;) {
       long long cand = -1;
+      float2 tot = z2;
+      bool have_tot = false;
+      if (p.direct) {
+        unsigned long long c = 0;
+        if (lane == 0) c = atomicAdd(p.work, 1ull);
+        c = __shfl_sync(kFull, c, 0);
+        if (p.list) {  // the candidates come from the list
+          if (static_cast<long long>(c) >= nlist_d) break;
+          cand = p.list[c];
+        } else {
+          cand = p.begin + static_cast<long long>(c) * p.stride;
+          if (cand >= p.end) break;
+        }
+        ++c_cand;
+        goto dtw_task;
+      }
+      {
       bool void_slot = false;
       if (lane == 0) {
         if (myslot < 0 && vload(p.qhead) < vload(p.qtail))
@@ -745,7 +784,6 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
       cand = __shfl_sync(kFull, cand, 0);
       void_slot = __shfl_sync(kFull, void_slot, 0);
       if (cand >= 0) {
-        float2 tot = z2;
         if (lane == 0) {
           __threadfence();
           const unsigned long long raw =
@@ -755,11 +793,9 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
         }
         tot.x = __shfl_sync(kFull, tot.x, 0);
         tot.y = __shfl_sync(kFull, tot.y, 0);
+        have_tot = p.use_lb != 0;
         myslot = -1;
-        PHASE_BEGIN();
-        run_dtw(cand, p.use_lb != 0, static_cast<double>(tot.x), static_cast<double>(tot.y));
-        PHASE_END(kClkDtw);
-        continue;
+        goto dtw_task;
       }
       myslot = __shfl_sync(kFull, myslot, 0);
       if (void_slot) break;
@@ -773,7 +809,9 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
             done = vload(p.chunks_done) >= static_cast<unsigned long long>(nchunks) &&
                    vload(p.qhead) >= vload(p.qtail);
           if (__shfl_sync(kFull, done, 0)) break;
+          PHASE_BEGIN();
           __nanosleep(256);
+          PHASE_END(kClkWait);
         }
         continue;  // claim a new slot, or wait for the pending one to be filled
       }
@@ -1110,6 +1148,12 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
         if (lane == 0) atomicAdd(p.chunks_done, my_chunks);
         flushed = true;
       }
+      continue;
+      }
+    dtw_task:
+      PHASE_BEGIN();
+      run_dtw(cand, have_tot, static_cast<double>(tot.x), static_cast<double>(tot.y));
+      PHASE_END(kClkDtw);
     }
   }
 
@@ -1136,6 +1180,9 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
     atomicAdd(&p.counters[kCntOverflows], c_ovf);
     atomicAdd(&p.counters[kCntScreened], c_scr);
     atomicAdd(&p.counters[kCntCellsF32], c_cells32);
+#ifdef EAPDTW_PHASE_CLOCKS
+    atomicAdd(&p.counters[kClkTotal], static_cast<unsigned long long>(clock64() - t_kernel0));
+#endif
   }
 }
 
@@ -1403,6 +1450,12 @@ __device__ double kim_layers_raw(const double* __restrict__ rw, int L, const dou
 #ifndef EAPDTW_NN1_MINB
 #define EAPDTW_NN1_MINB 4  // 4 blocks/SM (64 registers, spills off the step loop): cfg5 -2% vs 3, 2: +17%
 #endif
+// Per-warp buffer of nn1_kernel (doubles): the exact engine's row, aliased by
+// the FP32 screen's two float rows (forward and reversed pass).
+static __host__ __device__ inline size_t nn1_warp_doubles(int len, int ad_k) {
+  return padded_len(len, ad_k) + 64;
+}
+
 __global__ void __launch_bounds__(256, EAPDTW_NN1_MINB) nn1_kernel(Nn1Params p) {
   extern __shared__ double smem[];
   __shared__ unsigned long long s_next;
@@ -1410,15 +1463,21 @@ __global__ void __launch_bounds__(256, EAPDTW_NN1_MINB) nn1_kernel(Nn1Params p) 
   const int L = p.len;
   const int pad = smem_pad(p.ad_k);
   const size_t plen = padded_len(L, p.ad_k);
+  const size_t wlen = nn1_warp_doubles(L, p.ad_k);
   const long long qi = blockIdx.x / p.splits;
   const int part = blockIdx.x % p.splits;
   const long long k0 = p.nd * part / p.splits, k1 = p.nd * (part + 1) / p.splits;
   __shared__ int s_qbig;  // some |q| > f32_cmax: no FP32 screen for this query
   double* qsp = smem + pad;  // padded, 1-based
-  double* rowbuf = smem + plen + static_cast<size_t>(warp) * plen + pad;
-  float* q32base = reinterpret_cast<float*>(smem + static_cast<size_t>(blockDim.x / 32 + 1) * plen);
-  const float* qsp32 = q32base + pad;
+  double* rowbuf = smem + plen + static_cast<size_t>(warp) * wlen + pad;
+  float* q32base = reinterpret_cast<float*>(smem + plen + static_cast<size_t>(blockDim.x / 32) * wlen);
+  const float* qsp32 = q32base + kPadR;
+  const int q32n = static_cast<int>(q32_len(L));
   float* rowbuf32 = reinterpret_cast<float*>(rowbuf);  // aliases the FP64 row (dtw_f32.cuh)
+  // this warp's FP32 probe state (two F32Strip), after the float query
+  F32Strip* probe_st = reinterpret_cast<F32Strip*>(
+                           reinterpret_cast<unsigned char*>(q32base) + (q32_len(L) * 4 + 15) / 16 * 16) +
+                       2 * warp;
   const double INF = d_inf();
   if (threadIdx.x == 0) {
     s_next = 0;
@@ -1429,8 +1488,11 @@ __global__ void __launch_bounds__(256, EAPDTW_NN1_MINB) nn1_kernel(Nn1Params p) 
     const int j = k - pad;
     const double qv = (j >= 1 && j <= L) ? p.queries[qi * L + j - 1] : INF;
     smem[k] = qv;
-    q32base[k] = (j >= 1 && j <= L) ? __double2float_rn(qv) : f_inf();
     if (j >= 1 && j <= L && !(fabs(qv) <= static_cast<double>(p.f32_cmax))) s_qbig = 1;
+  }
+  for (int k = threadIdx.x; k < q32n; k += blockDim.x) {
+    const int j = k - kPadR;
+    q32base[k] = (j >= 1 && j <= L) ? __double2float_rn(p.queries[qi * L + j - 1]) : f_inf();
   }
   for (int k = lane; k < static_cast<int>(plen); k += 32) rowbuf[k - pad] = INF;
   __syncthreads();
@@ -1527,10 +1589,15 @@ __global__ void __launch_bounds__(256, EAPDTW_NN1_MINB) nn1_kernel(Nn1Params p) 
     if (use_f32 && __shfl_sync(kFull, ub, 0) < INF) {  // FP32 screen (dtw_f32.cuh)
       auto rownorm32 = [](double x) -> float { return __double2float_rn(x); };
       auto rowthr32 = [&](double u, int, int) -> float { return f32_threshold(u, g); };
-      int st = 0;
-      const float r32 = warp_dtw_f32<kNn1StepBlock, true>(rowraw, rownorm32, L, qsp32, L, p.w, p.f32_cmax, get_ub,
-                                     rowthr32, rowbuf32, cells32, st);
-      screened = st == 0 && r32 == f_inf();
+      {
+        // both directions probed, then the likelier to die (dtw_f32.cuh)
+        auto rowraw_r = [&](int r) -> double { return row[L - 1 - r]; };
+        int st = 0;
+        const float r32 = f32_probe_pair<kNn1StepBlock, true>(
+            rowraw, rowraw_r, rownorm32, L, qsp32, L, p.w, p.f32_cmax, get_ub, rowthr32, rowthr32,
+            rowbuf32, rowbuf32 + (L + 2 + kPadL + kPadR + 8), p.probe_strips, probe_st, cells32, st);
+        screened = st == 0 && r32 == f_inf();
+      }
       __syncwarp();
     }
     const double d = screened ? INF
@@ -1552,12 +1619,14 @@ __global__ void __launch_bounds__(256, EAPDTW_NN1_MINB) nn1_kernel(Nn1Params p) 
 
 cudaError_t launch_nn1(const Nn1Params& p, cudaStream_t stream) {
   const int warps = 8;
-  const size_t smem = static_cast<size_t>(warps + 1) * padded_len(p.len, p.ad_k) * sizeof(double) +
-                     padded_len(p.len, p.ad_k) * sizeof(float);
+  const size_t smem = padded_len(p.len, p.ad_k) * sizeof(double) +
+                      static_cast<size_t>(warps) * nn1_warp_doubles(p.len, p.ad_k) * sizeof(double) +
+                      (q32_len(p.len) * sizeof(float) + 15) / 16 * 16 +
+                      static_cast<size_t>(warps) * 2 * sizeof(F32Strip);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  const long long blocks = p.nq * p.splits;
   cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(nn1_kernel), smem);
   if (e != cudaSuccess) return e;
-  const long long blocks = p.nq * p.splits;
   nn1_kernel<<<static_cast<unsigned>(blocks), warps * 32, smem, stream>>>(p);
   return cudaGetLastError();
 }

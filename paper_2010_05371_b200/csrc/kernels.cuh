@@ -27,10 +27,12 @@ constexpr int kKimLongFrom = 768;
 #define EAPDTW_SUPER_CHUNK 4
 #endif
 constexpr int kSuperChunk = EAPDTW_SUPER_CHUNK;    // LB chunks (of 32 candidates) per claim
-constexpr int kStageExtra = 64;                    // extra doubles per warp buffer: EQ staging span
+constexpr int kStageExtra = 48;                    // extra doubles per warp buffer: EQ staging span (>= 2 super-chunks... 128 candidates + 2)
 constexpr int kLbHead = 256;                       // first leg of the Keogh tiers (positions of order[])
 // A, A2, B, B2, C indices; B, B2 EQ totals; C (EQ, EC) totals; A2, B2 partial sums
-constexpr int kStackBytesPerWarp = kStack * (5 * 4 + 2 * 4 + 8 + 2 * 8);
+// + the FP32 screen's probe state (two F32Strip, two cumulative-bound prefixes)
+constexpr int kProbeStateBytes = 128;
+constexpr int kStackBytesPerWarp = kStack * (5 * 4 + 2 * 4 + 8 + 2 * 8) + kProbeStateBytes;
 
 // Tier counters accumulated on the device (SearchReport, search.hpp:68-77).
 enum Counter : int {
@@ -54,6 +56,7 @@ enum Counter : int {
   kClkWait,
   kStageHit,
   kStageMiss,
+  kClkTotal,
   kNumCountersExt
 };
 
@@ -89,6 +92,7 @@ struct SearchParams {
   int ad_k;                      // anti-diagonal engine window 64*ad_k (0: strip engine only)
   int direct;                    // 1: every candidate is a DTW task (the probe)
   int screen_rows;               // phase-A lane screen depth (0: off)
+  int probe_strips;              // FP32 strip screen: strips probed in each direction (0: forward only)
   int use_f32;                   // FP32 screening engine ahead of the exact FP64 one
   float f32_a, f32_b, f32_cmax;  // its threshold guard (dtw_f32.cuh) and row-value bound
   unsigned long long* counters;  // kNumCounters
@@ -132,6 +136,7 @@ struct Nn1Params {
   float f32_a, f32_b, f32_cmax;   // guard built with qmax = cmax (dtw_f32.cuh)
   double guard_rel, guard_abs;    // layered LB_Kim guard (summation order)
   int warm;                       // per-warp warm start (best layered-Kim row first)
+  int probe_strips;               // FP32 screen: strips probed in each direction (0: forward only)
 };
 
 // Each launcher enqueues on `stream` and returns the launch error (no sync).

@@ -558,3 +558,50 @@ def test_nn1_cfg5_full_size_vs_reference(gpu):
     ai, ad = sh.search()
     assert np.array_equal(np.asarray(ai, dtype=np.uint64), want_arg)
     assert np.array_equal(ad.view(np.uint64), want_d.view(np.uint64))
+
+
+@pytest.mark.parametrize("n,m,ratio,lb", [(300_000, 256, 0.2, True), (200_000, 512, 0.1, False),
+                                          (150_000, 1024, 0.2, True), (60_000, 300, 1.0, True),
+                                          (100_000, 40, 0.5, True), (80_000, 200, 0.15, False)])
+def test_fp32_screen_probe_directions_agree(gpu, oracle_lib, n, m, ratio, lb):
+    """The FP32 screen's two-direction probe (probe_strips strips forward and
+    on the reversed pair, then the likelier direction to its end) and the
+    forward-only pass (probe_strips 0) both return the oracle's (location, d)
+    bit for bit, on plain walks and with planted exact and near-exact copies
+    (one time-warped by a quarter of the band, near a band edge)."""
+    ref = gpu.random_walk_normal(n, 80 + m)
+    q = gpu.random_walk_normal(m, 81 + m)
+    r = ref.copy()
+    a, b = n // 4, (3 * n) // 5
+    r[a:a + m] = q * 2.5 - 1.0
+    r[b + m // 2] += 1e-7
+    w = max(1, int(ratio * m) // 4)
+    warped = np.concatenate([np.repeat(q[:1], w), q[:m - w]])  # q delayed by w samples
+    r[b:b + m] = warped * 0.7 + 2.0
+    ctx = gpu.default_context()
+    cfg = gpu.SearchConfig(window_ratio=ratio, use_lower_bounds=lb, tighten_ub=lb)
+    for arr in (ref, r):
+        want = oracle_lib.similarity_search(arr, q, ratio, use_lb=lb, tighten=lb)
+        for k in (0, 1, 2, 4):
+            with ctx.options(probe_strips=k):
+                got = gpu.similarity_search(arr, q, cfg)
+            assert (got.best.location, got.best.distance_sq) == (want.location, want.distance_sq), k
+
+
+def test_nn1_probe_directions_agree(gpu, reference_lib_optional):
+    """NN1 with the two-direction FP32 probe and without it: the reference
+    loop's argmin and distance bits (unbounded and banded)."""
+    from paper_2010_05371_b200 import znormalize
+    rng = np.random.default_rng(606)
+    L = 300
+    db = np.stack([znormalize(np.cumsum(rng.standard_normal(L))) for _ in range(3000)])
+    qs = np.stack([znormalize(np.cumsum(rng.standard_normal(L))) for _ in range(24)])
+    db[1234] = qs[5]
+    ctx = gpu.default_context()
+    for band in (UNB, 40):
+        warg, wdist, _ = reference_lib_optional.nn1(qs, db, band)
+        for k in (0, 1, 3):
+            with ctx.options(probe_strips=k):
+                arg, dist, _ = gpu.nn1(qs, db, gpu.Band(band))
+            assert [int(x) for x in arg] == [int(x) for x in warg], k
+            assert np.array_equal(dist, wdist), k
