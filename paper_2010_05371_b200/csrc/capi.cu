@@ -74,6 +74,7 @@ enum Opt : int {
   kOptNn1Warm,        // NN1 per-warp warm start
   kOptSeriesCache,    // device-resident series keep their last stats
   kOptProbeStrips,    // FP32 strip screen: strips probed in each direction before committing (0: forward only)
+  kOptProducers,      // search sweep: SMSP-0 warps are LB producers until this queue backlog (0: off)
   kNumOpts
 };
 struct OptDef {
@@ -88,7 +89,7 @@ constexpr OptDef kOpts[kNumOpts] = {
     {"coarse_stride", 0, 0, 1 << 20}, {"probe", 2048, 1, 1 << 24}, {"probe_force", 0, 0, 1},
     {"tighten", 1, 0, 1},         {"cb_strip", 1, 1, 1 << 16},  {"warps", 0, 0, 8},
     {"nn1_splits", 0, 0, 1 << 16}, {"nn1_warm", 1, 0, 1},       {"series_cache", 1, 0, 1},
-    {"probe_strips", 1, 0, 8},
+    {"probe_strips", 1, 0, 8},    {"producers", 0, 0, 1 << 20},
 };
 
 // Grow-only device buffer.
@@ -788,6 +789,7 @@ static SearchParams base_params(eapdtw_search_plan* p) {
   s.direct = 0;
   s.screen_rows = p->screen_rows;
   s.probe_strips = static_cast<int>(p->ctx->opt[kOptProbeStrips]);
+  s.producer_smsp = static_cast<int>(p->ctx->opt[kOptProducers]);
   {
     // z-normalised rows satisfy |c| <= sqrt(m - 1); the engine checks the
     // bound per strip (degenerate statistics fall back to the exact engine)

@@ -197,14 +197,20 @@ __device__ void f32_strip_run(F32Strip& s, int max_strips, bool want_slack, cons
     // accumulated over the block of steps (alld).  The cost and the
     // accumulation are one FFMA (d*d + min, one rounding where the T32 bound
     // allows two).
+    // The block's column values and row-buffer cells are loaded up front
+    // (qb, rbb): the compiler cannot move a load above the writer's store to
+    // the same shared array, and the per-step load latency was the largest
+    // stall of the loop (ncu).  Reading rowbuf early is safe: the writer
+    // (lane wl >= 0) writes column j0 - wl + u at step u, lane 0 reads column
+    // j0 + u, so a column is read before it is written.
+    float qb[BLK], rbb[BLK];
     auto step = [&](auto range_tag, int u, bool& alld) {
       constexpr bool RANGE = decltype(range_tag)::value;
       const float sh = __shfl_up_sync(kFull, v, 1);
-      const float rb = rp[u];
-      const float top = is0 ? rb : sh;
+      const float top = is0 ? rbb[u] : sh;
       const float diag = top_prev;
       top_prev = top;
-      float d = __fsub_rn(c, REV ? qp[-u] : qp[u]);
+      float d = __fsub_rn(c, qb[u]);
       // the band test masks the difference (off the step's dependency
       // chain): inf * inf + min(...) = +inf
       if (RANGE) d = static_cast<unsigned>(jr + u) <= span ? d : INF;
@@ -217,6 +223,11 @@ __device__ void f32_strip_run(F32Strip& s, int max_strips, bool want_slack, cons
     for (;;) {
       const unsigned before = finmask;
       bool alld = true;
+#pragma unroll
+      for (int u = 0; u < BLK; ++u) {
+        qb[u] = REV ? qp[-u] : qp[u];
+        rbb[u] = rp[u];
+      }
       // Unbounded band: the band is the whole row, and the +inf padding of
       // qsp (dtw_warp.cuh) already makes every out-of-range column cost +inf,
       // so the per-step band test (3 ALU-pipe ops per cell) is dropped.

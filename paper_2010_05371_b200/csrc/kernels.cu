@@ -588,7 +588,17 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
         st.end_ec = min(m, k_ec);
         double eq = 0.0, ec = 0.0;
         for (int k = lane; k < st.end_eq; k += 32) eq = __dadd_rn(eq, contrib_eq(pos(k)));
-        for (int k = lane; k < st.end_ec; k += 32) ec = __dadd_rn(ec, contrib_ec(pos(k)));
+        // (4 positions per lane in flight: the envelope loads are L2 latency)
+        for (int k0 = lane; k0 < st.end_ec; k0 += 128) {
+          double t4[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int k = k0 + 32 * u;
+            t4[u] = k < st.end_ec ? contrib_ec(pos(k)) : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) ec = __dadd_rn(ec, t4[u]);
+        }
         for (int off = 16; off > 0; off >>= 1) {
           eq = __dadd_rn(eq, __shfl_xor_sync(kFull, eq, off));
           ec = __dadd_rn(ec, __shfl_xor_sync(kFull, ec, off));
@@ -750,6 +760,15 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
 
     const long long nlist_d =
         p.list ? min(static_cast<long long>(vload(p.nlist)), p.list_cap) : 0;
+    // Warp specialisation by scheduler (SMSP = warp slot mod 4): with
+    // p.producer_smsp, the warps of SMSP 0 run the lower-bound tiers and take
+    // a DTW task only once the queue holds a backlog (or their chunks are
+    // done); the other SMSPs drain the queue first.  Each SMSP's instruction
+    // cache then holds mostly one of the two code paths (ncu: instruction-
+    // fetch stalls were the largest stall reason with every warp mixing both).
+    unsigned warp_slot;
+    asm volatile("mov.u32 %0, %%warpid;" : "=r"(warp_slot));
+    const bool producer = p.producer_smsp != 0 && (warp_slot & 3u) == 0u;
     for (;;) {
       long long cand = -1;
       float2 tot = z2;
@@ -771,8 +790,11 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
       {
       bool void_slot = false;
       if (lane == 0) {
-        if (myslot < 0 && vload(p.qhead) < vload(p.qtail))
-          myslot = static_cast<long long>(atomicAdd(p.qhead, 1ull));
+        if (myslot < 0) {
+          const unsigned long long h = vload(p.qhead), t = vload(p.qtail);
+          if (h < t && (!producer || !chunks_left || t - h > static_cast<unsigned long long>(p.producer_smsp)))
+            myslot = static_cast<long long>(atomicAdd(p.qhead, 1ull));
+        }
         if (myslot >= 0) {
           cand = vload(p.queue + myslot);
           if (cand < 0 && flushed &&
