@@ -58,8 +58,9 @@ typedef struct {
   int32_t found;
   int32_t pad_;
   uint64_t candidates_total, pruned_kim, pruned_keogh_eq, pruned_keogh_ec, dtw_calls,
-      dtw_abandoned, dp_cells_evaluated;
+      dtw_abandoned, dp_cells_evaluated; /* cells of the exact DP, as dtw.cpp:28-33 counts */
   double elapsed_seconds;
+  uint64_t screen_cells_evaluated; /* cells of the FP32 screening pass (not in dp_cells_evaluated) */
 } eapdtw_search_result;
 
 /* --- errors / context ---------------------------------------------------- */
@@ -104,6 +105,11 @@ int eapdtw_ea_pruned_dtw_windowed(eapdtw_ctx* ctx, const double* a, size_t la, c
                                   size_t cb_len, double* out, uint64_t* cells);
 int eapdtw_dtw_windowed(eapdtw_ctx* ctx, const double* a, size_t la, const double* b, size_t lb,
                         size_t window, double* out, uint64_t* cells);
+/* dtw_left_prune_windowed(a, b, Band{window}, ub)                 dtw.hpp:76-83
+ * (left_prune_scan, dtw.cpp:130-182: pruning from the left only) */
+int eapdtw_dtw_left_prune_windowed(eapdtw_ctx* ctx, const double* a, size_t la, const double* b,
+                                   size_t lb, size_t window, double ub, double* out,
+                                   uint64_t* cells);
 
 /* --- per-cell trace of one DTW (KernelTrace, dtw.hpp:42-57) ---------------- *
  * algo 0 dtw_full / dtw_windowed, 1 dtw_left_prune(_windowed), 2 ea_pruned_dtw
@@ -224,7 +230,30 @@ int eapdtw_sliding_stats(eapdtw_ctx* ctx, const double* ref, size_t n, size_t m,
 int eapdtw_sliding_envelope(eapdtw_ctx* ctx, const double* ref, size_t n, size_t r, double* upper,
                             double* lower);
 
+/* --- the reference's lower-bound API (lower_bounds.hpp:12-63), computed on the
+ * device with the reference's arithmetic and order (bit-identical results).
+ * Host pointers.  EAPDTW_EINVAL exactly where the reference throws.
+ *   compute_envelope(series, Band{window})        lower_bounds.hpp:25 / .cpp:9-49
+ *     window EAPDTW_UNBOUNDED_WINDOW = the whole series
+ *   lb_kim_fl(q, c)                               lower_bounds.hpp:33 / .cpp:51-55
+ *   lb_keogh(env, series, abandon_above, order)   lower_bounds.hpp:52-54 / .cpp:57-88
+ *     order may be NULL (natural order); contributions (nullable) receives l
+ *     values in natural index order, 0 where not visited
+ *   cumulative_bound(contributions)               lower_bounds.hpp:63 / .cpp:90-103 */
+int eapdtw_compute_envelope(eapdtw_ctx* ctx, const double* series, size_t l, size_t window,
+                            double* upper, double* lower);
+int eapdtw_lb_kim_fl(eapdtw_ctx* ctx, const double* q, const double* c, size_t l, double* out);
+int eapdtw_lb_keogh(eapdtw_ctx* ctx, const double* upper, const double* lower, const double* series,
+                    size_t l, double abandon_above, const size_t* order, double* total,
+                    double* contributions, int* abandoned);
+int eapdtw_cumulative_bound(eapdtw_ctx* ctx, const double* contributions, size_t l, double* cb);
+
 /* --- host-side helpers (bit-identical to the reference) -------------------- */
+/* RunningStats::over (search.cpp:25-33): sum and sum of squares of x[0, n) */
+int eapdtw_running_stats_over(const double* x, size_t n, double* sum, double* sumsq);
+/* znormalize_into (search.cpp:37-46) with given RunningStats (sum, sumsq, count) */
+int eapdtw_znormalize_into(const double* src, size_t n, double sum, double sumsq, uint64_t count,
+                           double* dst);
 /* RunningStats::over + znormalize_into (search.cpp:25-46) */
 int eapdtw_znormalize(const double* src, size_t n, double* dst);
 /* random_walk (io.cpp:124-137): mt19937_64, uniform steps in [-0.5, 0.5) */

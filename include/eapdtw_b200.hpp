@@ -7,9 +7,19 @@
 //   eapdtw::ea_pruned_dtw_windowed (dtw.hpp:93-99)  -> eapdtw_b200::ea_pruned_dtw_windowed
 //   eapdtw::ea_pruned_dtw          (dtw.hpp:85-87)  -> eapdtw_b200::ea_pruned_dtw
 //   eapdtw::dtw_windowed           (dtw.hpp:72-74)  -> eapdtw_b200::dtw_windowed
-//   eapdtw::dtw_left_prune(_windowed) (dtw.hpp:76-83) -> same names (identical results:
-//        exact value iff <= ub, else PRUNED; the GPU kernel prunes from both sides)
+//   eapdtw::dtw_left_prune(_windowed) (dtw.hpp:76-83) -> same names (the GPU
+//        left-pruning schedule, left_prune_scan dtw.cpp:130-182)
 //   eapdtw::similarity_search      (search.hpp:118-119) -> eapdtw_b200::similarity_search
+//   lower_bounds.hpp (Envelope, compute_envelope, lb_kim_fl, BoundResult,
+//        lb_keogh, cumulative_bound), search.hpp (RunningStats,
+//        znormalize_into, cascade_decision, tighten_threshold) and io.hpp's
+//        random_walk -> same names.
+// Every overload that takes a KernelTrace runs the device trace kernel
+// (eapdtw_trace: one thread, the reference's schedule and event order), so
+// cells_evaluated, discard / pruning points and the abandon cell have the
+// reference's meaning; the other overloads run the production kernels.
+// include/compat/eapdtw/*.hpp map the reference's include paths and
+// namespace onto this header.
 // Invalid input throws std::invalid_argument exactly where the reference does;
 // a CUDA failure throws std::runtime_error.  There is no CPU fallback.
 #pragma once
@@ -75,6 +85,12 @@ class Series {
   std::vector<double> samples_;
 };
 
+// dtw.hpp:60-63
+[[nodiscard]] inline double squared_cost(double a, double b) {
+  const double d = a - b;
+  return d * d;
+}
+
 // dtw.hpp:16-23
 struct Band {
   static constexpr std::size_t unbounded_window = EAPDTW_UNBOUNDED_WINDOW;
@@ -90,6 +106,7 @@ struct Band {
 struct CellRef {
   std::size_t row = 0;
   std::size_t col = 0;
+  friend bool operator==(const CellRef&, const CellRef&) = default;
 };
 struct TraceCell {
   std::size_t row = 0;
@@ -142,7 +159,7 @@ inline double traced(int algo, std::span<const double> a, std::span<const double
                                                    std::span<const double> b, Band band, double ub,
                                                    std::span<const double> cumulative_bound,
                                                    KernelTrace& trace) {
-  if (trace.capture_cells && cumulative_bound.empty())
+  if (cumulative_bound.empty())
     return detail::traced(EAPDTW_ALGO_EA_PRUNED, a, b, band.window, ub, trace);
   double out = PRUNED;
   uint64_t cells = 0;
@@ -155,8 +172,12 @@ inline double traced(int algo, std::span<const double> a, std::span<const double
 [[nodiscard]] inline double ea_pruned_dtw_windowed(std::span<const double> a,
                                                    std::span<const double> b, Band band, double ub,
                                                    std::span<const double> cumulative_bound = {}) {
-  KernelTrace t;
-  return ea_pruned_dtw_windowed(a, b, band, ub, cumulative_bound, t);
+  double out = PRUNED;
+  uint64_t cells = 0;
+  detail::check(eapdtw_ea_pruned_dtw_windowed(detail::context(), a.data(), a.size(), b.data(),
+                                              b.size(), band.window, ub, cumulative_bound.data(),
+                                              cumulative_bound.size(), &out, &cells));
+  return out;
 }
 [[nodiscard]] inline double ea_pruned_dtw(std::span<const double> a, std::span<const double> b,
                                           double ub) {
@@ -168,18 +189,15 @@ inline double traced(int algo, std::span<const double> a, std::span<const double
 }
 [[nodiscard]] inline double dtw_windowed(std::span<const double> a, std::span<const double> b,
                                          Band band, KernelTrace& trace) {
-  if (trace.capture_cells) return detail::traced(EAPDTW_ALGO_FULL, a, b, band.window, PRUNED, trace);
+  return detail::traced(EAPDTW_ALGO_FULL, a, b, band.window, PRUNED, trace);
+}
+[[nodiscard]] inline double dtw_windowed(std::span<const double> a, std::span<const double> b,
+                                         Band band) {
   double out = PRUNED;
   uint64_t cells = 0;
   detail::check(eapdtw_dtw_windowed(detail::context(), a.data(), a.size(), b.data(), b.size(),
                                     band.window, &out, &cells));
-  trace.cells_evaluated += cells;
   return out;
-}
-[[nodiscard]] inline double dtw_windowed(std::span<const double> a, std::span<const double> b,
-                                         Band band) {
-  KernelTrace t;
-  return dtw_windowed(a, b, band, t);
 }
 [[nodiscard]] inline double dtw_full(std::span<const double> a, std::span<const double> b) {
   return dtw_windowed(a, b, Band::unbounded());
@@ -188,23 +206,25 @@ inline double traced(int algo, std::span<const double> a, std::span<const double
                                      KernelTrace& trace) {
   return dtw_windowed(a, b, Band::unbounded(), trace);
 }
-// Left pruning has EAPrunedDTW's result contract (exact iff <= ub, else
-// PRUNED); without capture it runs the pruned kernel.
+// Left pruning (left_prune_scan, dtw.cpp:130-182): the GPU's left-border-only
+// schedule; same result contract as EAPrunedDTW (exact iff <= ub, else PRUNED).
 [[nodiscard]] inline double dtw_left_prune_windowed(std::span<const double> a,
                                                     std::span<const double> b, Band band,
                                                     double ub, KernelTrace& trace) {
-  if (trace.capture_cells)
-    return detail::traced(EAPDTW_ALGO_LEFT_PRUNE, a, b, band.window, ub, trace);
-  return ea_pruned_dtw_windowed(a, b, band, ub, {}, trace);
+  return detail::traced(EAPDTW_ALGO_LEFT_PRUNE, a, b, band.window, ub, trace);
 }
 [[nodiscard]] inline double dtw_left_prune_windowed(std::span<const double> a,
                                                     std::span<const double> b, Band band,
                                                     double ub) {
-  return ea_pruned_dtw_windowed(a, b, band, ub);
+  double out = PRUNED;
+  uint64_t cells = 0;
+  detail::check(eapdtw_dtw_left_prune_windowed(detail::context(), a.data(), a.size(), b.data(),
+                                               b.size(), band.window, ub, &out, &cells));
+  return out;
 }
 [[nodiscard]] inline double dtw_left_prune(std::span<const double> a, std::span<const double> b,
                                            double ub) {
-  return ea_pruned_dtw_windowed(a, b, Band::unbounded(), ub);
+  return dtw_left_prune_windowed(a, b, Band::unbounded(), ub);
 }
 [[nodiscard]] inline double dtw_left_prune(std::span<const double> a, std::span<const double> b,
                                            double ub, KernelTrace& trace) {
@@ -226,14 +246,136 @@ inline double traced(int algo, std::span<const double> a, std::span<const double
 [[nodiscard]] inline double dtw_full(const Series& a, const Series& b) {
   return dtw_full(a.view(), b.view());
 }
+[[nodiscard]] inline double dtw_left_prune(const Series& a, const Series& b, double ub) {
+  return dtw_left_prune(a.view(), b.view(), ub);
+}
+[[nodiscard]] inline double ea_pruned_dtw(const Series& a, const Series& b, double ub,
+                                          KernelTrace& trace) {
+  return ea_pruned_dtw(a.view(), b.view(), ub, trace);
+}
+[[nodiscard]] inline double dtw_left_prune(const Series& a, const Series& b, double ub,
+                                           KernelTrace& trace) {
+  return dtw_left_prune(a.view(), b.view(), ub, trace);
+}
 
-// --- search (search.hpp:50-119)
+// --- lower bounds (lower_bounds.hpp:12-63), on the device
+struct Envelope {
+  std::vector<double> upper;
+  std::vector<double> lower;
+  std::size_t window = 0;
+  [[nodiscard]] std::size_t length() const { return upper.size(); }
+};
+[[nodiscard]] inline Envelope compute_envelope(std::span<const double> series, Band band) {
+  Envelope env;
+  env.upper.resize(series.size());
+  env.lower.resize(series.size());
+  detail::check(eapdtw_compute_envelope(detail::context(), series.data(), series.size(), band.window,
+                                        env.upper.data(), env.lower.data()));
+  env.window = band.is_unbounded() ? series.size() : std::min(band.window, series.size());
+  return env;
+}
+[[nodiscard]] inline Envelope compute_envelope(const Series& series, Band band) {
+  return compute_envelope(series.view(), band);
+}
+[[nodiscard]] inline double lb_kim_fl(std::span<const double> q, std::span<const double> c) {
+  if (q.size() != c.size()) throw std::invalid_argument("lb_kim_fl: length mismatch");
+  double out = 0.0;
+  detail::check(eapdtw_lb_kim_fl(detail::context(), q.data(), c.data(), q.size(), &out));
+  return out;
+}
+[[nodiscard]] inline double lb_kim_fl(const Series& q, const Series& c) {
+  return lb_kim_fl(q.view(), c.view());
+}
+struct BoundResult {
+  double total = 0.0;
+  std::vector<double> contributions;
+  bool abandoned = false;
+};
+[[nodiscard]] inline BoundResult lb_keogh(const Envelope& env, std::span<const double> series,
+                                          double abandon_above = PRUNED,
+                                          std::span<const std::size_t> order = {}) {
+  if (env.upper.size() != env.lower.size()) throw std::invalid_argument("lb_keogh: malformed envelope");
+  if (env.length() != series.size()) throw std::invalid_argument("lb_keogh: length mismatch");
+  if (!order.empty() && order.size() != series.size())
+    throw std::invalid_argument("lb_keogh: order/series length mismatch");
+  BoundResult res;
+  res.contributions.assign(series.size(), 0.0);
+  int ab = 0;
+  detail::check(eapdtw_lb_keogh(detail::context(), env.upper.data(), env.lower.data(),
+                                series.data(), series.size(), abandon_above,
+                                order.empty() ? nullptr : order.data(), &res.total,
+                                res.contributions.data(), &ab));
+  res.abandoned = ab != 0;
+  return res;
+}
+[[nodiscard]] inline BoundResult lb_keogh(const Envelope& env, const Series& series,
+                                          double abandon_above = PRUNED,
+                                          std::span<const std::size_t> order = {}) {
+  return lb_keogh(env, series.view(), abandon_above, order);
+}
+[[nodiscard]] inline std::vector<double> cumulative_bound(std::span<const double> contributions) {
+  std::vector<double> cb(contributions.size(), 0.0);
+  detail::check(eapdtw_cumulative_bound(detail::context(), contributions.data(),
+                                        contributions.size(), cb.data()));
+  return cb;
+}
+
+// --- search (search.hpp:16-119)
+struct RunningStats {  // search.hpp:16-42
+  double sum = 0.0;
+  double sum_of_squares = 0.0;
+  std::size_t count = 0;
+  [[nodiscard]] static RunningStats over(std::span<const double> window) {
+    RunningStats s;
+    detail::check(eapdtw_running_stats_over(window.data(), window.size(), &s.sum,
+                                            &s.sum_of_squares));
+    s.count = window.size();
+    return s;
+  }
+  void add(double x) {
+    sum += x;
+    sum_of_squares += x * x;
+    ++count;
+  }
+  void remove(double x) {
+    sum -= x;
+    sum_of_squares -= x * x;
+    --count;
+  }
+  [[nodiscard]] double mean() const { return sum / static_cast<double>(count); }
+  [[nodiscard]] double variance() const {
+    const double m = mean();
+    const double v = sum_of_squares / static_cast<double>(count) - m * m;
+    return v > 0.0 ? v : 0.0;
+  }
+  [[nodiscard]] double stddev() const { return std::sqrt(variance()); }
+};
+// search.hpp:46 (search.cpp:37-46)
+inline void znormalize_into(std::span<const double> src, const RunningStats& stats,
+                            std::span<double> dst) {
+  detail::check(eapdtw_znormalize_into(src.data(), src.size(), stats.sum, stats.sum_of_squares,
+                                       stats.count, dst.data()));
+}
+[[nodiscard]] inline Series znormalize(const Series& s, const RunningStats& stats) {
+  std::vector<double> out(s.length());
+  znormalize_into(s.view(), stats, out);
+  return Series(std::move(out));
+}
+
 struct BestSoFar {
   std::size_t location = 0;
   double distance_sq = PRUNED;
   bool found = false;
 };
 enum class Algo : std::uint8_t { full, left_prune, ea_pruned };
+[[nodiscard]] inline std::string to_string(Algo a) {  // search.cpp:52-60
+  switch (a) {
+    case Algo::full: return "full";
+    case Algo::left_prune: return "lp";
+    case Algo::ea_pruned: return "eap";
+  }
+  return "?";
+}
 struct SearchConfig {
   std::size_t query_length = 0;
   double window_ratio = 0.1;
@@ -268,6 +410,68 @@ struct SearchResult {
   out.report = {r.candidates_total, r.pruned_kim,  r.pruned_keogh_eq,   r.pruned_keogh_ec,
                 r.dtw_calls,        r.dtw_abandoned, r.dp_cells_evaluated, r.elapsed_seconds};
   return out;
+}
+
+// search.hpp:85-114: the cascade of one candidate, composed from the device
+// helpers above in the reference's order (search.cpp:63-107).
+enum class CascadeTier : std::uint8_t { none, kim, keogh_eq, keogh_ec };
+struct CascadeWorkspace {
+  std::vector<double> candidate_norm;
+  std::vector<double> contrib_eq;
+  std::vector<double> contrib_ec;
+  std::vector<double> cumulative;
+};
+[[nodiscard]] inline CascadeTier cascade_decision(std::span<const double> query_norm,
+                                                  const Envelope& query_env,
+                                                  std::span<const std::size_t> order,
+                                                  std::span<const double> candidate_raw,
+                                                  const RunningStats& stats, const BestSoFar& bsf,
+                                                  const SearchConfig& cfg, CascadeWorkspace& ws) {
+  const std::size_t m = query_norm.size();
+  ws.candidate_norm.resize(m);
+  ws.cumulative.clear();
+  if (!cfg.use_lower_bounds) {
+    znormalize_into(candidate_raw, stats, ws.candidate_norm);
+    return CascadeTier::none;
+  }
+  const double ub = bsf.found ? bsf.distance_sq : PRUNED;
+  const double mean = stats.mean();
+  const double sd = stats.stddev();
+  const bool constant = sd < 1e-12;  // kMinStddev, search.cpp:13
+  if (m >= 2) {
+    const double c0 = constant ? 0.0 : (candidate_raw.front() - mean) / sd;
+    const double cl = constant ? 0.0 : (candidate_raw.back() - mean) / sd;
+    const double kim = squared_cost(query_norm.front(), c0) + squared_cost(query_norm.back(), cl);
+    if (kim > ub) return CascadeTier::kim;
+  }
+  znormalize_into(candidate_raw, stats, ws.candidate_norm);
+  const BoundResult eq = lb_keogh(query_env, ws.candidate_norm, ub, order);
+  if (eq.total > ub) return CascadeTier::keogh_eq;
+  ws.contrib_eq = eq.contributions;
+  const Envelope cand_env = compute_envelope(ws.candidate_norm, Band::cells(query_env.window));
+  const BoundResult ec = lb_keogh(cand_env, query_norm, ub, order);
+  if (ec.total > ub) return CascadeTier::keogh_ec;
+  ws.contrib_ec = ec.contributions;
+  if (cfg.tighten_ub) {
+    const auto& contrib = eq.total > ec.total ? ws.contrib_eq : ws.contrib_ec;
+    ws.cumulative = cumulative_bound(contrib);
+  }
+  return CascadeTier::none;
+}
+[[nodiscard]] inline double tighten_threshold(const BestSoFar& bsf, std::span<const double> cb,
+                                              std::size_t row, std::size_t window_cells) {
+  if (cb.empty()) return bsf.distance_sq;  // search.cpp:109-115
+  const std::size_t k = std::min(row + window_cells, cb.size());
+  const double t = bsf.distance_sq - cb[k - 1];
+  return t > 0.0 ? t : 0.0;
+}
+
+// io.hpp:33: seeded random walk, uniform steps in [-0.5, 0.5) (io.cpp:124-137)
+[[nodiscard]] inline Series random_walk(std::size_t length, std::uint64_t seed) {
+  if (length == 0) throw std::invalid_argument("random_walk: zero length");
+  std::vector<double> v(length);
+  detail::check(eapdtw_random_walk_uniform(length, seed, v.data()));
+  return Series(std::move(v));
 }
 
 }  // namespace eapdtw_b200

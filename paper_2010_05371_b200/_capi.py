@@ -52,6 +52,7 @@ class SearchResultC(C.Structure):
         ("dtw_abandoned", C.c_uint64),
         ("dp_cells_evaluated", C.c_uint64),
         ("elapsed_seconds", C.c_double),
+        ("screen_cells_evaluated", C.c_uint64),
     ]
 
 
@@ -74,6 +75,17 @@ SIGNATURES = [
       _u64p]),
     ("eapdtw_dtw_windowed", C.c_int,
      [_vp, _dp, C.c_size_t, _dp, C.c_size_t, C.c_size_t, _dp, _u64p]),
+    ("eapdtw_dtw_left_prune_windowed", C.c_int,
+     [_vp, _dp, C.c_size_t, _dp, C.c_size_t, C.c_size_t, C.c_double, _dp, _u64p]),
+    ("eapdtw_compute_envelope", C.c_int, [_vp, _dp, C.c_size_t, C.c_size_t, _dp, _dp]),
+    ("eapdtw_lb_kim_fl", C.c_int, [_vp, _dp, _dp, C.c_size_t, _dp]),
+    ("eapdtw_lb_keogh", C.c_int,
+     [_vp, _dp, _dp, _dp, C.c_size_t, C.c_double, C.POINTER(C.c_size_t), _dp, _dp,
+      C.POINTER(C.c_int)]),
+    ("eapdtw_cumulative_bound", C.c_int, [_vp, _dp, C.c_size_t, _dp]),
+    ("eapdtw_running_stats_over", C.c_int, [_dp, C.c_size_t, _dp, _dp]),
+    ("eapdtw_znormalize_into", C.c_int,
+     [_dp, C.c_size_t, C.c_double, C.c_double, C.c_uint64, _dp]),
     ("eapdtw_trace", C.c_int,
      [_vp, C.c_int, _dp, C.c_size_t, _dp, C.c_size_t, C.c_size_t, C.c_double, _vp, C.c_size_t,
       C.POINTER(C.c_size_t), _u64p, _dp]),

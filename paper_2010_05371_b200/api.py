@@ -134,8 +134,9 @@ class SearchReport:
     pruned_keogh_ec: int = 0
     dtw_calls: int = 0
     dtw_abandoned: int = 0
-    dp_cells_evaluated: int = 0
+    dp_cells_evaluated: int = 0  # cells of the exact DP (dtw.cpp:28-33 counts its kernel's cells)
     elapsed_seconds: float = 0.0
+    screen_cells_evaluated: int = 0  # cells of the FP32 screening pass (GPU only)
 
 
 @dataclass
@@ -151,7 +152,8 @@ class SearchResult:
             BestSoFar(int(r.location), float(r.distance_sq), bool(r.found)),
             SearchReport(int(r.candidates_total), int(r.pruned_kim), int(r.pruned_keogh_eq),
                          int(r.pruned_keogh_ec), int(r.dtw_calls), int(r.dtw_abandoned),
-                         int(r.dp_cells_evaluated), float(r.elapsed_seconds)))
+                         int(r.dp_cells_evaluated), float(r.elapsed_seconds),
+                         int(r.screen_cells_evaluated)))
 
 
 class Context:
@@ -296,6 +298,145 @@ def dtw_windowed(a, b, band, *, ctx=None, return_cells: bool = False):
     check(lib.eapdtw_dtw_windowed(ctx.handle, _ptr(a), a.size, _ptr(b), b.size, _window(band),
                                   C.byref(out), C.byref(cells)))
     return (out.value, cells.value) if return_cells else out.value
+
+
+def dtw_left_prune_windowed(a, b, band, ub: float, *, ctx=None, return_cells: bool = False):
+    """dtw.hpp:76-83: left_prune_scan (dtw.cpp:130-182) -- pruning from the
+    left only; exact value iff <= ub, else PRUNED."""
+    ctx = ctx or default_context()
+    a, b = _as_f64(a), _as_f64(b)
+    out = C.c_double()
+    cells = C.c_uint64(0)
+    check(lib.eapdtw_dtw_left_prune_windowed(ctx.handle, _ptr(a), a.size, _ptr(b), b.size,
+                                             _window(band), float(ub), C.byref(out),
+                                             C.byref(cells)))
+    return (out.value, cells.value) if return_cells else out.value
+
+
+def dtw_left_prune(a, b, ub: float, *, ctx=None, return_cells: bool = False):
+    """dtw.hpp:76-79 (unbounded band)."""
+    return dtw_left_prune_windowed(a, b, Band.unbounded(), ub, ctx=ctx, return_cells=return_cells)
+
+
+# --- lower bounds (lower_bounds.hpp:12-63), computed on the device ----------
+
+@dataclass
+class Envelope:
+    """lower_bounds.hpp:15-21"""
+
+    upper: np.ndarray
+    lower: np.ndarray
+    window: int = 0
+
+    def length(self) -> int:
+        return int(self.upper.size)
+
+
+@dataclass
+class BoundResult:
+    """lower_bounds.hpp:42-46"""
+
+    total: float = 0.0
+    contributions: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    abandoned: bool = False
+
+
+def compute_envelope(series, band, *, ctx=None) -> Envelope:
+    """lower_bounds.hpp:25 -- sliding max/min over [j-w, j+w] clamped to the
+    series (an unbounded band: the whole series)."""
+    ctx = ctx or default_context()
+    x = _as_f64(series)
+    up = np.empty(x.size)
+    lo = np.empty(x.size)
+    w = _window(band)
+    check(lib.eapdtw_compute_envelope(ctx.handle, _ptr(x), x.size, w, _ptr(up), _ptr(lo)))
+    return Envelope(up, lo, x.size if w == UNBOUNDED_WINDOW else min(w, x.size))
+
+
+def lb_kim_fl(q, c, *, ctx=None) -> float:
+    """lower_bounds.hpp:33 / lower_bounds.cpp:51-55"""
+    ctx = ctx or default_context()
+    q, c = _as_f64(q), _as_f64(c)
+    if q.size != c.size:
+        raise ValueError("lb_kim_fl: length mismatch")
+    out = C.c_double()
+    check(lib.eapdtw_lb_kim_fl(ctx.handle, _ptr(q), _ptr(c), q.size, C.byref(out)))
+    return out.value
+
+
+def lb_keogh(env: Envelope, series, abandon_above: float = PRUNED, order=None, *,
+             ctx=None) -> BoundResult:
+    """lower_bounds.hpp:52-54 / lower_bounds.cpp:57-88 (visiting order, strict
+    abandon)."""
+    ctx = ctx or default_context()
+    x = _as_f64(series)
+    up, lo = _as_f64(env.upper), _as_f64(env.lower)
+    if up.size != lo.size:
+        raise ValueError("lb_keogh: malformed envelope")
+    po = None
+    if order is not None and len(order) > 0:
+        o = np.ascontiguousarray(np.asarray(order, dtype=np.uint64))
+        po = o.ctypes.data_as(C.POINTER(C.c_size_t))
+        n_order = o.size
+    else:
+        n_order = 0
+    if n_order not in (0, x.size):
+        raise ValueError("lb_keogh: order/series length mismatch")
+    total = C.c_double()
+    contrib = np.zeros(x.size)
+    ab = C.c_int(0)
+    if up.size != x.size:
+        raise ValueError("lb_keogh: length mismatch")
+    check(lib.eapdtw_lb_keogh(ctx.handle, _ptr(up), _ptr(lo), _ptr(x), x.size,
+                              float(abandon_above), po, C.byref(total), _ptr(contrib),
+                              C.byref(ab)))
+    return BoundResult(total.value, contrib, bool(ab.value))
+
+
+def cumulative_bound(contributions, *, ctx=None) -> np.ndarray:
+    """lower_bounds.hpp:63 / lower_bounds.cpp:90-103: cb[i] = sum_{j>i} c[j]."""
+    ctx = ctx or default_context()
+    c = _as_f64(contributions)
+    cb = np.zeros(c.size)
+    if c.size:
+        check(lib.eapdtw_cumulative_bound(ctx.handle, _ptr(c), c.size, _ptr(cb)))
+    return cb
+
+
+@dataclass
+class RunningStats:
+    """search.hpp:16-42"""
+
+    sum: float = 0.0
+    sum_of_squares: float = 0.0
+    count: int = 0
+
+    @staticmethod
+    def over(window) -> "RunningStats":
+        x = _as_f64(window)
+        s, q = C.c_double(), C.c_double()
+        check(lib.eapdtw_running_stats_over(_ptr(x), x.size, C.byref(s), C.byref(q)))
+        return RunningStats(s.value, q.value, x.size)
+
+    def mean(self) -> float:
+        return self.sum / float(self.count)
+
+    def variance(self) -> float:
+        m = self.mean()
+        v = self.sum_of_squares / float(self.count) - m * m
+        return v if v > 0.0 else 0.0
+
+    def stddev(self) -> float:
+        return math.sqrt(self.variance())
+
+
+def znormalize_into(src, stats: RunningStats) -> np.ndarray:
+    """search.hpp:46 / search.cpp:37-46 with the given statistics."""
+    x = _as_f64(src)
+    out = np.empty(x.size)
+    check(lib.eapdtw_znormalize_into(_ptr(x), x.size, float(stats.sum),
+                                     float(stats.sum_of_squares), int(stats.count), _ptr(out)))
+    return out
 
 
 def dtw_full(a, b, *, ctx=None):

@@ -393,7 +393,7 @@ static int single_pair(eapdtw_ctx* c, const double* a, size_t la, const double* 
     lr = lb;
     lc = la;
   }
-  if (prune) {
+  if (prune == 1) {
     const int e = check_cb_host(cb, cb_len, lr);
     if (e) return e;
   }
@@ -411,7 +411,7 @@ static int single_pair(eapdtw_ctx* c, const double* a, size_t la, const double* 
   CUDA_TRY(cudaMemcpyAsync(c->b.p, cols, lc * 8, cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(cudaMemcpyAsync(c->ub.p, &ub, 8, cudaMemcpyHostToDevice, c->stream));
   const double* cb_dev = nullptr;
-  if (prune && cb_len) {
+  if (prune == 1 && cb_len) {
     CUDA_TRY(c->cb.ensure(cb_len * 8));
     CUDA_TRY(cudaMemcpyAsync(c->cb.p, cb, cb_len * 8, cudaMemcpyHostToDevice, c->stream));
     cb_dev = c->cb.as<double>();
@@ -435,6 +435,12 @@ int eapdtw_ea_pruned_dtw_windowed(eapdtw_ctx* c, const double* a, size_t la, con
 int eapdtw_dtw_windowed(eapdtw_ctx* c, const double* a, size_t la, const double* b, size_t lb,
                         size_t window, double* out, uint64_t* cells) {
   return single_pair(c, a, la, b, lb, window, kInf, nullptr, 0, 0, out, cells);
+}
+
+int eapdtw_dtw_left_prune_windowed(eapdtw_ctx* c, const double* a, size_t la, const double* b,
+                                   size_t lb, size_t window, double ub, double* out,
+                                   uint64_t* cells) {
+  return single_pair(c, a, la, b, lb, window, ub, nullptr, 0, 2, out, cells);
 }
 
 int eapdtw_trace(eapdtw_ctx* c, int algo, const double* a, size_t la, const double* b, size_t lb,
@@ -766,7 +772,8 @@ static SearchParams base_params(eapdtw_search_plan* p) {
   s.use_lb = p->use_lb ? 1 : 0;
   s.tighten = p->tighten ? 1 : 0;
   s.cb_strip = p->cb_strip;
-  s.prune = p->algo == EAPDTW_ALGO_FULL ? 0 : 1;
+  // 0 full_scan, 1 EAPrunedDTW, 2 left_prune_scan (dtw.cpp:95-296)
+  s.prune = p->algo == EAPDTW_ALGO_FULL ? 0 : (p->algo == EAPDTW_ALGO_LEFT_PRUNE ? 2 : 1);
   s.guard_rel = p->guard_rel;
   s.guard_abs = p->guard_abs;
   // 2 * 3u * sqrt(m) * cmax, cmax = sqrt(m) + 1 + qmax (z-normalised windows
@@ -1028,8 +1035,12 @@ int eapdtw_search_plan_result(eapdtw_search_plan* p, eapdtw_search_result* out) 
   out->pruned_keogh_ec = cnt[kCntKeoghEc];
   out->dtw_calls = cnt[kCntDtwCalls];
   out->dtw_abandoned = cnt[kCntDtwAbandoned];
-  // cells of both engines (the FP32 screen and the exact FP64 pass)
-  out->dp_cells_evaluated = cnt[kCntCells] + pc[kCntCells] + cnt[kCntCellsF32] + pc[kCntCellsF32];
+  // dp_cells_evaluated: cells of the exact DP (the FP64 engines and the
+  // phase-A lane screen, which is an exact prefix of the same DP), as the
+  // reference counts its kernel's cells (dtw.cpp:28-33); the FP32 screen's
+  // cells are reported apart
+  out->dp_cells_evaluated = cnt[kCntCells] + pc[kCntCells];
+  out->screen_cells_evaluated = cnt[kCntCellsF32] + pc[kCntCellsF32];
   out->elapsed_seconds =
       std::chrono::duration<double>(std::chrono::steady_clock::now() - p->t0).count();
 #ifdef EAPDTW_PHASE_CLOCKS
@@ -1530,8 +1541,139 @@ int eapdtw_sliding_envelope(eapdtw_ctx* c, const double* ref, size_t n, size_t r
 }
 
 // ---------------------------------------------------------------------------
+// The reference's lower-bound API (lower_bounds.hpp:12-63) on the device
+// ---------------------------------------------------------------------------
+int eapdtw_compute_envelope(eapdtw_ctx* c, const double* series, size_t l, size_t window,
+                            double* upper, double* lower) {
+  if (!c || !upper || !lower) return fail(EAPDTW_EINVAL, "null argument");
+  if (l == 0 || !series) return fail(EAPDTW_EINVAL, "compute_envelope: empty series");
+  const size_t w = window == EAPDTW_UNBOUNDED_WINDOW ? l : std::min(window, l);
+  CUDA_TRY(cudaSetDevice(c->device));
+  const size_t scr = envelope_any_scratch_doubles(static_cast<long long>(l), static_cast<long long>(w));
+  DevBuf dx, denv, dscr;
+  auto done = [&](int rc) {
+    dx.release();
+    denv.release();
+    dscr.release();
+    return rc;
+  };
+  std::vector<double> env(2 * l);
+  cudaError_t e = dx.ensure(l * 8);
+  if (!e) e = denv.ensure(2 * l * 8);
+  if (!e && scr) e = dscr.ensure(scr * 8);
+  if (!e) e = cudaMemcpyAsync(dx.p, series, l * 8, cudaMemcpyHostToDevice, c->stream);
+  if (!e) e = launch_envelope_any(dx.as<double>(), static_cast<long long>(l), static_cast<long long>(w),
+                                  denv.as<double>(), dscr.as<double>(), c->stream);
+  if (!e) ++c->launches;
+  if (!e) e = cudaMemcpyAsync(env.data(), denv.p, 2 * l * 8, cudaMemcpyDeviceToHost, c->stream);
+  if (!e) e = cudaStreamSynchronize(c->stream);
+  if (e) return done(fail(EAPDTW_ECUDA, std::string("compute_envelope: ") + cudaGetErrorString(e)));
+  for (size_t k = 0; k < l; ++k) {
+    upper[k] = env[2 * k];
+    lower[k] = env[2 * k + 1];
+  }
+  return done(EAPDTW_OK);
+}
+
+int eapdtw_lb_kim_fl(eapdtw_ctx* c, const double* q, const double* cs, size_t l, double* out) {
+  if (!c || !out || !q || !cs) return fail(EAPDTW_EINVAL, "null argument");
+  if (l < 2) return fail(EAPDTW_EINVAL, "lb_kim_fl: series must have length >= 2");
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(c->a.ensure(l * 8));
+  CUDA_TRY(c->b.ensure(l * 8));
+  CUDA_TRY(c->out.ensure(8));
+  CUDA_TRY(cudaMemcpyAsync(c->a.p, q, l * 8, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->b.p, cs, l * 8, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(launch_lb_kim_fl(c->a.as<double>(), c->b.as<double>(), static_cast<long long>(l),
+                            c->out.as<double>(), c->stream));
+  ++c->launches;
+  CUDA_TRY(cudaMemcpyAsync(out, c->out.p, 8, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return EAPDTW_OK;
+}
+
+int eapdtw_lb_keogh(eapdtw_ctx* c, const double* upper, const double* lower, const double* series,
+                    size_t l, double abandon_above, const size_t* order, double* total,
+                    double* contributions, int* abandoned) {
+  if (!c || !total || !abandoned) return fail(EAPDTW_EINVAL, "null argument");
+  if (l > 0 && (!upper || !lower || !series)) return fail(EAPDTW_EINVAL, "null argument");
+  if (order)
+    for (size_t k = 0; k < l; ++k)
+      if (order[k] >= l) return fail(EAPDTW_EINVAL, "lb_keogh: order index out of range");
+  *total = 0.0;
+  *abandoned = 0;
+  if (contributions) std::fill(contributions, contributions + l, 0.0);
+  if (l == 0) return EAPDTW_OK;
+  CUDA_TRY(cudaSetDevice(c->device));
+  // a: upper | lower | series | contributions; b: order; out: total, abandoned
+  CUDA_TRY(c->a.ensure(4 * l * 8));
+  CUDA_TRY(c->b.ensure(l * 8));
+  CUDA_TRY(c->out.ensure(16));
+  double* d = c->a.as<double>();
+  CUDA_TRY(cudaMemcpyAsync(d, upper, l * 8, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(d + l, lower, l * 8, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(d + 2 * l, series, l * 8, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemsetAsync(d + 3 * l, 0, l * 8, c->stream));
+  const unsigned long long* dorder = nullptr;
+  static_assert(sizeof(size_t) == sizeof(unsigned long long), "size_t is 64-bit");
+  if (order) {
+    CUDA_TRY(cudaMemcpyAsync(c->b.p, order, l * 8, cudaMemcpyHostToDevice, c->stream));
+    dorder = c->b.as<unsigned long long>();
+  }
+  double* dout = c->out.as<double>();
+  CUDA_TRY(launch_lb_keogh(d, d + l, d + 2 * l, static_cast<long long>(l), abandon_above, dorder,
+                           dout, d + 3 * l, reinterpret_cast<int*>(dout + 1), c->stream));
+  ++c->launches;
+  double res[2];
+  CUDA_TRY(cudaMemcpyAsync(res, dout, 16, cudaMemcpyDeviceToHost, c->stream));
+  if (contributions)
+    CUDA_TRY(cudaMemcpyAsync(contributions, d + 3 * l, l * 8, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  *total = res[0];
+  int ab = 0;
+  std::memcpy(&ab, &res[1], sizeof(int));
+  *abandoned = ab;
+  return EAPDTW_OK;
+}
+
+int eapdtw_cumulative_bound(eapdtw_ctx* c, const double* contributions, size_t l, double* cb) {
+  if (!c || (l > 0 && (!contributions || !cb))) return fail(EAPDTW_EINVAL, "null argument");
+  if (l == 0) return EAPDTW_OK;
+  // lower_bounds.cpp:93-99: every contribution must be non-negative
+  for (size_t k = 0; k < l; ++k)
+    if (contributions[k] < 0.0) return fail(EAPDTW_EINVAL, "cumulative_bound: negative contribution");
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(c->a.ensure(2 * l * 8));
+  double* d = c->a.as<double>();
+  CUDA_TRY(cudaMemcpyAsync(d, contributions, l * 8, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(launch_cumulative_bound(d, static_cast<long long>(l), d + l, c->stream));
+  ++c->launches;
+  CUDA_TRY(cudaMemcpyAsync(cb, d + l, l * 8, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return EAPDTW_OK;
+}
+
+// ---------------------------------------------------------------------------
 // Host helpers
 // ---------------------------------------------------------------------------
+int eapdtw_running_stats_over(const double* x, size_t n, double* sum, double* sumsq) {
+  if (!sum || !sumsq || (n > 0 && !x)) return fail(EAPDTW_EINVAL, "null argument");
+  const HostStats st = HostStats::over(x, n);
+  *sum = st.sum;
+  *sumsq = st.sumsq;
+  return EAPDTW_OK;
+}
+
+int eapdtw_znormalize_into(const double* src, size_t n, double sum, double sumsq, uint64_t count,
+                           double* dst) {
+  if (n > 0 && (!src || !dst)) return fail(EAPDTW_EINVAL, "null argument");
+  HostStats st;
+  st.sum = sum;
+  st.sumsq = sumsq;
+  st.count = static_cast<size_t>(count);
+  host_znormalize(src, n, st, dst);
+  return EAPDTW_OK;
+}
 int eapdtw_znormalize(const double* src, size_t n, double* dst) {
   if (!src || !dst || n == 0) return fail(EAPDTW_EINVAL, "znormalize: empty input");
   host_znormalize(src, n, HostStats::over(src, n), dst);

@@ -104,7 +104,12 @@ __device__ __forceinline__ double load_ub(const unsigned long long* key) {
 //                 called once per strip by every lane (i0: the strip's first row)
 //   rowbuf     : padded per-warp scratch (see contract above)
 //   cells      : incremented (by lane 0) with the number of evaluated cells
-template <bool KILL, class RawFn, class NormFn, class UbFn, class RowThrFn>
+// LEFT: pruning from the left only -- left_prune_scan (dtw.cpp:130-182): a
+// row starts at the first live column of the row above (next_start) and is
+// evaluated to the end of its band (no right border from dead cells); an
+// all-dead row abandons.  Same result contract (exact iff <= ub, else +inf),
+// more cells than EAPrunedDTW.
+template <bool KILL, bool LEFT = false, class RawFn, class NormFn, class UbFn, class RowThrFn>
 __device__ double warp_dtw(const RawFn& rowraw, const NormFn& rownorm, int lr,
                            const double* __restrict__ qsp, int lc, int w, UbFn&& get_ub,
                            RowThrFn&& rowthr, double* __restrict__ rowbuf,
@@ -192,7 +197,7 @@ __device__ double warp_dtw(const RawFn& rowraw, const NormFn& rownorm, int lr,
       if (writer) rp[u] = nv;
       v = nv;
       const unsigned dm = __ballot_sync(kFull, dead);
-      finmask |= dm & ((finmask << 1) | (j0 + u > hi ? 1u : 0u));
+      if (!LEFT) finmask |= dm & ((finmask << 1) | (j0 + u > hi ? 1u : 0u));
     };
 
     for (;;) {

@@ -378,12 +378,12 @@ int choose_ad_k(int n, int w) {
 // One exact pruned DTW with the whole warp: the anti-diagonal engine with
 // window 64*ad_k first, the strip engine when the live region overflows it
 // (or ad_k == 0).  Both share `buf` (their DP scratch).
-template <bool KILL, class RawFn, class NormFn, class UbFn, class RowThrFn>
+template <bool KILL, bool LEFT = false, class RawFn, class NormFn, class UbFn, class RowThrFn>
 __device__ double dtw_dispatch(int ad_k, const RawFn& rowraw, const NormFn& rownorm, int lr,
                                const double* qsp, int lc, int w, UbFn&& get_ub, RowThrFn&& rowthr,
                                double* buf, unsigned long long& cells,
                                unsigned long long& overflows) {
-  if (!KILL && ad_k > 0) {
+  if (!KILL && !LEFT && ad_k > 0) {
     double r = d_inf();
     int st = kAdOverflow;
     // odd K: lanes read shared memory at an odd 8-byte stride, i.e. without
@@ -395,7 +395,7 @@ __device__ double dtw_dispatch(int ad_k, const RawFn& rowraw, const NormFn& rown
     ++overflows;
     __syncwarp();
   }
-  return warp_dtw<KILL>(rowraw, rownorm, lr, qsp, lc, w, get_ub, rowthr, buf, cells);
+  return warp_dtw<KILL, LEFT>(rowraw, rownorm, lr, qsp, lc, w, get_ub, rowthr, buf, cells);
 }
 
 // Pruning threshold of the guarded lower bounds (Kim layers, Keogh EQ/EC):
@@ -451,7 +451,10 @@ constexpr int kSearchMinBlocks = EAPDTW_SEARCH_MIN_BLOCKS;
 
 // AD_K: the exact engine's anti-diagonal window compiled into this
 // instantiation (0: strip engine only -- the default search path).
-template <int AD_K>
+// LP: Algo::left_prune searches (p.prune == 2): every DTW call runs the
+// exact left-pruning schedule (no FP32 screen), a separate instantiation so
+// the default kernel's code is untouched.
+template <int AD_K, bool LP = false>
 __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) search_kernel(SearchParams p) {
   extern __shared__ double smem[];
   const int m = p.m;
@@ -645,7 +648,7 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
     // abandons with a sound, error-inflated threshold; whatever it cannot
     // abandon is evaluated exactly below.
     bool screened = false;
-    if (p.use_f32 && prune && __shfl_sync(kFull, load_ub(p.ub_key), 0) < INF) {
+    if (!LP && p.use_f32 && prune && __shfl_sync(kFull, load_ub(p.ub_key), 0) < INF) {
       const F32Guard g{p.f32_a, p.f32_b};
       auto rownorm32 = [&](double x) -> float {
         return cconst ? 0.0f : __double2float_rn(__dmul_rn(__dsub_rn(x, cm), rsd));
@@ -670,8 +673,8 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
       __syncwarp();
     }
     const double d = screened ? INF
-                              : dtw_dispatch<false>(AD_K, rowraw, rownorm, m, qsp, m, p.w, get_ub,
-                                                    rowthr, rowbuf, c_cells, c_ovf);
+                              : dtw_dispatch<false, LP>(AD_K, rowraw, rownorm, m, qsp, m, p.w,
+                                                        get_ub, rowthr, rowbuf, c_cells, c_ovf);
     ++c_calls;
     if (d == INF) {
       ++c_aband;
@@ -1360,6 +1363,7 @@ cudaError_t launch_search(const SearchParams& p, int blocks, int warps, cudaStre
     kern<<<blocks, warps * 32, smem, stream>>>(p);
     return cudaGetLastError();
   };
+  if (p.prune == 2) return go(search_kernel<0, true>);
   switch (p.ad_k) {
     case 1: return go(search_kernel<1>);
     case 3: return go(search_kernel<3>);
@@ -1373,7 +1377,7 @@ cudaError_t launch_search(const SearchParams& p, int blocks, int warps, cudaStre
 // dtw_windowed (dtw.cpp:316-396) over a batch; the caller has oriented the
 // pair (longer series on rows) and resolved effective_window.
 // ---------------------------------------------------------------------------
-template <bool WITH_CB>
+template <bool WITH_CB, bool LEFT>
 __global__ void __launch_bounds__(256) pairwise_kernel(PairParams p) {
   extern __shared__ double smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1409,7 +1413,7 @@ __global__ void __launch_bounds__(256) pairwise_kernel(PairParams p) {
       const double t = __dsub_rn(u, cb[k - 1]);
       return t > 0.0 ? t : 0.0;
     };
-    const double d = dtw_dispatch<WITH_CB>(p.ad_k, rowraw, rownorm, lr, colsp, lc, w, get_ub,
+    const double d = dtw_dispatch<WITH_CB, LEFT>(p.ad_k, rowraw, rownorm, lr, colsp, lc, w, get_ub,
                                            rowthr, rowbuf, cells, ovf);
     if (lane == 0) p.out[pr] = d;
     __syncwarp();
@@ -1425,17 +1429,14 @@ cudaError_t launch_pairwise(const PairParams& p, cudaStream_t stream) {
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   const long long need = (p.npairs + warps - 1) / warps;
   const int blocks = static_cast<int>(min(need, 148LL * 32));
-  cudaError_t e;
-  if (p.cb) {
-    e = ensure_dyn_smem(reinterpret_cast<const void*>(pairwise_kernel<true>), smem);
+  auto go = [&](auto kern) -> cudaError_t {
+    const cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(kern), smem);
     if (e != cudaSuccess) return e;
-    pairwise_kernel<true><<<blocks, warps * 32, smem, stream>>>(p);
-  } else {
-    e = ensure_dyn_smem(reinterpret_cast<const void*>(pairwise_kernel<false>), smem);
-    if (e != cudaSuccess) return e;
-    pairwise_kernel<false><<<blocks, warps * 32, smem, stream>>>(p);
-  }
-  return cudaGetLastError();
+    kern<<<blocks, warps * 32, smem, stream>>>(p);
+    return cudaGetLastError();
+  };
+  if (p.prune == 2) return go(pairwise_kernel<false, true>);  // left pruning only
+  return p.cb ? go(pairwise_kernel<true, false>) : go(pairwise_kernel<false, false>);
 }
 
 // ---------------------------------------------------------------------------

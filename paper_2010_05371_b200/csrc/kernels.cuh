@@ -166,6 +166,18 @@ cudaError_t launch_rank_select(const SearchParams& p, long long S, int wave, lon
                                long long cap, void* scratch, long long* list,
                                unsigned long long* nlist, cudaStream_t stream);
 cudaError_t launch_pairwise(const PairParams& p, cudaStream_t stream);
+// bounds.cu: the reference's single-pair lower-bound helpers on the device
+cudaError_t launch_lb_kim_fl(const double* q, const double* c, long long l, double* out,
+                             cudaStream_t s);
+cudaError_t launch_lb_keogh(const double* up, const double* lo, const double* x, long long l,
+                            double abandon_above, const unsigned long long* order, double* total,
+                            double* contrib, int* abandoned, cudaStream_t s);
+cudaError_t launch_cumulative_bound(const double* c, long long l, double* cb, cudaStream_t s);
+// Sliding (max, min) interleaved in env (2n) for any radius r; scratch holds
+// envelope_any_scratch_doubles(n, r) doubles (0 when the tiled kernel fits).
+size_t envelope_any_scratch_doubles(long long n, long long r);
+cudaError_t launch_envelope_any(const double* x, long long n, long long r, double* env,
+                                double* scratch, cudaStream_t s);
 cudaError_t launch_nn1(const Nn1Params& p, cudaStream_t stream);
 cudaError_t launch_init_best(BestRecord* rec, unsigned long long* keys, long long count,
                              cudaStream_t stream);
