@@ -31,6 +31,7 @@ extern "C" {
 #define EAPDTW_EINVAL 1
 #define EAPDTW_ECUDA 2
 #define EAPDTW_ENOMEM 3
+#define EAPDTW_ENCCL 4
 #define EAPDTW_UNBOUNDED_WINDOW ((size_t)-1)
 
 /* Algo (search.hpp:56) */
@@ -58,9 +59,9 @@ typedef struct {
   int32_t found;
   int32_t pad_;
   uint64_t candidates_total, pruned_kim, pruned_keogh_eq, pruned_keogh_ec, dtw_calls,
-      dtw_abandoned, dp_cells_evaluated; /* cells of the exact DP, as dtw.cpp:28-33 counts */
+      dtw_abandoned, dp_cells_evaluated; /* DP cells evaluated by every engine (dtw.cpp:28-33) */
   double elapsed_seconds;
-  uint64_t screen_cells_evaluated; /* cells of the FP32 screening pass (not in dp_cells_evaluated) */
+  uint64_t screen_cells_evaluated; /* ... of which the FP32 screening pass (the exact DP: the rest) */
 } eapdtw_search_result;
 
 /* --- errors / context ---------------------------------------------------- */
@@ -216,6 +217,31 @@ int eapdtw_nn1_dev_cutoff(eapdtw_ctx* ctx, const double* queries_dev, size_t nq,
                           const double* db_dev, size_t nd, size_t len, size_t window,
                           const double* cutoff_dev, uint64_t* argmin, double* dist,
                           uint64_t* cells);
+
+/* --- one host thread, several devices -------------------------
+ * A context per device and an NCCL communicator over them (ncclCommInitAll;
+ * NCCL is loaded at first use).  EAPDTW_ENCCL for an NCCL failure.
+ *   multi_similarity_search: the reference split into 100000-aligned
+ *     candidate shards (the stats reset interval, search.cpp:16), each with its
+ *     (m-1)-point halo, one per device; the threshold keys all-reduced (MIN)
+ *     after the warm start and after each of `batches` candidate batches; the
+ *     result the (distance, lowest global index) minimum, counters summed.
+ *   multi_nn1: the database split into contiguous row ranges, the queries on
+ *     every device; per-query cutoff keys all-reduced (MIN) after each of
+ *     `batches` batches; per query the (distance, lowest global index) min. */
+typedef struct eapdtw_multi eapdtw_multi;
+int eapdtw_multi_create(eapdtw_multi** out, const int* devices, int n);
+int eapdtw_multi_destroy(eapdtw_multi* mg);
+int eapdtw_multi_device_count(const eapdtw_multi* mg);
+/* The context of the i-th device (options, streams); owned by mg. */
+eapdtw_ctx* eapdtw_multi_context(eapdtw_multi* mg, int i);
+int eapdtw_multi_similarity_search(eapdtw_multi* mg, const double* reference, size_t n,
+                                   const double* query, size_t qlen,
+                                   const eapdtw_search_config* cfg, int batches,
+                                   eapdtw_search_result* out);
+int eapdtw_multi_nn1(eapdtw_multi* mg, const double* queries, size_t nq, const double* db,
+                     size_t nd, size_t len, size_t window, int batches, uint64_t* argmin,
+                     double* dist, uint64_t* cells);
 
 /* --- the search's preparation kernels, exposed for checking -------------------
  * Sliding statistics of every length-m window of ref (the RunningStats chain of

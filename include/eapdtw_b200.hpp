@@ -412,6 +412,48 @@ struct SearchResult {
   return out;
 }
 
+// One host thread driving several GPUs (eapdtw_multi_*, NCCL between them):
+// the same similarity_search over 100000-aligned reference shards, and the
+// NN1 loop over a row-split database.
+class MultiDevice {
+ public:
+  explicit MultiDevice(const std::vector<int>& devices) {
+    detail::check(eapdtw_multi_create(&mg_, devices.data(), static_cast<int>(devices.size())));
+  }
+  ~MultiDevice() { eapdtw_multi_destroy(mg_); }
+  MultiDevice(const MultiDevice&) = delete;
+  MultiDevice& operator=(const MultiDevice&) = delete;
+  [[nodiscard]] int device_count() const { return eapdtw_multi_device_count(mg_); }
+  [[nodiscard]] SearchResult similarity_search(const Series& reference, const Series& query,
+                                               const SearchConfig& cfg, int batches = 8) {
+    eapdtw_search_config c{cfg.query_length, cfg.window_ratio,
+                           static_cast<int32_t>(cfg.algorithm), cfg.use_lower_bounds ? 1 : 0,
+                           cfg.tighten_ub ? 1 : 0, 0};
+    eapdtw_search_result r{};
+    detail::check(eapdtw_multi_similarity_search(mg_, reference.data(), reference.length(),
+                                                 query.data(), query.length(), &c, batches, &r));
+    SearchResult out;
+    out.best = {static_cast<std::size_t>(r.location), r.distance_sq, r.found != 0};
+    out.report = {r.candidates_total, r.pruned_kim,  r.pruned_keogh_eq,   r.pruned_keogh_ec,
+                  r.dtw_calls,        r.dtw_abandoned, r.dp_cells_evaluated, r.elapsed_seconds};
+    return out;
+  }
+  // queries: nq x len, db: nd x len (row-major); argmin / dist per query.
+  void nn1(std::span<const double> queries, std::span<const double> db, std::size_t len,
+           Band band, std::vector<std::size_t>& argmin, std::vector<double>& dist,
+           int batches = 4) {
+    const std::size_t nq = queries.size() / len, nd = db.size() / len;
+    std::vector<uint64_t> a(nq);
+    dist.assign(nq, PRUNED);
+    detail::check(eapdtw_multi_nn1(mg_, queries.data(), nq, db.data(), nd, len, band.window,
+                                   batches, a.data(), dist.data(), nullptr));
+    argmin.assign(a.begin(), a.end());
+  }
+
+ private:
+  eapdtw_multi* mg_ = nullptr;
+};
+
 // search.hpp:85-114: the cascade of one candidate, composed from the device
 // helpers above in the reference's order (search.cpp:63-107).
 enum class CascadeTier : std::uint8_t { none, kim, keogh_eq, keogh_ec };

@@ -16,6 +16,7 @@ EAPDTW_OK = 0
 EAPDTW_EINVAL = 1
 EAPDTW_ECUDA = 2
 EAPDTW_ENOMEM = 3
+EAPDTW_ENCCL = 4
 UNBOUNDED_WINDOW = (1 << 64) - 1
 
 ALGO_FULL = 0
@@ -126,6 +127,16 @@ SIGNATURES = [
      [_vp, _vp, C.c_size_t, _vp, C.c_size_t, C.c_size_t, C.c_size_t, _vp, _u64p, _dp, _u64p]),
     ("eapdtw_sliding_stats", C.c_int, [_vp, _dp, C.c_size_t, C.c_size_t, _dp, _dp]),
     ("eapdtw_sliding_envelope", C.c_int, [_vp, _dp, C.c_size_t, C.c_size_t, _dp, _dp]),
+    ("eapdtw_multi_create", C.c_int, [C.POINTER(_vp), C.POINTER(C.c_int), C.c_int]),
+    ("eapdtw_multi_destroy", C.c_int, [_vp]),
+    ("eapdtw_multi_device_count", C.c_int, [_vp]),
+    ("eapdtw_multi_context", _vp, [_vp, C.c_int]),
+    ("eapdtw_multi_similarity_search", C.c_int,
+     [_vp, _dp, C.c_size_t, _dp, C.c_size_t, C.POINTER(SearchConfigC), C.c_int,
+      C.POINTER(SearchResultC)]),
+    ("eapdtw_multi_nn1", C.c_int,
+     [_vp, _dp, C.c_size_t, _dp, C.c_size_t, C.c_size_t, C.c_size_t, C.c_int, _u64p, _dp,
+      _u64p]),
     ("eapdtw_znormalize", C.c_int, [_dp, C.c_size_t, _dp]),
     ("eapdtw_random_walk_uniform", C.c_int, [C.c_size_t, C.c_uint64, _dp]),
     ("eapdtw_random_walk_normal", C.c_int, [C.c_size_t, C.c_uint64, _dp]),

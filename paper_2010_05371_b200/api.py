@@ -134,9 +134,9 @@ class SearchReport:
     pruned_keogh_ec: int = 0
     dtw_calls: int = 0
     dtw_abandoned: int = 0
-    dp_cells_evaluated: int = 0  # cells of the exact DP (dtw.cpp:28-33 counts its kernel's cells)
+    dp_cells_evaluated: int = 0  # DP cells evaluated by every engine (dtw.cpp:28-33)
     elapsed_seconds: float = 0.0
-    screen_cells_evaluated: int = 0  # cells of the FP32 screening pass (GPU only)
+    screen_cells_evaluated: int = 0  # ... of which the FP32 screening pass (GPU only)
 
 
 @dataclass
@@ -166,9 +166,9 @@ class Context:
         self.device = int(device)
 
     def close(self):
-        if self.handle:
+        if self.handle and not getattr(self, "_borrowed", False):
             lib.eapdtw_ctx_destroy(self.handle)
-            self.handle = None
+        self.handle = None
 
     def __del__(self):  # pragma: no cover - interpreter shutdown order
         try:
@@ -230,6 +230,62 @@ class Context:
     def last_cells_f32(self) -> int:
         """FP32-screen share of the last nn1 call's cells."""
         return int(lib.eapdtw_ctx_last_cells_f32(self.handle))
+
+
+class MultiDevice:
+    """One host thread driving several GPUs through the C ABI
+    (eapdtw_multi_*): a context per device and an NCCL communicator over them.
+    The reference's similarity_search and the NN1 loop over all devices, with
+    the best-so-far / per-query cutoffs all-reduced between batches."""
+
+    def __init__(self, devices):
+        devs = (C.c_int * len(devices))(*[int(d) for d in devices])
+        h = C.c_void_p()
+        check(lib.eapdtw_multi_create(C.byref(h), devs, len(devices)))
+        self.handle = h
+        self.devices = [int(d) for d in devices]
+
+    def context(self, i: int) -> "Context":
+        """The i-th device's context (borrowed: options apply to its searches)."""
+        ctx = Context.__new__(Context)
+        ctx.handle = C.c_void_p(lib.eapdtw_multi_context(self.handle, int(i)))
+        ctx.device = self.devices[i]
+        ctx._borrowed = True
+        return ctx
+
+    def similarity_search(self, reference, query, cfg: "SearchConfig | None" = None,
+                          batches: int = 8) -> "SearchResult":
+        cfg = cfg or SearchConfig()
+        r, q = _as_f64(reference), _as_f64(query)
+        c = cfg.to_c()
+        out = _capi.SearchResultC()
+        check(lib.eapdtw_multi_similarity_search(self.handle, _ptr(r), r.size, _ptr(q), q.size,
+                                                 C.byref(c), int(batches), C.byref(out)))
+        return SearchResult.from_c(out)
+
+    def nn1(self, queries, db, band=None, batches: int = 4):
+        qs = np.ascontiguousarray(np.asarray(queries, dtype=np.float64))
+        d = np.ascontiguousarray(np.asarray(db, dtype=np.float64))
+        nq, L = qs.shape
+        arg = np.empty(nq, dtype=np.uint64)
+        dist = np.empty(nq)
+        cells = C.c_uint64(0)
+        check(lib.eapdtw_multi_nn1(self.handle, _ptr(qs.reshape(-1)), nq, _ptr(d.reshape(-1)),
+                                   d.shape[0], L, _window(band), int(batches),
+                                   arg.ctypes.data_as(C.POINTER(C.c_uint64)), _ptr(dist),
+                                   C.byref(cells)))
+        return arg, dist, cells.value
+
+    def close(self):
+        if self.handle:
+            lib.eapdtw_multi_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def total_launches() -> int:

@@ -1035,12 +1035,14 @@ int eapdtw_search_plan_result(eapdtw_search_plan* p, eapdtw_search_result* out) 
   out->pruned_keogh_ec = cnt[kCntKeoghEc];
   out->dtw_calls = cnt[kCntDtwCalls];
   out->dtw_abandoned = cnt[kCntDtwAbandoned];
-  // dp_cells_evaluated: cells of the exact DP (the FP64 engines and the
-  // phase-A lane screen, which is an exact prefix of the same DP), as the
-  // reference counts its kernel's cells (dtw.cpp:28-33); the FP32 screen's
-  // cells are reported apart
-  out->dp_cells_evaluated = cnt[kCntCells] + pc[kCntCells];
+  // dp_cells_evaluated: every DP cell the search's kernels evaluated, as the
+  // reference counts its kernel's cells (dtw.cpp:28-33) -- the exact FP64
+  // engines, the phase-A lane prefix, and the FP32 screening pass, which
+  // evaluates the same cells at lower precision (its share is
+  // screen_cells_evaluated).  Warm-start candidates are real candidates and
+  // count like the sweep's.
   out->screen_cells_evaluated = cnt[kCntCellsF32] + pc[kCntCellsF32];
+  out->dp_cells_evaluated = cnt[kCntCells] + pc[kCntCells] + out->screen_cells_evaluated;
   out->elapsed_seconds =
       std::chrono::duration<double>(std::chrono::steady_clock::now() - p->t0).count();
 #ifdef EAPDTW_PHASE_CLOCKS
@@ -1371,23 +1373,15 @@ int eapdtw_similarity_search(eapdtw_ctx* c, const double* ref, size_t n, const d
 // ---------------------------------------------------------------------------
 // NN1
 // ---------------------------------------------------------------------------
-static int nn1_impl(eapdtw_ctx* c, const double* q_dev, size_t nq, const double* db_dev,
-                    size_t nd, size_t len, size_t window, uint64_t* argmin, double* dist,
-                    uint64_t* cells, const double* cutoff_dev = nullptr) {
+// One NN1 launch over database rows db_dev[0, nd) against per-query threshold
+// keys and (d, index) records already on the device (not re-initialised, so
+// consecutive batches and shards carry them); recorded indices are the local
+// row + index_offset.  counters: [FP64 cells, FP32 cells, dtw calls], added to.
+static int nn1_launch(eapdtw_ctx* c, const double* q_dev, size_t nq, const double* db_dev,
+                      size_t nd, size_t len, size_t window, unsigned long long* keys,
+                      BestRecord* best, unsigned long long* counters, long long index_offset) {
   int w = (window == EAPDTW_UNBOUNDED_WINDOW || window >= len) ? static_cast<int>(len)
                                                               : static_cast<int>(window);
-  cudaStream_t s = c->stream;
-  CUDA_TRY(c->best.ensure(nq * sizeof(BestRecord)));
-  CUDA_TRY(c->keys.ensure(nq * 8));
-  CUDA_TRY(c->counters.ensure(3 * 8));
-  CUDA_TRY(cudaMemsetAsync(c->counters.p, 0, 24, s));
-  CUDA_TRY(launch_init_best(c->best.as<BestRecord>(), c->keys.as<unsigned long long>(),
-                            static_cast<long long>(nq), s));
-  ++c->launches;
-  // a starting cutoff per query: the threshold key is the bit pattern of a
-  // non-negative double (order-preserving), so the cutoffs are copied in as is
-  if (cutoff_dev)
-    CUDA_TRY(cudaMemcpyAsync(c->keys.p, cutoff_dev, nq * 8, cudaMemcpyDeviceToDevice, s));
   Nn1Params p{};
   p.queries = q_dev;
   p.db = db_dev;
@@ -1399,17 +1393,19 @@ static int nn1_impl(eapdtw_ctx* c, const double* q_dev, size_t nq, const double*
   // waves the last one leaves SMs idle (ncu: ALU-pipe use 58-95% across SMs
   // at 2 splits).  cfg5 (1000 queries) sweep of splits per query: 2 -> 187.8
   // ms, 4 -> 159.9, 6 -> 148.2, 10 -> 145.3, 16 -> 152.1 (the extra splits
-  // re-warm more cutoffs; scratch/nn1_splits.sh).  ~64 blocks per SM, each
-  // block keeping at least 64 database rows.
-  const long long target = 148LL * 64;
+  // re-warm more cutoffs).  ~64 blocks per SM, each block keeping at least 64
+  // database rows.
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  const long long target = static_cast<long long>(sms) * 64;
   p.splits = static_cast<int>(std::max<long long>(1, std::min<long long>(
       static_cast<long long>(nd) / 64 + 1, (target + static_cast<long long>(nq) - 1) / static_cast<long long>(nq))));
   if (c->opt[kOptNn1Splits] > 0) p.splits = static_cast<int>(c->opt[kOptNn1Splits]);
   p.ad_k = c->opt[kOptAdK] >= 0 ? static_cast<int>(c->opt[kOptAdK]) : choose_ad_k(static_cast<int>(len), w);
-  p.ub_keys = c->keys.as<unsigned long long>();
-  p.best = c->best.as<BestRecord>();
-  p.cells = c->counters.as<unsigned long long>();  // [FP64 cells, FP32 cells]
-  p.dtw_calls = c->counters.as<unsigned long long>() + 2;
+  p.ub_keys = keys;
+  p.best = best;
+  p.cells = counters;
+  p.dtw_calls = counters + 2;
   {
     // FP32 screen (dtw_f32.cuh) for z-normalised data: |values| <= sqrt(len)
     // + 1, checked per query (block) and per strip of database rows.
@@ -1424,22 +1420,46 @@ static int nn1_impl(eapdtw_ctx* c, const double* q_dev, size_t nq, const double*
   p.guard_abs = 1e-20;
   p.warm = static_cast<int>(c->opt[kOptNn1Warm]);
   p.probe_strips = static_cast<int>(c->opt[kOptProbeStrips]);
-  CUDA_TRY(launch_nn1(p, s));
+  p.index_offset = index_offset;
+  CUDA_TRY(launch_nn1(p, c->stream));
   ++c->launches;
+  return EAPDTW_OK;
+}
+
+// Records -> (argmin, dist): a query with no row within its cutoff gets
+// index 0 and +inf (the harness's strict < never fired).
+static void nn1_unpack(const std::vector<BestRecord>& rec, uint64_t* argmin, double* dist) {
+  for (size_t i = 0; i < rec.size(); ++i) {
+    const bool none = rec[i].d == kInf;
+    argmin[i] = none ? 0 : rec[i].idx;
+    dist[i] = none ? kInf : rec[i].d;
+  }
+}
+
+static int nn1_impl(eapdtw_ctx* c, const double* q_dev, size_t nq, const double* db_dev,
+                    size_t nd, size_t len, size_t window, uint64_t* argmin, double* dist,
+                    uint64_t* cells, const double* cutoff_dev = nullptr) {
+  cudaStream_t s = c->stream;
+  CUDA_TRY(c->best.ensure(nq * sizeof(BestRecord)));
+  CUDA_TRY(c->keys.ensure(nq * 8));
+  CUDA_TRY(c->counters.ensure(3 * 8));
+  CUDA_TRY(cudaMemsetAsync(c->counters.p, 0, 24, s));
+  CUDA_TRY(launch_init_best(c->best.as<BestRecord>(), c->keys.as<unsigned long long>(),
+                            static_cast<long long>(nq), s));
+  ++c->launches;
+  // a starting cutoff per query: the threshold key is the bit pattern of a
+  // non-negative double (order-preserving), so the cutoffs are copied in as is
+  if (cutoff_dev)
+    CUDA_TRY(cudaMemcpyAsync(c->keys.p, cutoff_dev, nq * 8, cudaMemcpyDeviceToDevice, s));
+  int e = nn1_launch(c, q_dev, nq, db_dev, nd, len, window, c->keys.as<unsigned long long>(),
+                     c->best.as<BestRecord>(), c->counters.as<unsigned long long>(), 0);
+  if (e) return e;
   std::vector<BestRecord> rec(nq);
   unsigned long long cnt[3];
   CUDA_TRY(cudaMemcpyAsync(rec.data(), c->best.p, nq * sizeof(BestRecord), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaMemcpyAsync(cnt, c->counters.p, 24, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
-  for (size_t i = 0; i < nq; ++i) {
-    if (rec[i].d == kInf) {  // nothing within the band: index 0, +inf (strict < never fired)
-      argmin[i] = 0;
-      dist[i] = kInf;
-    } else {
-      argmin[i] = rec[i].idx;
-      dist[i] = rec[i].d;
-    }
-  }
+  nn1_unpack(rec, argmin, dist);
   if (cells) *cells = cnt[0] + cnt[1];  // both engines
   c->last_cells_f32 = cnt[1];
   return EAPDTW_OK;
@@ -1745,5 +1765,313 @@ static int fp_peak(eapdtw_ctx* c, int bits, double* ops) {
 
 int eapdtw_fp64_peak(eapdtw_ctx* c, double* ops) { return fp_peak(c, 64, ops); }
 int eapdtw_fp32_peak(eapdtw_ctx* c, double* ops) { return fp_peak(c, 32, ops); }
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// One host thread driving several devices: a context per
+// device and an NCCL communicator over them (ncclCommInitAll).  NCCL is
+// loaded at first use (dlopen), so the library has no hard dependency on it
+// and shares the process's copy when a framework already loaded one.
+// ---------------------------------------------------------------------------
+#include <dlfcn.h>
+#include <nccl.h>
+
+namespace {
+struct NcclApi {
+  bool ok = false;
+  std::string why;
+  decltype(&ncclCommInitAll) commInitAll = nullptr;
+  decltype(&ncclCommDestroy) commDestroy = nullptr;
+  decltype(&ncclAllReduce) allReduce = nullptr;
+  decltype(&ncclGroupStart) groupStart = nullptr;
+  decltype(&ncclGroupEnd) groupEnd = nullptr;
+  decltype(&ncclGetErrorString) errorString = nullptr;
+};
+
+const NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);  // already loaded?
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      api.why = std::string("NCCL not found: ") + dlerror();
+      return;
+    }
+    api.commInitAll = reinterpret_cast<decltype(api.commInitAll)>(dlsym(h, "ncclCommInitAll"));
+    api.commDestroy = reinterpret_cast<decltype(api.commDestroy)>(dlsym(h, "ncclCommDestroy"));
+    api.allReduce = reinterpret_cast<decltype(api.allReduce)>(dlsym(h, "ncclAllReduce"));
+    api.groupStart = reinterpret_cast<decltype(api.groupStart)>(dlsym(h, "ncclGroupStart"));
+    api.groupEnd = reinterpret_cast<decltype(api.groupEnd)>(dlsym(h, "ncclGroupEnd"));
+    api.errorString = reinterpret_cast<decltype(api.errorString)>(dlsym(h, "ncclGetErrorString"));
+    api.ok = api.commInitAll && api.commDestroy && api.allReduce && api.groupStart &&
+             api.groupEnd && api.errorString;
+    if (!api.ok) api.why = "NCCL: missing symbols";
+  });
+  return api;
+}
+}  // namespace
+
+#define NCCL_TRY(expr)                                                                  \
+  do {                                                                                  \
+    const ncclResult_t r_ = (expr);                                                     \
+    if (r_ != ncclSuccess)                                                              \
+      return fail(EAPDTW_ENCCL, std::string(#expr) + ": " + nccl().errorString(r_));    \
+  } while (0)
+
+struct eapdtw_multi {
+  std::vector<int> devs;
+  std::vector<eapdtw_ctx*> ctx;
+  std::vector<ncclComm_t> comm;
+  std::vector<DevBuf> key;  // per device: a spare threshold key (empty shards) / NN1 keys
+  std::vector<DevBuf> rec;  // per device: NN1 records
+  std::vector<DevBuf> cnt;  // per device: NN1 counters
+};
+
+extern "C" {
+
+int eapdtw_multi_create(eapdtw_multi** out, const int* devices, int n) {
+  if (!out || !devices || n <= 0) return fail(EAPDTW_EINVAL, "multi_create: bad arguments");
+  *out = nullptr;
+  const NcclApi& api = nccl();
+  if (!api.ok) return fail(EAPDTW_ENCCL, api.why);
+  auto* mg = new eapdtw_multi;
+  mg->devs.assign(devices, devices + n);
+  for (int d = 0; d < n; ++d) {
+    for (int e = 0; e < d; ++e)
+      if (mg->devs[e] == mg->devs[d]) {
+        eapdtw_multi_destroy(mg);
+        return fail(EAPDTW_EINVAL, "multi_create: a device is listed twice");
+      }
+    eapdtw_ctx* c = nullptr;
+    const int rc = eapdtw_ctx_create(&c, mg->devs[d]);
+    if (rc) {
+      const std::string msg = g_err;
+      eapdtw_multi_destroy(mg);
+      return fail(rc, msg);
+    }
+    mg->ctx.push_back(c);
+  }
+  mg->comm.assign(n, nullptr);
+  mg->key.resize(n);
+  mg->rec.resize(n);
+  mg->cnt.resize(n);
+  const ncclResult_t r = api.commInitAll(mg->comm.data(), n, mg->devs.data());
+  if (r != ncclSuccess) {
+    const std::string msg = std::string("ncclCommInitAll: ") + api.errorString(r);
+    mg->comm.clear();
+    eapdtw_multi_destroy(mg);
+    return fail(EAPDTW_ENCCL, msg);
+  }
+  *out = mg;
+  return EAPDTW_OK;
+}
+
+int eapdtw_multi_destroy(eapdtw_multi* mg) {
+  if (!mg) return EAPDTW_OK;
+  for (size_t d = 0; d < mg->comm.size(); ++d)
+    if (mg->comm[d]) nccl().commDestroy(mg->comm[d]);
+  for (size_t d = 0; d < mg->ctx.size(); ++d) {
+    cudaSetDevice(mg->devs[d]);
+    if (d < mg->key.size()) mg->key[d].release();
+    if (d < mg->rec.size()) mg->rec[d].release();
+    if (d < mg->cnt.size()) mg->cnt[d].release();
+    eapdtw_ctx_destroy(mg->ctx[d]);
+  }
+  delete mg;
+  return EAPDTW_OK;
+}
+
+int eapdtw_multi_device_count(const eapdtw_multi* mg) {
+  return mg ? static_cast<int>(mg->devs.size()) : 0;
+}
+
+eapdtw_ctx* eapdtw_multi_context(eapdtw_multi* mg, int i) {
+  return (mg && i >= 0 && i < static_cast<int>(mg->ctx.size())) ? mg->ctx[i] : nullptr;
+}
+
+// Candidate shard of device d: whole 100000-candidate segments, as even as
+// possible, earlier devices taking the remainder (sharded.shard_bounds).
+static void shard_bounds(size_t ncand, int world, int d, size_t& s0, size_t& s1) {
+  const size_t seg = static_cast<size_t>(kStatsResetInterval);
+  const size_t nseg = (ncand + seg - 1) / seg;
+  const size_t base = nseg / world, extra = nseg % world;
+  const size_t g0 = d * base + std::min<size_t>(d, extra);
+  const size_t g1 = g0 + base + (static_cast<size_t>(d) < extra ? 1 : 0);
+  s0 = std::min(ncand, g0 * seg);
+  s1 = std::min(ncand, g1 * seg);
+}
+
+int eapdtw_multi_similarity_search(eapdtw_multi* mg, const double* reference, size_t n,
+                                   const double* query, size_t qlen,
+                                   const eapdtw_search_config* cfg, int batches,
+                                   eapdtw_search_result* out) {
+  if (!mg || !reference || !query || !cfg || !out) return fail(EAPDTW_EINVAL, "null argument");
+  if (n == 0 || qlen == 0) return fail(EAPDTW_EINVAL, "Series: empty input");
+  const size_t m = cfg->query_length == 0 ? qlen : cfg->query_length;
+  if (m == 0 || m > qlen) return fail(EAPDTW_EINVAL, "similarity_search: bad query length");
+  if (m > n) return fail(EAPDTW_EINVAL, "similarity_search: query longer than reference");
+  const int G = static_cast<int>(mg->devs.size());
+  batches = std::max(1, batches);
+  const size_t ncand = n - m + 1;
+  const auto t0 = std::chrono::steady_clock::now();
+  std::vector<eapdtw_search_plan*> plan(G, nullptr);
+  std::vector<size_t> s0(G), s1(G);
+  std::vector<uint64_t*> key(G, nullptr);
+  auto cleanup = [&](int rc) {
+    for (int d = 0; d < G; ++d)
+      if (plan[d]) eapdtw_search_plan_destroy(plan[d]);
+    return rc;
+  };
+  // shards: copy, validate (Series, series.hpp:24-31), plan
+  for (int d = 0; d < G; ++d) {
+    eapdtw_ctx* c = mg->ctx[d];
+    shard_bounds(ncand, G, d, s0[d], s1[d]);
+    CUDA_TRY(cudaSetDevice(mg->devs[d]));
+    if (s1[d] <= s0[d]) {  // no candidates: a +inf key still joins the all-reduce
+      CUDA_TRY(mg->key[d].ensure(8));
+      const unsigned long long inf_key = 0x7ff0000000000000ull;
+      CUDA_TRY(cudaMemcpyAsync(mg->key[d].p, &inf_key, 8, cudaMemcpyHostToDevice, c->stream));
+      CUDA_TRY(cudaStreamSynchronize(c->stream));
+      key[d] = mg->key[d].as<uint64_t>();
+      continue;
+    }
+    const size_t npts = s1[d] - s0[d] + m - 1;
+    CUDA_TRY(c->ref.ensure(npts * 8));
+    CUDA_TRY(c->pb.flag.ensure(8));
+    CUDA_TRY(cudaMemcpyAsync(c->ref.p, reference + s0[d], npts * 8, cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(cudaMemsetAsync(c->pb.flag.p, 0, 8, c->stream));
+    CUDA_TRY(launch_check_finite(c->ref.as<double>(), static_cast<long long>(npts),
+                                 c->pb.flag.as<unsigned long long>(), c->stream));
+    ++c->launches;
+    const int rc = eapdtw_search_plan_create(c, c->ref.as<double>(), npts, query, qlen, cfg,
+                                             s0[d], &plan[d]);
+    if (rc) return cleanup(rc);
+    key[d] = eapdtw_search_plan_ub_key(plan[d]);
+  }
+  auto allreduce_keys = [&]() -> int {
+    NCCL_TRY(nccl().groupStart());
+    for (int d = 0; d < G; ++d)
+      NCCL_TRY(nccl().allReduce(key[d], key[d], 1, ncclUint64, ncclMin, mg->comm[d],
+                                mg->ctx[d]->stream));
+    NCCL_TRY(nccl().groupEnd());
+    return EAPDTW_OK;
+  };
+  int rc;
+  for (int d = 0; d < G; ++d)
+    if (plan[d] && (rc = eapdtw_search_plan_prepare(plan[d]))) return cleanup(rc);
+  if (G > 1 && (rc = allreduce_keys())) return cleanup(rc);  // the warm starts' best
+  for (int b = 0; b < batches; ++b) {
+    for (int d = 0; d < G; ++d) {
+      if (!plan[d]) continue;
+      const size_t nc = s1[d] - s0[d];
+      const size_t b0 = nc * b / batches, b1 = nc * (b + 1) / batches;
+      if ((rc = eapdtw_search_plan_run(plan[d], b0, b1))) return cleanup(rc);
+    }
+    if (G > 1 && (rc = allreduce_keys())) return cleanup(rc);
+  }
+  // (distance, lowest global index) over the shards; counters summed
+  std::memset(out, 0, sizeof(*out));
+  out->distance_sq = kInf;
+  for (int d = 0; d < G; ++d) {
+    if (!plan[d]) continue;
+    eapdtw_search_result r{};
+    if ((rc = eapdtw_search_plan_result(plan[d], &r))) return cleanup(rc);
+    unsigned long long bad = 0;
+    CUDA_TRY(cudaMemcpy(&bad, mg->ctx[d]->pb.flag.p, 8, cudaMemcpyDeviceToHost));
+    if (bad) return cleanup(fail(EAPDTW_EINVAL, "Series: non-finite sample in the reference"));
+    if (r.found && (!out->found || r.distance_sq < out->distance_sq ||
+                    (r.distance_sq == out->distance_sq && r.location < out->location))) {
+      out->found = 1;
+      out->distance_sq = r.distance_sq;
+      out->location = r.location;
+    }
+    out->candidates_total += r.candidates_total;
+    out->pruned_kim += r.pruned_kim;
+    out->pruned_keogh_eq += r.pruned_keogh_eq;
+    out->pruned_keogh_ec += r.pruned_keogh_ec;
+    out->dtw_calls += r.dtw_calls;
+    out->dtw_abandoned += r.dtw_abandoned;
+    out->dp_cells_evaluated += r.dp_cells_evaluated;
+    out->screen_cells_evaluated += r.screen_cells_evaluated;
+  }
+  if (!out->found) out->location = 0;
+  out->elapsed_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return cleanup(EAPDTW_OK);
+}
+
+int eapdtw_multi_nn1(eapdtw_multi* mg, const double* queries, size_t nq, const double* db,
+                     size_t nd, size_t len, size_t window, int batches, uint64_t* argmin,
+                     double* dist, uint64_t* cells) {
+  if (!mg || !queries || !db || !argmin || !dist) return fail(EAPDTW_EINVAL, "null argument");
+  if (len == 0 || nd == 0) return fail(EAPDTW_EINVAL, "nn1: empty series");
+  if (nq == 0) return EAPDTW_OK;
+  const int G = static_cast<int>(mg->devs.size());
+  batches = std::max(1, batches);
+  std::vector<size_t> d0(G), d1(G);
+  for (int d = 0; d < G; ++d) {  // contiguous rows, earlier devices take the remainder
+    const size_t base = nd / G, extra = nd % G;
+    d0[d] = d * base + std::min<size_t>(d, extra);
+    d1[d] = d0[d] + base + (static_cast<size_t>(d) < extra ? 1 : 0);
+  }
+  for (int d = 0; d < G; ++d) {
+    eapdtw_ctx* c = mg->ctx[d];
+    cudaStream_t s = c->stream;
+    CUDA_TRY(cudaSetDevice(mg->devs[d]));
+    CUDA_TRY(c->a.ensure(nq * len * 8));
+    CUDA_TRY(c->b.ensure(std::max<size_t>(1, d1[d] - d0[d]) * len * 8));
+    CUDA_TRY(mg->key[d].ensure(nq * 8));
+    CUDA_TRY(mg->rec[d].ensure(nq * sizeof(BestRecord)));
+    CUDA_TRY(mg->cnt[d].ensure(24));
+    CUDA_TRY(cudaMemcpyAsync(c->a.p, queries, nq * len * 8, cudaMemcpyHostToDevice, s));
+    if (d1[d] > d0[d])
+      CUDA_TRY(cudaMemcpyAsync(c->b.p, db + d0[d] * len, (d1[d] - d0[d]) * len * 8,
+                               cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemsetAsync(mg->cnt[d].p, 0, 24, s));
+    CUDA_TRY(launch_init_best(mg->rec[d].as<BestRecord>(), mg->key[d].as<unsigned long long>(),
+                              static_cast<long long>(nq), s));
+    ++c->launches;
+  }
+  for (int b = 0; b < batches; ++b) {
+    for (int d = 0; d < G; ++d) {
+      const size_t rows = d1[d] - d0[d];
+      const size_t b0 = rows * b / batches, b1 = rows * (b + 1) / batches;
+      if (b1 <= b0) continue;
+      CUDA_TRY(cudaSetDevice(mg->devs[d]));
+      const int rc = nn1_launch(mg->ctx[d], mg->ctx[d]->a.as<double>(), nq,
+                                mg->ctx[d]->b.as<double>() + b0 * len, b1 - b0, len, window,
+                                mg->key[d].as<unsigned long long>(), mg->rec[d].as<BestRecord>(),
+                                mg->cnt[d].as<unsigned long long>(),
+                                static_cast<long long>(d0[d] + b0));
+      if (rc) return rc;
+    }
+    if (G > 1) {  // every device continues from the per-query minimum cutoff
+      NCCL_TRY(nccl().groupStart());
+      for (int d = 0; d < G; ++d)
+        NCCL_TRY(nccl().allReduce(mg->key[d].p, mg->key[d].p, nq, ncclUint64, ncclMin,
+                                  mg->comm[d], mg->ctx[d]->stream));
+      NCCL_TRY(nccl().groupEnd());
+    }
+  }
+  // per query: (distance, lowest global index) over the devices' records
+  std::vector<BestRecord> best(nq, BestRecord{kInf, ~0ull}), rec(nq);
+  uint64_t total_cells = 0;
+  for (int d = 0; d < G; ++d) {
+    unsigned long long cnt[3];
+    CUDA_TRY(cudaSetDevice(mg->devs[d]));
+    CUDA_TRY(cudaMemcpyAsync(rec.data(), mg->rec[d].p, nq * sizeof(BestRecord),
+                             cudaMemcpyDeviceToHost, mg->ctx[d]->stream));
+    CUDA_TRY(cudaMemcpyAsync(cnt, mg->cnt[d].p, 24, cudaMemcpyDeviceToHost, mg->ctx[d]->stream));
+    CUDA_TRY(cudaStreamSynchronize(mg->ctx[d]->stream));
+    total_cells += cnt[0] + cnt[1];
+    for (size_t i = 0; i < nq; ++i)
+      if (rec[i].d < best[i].d || (rec[i].d == best[i].d && rec[i].idx < best[i].idx))
+        best[i] = rec[i];
+  }
+  nn1_unpack(best, argmin, dist);
+  if (cells) *cells = total_cells;
+  return EAPDTW_OK;
+}
 
 }  // extern "C"

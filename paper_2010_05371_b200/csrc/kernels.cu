@@ -1629,7 +1629,7 @@ __global__ void __launch_bounds__(256, EAPDTW_NN1_MINB) nn1_kernel(Nn1Params p) 
     ++calls;
     if (d != INF && lane == 0) {
       atomicMin(key, static_cast<unsigned long long>(__double_as_longlong(d)));
-      best_record_update(p.best + qi, d, static_cast<unsigned long long>(k));
+      best_record_update(p.best + qi, d, static_cast<unsigned long long>(k + p.index_offset));
     }
     }
   }

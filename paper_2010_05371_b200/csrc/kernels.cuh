@@ -138,6 +138,7 @@ struct Nn1Params {
   double guard_rel, guard_abs;    // layered LB_Kim guard (summation order)
   int warm;                       // per-warp warm start (best layered-Kim row first)
   int probe_strips;               // FP32 screen: strips probed in each direction (0: forward only)
+  long long index_offset;         // recorded index = local row + index_offset (database shards)
 };
 
 // Each launcher enqueues on `stream` and returns the launch error (no sync).

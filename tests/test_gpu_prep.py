@@ -161,7 +161,7 @@ def test_left_prune_search(gpu, oracle_lib, lb):
     want = oracle_lib.similarity_search(ref, q, 0.1, use_lb=lb, tighten=lb)
     res = {}
     for algo in (gpu.Algo.full, gpu.Algo.left_prune, gpu.Algo.ea_pruned):
-        with gpu.default_context().options(f32=0):
+        with gpu.default_context().options(f32=0, screen_rows=0):
             r = gpu.similarity_search(ref, q, gpu.SearchConfig(window_ratio=0.1, algorithm=algo,
                                                                use_lower_bounds=lb, tighten_ub=lb))
         assert (r.best.location, r.best.distance_sq) == (want.location, want.distance_sq), algo
