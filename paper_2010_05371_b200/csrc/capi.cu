@@ -193,7 +193,7 @@ struct eapdtw_ctx {
   LaunchCounter launches;
   uint64_t last_cells_f32 = 0;  // FP32-screen share of the last nn1 call's cells
   // scratch for pairwise / nn1 host-pointer variants
-  DevBuf a, b, ub, cb, out, cells, best, keys, counters;
+  DevBuf a, b, ub, cb, out, cells, best, keys, counters, gscratch;
   DevBuf ref;  // host-pointer search copies the reference here
   PlanBuffers pb;  // scratch of the one-shot search API (grow-only, reused)
   cudaStream_t copy = nullptr;  // H2D stream of the streamed host-pointer search
@@ -231,6 +231,7 @@ struct eapdtw_search_plan {
   int probe = 2048;
   bool probe_force = false;
   size_t queue_slack = 0;  // spare survivor-queue slots (>= resident warps)
+  bool gmem = false;       // per-warp buffers in global memory (queries too long for shared memory)
   double guard_rel = 1e-9, guard_abs = 1e-20;
   double qmax = 0.0;  // max |normalised query|
   std::chrono::steady_clock::time_point t0;
@@ -273,7 +274,7 @@ int eapdtw_ctx_destroy(eapdtw_ctx* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   for (DevBuf* b : {&c->a, &c->b, &c->ub, &c->cb, &c->out, &c->cells, &c->best, &c->keys,
-                    &c->counters, &c->ref})
+                    &c->counters, &c->ref, &c->gscratch})
     b->release();
   c->pb.release();
   if (c->copy) {
@@ -356,6 +357,10 @@ static int pairwise_impl(eapdtw_ctx* c, const double* rows_dev, const double* co
   p.out = out_dev;
   p.cells = c->cells.as<unsigned long long>();
   p.npairs = static_cast<long long>(npairs);
+  if (const size_t g = pairwise_gscratch_doubles(p)) {  // series too long for shared memory
+    CUDA_TRY(c->gscratch.ensure(g * 8));
+    p.gscratch = c->gscratch.as<double>();
+  }
   CUDA_TRY(launch_pairwise(p, c->stream));
   ++c->launches;
   if (cells) {
@@ -688,10 +693,22 @@ static int plan_init(eapdtw_search_plan* p, eapdtw_ctx* c, const double* ref_dev
       best_blocks = per_sm;
     }
   }
-  if (best_warps == 0)
-    return fail(EAPDTW_EINVAL, "search: query length exceeds the shared-memory budget");
+  p->gmem = best_warps == 0;
+  if (p->gmem) {
+    // Long queries: the per-warp buffers in global memory (the query and the
+    // tier stacks stay in shared memory), one or two 8-warp blocks per SM.
+    const size_t smem = search_smem_bytes(static_cast<int>(m), 8, p->ad_k, true);
+    if (smem > static_cast<size_t>(optin))
+      return fail(EAPDTW_EINVAL, "search: query length exceeds the GPU limit (shared memory)");
+    best_w = 8;
+    best_blocks = std::max(1, std::min(search_blocks_per_sm_by_regs(),
+                                       static_cast<int>(max_smem / (smem + 1024))));
+  }
   p->warps = best_w;
   p->blocks = sms * best_blocks;
+  if (p->gmem)
+    CUDA_TRY(B.scratch.ensure(static_cast<size_t>(p->blocks) * p->warps *
+                              search_warp_buf_doubles(static_cast<int>(m), p->ad_k) * 8));
   if (o[kOptWarps] >= 1 && o[kOptWarps] < p->warps) p->warps = static_cast<int>(o[kOptWarps]);
   // One spare slot per resident warp: a consumer may hold a "future" slot past
   // the final tail, which must read as empty (-1) rather than stale data.
@@ -796,6 +813,7 @@ static SearchParams base_params(eapdtw_search_plan* p) {
   s.direct = 0;
   s.screen_rows = p->screen_rows;
   s.probe_strips = static_cast<int>(p->ctx->opt[kOptProbeStrips]);
+  s.gscratch = p->gmem ? B.scratch.as<double>() : nullptr;
   s.producer_smsp = static_cast<int>(p->ctx->opt[kOptProducers]);
   {
     // z-normalised rows satisfy |c| <= sqrt(m - 1); the engine checks the

@@ -357,9 +357,11 @@ static __host__ __device__ inline size_t q32_len(int m) {
   return static_cast<size_t>(m) + 2 + 2 * static_cast<size_t>(kPadR);
 }
 
-size_t search_smem_bytes(int m, int warps, int ad_k) {
+size_t search_warp_buf_doubles(int m, int ad_k) { return warp_buf_doubles(m, ad_k); }
+
+size_t search_smem_bytes(int m, int warps, int ad_k, bool gmem) {
   return padded_len(m, ad_k) * 8                        // q (padded, 1-based)
-         + static_cast<size_t>(warps) * warp_buf_doubles(m, ad_k) * 8  // per-warp buffers
+         + (gmem ? 0 : static_cast<size_t>(warps) * warp_buf_doubles(m, ad_k) * 8)  // per-warp buffers
          + static_cast<size_t>(warps) * kStackBytesPerWarp  // per-warp tier stacks
          + (q32_len(m) * 4 + 7) / 8 * 8                       // q as float (FP32 screens)
          + 64;
@@ -470,8 +472,12 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // per-warp buffer: the DTW row buffer, or the LB_Keogh EQ staging tile
   const size_t wlen = warp_buf_doubles(m, p.ad_k);
-  double* rowbuf = smem + plen + static_cast<size_t>(warp) * wlen + pad;
-  int* stacks = reinterpret_cast<int*>(smem + plen + static_cast<size_t>(blockDim.x >> 5) * wlen);
+  const bool gmem = p.gscratch != nullptr;  // long queries: the per-warp buffers in global memory
+  double* rowbuf =
+      (gmem ? p.gscratch + (static_cast<size_t>(blockIdx.x) * (blockDim.x >> 5) + warp) * wlen
+            : smem + plen + static_cast<size_t>(warp) * wlen) + pad;
+  int* stacks = reinterpret_cast<int*>(smem + plen +
+                                       (gmem ? 0 : static_cast<size_t>(blockDim.x >> 5) * wlen));
   // the query as float (FP32 screens), after the stacks
   float* q32base = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(stacks) +
                                             static_cast<size_t>(blockDim.x >> 5) * kStackBytesPerWarp);
@@ -1066,7 +1072,7 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
           if (lane == 0) atomicAdd(&p.counters[hi >= lo && len <= static_cast<long long>(wlen)
                                                    ? kStageHit : kStageMiss], 1ull);
 #endif
-          if (hi >= lo && len <= static_cast<long long>(wlen)) {
+          if (!gmem && hi >= lo && len <= static_cast<long long>(wlen)) {
             double* sbuf = rowbuf - pad;
             const double* src = ref + p.begin + lo;
             for (int t = lane; t < static_cast<int>(len); t += 32) sbuf[t] = src[t];
@@ -1356,7 +1362,7 @@ cudaError_t launch_rank_select(const SearchParams& p, long long S, int wave, lon
 int search_blocks_per_sm_by_regs() { return kSearchMinBlocks; }
 
 cudaError_t launch_search(const SearchParams& p, int blocks, int warps, cudaStream_t stream) {
-  const size_t smem = search_smem_bytes(p.m, warps, p.ad_k);
+  const size_t smem = search_smem_bytes(p.m, warps, p.ad_k, p.gscratch != nullptr);
   auto go = [&](auto kern) -> cudaError_t {
     cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(kern), smem);
     if (e != cudaSuccess) return e;
@@ -1385,7 +1391,9 @@ __global__ void __launch_bounds__(256) pairwise_kernel(PairParams p) {
   const int lc = p.lc;
   const int pad = smem_pad(p.ad_k);
   const size_t plen = padded_len(max(lc, p.lr), p.ad_k);
-  double* colsp = smem + static_cast<size_t>(warp) * 2 * plen + pad;  // padded, 1-based
+  // padded, 1-based; in global scratch for series too long for shared memory
+  double* colsp = (p.gscratch ? p.gscratch + (static_cast<size_t>(blockIdx.x) * wpb + warp) * 2 * plen
+                              : smem + static_cast<size_t>(warp) * 2 * plen) + pad;
   double* rowbuf = colsp + plen;
   const double INF = d_inf();
   unsigned long long cells = 0, ovf = 0;
@@ -1421,14 +1429,32 @@ __global__ void __launch_bounds__(256) pairwise_kernel(PairParams p) {
   if (lane == 0 && p.cells) atomicAdd(p.cells, cells);
 }
 
-cudaError_t launch_pairwise(const PairParams& p, cudaStream_t stream) {
-  int warps = 8;
+// Shape of a pairwise launch: warps per block, blocks, and whether the
+// per-warp buffers (2 padded series of max(lr, lc)) fit shared memory.
+static void pairwise_shape(const PairParams& p, int& warps, int& blocks, bool& gmem) {
+  warps = 8;
   const size_t plen = padded_len(max(p.lc, p.lr), p.ad_k);
   while (warps > 1 && static_cast<size_t>(warps) * 2 * plen * 8 > 200 * 1024) warps /= 2;
-  const size_t smem = static_cast<size_t>(warps) * 2 * plen * sizeof(double);
-  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  gmem = static_cast<size_t>(warps) * 2 * plen * 8 > 200 * 1024;
+  if (gmem) warps = 8;
   const long long need = (p.npairs + warps - 1) / warps;
-  const int blocks = static_cast<int>(min(need, 148LL * 32));
+  blocks = static_cast<int>(min(need, gmem ? 148LL * 4 : 148LL * 32));
+}
+
+size_t pairwise_gscratch_doubles(const PairParams& p) {
+  int warps, blocks;
+  bool gmem;
+  pairwise_shape(p, warps, blocks, gmem);
+  return gmem ? static_cast<size_t>(blocks) * warps * 2 * padded_len(max(p.lc, p.lr), p.ad_k) : 0;
+}
+
+cudaError_t launch_pairwise(const PairParams& p, cudaStream_t stream) {
+  int warps, blocks;
+  bool gmem;
+  pairwise_shape(p, warps, blocks, gmem);
+  if (gmem && !p.gscratch) return cudaErrorInvalidValue;
+  const size_t plen = padded_len(max(p.lc, p.lr), p.ad_k);
+  const size_t smem = gmem ? 0 : static_cast<size_t>(warps) * 2 * plen * sizeof(double);
   auto go = [&](auto kern) -> cudaError_t {
     const cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(kern), smem);
     if (e != cudaSuccess) return e;
@@ -1641,11 +1667,17 @@ __global__ void __launch_bounds__(256, EAPDTW_NN1_MINB) nn1_kernel(Nn1Params p) 
 }
 
 cudaError_t launch_nn1(const Nn1Params& p, cudaStream_t stream) {
-  const int warps = 8;
-  const size_t smem = padded_len(p.len, p.ad_k) * sizeof(double) +
-                      static_cast<size_t>(warps) * nn1_warp_doubles(p.len, p.ad_k) * sizeof(double) +
-                      (q32_len(p.len) * sizeof(float) + 15) / 16 * 16 +
-                      static_cast<size_t>(warps) * 2 * sizeof(F32Strip);
+  // 8 warps per block, fewer for long series (each warp's row buffer is in
+  // shared memory with the block's query)
+  int warps = 8;
+  auto smem_of = [&](int wv) {
+    return padded_len(p.len, p.ad_k) * sizeof(double) +
+           static_cast<size_t>(wv) * nn1_warp_doubles(p.len, p.ad_k) * sizeof(double) +
+           (q32_len(p.len) * sizeof(float) + 15) / 16 * 16 +
+           static_cast<size_t>(wv) * 2 * sizeof(F32Strip);
+  };
+  while (warps > 1 && smem_of(warps) > 200 * 1024) warps /= 2;
+  const size_t smem = smem_of(warps);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   const long long blocks = p.nq * p.splits;
   cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(nn1_kernel), smem);

@@ -104,6 +104,9 @@ struct SearchParams {
   const unsigned long long* nlist;
   long long list_cap;            // entries past it were not written
   int ub_only;                   // results tighten the threshold only (no record update)
+  double* gscratch;              // non-null: the per-warp buffers live here (global memory),
+                                 // warp_buf_doubles(m, ad_k) each, for queries whose buffers
+                                 // exceed shared memory
 };
 // Resident 8-warp search blocks per SM the kernel's register budget allows.
 int search_blocks_per_sm_by_regs();
@@ -120,7 +123,10 @@ struct PairParams {
   double* out;
   unsigned long long* cells;  // one counter
   long long npairs;
+  double* gscratch;  // non-null: each warp's (cols, row) buffers in global memory (long series)
 };
+// Global scratch doubles launch_pairwise needs for p (0: shared memory suffices).
+size_t pairwise_gscratch_doubles(const PairParams& p);
 
 struct Nn1Params {
   const double* queries;  // nq x len
@@ -150,7 +156,9 @@ cudaError_t launch_stats(const double* ref, long long n, int m, double* mean, do
 int envelope_tile(int r);
 cudaError_t launch_envelope(const double* ref, long long n, int r, double* env,
                             cudaStream_t stream, long long tile_begin = 0, long long tile_end = -1);
-size_t search_smem_bytes(int m, int warps, int ad_k);
+// gmem: the per-warp buffers are in SearchParams::gscratch, not shared memory.
+size_t search_smem_bytes(int m, int warps, int ad_k, bool gmem = false);
+size_t search_warp_buf_doubles(int m, int ad_k);
 // Window parameter of the anti-diagonal engine for a band of half width w
 // over series of length n: the smallest of 1/3/5 whose window 64K covers
 // the band, else 5 (odd K keeps shared-memory reads conflict-free).

@@ -605,3 +605,43 @@ def test_nn1_probe_directions_agree(gpu, reference_lib_optional):
                 arg, dist, _ = gpu.nn1(qs, db, gpu.Band(band))
             assert [int(x) for x in arg] == [int(x) for x in warg], k
             assert np.array_equal(dist, wdist), k
+
+
+@pytest.mark.timeout(900)
+def test_long_series_beyond_shared_memory(gpu, oracle_lib, reference_lib_optional):
+    """Lengths whose buffers exceed shared memory run with the per-warp
+    buffers in global memory (pairwise, search) or fewer warps per block
+    (NN1): pairwise L = 20000, search m = 12000, NN1 L = 4096, all equal to
+    the oracle / the reference loop."""
+    from paper_2010_05371_b200 import znormalize
+    rng = np.random.default_rng(4242)
+    # pairwise, L = 20000 (and an unequal pair), band and unbounded
+    a = znormalize(np.cumsum(rng.standard_normal(20_000)))
+    b = znormalize(np.cumsum(rng.standard_normal(20_000)))
+    c = znormalize(np.cumsum(rng.standard_normal(19_000)))
+    for x, y, w in ((a, b, 2000), (a, c, 1500), (b, c, UNB)):
+        d = oracle_lib.dtw_windowed(x, y, w)
+        assert gpu.dtw_windowed(x, y, gpu.Band(w)) == d
+        for ub in (d, d * 0.999, d * 1.5):
+            assert gpu.ea_pruned_dtw_windowed(x, y, gpu.Band(w), ub) == \
+                oracle_lib.ea_pruned_dtw_windowed(x, y, w, ub)
+    # search, m = 12000
+    ref = gpu.random_walk_normal(40_000, 4243)
+    q = gpu.random_walk_normal(12_000, 4244)
+    ref[21_000:33_000] = q * 0.8 + 1.0
+    ref[25_000] += 1e-3
+    for ratio, lb in ((0.02, True), (0.01, False)):
+        want = oracle_lib.similarity_search(ref, q, ratio, use_lb=lb, tighten=lb)
+        got = gpu.similarity_search(ref, q, gpu.SearchConfig(window_ratio=ratio,
+                                                             use_lower_bounds=lb, tighten_ub=lb))
+        assert (got.best.location, got.best.distance_sq) == (want.location, want.distance_sq)
+    # NN1, L = 4096
+    L = 4096
+    qs = np.stack([znormalize(np.cumsum(rng.standard_normal(L))) for _ in range(3)])
+    db = np.stack([znormalize(np.cumsum(rng.standard_normal(L))) for _ in range(24)])
+    db[17] = qs[1]
+    for band in (UNB, 300):
+        warg, wdist, _ = reference_lib_optional.nn1(qs, db, band)
+        arg, dist, _ = gpu.nn1(qs, db, gpu.Band(band))
+        assert [int(x) for x in arg] == [int(x) for x in warg]
+        assert np.array_equal(dist, wdist)
