@@ -75,6 +75,7 @@ enum Opt : int {
   kOptSeriesCache,    // device-resident series keep their last stats
   kOptProbeStrips,    // FP32 strip screen: strips probed in each direction before committing (0: forward only)
   kOptProducers,      // search sweep: SMSP-0 warps are LB producers until this queue backlog (0: off)
+  kOptProbeWarm,      // the FP32 probe also in the warm-start passes (probe, rank)
   kNumOpts
 };
 struct OptDef {
@@ -89,7 +90,7 @@ constexpr OptDef kOpts[kNumOpts] = {
     {"coarse_stride", 0, 0, 1 << 20}, {"probe", 2048, 1, 1 << 24}, {"probe_force", 0, 0, 1},
     {"tighten", 1, 0, 1},         {"cb_strip", 1, 1, 1 << 16},  {"warps", 0, 0, 8},
     {"nn1_splits", 0, 0, 1 << 16}, {"nn1_warm", 1, 0, 1},       {"series_cache", 1, 0, 1},
-    {"probe_strips", 1, 0, 8},    {"producers", 0, 0, 1 << 20},
+    {"probe_strips", 1, 0, 8},    {"producers", 0, 0, 1 << 20}, {"probe_warm", 1, 0, 1},
 };
 
 // Grow-only device buffer.
@@ -889,6 +890,7 @@ static int stage_probe(eapdtw_search_plan* p, size_t cand_end) {
   const size_t nprobe =
       std::min<size_t>(static_cast<size_t>(p->probe), std::max<size_t>(1, cand_end / 64));
   SearchParams sp = base_params(p);
+  if (!p->ctx->opt[kOptProbeWarm]) sp.probe_strips = 0;
   sp.use_lb = 0;
   sp.tighten = 0;
   sp.begin = 0;
@@ -922,6 +924,7 @@ static int stage_rank(eapdtw_search_plan* p, size_t cb, size_t ce) {
   CUDA_TRY(B.rank.ensure(rank_scratch_bytes(static_cast<long long>(ce - cb), S)));
   CUDA_TRY(B.rlist.ensure(static_cast<size_t>(cap) * 8 + 64));
   SearchParams rp = base_params(p);
+  if (!p->ctx->opt[kOptProbeWarm]) rp.probe_strips = 0;
   rp.begin = static_cast<long long>(cb);
   rp.end = static_cast<long long>(ce);
   rp.counters = B.probe_counters.as<unsigned long long>();

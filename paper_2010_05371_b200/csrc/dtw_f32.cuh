@@ -243,21 +243,21 @@ __device__ void f32_strip_run(F32Strip& s, int max_strips, bool want_slack, cons
       // the row buffer, dead beyond column hi) was finished after step u-1.
       // BLK chained updates, one per step, with the block's all-dead mask D.
       const unsigned D = __ballot_sync(kFull, alld);
-      if constexpr (BLK == 8) {
+      if constexpr (BLK == 8 || BLK == 16) {
         // Closed form of the BLK chained updates (same result; identity
         // checked in tests/test_finish_mask.py): a lane of D finishes if a
         // run of D lanes joins it to a seed within reach.  Seeds: lanes just
-        // above a finished lane (reach BLK-1 = 7 more lanes), and lane 0 once
+        // above a finished lane (reach BLK-1 more lanes), and lane 0 once
         // the row buffer is dead, from step u0 = hi - j0 + 1 on (reach
-        // BLK-1-u0).  Bounded propagation through D by doubling (1 + 2 + 4).
-        // Measured: cfg4 -3%, cfg3-nolb -2%, cfg5 -7.5% (ALU-pipe work).
+        // BLK-1-u0).  Bounded propagation through D by doubling (1 + 2 + 4
+        // [+ 8]).  Measured: cfg4 -3%, cfg3-nolb -2%, cfg5 -7.5% (ALU-pipe work).
         unsigned G = (finmask << 1) & D;
         unsigned P = D;
-        G |= P & (G << 1);
-        P &= P << 1;
-        G |= P & (G << 2);
-        P &= P << 2;
-        G |= P & (G << 4);
+#pragma unroll
+        for (int sh = 1; sh < BLK; sh *= 2) {
+          G |= P & (G << sh);
+          if (2 * sh < BLK) P &= P << sh;
+        }
         const int u0 = max(0, hi - j0 + 1);
         if (u0 < BLK) {
           const int run = __ffs(~D) - 1;  // D's trailing ones (-1: all 32)
