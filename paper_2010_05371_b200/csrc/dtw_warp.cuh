@@ -74,13 +74,18 @@ struct alignas(16) BestRecord {  // exact (distance, lowest index) record
 };
 
 // Lexicographic (d, idx) minimum, 16-byte CAS (ATOMG.E.CAS.128 on sm_100a).
-// The loop starts from a guess of the record (the initial {+inf, ~0}) rather
-// than two separate 8-byte loads, which could tear into a (new d, old idx)
-// pair and drop a lower-index tie: every comparison below uses a record the
-// 16-byte CAS returned atomically (or the guess, which the CAS checks).
+// The record's distance only decreases, so one 8-byte load (single-copy
+// atomic) rejects a d above it without touching the CAS; otherwise the loop
+// starts from the guess {that distance, ~0} rather than a separately loaded
+// index, which could tear into a (new d, old idx) pair and drop a lower-index
+// tie: every comparison below uses a record the 16-byte CAS returned
+// atomically (or the guess, which the CAS checks).  (A CAS for every result
+// serialised the warm start's many finite results on one address: +1.9 ms.)
 __device__ __forceinline__ void best_record_update(BestRecord* rec, double d,
                                                    unsigned long long idx) {
-  BestRecord cur{d_inf(), ~0ull};
+  const double d_now = *reinterpret_cast<volatile double*>(&rec->d);
+  if (d > d_now) return;
+  BestRecord cur{d_now, ~0ull};
   while (d < cur.d || (d == cur.d && idx < cur.idx)) {
     BestRecord want{d, idx};
     BestRecord seen = atomicCAS(rec, cur, want);

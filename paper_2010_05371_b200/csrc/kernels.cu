@@ -454,9 +454,10 @@ constexpr int kSearchMinBlocks = EAPDTW_SEARCH_MIN_BLOCKS;
 // AD_K: the exact engine's anti-diagonal window compiled into this
 // instantiation (0: strip engine only -- the default search path).
 // LP: Algo::left_prune searches (p.prune == 2): every DTW call runs the
-// exact left-pruning schedule (no FP32 screen), a separate instantiation so
-// the default kernel's code is untouched.
-template <int AD_K, bool LP = false>
+// exact left-pruning schedule (no FP32 screen).  GMEM: queries whose per-warp
+// buffers exceed shared memory (p.gscratch).  Separate instantiations, so the
+// default kernel's code is untouched by either.
+template <int AD_K, bool LP = false, bool GMEM = false>
 __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) search_kernel(SearchParams p) {
   extern __shared__ double smem[];
   const int m = p.m;
@@ -472,7 +473,7 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // per-warp buffer: the DTW row buffer, or the LB_Keogh EQ staging tile
   const size_t wlen = warp_buf_doubles(m, p.ad_k);
-  const bool gmem = p.gscratch != nullptr;  // long queries: the per-warp buffers in global memory
+  constexpr bool gmem = GMEM;  // long queries: the per-warp buffers in global memory
   double* rowbuf =
       (gmem ? p.gscratch + (static_cast<size_t>(blockIdx.x) * (blockDim.x >> 5) + warp) * wlen
             : smem + plen + static_cast<size_t>(warp) * wlen) + pad;
@@ -1369,6 +1370,7 @@ cudaError_t launch_search(const SearchParams& p, int blocks, int warps, cudaStre
     kern<<<blocks, warps * 32, smem, stream>>>(p);
     return cudaGetLastError();
   };
+  if (p.gscratch) return p.prune == 2 ? go(search_kernel<0, true, true>) : go(search_kernel<0, false, true>);
   if (p.prune == 2) return go(search_kernel<0, true>);
   switch (p.ad_k) {
     case 1: return go(search_kernel<1>);
