@@ -76,6 +76,7 @@ enum Opt : int {
   kOptProbeStrips,    // FP32 strip screen: strips probed in each direction before committing (0: forward only)
   kOptProducers,      // search sweep: SMSP-0 warps are LB producers until this queue backlog (0: off)
   kOptProbeWarm,      // the FP32 probe also in the warm-start passes (probe, rank)
+  kOptPrepOverlap,    // envelope beside the stats chain on a side stream (0: after it)
   kNumOpts
 };
 struct OptDef {
@@ -91,6 +92,7 @@ constexpr OptDef kOpts[kNumOpts] = {
     {"tighten", 1, 0, 1},         {"cb_strip", 1, 1, 1 << 16},  {"warps", 0, 0, 8},
     {"nn1_splits", 0, 0, 1 << 16}, {"nn1_warm", 1, 0, 1},       {"series_cache", 1, 0, 1},
     {"probe_strips", 1, 0, 8},    {"producers", 0, 0, 1 << 20}, {"probe_warm", 1, 0, 1},
+    {"prep_overlap", 1, 0, 1},
 };
 
 // Grow-only device buffer.
@@ -200,6 +202,9 @@ struct eapdtw_ctx {
   cudaStream_t copy = nullptr;  // H2D stream of the streamed host-pointer search
   cudaEvent_t copied[2] = {nullptr, nullptr};
   cudaEvent_t fork = nullptr;  // orders the streamed copy after earlier work
+  // side stream of the preparation: the envelope runs there beside the stats chain
+  cudaStream_t aux = nullptr;
+  cudaEvent_t aux_fork = nullptr, aux_join = nullptr;
 };
 
 struct eapdtw_search_plan {
@@ -285,6 +290,12 @@ int eapdtw_ctx_destroy(eapdtw_ctx* c) {
   for (cudaEvent_t& ev : c->copied)
     if (ev) cudaEventDestroy(ev);
   if (c->fork) cudaEventDestroy(c->fork);
+  if (c->aux) {
+    cudaStreamSynchronize(c->aux);
+    cudaStreamDestroy(c->aux);
+  }
+  if (c->aux_fork) cudaEventDestroy(c->aux_fork);
+  if (c->aux_join) cudaEventDestroy(c->aux_join);
   if (c->own) cudaStreamDestroy(c->own);
   delete c;
   return EAPDTW_OK;
@@ -832,14 +843,6 @@ static SearchParams base_params(eapdtw_search_plan* p) {
 }
 
 // ---- preparation stages (each enqueued on the context stream) ----
-static int stage_stats(eapdtw_search_plan* p, long long seg_b, long long seg_e) {
-  PlanBuffers& B = *p->buf;
-  CUDA_TRY(launch_stats(p->ref, static_cast<long long>(p->n), static_cast<int>(p->m),
-                        B.mean.as<double>(), B.sd.as<double>(), p->ctx->stream, seg_b, seg_e));
-  ++p->ctx->launches;
-  return EAPDTW_OK;
-}
-
 // first: decides whether the EC tier exists (the envelope window fits a tile)
 static int stage_env(eapdtw_search_plan* p, long long tile_b, long long tile_e, bool first,
                      cudaStream_t stream = nullptr) {
@@ -860,13 +863,51 @@ static int stage_env(eapdtw_search_plan* p, long long tile_b, long long tile_e, 
   return EAPDTW_OK;
 }
 
-// Stats chain then envelope on the context stream.  (Running them on two
-// streams measured slower: the latency-bound chain shares its SMs.)
+// Stats chain (segments [seg_b, seg_e)) on the context stream and, beside it
+// on the side stream, the envelope (tiles [tile_b, tile_e)): the chain is
+// latency-bound and holds one SM per 16 segments exclusively, so the envelope
+// runs on the other SMs.  The context stream continues once both are done.  `stats` false: the
+// statistics are already in the buffers (a series' cached stats).  `mid`:
+// recorded on the context stream after the statistics (phase timings).
 static int stage_stats_env(eapdtw_search_plan* p, long long seg_b, long long seg_e,
-                           long long tile_b, long long tile_e, bool first) {
-  int e;
-  if ((e = stage_stats(p, seg_b, seg_e))) return e;
-  return stage_env(p, tile_b, tile_e, first);
+                           long long tile_b, long long tile_e, bool first, bool stats = true,
+                           cudaEvent_t mid = nullptr) {
+  eapdtw_ctx* c = p->ctx;
+  PlanBuffers& B = *p->buf;
+  cudaStream_t s = c->stream;
+  const bool env = p->use_lb && p->m >= 2 && (first || p->have_env);
+  const long long n = static_cast<long long>(p->n);
+  if (!c->opt[kOptPrepOverlap]) {  // serial: chain, conversion, envelope
+    if (stats) {
+      CUDA_TRY(launch_stats(p->ref, n, static_cast<int>(p->m), B.mean.as<double>(), B.sd.as<double>(), s,
+                            seg_b, seg_e));
+      c->launches += kStatsLaunches;
+    }
+    if (mid) CUDA_TRY(cudaEventRecord(mid, s));
+    return env ? stage_env(p, tile_b, tile_e, first) : EAPDTW_OK;
+  }
+  const int m = static_cast<int>(p->m);
+  if (env) {
+    if (!c->aux) {
+      CUDA_TRY(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+      CUDA_TRY(cudaEventCreateWithFlags(&c->aux_fork, cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&c->aux_join, cudaEventDisableTiming));
+    }
+    CUDA_TRY(cudaEventRecord(c->aux_fork, s));  // before the chain: the envelope must not wait for it
+  }
+  if (stats) {
+    CUDA_TRY(launch_stats(p->ref, n, m, B.mean.as<double>(), B.sd.as<double>(), s, seg_b, seg_e));
+    c->launches += kStatsLaunches;
+  }
+  if (env) {
+    CUDA_TRY(cudaStreamWaitEvent(c->aux, c->aux_fork, 0));
+    const int e = stage_env(p, tile_b, tile_e, first, c->aux);
+    if (e) return e;
+    CUDA_TRY(cudaEventRecord(c->aux_join, c->aux));
+  }
+  if (mid) CUDA_TRY(cudaEventRecord(mid, s));
+  if (env) CUDA_TRY(cudaStreamWaitEvent(s, c->aux_join, 0));
+  return EAPDTW_OK;
 }
 
 // Probe: evaluate evenly spaced candidates of [0, cand_end) first (no lower
@@ -999,9 +1040,7 @@ int eapdtw_search_plan_prepare(eapdtw_search_plan* p) {
   int e;
   CUDA_TRY(cudaEventRecord(p->ev[0], s));
   p->have_env = false;
-  if (!p->stats_ready && (e = stage_stats(p, 0, -1))) return e;
-  CUDA_TRY(cudaEventRecord(p->ev[1], s));
-  if ((e = stage_env(p, 0, -1, true))) return e;
+  if ((e = stage_stats_env(p, 0, -1, 0, -1, true, !p->stats_ready, p->ev[1]))) return e;
   CUDA_TRY(cudaEventRecord(p->ev[2], s));
   if ((e = stage_probe(p, p->ncand))) return e;
   if ((e = stage_rank(p, 0, p->ncand))) return e;
@@ -1543,7 +1582,7 @@ int eapdtw_sliding_stats(eapdtw_ctx* c, const double* ref, size_t n, size_t m, d
   if (!e) e = cudaMemcpyAsync(dref.p, ref, n * 8, cudaMemcpyHostToDevice, c->stream);
   if (!e) e = launch_stats(dref.as<double>(), static_cast<long long>(n), static_cast<int>(m),
                            dmean.as<double>(), dsd.as<double>(), c->stream);
-  if (!e) ++c->launches;
+  if (!e) c->launches += kStatsLaunches;
   if (!e) e = cudaMemcpyAsync(mean, dmean.p, nc * 8, cudaMemcpyDeviceToHost, c->stream);
   if (!e) e = cudaMemcpyAsync(sd, dsd.p, nc * 8, cudaMemcpyDeviceToHost, c->stream);
   if (!e) e = cudaStreamSynchronize(c->stream);

@@ -1,7 +1,7 @@
 // kernels.cu -- sm_100a kernels of the subsequence-search hot path.
 //
 //   stats_chain_kernel   RunningStats chain, bit-identical to search.cpp:156-168
-//   envelope_kernel      global sliding max/min (van Herk/Gil-Werman, warp scans)
+//   envelope_gw_kernel   global sliding max/min (two-level van Herk/Gil-Werman)
 //   search_kernel        persistent: LB_Kim -> LB_Keogh EQ -> LB_Keogh EC -> pruned DTW
 //   pairwise_kernel      warp per pair (cfg1, and the single-pair drop-in calls)
 //   nn1_kernel           block per (query, database split) with a per-query cutoff (cfg5)
@@ -60,107 +60,221 @@ static cudaError_t ensure_dyn_smem(const void* func, size_t bytes) {
 // 1e-9 distance tolerance.  The chain is therefore reproduced step-for-step:
 // the 100000-slide segments are independent chains.
 //
-// A chain is a serial dependency (2 DADD of latency per slide), so the kernel
-// is latency-bound: what matters is the slide period and how many chains share
-// an SM.  An FP64 warp instruction occupies the pipe for the whole warp even
-// with one lane active, so kStatsChains chains run side by side in lanes
-// 0..kStatsChains-1 of warp 0 (measured: one chain per warp at 7 warps/SM ran
-// at 49 cycles/slide, FP64-pipe bound; alone it runs at ~20).  Their inputs
-// come from shared memory, one packed 16-byte (in, out) load per slide, and
-// their (sum, sumsq) go back as one 16-byte store (tiles padded against bank
-// conflicts).  Warp 1 keeps the next tile of every chain in flight with
-// cp.async (no register round trip; loading the chains straight from global
-// memory measured 71 cycles/slide, DRAM-latency bound), and warps 1..3
-// convert the previous tile's (sum, sumsq) into mean/stddev with correctly
-// rounded div/sqrt (RunningStats::mean/variance/stddev, search.hpp:34-41,
-// search.cpp:35) and write them out coalesced (per-slide global stores from
-// the chain lanes measured 184 cycles/slide).
+// A chain is a serial dependency (2 DADD of latency per slide), so the pass
+// is latency-bound and needs few SMs.  stats_chain_kernel: one block per
+// kChainLanes segments, eight warps (warp w runs on SMSP w % 4):
+//   * warp 0, the chains (lane = segment).  An FP64 warp instruction costs
+//     the same with 1 or 32 active lanes, so the chains of a block run at the
+//     speed of one.  They read their (in, out) values from shared memory as
+//     16-byte pairs two batches of 8 slides ahead, with the squares of the
+//     next batch computed during this one (the warp issues in order, so no
+//     instruction may wait on a load), and write (sum, sumsq) pairs.
+//   * warp 4 keeps the ring of kChainDepth tiles of every chain's `in` and
+//     `out` rows filled with 16-byte cp.async (rows start 16-byte aligned, one
+//     element early if needed): a few issue slots beside the chains on SMSP 0
+//     (measured faster than giving the loads to a converter warp).
+//   * warps 1-3 and 5-7 turn the previous tile's (sum, sumsq) into mean and
+//     stddev with correctly rounded div/sqrt (RunningStats::mean/variance/
+//     stddev, search.hpp:34-41, search.cpp:35) and store them as 16-byte
+//     pairs.  They run on SMSPs 1..3, so their FP64 work never delays the
+//     chains' pipe; two per SMSP hide the dependent div/sqrt latencies.
+// The warps hand tiles over through mbarriers (ring slot full / empty,
+// accumulator full / empty; the loads arrive through cp.async.mbarrier.arrive),
+// so no warp waits on a block-wide barrier: the chains stall only on data.
+// The block claims enough shared memory that no other kernel's block shares
+// its SM; the envelope runs beside it on the remaining SMs, on another stream.
+// (Measured on the way here: per-element cp.async staging 72 cycles/slide at
+// 32 chains, per-lane bulk copies 130, a separate conversion kernel 0.5 ms at
+// cfg4: the copy loops and the extra pass, not the chains, set the pace.)
 // ---------------------------------------------------------------------------
-#ifndef EAPDTW_STATS_CHAINS
-#define EAPDTW_STATS_CHAINS 2
+#ifndef EAPDTW_CHAIN_LANES
+#define EAPDTW_CHAIN_LANES 16
 #endif
-#ifndef EAPDTW_STATS_TILE
-#define EAPDTW_STATS_TILE 256
+#ifndef EAPDTW_CHAIN_DEPTH
+#define EAPDTW_CHAIN_DEPTH 3
 #endif
-constexpr int kStatsTile = EAPDTW_STATS_TILE;      // slides per tile
-constexpr int kStatsChains = EAPDTW_STATS_CHAINS;  // segments (chains) per block
-constexpr int kStatsRow = kStatsTile + 1;  // padded tile row (16-byte entries)
+constexpr int kChainLanes = EAPDTW_CHAIN_LANES;  // segments (chains) per block
+#ifndef EAPDTW_CHAIN_TILE
+#define EAPDTW_CHAIN_TILE 128
+#endif
+constexpr int kChainTile = EAPDTW_CHAIN_TILE;    // slides per tile
+constexpr int kChainDepth = EAPDTW_CHAIN_DEPTH;  // input ring slots
+// rows of kChainTile + 2 doubles: 16-byte multiples whose 4-word bank offset
+// keeps the chain lanes' 16-byte accesses conflict-free
+constexpr int kChainRow = kChainTile + 2;
+constexpr int kChainThreads = 256;  // warp 0: chains; warp 4: loads; warps 1-3, 5-7: conversion
+constexpr int kChainConverters = 6;
+constexpr size_t kChainRingDoubles = static_cast<size_t>(kChainDepth) * 2 * kChainLanes * kChainRow;
+constexpr size_t kChainAccDoubles = 2ull * 2 * kChainLanes * kChainRow;
+// mbarriers: full / empty per ring slot, full / empty per accumulator buffer
+constexpr size_t kChainSmemUsed = (kChainRingDoubles + kChainAccDoubles) * 8 + (2 * kChainDepth + 4) * 8;
+constexpr size_t kChainSmem = kChainSmemUsed > 150 * 1024 ? kChainSmemUsed : 150 * 1024;
 
-__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gmem_src) {
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
   const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gmem_src) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src) : "memory");
 }
 
-__global__ void __launch_bounds__(128) stats_chain_kernel(const double* __restrict__ ref, long long n,
-                                                          int m, double* __restrict__ mean_out,
-                                                          double* __restrict__ sd_out,
-                                                          long long seg_begin, long long seg_end) {
-  extern __shared__ double2 ssm[];
-  double2* s_io = ssm;                                     // [2][chains][row]: (in, out)
-  double2* s_acc = ssm + 2 * kStatsChains * kStatsRow;     // [2][chains][row]: (sum, sumsq)
-  const int tid = threadIdx.x;
-  const int lane = tid & 31;
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+// arrives once this thread's earlier cp.async copies have landed
+__device__ __forceinline__ void mbar_arrive_cp_async(unsigned long long* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+          smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// RunningStats::mean / stddev from (sum, sumsq); a power-of-two m divides
+// exactly by multiplying with 1/m.
+template <bool POW2>
+__device__ __forceinline__ void stats_of(double sum, double sq, double dm, double inv_m, double& mu,
+                                         double& sd) {
+  mu = POW2 ? __dmul_rn(sum, inv_m) : __ddiv_rn(sum, dm);
+  const double var = __dsub_rn(POW2 ? __dmul_rn(sq, inv_m) : __ddiv_rn(sq, dm), __dmul_rn(mu, mu));
+  sd = __dsqrt_rn(var > 0.0 ? var : 0.0);
+}
+
+// OFF_IN / OFF_OUT: position of a tile's first `in` / `out` value in its row.
+template <int OFF_IN, int OFF_OUT, bool POW2>
+__global__ void __launch_bounds__(kChainThreads, 1) stats_chain_kernel(
+    const double* __restrict__ ref, long long n, int m, double* __restrict__ mean_out,
+    double* __restrict__ sd_out, long long seg_begin, long long seg_end) {
+  extern __shared__ __align__(16) double csm[];
+  double* ring = csm;                     // [depth][in, out][lanes][row]
+  double* acc = csm + kChainRingDoubles;  // [2][sum, sumsq][lanes][row]
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(acc + kChainAccDoubles);
+  unsigned long long* slot_full = bars;                  // loads landed (32 loader lanes)
+  unsigned long long* slot_empty = bars + kChainDepth;   // chains done reading (1)
+  unsigned long long* acc_full = bars + 2 * kChainDepth; // chains wrote (sum, sumsq) (1)
+  unsigned long long* acc_empty = acc_full + 2;          // converters done (kChainConverters)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long ncand = n - m + 1;
-  const long long nseg = seg_end;  // segments [seg_begin, seg_end) of this launch
-  const long long seg0 = seg_begin + static_cast<long long>(blockIdx.x) * kStatsChains;
-  const int nch = static_cast<int>(min(static_cast<long long>(kStatsChains), nseg - seg0));
-  // chain 0 is the longest of the block (only the reference's last segment is short)
-  const long long len0 = min(static_cast<long long>(kStatsResetInterval),
-                             ncand - seg0 * kStatsResetInterval);
-  const int ntiles = static_cast<int>((len0 + kStatsTile - 1) / kStatsTile);
-  auto seg_len = [&](int c) -> long long {
-    const long long s0 = (seg0 + c) * kStatsResetInterval;
-    return min(static_cast<long long>(kStatsResetInterval), ncand - s0);
+  const long long seg0 = seg_begin + static_cast<long long>(blockIdx.x) * kChainLanes;
+  const int nch = static_cast<int>(min(static_cast<long long>(kChainLanes), seg_end - seg0));
+  // only the reference's last segment is short
+  auto seg_len = [&](int c) -> int {
+    return static_cast<int>(
+        min(static_cast<long long>(kStatsResetInterval), ncand - (seg0 + c) * kStatsResetInterval));
   };
-  auto tile_cnt = [&](int c, int tile) -> int {
-    const long long t0 = static_cast<long long>(tile) * kStatsTile;
-    return static_cast<int>(max(0LL, min(static_cast<long long>(kStatsTile), seg_len(c) - t0)));
-  };
+  const int ntiles = (seg_len(0) + kChainTile - 1) / kChainTile;
+  const int last_len = seg_len(nch - 1);
+  const long long s00 = seg0 * kStatsResetInterval;
+  const double dm = static_cast<double>(m), inv_m = 1.0 / dm;
 
-  auto stage = [&](int tile) {  // warp 1: (in, out) of `tile` for every chain, asynchronously
-    for (int c = 0; c < nch; ++c) {
-      const long long s0 = (seg0 + c) * kStatsResetInterval;
-      const long long t0 = static_cast<long long>(tile) * kStatsTile;
-      const int cnt = tile_cnt(c, tile);
-      double2* io = s_io + ((tile & 1) * kStatsChains + c) * kStatsRow;
-      for (int k = lane; k < cnt; k += 32) {
-        const long long s = s0 + t0 + k;
-        if (s > s0) {
-          cp_async8(&io[k].x, ref + s + m - 1);
-          cp_async8(&io[k].y, ref + s - 1);
+  // warp 4: tile t's `in` row of chain c starts at s0 + t*T + m - 1 - OFF_IN,
+  // its `out` row at s0 + t*T - 1 - OFF_OUT (16-byte aligned).  All rows of a
+  // tile lie inside [0, n) except in the reference's first and last tiles;
+  // those rows are filled element by element.
+  const long long last_row = (seg0 + nch - 1) * kStatsResetInterval;
+  auto produce = [&](int t) {
+    const int slot = t % kChainDepth;
+    const long long t0 = static_cast<long long>(t) * kChainTile;
+    const long long a_in = s00 + t0 + m - 1 - OFF_IN, a_out = s00 + t0 - 1 - OFF_OUT;
+    double* rin = ring + (slot * 2 + 0) * kChainLanes * kChainRow;
+    double* rout = ring + (slot * 2 + 1) * kChainLanes * kChainRow;
+    if (a_out >= 0 && last_row + t0 + m - 1 - OFF_IN + kChainRow <= n) {
+      const double* gi = ref + a_in + 2 * lane;
+      const double* go = ref + a_out + 2 * lane;
+#pragma unroll 4
+      for (int c = 0; c < nch; ++c) {
+#pragma unroll
+        for (int k = 2 * lane; k < kChainRow; k += 64) {
+          cp_async16(rin + c * kChainRow + k, gi + k - 2 * lane);
+          cp_async16(rout + c * kChainRow + k, go + k - 2 * lane);
+        }
+        gi += kStatsResetInterval;
+        go += kStatsResetInterval;
+      }
+      mbar_arrive_cp_async(&slot_full[slot]);
+    } else {
+      for (int c = 0; c < nch; ++c) {
+        const long long ai = a_in + c * kStatsResetInterval, ao = a_out + c * kStatsResetInterval;
+        for (int k = lane; k < kChainRow; k += 32) {
+          rin[c * kChainRow + k] = (ai + k >= 0 && ai + k < n) ? ref[ai + k] : 0.0;
+          rout[c * kChainRow + k] = (ao + k >= 0 && ao + k < n) ? ref[ao + k] : 0.0;
         }
       }
+      mbar_arrive(&slot_full[slot]);
     }
   };
-  // warps 1..3: (sum, sumsq) of `tile` -> mean, stddev (search.hpp:34-41,
-  // search.cpp:35), correctly rounded div/sqrt, written out coalesced
-  const double dm = static_cast<double>(m);
-  auto flush = [&](int tile) {
-    const int h = tid - 32;  // 0 .. 95
-    for (int c = 0; c < nch; ++c) {
-      const long long s0 = (seg0 + c) * kStatsResetInterval;
-      const long long t0 = static_cast<long long>(tile) * kStatsTile;
-      const int cnt = tile_cnt(c, tile);
-      const double2* acc = s_acc + ((tile & 1) * kStatsChains + c) * kStatsRow;
-      for (int k = h; k < cnt; k += 96) {
-        const double2 v = acc[k];
-        const double mu = __ddiv_rn(v.x, dm);
-        const double var = __dsub_rn(__ddiv_rn(v.y, dm), __dmul_rn(mu, mu));
-        mean_out[s0 + t0 + k] = mu;
-        sd_out[s0 + t0 + k] = __dsqrt_rn(var > 0.0 ? var : 0.0);
+  // converter warps: (sum, sumsq) of tile t -> (mean, stddev), 16-byte pairs
+  // (segments and tiles start at even indices; mean / sd are 16-byte aligned)
+  auto convert = [&](int t) {
+    const int b = t & 1;
+    const long long t0 = static_cast<long long>(t) * kChainTile;
+    const double* as = acc + (b * 2 + 0) * kChainLanes * kChainRow;
+    const double* aq = acc + (b * 2 + 1) * kChainLanes * kChainRow;
+    const int full_cnt = static_cast<int>(min(static_cast<long long>(kChainTile), kStatsResetInterval - t0));
+    const int last_cnt = static_cast<int>(max(0LL, min(static_cast<long long>(kChainTile), last_len - t0)));
+    const int rank = warp < 4 ? warp - 1 : warp - 2;
+    for (int i = rank * 32 + lane; i < nch * (kChainTile / 2); i += kChainConverters * 32) {
+      const int c = i / (kChainTile / 2), k = 2 * (i % (kChainTile / 2));
+      const int cnt = c == nch - 1 ? last_cnt : full_cnt;
+      if (k >= cnt) continue;
+      const double2 v = *reinterpret_cast<const double2*>(as + c * kChainRow + k);
+      const double2 w = *reinterpret_cast<const double2*>(aq + c * kChainRow + k);
+      const long long s = s00 + c * kStatsResetInterval + t0 + k;
+      double m0, d0, m1, d1;
+      stats_of<POW2>(v.x, w.x, dm, inv_m, m0, d0);
+      if (k + 1 < cnt) {
+        stats_of<POW2>(v.y, w.y, dm, inv_m, m1, d1);
+        *reinterpret_cast<double2*>(mean_out + s) = make_double2(m0, m1);
+        *reinterpret_cast<double2*>(sd_out + s) = make_double2(d0, d1);
+      } else {
+        mean_out[s] = m0;
+        sd_out[s] = d0;
       }
     }
   };
 
-  const bool chain = tid < nch;  // warp 0, lanes 0..nch-1
+  if (threadIdx.x == 0) {
+    for (int d = 0; d < kChainDepth; ++d) {
+      mbar_init(&slot_full[d], 32);
+      mbar_init(&slot_empty[d], 1);
+    }
+    for (int d = 0; d < 2; ++d) {
+      mbar_init(&acc_full[d], 1);
+      mbar_init(&acc_empty[d], kChainConverters);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  // No block-wide barrier after this point: every hand-over is an mbarrier
+  // phase (use u of a slot or buffer completes phase u, parity u & 1).
+  if (warp == 4) {  // loads run ahead as far as the ring allows
+    for (int t = 0; t < ntiles; ++t) {
+      if (t >= kChainDepth) mbar_wait(&slot_empty[t % kChainDepth], ((t / kChainDepth) - 1) & 1);
+      produce(t);
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    return;
+  }
+  if (warp >= 1) {  // converters
+    for (int t = 0; t < ntiles; ++t) {
+      mbar_wait(&acc_full[t & 1], (t >> 1) & 1);
+      convert(t);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[t & 1]);
+    }
+    return;
+  }
+  // warp 0: the chains
   double sum = 0.0, sq = 0.0;
-  int clen = 0;
-  if (chain) {  // RunningStats::over(ref[s0 : s0+m]) (search.cpp:25-33)
-    const long long s0 = (seg0 + tid) * kStatsResetInterval;
-    clen = static_cast<int>(seg_len(tid));
+  if (lane < nch) {  // RunningStats::over(ref[s0 : s0+m]) (search.cpp:25-33)
+    const long long s0 = (seg0 + lane) * kStatsResetInterval;
 #pragma unroll 16
     for (int k = 0; k < m; ++k) {
       const double x = ref[s0 + k];
@@ -168,47 +282,86 @@ __global__ void __launch_bounds__(128) stats_chain_kernel(const double* __restri
       sq = __dadd_rn(sq, __dmul_rn(x, x));
     }
   }
-  const bool stager = tid >= 32 && tid < 64;  // warp 1
-  if (stager) {
-    stage(0);
-    cp_async_wait_all();
-  }
-  __syncthreads();
-  for (int tile = 0; tile <= ntiles; ++tile) {
-    if (stager && tile + 1 < ntiles) stage(tile + 1);  // in flight during this tile
-    if (chain && tile < ntiles) {
-      const int t0 = tile * kStatsTile;
-      const int cnt = max(0, min(kStatsTile, clen - t0));
-      const double2* io = s_io + ((tile & 1) * kStatsChains + tid) * kStatsRow;
-      double2* acc = s_acc + ((tile & 1) * kStatsChains + tid) * kStatsRow;
-      int k = 0;
-      if (t0 == 0 && cnt > 0) {  // the segment's first position is the batch over() result
-        acc[0] = make_double2(sum, sq);
-        k = 1;
-      }
-      // stats.add(in); stats.remove(out) (search.hpp:23-32), 8 steps per batch
-      // of hoisted shared-memory loads so only the two DADD chains are exposed.
-      for (; k + 8 <= cnt; k += 8) {
-        double2 v[8];
+  for (int t = 0; t < ntiles; ++t) {
+    const int slot = t % kChainDepth;
+    mbar_wait(&slot_full[slot], (t / kChainDepth) & 1);
+    if (t >= 2) mbar_wait(&acc_empty[t & 1], ((t >> 1) - 1) & 1);
+    if (lane < kChainLanes) {
+      const double* rin = ring + ((slot * 2 + 0) * kChainLanes + lane) * kChainRow;
+      const double* rout = ring + ((slot * 2 + 1) * kChainLanes + lane) * kChainRow;
+      double* as = acc + (((t & 1) * 2 + 0) * kChainLanes + lane) * kChainRow;
+      double* aq = acc + (((t & 1) * 2 + 1) * kChainLanes + lane) * kChainRow;
+      // stats.add(in); stats.remove(out) (search.hpp:23-32).  A batch is 8
+      // slides: its (in, out) values and their squares are in registers
+      // before it starts.  Lanes past their segment's end (the short last
+      // one) compute on filler values that are never stored.
+      struct Batch {
+        double in[8], out[8], qi[8], qo[8];
+      };
+      auto load = [&](int k, Batch& b) {
+        double vi[10], vo[10];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = io[k + u];
+        for (int u = 0; u < 5; ++u) {
+          const double2 a = *reinterpret_cast<const double2*>(rin + k + 2 * u);
+          const double2 c = *reinterpret_cast<const double2*>(rout + k + 2 * u);
+          vi[2 * u] = a.x;
+          vi[2 * u + 1] = a.y;
+          vo[2 * u] = c.x;
+          vo[2 * u + 1] = c.y;
+        }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-          sum = __dsub_rn(__dadd_rn(sum, v[u].x), v[u].y);
-          sq = __dsub_rn(__dadd_rn(sq, __dmul_rn(v[u].x, v[u].x)), __dmul_rn(v[u].y, v[u].y));
-          acc[k + u] = make_double2(sum, sq);
+          b.in[u] = vi[u + OFF_IN];
+          b.out[u] = vo[u + OFF_OUT];
         }
-      }
-      for (; k < cnt; ++k) {
-        const double2 v = io[k];
-        sum = __dsub_rn(__dadd_rn(sum, v.x), v.y);
-        sq = __dsub_rn(__dadd_rn(sq, __dmul_rn(v.x, v.x)), __dmul_rn(v.y, v.y));
-        acc[k] = make_double2(sum, sq);
+      };
+      auto squares = [&](Batch& b) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          b.qi[u] = __dmul_rn(b.in[u], b.in[u]);
+          b.qo[u] = __dmul_rn(b.out[u], b.out[u]);
+        }
+      };
+      auto run = [&](int k, const Batch& b) {
+        double ps[8], pq[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (u == 0 && t == 0 && k == 0) {  // the segment's first position: the over() result
+            ps[0] = sum;
+            pq[0] = sq;
+            continue;
+          }
+          sum = __dsub_rn(__dadd_rn(sum, b.in[u]), b.out[u]);
+          sq = __dsub_rn(__dadd_rn(sq, b.qi[u]), b.qo[u]);
+          ps[u] = sum;
+          pq[u] = sq;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          *reinterpret_cast<double2*>(as + k + 2 * u) = make_double2(ps[2 * u], ps[2 * u + 1]);
+          *reinterpret_cast<double2*>(aq + k + 2 * u) = make_double2(pq[2 * u], pq[2 * u + 1]);
+        }
+      };
+      Batch b0, b1;
+      load(0, b0);
+      squares(b0);
+#pragma unroll 1
+      for (int k = 0; k < kChainTile; k += 16) {
+        load(k + 8, b1);
+        squares(b1);
+        run(k, b0);
+        if (k + 16 < kChainTile) {
+          load(k + 16, b0);
+          squares(b0);
+        }
+        run(k + 8, b1);
       }
     }
-    if (tid >= 32 && tile >= 1) flush(tile - 1);
-    if (stager) cp_async_wait_all();
-    __syncthreads();
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive(&slot_empty[slot]);
+      mbar_arrive(&acc_full[t & 1]);
+    }
   }
 }
 
@@ -218,14 +371,26 @@ cudaError_t launch_stats(const double* ref, long long n, int m, double* mean, do
   const long long nseg = (ncand + kStatsResetInterval - 1) / kStatsResetInterval;
   if (seg_end < 0 || seg_end > nseg) seg_end = nseg;
   if (seg_begin >= seg_end) return cudaSuccess;
-  const long long blocks = (seg_end - seg_begin + kStatsChains - 1) / kStatsChains;
-  const size_t smem = 4 * static_cast<size_t>(kStatsChains) * kStatsRow * sizeof(double2);
-  {
-    const cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(stats_chain_kernel), smem);
-    if (e != cudaSuccess) return e;
-  }
-  stats_chain_kernel<<<static_cast<unsigned>(blocks), 128, smem, stream>>>(ref, n, m, mean, sd,
-                                                                           seg_begin, seg_end);
+  // 16-byte pair stores (segments start at even indices)
+  if ((reinterpret_cast<uintptr_t>(mean) | reinterpret_cast<uintptr_t>(sd)) & 15) return cudaErrorInvalidValue;
+  // row starts s0 + t*T + m - 1 - OFF_IN and s0 + t*T - 1 - OFF_OUT must be
+  // 16-byte aligned; s0 + t*T is even
+  const unsigned par = static_cast<unsigned>((reinterpret_cast<uintptr_t>(ref) >> 3) & 1);
+  const int off_in = static_cast<int>((par + static_cast<unsigned>(m - 1)) & 1);
+  const int off_out = static_cast<int>((par + 1u) & 1);
+  const bool pow2 = (m & (m - 1)) == 0;
+  using Fn = void (*)(const double*, long long, int, double*, double*, long long, long long);
+  static const Fn fns[2][2][2] = {
+      {{stats_chain_kernel<0, 0, false>, stats_chain_kernel<0, 0, true>},
+       {stats_chain_kernel<0, 1, false>, stats_chain_kernel<0, 1, true>}},
+      {{stats_chain_kernel<1, 0, false>, stats_chain_kernel<1, 0, true>},
+       {stats_chain_kernel<1, 1, false>, stats_chain_kernel<1, 1, true>}}};
+  const Fn fn = fns[off_in][off_out][pow2 ? 1 : 0];
+  const cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(fn), kChainSmem);
+  if (e != cudaSuccess) return e;
+  const long long blocks = (seg_end - seg_begin + kChainLanes - 1) / kChainLanes;
+  fn<<<static_cast<unsigned>(blocks), kChainThreads, kChainSmem, stream>>>(ref, n, m, mean, sd, seg_begin,
+                                                                           seg_end);
   return cudaGetLastError();
 }
 
@@ -239,13 +404,150 @@ cudaError_t launch_stats(const double* ref, long long n, int m, double* mean, do
 // envelope is built ONCE for the whole reference with radius r; at the two
 // candidate edges (j < r or j > m-1-r) the global window is a superset of the
 // candidate's clamped window, which only loosens the bound (still sound).
-// Sparse-table doubling in shared memory: with K = 2r+1 and P the largest
-// power of two <= K, max over [p-r, p+r] = max(M_P[p-r], M_P[p+r-P+1]) where
-// M_s[i] = max(a[i .. i+s-1]).  M_P is built from M_1 = a in log2(P) fully
-// parallel passes (ping-pong buffers); max and min are done one after the
-// other.  Every pass touches the whole tile with all threads, so the kernel
-// streams at shared-memory speed instead of following a dependent scan.
+//
+// Window K = 2r+1 >= 8: two-level van Herk / Gil-Werman per tile.  Level 1:
+// blocks of 8 positions, one per thread, prefix and suffix max/min in
+// registers -> shared memory (g, h).  Level 2: the block maxima/minima,
+// doubled k times (k = floor(log2(q-1)), q = floor((K-1)/8)) so that one
+// lookup pair covers any run of q-1 or q whole blocks.  The window [s, s+K-1]
+// is then h[s] (rest of s's block), g[s+K-1] (the last block up to s+K-1) and
+// the whole blocks strictly between: ~12 shared-memory accesses per position
+// for both envelopes instead of the ~50 of plain doubling, so the kernel runs
+// at HBM speed (reads 8 B, writes 16 B per position).
+// K < 8 (or a tile too large for shared memory): sparse-table doubling.
 // ---------------------------------------------------------------------------
+constexpr int kEnvThreads = 256;
+struct EnvGeom {
+  int gw;      // 1: Gil-Werman kernel, 0: doubling kernel
+  int len, T;  // loaded positions, outputs per tile
+  int nb, k;   // Gil-Werman: blocks of 8 per tile, doubling passes over them
+  size_t smem;
+};
+__host__ __device__ inline int env_pad(int i) { return i + (i >> 3); }  // 9-double lane stride
+
+static EnvGeom env_geom(int r) {
+  EnvGeom g{};
+  const long long K = 2LL * r + 1;
+  if (K >= 8) {
+    const long long len = std::max<long long>(2048, (2LL * r + 1 + 1024 + 63) / 64 * 64);
+    const long long nb = len / 8;
+    const long long q = (K - 1) / 8;
+    int k = 0;
+    while ((2LL << k) <= q - 1) ++k;
+    const size_t smem = 4 * static_cast<size_t>(env_pad(static_cast<int>(std::min(len, 1LL << 24)))) * 8 +
+                        4 * static_cast<size_t>(nb) * 8;
+    if (len < (1LL << 24) && smem <= 200 * 1024) {
+      g.gw = 1;
+      g.len = static_cast<int>(len);
+      g.T = static_cast<int>(len - 2 * r - 1);
+      g.nb = static_cast<int>(nb);
+      g.k = k;
+      g.smem = smem;
+      return g;
+    }
+  }
+  // two ping-pong arrays of (T + 2r) doubles within 64 KB (3 blocks per SM)
+  const long long cap = (64 * 1024) / (2 * 8);
+  long long T = cap - 2LL * r;
+  if (T > 8192) T = 8192;
+  g.gw = 0;
+  g.T = static_cast<int>(std::max<long long>(T, -1));
+  g.len = static_cast<int>(std::max<long long>(T + 2LL * r, 0));
+  g.smem = 2 * static_cast<size_t>(std::max(g.len, 0)) * sizeof(double);
+  return g;
+}
+
+__global__ void __launch_bounds__(kEnvThreads) envelope_gw_kernel(
+    const double* __restrict__ ref, long long n, int r, int T, int len, int nb, int k,
+    double2* __restrict__ env, long long tile_begin) {
+  extern __shared__ double esm[];
+  const int plen = env_pad(len);
+  double* gmax = esm;
+  double* gmin = esm + plen;
+  double* hmax = esm + 2 * plen;
+  double* hmin = esm + 3 * plen;
+  double* st = esm + 4 * plen;  // [2 ping-pong][max, min][nb]
+  const long long P0 = (tile_begin + blockIdx.x) * static_cast<long long>(T);  // first output
+  // first loaded position, even-aligned in memory so blocks load as 16-byte pairs
+  const long long Ar = P0 - r;
+  const int d = static_cast<int>(((reinterpret_cast<uintptr_t>(ref) >> 3) + static_cast<uintptr_t>(Ar)) & 1);
+  const long long A = Ar - d;
+  // level 1: prefix / suffix max and min of each 8-position block
+  for (int b = threadIdx.x; b < nb; b += kEnvThreads) {
+    const long long p = A + 8LL * b;
+    double vx[8], vn[8];
+    if (p >= 0 && p + 8 <= n) {
+      const double2* src = reinterpret_cast<const double2*>(ref + p);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double2 t = __ldg(src + u);
+        vx[2 * u] = vn[2 * u] = t.x;
+        vx[2 * u + 1] = vn[2 * u + 1] = t.y;
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const bool in = p + u >= 0 && p + u < n;
+        const double x = in ? ref[p + u] : 0.0;
+        vx[u] = in ? x : -d_inf();
+        vn[u] = in ? x : d_inf();
+      }
+    }
+    const int o = env_pad(8 * b);
+    double ax = vx[0], an = vn[0];
+    gmax[o] = ax;
+    gmin[o] = an;
+#pragma unroll
+    for (int u = 1; u < 8; ++u) {
+      ax = fmax(ax, vx[u]);
+      an = fmin(an, vn[u]);
+      gmax[o + u] = ax;
+      gmin[o + u] = an;
+    }
+    st[b] = ax;       // block maximum
+    st[nb + b] = an;  // block minimum
+    ax = vx[7];
+    an = vn[7];
+    hmax[o + 7] = ax;
+    hmin[o + 7] = an;
+#pragma unroll
+    for (int u = 6; u >= 0; --u) {
+      ax = fmax(ax, vx[u]);
+      an = fmin(an, vn[u]);
+      hmax[o + u] = ax;
+      hmin[o + u] = an;
+    }
+  }
+  __syncthreads();
+  // level 2: block extrema over runs of 2^k blocks
+  for (int j = 0; j < k; ++j) {
+    const double* sx = st + (j & 1) * 2 * nb;
+    double* dx = st + ((j + 1) & 1) * 2 * nb;
+    const int valid = nb - (2 << j) + 1;
+    for (int b = threadIdx.x; b < valid; b += kEnvThreads) {
+      dx[b] = fmax(sx[b], sx[b + (1 << j)]);
+      dx[nb + b] = fmin(sx[nb + b], sx[nb + b + (1 << j)]);
+    }
+    __syncthreads();
+  }
+  const double* sk = st + (k & 1) * 2 * nb;
+  const int K = 2 * r + 1;
+  for (int t = threadIdx.x; t < T; t += kEnvThreads) {
+    const long long P = P0 + t;
+    if (P >= n) break;
+    const int s = t + d, e = s + K - 1;
+    double mx = fmax(hmax[env_pad(s)], gmax[env_pad(e)]);
+    double mn = fmin(hmin[env_pad(s)], gmin[env_pad(e)]);
+    const int a = s >> 3, z = e >> 3;
+    if (z - a >= 2) {  // whole blocks a+1 .. z-1: two overlapping runs of 2^k
+      const int lo = a + 1, hi = z - (1 << k);
+      mx = fmax(mx, fmax(sk[lo], sk[hi]));
+      mn = fmin(mn, fmin(sk[nb + lo], sk[nb + hi]));
+    }
+    env[P] = make_double2(mx, mn);
+  }
+}
+
 template <bool MAX>
 __device__ __forceinline__ double pick(double a, double b) {
   return MAX ? (a > b ? a : b) : (a < b ? a : b);
@@ -291,26 +593,25 @@ __global__ void __launch_bounds__(512) envelope_kernel(const double* __restrict_
   envelope_doubling<false>(ref, n, A, len, r, T, P0, smem, smem + len, env);
 }
 
-int envelope_tile(int r) {
-  // two ping-pong arrays of (T + 2r) doubles within 64 KB (3 blocks per SM)
-  const int cap = (64 * 1024) / (2 * 8);
-  int T = cap - 2 * r;
-  if (T > 8192) T = 8192;
-  return T;
-}
+int envelope_tile(int r) { return env_geom(r).T; }
 
 cudaError_t launch_envelope(const double* ref, long long n, int r, double* env,
                             cudaStream_t stream, long long tile_begin, long long tile_end) {
-  const int T = envelope_tile(r);
-  if (T < 256) return cudaErrorInvalidValue;  // caller disables the EC tier
-  const size_t smem = 2 * static_cast<size_t>(T + 2 * r) * sizeof(double);
-  cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(envelope_kernel), smem);
+  const EnvGeom g = env_geom(r);
+  if (g.T < 256) return cudaErrorInvalidValue;  // caller disables the EC tier
+  const void* fn = g.gw ? reinterpret_cast<const void*>(envelope_gw_kernel)
+                        : reinterpret_cast<const void*>(envelope_kernel);
+  cudaError_t e = ensure_dyn_smem(fn, g.smem);
   if (e != cudaSuccess) return e;
-  const long long ntiles = (n + T - 1) / T;
+  const long long ntiles = (n + g.T - 1) / g.T;
   if (tile_end < 0 || tile_end > ntiles) tile_end = ntiles;
   if (tile_begin >= tile_end) return cudaSuccess;
-  envelope_kernel<<<static_cast<unsigned>(tile_end - tile_begin), 512, smem, stream>>>(
-      ref, n, r, T, env, tile_begin);
+  const unsigned grid = static_cast<unsigned>(tile_end - tile_begin);
+  if (g.gw)
+    envelope_gw_kernel<<<grid, kEnvThreads, g.smem, stream>>>(ref, n, r, g.T, g.len, g.nb, g.k,
+                                                              reinterpret_cast<double2*>(env), tile_begin);
+  else
+    envelope_kernel<<<grid, 512, g.smem, stream>>>(ref, n, r, g.T, env, tile_begin);
   return cudaGetLastError();
 }
 

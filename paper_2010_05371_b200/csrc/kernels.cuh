@@ -149,6 +149,7 @@ struct Nn1Params {
 
 // Each launcher enqueues on `stream` and returns the launch error (no sync).
 // Segments [seg_begin, seg_end) of kStatsResetInterval candidates (-1: all).
+constexpr int kStatsLaunches = 1;
 cudaError_t launch_stats(const double* ref, long long n, int m, double* mean, double* sd,
                          cudaStream_t stream, long long seg_begin = 0, long long seg_end = -1);
 // env: 2n doubles, (max, min) interleaved; output tiles [tile_begin, tile_end)

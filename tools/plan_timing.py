@@ -2,6 +2,7 @@
 given build of the library (A/B and bisection of builds):
     python tools/plan_timing.py lib1.so [lib2.so ...]"""
 import ctypes as C
+import os
 import sys
 
 import numpy as np
@@ -14,7 +15,7 @@ class Cfg(C.Structure):
                 ("tighten_ub", C.c_int32), ("reserved_", C.c_int32)]
 
 
-def run(path, n=100_000_000, m=1024, ratio=205 / 1024, reps=int(__import__("os").environ.get("REPS", "4"))):
+def run(path, n=100_000_000, m=1024, ratio=205 / 1024, reps=int(os.environ.get("REPS", "4"))):
     L = C.CDLL(path)
     vp = C.c_void_p
     L.eapdtw_ctx_create.argtypes = [C.POINTER(vp), C.c_int]
@@ -28,6 +29,10 @@ def run(path, n=100_000_000, m=1024, ratio=205 / 1024, reps=int(__import__("os")
     L.eapdtw_search_plan_result.argtypes = [vp, C.c_char_p]
     ctx = vp()
     assert L.eapdtw_ctx_create(C.byref(ctx), 0) == 0
+    for kv in filter(None, os.environ.get("OPTS", "").split(",")):
+        k, v = kv.split("=")
+        L.eapdtw_ctx_set_option.argtypes = [vp, C.c_char_p, C.c_longlong]
+        assert L.eapdtw_ctx_set_option(ctx, k.encode(), int(v)) == 0, kv
     ref = np.empty(n)
     q = np.empty(m)
     L.eapdtw_random_walk_normal(n, 20261019, ref.ctypes.data_as(C.POINTER(C.c_double)))
@@ -49,10 +54,13 @@ def run(path, n=100_000_000, m=1024, ratio=205 / 1024, reps=int(__import__("os")
         rows.append(list(t))
     L.eapdtw_search_plan_destroy(plan)
     med = np.median(np.array(rows[1:]), axis=0)
-    print(f"{path}: stats {med[0]:.3f} env {med[1]:.3f} warm {med[2]:.3f} sweep {med[3]:.3f} total {med.sum():.3f}",
+    print(f"{path} {os.environ.get('OPTS', '')}: stats {med[0]:.3f} env {med[1]:.3f} warm {med[2]:.3f} sweep {med[3]:.3f} total {med.sum():.3f}",
           flush=True)
 
 
 if __name__ == "__main__":
+    # CFG=cfg2|cfg3|cfg4 (bench.py's sizes)
+    size = {"cfg2": (1_000_000, 128, 0.05), "cfg3": (10_000_000, 512, 0.1),
+            "cfg4": (100_000_000, 1024, 205 / 1024)}[os.environ.get("CFG", "cfg4")]
     for p in sys.argv[1:]:
-        run(p)
+        run(p, *size)
