@@ -83,7 +83,8 @@ int eapdtw_ctx_set_stream(eapdtw_ctx* ctx, void* cuda_stream);
  *   rank_ub_w 4, rank_ub_k 16, rank_cascade 1, coarse_stride 0, probe 2048,
  *   probe_force 0, tighten 1, cb_strip 1, warps 0, nn1_splits 0, nn1_warm 1,
  *   series_cache 1, probe_strips 1 (FP32 screen: strips probed in each direction),
- *   producers 0, probe_warm 1, prep_overlap 1 (envelope beside the stats chain).
+ *   producers 0, probe_warm 0, prep_overlap 1 (envelope beside the stats chain),
+ *   warm_f32 1.
  * Every value returns the reference's answer; the defaults are the fastest
  * measured.  EAPDTW_EINVAL for an unknown name or out-of-range value. */
 int eapdtw_ctx_set_option(eapdtw_ctx* ctx, const char* name, int64_t value);

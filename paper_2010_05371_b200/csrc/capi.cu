@@ -77,6 +77,7 @@ enum Opt : int {
   kOptProducers,      // search sweep: SMSP-0 warps are LB producers until this queue backlog (0: off)
   kOptProbeWarm,      // the FP32 probe also in the warm-start passes (probe, rank)
   kOptPrepOverlap,    // envelope beside the stats chain on a side stream (0: after it)
+  kOptWarmF32,        // FP32 screen in the warm-start cascade (upper-bound wave and ranked list)
   kNumOpts
 };
 struct OptDef {
@@ -91,8 +92,8 @@ constexpr OptDef kOpts[kNumOpts] = {
     {"coarse_stride", 0, 0, 1 << 20}, {"probe", 2048, 1, 1 << 24}, {"probe_force", 0, 0, 1},
     {"tighten", 1, 0, 1},         {"cb_strip", 1, 1, 1 << 16},  {"warps", 0, 0, 8},
     {"nn1_splits", 0, 0, 1 << 16}, {"nn1_warm", 1, 0, 1},       {"series_cache", 1, 0, 1},
-    {"probe_strips", 1, 0, 8},    {"producers", 0, 0, 1 << 20}, {"probe_warm", 1, 0, 1},
-    {"prep_overlap", 1, 0, 1},
+    {"probe_strips", 1, 0, 8},    {"producers", 0, 0, 1 << 20}, {"probe_warm", 0, 0, 1},
+    {"prep_overlap", 1, 0, 1},   {"warm_f32", 1, 0, 1},
 };
 
 // Grow-only device buffer.
@@ -639,7 +640,10 @@ static int plan_init(eapdtw_search_plan* p, eapdtw_ctx* c, const double* ref_dev
     return fa != fb ? fa > fb : a < b;
   });
   std::copy(qn.begin(), qn.end(), q1.begin() + 1);
-  // (upper, lower) per position, and the same in visiting order
+  // (upper, lower) per position, and the same in visiting order.  (Outward-
+  // rounded floats for the visiting-order copy, half its L1 footprint,
+  // measured slower: cfg4 sweep +1.4 ms, the conversions and looser terms
+  // cost more than the cache hits gained.)
   std::vector<double> qul(2 * m), qperm(2 * m);
   for (size_t j = 0; j < m; ++j) {
     qul[2 * j] = qu[j];
@@ -656,7 +660,7 @@ static int plan_init(eapdtw_search_plan* p, eapdtw_ctx* c, const double* ref_dev
   CUDA_TRY(B.sd.ensure(nc * 8));
   CUDA_TRY(B.q.ensure((m + 1) * 8));
   CUDA_TRY(B.qul.ensure(m * 16));
-  CUDA_TRY(B.qperm.ensure(m * 16 + m * 8));  // double2 per position, then the float2 copy
+  CUDA_TRY(B.qperm.ensure(m * 16));
   CUDA_TRY(B.order.ensure(m * 4));
   CUDA_TRY(B.best.ensure(sizeof(BestRecord)));
   CUDA_TRY(B.key.ensure(8));
@@ -674,13 +678,6 @@ static int plan_init(eapdtw_search_plan* p, eapdtw_ctx* c, const double* ref_dev
   CUDA_TRY(cudaMemcpyAsync(B.q.p, q1.data(), (m + 1) * 8, cudaMemcpyHostToDevice, s));
   CUDA_TRY(cudaMemcpyAsync(B.qul.p, qul.data(), m * 16, cudaMemcpyHostToDevice, s));
   CUDA_TRY(cudaMemcpyAsync(B.qperm.p, qperm.data(), m * 16, cudaMemcpyHostToDevice, s));
-  {
-    std::vector<float> qp32(2 * m);  // FP32 Keogh tiers: fl32 of the envelope (guarded)
-    for (size_t k = 0; k < 2 * m; ++k) qp32[k] = static_cast<float>(qperm[k]);
-    // synchronous: the host vector dies at scope exit
-    CUDA_TRY(cudaMemcpy(static_cast<char*>(B.qperm.p) + m * 16, qp32.data(), m * 8,
-                        cudaMemcpyHostToDevice));
-  }
   CUDA_TRY(cudaMemcpyAsync(B.order.p, order.data(), m * 4, cudaMemcpyHostToDevice, s));
   // the staging vectors are pageable locals: wait until the copies consumed them
   CUDA_TRY(cudaStreamSynchronize(s));
@@ -966,6 +963,7 @@ static int stage_rank(eapdtw_search_plan* p, size_t cb, size_t ce) {
   CUDA_TRY(B.rlist.ensure(static_cast<size_t>(cap) * 8 + 64));
   SearchParams rp = base_params(p);
   if (!p->ctx->opt[kOptProbeWarm]) rp.probe_strips = 0;
+  if (!p->ctx->opt[kOptWarmF32]) rp.use_f32 = 0;
   rp.begin = static_cast<long long>(cb);
   rp.end = static_cast<long long>(ce);
   rp.counters = B.probe_counters.as<unsigned long long>();
