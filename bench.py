@@ -310,6 +310,16 @@ def apply_opts(ctx, args):
         ctx.set_option(k, int(v))
 
 
+def hbm_peak_gbs():
+    """The measured HBM copy bandwidth (MEASURED_PEAKS.json, driver-written), else
+    the profiling recipe's fallback for B200."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return {"value": float(json.load(f)["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    except (OSError, KeyError, ValueError):
+        return {"value": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
 def committed_ncu(cfg):
     """(DRAM bytes per launch, pipe/issue utilisation) of cfg's dominant kernel
     from the committed ncu capture (profiles/summarize.py report ... cfg)."""
@@ -742,6 +752,30 @@ def main():
         best, res = runner.search()
     torch.cuda.synchronize()
 
+    # ---- the preparation kernels timed apart (the searches below run the
+    #      envelope beside the stats chain on a side stream): achieved HBM GB/s
+    #      against the measured peak, algorithmic bytes = 8 B read per point +
+    #      16 B written per candidate (stats) / per point (envelope)
+    prep_kernels = None
+    if world == 1:
+        ctx.set_option("prep_overlap", 0)
+        pp = []
+        for _ in range(3):
+            runner.search()
+            pp.append(shard.plan.timings())
+        ctx.set_option("prep_overlap", int(dict(kv.split("=") for kv in args.opt).get("prep_overlap", 1)))
+        torch.cuda.synchronize()
+        hbm = hbm_peak_gbs()
+        prep_kernels = {}
+        for name, key_, nbytes in (("stats_chain_kernel", "stats", 8 * npts + 16 * ncand),
+                                   ("envelope_gw_kernel", "envelope", 24 * npts)):
+            ms_k = statistics.median(p_[key_] for p_ in pp)
+            if ms_k > 1e-3:
+                gbs = nbytes / (ms_k * 1e-3) / 1e9
+                prep_kernels[name] = {"ms": ms_k, "algorithmic_bytes": nbytes, "achieved_gbs": gbs,
+                                      "hbm_peak_gbs": hbm["value"], "peak_source": hbm["source"],
+                                      "frac": gbs / hbm["value"]}
+
     # ---- timed region: K device-resident searches
     launches0 = ctx.launches
     phases = []
@@ -844,6 +878,7 @@ def main():
             "dtw_gcups_counted": cells_mean / (ms_max * 1e-3) / 1e9,
             "full_band_equiv_gcups": ncand * band_cells(m, w) / (ms_max * 1e-3) / 1e9,
             "phase_ms": phase_ms,
+            "prep_kernels": prep_kernels,
             "counted_cells_per_search": cells_mean,
             "sweep_counters": shard.plan.counters(),
             "result": {"location": best[2], "distance_sq": best[1]},

@@ -82,6 +82,11 @@ __device__ __forceinline__ float f32_lower(float x, F32Guard g) {
   return s > 0.0f ? __fmul_rd(s, s) : 0.0f;
 }
 
+#ifndef EAPDTW_F32_BANDTEST
+#define EAPDTW_F32_BANDTEST 1
+#endif
+constexpr bool kF32BandTest = EAPDTW_F32_BANDTEST != 0;
+
 constexpr int kF32Undecided = 1;  // a row value exceeded cmax: run the FP64 engine
 
 // FP32 screening strip engine: the schedule of warp_dtw<false> (dtw_warp.cuh)
@@ -231,7 +236,12 @@ __device__ void f32_strip_run(F32Strip& s, int max_strips, bool want_slack, cons
       // Unbounded band: the band is the whole row, and the +inf padding of
       // qsp (dtw_warp.cuh) already makes every out-of-range column cost +inf,
       // so the per-step band test (3 ALU-pipe ops per cell) is dropped.
-      if (UNB && !banded) {
+      // EAPDTW_F32_BANDTEST=0: no per-step band test for banded pairs
+      // either.  Cells beyond a lane's band edges then take real costs: the
+      // DP of a wider band, a lower bound of the banded one, so an abandon is
+      // still sound (the exact engine applies the band); lanes still finish
+      // at their right band edge (finmask below).
+      if ((UNB && !banded) || !kF32BandTest) {
 #pragma unroll
         for (int u = 0; u < BLK; ++u) step(std::false_type{}, u, alld);
       } else {

@@ -1079,7 +1079,14 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
     // fetch stalls were the largest stall reason with every warp mixing both).
     unsigned warp_slot;
     asm volatile("mov.u32 %0, %%warpid;" : "=r"(warp_slot));
-    const bool producer = p.producer_smsp != 0 && (warp_slot & 3u) == 0u;
+    // p.producer_sm = M: the same split by SM (smid % M == 0 produces), so a
+    // whole SM's instruction cache holds one of the two code paths.
+    unsigned sm_id;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm_id));
+    const bool producer = (p.producer_smsp != 0 && (warp_slot & 3u) == 0u) ||
+                          (p.producer_sm > 0 && sm_id % static_cast<unsigned>(p.producer_sm) == 0u);
+    const unsigned long long backlog =
+        p.producer_smsp > 0 ? static_cast<unsigned long long>(p.producer_smsp) : 1024ull;
     for (;;) {
       long long cand = -1;
       float2 tot = z2;
@@ -1103,7 +1110,7 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
       if (lane == 0) {
         if (myslot < 0) {
           const unsigned long long h = vload(p.qhead), t = vload(p.qtail);
-          if (h < t && (!producer || !chunks_left || t - h > static_cast<unsigned long long>(p.producer_smsp)))
+          if (h < t && (!producer || !chunks_left || t - h > backlog))
             myslot = static_cast<long long>(atomicAdd(p.qhead, 1ull));
         }
         if (myslot >= 0) {

@@ -94,6 +94,7 @@ struct SearchParams {
   int screen_rows;               // phase-A lane screen depth (0: off)
   int probe_strips;              // FP32 strip screen: strips probed in each direction (0: forward only)
   int producer_smsp;             // > 0: SMSP-0 warps run the LB tiers, taking DTW tasks only past this backlog
+  int producer_sm;               // M > 0: every warp of the SMs with smid % M == 0 is such a producer
   int use_f32;                   // FP32 screening engine ahead of the exact FP64 one
   float f32_a, f32_b, f32_cmax;  // its threshold guard (dtw_f32.cuh) and row-value bound
   unsigned long long* counters;  // kNumCounters
