@@ -78,7 +78,7 @@ enum Opt : int {
   kOptProbeWarm,      // the FP32 probe also in the warm-start passes (probe, rank)
   kOptPrepOverlap,    // envelope beside the stats chain on a side stream (0: after it)
   kOptWarmF32,        // FP32 screen in the warm-start cascade (upper-bound wave and ranked list)
-  kOptProducerSms,    // search sweep: the SMs with smid % M == 0 are LB producers (0: off)
+  kOptCbEcStrip,      // first strip whose cumulative-bound thresholds also use the EC suffix
   kNumOpts
 };
 struct OptDef {
@@ -94,7 +94,7 @@ constexpr OptDef kOpts[kNumOpts] = {
     {"tighten", 1, 0, 1},         {"cb_strip", 1, 1, 1 << 16},  {"warps", 0, 0, 8},
     {"nn1_splits", 0, 0, 1 << 16}, {"nn1_warm", 1, 0, 1},       {"series_cache", 1, 0, 1},
     {"probe_strips", 1, 0, 8},    {"producers", 0, 0, 1 << 20}, {"probe_warm", 0, 0, 1},
-    {"prep_overlap", 1, 0, 1},   {"warm_f32", 1, 0, 1},      {"producer_sms", 0, 0, 148},
+    {"prep_overlap", 1, 0, 1},   {"warm_f32", 1, 0, 1},      {"cb_ec_strip", 2, 1, 1 << 16},
 };
 
 // Grow-only device buffer.
@@ -799,6 +799,7 @@ static SearchParams base_params(eapdtw_search_plan* p) {
   s.use_lb = p->use_lb ? 1 : 0;
   s.tighten = p->tighten ? 1 : 0;
   s.cb_strip = p->cb_strip;
+  s.cb_ec_strip = static_cast<int>(p->ctx->opt[kOptCbEcStrip]);
   // 0 full_scan, 1 EAPrunedDTW, 2 left_prune_scan (dtw.cpp:95-296)
   s.prune = p->algo == EAPDTW_ALGO_FULL ? 0 : (p->algo == EAPDTW_ALGO_LEFT_PRUNE ? 2 : 1);
   s.guard_rel = p->guard_rel;
@@ -825,7 +826,6 @@ static SearchParams base_params(eapdtw_search_plan* p) {
   s.probe_strips = static_cast<int>(p->ctx->opt[kOptProbeStrips]);
   s.gscratch = p->gmem ? B.scratch.as<double>() : nullptr;
   s.producer_smsp = static_cast<int>(p->ctx->opt[kOptProducers]);
-  s.producer_sm = static_cast<int>(p->ctx->opt[kOptProducerSms]);
   {
     // z-normalised rows satisfy |c| <= sqrt(m - 1); the engine checks the
     // bound per strip (degenerate statistics fall back to the exact engine)

@@ -82,8 +82,10 @@ __device__ __forceinline__ float f32_lower(float x, F32Guard g) {
   return s > 0.0f ? __fmul_rd(s, s) : 0.0f;
 }
 
+// Per-step band test of banded pairs: off (cfg4 sweep 41.5 -> 39.4 ms, all
+// parity tests green); see f32_strip_run.
 #ifndef EAPDTW_F32_BANDTEST
-#define EAPDTW_F32_BANDTEST 1
+#define EAPDTW_F32_BANDTEST 0
 #endif
 constexpr bool kF32BandTest = EAPDTW_F32_BANDTEST != 0;
 

@@ -894,11 +894,21 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
       if (!tight || i0 < 1 + 32 * (p.cb_strip - 1)) return u;
       auto pos = [&](int k) { return REV ? m - 1 - k : k; };
       const int k_eq = i0 - 1, k_ec = i0 + p.w - 1;  // lane 0's positions
+      // The EC prefix starts with strip p.cb_ec_strip (default 2): its first
+      // use sums the w + 32 positions before the strip's rows (L2 gathers of
+      // the candidate's envelope), which the many tasks that die in their
+      // first strip then never pay; until then cb is the EQ suffix alone.
+      const bool use_ec = have_ec && i0 >= 1 + 32 * (p.cb_ec_strip - 1);
       if (st.end_eq < 0) {  // positions before this strip's first ones
         st.end_eq = min(m, k_eq);
-        st.end_ec = min(m, k_ec);
-        double eq = 0.0, ec = 0.0;
+        double eq = 0.0;
         for (int k = lane; k < st.end_eq; k += 32) eq = __dadd_rn(eq, contrib_eq(pos(k)));
+        for (int off = 16; off > 0; off >>= 1) eq = __dadd_rn(eq, __shfl_xor_sync(kFull, eq, off));
+        st.eq = eq;
+      }
+      if (use_ec && st.end_ec < 0) {
+        st.end_ec = min(m, k_ec);
+        double ec = 0.0;
         // (4 positions per lane in flight: the envelope loads are L2 latency)
         for (int k0 = lane; k0 < st.end_ec; k0 += 128) {
           double t4[4];
@@ -910,18 +920,14 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
 #pragma unroll
           for (int u = 0; u < 4; ++u) ec = __dadd_rn(ec, t4[u]);
         }
-        for (int off = 16; off > 0; off >>= 1) {
-          eq = __dadd_rn(eq, __shfl_xor_sync(kFull, eq, off));
-          ec = __dadd_rn(ec, __shfl_xor_sync(kFull, ec, off));
-        }
-        st.eq = eq;
+        for (int off = 16; off > 0; off >>= 1) ec = __dadd_rn(ec, __shfl_xor_sync(kFull, ec, off));
         st.ec = ec;
       }
       // this strip's rows need prefixes through k_eq + lane and k_ec + lane
       const int ke = k_eq + lane, kc = k_ec + lane;
       double a = 0.0, b = 0.0;
       if (ke >= st.end_eq && ke < m) a = contrib_eq(pos(ke));
-      if (kc >= st.end_ec && kc < m) b = contrib_ec(pos(kc));
+      if (use_ec && kc >= st.end_ec && kc < m) b = contrib_ec(pos(kc));
       for (int off = 1; off < 32; off <<= 1) {  // inclusive prefix scans
         const double x = __shfl_up_sync(kFull, a, off);
         const double y = __shfl_up_sync(kFull, b, off);
@@ -937,13 +943,13 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
         st.eq = __shfl_sync(kFull, peq, min(31, nxe - 1 - k_eq));
         st.end_eq = nxe;
       }
-      if (nxc > st.end_ec) {
+      if (use_ec && nxc > st.end_ec) {
         st.ec = __shfl_sync(kFull, pec, min(31, nxc - 1 - k_ec));
         st.end_ec = nxc;
       }
       if (i >= m) return u;  // the last row: nothing left
       const double ceq = __dsub_rn(teq, peq);
-      const double cec = kc < m - 1 ? __dsub_rn(tec, pec) : 0.0;
+      const double cec = use_ec && kc < m - 1 ? __dsub_rn(tec, pec) : 0.0;
       const double cbv = __dsub_rn(fmax(ceq, cec), cb_guard);
       if (!(cbv > 0.0)) return u;
       const double t = __dsub_rn(__dmul_rn(u, 1.0 + p.guard_rel), cbv);
@@ -1079,14 +1085,9 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
     // fetch stalls were the largest stall reason with every warp mixing both).
     unsigned warp_slot;
     asm volatile("mov.u32 %0, %%warpid;" : "=r"(warp_slot));
-    // p.producer_sm = M: the same split by SM (smid % M == 0 produces), so a
-    // whole SM's instruction cache holds one of the two code paths.
-    unsigned sm_id;
-    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm_id));
-    const bool producer = (p.producer_smsp != 0 && (warp_slot & 3u) == 0u) ||
-                          (p.producer_sm > 0 && sm_id % static_cast<unsigned>(p.producer_sm) == 0u);
-    const unsigned long long backlog =
-        p.producer_smsp > 0 ? static_cast<unsigned long long>(p.producer_smsp) : 1024ull;
+    // (The same split by SM -- smid % M == 0 produces, M = 2, 3, 4 -- measured
+    // +0.3 to +1 ms on the cfg4 sweep: not kept.)
+    const bool producer = p.producer_smsp != 0 && (warp_slot & 3u) == 0u;
     for (;;) {
       long long cand = -1;
       float2 tot = z2;
@@ -1110,7 +1111,7 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
       if (lane == 0) {
         if (myslot < 0) {
           const unsigned long long h = vload(p.qhead), t = vload(p.qtail);
-          if (h < t && (!producer || !chunks_left || t - h > backlog))
+          if (h < t && (!producer || !chunks_left || t - h > static_cast<unsigned long long>(p.producer_smsp)))
             myslot = static_cast<long long>(atomicAdd(p.qhead, 1ull));
         }
         if (myslot >= 0) {

@@ -76,6 +76,7 @@ struct SearchParams {
   int use_lb;                    // Kim -> Keogh EQ -> Keogh EC cascade
   int tighten;                   // per-row thresholds from the Keogh cumulative bound (search.cpp:101-105)
   int cb_strip;                  // first strip (1-based) that uses them
+  int cb_ec_strip;               // first strip whose thresholds also use the EC suffix (before: EQ alone)
   int prune;                     // 0: Algo::full (no pruning), 1: pruned DTW
   double guard_rel, guard_abs;   // LB soundness guard
   double guard_sqrt;             // ... and its reciprocal-normalisation term (lb_guard)
@@ -94,7 +95,6 @@ struct SearchParams {
   int screen_rows;               // phase-A lane screen depth (0: off)
   int probe_strips;              // FP32 strip screen: strips probed in each direction (0: forward only)
   int producer_smsp;             // > 0: SMSP-0 warps run the LB tiers, taking DTW tasks only past this backlog
-  int producer_sm;               // M > 0: every warp of the SMs with smid % M == 0 is such a producer
   int use_f32;                   // FP32 screening engine ahead of the exact FP64 one
   float f32_a, f32_b, f32_cmax;  // its threshold guard (dtw_f32.cuh) and row-value bound
   unsigned long long* counters;  // kNumCounters

@@ -101,6 +101,8 @@ int main(int argc, char** argv) {
   long long maxhist[12] = {0};        /* per-task max width */
   long long cells_by_max[12] = {0};   /* live cells, by the task's max width */
   const int edges[11] = {16, 32, 48, 64, 88, 104, 128, 144, 192, 256, 384};
+  long long rowhist[12] = {0}, rowcells[12] = {0}; /* rows survived: 0,1,2,<=4,8,16,32,64,128,256,512,>512 */
+  long long eqrow_hist[12] = {0}; /* the same with EQ-only thresholds (rows < 16 only) */
   long long drift_hist[8] = {0};      /* |centre(i) - centre(i-16)| per 16 rows: <=2,4,8,16,32,64,128,>128 */
   /* by d / ub of the task (full banded DTW): <=1, 1.1, 1.25, 1.5, 2, 3, >3 */
   long long dr_tasks[7] = {0}, dr_cells[7] = {0}, imp_tasks = 0, imp_cells = 0;
@@ -110,7 +112,7 @@ int main(int argc, char** argv) {
   long long greedy_cells[3] = {0};
   long long alt_cells[3] = {0};  /* K = 32: slack/T, extrapolated death row, slack at 32 + width */  /* strip-granular races: greedy least-slack (S = 16, 32, 64) */
   const double dedges[6] = {1.0, 1.1, 1.25, 1.5, 2.0, 3.0};
-#pragma omp parallel reduction(+ : tasks, cells, rows_sum, whist[:12], maxhist[:12], cells_by_max[:12], drift_hist[:8], dr_tasks[:7], dr_cells[:7], imp_tasks, imp_cells, rev_rows, rev_cells, min_rows, min_cells2, best_cells, pred_cells, pk_cells[:4][:2], greedy_cells[:3], alt_cells[:3])
+#pragma omp parallel reduction(+ : rowhist[:12], rowcells[:12], eqrow_hist[:12], tasks, cells, rows_sum, whist[:12], maxhist[:12], cells_by_max[:12], drift_hist[:8], dr_tasks[:7], dr_cells[:7], imp_tasks, imp_cells, rev_rows, rev_cells, min_rows, min_cells2, best_cells, pred_cells, pk_cells[:4][:2], greedy_cells[:3], alt_cells[:3])
   {
     double *c = malloc(m * 8), *cu = malloc(m * 8), *cl = malloc(m * 8);
     double *ceq = malloc(m * 8), *cec = malloc(m * 8), *cbnd = malloc(m * 8), *cbig = malloc(m * 8);
@@ -178,6 +180,45 @@ int main(int argc, char** argv) {
       }
       cells += tc;
       rows_sum += rows;
+      {
+        const int redges[11] = {0, 1, 2, 4, 8, 16, 32, 64, 128, 256, 512};
+        int rb = 0;
+        while (rb < 11 && rows > redges[rb]) ++rb;
+        rowhist[rb]++;
+        rowcells[rb] += tc;
+        /* EQ-only thresholds, first 16 rows */
+        orc_cumulative_bound(ceq, m, cbig);
+        long long c2 = 0;
+        /* thr(i) = ub - sum_{k >= i} ceq[k] (EQ terms are per row: rows after i still to pay) */
+        double suf = 0; 
+        double* sufa = cbig; /* reuse: suffix sums */
+        for (size_t k = m; k-- > 0;) { suf += ceq[k]; sufa[k] = suf; }
+        for (size_t j = 0; j <= m + 1; ++j) prev[j] = INFINITY;
+        prev[0] = 0.0;
+        int r2 = 0;
+        for (size_t i = 1; i <= 16; ++i) {
+          double thr = ub - (i < m ? sufa[i] : 0.0);
+          int any = 0;
+          const size_t bl = i > w ? i - w : 1, bh = i + w < m ? i + w : m;
+          for (size_t j = 0; j <= m + 1; ++j) cur[j] = INFINITY;
+          for (size_t j = bl; j <= bh && j <= i + 40; ++j) {
+            double mn = prev[j - 1];
+            if (prev[j] < mn) mn = prev[j];
+            if (cur[j - 1] < mn) mn = cur[j - 1];
+            if (mn == INFINITY) continue;
+            const double d = c[i - 1] - qn[j - 1];
+            const double v = d * d + mn;
+            if (v > thr) continue;
+            cur[j] = v; ++any;
+          }
+          if (!any) break;
+          ++r2;
+          double* t = prev; prev = cur; cur = t;
+        }
+        rb = 0;
+        while (rb < 11 && r2 > redges[rb]) ++rb;
+        eqrow_hist[rb]++;
+      }
       {  /* full banded DTW of the task, and LB_Improved (Lemire) both ways */
         for (size_t j = 0; j <= m + 1; ++j) prev[j] = INFINITY;
         prev[0] = 0.0;
@@ -340,6 +381,12 @@ int main(int argc, char** argv) {
   for (int b = 0; b < 12; ++b) printf(" %lld", maxhist[b]);
   printf("\nlive cells by task max width (%%):");
   for (int b = 0; b < 12; ++b) printf(" %.1f", 100.0 * cells_by_max[b] / cells);
+  printf("\nrows survived (0,1,2,<=4,8,16,32,64,128,256,512,>512): tasks");
+  for (int b = 0; b < 12; ++b) printf(" %lld", rowhist[b]);
+  printf(" | cells %%");
+  for (int b = 0; b < 12; ++b) printf(" %.1f", 100.0 * rowcells[b] / cells);
+  printf("\nEQ-only thresholds, rows survived of the first 16:");
+  for (int b = 0; b < 12; ++b) printf(" %lld", eqrow_hist[b]);
   printf("\ncentre drift per 16 rows (<=2,4,8,16,32,64,128,>128):");
   for (int b = 0; b < 8; ++b) printf(" %lld", drift_hist[b]);
   printf("\nby d/ub (<=1,1.1,1.25,1.5,2,3,>3): tasks");
