@@ -79,6 +79,7 @@ enum Opt : int {
   kOptPrepOverlap,    // envelope beside the stats chain on a side stream (0: after it)
   kOptWarmF32,        // FP32 screen in the warm-start cascade (upper-bound wave and ranked list)
   kOptCbEcStrip,      // first strip whose cumulative-bound thresholds also use the EC suffix
+  kOptProbeExcess,    // FP32 probe: the dropped direction's frontier minimum tightens the other's bound
   kNumOpts
 };
 struct OptDef {
@@ -95,6 +96,7 @@ constexpr OptDef kOpts[kNumOpts] = {
     {"nn1_splits", 0, 0, 1 << 16}, {"nn1_warm", 1, 0, 1},       {"series_cache", 1, 0, 1},
     {"probe_strips", 1, 0, 8},    {"producers", 0, 0, 1 << 20}, {"probe_warm", 0, 0, 1},
     {"prep_overlap", 1, 0, 1},   {"warm_f32", 1, 0, 1},      {"cb_ec_strip", 2, 1, 1 << 16},
+    {"probe_excess", 1, 0, 1},
 };
 
 // Grow-only device buffer.
@@ -800,6 +802,7 @@ static SearchParams base_params(eapdtw_search_plan* p) {
   s.tighten = p->tighten ? 1 : 0;
   s.cb_strip = p->cb_strip;
   s.cb_ec_strip = static_cast<int>(p->ctx->opt[kOptCbEcStrip]);
+  s.probe_excess = static_cast<int>(p->ctx->opt[kOptProbeExcess]);
   // 0 full_scan, 1 EAPrunedDTW, 2 left_prune_scan (dtw.cpp:95-296)
   s.prune = p->algo == EAPDTW_ALGO_FULL ? 0 : (p->algo == EAPDTW_ALGO_LEFT_PRUNE ? 2 : 1);
   s.guard_rel = p->guard_rel;
@@ -834,6 +837,7 @@ static SearchParams base_params(eapdtw_search_plan* p) {
     s.use_f32 = p->use_f32;
     s.f32_a = g.a;
     s.f32_b = g.b;
+    s.f32_ia = std::nextafter(static_cast<float>(1.0 / static_cast<double>(g.a)) , 0.0f);
     s.f32_cmax = static_cast<float>(cmax);
   }
   s.counters = B.counters.as<unsigned long long>();

@@ -120,6 +120,7 @@ struct F32Strip {
   unsigned cnt;   // evaluated cells (warp total)
   float ub_last;  // threshold of the row held in rowbuf
   float slack;    // ub_last - min of that row (after a strip run with want_slack)
+  float vmin;     // that minimum (over every cell of the row the strip evaluated)
   int status;     // 0, or kF32Undecided
 };
 
@@ -134,6 +135,7 @@ __device__ inline void f32_strip_begin(F32Strip& s, int lc, float* __restrict__ 
   s.cnt = 0;
   s.ub_last = INF;
   s.slack = INF;
+  s.vmin = 0.0f;
   s.status = 0;
   __syncwarp();
 }
@@ -315,6 +317,7 @@ __device__ void f32_strip_run(F32Strip& s, int max_strips, bool want_slack, cons
     if (want_slack) {
       for (int off = 16; off > 0; off >>= 1) vmin = fminf(vmin, __shfl_xor_sync(kFull, vmin, off));
       s.slack = ub_last - vmin;
+      s.vmin = vmin;
     }
     if (nhi < 0) {
       lo = -1;
@@ -382,17 +385,29 @@ __device__ float warp_dtw_f32(const RawFn& rowraw, const NormFn& rownorm, int lr
 // st: two F32Strip in shared memory (the warp's): the inactive direction's
 // state stays there, not in registers (the search kernel is at its register
 // budget; local memory would miss L1 under the large shared-memory carve-out).
-template <int BLK, bool UNB, class RawF, class RawR, class NormFn, class UbFn, class ThrF, class ThrR>
+// on_pick(use_r, vmin): called once both probes are alive, before the chosen
+// direction continues, with the minimum of the DROPPED direction's frontier
+// row: every path pays at least that (less the FP32 error) inside the rows
+// the dropped probe covered, which the caller may add to the continuing
+// direction's cumulative bound (kernels.cu: run_dtw).  If it did (returns
+// true), the bound no longer holds inside those rows: the continuing pass
+// stops before them, undecided if still alive.
+struct NoPick {
+  __device__ bool operator()(bool, float) const { return false; }
+};
+template <int BLK, bool UNB, class RawF, class RawR, class NormFn, class UbFn, class ThrF, class ThrR,
+          class PickFn = NoPick>
 __device__ float f32_probe_pair(const RawF& raw_f, const RawR& raw_r, const NormFn& rownorm, int lr,
                                 const float* __restrict__ qsp, int lc, int w, float cmax,
                                 UbFn&& get_ub, ThrF&& thr_f, ThrR&& thr_r,
                                 float* __restrict__ rowbuf_f, float* __restrict__ rowbuf_r,
-                                int probe, F32Strip* st, unsigned long long& cells, int& status) {
+                                int probe, F32Strip* st, unsigned long long& cells, int& status,
+                                PickFn&& on_pick = NoPick{}) {
   F32Strip& f = st[0];
   F32Strip& r = st[1];
   f32_strip_begin(f, lc, rowbuf_f);
   if (probe <= 0 || lr <= 32 * probe) probe = 0;
-  bool use_r = false;
+  bool use_r = false, limited = false;
   // phase 0: forward probe (or the whole forward pass); 1: reversed probe;
   // 2: the rest of the chosen direction
   for (int phase = 0; phase < 3; ++phase) {
@@ -402,12 +417,14 @@ __device__ float f32_probe_pair(const RawF& raw_f, const RawR& raw_r, const Norm
     }
     if (phase == 2) {
       use_r = r.lo < 0 || r.status != 0 || r.slack < f.slack;
+      if (r.lo >= 0 && r.status == 0) limited = on_pick(use_r, use_r ? f.vmin : r.vmin);
       int unused;
       if (use_r) f32_strip_end(f, lc, rowbuf_f, cells, unused);  // the dropped direction's cells count
       else f32_strip_end(r, lc, rowbuf_r, cells, unused);
     }
     const bool rev = phase == 1 || (phase == 2 && use_r);
-    const int n = (phase < 2 && probe > 0) ? probe : lr;
+    // (limited: the whole strips before the last 32 * probe rows)
+    const int n = (phase < 2 && probe > 0) ? probe : (limited ? (lr - 32 * probe) / 32 - probe : lr);
     if (rev)
       f32_strip_run<BLK, UNB, true>(r, n, phase == 1, raw_r, rownorm, lr, qsp, lc, w, cmax, get_ub,
                                     thr_r, rowbuf_r);
@@ -415,6 +432,11 @@ __device__ float f32_probe_pair(const RawF& raw_f, const RawR& raw_r, const Norm
       f32_strip_run<BLK, UNB, false>(f, n, phase == 0, raw_f, rownorm, lr, qsp, lc, w, cmax,
                                      get_ub, thr_f, rowbuf_f);
     if (phase == 0 && probe == 0) break;
+  }
+  if (limited) {
+    F32Strip& c = use_r ? r : f;
+    if (c.status == 0 && c.lo >= 0 && c.i0 <= lr) c.status = kF32Undecided;
+    __syncwarp();
   }
   return use_r ? f32_strip_end(r, lc, rowbuf_r, cells, status)
                : f32_strip_end(f, lc, rowbuf_f, cells, status);

@@ -889,6 +889,21 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
     CbPrefix* cbp = reinterpret_cast<CbPrefix*>(pstate + 2 * sizeof(F32Strip));
     if (lane == 0) cbp[0] = cbp[1] = CbPrefix{0.0, 0.0, -1, -1};
     __syncwarp();
+    // Both probes' evidence in one bound.  Once the FP32 screen has probed P
+    // rows from each end and picked a direction, the dropped probe's frontier
+    // row still says something: any path's cells in the P rows that probe
+    // covered cost at least the minimum R of that row (its DP runs from the
+    // corner to that row; as an FP32 value, at least f32_lower(R) in exact
+    // terms, dtw_f32.cuh).  The continuing direction's EQ suffix counts those
+    // P rows with their Keogh terms only (their sum is the dropped probe's EQ
+    // prefix), so for the rows before them the suffix grows by
+    // x = f32_lower(R) - prefix (when positive): every path still pays the
+    // Keogh terms of the rows in between plus R.  on_pick (below) subtracts x
+    // from the continuing pass's EQ prefix, which adds it to every later
+    // suffix at no cost per row; the bound does not hold inside the last P
+    // rows, so the screen then stops before them (undecided: the exact
+    // engine runs).  Design study (tools/live_study.c): 14% fewer live cells
+    // than the probe alone.
     auto rowthr_dir = [&](auto rev_tag, CbPrefix& st, double u, int i, int i0) -> double {
       constexpr bool REV = decltype(rev_tag)::value;
       if (!tight || i0 < 1 + 32 * (p.cb_strip - 1)) return u;
@@ -974,12 +989,29 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
         return f32_threshold(rowthr_dir(std::true_type{}, cbp[1], u, i, i0), g);
       };
       auto rowraw_r = [&](int r) -> double { return crow[m - 1 - r]; };
+      auto on_pick = [&](bool use_r, float other_vmin) -> bool {
+        if (!tight || !p.probe_excess) return false;
+        const CbPrefix& o = cbp[use_r ? 0 : 1];  // the dropped direction's prefixes
+        if (o.end_eq <= 0 || o.end_eq >= m) return false;
+        // rounded down, and less twice the bound's guard for the prefix's own error
+        // f32_lower without its division and root: (sqrt(y) - b)^2 >= y - 2 b sqrt(y)
+        // >= y (1 - b) - b with y = R / a (2 sqrt(y) <= 1 + y)
+        const float y = __fmul_rd(other_vmin, p.f32_ia);
+        const float lb = __fsub_rd(__fmul_rd(y, __fsub_rd(1.0f, p.f32_b)), p.f32_b);
+        const double x = __dsub_rd(__dsub_rd(static_cast<double>(lb), o.eq), 2.0 * cb_guard);
+        if (!(x > 0.0)) return false;
+        __syncwarp();
+        if (lane == 0) cbp[use_r ? 1 : 0].eq = __dsub_rd(cbp[use_r ? 1 : 0].eq, x);
+        __syncwarp();
+        return true;
+      };
       {
         // both directions probed, then the likelier to die (dtw_f32.cuh)
         int st = 0;
         const float r32 = f32_probe_pair<kSearchStepBlock, false>(
             rowraw, rowraw_r, rownorm32, m, qsp32, m, p.w, p.f32_cmax, get_ub, rowthr32,
-            rowthr32_r, rowbuf32, rowbuf32 + rowbuf32_len, p.probe_strips, probe_st, c_cells32, st);
+            rowthr32_r, rowbuf32, rowbuf32 + rowbuf32_len, p.probe_strips, probe_st, c_cells32, st,
+            on_pick);
         screened = st == 0 && r32 == f_inf();
       }
       // the cumulative-bound prefixes restart for the exact pass

@@ -76,6 +76,7 @@ struct SearchParams {
   int use_lb;                    // Kim -> Keogh EQ -> Keogh EC cascade
   int tighten;                   // per-row thresholds from the Keogh cumulative bound (search.cpp:101-105)
   int cb_strip;                  // first strip (1-based) that uses them
+  int probe_excess;              // the dropped probe's frontier minimum joins the continuing pass's bound
   int cb_ec_strip;               // first strip whose thresholds also use the EC suffix (before: EQ alone)
   int prune;                     // 0: Algo::full (no pruning), 1: pruned DTW
   double guard_rel, guard_abs;   // LB soundness guard
@@ -97,6 +98,7 @@ struct SearchParams {
   int producer_smsp;             // > 0: SMSP-0 warps run the LB tiers, taking DTW tasks only past this backlog
   int use_f32;                   // FP32 screening engine ahead of the exact FP64 one
   float f32_a, f32_b, f32_cmax;  // its threshold guard (dtw_f32.cuh) and row-value bound
+  float f32_ia;                  // <= 1 / f32_a (the guard's inverse without a division)
   unsigned long long* counters;  // kNumCounters
   long long index_offset;        // shard start in the global reference
   // list mode (rank pass): chunk c covers list[32c .. 32c+31] (candidate

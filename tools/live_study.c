@@ -30,6 +30,7 @@ int orc_cumulative_bound(const double* c, size_t l, double* cb);
 
 /* Pruned DP (dead cells killed) with row thresholds ub - cb[min(i+w, m) - 1]:
    returns rows survived, adds live cells to *cells. */
+static _Thread_local double g_extra = 0.0; static _Thread_local size_t g_kk_limit = 0;
 static int pruned_rows(const double* c, const double* qn, const double* cbnd, size_t m, size_t w,
                        double ub, double* prev, double* cur, long long* cells, int* rowcells,
                        double* slack) {
@@ -39,6 +40,7 @@ static int pruned_rows(const double* c, const double* qn, const double* cbnd, si
   for (size_t i = 1; i <= m; ++i) {
     const size_t kk = (i + w < m ? i + w : m) - 1;
     double thr = ub - cbnd[kk];
+    if (g_extra > 0 && kk <= g_kk_limit) thr -= g_extra;
     if (thr < 0) thr = 0;
     int any = 0;
     double vmin = INFINITY;
@@ -109,10 +111,11 @@ int main(int argc, char** argv) {
   long long rev_rows = 0, rev_cells = 0, min_rows = 0, min_cells2 = 0, best_cells = 0, pred_cells = 0;
   long long pk_cells[4][2] = {{0}};  /* probe k = 16, 32, 64, 128 rows both ways: [by slack, by live count] */
   const int pks[4] = {16, 32, 64, 128};
+  long long comb_cells = 0, comb_plain = 0;
   long long greedy_cells[3] = {0};
   long long alt_cells[3] = {0};  /* K = 32: slack/T, extrapolated death row, slack at 32 + width */  /* strip-granular races: greedy least-slack (S = 16, 32, 64) */
   const double dedges[6] = {1.0, 1.1, 1.25, 1.5, 2.0, 3.0};
-#pragma omp parallel reduction(+ : rowhist[:12], rowcells[:12], eqrow_hist[:12], tasks, cells, rows_sum, whist[:12], maxhist[:12], cells_by_max[:12], drift_hist[:8], dr_tasks[:7], dr_cells[:7], imp_tasks, imp_cells, rev_rows, rev_cells, min_rows, min_cells2, best_cells, pred_cells, pk_cells[:4][:2], greedy_cells[:3], alt_cells[:3])
+#pragma omp parallel reduction(+ : comb_cells, comb_plain, rowhist[:12], rowcells[:12], eqrow_hist[:12], tasks, cells, rows_sum, whist[:12], maxhist[:12], cells_by_max[:12], drift_hist[:8], dr_tasks[:7], dr_cells[:7], imp_tasks, imp_cells, rev_rows, rev_cells, min_rows, min_cells2, best_cells, pred_cells, pk_cells[:4][:2], greedy_cells[:3], alt_cells[:3])
   {
     double *c = malloc(m * 8), *cu = malloc(m * 8), *cl = malloc(m * 8);
     double *ceq = malloc(m * 8), *cec = malloc(m * 8), *cbnd = malloc(m * 8), *cbig = malloc(m * 8);
@@ -316,6 +319,41 @@ int main(int argc, char** argv) {
               alt_cells[crit] += cost;
             }
           }
+          {  /* probe 32 both ways, pick by slack, continue with the other probe's excess added to cb */
+            const int K = 32;
+            long long pf = 0, pr = 0;
+            for (int k = 1; k <= K; ++k) { pf += rcf[k]; pr += rcr[k]; }
+            const int fdead = rcf[K] == 0, rdead = rcr[K] == 0;
+            long long cost, plain;
+            if (fdead || rdead) {
+              cost = fdead && rdead ? pf + pr : (fdead ? pf + (pr < pf ? pr : pf) : pr + (pf < pr ? pf : pr));
+              plain = cost;
+            } else {
+              const int pick_rev = slr[K] < slf[K];
+              const size_t kkK = (K + w < m ? K + w : m) - 1;
+              plain = pf + pr + (pick_rev ? rcc - pr : fcc - pf);
+              long long tcells = 0;
+              if (!pick_rev) {
+                /* forward continues; reverse probe's frontier minimum replaces the last 32 positions' bound */
+                const double rmin = (ub - rcb[kkK]) - slr[K];
+                const double tail = cbnd[m - 33];
+                g_extra = rmin > tail ? rmin - tail : 0.0;
+                g_kk_limit = m - 33;
+                pruned_rows(c, qn, cbnd, m, w, ub, prev, cur, &tcells, NULL, NULL);
+              } else {
+                const double fmin = (ub - cbnd[kkK]) - slf[K];
+                const double head = rcb[m - 33];
+                g_extra = fmin > head ? fmin - head : 0.0;
+                g_kk_limit = m - 33;
+                pruned_rows(rc, rq, rcb, m, w, ub, prev, cur, &tcells, NULL, NULL);
+              }
+              g_extra = 0.0;
+              const long long own = pick_rev ? pr : pf;
+              cost = pf + pr + (tcells > own ? tcells - own : 0);
+            }
+            comb_cells += cost;
+            comb_plain += plain;
+          }
           /* greedy race: after one strip each, always advance the direction
              with less slack at its frontier; stop when either dies */
           for (int gi = 0; gi < 3; ++gi) {
@@ -402,6 +440,7 @@ int main(int argc, char** argv) {
            pks[pi], (double)pk_cells[pi][0] / tasks, (double)pk_cells[pi][1] / tasks);
   printf("\ngreedy least-slack race, strips of 16/32/64 rows: %.0f %.0f %.0f cells/task",
          (double)greedy_cells[0] / tasks, (double)greedy_cells[1] / tasks, (double)greedy_cells[2] / tasks);
+  printf("\nprobe 32 + other probe's excess in cb: %.0f cells/task (plain probe 32: %.0f)", (double)comb_cells / tasks, (double)comb_plain / tasks);
   printf("\nK=32 criteria: slack/T %.0f, extrapolated death %.0f, slack*live %.0f cells/task",
          (double)alt_cells[0] / tasks, (double)alt_cells[1] / tasks, (double)alt_cells[2] / tasks);
   printf("\nLB_Improved(EQ) > ub: %lld tasks (%.1f%%), %.1f%% of live cells\n", imp_tasks,
