@@ -758,23 +758,35 @@ def main():
     #      16 B written per candidate (stats) / per point (envelope)
     prep_kernels = None
     if world == 1:
-        ctx.set_option("prep_overlap", 0)
-        pp = []
-        for _ in range(3):
-            runner.search()
-            pp.append(shard.plan.timings())
-        ctx.set_option("prep_overlap", int(dict(kv.split("=") for kv in args.opt).get("prep_overlap", 1)))
-        torch.cuda.synchronize()
+        user = dict(kv.split("=") for kv in args.opt)
         hbm = hbm_peak_gbs()
         prep_kernels = {}
-        for name, key_, nbytes in (("stats_chain_kernel", "stats", 8 * npts + 16 * ncand),
-                                   ("envelope_gw_kernel", "envelope", 24 * npts)):
+
+        def prep_phases(spec):
+            ctx.set_option("prep_overlap", 0)
+            ctx.set_option("spec_stats", spec)
+            pp = []
+            for _ in range(3):
+                runner.search()
+                pp.append(shard.plan.timings())
+            torch.cuda.synchronize()
+            return pp
+
+        def add(name, pp, key_, nbytes):
             ms_k = statistics.median(p_[key_] for p_ in pp)
             if ms_k > 1e-3:
                 gbs = nbytes / (ms_k * 1e-3) / 1e9
                 prep_kernels[name] = {"ms": ms_k, "algorithmic_bytes": nbytes, "achieved_gbs": gbs,
                                       "hbm_peak_gbs": hbm["value"], "peak_source": hbm["source"],
                                       "frac": gbs / hbm["value"]}
+
+        pp = prep_phases(0)
+        add("stats_chain_kernel", pp, "stats", 8 * npts + 16 * ncand)
+        add("envelope_gw_kernel", pp, "envelope", 24 * npts)
+        # the speculative search's prefix-sum statistics (the chain runs beside them)
+        add("fast_stats_kernel", prep_phases(1), "stats", 8 * npts + 16 * ncand)
+        ctx.set_option("prep_overlap", int(user.get("prep_overlap", 1)))
+        ctx.set_option("spec_stats", int(user.get("spec_stats", -1)))
 
     # ---- timed region: K device-resident searches
     launches0 = ctx.launches
@@ -879,6 +891,7 @@ def main():
             "full_band_equiv_gcups": ncand * band_cells(m, w) / (ms_max * 1e-3) / 1e9,
             "phase_ms": phase_ms,
             "prep_kernels": prep_kernels,
+            "speculative_stats": ctx.spec_info(),
             "counted_cells_per_search": cells_mean,
             "sweep_counters": shard.plan.counters(),
             "result": {"location": best[2], "distance_sq": best[1]},

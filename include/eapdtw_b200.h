@@ -97,6 +97,14 @@ uint64_t eapdtw_total_launches(void);
 /* Cells of the last eapdtw_nn1(_dev) call evaluated by the FP32 screening
  * engine (included in that call's *cells total). */
 uint64_t eapdtw_ctx_last_cells_f32(const eapdtw_ctx* ctx);
+/* Speculative statistics (option spec_stats; search.cpp:156-168 is the exact
+ * chain they run beside): the last search's measured deviation of the
+ * prefix-sum statistics from the chain's (max |delta| / stddev; < 0: the last
+ * search did not speculate), the candidates it re-evaluated exactly, and the
+ * number of searches this process redid on the exact statistics because the
+ * deviation exceeded option spec_eps. */
+int eapdtw_ctx_spec_info(const eapdtw_ctx* ctx, double* deviation, uint64_t* listed,
+                         uint64_t* fallbacks);
 
 /* --- DTW kernels, one pair (dtw.hpp:69-99) ------------------------------- *
  * ea_pruned_dtw_windowed(a, b, Band{window}, ub, cumulative_bound)  dtw.hpp:93-99

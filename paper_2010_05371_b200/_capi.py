@@ -71,6 +71,8 @@ SIGNATURES = [
     ("eapdtw_ctx_launches", C.c_uint64, [_vp]),
     ("eapdtw_total_launches", C.c_uint64, []),
     ("eapdtw_ctx_last_cells_f32", C.c_uint64, [_vp]),
+    ("eapdtw_ctx_spec_info", C.c_int, [_vp, C.POINTER(C.c_double), C.POINTER(C.c_uint64),
+                                       C.POINTER(C.c_uint64)]),
     ("eapdtw_ea_pruned_dtw_windowed", C.c_int,
      [_vp, _dp, C.c_size_t, _dp, C.c_size_t, C.c_size_t, C.c_double, _dp, C.c_size_t, _dp,
       _u64p]),

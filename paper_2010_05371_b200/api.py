@@ -231,6 +231,14 @@ class Context:
         """FP32-screen share of the last nn1 call's cells."""
         return int(lib.eapdtw_ctx_last_cells_f32(self.handle))
 
+    def spec_info(self) -> dict:
+        """Speculative statistics of the last search (eapdtw_ctx_spec_info):
+        measured deviation (< 0: no speculation), candidates re-evaluated
+        exactly, and the process-wide count of searches redone on the chain."""
+        dev, listed, fb = C.c_double(), C.c_uint64(), C.c_uint64()
+        check(lib.eapdtw_ctx_spec_info(self.handle, C.byref(dev), C.byref(listed), C.byref(fb)))
+        return {"deviation": dev.value, "listed": int(listed.value), "fallbacks": int(fb.value)}
+
 
 class MultiDevice:
     """One host thread driving several GPUs through the C ABI

@@ -80,6 +80,8 @@ enum Opt : int {
   kOptWarmF32,        // FP32 screen in the warm-start cascade (upper-bound wave and ranked list)
   kOptCbEcStrip,      // first strip whose cumulative-bound thresholds also use the EC suffix
   kOptProbeExcess,    // FP32 probe: the dropped direction's frontier minimum tightens the other's bound
+  kOptSpecStats,      // speculative prefix-sum statistics beside the exact chain: -1 auto, 0 (the chain first), 1
+  kOptSpecEps,        // ... their assumed deviation from the chain's, in units of 1e-9
   kNumOpts
 };
 struct OptDef {
@@ -96,7 +98,7 @@ constexpr OptDef kOpts[kNumOpts] = {
     {"nn1_splits", 0, 0, 1 << 16}, {"nn1_warm", 1, 0, 1},       {"series_cache", 1, 0, 1},
     {"probe_strips", 1, 0, 8},    {"producers", 0, 0, 1 << 20}, {"probe_warm", 0, 0, 1},
     {"prep_overlap", 1, 0, 1},   {"warm_f32", 1, 0, 1},      {"cb_ec_strip", 2, 1, 1 << 16},
-    {"probe_excess", 1, 0, 1},
+    {"probe_excess", 1, 0, 1},     {"spec_stats", -1, -1, 1},      {"spec_eps", 8000, 1, 1000000},
 };
 
 // Grow-only device buffer.
@@ -164,9 +166,13 @@ bool all_finite(const double* x, size_t n) {
 struct PlanBuffers {
   DevBuf mean, sd, env, q, qul, qperm, order, best, key, work, counters, probe_counters, flag,
       queue, qtot, qctr, rank, rlist, scratch;
+  // speculation: prefix-sum statistics, the completed candidates' list, and
+  // {deviation bits, rule mismatches, list count}
+  DevBuf mean_a, sd_a, vlist, spec;
   void release() {
     for (DevBuf* b : {&mean, &sd, &env, &q, &qul, &qperm, &order, &best, &key, &work, &counters,
-                      &probe_counters, &flag, &queue, &qtot, &qctr, &rank, &rlist, &scratch})
+                      &probe_counters, &flag, &queue, &qtot, &qctr, &rank, &rlist, &scratch,
+                      &mean_a, &sd_a, &vlist, &spec})
       b->release();
   }
 };
@@ -174,6 +180,7 @@ struct PlanBuffers {
 // Kernel launches of one context, also added to a process-wide total (the
 // concurrent grid's worker contexts are short-lived).
 static std::atomic<uint64_t> g_total_launches{0};
+static std::atomic<uint64_t> g_spec_fallbacks{0};  // speculative searches redone on the exact statistics
 struct LaunchCounter {
   uint64_t n = 0;
   LaunchCounter& operator++() {
@@ -209,6 +216,11 @@ struct eapdtw_ctx {
   // side stream of the preparation: the envelope runs there beside the stats chain
   cudaStream_t aux = nullptr;
   cudaEvent_t aux_fork = nullptr, aux_join = nullptr;
+  // speculation: the exact chain (then its verification) runs on this stream
+  cudaStream_t aux2 = nullptr;
+  cudaEvent_t spec_fork = nullptr, spec_fast = nullptr, spec_done = nullptr;
+  double spec_dev = -1.0;     // last search: measured deviation (< 0: no speculation)
+  uint64_t spec_listed = 0;   // ... candidates re-evaluated with the exact statistics
 };
 
 struct eapdtw_search_plan {
@@ -245,6 +257,15 @@ struct eapdtw_search_plan {
   double guard_rel = 1e-9, guard_abs = 1e-20;
   double qmax = 0.0;  // max |normalised query|
   std::chrono::steady_clock::time_point t0;
+  // Speculative statistics (kernels.cu: fast_stats_kernel).  spec: allowed for
+  // this plan; spec_active: this preparation runs on them (the exact chain is
+  // in flight on the context's second side stream); spec_final: the exact
+  // pass over the completed candidates is enqueued; runs: the candidate ranges
+  // searched so far (replayed without speculation if the verification fails).
+  bool spec = false, spec_active = false, spec_final = false;
+  double spec_eps = 0.0;
+  long long vcap = 0;
+  std::vector<std::pair<size_t, size_t>> runs;
 };
 
 extern "C" {
@@ -300,6 +321,12 @@ int eapdtw_ctx_destroy(eapdtw_ctx* c) {
   }
   if (c->aux_fork) cudaEventDestroy(c->aux_fork);
   if (c->aux_join) cudaEventDestroy(c->aux_join);
+  if (c->aux2) {
+    cudaStreamSynchronize(c->aux2);
+    cudaStreamDestroy(c->aux2);
+  }
+  for (cudaEvent_t ev : {c->spec_fork, c->spec_fast, c->spec_done})
+    if (ev) cudaEventDestroy(ev);
   if (c->own) cudaStreamDestroy(c->own);
   delete c;
   return EAPDTW_OK;
@@ -727,6 +754,9 @@ static int plan_init(eapdtw_search_plan* p, eapdtw_ctx* c, const double* ref_dev
   p->queue_slack = static_cast<size_t>(p->blocks) * p->warps + 64;
   CUDA_TRY(B.queue.ensure((nc + p->queue_slack) * 8));
   CUDA_TRY(B.qtot.ensure((nc + p->queue_slack) * 8));
+  // speculative statistics: pruned searches only (without a threshold every
+  // candidate completes and would be evaluated twice)
+  p->spec = p->algo == EAPDTW_ALGO_EA_PRUNED;
   return eapdtw_search_plan_reset(p);
 }
 
@@ -842,6 +872,33 @@ static SearchParams base_params(eapdtw_search_plan* p) {
   }
   s.counters = B.counters.as<unsigned long long>();
   s.index_offset = static_cast<long long>(p->offset);
+  if (p->spec_active && !p->spec_final) {
+    // Speculative statistics: every normalised value is within
+    // dc = eps (1 + |c|) <= eps (2 + sqrt(m)) of the chain's.  A lower bound or
+    // a DTW over at most 2m cells then moves by at most dc sqrt(2m) in its
+    // square root (Minkowski): the sqrt-term of lb_guard and its square; the
+    // FP32 screen's guard takes dc through its value factor; cb_eps widens the
+    // cumulative-bound guard (kernels.cu: cb_guard).
+    const double sm = std::sqrt(static_cast<double>(p->m));
+    const double dc = p->spec_eps * (2.0 + sm);
+    const double dsq = dc * std::sqrt(2.0 * static_cast<double>(p->m));
+    s.approx = 1;
+    s.mean = B.mean_a.as<double>();
+    s.sd = B.sd_a.as<double>();
+    s.guard_sqrt += 2.5 * dsq;
+    s.guard_abs += 1.5 * dsq * dsq;
+    s.cb_eps = 2.5 * dc;
+    s.vlist = B.vlist.as<long long>();
+    s.vcount = B.spec.as<unsigned long long>() + 2;
+    s.vcap = p->vcap;
+    const double cmax = sm + 1.0;
+    const double up = 0x1.0p-24 + 0x1.0p-49;
+    const F32Guard g = make_f32_guard(static_cast<int>(p->m), static_cast<int>(p->m), cmax, p->qmax,
+                                      1.0 + 1.5 * p->spec_eps * (2.0 + sm) / (up * cmax));
+    s.f32_a = g.a;
+    s.f32_b = g.b;
+    s.f32_ia = std::nextafter(static_cast<float>(1.0 / static_cast<double>(g.a)), 0.0f);
+  }
   return s;
 }
 
@@ -1044,7 +1101,51 @@ int eapdtw_search_plan_prepare(eapdtw_search_plan* p) {
   int e;
   CUDA_TRY(cudaEventRecord(p->ev[0], s));
   p->have_env = false;
-  if ((e = stage_stats_env(p, 0, -1, 0, -1, true, !p->stats_ready, p->ev[1]))) return e;
+  p->runs.clear();
+  p->spec_final = false;
+  // auto: where the chain's ~1.8 ms outweigh what the wider guards cost the
+  // sweep (cfg2 2.37 -> 1.98 ms, cfg3 4.25 -> 3.10; at cfg4 the guards cost 7%
+  // more DTW work, 45.7 -> 50.9 ms)
+  const long long spec_opt = c->opt[kOptSpecStats];
+  p->spec_active = p->spec && !p->stats_ready &&
+                   (spec_opt == 1 || (spec_opt < 0 && p->ncand <= 40000000)) &&
+                   fast_stats_tile(static_cast<int>(p->m)) > 0 && p->ncand >= 1000;
+  if (p->spec_active) {
+    // The exact chain first, on its own stream (its blocks take their SMs
+    // before the search kernels fill the GPU), then the prefix-sum statistics
+    // on the context stream; the verification follows the chain.
+    PlanBuffers& B = *p->buf;
+    const long long n = static_cast<long long>(p->n);
+    const int m = static_cast<int>(p->m);
+    p->spec_eps = static_cast<double>(c->opt[kOptSpecEps]) * 1e-9;
+    p->vcap = static_cast<long long>(std::min<size_t>(p->ncand, size_t{1} << 20));
+    CUDA_TRY(B.mean_a.ensure(p->ncand * 8));
+    CUDA_TRY(B.sd_a.ensure(p->ncand * 8));
+    CUDA_TRY(B.vlist.ensure(static_cast<size_t>(p->vcap) * 8));
+    CUDA_TRY(B.spec.ensure(32));
+    if (!c->aux2) {
+      CUDA_TRY(cudaStreamCreateWithFlags(&c->aux2, cudaStreamNonBlocking));
+      CUDA_TRY(cudaEventCreateWithFlags(&c->spec_fork, cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&c->spec_fast, cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&c->spec_done, cudaEventDisableTiming));
+    }
+    CUDA_TRY(cudaMemsetAsync(B.spec.p, 0, 32, s));
+    CUDA_TRY(cudaEventRecord(c->spec_fork, s));
+    CUDA_TRY(cudaStreamWaitEvent(c->aux2, c->spec_fork, 0));
+    CUDA_TRY(launch_stats(p->ref, n, m, B.mean.as<double>(), B.sd.as<double>(), c->aux2, 0, -1));
+    c->launches += kStatsLaunches;
+    CUDA_TRY(launch_fast_stats(p->ref, n, m, B.mean_a.as<double>(), B.sd_a.as<double>(), s));
+    ++c->launches;
+    CUDA_TRY(cudaEventRecord(c->spec_fast, s));
+    CUDA_TRY(cudaStreamWaitEvent(c->aux2, c->spec_fast, 0));
+    CUDA_TRY(launch_stats_verify(B.mean.as<double>(), B.sd.as<double>(), B.mean_a.as<double>(),
+                                 B.sd_a.as<double>(), static_cast<long long>(p->ncand),
+                                 B.spec.as<unsigned long long>(), c->aux2));
+    ++c->launches;
+    CUDA_TRY(cudaEventRecord(c->spec_done, c->aux2));
+  }
+  if ((e = stage_stats_env(p, 0, -1, 0, -1, true, !p->stats_ready && !p->spec_active, p->ev[1])))
+    return e;
   CUDA_TRY(cudaEventRecord(p->ev[2], s));
   if ((e = stage_probe(p, p->ncand))) return e;
   if ((e = stage_rank(p, 0, p->ncand))) return e;
@@ -1070,6 +1171,7 @@ int eapdtw_search_plan_run(eapdtw_search_plan* p, size_t begin, size_t end) {
   sp.end = static_cast<long long>(end);
   sp.stride = 1;
   if (!p->ran) CUDA_TRY(cudaEventRecord(p->ev[4], s));
+  if (p->spec_active) p->runs.emplace_back(begin, end);
   CUDA_TRY(reset_work(p, static_cast<long long>(end - begin), s));
   CUDA_TRY(launch_search(sp, p->blocks, p->warps, s));
   ++c->launches;
@@ -1083,12 +1185,62 @@ int eapdtw_search_plan_result(eapdtw_search_plan* p, eapdtw_search_result* out) 
   eapdtw_ctx* c = p->ctx;
   PlanBuffers& B = *p->buf;
   CUDA_TRY(cudaSetDevice(c->device));
+  unsigned long long spec_out[4] = {0, 0, 0, 0};
+  if (p->spec_active) {
+    if (!p->spec_final) {
+      // The chain and its verification are done: the completed candidates
+      // again, now with the exact statistics (every one a DTW task; the
+      // threshold key holds a valid upper bound, the record takes the values).
+      CUDA_TRY(cudaStreamWaitEvent(c->stream, c->spec_done, 0));
+      p->spec_final = true;
+      SearchParams xp = base_params(p);
+      xp.direct = 1;
+      xp.direct_chunk = 1;
+      xp.use_lb = 0;
+      xp.tighten = 0;
+      xp.begin = 0;
+      xp.end = static_cast<long long>(p->ncand);
+      xp.list = B.vlist.as<long long>();
+      xp.nlist = B.spec.as<unsigned long long>() + 2;
+      xp.list_cap = p->vcap;
+      // second evaluations: counted with the warm start's work, not as candidates
+      xp.counters = B.probe_counters.as<unsigned long long>();
+      CUDA_TRY(reset_work(p, 0, c->stream));
+      CUDA_TRY(launch_search(xp, p->blocks, p->warps, c->stream));
+      ++c->launches;
+    }
+    CUDA_TRY(cudaMemcpyAsync(spec_out, B.spec.p, 32, cudaMemcpyDeviceToHost, c->stream));
+  }
   BestRecord rec{};
   unsigned long long cnt[kNumCountersExt], pc[kNumCountersExt];
   CUDA_TRY(cudaMemcpyAsync(&rec, B.best.p, sizeof(rec), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaMemcpyAsync(cnt, B.counters.p, sizeof(cnt), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaMemcpyAsync(pc, B.probe_counters.p, sizeof(pc), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
+  c->spec_dev = -1.0;
+  if (p->spec_active) {
+    double dev;
+    std::memcpy(&dev, &spec_out[0], 8);
+    c->spec_dev = dev;
+    c->spec_listed = spec_out[2];
+    if (!(dev <= p->spec_eps) || spec_out[1] != 0 ||
+        spec_out[2] > static_cast<unsigned long long>(p->vcap)) {
+      // The prefix-sum statistics were further from the chain's than assumed
+      // (or disagreed on a constant window, or too many candidates completed):
+      // nothing of the speculative pass is kept.  Search again on the exact
+      // statistics, which are in the buffers now.
+      const std::vector<std::pair<size_t, size_t>> runs = p->runs;
+      p->spec = false;
+      ++g_spec_fallbacks;
+      int e = eapdtw_search_plan_reset(p);
+      p->stats_ready = true;
+      if (!e) e = eapdtw_search_plan_prepare(p);
+      p->stats_ready = false;
+      for (const auto& r : runs)
+        if (!e) e = eapdtw_search_plan_run(p, r.first, r.second);
+      return e ? e : eapdtw_search_plan_result(p, out);
+    }
+  }
   std::memset(out, 0, sizeof(*out));
   out->found = rec.d != kInf ? 1 : 0;
   out->distance_sq = rec.d;
@@ -1182,6 +1334,7 @@ static int one_shot(eapdtw_ctx* c, const double* ref_dev, size_t n, const double
   p.buf = &c->pb;  // reuse the context's grow-only scratch
   int e = plan_init(&p, c, ref_dev, n, query, qlen, cfg, 0);
   bool fill_cache = false;
+  if (cache) p.spec = false;  // a cached series wants the exact statistics on the context stream
   if (!e && cache) {
     const size_t bytes = p.ncand * 8;
     if (cache->m == p.m) {
@@ -1373,6 +1526,7 @@ static int one_shot_streamed(eapdtw_ctx* c, const double* host_ref, size_t n,
   CUDA_TRY_F(cudaEventRecord(c->copied[1], c->copy));
 
   int e = plan_init(&p, c, dref, n, query, qlen, cfg, 0);
+  p.spec = false;  // the streamed parts run their stages themselves, on the exact chain
   if (e) return finish(e);
   long long te1 = 0;
   const int T = envelope_tile(p.env_r);
@@ -1530,6 +1684,14 @@ static int nn1_impl(eapdtw_ctx* c, const double* q_dev, size_t nq, const double*
 }
 
 uint64_t eapdtw_ctx_last_cells_f32(const eapdtw_ctx* c) { return c ? c->last_cells_f32 : 0; }
+int eapdtw_ctx_spec_info(const eapdtw_ctx* c, double* deviation, uint64_t* listed,
+                         uint64_t* fallbacks) {
+  if (!c) return fail(EAPDTW_EINVAL, "null ctx");
+  if (deviation) *deviation = c->spec_dev;
+  if (listed) *listed = c->spec_listed;
+  if (fallbacks) *fallbacks = g_spec_fallbacks.load();
+  return EAPDTW_OK;
+}
 
 int eapdtw_nn1_dev(eapdtw_ctx* c, const double* q_dev, size_t nq, const double* db_dev, size_t nd,
                    size_t len, size_t window, uint64_t* argmin, double* dist, uint64_t* cells) {

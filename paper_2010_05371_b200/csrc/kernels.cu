@@ -395,6 +395,166 @@ cudaError_t launch_stats(const double* ref, long long n, int m, double* mean, do
 }
 
 // ---------------------------------------------------------------------------
+// Speculative statistics (north_star (1): running mean / stddev via prefix
+// sums).  The exact chain above is a serial dependency of 100000 slides per
+// segment (~1.5 ms whatever the size of the search); everything that only has
+// to be SOUND, not bit-exact -- the lower-bound tiers, the FP32 screen, the
+// warm start's thresholds -- can run on statistics from per-tile prefix sums
+// instead, with its guards widened for an assumed deviation eps, while the
+// chain runs beside it on a few SMs.  Once the chain is done,
+// stats_verify_kernel measures the actual deviation of the prefix statistics
+// from the chain's; only candidates whose evaluation completed are then
+// re-evaluated with the exact statistics (capi.cu: speculation).
+//
+// fast_stats_kernel: a tile of T candidates per block; the T + m - 1 points
+// are staged in shared memory, each thread runs an inclusive prefix over its
+// contiguous chunk (sum and sum of squares), the chunk totals are scanned
+// across the block, and a window's sums are prefix differences.  Same
+// mean / variance formulas as RunningStats (search.hpp:34-41).
+// ---------------------------------------------------------------------------
+constexpr int kFastThreads = 256;
+int fast_stats_tile(int m) {
+  // (T + m) * 16 bytes of shared memory within ~96 KB (2 blocks per SM)
+  const long long cap = (96 * 1024) / 16;
+  long long T = cap - m;
+  if (T > 4096) T = 4096;
+  return T >= 256 ? static_cast<int>(T) : 0;  // 0: the window is too long for a tile
+}
+
+template <bool POW2>
+__global__ void __launch_bounds__(kFastThreads) fast_stats_kernel(const double* __restrict__ ref,
+                                                                  long long n, int m, int T,
+                                                                  double* __restrict__ mean,
+                                                                  double* __restrict__ sd) {
+  extern __shared__ double fsm[];
+  const long long ncand = n - m + 1;
+  const long long s0 = static_cast<long long>(blockIdx.x) * T;
+  const int cnt = static_cast<int>(min(static_cast<long long>(T), ncand - s0));
+  const int L = cnt + m - 1;
+  double* P1 = fsm;              // P1[i + 1]: inclusive prefix of x over the tile, P1[0] = 0
+  double* P2 = fsm + (T + m);    // the same of x^2
+  __shared__ double tot1[kFastThreads], tot2[kFastThreads];
+  const int t = threadIdx.x;
+  for (int i = t; i < L; i += kFastThreads) P1[i + 1] = ref[s0 + i];
+  if (t == 0) {
+    P1[0] = 0.0;
+    P2[0] = 0.0;
+  }
+  __syncthreads();
+  // odd chunk length: the threads' strided accesses fall in different banks
+  const int c = ((L + kFastThreads - 1) / kFastThreads) | 1;
+  const int b = min(L, t * c), e = min(L, b + c);
+  double a1 = 0.0, a2 = 0.0;
+  for (int i = b; i < e; ++i) {
+    const double x = P1[i + 1];
+    a1 += x;
+    a2 += x * x;
+    P1[i + 1] = a1;
+    P2[i + 1] = a2;
+  }
+  tot1[t] = a1;
+  tot2[t] = a2;
+  __syncthreads();
+  // exclusive scan of the chunk totals (256 values: one warp, 8 per lane)
+  if (t < 32) {
+    double r1[8], r2[8], l1 = 0.0, l2 = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      r1[k] = l1;
+      r2[k] = l2;
+      l1 += tot1[8 * t + k];
+      l2 += tot2[8 * t + k];
+    }
+    double i1 = l1, i2 = l2;
+    for (int off = 1; off < 32; off <<= 1) {
+      const double y1 = __shfl_up_sync(0xffffffffu, i1, off), y2 = __shfl_up_sync(0xffffffffu, i2, off);
+      if (t >= off) {
+        i1 += y1;
+        i2 += y2;
+      }
+    }
+    const double e1 = i1 - l1, e2 = i2 - l2;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      tot1[8 * t + k] = e1 + r1[k];
+      tot2[8 * t + k] = e2 + r2[k];
+    }
+  }
+  __syncthreads();
+  const double o1 = tot1[t], o2 = tot2[t];
+  for (int i = b; i < e; ++i) {
+    P1[i + 1] += o1;
+    P2[i + 1] += o2;
+  }
+  __syncthreads();
+  const double dm = static_cast<double>(m), inv_m = 1.0 / dm;
+  for (int k = t; k < cnt; k += kFastThreads) {
+    double mu, sg;
+    stats_of<POW2>(P1[k + m] - P1[k], P2[k + m] - P2[k], dm, inv_m, mu, sg);
+    mean[s0 + k] = mu;
+    sd[s0 + k] = sg;
+  }
+}
+
+cudaError_t launch_fast_stats(const double* ref, long long n, int m, double* mean, double* sd,
+                              cudaStream_t stream) {
+  const int T = fast_stats_tile(m);
+  if (T <= 0) return cudaErrorInvalidValue;
+  const long long ncand = n - m + 1;
+  const size_t smem = static_cast<size_t>(T + m) * 16;
+  const bool pow2 = (m & (m - 1)) == 0;
+  const void* fn = pow2 ? reinterpret_cast<const void*>(fast_stats_kernel<true>)
+                        : reinterpret_cast<const void*>(fast_stats_kernel<false>);
+  const cudaError_t e = ensure_dyn_smem(fn, smem);
+  if (e != cudaSuccess) return e;
+  const unsigned grid = static_cast<unsigned>((ncand + T - 1) / T);
+  if (pow2) fast_stats_kernel<true><<<grid, kFastThreads, smem, stream>>>(ref, n, m, T, mean, sd);
+  else fast_stats_kernel<false><<<grid, kFastThreads, smem, stream>>>(ref, n, m, T, mean, sd);
+  return cudaGetLastError();
+}
+
+// out[0]: max over the candidates of max(|mean_a - mean|, |sd_a - sd|) / sd as
+// order-preserving bits (a deviation of the normalised value c of at most
+// out[0] * (1 + |c|)); out[1]: candidates on different sides of kMinStddev
+// (the constant-window rule, search.cpp:37-46) or with non-finite statistics.
+__global__ void __launch_bounds__(256) stats_verify_kernel(const double* __restrict__ mean,
+                                                           const double* __restrict__ sd,
+                                                           const double* __restrict__ mean_a,
+                                                           const double* __restrict__ sd_a,
+                                                           long long ncand,
+                                                           unsigned long long* __restrict__ out) {
+  double worst = 0.0;
+  unsigned long long bad = 0;
+  for (long long k = blockIdx.x * 256LL + threadIdx.x; k < ncand; k += 256LL * gridDim.x) {
+    const double mu = mean[k], sg = sd[k], ma = mean_a[k], sa = sd_a[k];
+    const bool c0 = sg < kMinStddev, c1 = sa < kMinStddev;
+    if (c0 != c1 || !(fabs(ma) <= DBL_MAX) || !(sa <= DBL_MAX) || !(sg <= DBL_MAX)) {
+      ++bad;
+    } else if (!c0) {
+      const double r = 1.0 / sg;
+      worst = fmax(worst, fmax(fabs(ma - mu), fabs(sa - sg)) * r);
+    }
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    worst = fmax(worst, __shfl_xor_sync(0xffffffffu, worst, off));
+    bad += __shfl_xor_sync(0xffffffffu, bad, off);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(out, static_cast<unsigned long long>(__double_as_longlong(worst)));
+    if (bad) atomicAdd(out + 1, bad);
+  }
+}
+
+cudaError_t launch_stats_verify(const double* mean, const double* sd, const double* mean_a,
+                                const double* sd_a, long long ncand, unsigned long long* out,
+                                cudaStream_t stream) {
+  const long long blocks = std::min<long long>((ncand + 255) / 256, 148LL * 8);
+  stats_verify_kernel<<<static_cast<unsigned>(std::max<long long>(1, blocks)), 256, 0, stream>>>(
+      mean, sd, mean_a, sd_a, ncand, out);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // Global raw envelope for the LB_Keogh EC tier.
 //
 // The reference builds, per surviving candidate, the envelope of the
@@ -865,9 +1025,11 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
       return __dmul_rn(d2, d2);
     };
     const double tmax = fmax(teq, tec);
+    // (p.cb_eps: speculative statistics move each normalised value by up to
+    // eps (1 + |c|), hence the sum of the terms by 2 eps (1 + cmax) sqrt(m T))
+    const double sq_mt = __dsqrt_rn(static_cast<double>(m) * tmax);
     const double cb_guard =
-        p.guard_rel * tmax +
-        8.0 * 0x1.0p-52 * (tmax + p.qmax * __dsqrt_rn(static_cast<double>(m) * tmax));
+        p.guard_rel * tmax + 8.0 * 0x1.0p-52 * (tmax + p.qmax * sq_mt) + p.cb_eps * sq_mt;
     // Row i's remaining cost: every path still visits every later row
     // (0-based positions >= i: EQ terms are per candidate position = row),
     // and every column past i+w (0-based >= i+w: EC terms are per query
@@ -1025,11 +1187,25 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
     if (d == INF) {
       ++c_aband;
     } else if (lane == 0) {
-      atomicMin(p.ub_key, static_cast<unsigned long long>(__double_as_longlong(d)));
-      // ub_only: d is an upper bound (a narrower band's DTW), a threshold
-      // but not an answer
-      if (!p.ub_only)
-        best_record_update(p.best, d, static_cast<unsigned long long>(cand + p.index_offset));
+      if (p.approx) {
+        // Speculative statistics: d is within the guard of the exact value,
+        // so guard(d) bounds it from above, and guard(guard(d)) bounds what
+        // an approximate evaluation of any candidate at least as good can
+        // return: that is the threshold.  The candidate itself is listed for
+        // the exact pass (capi.cu); the record only takes exact values.
+        const double u2 = lb_guard(p, lb_guard(p, d));
+        atomicMin(p.ub_key, static_cast<unsigned long long>(__double_as_longlong(u2)));
+        if (!p.ub_only) {
+          const unsigned long long at = atomicAdd(p.vcount, 1ull);
+          if (at < static_cast<unsigned long long>(p.vcap)) p.vlist[at] = cand;
+        }
+      } else {
+        atomicMin(p.ub_key, static_cast<unsigned long long>(__double_as_longlong(d)));
+        // ub_only: d is an upper bound (a narrower band's DTW), a threshold
+        // but not an answer
+        if (!p.ub_only)
+          best_record_update(p.best, d, static_cast<unsigned long long>(cand + p.index_offset));
+      }
     }
   };
 

@@ -107,6 +107,13 @@ struct SearchParams {
   const unsigned long long* nlist;
   long long list_cap;            // entries past it were not written
   int ub_only;                   // results tighten the threshold only (no record update)
+  // speculative statistics (capi.cu): mean / sd are the prefix-sum ones, the
+  // guards are widened, completed candidates are listed for the exact pass
+  int approx;
+  double cb_eps;                 // extra cumulative-bound guard per sqrt(m T) (0 unless approx)
+  long long* vlist;              // completed candidates (plan-relative indices)
+  unsigned long long* vcount;    // entries claimed (may exceed vcap: overflow)
+  long long vcap;
   double* gscratch;              // non-null: the per-warp buffers live here (global memory),
                                  // warp_buf_doubles(m, ad_k) each, for queries whose buffers
                                  // exceed shared memory
@@ -157,6 +164,15 @@ cudaError_t launch_stats(const double* ref, long long n, int m, double* mean, do
                          cudaStream_t stream, long long seg_begin = 0, long long seg_end = -1);
 // env: 2n doubles, (max, min) interleaved; output tiles [tile_begin, tile_end)
 // of envelope_tile(r) positions (-1: all).  Tile t reads ref[tT - r, (t+1)T + r).
+// Speculative statistics: per-tile prefix sums, and their measured deviation
+// from the chain's (out[0]: max relative deviation as bits, out[1]: candidates
+// on different sides of the constant-window rule).
+int fast_stats_tile(int m);  // 0: window too long
+cudaError_t launch_fast_stats(const double* ref, long long n, int m, double* mean, double* sd,
+                              cudaStream_t stream);
+cudaError_t launch_stats_verify(const double* mean, const double* sd, const double* mean_a,
+                                const double* sd_a, long long ncand, unsigned long long* out,
+                                cudaStream_t stream);
 int envelope_tile(int r);
 cudaError_t launch_envelope(const double* ref, long long n, int r, double* env,
                             cudaStream_t stream, long long tile_begin = 0, long long tile_end = -1);

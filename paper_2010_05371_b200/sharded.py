@@ -148,6 +148,10 @@ class ShardedSearch:
             if self.world > 1:
                 all_reduce_min(b.key, self.group)
         res = b.result()
+        if self.world > 1:
+            # a speculative search (csrc/capi.cu) only learns its exact best in
+            # result(): every rank's key ends at the global exact minimum
+            all_reduce_min(b.key, self.group)
         return self.finalize(res)
 
     def finalize(self, res):

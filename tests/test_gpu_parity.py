@@ -645,3 +645,63 @@ def test_long_series_beyond_shared_memory(gpu, oracle_lib, reference_lib_optiona
         arg, dist, _ = gpu.nn1(qs, db, gpu.Band(band))
         assert [int(x) for x in arg] == [int(x) for x in warg]
         assert np.array_equal(dist, wdist)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,m,ratio,lb", [(300_000, 128, 0.05, True), (250_000, 512, 0.1, True),
+                                          (250_000, 512, 0.1, False), (120_000, 1024, 0.2, True),
+                                          (60_000, 257, 1.0, True)])
+def test_speculative_statistics_never_change_the_result(gpu, oracle_lib, n, m, ratio, lb):
+    """Speculative prefix-sum statistics (option spec_stats; fast_stats_kernel
+    beside the exact chain of search.cpp:156-168): the search prunes on them
+    with widened guards, re-evaluates the completed candidates on the chain's
+    statistics, and returns the oracle's (location, d) bit for bit -- with
+    planted exact ties (lowest index wins) and a near-tie 1e-7 above."""
+    ref = gpu.random_walk_normal(n, 170 + m)
+    q = gpu.random_walk_normal(m, 171 + m)
+    r = ref.copy()
+    a, b = n // 3, (2 * n) // 3
+    r[a:a + m] = q * 3.0 + 7.0
+    r[b:b + m] = q * 3.0 + 7.0
+    r[b + m // 2] += 1e-7
+    ctx = gpu.default_context()
+    for arr in (ref, r):
+        want = oracle_lib.similarity_search(arr, q, ratio, use_lb=lb, tighten=lb)
+        cfg = gpu.SearchConfig(window_ratio=ratio, use_lower_bounds=lb, tighten_ub=lb)
+        with ctx.options(spec_stats=1, streamed=0):
+            on = gpu.similarity_search(arr, q, cfg)
+            info = ctx.spec_info()
+        with ctx.options(spec_stats=0, streamed=0):
+            off = gpu.similarity_search(arr, q, cfg)
+        assert (on.best.location, on.best.distance_sq) == (want.location, want.distance_sq)
+        assert (off.best.location, off.best.distance_sq) == (want.location, want.distance_sq)
+        assert 0.0 <= info["deviation"] <= 8e-6 and info["listed"] >= 1
+        rep = on.report
+        assert rep.candidates_total == n - m + 1
+        assert rep.candidates_total == (rep.pruned_kim + rep.pruned_keogh_eq + rep.pruned_keogh_ec
+                                        + rep.dtw_calls)
+
+
+@pytest.mark.gpu
+def test_speculative_statistics_fall_back_to_the_chain(gpu, oracle_lib):
+    """When the prefix-sum statistics are further from the chain's than
+    assumed (here: an assumed deviation of 1e-9, below what a random walk
+    shows), or disagree on a constant window (sd below 1e-12, search.cpp:13),
+    nothing of the speculative pass is kept: the search is redone on the
+    exact statistics and still equals the oracle."""
+    n, m, ratio = 200_000, 256, 0.1
+    ref = gpu.random_walk_normal(n, 991) * 50.0 + 4.0e5  # a large offset: a noisy chain
+    q = gpu.random_walk_normal(m, 992)
+    flat = ref.copy()
+    flat[50_000:50_000 + 3 * m] = 1234.5  # constant windows
+    ctx = gpu.default_context()
+    for arr, opts in ((ref, dict(spec_stats=1, spec_eps=1, streamed=0)),
+                      (flat, dict(spec_stats=1, streamed=0))):
+        want = oracle_lib.similarity_search(arr, q, ratio)
+        before = ctx.spec_info()["fallbacks"]
+        with ctx.options(**opts):
+            got = gpu.similarity_search(arr, q, gpu.SearchConfig(window_ratio=ratio))
+            after = ctx.spec_info()
+        assert (got.best.location, got.best.distance_sq) == (want.location, want.distance_sq)
+        if arr is ref:
+            assert after["fallbacks"] == before + 1
