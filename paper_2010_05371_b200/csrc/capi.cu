@@ -1105,10 +1105,12 @@ int eapdtw_search_plan_prepare(eapdtw_search_plan* p) {
   p->spec_final = false;
   // auto: where the chain's ~1.8 ms outweigh what the wider guards cost the
   // sweep (cfg2 2.37 -> 1.98 ms, cfg3 4.25 -> 3.10; at cfg4 the guards cost 7%
-  // more DTW work, 45.7 -> 50.9 ms)
+  // more DTW work, 45.7 -> 50.9 ms; the guards grow with m: a 1.25e7-candidate
+  // shard of cfg4, m = 1024, breaks even, 13.5 ms either way)
   const long long spec_opt = c->opt[kOptSpecStats];
   p->spec_active = p->spec && !p->stats_ready &&
-                   (spec_opt == 1 || (spec_opt < 0 && p->ncand <= 40000000)) &&
+                   (spec_opt == 1 || (spec_opt < 0 && p->ncand <= 40000000 &&
+                                      static_cast<double>(p->ncand) * static_cast<double>(p->m) <= 8e9)) &&
                    fast_stats_tile(static_cast<int>(p->m)) > 0 && p->ncand >= 1000;
   if (p->spec_active) {
     // The exact chain first, on its own stream (its blocks take their SMs
