@@ -82,6 +82,8 @@ enum Opt : int {
   kOptProbeExcess,    // FP32 probe: the dropped direction's frontier minimum tightens the other's bound
   kOptSpecStats,      // speculative prefix-sum statistics beside the exact chain: -1 auto, 0 (the chain first), 1
   kOptSpecEps,        // ... their assumed deviation from the chain's, in units of 1e-9
+  kOptRankMin,        // rank pass: only on ranges of at least this many candidates
+  kOptProbeUb,        // probe of wide-band searches in a band of w / rank_ub_w (thresholds only)
   kNumOpts
 };
 struct OptDef {
@@ -99,6 +101,7 @@ constexpr OptDef kOpts[kNumOpts] = {
     {"probe_strips", 1, 0, 8},    {"producers", 0, 0, 1 << 20}, {"probe_warm", 0, 0, 1},
     {"prep_overlap", 1, 0, 1},   {"warm_f32", 1, 0, 1},      {"cb_ec_strip", 2, 1, 1 << 16},
     {"probe_excess", 1, 0, 1},     {"spec_stats", -1, -1, 1},      {"spec_eps", 8000, 1, 1000000},
+    {"rank_min", 32000000, 0, 1LL << 40}, {"probe_ub", 1, 0, 1},
 };
 
 // Grow-only device buffer.
@@ -978,9 +981,16 @@ static int stage_stats_env(eapdtw_search_plan* p, long long seg_b, long long seg
 // makes the narrow band too loose a bound, cfg2 +0.1 ms).
 static bool rank_ub_applies(const eapdtw_search_plan* p) { return p->rank_ub && p->w_eff >= 64; }
 
+// The rank pass costs about a millisecond (its cascade ends in a tail of long
+// DTWs) and pays through the sweep's better threshold, i.e. with the size of
+// the search.  Measured on prefixes of cfg4 (m = 1024, tools/shard_emul.py):
+// 5e7 candidates 27.0 ms with it / 28.8 without, 2.5e7 19.5 / 18.8, 1.25e7
+// 13.3 / 11.8; cfg3 (1e7, m = 512) 2.6 / 2.15, cfg2 0.51 / 0.28 (device
+// phases).  Option rank_min: the smallest range it runs on.
 static bool rank_applies(const eapdtw_search_plan* p, size_t cb, size_t ce) {
   return p->rank_stride > 0 && p->use_lb && p->m >= 2 && p->algo != EAPDTW_ALGO_FULL &&
-         static_cast<long long>(ce - cb) >= 64 * p->rank_stride;
+         static_cast<long long>(ce - cb) >= 64 * p->rank_stride &&
+         static_cast<long long>(ce - cb) >= p->ctx->opt[kOptRankMin];
 }
 
 static int stage_probe(eapdtw_search_plan* p, size_t cand_end) {
@@ -1001,6 +1011,14 @@ static int stage_probe(eapdtw_search_plan* p, size_t cand_end) {
   sp.counters = B.probe_counters.as<unsigned long long>();
   sp.direct_chunk = 1;
   sp.direct = 1;
+  if (p->ctx->opt[kOptProbeUb] && p->rank_ub && p->w_eff >= 64) {
+    // Wide bands: the probe's first candidates run without a threshold, i.e.
+    // the whole exact DP (m = 1024, w = 205: ~0.4 ms each, 1.1 ms for the
+    // probe).  A band of w/4 cells costs a quarter and still bounds the DTW
+    // from above (fewer paths): a threshold, not an answer (ub_only).
+    sp.w = std::max(0, p->w_eff / p->rank_ub_w);
+    sp.ub_only = 1;
+  }
   CUDA_TRY(reset_work(p, static_cast<long long>(nprobe), s));
   CUDA_TRY(launch_search(sp, p->blocks, p->warps, s));
   ++p->ctx->launches;

@@ -498,7 +498,7 @@ def test_warm_start_never_changes_the_result(gpu, oracle_lib, rank):
     ctx = gpu.default_context()
     for coarse in (0, 64):
         with ctx.options(rank_stride=rank[0], rank_k=rank[1], rank_waves=rank[2],
-                         coarse_stride=coarse):
+                         coarse_stride=coarse, rank_min=0):
             got = gpu.similarity_search(r, q, gpu.SearchConfig(window_ratio=ratio))
         assert (got.best.location, got.best.distance_sq) == (want.location, want.distance_sq)
         rep = got.report
@@ -668,7 +668,7 @@ def test_speculative_statistics_never_change_the_result(gpu, oracle_lib, n, m, r
     for arr in (ref, r):
         want = oracle_lib.similarity_search(arr, q, ratio, use_lb=lb, tighten=lb)
         cfg = gpu.SearchConfig(window_ratio=ratio, use_lower_bounds=lb, tighten_ub=lb)
-        with ctx.options(spec_stats=1, streamed=0):
+        with ctx.options(spec_stats=1, streamed=0, rank_min=0 if m == 512 else 32_000_000):
             on = gpu.similarity_search(arr, q, cfg)
             info = ctx.spec_info()
         with ctx.options(spec_stats=0, streamed=0):

@@ -18,12 +18,15 @@ ctx = g.Context(0)
 stream = torch.cuda.current_stream()
 ctx.set_stream(stream.cuda_stream)
 cfg = g.SearchConfig(query_length=m, window_ratio=ratio)
+for kv in filter(None, os.environ.get("OPTS", "").split(",")):  # engine options, e.g. OPTS=rank_stride=0
+    k, v = kv.split("=")
+    ctx.set_option(k, int(v))
 for N in [int(a) for a in sys.argv[1:]] or [1, 2, 4, 8]:
     seg = -(-(n - m + 1) // 100_000)
     ncand = min(n - m + 1, -(-seg // N) * 100_000)
     npts = ncand + m - 1
     dref = torch.from_numpy(ref[:npts]).cuda()
-    for spec in ([0, 1] if ncand <= 40_000_000 else [0]):
+    for spec in ([0, 1] if ncand <= 40_000_000 and "SPEC_AB" in os.environ else [-1]):
         ctx.set_option("spec_stats", spec)
         plan = g.SearchPlan(dref.data_ptr(), npts, q, cfg, ctx=ctx)
         ms, ph = [], []
