@@ -83,7 +83,6 @@ enum Opt : int {
   kOptSpecStats,      // speculative prefix-sum statistics beside the exact chain: -1 auto, 0 (the chain first), 1
   kOptSpecEps,        // ... their assumed deviation from the chain's, in units of 1e-9
   kOptRankMin,        // rank pass: only on ranges of at least this many candidates
-  kOptProbeUb,        // probe of wide-band searches in a band of w / rank_ub_w (thresholds only)
   kNumOpts
 };
 struct OptDef {
@@ -101,7 +100,7 @@ constexpr OptDef kOpts[kNumOpts] = {
     {"probe_strips", 1, 0, 8},    {"producers", 0, 0, 1 << 20}, {"probe_warm", 0, 0, 1},
     {"prep_overlap", 1, 0, 1},   {"warm_f32", 1, 0, 1},      {"cb_ec_strip", 2, 1, 1 << 16},
     {"probe_excess", 1, 0, 1},     {"spec_stats", -1, -1, 1},      {"spec_eps", 8000, 1, 1000000},
-    {"rank_min", 32000000, 0, 1LL << 40}, {"probe_ub", 1, 0, 1},
+    {"rank_min", 32000000, 0, 1LL << 40},
 };
 
 // Grow-only device buffer.
@@ -1011,14 +1010,8 @@ static int stage_probe(eapdtw_search_plan* p, size_t cand_end) {
   sp.counters = B.probe_counters.as<unsigned long long>();
   sp.direct_chunk = 1;
   sp.direct = 1;
-  if (p->ctx->opt[kOptProbeUb] && p->rank_ub && p->w_eff >= 64) {
-    // Wide bands: the probe's first candidates run without a threshold, i.e.
-    // the whole exact DP (m = 1024, w = 205: ~0.4 ms each, 1.1 ms for the
-    // probe).  A band of w/4 cells costs a quarter and still bounds the DTW
-    // from above (fewer paths): a threshold, not an answer (ub_only).
-    sp.w = std::max(0, p->w_eff / p->rank_ub_w);
-    sp.ub_only = 1;
-  }
+  // (A probe in a band of w/4, thresholds only, measured slower on cfg4 shards:
+  // probe 1.1 -> 0.5 ms, but the looser threshold costs the sweep 2 ms.)
   CUDA_TRY(reset_work(p, static_cast<long long>(nprobe), s));
   CUDA_TRY(launch_search(sp, p->blocks, p->warps, s));
   ++p->ctx->launches;
