@@ -221,6 +221,7 @@ struct eapdtw_ctx {
   // speculation: the exact chain (then its verification) runs on this stream
   cudaStream_t aux2 = nullptr;
   cudaEvent_t spec_fork = nullptr, spec_fast = nullptr, spec_done = nullptr;
+  int spec_cooldown = 0;      // searches left without speculation after a fallback (auto mode)
   double spec_dev = -1.0;     // last search: measured deviation (< 0: no speculation)
   uint64_t spec_listed = 0;   // ... candidates re-evaluated with the exact statistics
 };
@@ -349,6 +350,7 @@ int eapdtw_ctx_set_option(eapdtw_ctx* c, const char* name, int64_t value) {
     if (k == kOptAdK && !(value == -1 || value == 0 || value == 1 || value == 3 || value == 5))
       return fail(EAPDTW_EINVAL, "option ad_k: -1, 0, 1, 3 or 5");
     c->opt[k] = value;
+    if (k == kOptSpecStats) c->spec_cooldown = 0;
     return EAPDTW_OK;
   }
   return fail(EAPDTW_EINVAL, std::string("unknown option: ") + name);
@@ -1120,9 +1122,10 @@ int eapdtw_search_plan_prepare(eapdtw_search_plan* p) {
   // shard of cfg4, m = 1024, breaks even, 13.5 ms either way)
   const long long spec_opt = c->opt[kOptSpecStats];
   p->spec_active = p->spec && !p->stats_ready &&
-                   (spec_opt == 1 || (spec_opt < 0 && p->ncand <= 40000000 &&
+                   (spec_opt == 1 || (spec_opt < 0 && c->spec_cooldown == 0 && p->ncand <= 40000000 &&
                                       static_cast<double>(p->ncand) * static_cast<double>(p->m) <= 8e9)) &&
                    fast_stats_tile(static_cast<int>(p->m)) > 0 && p->ncand >= 1000;
+  if (!p->spec_active && c->spec_cooldown > 0 && p->spec && !p->stats_ready) --c->spec_cooldown;
   if (p->spec_active) {
     // The exact chain first, on its own stream (its blocks take their SMs
     // before the search kernels fill the GPU), then the prefix-sum statistics
@@ -1245,6 +1248,9 @@ int eapdtw_search_plan_result(eapdtw_search_plan* p, eapdtw_search_result* out) 
       const std::vector<std::pair<size_t, size_t>> runs = p->runs;
       p->spec = false;
       ++g_spec_fallbacks;
+      // data like this would fail again: the context's next searches do not
+      // speculate (one-shot searches build a new plan per call)
+      c->spec_cooldown = 64;
       int e = eapdtw_search_plan_reset(p);
       p->stats_ready = true;
       if (!e) e = eapdtw_search_plan_prepare(p);
