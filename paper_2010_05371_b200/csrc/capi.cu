@@ -370,6 +370,8 @@ int eapdtw_ctx_synchronize(eapdtw_ctx* c) {
   if (!c) return fail(EAPDTW_EINVAL, "null ctx");
   CUDA_TRY(cudaSetDevice(c->device));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (c->aux) CUDA_TRY(cudaStreamSynchronize(c->aux));
+  if (c->aux2) CUDA_TRY(cudaStreamSynchronize(c->aux2));
   return EAPDTW_OK;
 }
 
@@ -1326,6 +1328,9 @@ int eapdtw_search_plan_destroy(eapdtw_search_plan* p) {
   if (p->ctx) {
     cudaSetDevice(p->ctx->device);
     cudaStreamSynchronize(p->ctx->stream);
+    // a speculative preparation's chain may still be writing the plan's buffers
+    if (p->ctx->aux2) cudaStreamSynchronize(p->ctx->aux2);
+    if (p->ctx->aux) cudaStreamSynchronize(p->ctx->aux);
   }
   p->own.release();
   for (auto& ev : p->ev)
