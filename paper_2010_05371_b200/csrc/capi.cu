@@ -853,6 +853,10 @@ static SearchParams base_params(eapdtw_search_plan* p) {
   s.queue = B.queue.as<long long>();
   s.qtot = B.qtot.as<float2>();
   s.qmax = p->qmax;
+  {
+    const double R = p->qmax + std::sqrt(static_cast<double>(p->m)) + 1.0;
+    s.kim_f32_guard = 72.0 * 0x1.0p-24 * R * R * 1.01;
+  }
   s.qhead = B.qctr.as<unsigned long long>();
   s.qtail = B.qctr.as<unsigned long long>() + 1;
   s.chunks_done = B.qctr.as<unsigned long long>() + 2;

@@ -901,6 +901,9 @@ void debug_read_reset(unsigned long long* out8) {
 #ifndef EAPDTW_KIM_CORNER_RSD
 #define EAPDTW_KIM_CORNER_RSD 1  // corner LB_Kim by reciprocal too (guarded)
 #endif
+#ifndef EAPDTW_KIM_F32
+#define EAPDTW_KIM_F32 1  // LB_Kim layers in FP32 (guarded): cfg4 sweep 39.2 -> 36.6 ms, total -1.9 ms
+#endif
 #ifndef EAPDTW_KIM_RSD
 #define EAPDTW_KIM_RSD 1  // Kim layers normalised by reciprocal multiplication
 #endif
@@ -1467,6 +1470,41 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
                 for (int t = 0; t < L; ++t) {
                   cf[t] = constant ? 0.0 : __ddiv_rn(__dsub_rn(ref[s + t], mean), sd);
                   cb[t] = constant ? 0.0 : __ddiv_rn(__dsub_rn(ref[s + m - 1 - t], mean), sd);
+                }
+#endif
+#if EAPDTW_KIM_F32
+                // The layers in FP32 (half the instructions and registers of
+                // this unrolled block; the bound is guarded anyway).  A float
+                // cost exceeds the exact one by at most ~5.1 u R^2 (u = 2^-24,
+                // R = qmax + cmax >= |q - c|: both values and the difference
+                // round once each); a layer's minimum inherits that, the sums
+                // round down, and p.kim_f32_guard = 72 u R^2 (14 layer terms
+                // at L = 8) is taken off the total.
+                {
+                  float cff[L], cbf[L];
+#pragma unroll
+                  for (int t = 0; t < L; ++t) {
+                    cff[t] = __double2float_rn(cf[t]);
+                    cbf[t] = __double2float_rn(cb[t]);
+                  }
+                  auto sqf = [](float a, float b) {
+                    const float d = __fsub_rn(a, b);
+                    return __fmul_rn(d, d);
+                  };
+                  float lbf = 0.0f;
+#pragma unroll
+                  for (int l = 1; l < L; ++l) {
+                    const float qa = qsp32[1 + l], qz = qsp32[m - l];
+                    float f = sqf(qa, cff[l]);
+                    float bk = sqf(qz, cbf[l]);
+#pragma unroll
+                    for (int t = 0; t < l; ++t) {
+                      f = fmin3f(f, sqf(qa, cff[t]), sqf(qsp32[1 + t], cff[l]));
+                      bk = fmin3f(bk, sqf(qz, cbf[t]), sqf(qsp32[m - t], cbf[l]));
+                    }
+                    lbf = __fadd_rd(lbf, __fadd_rd(f, bk));
+                  }
+                  return __dadd_rn(kim, __dsub_rd(static_cast<double>(lbf), p.kim_f32_guard));
                 }
 #endif
                 double lb = kim;

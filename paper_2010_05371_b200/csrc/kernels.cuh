@@ -82,6 +82,7 @@ struct SearchParams {
   double guard_rel, guard_abs;   // LB soundness guard
   double guard_sqrt;             // ... and its reciprocal-normalisation term (lb_guard)
   double qmax;                   // max |q| (cumulative-bound guard)
+  double kim_f32_guard;          // FP32 LB_Kim layers: what their rounding can add (kernels.cu)
   unsigned long long* ub_key;    // running threshold key (order-preserving bits)
   BestRecord* best;              // exact (d, lowest index) record
   unsigned long long* work;      // chunk counter (zeroed before launch)
