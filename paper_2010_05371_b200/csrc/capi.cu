@@ -171,10 +171,11 @@ struct PlanBuffers {
   // speculation: prefix-sum statistics, the completed candidates' list, and
   // {deviation bits, rule mismatches, list count}
   DevBuf mean_a, sd_a, vlist, spec;
+  DevBuf qperm32;  // the visiting-order query envelope as outward-rounded floats
   void release() {
     for (DevBuf* b : {&mean, &sd, &env, &q, &qul, &qperm, &order, &best, &key, &work, &counters,
                       &probe_counters, &flag, &queue, &qtot, &qctr, &rank, &rlist, &scratch,
-                      &mean_a, &sd_a, &vlist, &spec})
+                      &mean_a, &sd_a, &vlist, &spec, &qperm32})
       b->release();
   }
 };
@@ -697,6 +698,7 @@ static int plan_init(eapdtw_search_plan* p, eapdtw_ctx* c, const double* ref_dev
   CUDA_TRY(B.q.ensure((m + 1) * 8));
   CUDA_TRY(B.qul.ensure(m * 16));
   CUDA_TRY(B.qperm.ensure(m * 16));
+  CUDA_TRY(B.qperm32.ensure(m * 8));
   CUDA_TRY(B.order.ensure(m * 4));
   CUDA_TRY(B.best.ensure(sizeof(BestRecord)));
   CUDA_TRY(B.key.ensure(8));
@@ -714,6 +716,15 @@ static int plan_init(eapdtw_search_plan* p, eapdtw_ctx* c, const double* ref_dev
   CUDA_TRY(cudaMemcpyAsync(B.q.p, q1.data(), (m + 1) * 8, cudaMemcpyHostToDevice, s));
   CUDA_TRY(cudaMemcpyAsync(B.qul.p, qul.data(), m * 16, cudaMemcpyHostToDevice, s));
   CUDA_TRY(cudaMemcpyAsync(B.qperm.p, qperm.data(), m * 16, cudaMemcpyHostToDevice, s));
+  std::vector<float> qperm32(2 * m);
+  for (size_t j = 0; j < m; ++j) {  // outward: the float envelope contains the double one
+    float u = static_cast<float>(qperm[2 * j]), l = static_cast<float>(qperm[2 * j + 1]);
+    if (static_cast<double>(u) < qperm[2 * j]) u = std::nextafter(u, std::numeric_limits<float>::infinity());
+    if (static_cast<double>(l) > qperm[2 * j + 1]) l = std::nextafter(l, -std::numeric_limits<float>::infinity());
+    qperm32[2 * j] = u;
+    qperm32[2 * j + 1] = l;
+  }
+  CUDA_TRY(cudaMemcpyAsync(B.qperm32.p, qperm32.data(), m * 8, cudaMemcpyHostToDevice, s));
   CUDA_TRY(cudaMemcpyAsync(B.order.p, order.data(), m * 4, cudaMemcpyHostToDevice, s));
   // the staging vectors are pageable locals: wait until the copies consumed them
   CUDA_TRY(cudaStreamSynchronize(s));
@@ -830,6 +841,10 @@ static SearchParams base_params(eapdtw_search_plan* p) {
   s.q = B.q.as<double>();
   s.qul = B.qul.as<double2>();
   s.qperm = B.qperm.as<double2>();
+  s.qperm32 = B.qperm32.as<float2>();
+  // a term's FP32 distance error: the value (|.| <= cmax or qmax) and the
+  // difference (<= cmax + qmax) round once each, with margin
+  s.lb_f32_e = 4.0 * 0x1.0p-24 * (std::sqrt(static_cast<double>(p->m)) + 1.0 + p->qmax);
   s.order = B.order.as<int>();
   s.ncand = static_cast<long long>(p->ncand);
   s.m = static_cast<int>(p->m);

@@ -871,6 +871,27 @@ __device__ __forceinline__ double lb_guard(const SearchParams& p, double ub) {
   return ub * (1.0 + p.guard_rel) + p.guard_abs + p.guard_sqrt * __dsqrt_ru(ub);
 }
 
+#ifndef EAPDTW_LB_F32
+#define EAPDTW_LB_F32 1  // LB_Keogh terms in FP32 (guarded): cfg4 sweep 36.7 -> 34.9 ms, cfg3 1.78 -> 1.64
+#endif
+// FP32 Keogh terms: an upper bound of (float sum) - (true sum T).  A term's
+// distance dd moves by at most e = lb_f32_e (its FP32 value and difference
+// round once each; the envelope is rounded outward, which only lowers dd), so
+// the sum of squares moves by at most 2 e sum(dd) + m e^2 <= 2 e sqrt(m T) +
+// m e^2, and the float products / group sums by a relative 12 u.
+__device__ __forceinline__ double lb_f32_excess(const SearchParams& p, double T) {
+  if (!(T < DBL_MAX)) return 0.0;
+  const double dm = static_cast<double>(p.m);
+  return __dadd_ru(__dadd_ru(__dmul_ru(12.0 * 0x1.0p-24, T),
+                             __dmul_ru(2.0 * p.lb_f32_e, __dsqrt_ru(__dmul_ru(dm, T)))),
+                   __dmul_ru(dm, __dmul_ru(p.lb_f32_e, p.lb_f32_e)));
+}
+__device__ __forceinline__ float fmax3f(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
 __device__ __forceinline__ long long vload(const long long* p) {
   return *reinterpret_cast<const volatile long long*>(p);
 }
@@ -1552,6 +1573,48 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
         constexpr bool EC = decltype(ec_tag)::value;
         bool alive = pending;
         const double2* es = EC ? p.env + s : nullptr;
+#if EAPDTW_LB_F32
+        // The terms in FP32 (a third fewer instructions, and FFMA's latency in
+        // the accumulation instead of DMUL + DADD): the candidate value (EQ)
+        // or the normalised envelope (EC) is formed in FP64 and converted --
+        // the envelope outward (upper up, lower down), which only shrinks a
+        // term -- and groups of kLbGroup terms accumulate in a float.  What the
+        // roundings can ADD to the sum is bounded in lb_f32_excess (applied to
+        // the pruning threshold by the caller and taken off the totals).
+        const float2* __restrict__ qperm32 = p.qperm32;
+        auto term = [&](int k, float& g) {
+          const int j = order[k];
+          float a, U, L;
+          if (!EC) {
+            const float2 b = qperm32[k];
+            a = __double2float_rn(__dmul_rn(__dsub_rn(xs[j], mean), rsd));
+            U = b.x;
+            L = b.y;
+          } else {
+            const double2 e = es[j];
+            a = qsp32[j + 1];
+            U = __double2float_ru(__dmul_rn(__dsub_rn(e.x, mean), rsd));
+            L = __double2float_rd(__dmul_rn(__dsub_rn(e.y, mean), rsd));
+          }
+          const float dd = fmax3f(__fsub_rn(a, U), __fsub_rn(L, a), 0.0f);
+          g = __fmaf_rn(dd, dd, g);
+        };
+        for (int kb = k0; kb < k1; kb += kLbGroup) {
+          float g = 0.0f;
+          if (kb + kLbGroup <= k1) {
+#pragma unroll
+            for (int u = 0; u < kLbGroup; ++u) term(kb + u, g);
+          } else {
+            for (int k = kb; k < k1; ++k) term(k, g);
+          }
+          acc = __dadd_rn(acc, static_cast<double>(g));
+          if (pending && acc > ubg) {
+            pending = false;
+            alive = false;
+          }
+          if (!__any_sync(kFull, pending)) break;
+        }
+#else
         auto term = [&](int k) {
           const int j = order[k];
           double a, U, L;
@@ -1584,6 +1647,7 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
           }
           if (!__any_sync(kFull, pending)) break;
         }
+#endif
         return alive;
       };
 
@@ -1611,7 +1675,13 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
         const double mean = p.mean[s];
         const double sd = p.sd[s];
         const double rsd = sd < kMinStddev ? 0.0 : __drcp_rn(sd);
+#if EAPDTW_LB_F32
+        // (prune iff the float sum exceeds what a true sum of ubg can round to)
+        const double ubg0 = lb_guard(p, load_ub(p.ub_key));
+        const double ubg = __dadd_ru(ubg0, lb_f32_excess(p, ubg0));
+#else
         const double ubg = lb_guard(p, load_ub(p.ub_key));
+#endif
         // EQ: stage the batch's stretch of the reference in the warp's buffer
         // when it fits, so the order[]-permuted reads hit shared memory
         // instead of L2 (the DP row buffer is free between DTW tasks).
@@ -1643,7 +1713,12 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
           if (EC) ++c_ec;
           else ++c_eq;
         }
+#if EAPDTW_LB_F32
+        // rounded down, less what the float terms may have added: a weaker, sound total
+        const float tot = fmaxf(0.0f, __double2float_rd(__dsub_rd(acc, lb_f32_excess(p, acc))));
+#else
         const float tot = __double2float_rz(acc);  // rounded down: a weaker, sound total
+#endif
         if (!leg2 && head < m) {
           if (EC) push(stkB2, nB2, alive, s, accB2, acc, teqB2, teq, nullptr, z2);
           else push(stkA2, nA2, alive, s, accA2, acc, nullptr, 0.0f, nullptr, z2);

@@ -68,6 +68,8 @@ struct SearchParams {
   const double* q;       // normalised query, 1-based: q[1..m] (q[0] unused)
   const double2* qul;    // query envelope (upper, lower) per position, 0-based
   const double2* qperm;  // the same in visiting order: qperm[k] = qul[order[k]]
+  const float2* qperm32; // ... as floats rounded outward (upper up, lower down), for FP32 Keogh terms
+  double lb_f32_e;       // FP32 Keogh terms: bound on a term's distance error (kernels.cu: lb_f32_excess)
   const int* order;      // Keogh visiting order (search.cpp:143-149)
   long long ncand;
   long long begin, end, stride;  // candidates begin, begin+stride, ... < end
