@@ -4,17 +4,18 @@ import re
 import sys
 
 REGIONS = [  # (file, first line, last line, name) -- line numbers of the build profiled
-    ("dtw_f32.cuh", 215, 292, "FP32 strip engine: step loop + finish masks"),
+    ("dtw_f32.cuh", 215, 297, "FP32 strip engine: step loop + finish masks"),
+    ("dtw_f32.cuh", 46, 46, "FP32 strip engine: step loop + finish masks"),  # fmin3f of the step
     ("dtw_f32.cuh", 0, 10**9, "FP32 strip engine: strip prologue / epilogue, probe"),
-    ("dtw_warp.cuh", 0, 10**9, "dtw_warp.cuh (sq_cost / dmin2 of the LB tiers, exact engine, record)"),
+    ("dtw_warp.cuh", 0, 10**9, "dtw_warp.cuh (sq_cost of the corners, exact engine, record)"),
     ("screen.cuh", 0, 10**9, "phase-A lane screen"),
-    ("kernels.cu", 982, 1211, "run_dtw: setup, cumulative-bound row thresholds"),
-    ("kernels.cu", 1299, 1366, "queue: claim / pop"),
-    ("kernels.cu", 1367, 1501, "LB_Kim corner + layers"),
-    ("kernels.cu", 1511, 1556, "LB_Keogh terms (lb_range)"),
-    ("kernels.cu", 1557, 1622, "Keogh tier stage (pop, staging, push)"),
-    ("kernels.cu", 1258, 1298, "stack push / pop"),
-    ("kernels.cu", 1623, 1660, "phase-A stage + publish"),
+    ("kernels.cu", 1006, 1235, "run_dtw: setup, cumulative-bound row thresholds"),
+    ("kernels.cu", 1323, 1390, "queue: claim / pop"),
+    ("kernels.cu", 1391, 1560, "LB_Kim corner + layers"),
+    ("kernels.cu", 1570, 1658, "LB_Keogh terms (lb_range)"),
+    ("kernels.cu", 1659, 1735, "Keogh tier stage (pop, staging, push)"),
+    ("kernels.cu", 1282, 1322, "stack push / pop"),
+    ("kernels.cu", 1736, 1773, "phase-A stage + publish"),
     ("kernels.cu", 0, 10**9, "kernels.cu other"),
 ]
 tot = [0, 0, 0]
