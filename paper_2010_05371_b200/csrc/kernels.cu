@@ -871,6 +871,9 @@ __device__ __forceinline__ double lb_guard(const SearchParams& p, double ub) {
   return ub * (1.0 + p.guard_rel) + p.guard_abs + p.guard_sqrt * __dsqrt_ru(ub);
 }
 
+#ifndef EAPDTW_CB_F32
+#define EAPDTW_CB_F32 1  // cumulative-bound prefixes (row thresholds) in FP32, rounded up: cfg4 sweep 34.6 -> 33.5 ms
+#endif
 #ifndef EAPDTW_LB_F32
 #define EAPDTW_LB_F32 1  // LB_Keogh terms in FP32 (guarded): cfg4 sweep 36.7 -> 34.9 ms, cfg3 1.78 -> 1.64
 #endif
@@ -1065,15 +1068,45 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
     // sees position k of the pass at the candidate's / query's position
     // m-1-k, so its prefixes run over the positions from the end: the same
     // bound for the mirrored problem.
+#if EAPDTW_CB_F32
+    // The prefixes as floats: every contribution rounded UP (envelope rounded
+    // inward, the distance raised by the FP32 term error lb_f32_e, products and
+    // sums rounded up), so total - prefix stays a lower bound of the suffix.
+    using cb_t = float;
+    const float cb_ef = __double2float_ru(p.lb_f32_e);
+    auto cb_add = [](float x, float y) { return __fadd_ru(x, y); };
+    auto contrib_eq_c = [&](int k) -> float {
+      if (k >= m) return 0.0f;
+      const float c = __double2float_rn(__dmul_rn(__dsub_rn(crow[k], cm), rsd));
+      const double2 b = qul[k];
+      const float U = __double2float_rd(b.x), L = __double2float_ru(b.y);
+      const float dd = __fadd_ru(fmax3f(__fsub_ru(c, U), __fsub_ru(L, c), 0.0f), cb_ef);
+      return __fmul_ru(dd, dd);
+    };
+    auto contrib_ec_c = [&](int k) -> float {
+      if (k >= m || !have_ec) return 0.0f;
+      const double2 e = p.env[cand + k];
+      const float U = __double2float_rd(__dmul_rn(__dsub_rn(e.x, cm), rsd));
+      const float L = __double2float_ru(__dmul_rn(__dsub_rn(e.y, cm), rsd));
+      const float qk = qsp32[k + 1];
+      const float dd = __fadd_ru(fmax3f(__fsub_ru(qk, U), __fsub_ru(L, qk), 0.0f), cb_ef);
+      return __fmul_ru(dd, dd);
+    };
+#else
+    using cb_t = double;
+    auto cb_add = [](double x, double y) { return __dadd_rn(x, y); };
+    auto& contrib_eq_c = contrib_eq;
+    auto& contrib_ec_c = contrib_ec;
+#endif
     struct CbPrefix {
-      double eq, ec;
+      cb_t eq, ec;
       int end_eq, end_ec;  // the prefixes cover pass positions [0, end) once started (-1: not yet)
     };
     static_assert(2 * sizeof(F32Strip) + 2 * sizeof(CbPrefix) <= kProbeStateBytes, "probe state");
     // (both directions' prefix states in the warp's shared probe state:
     // memory, not registers -- the kernel is at its register budget)
     CbPrefix* cbp = reinterpret_cast<CbPrefix*>(pstate + 2 * sizeof(F32Strip));
-    if (lane == 0) cbp[0] = cbp[1] = CbPrefix{0.0, 0.0, -1, -1};
+    if (lane == 0) cbp[0] = cbp[1] = CbPrefix{cb_t(0), cb_t(0), -1, -1};
     __syncwarp();
     // Both probes' evidence in one bound.  Once the FP32 screen has probed P
     // rows from each end and picked a direction, the dropped probe's frontier
@@ -1102,42 +1135,42 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
       const bool use_ec = have_ec && i0 >= 1 + 32 * (p.cb_ec_strip - 1);
       if (st.end_eq < 0) {  // positions before this strip's first ones
         st.end_eq = min(m, k_eq);
-        double eq = 0.0;
-        for (int k = lane; k < st.end_eq; k += 32) eq = __dadd_rn(eq, contrib_eq(pos(k)));
-        for (int off = 16; off > 0; off >>= 1) eq = __dadd_rn(eq, __shfl_xor_sync(kFull, eq, off));
+        cb_t eq = 0;
+        for (int k = lane; k < st.end_eq; k += 32) eq = cb_add(eq, contrib_eq_c(pos(k)));
+        for (int off = 16; off > 0; off >>= 1) eq = cb_add(eq, __shfl_xor_sync(kFull, eq, off));
         st.eq = eq;
       }
       if (use_ec && st.end_ec < 0) {
         st.end_ec = min(m, k_ec);
-        double ec = 0.0;
+        cb_t ec = 0;
         // (4 positions per lane in flight: the envelope loads are L2 latency)
         for (int k0 = lane; k0 < st.end_ec; k0 += 128) {
-          double t4[4];
+          cb_t t4[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const int k = k0 + 32 * u;
-            t4[u] = k < st.end_ec ? contrib_ec(pos(k)) : 0.0;
+            t4[u] = k < st.end_ec ? contrib_ec_c(pos(k)) : cb_t(0);
           }
 #pragma unroll
-          for (int u = 0; u < 4; ++u) ec = __dadd_rn(ec, t4[u]);
+          for (int u = 0; u < 4; ++u) ec = cb_add(ec, t4[u]);
         }
-        for (int off = 16; off > 0; off >>= 1) ec = __dadd_rn(ec, __shfl_xor_sync(kFull, ec, off));
+        for (int off = 16; off > 0; off >>= 1) ec = cb_add(ec, __shfl_xor_sync(kFull, ec, off));
         st.ec = ec;
       }
       // this strip's rows need prefixes through k_eq + lane and k_ec + lane
       const int ke = k_eq + lane, kc = k_ec + lane;
-      double a = 0.0, b = 0.0;
-      if (ke >= st.end_eq && ke < m) a = contrib_eq(pos(ke));
-      if (use_ec && kc >= st.end_ec && kc < m) b = contrib_ec(pos(kc));
+      cb_t a = 0, b = 0;
+      if (ke >= st.end_eq && ke < m) a = contrib_eq_c(pos(ke));
+      if (use_ec && kc >= st.end_ec && kc < m) b = contrib_ec_c(pos(kc));
       for (int off = 1; off < 32; off <<= 1) {  // inclusive prefix scans
-        const double x = __shfl_up_sync(kFull, a, off);
-        const double y = __shfl_up_sync(kFull, b, off);
+        const cb_t x = __shfl_up_sync(kFull, a, off);
+        const cb_t y = __shfl_up_sync(kFull, b, off);
         if (lane >= off) {
-          a = __dadd_rn(a, x);
-          b = __dadd_rn(b, y);
+          a = cb_add(a, x);
+          b = cb_add(b, y);
         }
       }
-      const double peq = __dadd_rn(st.eq, a), pec = __dadd_rn(st.ec, b);
+      const cb_t peq = cb_add(st.eq, a), pec = cb_add(st.ec, b);
       // the next strip starts where this one's rows end
       const int nxe = min(m, k_eq + 32), nxc = min(m, k_ec + 32);
       if (nxe > st.end_eq) {
@@ -1149,8 +1182,8 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
         st.end_ec = nxc;
       }
       if (i >= m) return u;  // the last row: nothing left
-      const double ceq = __dsub_rn(teq, peq);
-      const double cec = use_ec && kc < m - 1 ? __dsub_rn(tec, pec) : 0.0;
+      const double ceq = __dsub_rn(teq, static_cast<double>(peq));
+      const double cec = use_ec && kc < m - 1 ? __dsub_rn(tec, static_cast<double>(pec)) : 0.0;
       const double cbv = __dsub_rn(fmax(ceq, cec), cb_guard);
       if (!(cbv > 0.0)) return u;
       const double t = __dsub_rn(__dmul_rn(u, 1.0 + p.guard_rel), cbv);
@@ -1184,10 +1217,18 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
         // >= y (1 - b) - b with y = R / a (2 sqrt(y) <= 1 + y)
         const float y = __fmul_rd(other_vmin, p.f32_ia);
         const float lb = __fsub_rd(__fmul_rd(y, __fsub_rd(1.0f, p.f32_b)), p.f32_b);
-        const double x = __dsub_rd(__dsub_rd(static_cast<double>(lb), o.eq), 2.0 * cb_guard);
+        const double x = __dsub_rd(__dsub_rd(static_cast<double>(lb), static_cast<double>(o.eq)),
+                                   2.0 * cb_guard);
         if (!(x > 0.0)) return false;
         __syncwarp();
-        if (lane == 0) cbp[use_r ? 1 : 0].eq = __dsub_rd(cbp[use_r ? 1 : 0].eq, x);
+        // (the prefix less at most x: rounded so that it stays an upper bound)
+        if (lane == 0) {
+#if EAPDTW_CB_F32
+          cbp[use_r ? 1 : 0].eq = __fsub_ru(cbp[use_r ? 1 : 0].eq, __double2float_rd(x));
+#else
+          cbp[use_r ? 1 : 0].eq = __dsub_rd(cbp[use_r ? 1 : 0].eq, x);
+#endif
+        }
         __syncwarp();
         return true;
       };
@@ -1201,7 +1242,7 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
         screened = st == 0 && r32 == f_inf();
       }
       // the cumulative-bound prefixes restart for the exact pass
-      if (lane == 0) cbp[0] = CbPrefix{0.0, 0.0, -1, -1};
+      if (lane == 0) cbp[0] = CbPrefix{cb_t(0), cb_t(0), -1, -1};
       __syncwarp();
     }
     const double d = screened ? INF
