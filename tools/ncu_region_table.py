@@ -9,13 +9,13 @@ REGIONS = [  # (file, first line, last line, name) -- line numbers of the build 
     ("dtw_f32.cuh", 0, 10**9, "FP32 strip engine: strip prologue / epilogue, probe"),
     ("dtw_warp.cuh", 0, 10**9, "dtw_warp.cuh (sq_cost of the corners, exact engine, record)"),
     ("screen.cuh", 0, 10**9, "phase-A lane screen"),
-    ("kernels.cu", 1006, 1235, "run_dtw: setup, cumulative-bound row thresholds"),
-    ("kernels.cu", 1323, 1390, "queue: claim / pop"),
-    ("kernels.cu", 1391, 1560, "LB_Kim corner + layers"),
-    ("kernels.cu", 1570, 1658, "LB_Keogh terms (lb_range)"),
-    ("kernels.cu", 1659, 1735, "Keogh tier stage (pop, staging, push)"),
-    ("kernels.cu", 1282, 1322, "stack push / pop"),
-    ("kernels.cu", 1736, 1773, "phase-A stage + publish"),
+    ("kernels.cu", 1009, 1276, "run_dtw: setup, cumulative-bound row thresholds"),
+    ("kernels.cu", 1364, 1431, "queue: claim / pop"),
+    ("kernels.cu", 1432, 1601, "LB_Kim corner + layers"),
+    ("kernels.cu", 1611, 1699, "LB_Keogh terms (lb_range)"),
+    ("kernels.cu", 1700, 1776, "Keogh tier stage (pop, staging, push)"),
+    ("kernels.cu", 1323, 1363, "stack push / pop"),
+    ("kernels.cu", 1777, 1814, "phase-A stage + publish"),
     ("kernels.cu", 0, 10**9, "kernels.cu other"),
 ]
 tot = [0, 0, 0]
