@@ -84,7 +84,11 @@ int eapdtw_ctx_set_stream(eapdtw_ctx* ctx, void* cuda_stream);
  *   probe_force 0, tighten 1, cb_strip 1, warps 0, nn1_splits 0, nn1_warm 1,
  *   series_cache 1, probe_strips 1 (FP32 screen: strips probed in each direction),
  *   producers 0, probe_warm 0, prep_overlap 1 (envelope beside the stats chain),
- *   warm_f32 1.
+ *   warm_f32 1, cb_ec_strip 2 (first strip whose row thresholds use the EC suffix),
+ *   probe_excess 1 (the dropped probe's frontier minimum joins the other's bound),
+ *   spec_stats -1 (speculative prefix-sum statistics beside the exact chain of
+ *   search.cpp:156-168: -1 auto, 0, 1), spec_eps 8000 (their assumed deviation,
+ *   in 1e-9), rank_min 32000000 (smallest candidate range the rank pass runs on).
  * Every value returns the reference's answer; the defaults are the fastest
  * measured.  EAPDTW_EINVAL for an unknown name or out-of-range value. */
 int eapdtw_ctx_set_option(eapdtw_ctx* ctx, const char* name, int64_t value);
