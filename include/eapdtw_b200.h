@@ -88,7 +88,8 @@ int eapdtw_ctx_set_stream(eapdtw_ctx* ctx, void* cuda_stream);
  *   probe_excess 1 (the dropped probe's frontier minimum joins the other's bound),
  *   spec_stats -1 (speculative prefix-sum statistics beside the exact chain of
  *   search.cpp:156-168: -1 auto, 0, 1), spec_eps 8000 (their assumed deviation,
- *   in 1e-9), rank_min 32000000 (smallest candidate range the rank pass runs on).
+ *   in 1e-9), rank_min 32000000 (smallest candidate range the rank pass runs on),
+ *   lb_blocks 1 (Keogh visiting order by parts: the first 256 positions, then the rest).
  * Every value returns the reference's answer; the defaults are the fastest
  * measured.  EAPDTW_EINVAL for an unknown name or out-of-range value. */
 int eapdtw_ctx_set_option(eapdtw_ctx* ctx, const char* name, int64_t value);

@@ -83,6 +83,7 @@ enum Opt : int {
   kOptSpecStats,      // speculative prefix-sum statistics beside the exact chain: -1 auto, 0 (the chain first), 1
   kOptSpecEps,        // ... their assumed deviation from the chain's, in units of 1e-9
   kOptRankMin,        // rank pass: only on ranges of at least this many candidates
+  kOptLbBlocks,       // Keogh visiting order by parts (first 256 positions, then the rest)
   kNumOpts
 };
 struct OptDef {
@@ -100,7 +101,7 @@ constexpr OptDef kOpts[kNumOpts] = {
     {"probe_strips", 1, 0, 8},    {"producers", 0, 0, 1 << 20}, {"probe_warm", 0, 0, 1},
     {"prep_overlap", 1, 0, 1},   {"warm_f32", 1, 0, 1},      {"cb_ec_strip", 2, 1, 1 << 16},
     {"probe_excess", 1, 0, 1},     {"spec_stats", -1, -1, 1},      {"spec_eps", 8000, 1, 1000000},
-    {"rank_min", 32000000, 0, 1LL << 40},
+    {"rank_min", 32000000, 0, 1LL << 40}, {"lb_blocks", 1, 0, 1},
 };
 
 // Grow-only device buffer.
@@ -266,6 +267,7 @@ struct eapdtw_search_plan {
   // in flight on the context's second side stream); spec_final: the exact
   // pass over the completed candidates is enqueued; runs: the candidate ranges
   // searched so far (replayed without speculation if the verification fails).
+  bool lb_block_order = false;  // order[] by parts (plan_init)
   bool spec = false, spec_active = false, spec_final = false;
   double spec_eps = 0.0;
   long long vcap = 0;
@@ -672,10 +674,21 @@ static int plan_init(eapdtw_search_plan* p, eapdtw_ctx* c, const double* ref_dev
   }
   std::vector<int> order(m);
   std::iota(order.begin(), order.end(), 0);
-  std::sort(order.begin(), order.end(), [&](int a, int b) {
+  // Descending |q| (search.cpp:143-149); with option lb_blocks inside each of
+  // two parts, the first kLbHead positions and the rest: any visiting order
+  // gives the same sums, and a tier's leg then reads one part of the
+  // reference stretch only (kernels.cu: EQ staging).
+  const auto by_absq = [&](int a, int b) {
     const double fa = std::fabs(qn[a]), fb = std::fabs(qn[b]);
     return fa != fb ? fa > fb : a < b;
-  });
+  };
+  p->lb_block_order = o[kOptLbBlocks] != 0 && m > static_cast<size_t>(kLbHead);
+  if (p->lb_block_order) {
+    std::sort(order.begin(), order.begin() + kLbHead, by_absq);
+    std::sort(order.begin() + kLbHead, order.end(), by_absq);
+  } else {
+    std::sort(order.begin(), order.end(), by_absq);
+  }
   std::copy(qn.begin(), qn.end(), q1.begin() + 1);
   // (upper, lower) per position, and the same in visiting order.  (Outward-
   // rounded floats for the visiting-order copy, half its L1 footprint,
@@ -846,6 +859,7 @@ static SearchParams base_params(eapdtw_search_plan* p) {
   // difference (<= cmax + qmax) round once each, with margin
   s.lb_f32_e = 4.0 * 0x1.0p-24 * (std::sqrt(static_cast<double>(p->m)) + 1.0 + p->qmax);
   s.order = B.order.as<int>();
+  s.lb_block_order = p->lb_block_order ? 1 : 0;
   s.ncand = static_cast<long long>(p->ncand);
   s.m = static_cast<int>(p->m);
   s.w = p->w_eff;

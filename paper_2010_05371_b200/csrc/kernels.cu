@@ -1734,17 +1734,24 @@ __global__ void __launch_bounds__(EAPDTW_SEARCH_THREADS, kSearchMinBlocks) searc
             lo = min(lo, __shfl_xor_sync(kFull, lo, off));
             hi = max(hi, __shfl_xor_sync(kFull, hi, off));
           }
-          const long long len = static_cast<long long>(hi) - lo + m;
+          // p.lb_block_order: order[] visits the first kLbHead positions, then
+          // the rest (by descending |q| inside each part), so a leg only needs
+          // its own part of the stretch and the staging fits for survivors
+          // spread over up to wlen - part positions (all m positions: only
+          // for candidates within ~130 of one another at m = 1024)
+          const int p0 = p.lb_block_order ? (leg2 ? head : 0) : 0;
+          const int part = p.lb_block_order ? (leg2 ? m - head : head) : m;
+          const long long len = static_cast<long long>(hi) - lo + part;
 #ifdef EAPDTW_PHASE_CLOCKS
           if (lane == 0) atomicAdd(&p.counters[hi >= lo && len <= static_cast<long long>(wlen)
                                                    ? kStageHit : kStageMiss], 1ull);
 #endif
           if (!gmem && hi >= lo && len <= static_cast<long long>(wlen)) {
             double* sbuf = rowbuf - pad;
-            const double* src = ref + p.begin + lo;
+            const double* src = ref + p.begin + lo + p0;
             for (int t = lane; t < static_cast<int>(len); t += 32) sbuf[t] = src[t];
             __syncwarp();
-            if (pending) xs = sbuf + (s - p.begin - lo);
+            if (pending) xs = sbuf + (s - p.begin - lo) - p0;
           }
         }
         const bool alive = lb_range(ec_tag, xs, s, pending, mean, rsd, ubg, leg2 ? head : 0,

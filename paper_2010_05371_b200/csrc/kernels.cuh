@@ -71,6 +71,7 @@ struct SearchParams {
   const float2* qperm32; // ... as floats rounded outward (upper up, lower down), for FP32 Keogh terms
   double lb_f32_e;       // FP32 Keogh terms: bound on a term's distance error (kernels.cu: lb_f32_excess)
   const int* order;      // Keogh visiting order (search.cpp:143-149)
+  int lb_block_order;    // order[] lists the first kLbHead positions first (partial EQ staging)
   long long ncand;
   long long begin, end, stride;  // candidates begin, begin+stride, ... < end
   long long chunk_span;          // cascade: chunk c starts at begin + c*chunk_span (0: 32*stride)
