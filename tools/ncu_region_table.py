@@ -13,9 +13,9 @@ REGIONS = [  # (file, first line, last line, name) -- line numbers of the build 
     ("kernels.cu", 1364, 1431, "queue: claim / pop"),
     ("kernels.cu", 1432, 1601, "LB_Kim corner + layers"),
     ("kernels.cu", 1611, 1699, "LB_Keogh terms (lb_range)"),
-    ("kernels.cu", 1700, 1776, "Keogh tier stage (pop, staging, push)"),
+    ("kernels.cu", 1700, 1783, "Keogh tier stage (pop, staging, push)"),
     ("kernels.cu", 1323, 1363, "stack push / pop"),
-    ("kernels.cu", 1777, 1814, "phase-A stage + publish"),
+    ("kernels.cu", 1784, 1821, "phase-A stage + publish"),
     ("kernels.cu", 0, 10**9, "kernels.cu other"),
 ]
 tot = [0, 0, 0]
