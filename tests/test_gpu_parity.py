@@ -705,3 +705,24 @@ def test_speculative_statistics_fall_back_to_the_chain(gpu, oracle_lib):
         assert (got.best.location, got.best.distance_sq) == (want.location, want.distance_sq)
         if arr is ref:
             assert after["fallbacks"] == before + 1
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,m,ratio", [(200_000, 300, 0.1), (150_000, 1024, 0.2), (120_000, 257, 0.05)])
+def test_keogh_visiting_order_never_changes_the_result(gpu, oracle_lib, n, m, ratio):
+    """The LB_Keogh tiers visit the positions by descending |q| like the
+    reference (search.cpp:143-149, option lb_blocks=0) or by parts (the first
+    256 positions, then the rest: lb_blocks=1, the default): any order gives
+    the same sums, so both return the oracle's (location, d) bit for bit, and
+    the counter invariant holds."""
+    ref = gpu.random_walk_normal(n, 270 + m)
+    q = gpu.random_walk_normal(m, 271 + m)
+    want = oracle_lib.similarity_search(ref, q, ratio)
+    ctx = gpu.default_context()
+    for blocks in (0, 1):
+        with ctx.options(lb_blocks=blocks):
+            got = gpu.similarity_search(ref, q, gpu.SearchConfig(window_ratio=ratio))
+        assert (got.best.location, got.best.distance_sq) == (want.location, want.distance_sq)
+        rep = got.report
+        assert rep.candidates_total == (rep.pruned_kim + rep.pruned_keogh_eq + rep.pruned_keogh_ec
+                                        + rep.dtw_calls)
